@@ -1,0 +1,151 @@
+/*
+ * tmotif_b200.h -- C-ABI of the B200-native temporal motif counter.
+ *
+ * Drop-in boundary for the reference's counting path (arXiv 2204.09236
+ * FAST-Star / FAST-Tri / HARE; reference tree /root/reference/proj).  Every
+ * entry point takes plain pointers and sizes; no torch or CUDA C++ types
+ * cross this line (streams are passed as opaque `void*` cudaStream_t).
+ *
+ * Counter layouts are the reference's, cell-for-cell:
+ *   star[24]  index ((type*2 + d1)*2 + d2)*2 + d3   (motifs.hpp:78-83)
+ *   pair[8]   index (d1*2 + d2)*2 + d3              (motifs.hpp:103-106)
+ *   tri[24]   index ((type*2 + di)*2 + dj)*2 + dk   (motifs.hpp:127-131)
+ *   census[36] in lexicographic signature order      (motifs.hpp:159-161)
+ * with Direction outward = 0, inward = 1 (types.hpp:15).
+ *
+ * Error codes mirror the reference CLI's exit codes (tmotif_main.cpp:20-30)
+ * so that a binding can map them 1:1 onto the reference's exception types.
+ */
+#ifndef TMOTIF_B200_H
+#define TMOTIF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TM_OK 0
+#define TM_ERR_INVALID 1     /* std::invalid_argument (graph.cpp:20,29,32)      */
+#define TM_ERR_OVERFLOW 3    /* CounterOverflowError (types.hpp:50)             */
+#define TM_ERR_CONFIG 4      /* ConfigError (types.hpp:46, executor.cpp:151-156)  */
+#define TM_ERR_CONSISTENCY 5 /* ConsistencyError (types.hpp:55, motifs.cpp:254) */
+#define TM_ERR_CUDA 8        /* no device / CUDA failure: the path never falls back */
+#define TM_ERR_LIMIT 9       /* graph exceeds the 32-bit position layout         */
+
+#define TM_TRI_COUNT_ALL 0 /* TriangleMode::count_all (motifs.hpp:36) */
+#define TM_TRI_REMOVAL 1   /* TriangleMode::removal   (motifs.hpp:37) */
+
+#define TM_MOTIF_STAR 1u
+#define TM_MOTIF_PAIR 2u
+#define TM_MOTIF_TRIANGLE 4u
+
+typedef struct tm_graph tm_graph; /* device-resident GraphContext (indexes.hpp:95-105) */
+
+typedef struct tm_counters {
+    uint64_t star[24];
+    uint64_t pair[8];
+    uint64_t tri[24];
+} tm_counters;
+
+/* RunConfig (executor.hpp:36-46) plus a center partition for multi-GPU. */
+typedef struct tm_run_config {
+    int64_t delta;
+    uint32_t workers;          /* kept for the removal-mode check only            */
+    int64_t degree_threshold;  /* < 0: auto top-20 rule (executor.cpp:15)          */
+    int32_t triangle_mode;     /* TM_TRI_COUNT_ALL | TM_TRI_REMOVAL                */
+    uint32_t motifs;           /* TM_MOTIF_* bit set; 0 means all                   */
+    uint64_t shard_target;     /* accepted for API parity; semantics-free           */
+    uint32_t center_begin;     /* center partition [begin, end); end == 0: all      */
+    uint32_t center_end;
+} tm_run_config;
+
+/* PhaseTimings (executor.hpp:55-65); device-event times in ms. */
+typedef struct tm_phase_timings {
+    double index_ms;
+    double star_pair_ms;
+    double triangle_ms;
+    double merge_ms;
+} tm_phase_timings;
+
+/* ---- graph construction --------------------------------------------------
+ * Replaces TemporalGraph::build (graph.cpp:13-44) + GraphContext::build
+ * (indexes.hpp:99-103): edges arrive in ingestion order (ordinal = index),
+ * self-loops / out-of-range endpoints are rejected with TM_ERR_INVALID.
+ * `device_ptrs` != 0: src/dst/t are device pointers, else host pointers
+ * (copied in with cudaMemcpyAsync).  `stream` may be NULL (library stream). */
+int tm_graph_build(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
+                   uint64_t n, int device_ptrs, void* stream, tm_graph** out);
+void tm_graph_free(tm_graph* g);
+uint64_t tm_graph_node_count(const tm_graph* g);
+uint64_t tm_graph_edge_count(const tm_graph* g);
+void* tm_graph_stream(const tm_graph* g);
+
+/* TemporalGraph::degrees (graph.cpp:52-59); out_host has n entries. */
+int tm_graph_degrees(const tm_graph* g, uint64_t* out_host);
+/* NodeSequenceIndex::sequence (indexes.hpp:28-30) copied to host; len = S_u. */
+int tm_graph_sequence(const tm_graph* g, uint32_t u, int64_t* t, uint64_t* ordinal,
+                      uint32_t* other, uint8_t* dir, uint64_t cap, uint64_t* len);
+/* PairEdgeIndex::edges_in_window (indexes.cpp:75-85). */
+int tm_pair_window(const tm_graph* g, uint32_t v, uint32_t w, int64_t lo, int64_t hi,
+                   int64_t* t, uint64_t* ordinal, uint8_t* dir_rel_v, uint64_t cap,
+                   uint64_t* len);
+/* auto_degree_threshold (executor.cpp:15-21). */
+int tm_auto_degree_threshold(const tm_graph* g, uint64_t* out);
+
+/* ---- counting ----------------------------------------------------------- */
+/* count_star_pair (star_engine.cpp:129-136). */
+int tm_count_star_pair(tm_graph* g, int64_t delta, uint64_t* star24, uint64_t* pair8);
+/* count_triangles (triangle_engine.cpp:64-84): mode TM_TRI_*. */
+int tm_count_triangles(tm_graph* g, int64_t delta, int mode, uint64_t* tri24);
+/* count_star_pair_at_center (star_engine.cpp:64) batched over work items
+ * (node, [begin, end)) -- the HARE plan items (executor.cpp:31-52). */
+int tm_count_star_pair_items(tm_graph* g, int64_t delta, uint64_t n_items, const uint32_t* nodes,
+                             const uint64_t* begin, const uint64_t* end, uint64_t* star_out,
+                             uint64_t* pair_out);
+/* count_triangles_at_center (triangle_engine.cpp:20) batched; live: host
+ * array of n bytes or NULL (removal-mode live mask). */
+int tm_count_triangles_items(tm_graph* g, int64_t delta, uint64_t n_items, const uint32_t* nodes,
+                             const uint64_t* begin, const uint64_t* end, const uint8_t* live,
+                             uint64_t* tri_out);
+/* run_parallel (executor.cpp:149-215).  With a proper center partition the
+ * raw counters are partial sums and census is left zeroed (merge after the
+ * all-reduce); for the full range census holds merge_census(raw). */
+int tm_run_parallel(tm_graph* g, const tm_run_config* cfg, tm_counters* raw, uint64_t* census36,
+                    tm_phase_timings* timings);
+/* Whole pipeline for one step: build + run_parallel + free. */
+int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
+                   uint64_t n, int device_ptrs, void* stream, const tm_run_config* cfg,
+                   tm_counters* raw, uint64_t* census36, tm_phase_timings* timings);
+/* Degree-cost balanced center partition for rank `rank` of `world`. */
+int tm_partition_centers(const tm_graph* g, uint32_t world, uint32_t rank, uint32_t* begin,
+                         uint32_t* end);
+
+/* ---- taxonomy (host only) ----------------------------------------------- */
+/* merge_census (motifs.cpp:233-281). */
+int tm_merge_census(const uint64_t* star24, const uint64_t* pair8, const uint64_t* tri24,
+                    int mode, uint64_t* census36);
+/* all_signatures()[idx] (motifs.cpp:196) as "sd|sd|sd" + NUL. */
+int tm_signature(int idx, char* out9);
+/* signature index of a counter cell; kind 0 star, 1 pair, 2 tri. */
+int tm_cell_signature(int kind, int cell);
+/* label_for_signature (motifs.cpp:207). */
+int tm_signature_label(int idx, char* out16);
+/* generate_random_graph (graph.cpp:140-168), ingestion order. */
+int tm_generate_random_graph(uint64_t nodes, uint64_t m, int64_t t_max, uint64_t seed,
+                             uint32_t* src, uint32_t* dst, int64_t* t);
+
+/* ---- diagnostics -------------------------------------------------------- */
+const char* tm_last_error(void);
+/* Number of this library's kernels launched since load. */
+uint64_t tm_kernel_launches(void);
+/* Per-kernel CUDA-event timing on the launching stream. */
+void tm_kernel_timing_enable(int on);
+void tm_kernel_timing_reset(void);
+/* Aggregated device time of kernels whose name matches `name` exactly. */
+int tm_kernel_timing_get(const char* name, double* total_ms, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TMOTIF_B200_H */

@@ -1,0 +1,820 @@
+// tm_capi.cu -- extern "C" boundary (include/tmotif_b200.h) and host logic:
+// run_parallel orchestration (executor.cpp:149-215), census merge
+// (motifs.cpp:233-281), signature taxonomy (motifs.cpp:49-123, 145-219).
+// There is no CPU counting path here: every count comes from the kernels in
+// tm_star.cu / tm_tri.cu, and a missing device is reported as TM_ERR_CUDA.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <random>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/tmotif_b200.h"
+#include "tm_primitives.cuh"
+
+struct tm_graph {
+    tmb::DeviceGraph g;
+    std::vector<uint32_t> h_off;  // lazily mirrored CSR offsets
+};
+
+namespace tmb {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_timing{0};
+std::mutex g_timing_mu;
+struct PendingEv {
+    std::string name;
+    cudaEvent_t a, b;
+};
+std::vector<PendingEv> g_pending;
+std::map<std::string, std::pair<double, uint64_t>> g_ktotals;
+}  // namespace
+
+void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        throw tm_error(TM_ERR_CUDA, std::string(cudaGetErrorString(e)) + " at " + file + ":" +
+                                        std::to_string(line) + " (" + what + ")");
+    }
+}
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+KernelScope::KernelScope(const char* n, cudaStream_t s) : name(n), stream(s), ev0(nullptr) {
+    if (g_timing.load(std::memory_order_relaxed)) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) == cudaSuccess) {
+            cudaEventRecord(e, s);
+            ev0 = e;
+        }
+    }
+}
+KernelScope::~KernelScope() {
+    if (!ev0) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, stream);
+    std::lock_guard<std::mutex> lk(g_timing_mu);
+    g_pending.push_back({name, static_cast<cudaEvent_t>(ev0), e});
+}
+
+int sm_count() {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached = v > 0 ? v : 148;
+    }
+    return cached;
+}
+
+// ---------------------------------------------------------------------------
+// taxonomy (host)
+namespace {
+
+struct Universe {
+    std::vector<std::string> all;  // 36, lexicographic
+    int star_sig[24], pair_sig[8], tri_sig[24];
+};
+
+std::string canonical(const uint32_t e[3][2]) {
+    uint32_t seen[3];
+    int distinct = 0;
+    std::string s = "12|12|12";
+    for (int k = 0; k < 3; ++k)
+        for (int side = 0; side < 2; ++side) {
+            int lab = 0;
+            for (int q = 0; q < distinct; ++q)
+                if (seen[q] == e[k][side]) lab = q + 1;
+            if (!lab) {
+                seen[distinct++] = e[k][side];
+                lab = distinct;
+            }
+            s[3 * k + side] = char('0' + lab);
+        }
+    return s;
+}
+void orient(int d, uint32_t from, uint32_t to, uint32_t out[2]) {
+    out[0] = d ? to : from;
+    out[1] = d ? from : to;
+}
+std::string star_sig(int type, int d1, int d2, int d3) {
+    uint32_t e[3][2];
+    const int d[3] = {d1, d2, d3};
+    for (int p = 0; p < 3; ++p) orient(d[p], 0, p == type ? 2 : 1, e[p]);
+    return canonical(e);
+}
+std::string pair_sig(int d1, int d2, int d3) {
+    uint32_t e[3][2];
+    orient(d1, 0, 1, e[0]);
+    orient(d2, 0, 1, e[1]);
+    orient(d3, 0, 1, e[2]);
+    return canonical(e);
+}
+std::string tri_sig(int type, int di, int dj, int dk) {
+    uint32_t ei[2], ej[2], ek[2];
+    orient(di, 0, 1, ei);
+    orient(dj, 0, 2, ej);
+    orient(dk, 1, 2, ek);
+    const uint32_t* ord[3];
+    if (type == 0) { ord[0] = ek; ord[1] = ei; ord[2] = ej; }
+    else if (type == 1) { ord[0] = ei; ord[1] = ek; ord[2] = ej; }
+    else { ord[0] = ei; ord[1] = ej; ord[2] = ek; }
+    uint32_t e[3][2];
+    for (int k = 0; k < 3; ++k) { e[k][0] = ord[k][0]; e[k][1] = ord[k][1]; }
+    return canonical(e);
+}
+
+const Universe& universe() {
+    static const Universe U = [] {
+        Universe u;
+        std::set<std::string> all;
+        std::string st[24], pr[8], tr[24];
+        for (int c = 0; c < 24; ++c) all.insert(st[c] = star_sig(c >> 3, (c >> 2) & 1, (c >> 1) & 1, c & 1));
+        for (int c = 0; c < 8; ++c) all.insert(pr[c] = pair_sig(c >> 2, (c >> 1) & 1, c & 1));
+        for (int c = 0; c < 24; ++c) all.insert(tr[c] = tri_sig(c >> 3, (c >> 2) & 1, (c >> 1) & 1, c & 1));
+        u.all.assign(all.begin(), all.end());
+        auto idx = [&](const std::string& s) {
+            return int(std::lower_bound(u.all.begin(), u.all.end(), s) - u.all.begin());
+        };
+        for (int c = 0; c < 24; ++c) u.star_sig[c] = idx(st[c]);
+        for (int c = 0; c < 8; ++c) u.pair_sig[c] = idx(pr[c]);
+        for (int c = 0; c < 24; ++c) u.tri_sig[c] = idx(tr[c]);
+        return u;
+    }();
+    return U;
+}
+
+bool add_checked(uint64_t& cell, uint64_t v) {
+    if (cell > UINT64_MAX - v) return false;
+    cell += v;
+    return true;
+}
+
+int merge_census_impl(const uint64_t* star, const uint64_t* pair, const uint64_t* tri, int mode,
+                      uint64_t* census) {
+    const Universe& u = universe();
+    if ((int)u.all.size() != 36) {
+        g_last_error = "signature universe is not 36 classes";
+        return TM_ERR_CONSISTENCY;
+    }
+    uint64_t out[36] = {0};
+    for (int c = 0; c < 24; ++c)
+        if (!add_checked(out[u.star_sig[c]], star[c])) return TM_ERR_OVERFLOW;
+    for (int c = 0; c < 4; ++c) {  // d1 = outward; complement flips all bits
+        if (pair[c] != pair[7 - c]) {
+            g_last_error = "complementary pair cells disagree for " + u.all[u.pair_sig[c]];
+            return TM_ERR_CONSISTENCY;
+        }
+        if (!add_checked(out[u.pair_sig[c]], pair[c])) return TM_ERR_OVERFLOW;
+    }
+    uint64_t sums[36] = {0};
+    bool is_tri[36] = {false};
+    for (int c = 0; c < 24; ++c) {
+        if (!add_checked(sums[u.tri_sig[c]], tri[c])) return TM_ERR_OVERFLOW;
+        is_tri[u.tri_sig[c]] = true;
+    }
+    for (int k = 0; k < 36; ++k) {
+        if (!is_tri[k]) continue;
+        if (mode == TM_TRI_COUNT_ALL) {
+            if (sums[k] % 3) {
+                g_last_error = "triangle class sum not divisible by 3 for " + u.all[k];
+                return TM_ERR_CONSISTENCY;
+            }
+            if (!add_checked(out[k], sums[k] / 3)) return TM_ERR_OVERFLOW;
+        } else if (!add_checked(out[k], sums[k])) {
+            return TM_ERR_OVERFLOW;
+        }
+    }
+    std::memcpy(census, out, sizeof(out));
+    return TM_OK;
+}
+
+// raw star sums (Pair, C, B, A) -> reference Star / Pair cells
+void finish_star(const uint64_t* raw, uint64_t* star, uint64_t* pair) {
+    for (int c = 0; c < 8; ++c) {
+        const uint64_t p = raw[c];
+        if (pair) pair[c] = p;
+        if (star) {
+            star[0 * 8 + c] = raw[8 + c] - p;   // isolated_first  = C - Pair
+            star[1 * 8 + c] = raw[16 + c] - p;  // isolated_second = B - Pair
+            star[2 * 8 + c] = raw[24 + c] - p;  // isolated_third  = A - Pair
+        }
+    }
+}
+
+// once-counted cells -> count_all cells: every instance lands once in each
+// cell of its class (triangle_engine.hpp:57-60)
+void expand_count_all(const uint64_t* once, uint64_t* tri) {
+    const Universe& u = universe();
+    uint64_t cls[36] = {0};
+    for (int c = 0; c < 24; ++c) cls[u.tri_sig[c]] += once[c];
+    for (int c = 0; c < 24; ++c) tri[c] = cls[u.tri_sig[c]];
+}
+
+struct PinnedAcc {
+    uint64_t* h = nullptr;
+    PinnedAcc() {
+        if (cudaMallocHost(&h, 64 * sizeof(uint64_t)) != cudaSuccess) h = nullptr;
+    }
+};
+uint64_t* pinned_acc() {
+    static thread_local PinnedAcc p;
+    if (!p.h) throw tm_error(TM_ERR_CUDA, "cannot allocate pinned host buffer");
+    return p.h;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const tm_error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return TM_ERR_CUDA;
+    }
+}
+
+void ensure_device() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw tm_error(TM_ERR_CUDA, "no CUDA device: the B200 path has no CPU fallback");
+}
+
+const std::vector<uint32_t>& host_off(tm_graph* G) {
+    if (G->h_off.size() != G->g.n + 1) {
+        G->h_off.resize(G->g.n + 1);
+        TM_CUDA(cudaMemcpyAsync(G->h_off.data(), G->g.off, (G->g.n + 1) * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, G->g.stream));
+        TM_CUDA(cudaStreamSynchronize(G->g.stream));
+    }
+    return G->h_off;
+}
+
+uint32_t read_u32(const uint32_t* d, uint64_t idx, cudaStream_t s) {
+    uint32_t v = 0;
+    TM_CUDA(cudaMemcpyAsync(&v, d + idx, sizeof(v), cudaMemcpyDeviceToHost, s));
+    TM_CUDA(cudaStreamSynchronize(s));
+    return v;
+}
+
+// one counting pass into the 64-entry device accumulator; returns raw on host
+struct PassResult {
+    uint64_t star_raw[32];
+    uint64_t tri_once[24];
+};
+
+void run_passes(tm_graph* G, int64_t delta, bool do_star, bool do_tri, int tri_mode,
+                uint32_t cb, uint32_t ce, PassResult& r, tm_phase_timings* tm) {
+    DeviceGraph& g = G->g;
+    cudaStream_t s = g.stream;
+    if (!g.d_acc) g.d_acc = dalloc<uint64_t>(64, s);
+    TM_CUDA(cudaMemsetAsync(g.d_acc, 0, 64 * sizeof(uint64_t), s));
+    const bool full = (cb == 0 && ce == g.n);
+    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    if (tm) {
+        TM_CUDA(cudaEventCreate(&e0));
+        TM_CUDA(cudaEventCreate(&e1));
+        TM_CUDA(cudaEventCreate(&e2));
+        TM_CUDA(cudaEventRecord(e0, s));
+    }
+    if (do_star && g.R) {
+        uint32_t qb = 0, qe = (uint32_t)g.R;
+        if (!full) {
+            qb = read_u32(g.off, cb, s);
+            qe = read_u32(g.off, ce, s);
+        }
+        star_full(g, delta, qb, qe, g.d_acc);
+    }
+    if (tm) TM_CUDA(cudaEventRecord(e1, s));
+    if (do_tri && g.R) {
+        const int fm = tri_mode == TM_TRI_REMOVAL ? 1 : 0;
+        build_forward(g, fm);
+        const Forward& f = g.fwd[fm];
+        uint32_t fb = 0, fe = (uint32_t)f.len;
+        if (!full) {
+            fb = read_u32(f.off, cb, s);
+            fe = read_u32(f.off, ce, s);
+        }
+        tri_oriented(g, f, delta, fb, fe, g.d_acc + 32);
+    }
+    if (tm) TM_CUDA(cudaEventRecord(e2, s));
+    uint64_t* h = pinned_acc();
+    TM_CUDA(cudaMemcpyAsync(h, g.d_acc, 64 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    TM_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(r.star_raw, h, 32 * sizeof(uint64_t));
+    std::memcpy(r.tri_once, h + 32, 24 * sizeof(uint64_t));
+    if (tm) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, e0, e1);
+        cudaEventElapsedTime(&b, e1, e2);
+        tm->star_pair_ms = a;
+        tm->triangle_ms = b;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+    }
+}
+
+int run_parallel_impl(tm_graph* G, const tm_run_config* cfg, tm_counters* raw, uint64_t* census,
+                      tm_phase_timings* tm) {
+    if (!G || !cfg) throw tm_error(TM_ERR_INVALID, "null graph or config");
+    if (cfg->workers < 1) throw tm_error(TM_ERR_CONFIG, "workers must be >= 1");
+    if (cfg->delta < 0) throw tm_error(TM_ERR_CONFIG, "delta must be >= 0");
+    if (cfg->triangle_mode == TM_TRI_REMOVAL && cfg->workers > 1)
+        throw tm_error(TM_ERR_CONFIG, "removal triangle mode requires a single worker");
+    if (cfg->triangle_mode != TM_TRI_REMOVAL && cfg->triangle_mode != TM_TRI_COUNT_ALL)
+        throw tm_error(TM_ERR_CONFIG, "triangle mode must be countall or removal");
+    const uint32_t motifs = cfg->motifs ? cfg->motifs : 7u;
+    const uint32_t cb = cfg->center_begin;
+    const uint32_t ce = cfg->center_end ? cfg->center_end : (uint32_t)G->g.n;
+    if (cb > ce || ce > G->g.n) throw tm_error(TM_ERR_INVALID, "bad center partition");
+    const bool full = (cb == 0 && ce == G->g.n);
+
+    PassResult r;
+    auto t0 = std::chrono::steady_clock::now();
+    run_passes(G, cfg->delta, (motifs & 3u) != 0, (motifs & 4u) != 0, cfg->triangle_mode, cb, ce, r,
+               tm);
+    tm_counters out;
+    std::memset(&out, 0, sizeof(out));
+    finish_star(r.star_raw, out.star, out.pair);
+    if (cfg->triangle_mode == TM_TRI_COUNT_ALL) expand_count_all(r.tri_once, out.tri);
+    else std::memcpy(out.tri, r.tri_once, sizeof(out.tri));
+    if (!(motifs & TM_MOTIF_STAR)) std::memset(out.star, 0, sizeof(out.star));
+    if (!(motifs & TM_MOTIF_PAIR)) std::memset(out.pair, 0, sizeof(out.pair));
+    if (!(motifs & TM_MOTIF_TRIANGLE)) std::memset(out.tri, 0, sizeof(out.tri));
+    if (raw) *raw = out;
+    auto t1 = std::chrono::steady_clock::now();
+    if (census) {
+        std::memset(census, 0, 36 * sizeof(uint64_t));
+        if (full) {
+            int rc = merge_census_impl(out.star, out.pair, out.tri, cfg->triangle_mode, census);
+            if (rc) throw tm_error(rc, g_last_error.empty() ? "merge failed" : g_last_error);
+        }
+    }
+    if (tm) tm->merge_ms = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t1).count();
+    (void)t0;
+    return TM_OK;
+}
+
+tm_graph* build_impl(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
+                     uint64_t n, int device_ptrs, void* stream, double* index_ms) {
+    ensure_device();
+    if (m && (!src || !dst || !t)) throw tm_error(TM_ERR_INVALID, "null edge arrays");
+    auto* G = new tm_graph();
+    try {
+        if (stream) {
+            G->g.stream = static_cast<cudaStream_t>(stream);
+        } else {
+            TM_CUDA(cudaStreamCreateWithFlags(&G->g.stream, cudaStreamNonBlocking));
+            G->g.owns_stream = true;
+        }
+        cudaStream_t s = G->g.stream;
+        static bool pool_set = false;
+        if (!pool_set) {  // keep freed blocks in the pool across steps
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            pool_set = true;
+        }
+        cudaEvent_t e0, e1;
+        if (index_ms) {
+            TM_CUDA(cudaEventCreate(&e0));
+            TM_CUDA(cudaEventCreate(&e1));
+            TM_CUDA(cudaEventRecord(e0, s));
+        }
+        const uint32_t *ds = src, *dd = dst;
+        const int64_t* dt = t;
+        uint32_t *hs = nullptr, *hd = nullptr;
+        int64_t* ht = nullptr;
+        if (!device_ptrs && m) {
+            hs = dalloc<uint32_t>(m, s);
+            hd = dalloc<uint32_t>(m, s);
+            ht = dalloc<int64_t>(m, s);
+            TM_CUDA(cudaMemcpyAsync(hs, src, m * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+            TM_CUDA(cudaMemcpyAsync(hd, dst, m * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+            TM_CUDA(cudaMemcpyAsync(ht, t, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+            ds = hs;
+            dd = hd;
+            dt = ht;
+        }
+        build_graph(G->g, ds, dd, dt, m, n);
+        dfree(hs, s);
+        dfree(hd, s);
+        dfree(ht, s);
+        if (index_ms) {
+            TM_CUDA(cudaEventRecord(e1, s));
+            TM_CUDA(cudaEventSynchronize(e1));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            *index_ms = ms;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
+    } catch (...) {
+        free_graph(G->g);
+        if (G->g.owns_stream) cudaStreamDestroy(G->g.stream);
+        delete G;
+        throw;
+    }
+    return G;
+}
+
+void free_impl(tm_graph* G) {
+    if (!G) return;
+    free_graph(G->g);
+    cudaStreamSynchronize(G->g.stream);
+    if (G->g.owns_stream) cudaStreamDestroy(G->g.stream);
+    delete G;
+}
+
+}  // namespace
+}  // namespace tmb
+
+using namespace tmb;
+
+extern "C" {
+
+int tm_graph_build(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
+                   uint64_t n, int device_ptrs, void* stream, tm_graph** out) {
+    return guarded([&] {
+        if (!out) throw tm_error(TM_ERR_INVALID, "null output handle");
+        *out = build_impl(src, dst, t, m, n, device_ptrs, stream, nullptr);
+        return TM_OK;
+    });
+}
+
+void tm_graph_free(tm_graph* g) {
+    try {
+        free_impl(g);
+    } catch (...) {
+    }
+}
+
+uint64_t tm_graph_node_count(const tm_graph* g) { return g ? g->g.n : 0; }
+uint64_t tm_graph_edge_count(const tm_graph* g) { return g ? g->g.m : 0; }
+void* tm_graph_stream(const tm_graph* g) { return g ? (void*)g->g.stream : nullptr; }
+
+int tm_graph_degrees(const tm_graph* g, uint64_t* out) {
+    return guarded([&] {
+        auto* G = const_cast<tm_graph*>(g);
+        const auto& off = host_off(G);
+        for (uint64_t u = 0; u < G->g.n; ++u) out[u] = off[u + 1] - off[u];
+        return TM_OK;
+    });
+}
+
+int tm_graph_sequence(const tm_graph* g, uint32_t u, int64_t* t, uint64_t* ordinal, uint32_t* other,
+                      uint8_t* dir, uint64_t cap, uint64_t* len) {
+    return guarded([&] {
+        auto* G = const_cast<tm_graph*>(g);
+        if (u >= G->g.n) throw tm_error(TM_ERR_INVALID, "node out of range");
+        const auto& off = host_off(G);
+        const uint64_t b = off[u], s = off[u + 1] - off[u];
+        if (len) *len = s;
+        if (s > cap) return TM_ERR_INVALID;
+        std::vector<int64_t> ht(s);
+        std::vector<uint32_t> hn(s), ho(s);
+        cudaStream_t st = G->g.stream;
+        if (s) {
+            TM_CUDA(cudaMemcpyAsync(ht.data(), G->g.S_t + b, s * 8, cudaMemcpyDeviceToHost, st));
+            TM_CUDA(cudaMemcpyAsync(hn.data(), G->g.S_nbr + b, s * 4, cudaMemcpyDeviceToHost, st));
+            TM_CUDA(cudaMemcpyAsync(ho.data(), G->g.S_ord + b, s * 4, cudaMemcpyDeviceToHost, st));
+            TM_CUDA(cudaStreamSynchronize(st));
+        }
+        for (uint64_t k = 0; k < s; ++k) {
+            if (t) t[k] = ht[k];
+            if (ordinal) ordinal[k] = ho[k];
+            if (other) other[k] = hn[k] & kNodeMask;
+            if (dir) dir[k] = (uint8_t)(hn[k] >> 31);
+        }
+        return TM_OK;
+    });
+}
+
+int tm_pair_window(const tm_graph* g, uint32_t v, uint32_t w, int64_t lo, int64_t hi, int64_t* t,
+                   uint64_t* ordinal, uint8_t* dir_rel_v, uint64_t cap, uint64_t* len) {
+    return guarded([&] {
+        auto* G = const_cast<tm_graph*>(g);
+        if (v >= G->g.n || w >= G->g.n) throw tm_error(TM_ERR_INVALID, "node out of range");
+        if (len) *len = 0;
+        cudaStream_t st = G->g.stream;
+        const uint32_t g0 = read_u32(G->g.node_grp, v, st), g1 = read_u32(G->g.node_grp, v + 1, st);
+        std::vector<uint32_t> nb(g1 - g0);
+        if (g1 > g0) {
+            TM_CUDA(cudaMemcpyAsync(nb.data(), G->g.grp_nbr + g0, (g1 - g0) * 4,
+                                    cudaMemcpyDeviceToHost, st));
+            TM_CUDA(cudaStreamSynchronize(st));
+        }
+        auto it = std::lower_bound(nb.begin(), nb.end(), w);
+        if (it == nb.end() || *it != w || lo > hi) return TM_OK;
+        const uint32_t gi = g0 + (uint32_t)(it - nb.begin());
+        const uint32_t kb = read_u32(G->g.grp_off, gi, st), ke = read_u32(G->g.grp_off, gi + 1, st);
+        std::vector<int64_t> ht(ke - kb);
+        std::vector<uint32_t> ho(ke - kb), hw(ke - kb);
+        TM_CUDA(cudaMemcpyAsync(ht.data(), G->g.G_t + kb, (ke - kb) * 8, cudaMemcpyDeviceToHost, st));
+        TM_CUDA(cudaMemcpyAsync(ho.data(), G->g.G_ord + kb, (ke - kb) * 4, cudaMemcpyDeviceToHost, st));
+        TM_CUDA(cudaMemcpyAsync(hw.data(), G->g.G_w2 + kb, (ke - kb) * 4, cudaMemcpyDeviceToHost, st));
+        TM_CUDA(cudaStreamSynchronize(st));
+        uint64_t k = 0;
+        for (uint32_t x = 0; x < ke - kb; ++x) {
+            if (ht[x] < lo || ht[x] > hi) continue;
+            if (k < cap) {
+                if (t) t[k] = ht[x];
+                if (ordinal) ordinal[k] = ho[x];
+                if (dir_rel_v) dir_rel_v[k] = (uint8_t)(hw[x] >> 31);
+            }
+            ++k;
+        }
+        if (len) *len = k;
+        return k > cap ? TM_ERR_INVALID : TM_OK;
+    });
+}
+
+int tm_auto_degree_threshold(const tm_graph* g, uint64_t* out) {
+    return guarded([&] {
+        auto* G = const_cast<tm_graph*>(g);
+        const auto& off = host_off(G);
+        std::vector<uint64_t> d(G->g.n);
+        for (uint64_t u = 0; u < G->g.n; ++u) d[u] = off[u + 1] - off[u];
+        if (d.empty()) {
+            *out = 0;
+            return TM_OK;
+        }
+        if (d.size() < 20) {
+            *out = *std::max_element(d.begin(), d.end());
+            return TM_OK;
+        }
+        std::nth_element(d.begin(), d.begin() + 19, d.end(), std::greater<uint64_t>());
+        *out = d[19];
+        return TM_OK;
+    });
+}
+
+int tm_count_star_pair(tm_graph* g, int64_t delta, uint64_t* star24, uint64_t* pair8) {
+    return guarded([&] {
+        if (delta < 0) throw tm_error(TM_ERR_CONFIG, "delta must be >= 0");
+        PassResult r;
+        run_passes(g, delta, true, false, 0, 0, (uint32_t)g->g.n, r, nullptr);
+        finish_star(r.star_raw, star24, pair8);
+        return TM_OK;
+    });
+}
+
+int tm_count_triangles(tm_graph* g, int64_t delta, int mode, uint64_t* tri24) {
+    return guarded([&] {
+        if (delta < 0) throw tm_error(TM_ERR_CONFIG, "delta must be >= 0");
+        if (mode != TM_TRI_COUNT_ALL && mode != TM_TRI_REMOVAL)
+            throw tm_error(TM_ERR_CONFIG, "triangle mode must be countall or removal");
+        PassResult r;
+        run_passes(g, delta, false, true, mode, 0, (uint32_t)g->g.n, r, nullptr);
+        if (mode == TM_TRI_COUNT_ALL) expand_count_all(r.tri_once, tri24);
+        else std::memcpy(tri24, r.tri_once, 24 * sizeof(uint64_t));
+        return TM_OK;
+    });
+}
+
+int tm_count_star_pair_items(tm_graph* g, int64_t delta, uint64_t n_items, const uint32_t* nodes,
+                             const uint64_t* begin, const uint64_t* end, uint64_t* star_out,
+                             uint64_t* pair_out) {
+    return guarded([&] {
+        if (delta < 0) throw tm_error(TM_ERR_CONFIG, "delta must be >= 0");
+        const auto& off = host_off(g);
+        std::vector<uint64_t> fo(n_items + 1, 0), to(n_items + 1, 0), b(n_items), e(n_items);
+        for (uint64_t it = 0; it < n_items; ++it) {
+            if (nodes[it] >= g->g.n) throw tm_error(TM_ERR_INVALID, "node out of range");
+            const uint64_t s = off[nodes[it] + 1] - off[nodes[it]];
+            b[it] = std::min<uint64_t>(begin[it], s);
+            e[it] = std::min<uint64_t>(std::max(end[it], b[it]), s);
+            fo[it + 1] = fo[it] + (e[it] - b[it]);
+            to[it + 1] = to[it] + (s > b[it] + 1 ? s - b[it] - 1 : 0);
+            if (end[it] <= begin[it]) to[it + 1] = to[it];  // empty range counts nothing
+        }
+        cudaStream_t s = g->g.stream;
+        uint32_t* dn = dalloc<uint32_t>(n_items, s);
+        uint64_t *db = dalloc<uint64_t>(n_items, s), *de = dalloc<uint64_t>(n_items, s);
+        uint64_t *dfo = dalloc<uint64_t>(n_items + 1, s), *dto = dalloc<uint64_t>(n_items + 1, s);
+        uint64_t* dout = dalloc<uint64_t>(n_items * 32, s);
+        TM_CUDA(cudaMemcpyAsync(dn, nodes, n_items * 4, cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaMemcpyAsync(db, b.data(), n_items * 8, cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaMemcpyAsync(de, e.data(), n_items * 8, cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaMemcpyAsync(dfo, fo.data(), (n_items + 1) * 8, cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaMemcpyAsync(dto, to.data(), (n_items + 1) * 8, cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaMemsetAsync(dout, 0, n_items * 32 * 8, s));
+        star_items(g->g, delta, n_items, dn, db, de, dfo, fo[n_items], to[n_items], dto, dout);
+        std::vector<uint64_t> raw(n_items * 32);
+        TM_CUDA(cudaMemcpyAsync(raw.data(), dout, n_items * 32 * 8, cudaMemcpyDeviceToHost, s));
+        dfree(dn, s); dfree(db, s); dfree(de, s); dfree(dfo, s); dfree(dto, s); dfree(dout, s);
+        TM_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t it = 0; it < n_items; ++it)
+            finish_star(&raw[it * 32], star_out ? star_out + it * 24 : nullptr,
+                        pair_out ? pair_out + it * 8 : nullptr);
+        return TM_OK;
+    });
+}
+
+int tm_count_triangles_items(tm_graph* g, int64_t delta, uint64_t n_items, const uint32_t* nodes,
+                             const uint64_t* begin, const uint64_t* end, const uint8_t* live,
+                             uint64_t* tri_out) {
+    return guarded([&] {
+        if (delta < 0) throw tm_error(TM_ERR_CONFIG, "delta must be >= 0");
+        const auto& off = host_off(g);
+        std::vector<uint64_t> io(n_items + 1, 0), b(n_items);
+        for (uint64_t it = 0; it < n_items; ++it) {
+            if (nodes[it] >= g->g.n) throw tm_error(TM_ERR_INVALID, "node out of range");
+            const uint64_t s = off[nodes[it] + 1] - off[nodes[it]];
+            const uint64_t lim = s >= 2 ? s - 1 : 0;
+            b[it] = std::min<uint64_t>(begin[it], lim);
+            const uint64_t e = std::min<uint64_t>(std::max(end[it], b[it]), lim);
+            io[it + 1] = io[it] + (e - b[it]);
+        }
+        cudaStream_t s = g->g.stream;
+        uint32_t* dn = dalloc<uint32_t>(n_items, s);
+        uint64_t *db = dalloc<uint64_t>(n_items, s), *dio = dalloc<uint64_t>(n_items + 1, s);
+        uint64_t* dout = dalloc<uint64_t>(n_items * 24, s);
+        uint8_t* dl = nullptr;
+        TM_CUDA(cudaMemcpyAsync(dn, nodes, n_items * 4, cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaMemcpyAsync(db, b.data(), n_items * 8, cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaMemcpyAsync(dio, io.data(), (n_items + 1) * 8, cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaMemsetAsync(dout, 0, n_items * 24 * 8, s));
+        if (live) {
+            dl = dalloc<uint8_t>(g->g.n, s);
+            TM_CUDA(cudaMemcpyAsync(dl, live, g->g.n, cudaMemcpyHostToDevice, s));
+        }
+        tri_items(g->g, delta, n_items, dn, db, dio, io[n_items], dl, dout);
+        TM_CUDA(cudaMemcpyAsync(tri_out, dout, n_items * 24 * 8, cudaMemcpyDeviceToHost, s));
+        dfree(dn, s); dfree(db, s); dfree(dio, s); dfree(dout, s); dfree(dl, s);
+        TM_CUDA(cudaStreamSynchronize(s));
+        return TM_OK;
+    });
+}
+
+int tm_run_parallel(tm_graph* g, const tm_run_config* cfg, tm_counters* raw, uint64_t* census36,
+                    tm_phase_timings* timings) {
+    return guarded([&] { return run_parallel_impl(g, cfg, raw, census36, timings); });
+}
+
+int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
+                   uint64_t n, int device_ptrs, void* stream, const tm_run_config* cfg,
+                   tm_counters* raw, uint64_t* census36, tm_phase_timings* timings) {
+    return guarded([&] {
+        double index_ms = 0;
+        tm_graph* G = build_impl(src, dst, t, m, n, device_ptrs, stream, timings ? &index_ms : nullptr);
+        int rc;
+        try {
+            rc = run_parallel_impl(G, cfg, raw, census36, timings);
+        } catch (...) {
+            free_impl(G);
+            throw;
+        }
+        free_impl(G);
+        if (timings) timings->index_ms = index_ms;
+        return rc;
+    });
+}
+
+int tm_partition_centers(const tm_graph* g, uint32_t world, uint32_t rank, uint32_t* begin,
+                         uint32_t* end) {
+    return guarded([&] {
+        if (world == 0 || rank >= world) throw tm_error(TM_ERR_INVALID, "bad rank/world");
+        auto* G = const_cast<tm_graph*>(g);
+        const uint64_t n = G->g.n;
+        const auto& off = host_off(G);
+        // cost(u) = |S_u| + |F_u| (star records + forward wedges' first edges)
+        build_forward(G->g, 0);
+        std::vector<uint32_t> foff(n + 1);
+        TM_CUDA(cudaMemcpyAsync(foff.data(), G->g.fwd[0].off, (n + 1) * 4, cudaMemcpyDeviceToHost,
+                                G->g.stream));
+        TM_CUDA(cudaStreamSynchronize(G->g.stream));
+        const uint64_t total = (uint64_t)off[n] + foff[n];
+        auto bound = [&](uint64_t r) -> uint32_t {
+            if (r == 0) return 0;
+            if (r >= world) return (uint32_t)n;
+            const uint64_t target = total * r / world;
+            uint64_t lo = 0, hi = n;  // first u with cost prefix >= target
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) / 2;
+                if ((uint64_t)off[mid] + foff[mid] < target) lo = mid + 1; else hi = mid;
+            }
+            return (uint32_t)lo;
+        };
+        *begin = bound(rank);
+        *end = bound(rank + 1);
+        return TM_OK;
+    });
+}
+
+int tm_merge_census(const uint64_t* star24, const uint64_t* pair8, const uint64_t* tri24, int mode,
+                    uint64_t* census36) {
+    return guarded([&] { return merge_census_impl(star24, pair8, tri24, mode, census36); });
+}
+
+int tm_signature(int idx, char* out9) {
+    const auto& u = universe();
+    if (idx < 0 || idx >= (int)u.all.size()) return TM_ERR_INVALID;
+    std::memcpy(out9, u.all[idx].c_str(), 9);
+    return TM_OK;
+}
+
+int tm_cell_signature(int kind, int cell) {
+    const auto& u = universe();
+    if (kind == 0 && cell >= 0 && cell < 24) return u.star_sig[cell];
+    if (kind == 1 && cell >= 0 && cell < 8) return u.pair_sig[cell];
+    if (kind == 2 && cell >= 0 && cell < 24) return u.tri_sig[cell];
+    return -1;
+}
+
+int tm_signature_label(int idx, char* out16) {
+    // anchored M_ij names (motifs.cpp:207-219); others label as themselves
+    static const std::map<std::string, std::string> anchors = {
+        {"12|23|32", "M_24"}, {"12|31|23", "M_25"}, {"12|23|31", "M_26"},
+        {"12|32|31", "M_46"}, {"12|12|12", "M_55"}, {"12|21|21", "M_56"},
+        {"12|12|31", "M_63"}, {"12|21|12", "M_65"}, {"12|12|21", "M_66"},
+    };
+    const auto& u = universe();
+    if (idx < 0 || idx >= (int)u.all.size()) return TM_ERR_INVALID;
+    auto it = anchors.find(u.all[idx]);
+    const std::string& s = it != anchors.end() ? it->second : u.all[idx];
+    std::memcpy(out16, s.c_str(), s.size() + 1);
+    return TM_OK;
+}
+
+int tm_generate_random_graph(uint64_t nodes, uint64_t m, int64_t t_max, uint64_t seed, uint32_t* src,
+                             uint32_t* dst, int64_t* t) {
+    if (m > 0 && nodes < 2) {
+        g_last_error = "need at least 2 nodes to place edges";
+        return TM_ERR_INVALID;
+    }
+    if (t_max < 0) {
+        g_last_error = "t_max must be non-negative";
+        return TM_ERR_INVALID;
+    }
+    std::mt19937_64 rng(seed);
+    auto draw = [&](uint64_t bound) -> uint64_t {
+        if (bound == 0) return 0;
+        const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+        uint64_t x;
+        do {
+            x = rng();
+        } while (x >= limit);
+        return x % bound;
+    };
+    for (uint64_t i = 0; i < m; ++i) {
+        const uint32_t s = (uint32_t)draw(nodes);
+        const uint32_t o = (uint32_t)draw(nodes - 1);
+        src[i] = s;
+        dst[i] = o + (o >= s ? 1 : 0);
+        t[i] = (int64_t)draw((uint64_t)t_max + 1);
+    }
+    return TM_OK;
+}
+
+const char* tm_last_error(void) { return g_last_error.c_str(); }
+uint64_t tm_kernel_launches(void) { return g_launches.load(); }
+void tm_kernel_timing_enable(int on) { g_timing.store(on ? 1 : 0); }
+
+void tm_kernel_timing_reset(void) {
+    std::lock_guard<std::mutex> lk(g_timing_mu);
+    for (auto& p : g_pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    g_pending.clear();
+    g_ktotals.clear();
+}
+
+int tm_kernel_timing_get(const char* name, double* total_ms, uint64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_timing_mu);
+    for (auto& p : g_pending) {
+        cudaEventSynchronize(p.b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        auto& tot = g_ktotals[p.name];
+        tot.first += ms;
+        tot.second += 1;
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    g_pending.clear();
+    auto it = g_ktotals.find(name);
+    if (total_ms) *total_ms = it == g_ktotals.end() ? 0.0 : it->second.first;
+    if (launches) *launches = it == g_ktotals.end() ? 0 : it->second.second;
+    return TM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,178 @@
+// tm_internal.cuh -- shared device structures of the B200 temporal motif path.
+//
+// HBM layout (all positions are 32-bit; R = 2m incident records):
+//   S (time-ordered per-node sequences, NodeSequenceIndex, indexes.hpp:22-40)
+//     S_t[R]    int64  timestamp
+//     S_nbr[R]  u32    other endpoint | dir << 31   (dir 0 = outward)
+//     S_ord[R]  u32    ingestion ordinal
+//     S_node[R] u32    center node
+//     S_pg[R+1] u32    global exclusive prefix count of outward records
+//     S_gidx[R] u32    position of this record in G
+//     off[n+1]  u32    CSR offsets
+//   G (per-node records grouped by neighbour, time-ordered inside a group;
+//      its (v, w) groups double as PairEdgeIndex, indexes.hpp:63-92)
+//     G_t[R]    int64
+//     G_ord[R]  u32
+//     G_w2[R]   u32    local S position (29 b) | first<<29 | last<<30 | dir<<31
+//     G_pg[R]   u32    S_pg at that record's S position
+//     G_dscan[R+1] u32 exclusive prefix count of inward records in G order
+//     grp_nbr[ng], grp_off[ng+1], node_grp[n+1]   group table
+//   F (forward-oriented sequences for the triangle pass, one per orientation)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace tmb {
+
+constexpr uint32_t kDirBit = 0x80000000u;
+constexpr uint32_t kNodeMask = 0x7fffffffu;
+constexpr uint32_t kFirstBit = 1u << 29;
+constexpr uint32_t kLastBit = 1u << 30;
+constexpr uint32_t kPosMask = (1u << 29) - 1;
+
+struct tm_error : std::runtime_error {
+    int code;
+    tm_error(int c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+
+void check_cuda(cudaError_t e, const char* what, const char* file, int line);
+#define TM_CUDA(x) ::tmb::check_cuda((x), #x, __FILE__, __LINE__)
+
+// launch accounting + optional CUDA-event timing per kernel name
+void note_launch();
+struct KernelScope {
+    const char* name;
+    cudaStream_t stream;
+    void* ev0;
+    KernelScope(const char* n, cudaStream_t s);
+    ~KernelScope();
+};
+#define TM_LAUNCH(name, stream, kernel, grid, block, smem, ...)                    \
+    do {                                                                           \
+        ::tmb::KernelScope _ks(name, stream);                                      \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                \
+        TM_CUDA(cudaGetLastError());                                               \
+        ::tmb::note_launch();                                                      \
+    } while (0)
+
+int sm_count();
+
+// stream-ordered device allocation from the default mempool
+template <typename T>
+T* dalloc(size_t count, cudaStream_t s) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    TM_CUDA(cudaMallocAsync(&p, count * sizeof(T), s));
+    return static_cast<T*>(p);
+}
+template <typename T>
+void dfree(T*& p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+}
+
+struct Forward {
+    bool valid = false;
+    int mode = 0;  // 0: degree rank (count_all), 1: node index (removal)
+    uint64_t len = 0;
+    int64_t* t = nullptr;
+    uint32_t* nbr = nullptr;
+    uint32_t* ord = nullptr;
+    uint32_t* node = nullptr;
+    uint32_t* off = nullptr;  // n+1
+};
+
+struct DeviceGraph {
+    uint64_t n = 0, m = 0, R = 0, ng = 0;
+    uint32_t max_degree = 0;
+    cudaStream_t stream = nullptr;
+    bool owns_stream = false;
+
+    int64_t* S_t = nullptr;
+    uint32_t* S_nbr = nullptr;
+    uint32_t* S_ord = nullptr;
+    uint32_t* S_node = nullptr;
+    uint32_t* S_pg = nullptr;
+    uint32_t* S_gidx = nullptr;
+    uint32_t* off = nullptr;
+
+    int64_t* G_t = nullptr;
+    uint32_t* G_ord = nullptr;
+    uint32_t* G_w2 = nullptr;
+    uint32_t* G_pg = nullptr;
+    uint32_t* G_dscan = nullptr;
+    uint32_t* grp_nbr = nullptr;
+    uint32_t* grp_off = nullptr;
+    uint32_t* node_grp = nullptr;
+
+    Forward fwd[2];
+
+    uint64_t* d_acc = nullptr;     // 64 u64 device accumulators
+    uint64_t* h_acc = nullptr;     // pinned mirror
+};
+
+// read-only views passed by value to kernels
+struct SView {
+    const int64_t* t;
+    const uint32_t* nbr;
+    const uint32_t* ord;
+    const uint32_t* node;
+    const uint32_t* pg;
+    const uint32_t* gidx;
+    const uint32_t* off;
+};
+struct GView {
+    const int64_t* t;
+    const uint32_t* ord;
+    const uint32_t* w2;
+    const uint32_t* pg;
+    const uint32_t* dscan;
+    const uint32_t* grp_nbr;
+    const uint32_t* grp_off;
+    const uint32_t* node_grp;
+};
+inline SView sview(const DeviceGraph& g) {
+    return {g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_pg, g.S_gidx, g.off};
+}
+inline GView gview(const DeviceGraph& g) {
+    return {g.G_t, g.G_ord, g.G_w2, g.G_pg, g.G_dscan, g.grp_nbr, g.grp_off, g.node_grp};
+}
+
+// ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------
+void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst,
+                 const int64_t* d_t, uint64_t m, uint64_t n);
+void free_graph(DeviceGraph& g);
+void build_forward(DeviceGraph& g, int mode);
+
+// raw star sums (32 u64: Pair[8], C[8], B[8], A[8]) for S positions
+// [q_begin, q_end), added into d_out.
+void star_full(const DeviceGraph& g, int64_t delta, uint32_t q_begin, uint32_t q_end,
+               uint64_t* d_out);
+void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
+                const uint64_t* d_begin, const uint64_t* d_end, const uint64_t* d_item_off,
+                uint64_t total_first, uint64_t total_third, const uint64_t* d_third_off,
+                uint64_t* d_out);
+// once-counted triangle cells (24 u64) over forward positions [f_begin, f_end)
+void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
+                  uint32_t f_end, uint64_t* d_out);
+void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
+               const uint64_t* d_begin, const uint64_t* d_item_off, uint64_t total,
+               const uint8_t* d_live, uint64_t* d_out);
+
+// ---- saturating arithmetic (types.hpp:72-89) ------------------------------
+__host__ __device__ inline int64_t sat_add(int64_t a, int64_t b) {
+    if (b > 0 && a > INT64_MAX - b) return INT64_MAX;
+    if (b < 0 && a < INT64_MIN - b) return INT64_MIN;
+    return a + b;
+}
+__host__ __device__ inline int64_t sat_sub(int64_t a, int64_t b) {
+    if (b < 0 && a > INT64_MAX + b) return INT64_MAX;
+    if (b > 0 && a < INT64_MIN + b) return INT64_MIN;
+    return a - b;
+}
+
+}  // namespace tmb

@@ -1,0 +1,299 @@
+// tm_star.cu -- FAST-Star (Algorithm 1, star_engine.cpp:64-127) on B200.
+//
+// The reference walks, for every first edge a of S_u, all third edges c in the
+// delta window and keeps per-neighbour tallies of the edges in between
+// (m_in / m_out), i.e. O(|S_u| * d^delta) per center.  Every tally it reads is
+// a count of same-neighbour records in a position interval, so the same cells
+// can be written as sums over the *neighbour group* of one record only:
+//
+//   for first edge a (window W(a) = (a, e(a)), g = group of a):
+//     Pair[d1,d2,d3]   += #{b<c in W, x_b = x_c = x_a}
+//     A                 = #{b<c in W, x_b = x_a}           Star-III = A - Pair
+//     B                 = #{b<c in W, x_c = x_a}           Star-II  = B - Pair
+//   and, charged to the third edge c (lo(c) = first index with t >= t_c - d):
+//     C                 = sum over b in g(c), lo(c) < b < c of
+//                         #{a in [lo(c), b), dir_a = d1}   Star-I   = C - Pair
+//
+// A, B and Pair only need the same-neighbour records of a inside its window
+// (walked in G, which stores each group contiguously) plus global prefix
+// counts of outward records (S_pg); C walks the same-neighbour records of c
+// backwards.  Each record is handled by one thread, so a hub needs no special
+// treatment and there is no per-center state at all.  Work per record is
+// O(log d^delta) for the window search plus the same-neighbour window length.
+//
+// Output: 32 raw u64 sums  [0..8) Pair, [8..16) C, [16..24) B, [24..32) A,
+// each indexed d1*4 + d2*2 + d3; the host forms Star = raw - Pair
+// (all arithmetic modulo 2^64, exact because every final cell is >= 0).
+#include "tm_primitives.cuh"
+
+namespace tmb {
+
+namespace {
+
+// first index in [beg, end) with T[idx] > lim (end if none); T ascending
+__device__ __forceinline__ uint32_t gallop_upper(const int64_t* __restrict__ T, uint32_t beg,
+                                                 uint32_t end, int64_t lim) {
+    uint32_t lo = beg, hi = end;
+    uint32_t span = 1;
+    while (true) {
+        const uint64_t probe = (uint64_t)lo + span - 1;
+        if (probe >= end) break;
+        if (T[probe] > lim) {
+            hi = (uint32_t)probe;
+            break;
+        }
+        lo = (uint32_t)probe + 1;
+        span <<= 1;
+    }
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (T[mid] > lim) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+// first index in [beg, from] with T[idx] >= lim, given T[from] >= lim
+__device__ __forceinline__ uint32_t gallop_lower_back(const int64_t* __restrict__ T, uint32_t beg,
+                                                      uint32_t from, int64_t lim) {
+    uint32_t hi = from, lo = beg;
+    uint32_t span = 1;
+    while (true) {
+        if (hi < beg + span) break;
+        const uint32_t probe = hi - span;
+        if (T[probe] < lim) {
+            lo = probe + 1;
+            break;
+        }
+        hi = probe;
+        span <<= 1;
+    }
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (T[mid] >= lim) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+struct StarAcc {
+    uint64_t v[32];
+};
+
+__device__ __forceinline__ void add_d1(StarAcc& acc, int base, uint32_t d1, const uint64_t x[4]) {
+    const uint64_t m0 = d1 ? 0ull : ~0ull;
+    const uint64_t m1 = ~m0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        acc.v[base + j] += x[j] & m0;
+        acc.v[base + 4 + j] += x[j] & m1;
+    }
+}
+
+// first-edge role of S position q (node range [start, end)): Pair, A, B.
+__device__ __forceinline__ void first_role(const SView& S, const GView& G, uint32_t q,
+                                           uint32_t start, uint32_t end, int64_t delta,
+                                           StarAcc& acc) {
+    const int64_t ta = S.t[q];
+    const uint32_t da = S.nbr[q] >> 31;
+    const int64_t lim = sat_add(ta, delta);
+    uint32_t k = S.gidx[q];
+    if (G.w2[k] & kLastBit) return;
+    if (G.t[k + 1] > lim) return;  // no same-neighbour record in the window
+
+    const uint32_t base = S.pg[start];
+    const uint32_t e = gallop_upper(S.t, q + 1, end, lim);
+    const uint64_t pe_o = S.pg[e] - base, pe_i = (uint64_t)(e - start) - pe_o;
+    const uint64_t pa_o = (uint64_t)(S.pg[q] - base) + (da ? 0u : 1u);
+    const uint64_t pa_i = (uint64_t)(q - start + 1) - pa_o;
+
+    uint64_t n0 = 0, n1 = 0;
+    uint64_t A00 = 0, A01 = 0, A10 = 0, A11 = 0;   // A[d2][d3]: sum [dir_b=d2] P_d3(b+1)
+    uint64_t B00 = 0, B01 = 0, B10 = 0, B11 = 0;   // B[d3][d2]: sum [dir_c=d3] P_d2(c)
+    uint64_t P00 = 0, P01 = 0, P10 = 0, P11 = 0;   // Pair[d2][d3]
+    for (++k;; ++k) {
+        if (G.t[k] > lim) break;
+        const uint32_t w2 = G.w2[k];
+        const uint64_t pos = w2 & kPosMask;
+        const uint64_t pb_o = G.pg[k] - base;
+        const uint64_t pb_i = pos - pb_o;
+        if (w2 & kDirBit) {  // inward
+            A10 += pb_o;
+            A11 += pos + 1 - pb_o;
+            B10 += pb_o;
+            B11 += pb_i;
+            P01 += n0;
+            P11 += n1;
+            ++n1;
+        } else {
+            A00 += pb_o + 1;
+            A01 += pos - pb_o;
+            B00 += pb_o;
+            B01 += pb_i;
+            P00 += n0;
+            P10 += n1;
+            ++n0;
+        }
+        if (w2 & kLastBit) break;
+    }
+    uint64_t pair[4] = {P00, P01, P10, P11};
+    // A(d2,d3) = n[d2] * P_d3(e) - Aacc[d2][d3]
+    uint64_t a[4] = {n0 * pe_o - A00, n0 * pe_i - A01, n1 * pe_o - A10, n1 * pe_i - A11};
+    // B(d2,d3) = Bacc[d3][d2] - n[d3] * P_d2(a+1)
+    uint64_t b[4] = {B00 - n0 * pa_o, B10 - n1 * pa_o, B01 - n0 * pa_i, B11 - n1 * pa_i};
+    add_d1(acc, 0, da, pair);
+    add_d1(acc, 24, da, a);
+    add_d1(acc, 16, da, b);
+}
+
+// third-edge role of S position q: the Star-I pair term C.
+// rb/re: first-edge range (local), clipped; full run passes rb=0, re=s.
+__device__ __forceinline__ void third_role(const SView& S, const GView& G, uint32_t q,
+                                           uint32_t start, int64_t delta, uint32_t rb,
+                                           uint32_t re, StarAcc& acc) {
+    uint32_t k = S.gidx[q];
+    if (G.w2[k] & kFirstBit) return;
+    const int64_t tc = S.t[q];
+    const int64_t lo_lim = sat_sub(tc, delta);
+    // quick reject: previous same-neighbour record already before the window
+    if (G.t[k - 1] < lo_lim) return;
+    const uint32_t dc = S.nbr[q] >> 31;
+    const uint32_t lo = gallop_lower_back(S.t, start, q, lo_lim);
+    const uint32_t L = max(lo, start + rb);
+    const uint32_t pl = S.pg[L];
+    const uint32_t hiq = start + re;
+    uint64_t x0 = 0, x1 = 0, y0 = 0, y1 = 0;  // x: d1 = out, y: d1 = in ; index d2
+    for (--k;; --k) {
+        const uint32_t w2 = G.w2[k];
+        const uint32_t posb = start + (w2 & kPosMask);
+        if (posb <= L) break;
+        const uint32_t mhi = min(posb, hiq);
+        if (mhi > L) {
+            const uint64_t x = (uint64_t)((mhi == posb ? G.pg[k] : S.pg[mhi]) - pl);
+            const uint64_t y = (uint64_t)(mhi - L) - x;
+            if (w2 & kDirBit) { x1 += x; y1 += y; } else { x0 += x; y0 += y; }
+        }
+        if (w2 & kFirstBit) break;
+    }
+    // cells C[d1][d2][dc]
+    const uint64_t mo = dc ? 0ull : ~0ull, mi = ~mo;
+    acc.v[8 + 0 + 0 + 0] += x0 & mo;
+    acc.v[8 + 0 + 0 + 1] += x0 & mi;
+    acc.v[8 + 0 + 2 + 0] += x1 & mo;
+    acc.v[8 + 0 + 2 + 1] += x1 & mi;
+    acc.v[8 + 4 + 0 + 0] += y0 & mo;
+    acc.v[8 + 4 + 0 + 1] += y0 & mi;
+    acc.v[8 + 4 + 2 + 0] += y1 & mo;
+    acc.v[8 + 4 + 2 + 1] += y1 & mi;
+}
+
+// block-reduce 32 u64 and add into out[0..32)
+__device__ __forceinline__ void flush_acc(StarAcc& acc, uint64_t* out) {
+    __shared__ uint64_t red[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        uint64_t v = acc.v[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == j) red[w][j] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        uint64_t s = 0;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) s += red[ww][threadIdx.x];
+        if (s) atomicAdd((unsigned long long*)&out[threadIdx.x], (unsigned long long)s);
+    }
+}
+
+__global__ void __launch_bounds__(256) star_full_kernel(SView S, GView G, int64_t delta,
+                                                        uint32_t q_begin, uint32_t q_end,
+                                                        uint64_t* __restrict__ out) {
+    StarAcc acc;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc.v[j] = 0;
+    for (uint64_t qq = (uint64_t)q_begin + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+         qq < q_end; qq += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t q = (uint32_t)qq;
+        const uint32_t u = S.node[q];
+        const uint32_t start = S.off[u], end = S.off[u + 1];
+        first_role(S, G, q, start, end, delta, acc);
+        third_role(S, G, q, start, delta, 0u, end - start, acc);
+    }
+    flush_acc(acc, out);
+}
+
+__device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ item_off, uint64_t n_items,
+                                              uint64_t idx) {
+    uint64_t lo = 0, hi = n_items;  // last item with item_off[it] <= idx
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (item_off[mid] <= idx) lo = mid; else hi = mid;
+    }
+    return (uint32_t)lo;
+}
+
+// per-item star/pair: first-edge positions [rb, min(re, s)), third positions (rb, s)
+__global__ void __launch_bounds__(256) star_items_kernel(
+    SView S, GView G, int64_t delta, uint64_t n_items, const uint32_t* __restrict__ nodes,
+    const uint64_t* __restrict__ begin, const uint64_t* __restrict__ endr,
+    const uint64_t* __restrict__ first_off, uint64_t total_first,
+    const uint64_t* __restrict__ third_off, uint64_t total_third, uint64_t* __restrict__ out) {
+    const uint64_t total = total_first + total_third;
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        StarAcc acc;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc.v[j] = 0;
+        uint32_t it;
+        if (idx < total_first) {
+            it = find_item(first_off, n_items, idx);
+            const uint32_t u = nodes[it];
+            const uint32_t start = S.off[u], end = S.off[u + 1];
+            const uint32_t q = start + (uint32_t)begin[it] + (uint32_t)(idx - first_off[it]);
+            first_role(S, G, q, start, end, delta, acc);
+        } else {
+            const uint64_t j = idx - total_first;
+            it = find_item(third_off, n_items, j);
+            const uint32_t u = nodes[it];
+            const uint32_t start = S.off[u], end = S.off[u + 1];
+            const uint32_t s = end - start;
+            const uint32_t rb = (uint32_t)begin[it];
+            const uint32_t re = (uint32_t)(endr[it] < (uint64_t)s ? endr[it] : (uint64_t)s);
+            const uint32_t q = start + rb + 1 + (uint32_t)(j - third_off[it]);
+            third_role(S, G, q, start, delta, rb, re, acc);
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (acc.v[c]) atomicAdd((unsigned long long*)&out[(uint64_t)it * 32 + c],
+                                    (unsigned long long)acc.v[c]);
+    }
+}
+
+}  // namespace
+
+void star_full(const DeviceGraph& g, int64_t delta, uint32_t q_begin, uint32_t q_end,
+               uint64_t* d_out) {
+    if (q_end <= q_begin) return;
+    const uint64_t work = q_end - q_begin;
+    const uint64_t cap = (uint64_t)sm_count() * 8;
+    uint64_t grid = (work + 255) / 256;
+    if (grid > cap) grid = cap;
+    TM_LAUNCH("star_full", g.stream, star_full_kernel, (unsigned)grid, 256, 0, sview(g), gview(g),
+              delta, q_begin, q_end, d_out);
+}
+
+void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
+                const uint64_t* d_begin, const uint64_t* d_end, const uint64_t* d_first_off,
+                uint64_t total_first, uint64_t total_third, const uint64_t* d_third_off,
+                uint64_t* d_out) {
+    const uint64_t total = total_first + total_third;
+    if (total == 0) return;
+    const uint64_t cap = (uint64_t)sm_count() * 8;
+    uint64_t grid = (total + 255) / 256;
+    if (grid > cap) grid = cap;
+    TM_LAUNCH("star_items", g.stream, star_items_kernel, (unsigned)grid, 256, 0, sview(g), gview(g),
+              delta, n_items, d_nodes, d_begin, d_end, d_first_off, total_first, d_third_off,
+              total_third, d_out);
+}
+
+}  // namespace tmb

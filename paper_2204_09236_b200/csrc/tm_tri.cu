@@ -1,0 +1,233 @@
+// tm_tri.cu -- FAST-Tri (Algorithm 2, triangle_engine.cpp:20-62) on B200.
+//
+// Per center u, every in-window pair (e_i, e_j) of incident edges to distinct
+// neighbours v, w is a wedge; the closing edges are the v-w records with
+// t in [t_j - delta, t_i + delta], typed I/II/III by their (t, ordinal) place
+// relative to e_i and e_j (triangle_engine.cpp:10-16, 43-51).  The v-w list
+// is found in the neighbour-grouped G layout: binary search of w in v's
+// distinct-neighbour table (the smaller side), then either a short linear
+// scan (<= 16 records) or four binary searches plus G_dscan prefix counts.
+//
+// Full-graph passes run on the forward-oriented sequences F (each edge kept
+// at one endpoint under a strict total order), so every triangle instance is
+// enumerated exactly once, at its lowest-ranked vertex:
+//   * node-index order  == the reference's removal mode (alive = later nodes),
+//     giving Tri cells identical to count_triangles(removal);
+//   * (degree, id) order == the same instances with hubs last, used for
+//     count_all: each instance lands once in every cell of its isomorphism
+//     class (one per type, motifs.cpp fibers), so the host expands class sums
+//     into the reference's count_all cells.
+// Per-center work items (count_triangles_at_center with ranges / live mask)
+// use the unoriented S sequences exactly as the reference does.
+#include "tm_primitives.cuh"
+
+namespace tmb {
+
+namespace {
+
+// counts of closing records for one wedge: c[type*2 + dk], dk relative to v
+__device__ __forceinline__ void closing_counts(const GView& G, uint32_t v, uint32_t w, int64_t lo,
+                                               int64_t hi, int64_t ti, uint32_t oi, int64_t tj,
+                                               uint32_t oj, uint32_t c[6]) {
+#pragma unroll
+    for (int j = 0; j < 6; ++j) c[j] = 0;
+    const uint32_t gv0 = G.node_grp[v], gv1 = G.node_grp[v + 1];
+    const uint32_t gw0 = G.node_grp[w], gw1 = G.node_grp[w + 1];
+    uint32_t a, b, y, flip;
+    if (gv1 - gv0 <= gw1 - gw0) { a = gv0; b = gv1; y = w; flip = 0; }
+    else { a = gw0; b = gw1; y = v; flip = 1; }
+    // lower_bound of y in grp_nbr[a, b)
+    while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (G.grp_nbr[mid] < y) a = mid + 1; else b = mid;
+    }
+    if (a >= (flip ? gw1 : gv1) || G.grp_nbr[a] != y) return;
+    const uint32_t kb = G.grp_off[a], ke = G.grp_off[a + 1];
+    if (ke - kb <= 16) {
+        for (uint32_t k = kb; k < ke; ++k) {
+            const int64_t tk = G.t[k];
+            if (tk < lo) continue;
+            if (tk > hi) break;
+            const uint32_t dk = (G.w2[k] >> 31) ^ flip;
+            uint32_t type;
+            if (tk < ti || (tk == ti && G.ord[k] < oi)) type = 0;
+            else if (tk > tj || (tk == tj && G.ord[k] > oj)) type = 2;
+            else type = 1;
+            c[type * 2 + dk] += 1;
+        }
+        return;
+    }
+    // k1: first t >= lo ; k4: first t > hi
+    uint32_t l = kb, r = ke;
+    while (l < r) { const uint32_t mid = (l + r) >> 1; if (G.t[mid] < lo) l = mid + 1; else r = mid; }
+    const uint32_t k1 = l;
+    r = ke;
+    while (l < r) { const uint32_t mid = (l + r) >> 1; if (G.t[mid] <= hi) l = mid + 1; else r = mid; }
+    const uint32_t k4 = l;
+    // k2: first (t, ord) > (ti, oi) in [k1, k4)
+    l = k1; r = k4;
+    while (l < r) {
+        const uint32_t mid = (l + r) >> 1;
+        const int64_t tm = G.t[mid];
+        if (tm < ti || (tm == ti && G.ord[mid] < oi)) l = mid + 1; else r = mid;
+    }
+    const uint32_t k2 = l;
+    r = k4;
+    while (l < r) {
+        const uint32_t mid = (l + r) >> 1;
+        const int64_t tm = G.t[mid];
+        if (tm < tj || (tm == tj && G.ord[mid] < oj)) l = mid + 1; else r = mid;
+    }
+    const uint32_t k3 = l;
+    const uint32_t in1 = G.dscan[k2] - G.dscan[k1];
+    const uint32_t in2 = G.dscan[k3] - G.dscan[k2];
+    const uint32_t in3 = G.dscan[k4] - G.dscan[k3];
+    const uint32_t out1 = (k2 - k1) - in1, out2 = (k3 - k2) - in2, out3 = (k4 - k3) - in3;
+    c[0] = flip ? in1 : out1;  c[1] = flip ? out1 : in1;
+    c[2] = flip ? in2 : out2;  c[3] = flip ? out2 : in2;
+    c[4] = flip ? in3 : out3;  c[5] = flip ? out3 : in3;
+}
+
+struct TriAcc {
+    uint64_t v[24];
+};
+
+// all wedges with first edge i in sequence arrays (T, NBR, ORD) ending at end
+__device__ __forceinline__ void wedges_from(const GView& G, const int64_t* __restrict__ T,
+                                            const uint32_t* __restrict__ NBR,
+                                            const uint32_t* __restrict__ ORD, uint32_t i,
+                                            uint32_t end, int64_t delta,
+                                            const uint8_t* __restrict__ live, TriAcc& acc) {
+    const uint32_t ni = NBR[i];
+    const uint32_t v = ni & kNodeMask, di = ni >> 31;
+    if (live && !live[v]) return;
+    const int64_t ti = T[i];
+    const uint32_t oi = ORD[i];
+    const int64_t lim = sat_add(ti, delta);
+    uint64_t a0[6] = {0, 0, 0, 0, 0, 0}, a1[6] = {0, 0, 0, 0, 0, 0};
+    for (uint32_t j = i + 1; j < end; ++j) {
+        const int64_t tj = T[j];
+        if (tj > lim) break;
+        const uint32_t nj = NBR[j];
+        const uint32_t w = nj & kNodeMask;
+        if (w == v) continue;
+        if (live && !live[w]) continue;
+        uint32_t c[6];
+        closing_counts(G, v, w, sat_sub(tj, delta), lim, ti, oi, tj, ORD[j], c);
+        const uint64_t m1 = (nj >> 31) ? ~0ull : 0ull, m0 = ~m1;
+#pragma unroll
+        for (int x = 0; x < 6; ++x) {
+            a0[x] += c[x] & m0;
+            a1[x] += c[x] & m1;
+        }
+    }
+    const uint64_t mi = di ? ~0ull : 0ull, mo = ~mi;
+#pragma unroll
+    for (int ty = 0; ty < 3; ++ty)
+#pragma unroll
+        for (int dk = 0; dk < 2; ++dk) {
+            acc.v[ty * 8 + 0 + 0 + dk] += a0[ty * 2 + dk] & mo;
+            acc.v[ty * 8 + 0 + 2 + dk] += a1[ty * 2 + dk] & mo;
+            acc.v[ty * 8 + 4 + 0 + dk] += a0[ty * 2 + dk] & mi;
+            acc.v[ty * 8 + 4 + 2 + dk] += a1[ty * 2 + dk] & mi;
+        }
+}
+
+__device__ __forceinline__ void flush_tri(TriAcc& acc, uint64_t* out) {
+    __shared__ uint64_t red[8][24];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < 24; ++j) {
+        uint64_t v = acc.v[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == j) red[w][j] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 24) {
+        uint64_t s = 0;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) s += red[ww][threadIdx.x];
+        if (s) atomicAdd((unsigned long long*)&out[threadIdx.x], (unsigned long long)s);
+    }
+}
+
+__global__ void __launch_bounds__(256) tri_oriented_kernel(GView G, const int64_t* __restrict__ FT,
+                                                           const uint32_t* __restrict__ FN,
+                                                           const uint32_t* __restrict__ FO,
+                                                           const uint32_t* __restrict__ Fnode,
+                                                           const uint32_t* __restrict__ Foff,
+                                                           int64_t delta, uint32_t f_begin,
+                                                           uint32_t f_end, uint64_t* out) {
+    TriAcc acc;
+#pragma unroll
+    for (int j = 0; j < 24; ++j) acc.v[j] = 0;
+    for (uint64_t ii = (uint64_t)f_begin + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+         ii < f_end; ii += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = (uint32_t)ii;
+        const uint32_t end = Foff[Fnode[i] + 1];
+        wedges_from(G, FT, FN, FO, i, end, delta, nullptr, acc);
+    }
+    flush_tri(acc, out);
+}
+
+__device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ item_off, uint64_t n_items,
+                                              uint64_t idx) {
+    uint64_t lo = 0, hi = n_items;
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (item_off[mid] <= idx) lo = mid; else hi = mid;
+    }
+    return (uint32_t)lo;
+}
+
+__global__ void __launch_bounds__(256) tri_items_kernel(SView S, GView G, int64_t delta,
+                                                        uint64_t n_items,
+                                                        const uint32_t* __restrict__ nodes,
+                                                        const uint64_t* __restrict__ begin,
+                                                        const uint64_t* __restrict__ item_off,
+                                                        uint64_t total,
+                                                        const uint8_t* __restrict__ live,
+                                                        uint64_t* __restrict__ out) {
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t it = find_item(item_off, n_items, idx);
+        const uint32_t u = nodes[it];
+        const uint32_t start = S.off[u], end = S.off[u + 1];
+        const uint32_t i = start + (uint32_t)begin[it] + (uint32_t)(idx - item_off[it]);
+        TriAcc acc;
+#pragma unroll
+        for (int j = 0; j < 24; ++j) acc.v[j] = 0;
+        wedges_from(G, S.t, S.nbr, S.ord, i, end, delta, live, acc);
+#pragma unroll
+        for (int c = 0; c < 24; ++c)
+            if (acc.v[c]) atomicAdd((unsigned long long*)&out[(uint64_t)it * 24 + c],
+                                    (unsigned long long)acc.v[c]);
+    }
+}
+
+}  // namespace
+
+void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
+                  uint32_t f_end, uint64_t* d_out) {
+    if (f_end <= f_begin) return;
+    const uint64_t work = f_end - f_begin;
+    const uint64_t cap = (uint64_t)sm_count() * 8;
+    uint64_t grid = (work + 255) / 256;
+    if (grid > cap) grid = cap;
+    TM_LAUNCH("tri_oriented", g.stream, tri_oriented_kernel, (unsigned)grid, 256, 0, gview(g), f.t,
+              f.nbr, f.ord, f.node, f.off, delta, f_begin, f_end, d_out);
+}
+
+void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
+               const uint64_t* d_begin, const uint64_t* d_item_off, uint64_t total,
+               const uint8_t* d_live, uint64_t* d_out) {
+    if (total == 0) return;
+    const uint64_t cap = (uint64_t)sm_count() * 8;
+    uint64_t grid = (total + 255) / 256;
+    if (grid > cap) grid = cap;
+    TM_LAUNCH("tri_items", g.stream, tri_items_kernel, (unsigned)grid, 256, 0, sview(g), gview(g),
+              delta, n_items, d_nodes, d_begin, d_item_off, total, d_live, d_out);
+}
+
+}  // namespace tmb

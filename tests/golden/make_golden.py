@@ -1,0 +1,135 @@
+"""Generate tests/golden/*.json from the reference itself (run in the build
+container, where /root/reference exists).
+
+  toy.txt               the Fig.-1 toy edge list (reference proj/tests/data/toy.txt)
+  toy_frozen.json       the reference's frozen toy census (proj/tests/test_util.hpp:116-131)
+  toy_reference.json    reference counters / census / per-center cells on the toy graph
+  random_reference.json reference counters + census on seeded generate_random_graph inputs
+                        (the SPEC acceptance sweep shapes: nodes 5..60, edges 10..600,
+                        t in [0, 1e4], delta in {1, 10, 100, 1000}) plus tie-heavy cases
+  uniform_reference.json reference census for BASELINE config 0
+                        (10k nodes, 200k edges, t uniform in [0, 1e6), delta 1000)
+  powerlaw_reference.json reference census for BASELINE config 1 (optional, slow)
+
+Usage: python tests/golden/make_golden.py [--powerlaw]
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import re
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+REF_TESTS = "/root/reference/proj/tests"
+
+from oracle import Reference  # noqa: E402
+
+
+def edge_hash(src, dst, t) -> str:
+    h = hashlib.sha256()
+    for a in (src, dst, t):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()[:16]
+
+
+def parse_toy(text):
+    ids, index, src, dst, t = [], {}, [], [], []
+    for line in text.splitlines():
+        f = line.split()
+        if not f or f[0].startswith("#"):
+            continue
+        for tok in f[:2]:
+            if tok not in index:
+                index[tok] = len(ids)
+                ids.append(tok)
+        src.append(index[f[0]]); dst.append(index[f[1]]); t.append(int(f[2]))
+    return ids, np.array(src, np.uint32), np.array(dst, np.uint32), np.array(t, np.int64)
+
+
+def counters(R, g, delta):
+    st, pr, tr = R.counters(g, delta, removal=False)
+    _, _, trr = R.counters(g, delta, removal=True)
+    return {"star": [int(x) for x in st], "pair": [int(x) for x in pr],
+            "tri_countall": [int(x) for x in tr], "tri_removal": [int(x) for x in trr]}
+
+
+def main(with_powerlaw: bool):
+    R = Reference()
+    sigs = R.signatures()
+
+    toy_text = open(os.path.join(REF_TESTS, "data", "toy.txt")).read()
+    open(os.path.join(HERE, "toy.txt"), "w").write(toy_text)
+
+    util = open(os.path.join(REF_TESTS, "test_util.hpp")).read()
+    block = util[util.index("frozen_toy_census"):]
+    frozen = {m.group(1): int(m.group(2)) for m in re.finditer(r'\{"([123|]{8})", (\d+)\}', block)}
+    assert len(frozen) == 36
+    json.dump({"source": "proj/tests/test_util.hpp frozen_toy_census (delta = 10)",
+               "delta": 10, "census": frozen}, open(os.path.join(HERE, "toy_frozen.json"), "w"), indent=1)
+
+    ids, src, dst, t = parse_toy(toy_text)
+    g = R.build_graph(len(ids), src, dst, t)
+    toy = {"node_ids": ids, "signatures": sigs, "cases": []}
+    for delta in (0, 1, 5, 10, 100):
+        case = {"delta": delta, **counters(R, g, delta),
+                "census": [int(x) for x in R.run_parallel(g, delta, 1)],
+                "oracle_census": [int(x) for x in R.oracle_census(g, delta)],
+                "per_center": []}
+        for u in range(len(ids)):
+            s = int(np.sum(src == u) + np.sum(dst == u))
+            st, pr = R.star_pair_at_center(g, u, delta, 0, max(s - 2, 0))
+            tr = R.triangles_at_center(g, u, delta, 0, max(s - 1, 0))
+            case["per_center"].append({"node": u, "degree": s, "star": [int(x) for x in st],
+                                       "pair": [int(x) for x in pr], "tri": [int(x) for x in tr]})
+        toy["cases"].append(case)
+    R.free(g)
+    json.dump(toy, open(os.path.join(HERE, "toy_reference.json"), "w"))
+
+    rng = np.random.default_rng(20220419)
+    cases = []
+    for k in range(48):
+        n = int(rng.integers(5, 61)); m = int(rng.integers(10, 601))
+        t_max = 10_000 if k % 4 else int(rng.integers(5, 60))  # every 4th case: heavy timestamp ties
+        seed = int(rng.integers(1, 2 ** 31))
+        s, d, tt = R.generate_random_graph(n, m, t_max, seed)
+        g = R.build_graph(n, s, d, tt)
+        entry = {"nodes": n, "edges": m, "t_max": t_max, "seed": seed, "hash": edge_hash(s, d, tt),
+                 "auto_threshold": R.auto_degree_threshold(g), "deltas": []}
+        for delta in (0, 1, 10, 100, 1000):
+            entry["deltas"].append({"delta": delta, **counters(R, g, delta),
+                                    "census": [int(x) for x in R.run_parallel(g, delta, 4)],
+                                    "census_removal": [int(x) for x in R.run_parallel(g, delta, 1, -1, True)]})
+        R.free(g)
+        cases.append(entry)
+    json.dump({"signatures": sigs, "cases": cases}, open(os.path.join(HERE, "random_reference.json"), "w"))
+
+    # BASELINE config 0 (same generator as the reference)
+    n, m, t_max, seed, delta = 10_000, 200_000, 999_999, 2204, 1000
+    s, d, tt = R.generate_random_graph(n, m, t_max, seed)
+    g = R.build_graph(n, s, d, tt)
+    out = {"config": "uniform_10k_200k", "nodes": n, "edges": m, "t_max": t_max, "seed": seed,
+           "hash": edge_hash(s, d, tt), "delta": delta, **counters(R, g, delta),
+           "census": [int(x) for x in R.run_parallel(g, delta, os.cpu_count() or 1)]}
+    R.free(g)
+    json.dump(out, open(os.path.join(HERE, "uniform_reference.json"), "w"))
+
+    if with_powerlaw:
+        from paper_2204_09236_b200 import synth
+        n, s, d, tt = synth.power_law()
+        delta = 3600
+        g = R.build_graph(n, s, d, tt)
+        out = {"config": "powerlaw_1m_10m", "nodes": n, "edges": int(len(s)), "hash": edge_hash(s, d, tt),
+               "delta": delta, "census": [int(x) for x in R.run_parallel(g, delta, os.cpu_count() or 1)]}
+        R.free(g)
+        json.dump(out, open(os.path.join(HERE, "powerlaw_reference.json"), "w"))
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main("--powerlaw" in sys.argv)

@@ -1,0 +1,328 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle and the
+reference's own golden vectors.  Integer counts: bit-exact, zero tolerance.
+
+Mirrors the reference's tests: test_star_engine.cpp, test_triangle_engine.cpp,
+test_executor.cpp, test_oracle.cpp, test_indexes.cpp (file:line cited inline).
+"""
+import numpy as np
+import pytest
+
+from conftest import load_golden, toy_arrays
+
+pytestmark = pytest.mark.gpu
+
+O_, IN_ = 0, 1
+
+
+def ctx_of(tm, g):
+    return tm.GraphContext.build(g)
+
+
+def oracle_graph(oracle, g):
+    return oracle.build_graph(g.node_count(), g.src, g.dst, g.t)
+
+
+# --- toy graph (Fig. 1) ---------------------------------------------------------
+def test_toy_frozen_census(cuda, tm):
+    """test_oracle.cpp 'toy census at delta 10 matches the frozen vector'."""
+    frozen = load_golden("toy_frozen.json")["census"]
+    g = toy_arrays()
+    census = tm.run_parallel(ctx_of(tm, g), tm.RunConfig(delta=10))
+    for sig, c in frozen.items():
+        assert census.count(sig) == c, sig
+    assert census.total() == sum(frozen.values())
+
+
+def test_toy_reference_counters_all_deltas(cuda, tm):
+    ref = load_golden("toy_reference.json")
+    g = toy_arrays()
+    assert list(g.node_ids) == ref["node_ids"]
+    ctx = ctx_of(tm, g)
+    for case in ref["cases"]:
+        d = case["delta"]
+        sp = tm.count_star_pair(ctx, d)
+        assert sp.star.cells.tolist() == case["star"], d
+        assert sp.pair.cells.tolist() == case["pair"], d
+        assert tm.count_triangles(ctx, d).cells.tolist() == case["tri_countall"], d
+        assert tm.count_triangles(ctx, d, tm.TriangleMode.removal).cells.tolist() == case["tri_removal"], d
+        assert tm.run_parallel(ctx, tm.RunConfig(delta=d)).counts.tolist() == case["census"], d
+        assert case["census"] == case["oracle_census"]
+        nodes = [pc["node"] for pc in case["per_center"]]
+        stars = tm.count_star_pair_items(ctx, d, nodes, [tm.full_star_range(pc["degree"]) for pc in case["per_center"]])
+        tris = tm.count_triangles_items(ctx, d, nodes, [tm.full_triangle_range(pc["degree"]) for pc in case["per_center"]])
+        for pc, s, t in zip(case["per_center"], stars, tris):
+            assert s.star.cells.tolist() == pc["star"], (d, pc["node"])
+            assert s.pair.cells.tolist() == pc["pair"], (d, pc["node"])
+            assert t.cells.tolist() == pc["tri"], (d, pc["node"])
+
+
+def test_toy_center_a_worked_increments(cuda, tm):
+    """test_star_engine.cpp:16-34: Star[III,o,o,in], Star[III,o,o,o],
+    Star[II,o,in,o], Star[II,o,o,o] each 1, nothing else."""
+    g = toy_arrays()
+    ctx = ctx_of(tm, g)
+    a = g.find_node("a")
+    r = tm.count_star_pair_at_center(ctx, a, 10, tm.full_star_range(ctx.degree(a)))
+    T = tm.StarType
+    assert r.star.at(T.isolated_third, O_, O_, IN_) == 1
+    assert r.star.at(T.isolated_third, O_, O_, O_) == 1
+    assert r.star.at(T.isolated_second, O_, IN_, O_) == 1
+    assert r.star.at(T.isolated_second, O_, O_, O_) == 1
+    assert int(r.star.cells.sum()) == 4
+    assert int(r.pair.cells.sum()) == 0
+
+
+def test_toy_center_e_triangles(cuda, tm):
+    """test_triangle_engine.cpp:19-32."""
+    g = toy_arrays()
+    ctx = ctx_of(tm, g)
+    e = g.find_node("e")
+    r = tm.count_triangles_at_center(ctx, e, 10, tm.full_triangle_range(ctx.degree(e)))
+    T = tm.TriangleType
+    assert r.at(T.closing_last, O_, O_, O_) == 1
+    assert r.at(T.closing_middle, O_, IN_, IN_) == 1
+    assert int(r.cells.sum()) == 2
+
+
+def test_toy_sequences_and_pair_index(cuda, tm):
+    """test_indexes.cpp:24-75 and 77-99 (device-built S and G)."""
+    g = toy_arrays()
+    ctx = ctx_of(tm, g)
+    n = lambda x: g.find_node(x)
+    sa = ctx.sequence(n("a"))
+    assert [(r.t, r.other, int(r.dir)) for r in sa] == [
+        (4, n("c"), 0), (8, n("c"), 0), (9, n("d"), 1), (11, n("b"), 0), (15, n("c"), 0)]
+    se = ctx.sequence(n("e"))
+    assert [(r.t, r.other, int(r.dir)) for r in se] == [
+        (1, n("d"), 0), (6, n("c"), 0), (14, n("d"), 1), (18, n("d"), 0), (21, n("d"), 1)]
+    rel_c = ctx.edges_in_window(n("c"), n("d"), -2 ** 63, 2 ** 63 - 1)
+    assert [(t, int(d)) for t, _, d in rel_c] == [(10, 1), (17, 0)]
+    rel_d = ctx.edges_in_window(n("d"), n("c"), 4, 14)
+    assert [(t, int(d)) for t, _, d in rel_d] == [(10, 0)]
+    assert ctx.edges_in_window(n("c"), n("d"), 11, 16) == []
+    assert ctx.edges_in_window(n("b"), n("e"), 0, 100) == []
+
+
+# --- reference golden sweep ------------------------------------------------------
+@pytest.fixture(scope="module")
+def random_golden():
+    return load_golden("random_reference.json")
+
+
+def test_random_sweep_matches_reference(cuda, tm, random_golden):
+    """SPEC acceptance 1/3/4: 48 seeded graphs x 5 deltas, counters + census."""
+    for case in random_golden["cases"]:
+        g = tm.generate_random_graph(case["nodes"], case["edges"], case["t_max"], case["seed"])
+        ctx = ctx_of(tm, g)
+        assert tm.auto_degree_threshold(ctx) == case["auto_threshold"]
+        for dc in case["deltas"]:
+            d = dc["delta"]
+            sp = tm.count_star_pair(ctx, d)
+            assert sp.star.cells.tolist() == dc["star"], (case["seed"], d)
+            assert sp.pair.cells.tolist() == dc["pair"], (case["seed"], d)
+            assert tm.count_triangles(ctx, d).cells.tolist() == dc["tri_countall"], (case["seed"], d)
+            assert tm.count_triangles(ctx, d, tm.TriangleMode.removal).cells.tolist() == dc["tri_removal"]
+            assert tm.run_parallel(ctx, tm.RunConfig(delta=d)).counts.tolist() == dc["census"]
+            rem = tm.run_parallel(ctx, tm.RunConfig(delta=d, triangle_mode=tm.TriangleMode.removal))
+            assert rem.counts.tolist() == dc["census_removal"]
+        ctx.close()
+
+
+def test_per_center_items_and_range_additivity(cuda, tm, oracle):
+    """test_star_engine.cpp:77-121, test_triangle_engine.cpp:63-79 / 130-146."""
+    rng = np.random.default_rng(5)
+    for seed in (1, 2, 3, 4, 5, 6):
+        g = tm.generate_random_graph(12, 150, 40 if seed % 2 else 4000, seed)
+        og = oracle_graph(oracle, g)
+        ctx = ctx_of(tm, g)
+        degs = ctx.degrees()
+        for delta in (0, 3, 50, 5000):
+            nodes = list(range(g.node_count()))
+            stars = tm.count_star_pair_items(ctx, delta, nodes, [tm.full_star_range(int(degs[u])) for u in nodes])
+            tris = tm.count_triangles_items(ctx, delta, nodes, [tm.full_triangle_range(int(degs[u])) for u in nodes])
+            for u in nodes:
+                s = int(degs[u])
+                st, pr = oracle.star_pair_at_center(og, u, delta, 0, max(s - 2, 0))
+                assert (stars[u].star.cells == st).all() and (stars[u].pair.cells == pr).all()
+                assert (tris[u].cells == oracle.triangles_at_center(og, u, delta, 0, max(s - 1, 0))).all()
+                # random split points and arbitrary sub-ranges
+                for _ in range(3):
+                    lo = int(rng.integers(0, s + 1)); hi = int(rng.integers(lo, s + 2))
+                    a = tm.count_star_pair_at_center(ctx, u, delta, (lo, hi))
+                    st, pr = oracle.star_pair_at_center(og, u, delta, lo, hi)
+                    assert (a.star.cells == st).all() and (a.pair.cells == pr).all(), (seed, u, lo, hi)
+                    tt = tm.count_triangles_at_center(ctx, u, delta, (lo, hi))
+                    assert (tt.cells == oracle.triangles_at_center(og, u, delta, lo, hi)).all()
+        oracle.free(og)
+
+
+def test_live_mask_items(cuda, tm, oracle):
+    """Removal-mode center calls with a live mask (triangle_engine.cpp:75-83)."""
+    for seed in (3, 9, 27):
+        g = tm.generate_random_graph(11, 160, 25 if seed % 2 else 3000, seed)
+        og = oracle_graph(oracle, g)
+        ctx = ctx_of(tm, g)
+        degs = ctx.degrees()
+        live = np.ones(11, np.uint8)
+        for u in range(11):
+            got = tm.count_triangles_at_center(ctx, u, 300, tm.full_triangle_range(int(degs[u])), live)
+            exp = oracle.triangles_at_center(og, u, 300, 0, max(int(degs[u]) - 1, 0), live)
+            assert (got.cells == exp).all()
+            live[u] = 0
+        oracle.free(og)
+
+
+# --- edge cases ----------------------------------------------------------------------
+def test_empty_and_tiny_graphs(cuda, tm):
+    g = tm.TemporalGraph([], np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.int64))
+    ctx = ctx_of(tm, g)
+    assert tm.run_parallel(ctx, tm.RunConfig(delta=100)).total() == 0
+    g = tm.TemporalGraph(["a", "b", "c"], np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.int64))
+    assert tm.run_parallel(ctx_of(tm, g), tm.RunConfig(delta=5)).total() == 0
+    # three parallel edges: one pair instance seen from both ends (test_star_engine.cpp:64-75)
+    g = tm.parse_edge_list("a b 1\na b 2\na b 3\n")
+    ctx = ctx_of(tm, g)
+    r = tm.count_star_pair(ctx, 10)
+    assert r.pair.at(O_, O_, O_) == 1 and r.pair.at(IN_, IN_, IN_) == 1
+    assert int(r.pair.cells.sum()) == 2 and int(r.star.cells.sum()) == 0
+    assert tm.run_parallel(ctx, tm.RunConfig(delta=5)).count("12|12|12") == 1
+    # a single triangle lands once in each cell of its class (test_triangle_engine.cpp:82-101)
+    g = tm.parse_edge_list("a c 8\nd a 9\nc d 17\n")
+    r = tm.count_triangles(ctx_of(tm, g), 9)
+    T = tm.TriangleType
+    assert r.at(T.closing_last, O_, IN_, O_) == 1
+    assert r.at(T.closing_middle, IN_, O_, IN_) == 1
+    assert r.at(T.closing_first, O_, IN_, O_) == 1
+    assert int(r.cells.sum()) == 3
+
+
+def test_ties_and_zero_delta(cuda, tm, oracle):
+    """test_oracle.cpp:58-71: tied timestamps fit a zero window."""
+    g = tm.parse_edge_list("a b 7\na b 7\nb a 7\n")
+    assert tm.run_parallel(ctx_of(tm, g), tm.RunConfig(delta=0)).count("12|12|21") == 1
+    for seed in range(10):
+        g = tm.generate_random_graph(8, 300, 3, seed)  # massive ties
+        og = oracle_graph(oracle, g)
+        ctx = ctx_of(tm, g)
+        for d in (0, 1, 2):
+            for rem in (False, True):
+                mode = tm.TriangleMode.removal if rem else tm.TriangleMode.count_all
+                got = tm.run_parallel(ctx, tm.RunConfig(delta=d, triangle_mode=mode)).counts
+                assert (got == oracle.census(og, d, rem)).all(), (seed, d, rem)
+        oracle.free(og)
+
+
+def test_extreme_timestamps_saturate(cuda, tm, oracle):
+    """sat_add / sat_sub window bounds (types.hpp:72-89) near int64 limits."""
+    big = 2 ** 63 - 1
+    for base in (big - 50, -(2 ** 63) + 3):
+        rng = np.random.default_rng(abs(base) % 1000)
+        n, m = 6, 120
+        src = rng.integers(0, n, m).astype(np.uint32)
+        dst = ((src + rng.integers(1, n, m)) % n).astype(np.uint32)
+        off = rng.integers(0, 40, m)
+        t = (np.int64(base) - off.astype(np.int64)) if base > 0 else (np.int64(base) + off.astype(np.int64))
+        g = tm.TemporalGraph([str(i) for i in range(n)], src, dst, t)
+        og = oracle_graph(oracle, g)
+        ctx = ctx_of(tm, g)
+        for d in (0, 7, 2 ** 62, big):
+            assert (tm.run_parallel(ctx, tm.RunConfig(delta=d)).counts == oracle.census(og, d)).all(), d
+        oracle.free(og)
+
+
+def test_errors_mirror_reference(cuda, tm):
+    g = toy_arrays()
+    ctx = ctx_of(tm, g)
+    with pytest.raises(tm.ConfigError):
+        tm.run_parallel(ctx, tm.RunConfig(delta=10, workers=4, triangle_mode=tm.TriangleMode.removal))
+    with pytest.raises(tm.ConfigError):
+        tm.run_parallel(ctx, tm.RunConfig(delta=-1))
+    assert tm.run_parallel(ctx, tm.RunConfig(delta=10, workers=64)).total() > 0
+    with pytest.raises(ValueError):
+        tm.GraphContext.build(tm.TemporalGraph.from_arrays(3, [0, 1], [1, 5], [1, 2]))
+
+
+def test_motif_filter(cuda, tm):
+    """test_executor.cpp:181-214."""
+    g = tm.generate_random_graph(25, 300, 150, 19)
+    ctx = ctx_of(tm, g)
+    full = tm.run_parallel(ctx, tm.RunConfig(delta=40))
+    parts = {}
+    for name, f in (("star", tm.MotifFilter(True, False, False)), ("pair", tm.MotifFilter(False, True, False)),
+                    ("triangle", tm.MotifFilter(False, False, True))):
+        parts[name] = tm.run_parallel(ctx, tm.RunConfig(delta=40, motifs=f))
+    for s in tm.all_signatures():
+        cat = tm.signature_category(s)
+        for name, c in parts.items():
+            assert c.count(s) == (full.count(s) if name == cat else 0)
+
+
+def test_center_partition_sums_to_full(cuda, tm):
+    """Multi-GPU data path on one device: partial counters over a degree-cost
+    partition sum to the full run (the all-reduce is a plain u64 sum)."""
+    g = tm.generate_random_graph(300, 20000, 5000, 11)
+    ctx = ctx_of(tm, g)
+    for mode in (tm.TriangleMode.count_all, tm.TriangleMode.removal):
+        cfg = tm.RunConfig(delta=200, triangle_mode=mode)
+        full_raw, full_census = tm.run_parallel_raw(ctx, cfg)
+        for world in (2, 3, 8):
+            acc = np.zeros(56, np.uint64)
+            bounds = [ctx.partition(world, r) for r in range(world)]
+            assert bounds[0][0] == 0 and bounds[-1][1] == g.node_count()
+            for (b, e), (b2, _) in zip(bounds, bounds[1:]):
+                assert e == b2
+            for b, e in bounds:
+                if b == e:
+                    continue
+                raw, _ = tm.run_parallel_raw(ctx, cfg, b, e)
+                acc += raw.as_array()
+            assert (acc == full_raw.as_array()).all()
+        merged = tm.merge_census(full_raw.star, full_raw.pair, full_raw.tri, mode)
+        assert (merged.counts == full_census).all()
+
+
+# --- full-size configs --------------------------------------------------------------
+def test_config0_uniform_full_size_matches_reference(cuda, tm):
+    ref = load_golden("uniform_reference.json")
+    from paper_2204_09236_b200 import synth
+    n, s, d, t = synth.uniform(ref["nodes"], ref["edges"], ref["t_max"], ref["seed"])
+    ctx = tm.GraphContext.build(tm.TemporalGraph.from_arrays(n, s, d, t))
+    raw, census = tm.run_parallel_raw(ctx, tm.RunConfig(delta=ref["delta"]))
+    assert raw.star.cells.tolist() == ref["star"]
+    assert raw.pair.cells.tolist() == ref["pair"]
+    assert raw.tri.cells.tolist() == ref["tri_countall"]
+    assert census.tolist() == ref["census"]
+    assert tm.count_triangles(ctx, ref["delta"], tm.TriangleMode.removal).cells.tolist() == ref["tri_removal"]
+
+
+def _class_checks(tm, raw):
+    # pair complementary-cell equality, triangle class-cell equality (SPEC acceptance 3)
+    p = raw.pair.cells
+    for c in range(8):
+        assert p[c] == p[7 - c]
+    cls = {}
+    for c in range(24):
+        cls.setdefault(tm.tri_cell_signature(c >> 3, (c >> 2) & 1, (c >> 1) & 1, c & 1), []).append(int(raw.tri.cells[c]))
+    assert len(cls) == 8
+    for v in cls.values():
+        assert len(v) == 3 and v[0] == v[1] == v[2]
+
+
+def test_config1_powerlaw_full_size_properties(cuda, tm):
+    """BASELINE config 1 at full size (1M nodes, 10M edges, delta 3600):
+    size-independent properties + the reference's census when the golden
+    vector was generated (tests/golden/powerlaw_reference.json)."""
+    import os
+    from paper_2204_09236_b200 import synth
+    n, s, d, t = synth.power_law()
+    ctx = tm.GraphContext.build(tm.TemporalGraph.from_arrays(n, s, d, t))
+    raw, census = tm.run_parallel_raw(ctx, tm.RunConfig(delta=3600))
+    _class_checks(tm, raw)
+    rem = tm.run_parallel(ctx, tm.RunConfig(delta=3600, triangle_mode=tm.TriangleMode.removal))
+    assert (rem.counts == census).all()  # mode equivalence (SPEC acceptance 4)
+    small = tm.run_parallel(ctx, tm.RunConfig(delta=600))
+    assert (small.counts <= census).all()  # delta monotonicity (SPEC acceptance 6)
+    path = os.path.join(os.path.dirname(__file__), "golden", "powerlaw_reference.json")
+    if os.path.exists(path):
+        ref = load_golden("powerlaw_reference.json")
+        assert census.tolist() == ref["census"]
