@@ -1,0 +1,316 @@
+"""bench.py -- exact 36-motif temporal census throughput on B200.
+
+Step = one full census of the BASELINE workload from edge arrays resident in
+HBM: GPU index build (radix sorts -> S / G / F layouts) + FAST-Star pass +
+FAST-Tri pass + counter all-reduce (N > 1) + merge.  value = edges x steps /
+max-over-ranks device time.  e2e = the same step through the C-ABI from
+pinned HOST arrays, host->device copies and the counter read-back inside the
+timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation (oracle/_ref:
+the unmodified reference sources, std::thread HARE executor with all host
+threads) on a bounded time slice of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "temporal edges/sec, exact 36-motif count (1/2/4/8 B200); % of HBM roofline"
+
+# Algorithmic bytes per unit for the kernels that can dominate a step (see
+# DESIGN.md "Roofline"): bytes that must cross HBM at least once per launch.
+#   star_full    per incident record: S t/nbr/node/gidx/pg (24 B) + its G record t/w2/pg (16 B)
+#   tri_oriented per forward record: F t/nbr/ord/node (20 B) + its G group probe (node_grp x2, 8 B)
+#   radix_downsweep per key: key+value read + key+value write
+ALGO_BYTES = {
+    "star_full": lambda m: 2 * m * 40,
+    "tri_oriented": lambda m: m * 28,
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_workload(name: str):
+    from paper_2204_09236_b200 import synth
+    cfg = synth.CONFIGS[name]
+    n, src, dst, t = cfg["fn"]()
+    return n, src, dst, t, cfg["delta"]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_reference(n, src, dst, t, delta, steps, warmup, sample_edges, threads):
+    """Time the reference's own pipeline (TemporalGraph::build + GraphContext::build
+    + run_parallel) on the first `sample_edges` edges in time order."""
+    from oracle import Reference
+    R = Reference()
+    order = np.argsort(t, kind="stable")[:sample_edges]
+    order.sort()  # keep ingestion order of the slice
+    s, d, tt = src[order], dst[order], t[order]
+    times = []
+    census = None
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        census, mb, mc = R.pipeline(n, s, d, tt, delta, threads)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    sec = float(np.mean(times))
+    return {"value": len(s) / sec, "sec_per_step": sec, "edges": int(len(s)), "census_total": int(census.sum())}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="powerlaw_1m_10m")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-edges", type=int, default=1_000_000)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    threads = os.cpu_count() or 1
+
+    n, src, dst, t, delta = load_workload(args.config)
+    m = len(src)
+    base_cfg = {"workload": args.config, "nodes": int(n), "edges": int(m), "delta": int(delta),
+                "inputs": "time-ordered synthetic edge list (seed 2204), ingestion order = time order",
+                "l2": "inputs + indexes (~1 GB) exceed the 126 MB L2; no explicit flush"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        res = cpu_reference(n, src, dst, t, delta, args.steps, args.warmup, min(args.cpu_sample_edges, m), threads)
+        sample = f"first {res['edges']} of {m} edges in time order (a time slice of the same workload)"
+        line = {"metric": METRIC, "value": res["value"], "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": res["sec_per_step"] * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+                "impl": "reference",
+                "config": dict(base_cfg, parallelism="cpu", sample=sample),
+                "cpu_baseline": {"value": res["value"], "unit": "edges/s", "cores": threads, "kind": "reference",
+                                 "sample": sample},
+                "e2e": {"value": res["value"], "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2204_09236_b200 as tm
+
+    stream = torch.cuda.Stream(device=dev)
+    sptr = stream.cuda_stream
+    # inputs resident in HBM
+    d_src = torch.from_numpy(src.view(np.int32)).to(dev)
+    d_dst = torch.from_numpy(dst.view(np.int32)).to(dev)
+    d_t = torch.from_numpy(t).to(dev)
+    # pinned host copies for the e2e leg
+    h_src = torch.from_numpy(src.view(np.int32)).pin_memory()
+    h_dst = torch.from_numpy(dst.view(np.int32)).pin_memory()
+    h_t = torch.from_numpy(t).pin_memory()
+    torch.cuda.synchronize()
+
+    cfg = tm.RunConfig(delta=delta)
+    ctx = tm.GraphContext.build_device(n, d_src.data_ptr(), d_dst.data_ptr(), d_t.data_ptr(), m, stream=sptr)
+    b, e = ctx.partition(world, rank)
+    ctx.close()
+    center = (b, e) if world > 1 else (0, 0)
+    red = torch.zeros(56, dtype=torch.int64, device=dev)
+    raw = np.zeros(56, np.uint64)
+
+    def step(host: bool):
+        if host:
+            census = tm.count_edges(n, h_src.numpy().view(np.uint32), h_dst.numpy().view(np.uint32), h_t.numpy(),
+                                    cfg, stream=sptr, raw_out=raw, center=center)
+        else:
+            census = tm.count_edges_device(n, m, d_src.data_ptr(), d_dst.data_ptr(), d_t.data_ptr(), cfg,
+                                           stream=sptr, center=center, raw_out=raw)
+        if world > 1:
+            with torch.cuda.stream(stream):
+                red.copy_(torch.from_numpy(raw.view(np.int64)), non_blocking=False)
+                dist.all_reduce(red)
+                tot = red.cpu().numpy().view(np.uint64)
+            census = tm.merge_census(tm.StarCounter(tot[:24]), tm.PairCounter(tot[24:32]), tm.TriCounter(tot[32:]),
+                                     cfg.triangle_mode).counts
+        return census
+
+    def timed(host: bool, steps: int, warmup: int):
+        for _ in range(warmup):
+            census = step(host)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = tm.kernel_launches()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+        for _ in range(steps):
+            census = step(host)
+        with torch.cuda.stream(stream):
+            ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ms = ev0.elapsed_time(ev1)
+        if dist:
+            x = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            ms = float(x.item())
+        return ms / steps, census, tm.kernel_launches() - l0
+
+    with ClockSampler(local) as clk:
+        ms_step, census, launches = timed(False, args.steps, args.warmup)
+    ms_e2e, census_e2e, _ = timed(True, max(2, args.steps // 2), 1)
+    assert (census == census_e2e).all(), "device and host paths disagree"
+
+    # per-kernel device time with CUDA events on the launching stream (separate instrumented pass)
+    tm.kernel_timing(enable=True, reset=True)
+    kk = max(2, min(args.steps, 5))
+    for _ in range(kk):
+        step(False)
+    torch.cuda.synchronize()
+    tm.kernel_timing(enable=False)
+    names = ["star_full", "tri_oriented", "radix_downsweep", "radix_upsweep", "scan_down", "scan_reduce",
+             "gather_s", "gather_g", "forward_scatter", "node_keys", "group_keys", "validate", "offsets"]
+    ktimes = {}
+    for nm in names:
+        tot_ms, cnt = tm.kernel_time(nm)
+        if cnt:
+            ktimes[nm] = {"ms_per_step": tot_ms / kk, "launches_per_step": cnt / kk}
+    dom = max(ALGO_BYTES, key=lambda k: ktimes.get(k, {}).get("ms_per_step", 0))
+    dom_ms = ktimes[dom]["ms_per_step"] / max(1.0, ktimes[dom]["launches_per_step"])
+    algo = ALGO_BYTES[dom](m)
+    peak, peak_kind = peaks()
+    achieved = algo / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{dom}_{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # reported CPU baseline: the reference's own code on host cores, rank 0, N = 1 only
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import Reference
+            if Reference.available():
+                res = cpu_reference(n, src, dst, t, delta, 1, 0, min(args.cpu_sample_edges, m), threads)
+                cpu = {"value": res["value"], "unit": "edges/s", "cores": threads, "kind": "reference",
+                       "sample": f"first {res['edges']} of {m} edges in time order (one pipeline run: "
+                                 f"build + run_parallel, {threads} std::threads)"}
+        except Exception as ex:  # pragma: no cover
+            log("cpu baseline failed:", ex)
+
+    value = m / (ms_step * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": dict(base_cfg, parallelism=f"centers partitioned over {world} GPU(s), graph replicated"),
+        "census_total": int(np.asarray(census, np.uint64).sum()),
+        "e2e": {"value": m / (ms_e2e * 1e-3), "unit": "edges/s", "h2d_bytes_per_step": int(m * 16),
+                "d2h_bytes_per_step": int(56 * 8 + 36 * 8)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "algo_bytes_per_launch": algo, "launch_ms": dom_ms},
+        "kernels": ktimes,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -768,13 +768,14 @@ def run_parallel(ctx: GraphContext, config: RunConfig, timings: Optional[PhaseTi
 
 
 def count_edges(n: int, src, dst, t, config: RunConfig, stream: Optional[int] = None,
-                timings: Optional[PhaseTimings] = None, raw_out: Optional[np.ndarray] = None):
+                timings: Optional[PhaseTimings] = None, raw_out: Optional[np.ndarray] = None,
+                center: Tuple[int, int] = (0, 0)):
     """One full step from HOST edge arrays: H2D copy + build + count + free."""
     L = lib()
     src = np.ascontiguousarray(src, np.uint32)
     dst = np.ascontiguousarray(dst, np.uint32)
     t = np.ascontiguousarray(t, np.int64)
-    cfg = config.to_c()
+    cfg = config.to_c(*center)
     raw = _Counters()
     census = np.zeros(36, np.uint64)
     tm = _Timings()

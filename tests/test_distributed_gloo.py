@@ -1,0 +1,67 @@
+"""CPU, world_size 2 over gloo: the multi-GPU host path (degree-cost center
+partition -> per-rank counters -> one all-reduce -> merge) reproduces the
+single-process census.  Per-rank compute here is the oracle's per-center
+counters (test stand-in for the GPU kernels), so this checks the partition
+and reduction logic, not the kernels."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_q, n, src, dst, t, delta):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import Oracle
+    from paper_2204_09236_b200.distributed import allreduce_counters, partition_bounds
+    O = Oracle()
+    g = O.build_graph(n, src, dst, t)
+    deg = np.array([O.degree(g, u) for u in range(n)], np.uint64)
+    cost = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint64)
+    b, e = partition_bounds(cost, world)[rank]
+    raw = np.zeros(56, np.uint64)
+    for u in range(b, e):
+        s = int(deg[u])
+        st, pr = O.star_pair_at_center(g, u, delta, 0, max(s - 2, 0))
+        tr = O.triangles_at_center(g, u, delta, 0, max(s - 1, 0))
+        raw[:24] += st; raw[24:32] += pr; raw[32:] += tr
+    tot = allreduce_counters(raw)
+    census = O.merge_census(tot[:24], tot[24:32], tot[32:])
+    out_q.put((rank, (b, e), census.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_partition_allreduce_matches_single(world, oracle):
+    n, m, delta = 60, 2500, 150
+    src, dst, t = oracle.generate_random_graph(n, m, 8000, 4242)
+    g = oracle.build_graph(n, src, dst, t)
+    expect = oracle.census(g, delta).tolist()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, src, dst, t, delta)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    assert res[0][1][0] == 0 and res[-1][1][1] == n and res[0][1][1] == res[1][1][0]
+    for _, _, census in res:
+        assert census == expect

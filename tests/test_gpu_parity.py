@@ -326,3 +326,23 @@ def test_config1_powerlaw_full_size_properties(cuda, tm):
     if os.path.exists(path):
         ref = load_golden("powerlaw_reference.json")
         assert census.tolist() == ref["census"]
+
+
+def test_cpp_host_mirror_driver(cuda, tm, oracle):
+    """The C++ header mirror (include/tmotif_b200.hpp) used as a reference
+    caller would: toy census == frozen vector; random graph == oracle."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "capi_parity")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    got = dict((l.split()[0], int(l.split()[1])) for l in out.stdout.splitlines())
+    assert got == load_golden("toy_frozen.json")["census"]
+    n, m, delta = 80, 4000, 300
+    s, d, t = oracle.generate_random_graph(n, m, 20000, 31337)
+    inp = "".join(f"{a} {b} {c}\n" for a, b, c in zip(s, d, t))
+    out = subprocess.run([exe, str(n), str(delta)], input=inp, capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    counts = [int(l.split()[1]) for l in out.stdout.splitlines()]
+    og = oracle.build_graph(n, s, d, t)
+    assert counts == oracle.census(og, delta).tolist()
