@@ -31,15 +31,26 @@ sys.path.insert(0, ROOT)
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "temporal edges/sec, exact 36-motif count (1/2/4/8 B200); % of HBM roofline"
 
-# Algorithmic bytes per unit for the kernels that can dominate a step (see
-# DESIGN.md "Roofline"): bytes that must cross HBM at least once per launch.
-#   star_full    per incident record: S t/nbr/node/gidx/pg (24 B) + its G record t/w2/pg (16 B)
-#   tri_oriented per forward record: F t/nbr/ord/node (20 B) + its G group probe (node_grp x2, 8 B)
-#   radix_downsweep per key: key+value read + key+value write
-ALGO_BYTES = {
-    "star_full": lambda m: 2 * m * 40,
-    "tri_oriented": lambda m: m * 28,
-}
+# Algorithmic bytes per STEP for each kernel family that can dominate a step
+# (DESIGN.md "Roofline"): bytes that must cross HBM at least once.
+#   star_filter   per incident record: G t (8 B) + w2 (4 B), neighbours' t from the same lines
+#   tri_filter    per forward record (one per edge): F t (8 B) + node (4 B)
+#   star_work / tri_work run on the filtered worklists only (random access, no streaming model)
+#   onesweep_pass per key per digit pass: (key + u32 value) read + write
+#                 node sort: u32 keys over 2m records, ceil(nb/8) passes
+#                 G sort:    u64 keys over 2m records, ceil(2nb/8) passes
+#                 t sort:    u64 keys over m edges, ceil(tbits/8) passes (only for unsorted input)
+#   scan          per element: predicate inputs read (4 B) + u32 output written (4 B)
+def algo_bytes(n, m, t):
+    R = 2 * m
+    nb = max(1, int(n - 1).bit_length())
+    tb = int(int(t.max()) - int(t.min())).bit_length() if m else 0
+    unsorted = bool(m > 1 and (np.diff(t) < 0).any())
+    sort = R * 8 * 2 * ((nb + 7) // 8) + R * 12 * 2 * ((2 * nb + 7) // 8)
+    if unsorted:
+        sort += m * 12 * 2 * ((tb + 7) // 8)
+    return {"star_filter": R * 12, "tri_filter": m * 12, "onesweep_pass": sort, "radix_downsweep": sort,
+            "scan": 4 * R * 8 + m * 8}
 
 
 def log(*a):
@@ -252,18 +263,22 @@ def main():
         step(False)
     torch.cuda.synchronize()
     tm.kernel_timing(enable=False)
-    names = ["star_full", "tri_oriented", "radix_downsweep", "radix_upsweep", "scan_down", "scan_reduce",
-             "gather_s", "gather_g", "forward_scatter", "node_keys", "group_keys", "validate", "offsets"]
+    names = ["star_filter", "star_work", "tri_filter", "tri_wedge", "tri_long", "onesweep_pass", "onesweep_hist", "scan", "gather_s", "gather_g",
+             "forward_scatter", "node_keys", "group_keys", "validate", "offsets", "group_table", "max_degree",
+             "node_group", "forward_off", "onesweep_base", "radix_upsweep", "radix_downsweep"]
     ktimes = {}
     for nm in names:
         tot_ms, cnt = tm.kernel_time(nm)
         if cnt:
             ktimes[nm] = {"ms_per_step": tot_ms / kk, "launches_per_step": cnt / kk}
-    dom = max(ALGO_BYTES, key=lambda k: ktimes.get(k, {}).get("ms_per_step", 0))
-    dom_ms = ktimes[dom]["ms_per_step"] / max(1.0, ktimes[dom]["launches_per_step"])
-    algo = ALGO_BYTES[dom](m)
+    abytes = algo_bytes(n, m, t)
+    dom = max(abytes, key=lambda k: ktimes.get(k, {}).get("ms_per_step", 0))
+    dom_ms = ktimes[dom]["ms_per_step"]
+    dom_launches = max(1.0, ktimes[dom]["launches_per_step"])
+    algo = abytes[dom] / dom_launches
+    launch_ms = dom_ms / dom_launches
     peak, peak_kind = peaks()
-    achieved = algo / (dom_ms * 1e-3) / 1e9
+    achieved = algo / (launch_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{dom}_{args.config}.json")
     if os.path.exists(tpath):
@@ -271,6 +286,9 @@ def main():
             traffic = json.load(open(tpath)).get("bytes_per_launch")
         except Exception:
             traffic = None
+    for k, v in ktimes.items():
+        if k in abytes:
+            v["algo_GBps"] = abytes[k] / (v["ms_per_step"] * 1e-3) / 1e9
 
     if rank != 0:
         if dist:
@@ -302,7 +320,8 @@ def main():
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "algo_bytes_per_launch": algo, "launch_ms": dom_ms},
+                     "algo_bytes_per_launch": algo, "launch_ms": launch_ms,
+                     "share_of_step": dom_ms / ms_step},
         "kernels": ktimes,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

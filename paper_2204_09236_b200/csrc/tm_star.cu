@@ -205,19 +205,48 @@ __device__ __forceinline__ void flush_acc(StarAcc& acc, uint64_t* out) {
     }
 }
 
-__global__ void __launch_bounds__(256) star_full_kernel(SView S, GView G, int64_t delta,
-                                                        uint32_t q_begin, uint32_t q_end,
+// Filter: one coalesced pass over G.  A record can contribute as a first
+// edge only if the next record of its neighbour group is inside its window,
+// and as a third edge only if the previous one is (otherwise every term of
+// first_role / third_role is zero).  Survivors go to two worklists.
+__global__ void __launch_bounds__(256) star_filter_kernel(GView G, int64_t delta, uint32_t kb,
+                                                          uint32_t ke, uint32_t* __restrict__ first_list,
+                                                          uint32_t* __restrict__ third_list,
+                                                          uint32_t* __restrict__ counters) {
+    for (uint64_t base = (uint64_t)kb + (uint64_t)blockIdx.x * blockDim.x; base < ke;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = base + threadIdx.x;
+        bool f = false, th = false;
+        if (k < ke) {
+            const uint32_t w2 = G.w2[k];
+            const int64_t t = G.t[k];
+            f = !(w2 & kLastBit) && G.t[k + 1] <= sat_add(t, delta);
+            th = !(w2 & kFirstBit) && G.t[k - 1] >= sat_sub(t, delta);
+        }
+        warp_append(f, (uint32_t)k, first_list, counters);
+        warp_append(th, (uint32_t)k, third_list, counters + 1);
+    }
+}
+
+// Work: the full first_role / third_role sums for the surviving records.
+__global__ void __launch_bounds__(256) star_work_kernel(SView S, GView G, int64_t delta, uint64_t n,
+                                                        const uint32_t* __restrict__ first_list,
+                                                        const uint32_t* __restrict__ third_list,
+                                                        const uint32_t* __restrict__ counters,
                                                         uint64_t* __restrict__ out) {
     StarAcc acc;
 #pragma unroll
     for (int j = 0; j < 32; ++j) acc.v[j] = 0;
-    for (uint64_t qq = (uint64_t)q_begin + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-         qq < q_end; qq += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t q = (uint32_t)qq;
-        const uint32_t u = S.node[q];
+    const uint32_t nf = counters[0], nt = counters[1];
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (uint64_t)nf + nt;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const bool first = idx < nf;
+        const uint32_t k = first ? first_list[idx] : third_list[idx - nf];
+        const uint32_t u = owner_of(S.off, n, k);
         const uint32_t start = S.off[u], end = S.off[u + 1];
-        first_role(S, G, q, start, end, delta, acc);
-        third_role(S, G, q, start, delta, 0u, end - start, acc);
+        const uint32_t q = start + (G.w2[k] & kPosMask);
+        if (first) first_role(S, G, q, start, end, delta, acc);
+        else third_role(S, G, q, start, delta, 0u, end - start, acc);
     }
     flush_acc(acc, out);
 }
@@ -274,12 +303,20 @@ __global__ void __launch_bounds__(256) star_items_kernel(
 void star_full(const DeviceGraph& g, int64_t delta, uint32_t q_begin, uint32_t q_end,
                uint64_t* d_out) {
     if (q_end <= q_begin) return;
+    cudaStream_t st = g.stream;
     const uint64_t work = q_end - q_begin;
     const uint64_t cap = (uint64_t)sm_count() * 8;
     uint64_t grid = (work + 255) / 256;
     if (grid > cap) grid = cap;
-    TM_LAUNCH("star_full", g.stream, star_full_kernel, (unsigned)grid, 256, 0, sview(g), gview(g),
-              delta, q_begin, q_end, d_out);
+    uint32_t* lists = dalloc<uint32_t>(2 * work + 2, st);
+    uint32_t* counters = lists + 2 * work;
+    TM_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), st));
+    // G positions of nodes [cb, ce) are the same range as their S positions
+    TM_LAUNCH("star_filter", st, star_filter_kernel, (unsigned)grid, 256, 0, gview(g), delta, q_begin,
+              q_end, lists, lists + work, counters);
+    TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), gview(g), delta, g.n,
+              lists, lists + work, counters, d_out);
+    dfree(lists, st);
 }
 
 void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,

@@ -152,21 +152,138 @@ __device__ __forceinline__ void flush_tri(TriAcc& acc, uint64_t* out) {
     }
 }
 
-__global__ void __launch_bounds__(256) tri_oriented_kernel(GView G, const int64_t* __restrict__ FT,
-                                                           const uint32_t* __restrict__ FN,
-                                                           const uint32_t* __restrict__ FO,
-                                                           const uint32_t* __restrict__ Fnode,
-                                                           const uint32_t* __restrict__ Foff,
-                                                           int64_t delta, uint32_t f_begin,
-                                                           uint32_t f_end, uint64_t* out) {
+// Filter + wedge expansion: one pass over F.  Thread i scans the next
+// kWedgeScan forward records of its center; every in-window record to a
+// different neighbour is a wedge (i, j), reserved warp-aggregated in one
+// atomic per warp and written to the wedge list.  A first edge whose window
+// runs past kWedgeScan records (or whose wedges do not fit the list) goes to
+// the long list instead and is enumerated by tri_long_kernel.
+constexpr int kWedgeScan = 8;
+
+__global__ void __launch_bounds__(256) tri_filter_kernel(const int64_t* __restrict__ FT,
+                                                         const uint32_t* __restrict__ FN,
+                                                         const uint32_t* __restrict__ Fnode,
+                                                         int64_t delta, uint32_t fb, uint32_t fe,
+                                                         uint64_t* __restrict__ wedges,
+                                                         uint32_t wedge_cap,
+                                                         uint32_t* __restrict__ long_list,
+                                                         uint32_t* __restrict__ counters) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t base = (uint64_t)fb + (uint64_t)blockIdx.x * blockDim.x; base < fe;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = base + threadIdx.x;
+        uint32_t node = 0, v = 0, nw = 0;
+        int64_t lim = 0;
+        bool alive = false, is_long = false;
+        if (i + 1 < fe) {
+            node = Fnode[i];
+            v = FN[i] & kNodeMask;
+            lim = sat_add(FT[i], delta);
+            alive = true;
+        }
+        uint32_t hits = 0;  // bit s-1: record i+s is a wedge partner
+#pragma unroll
+        for (int s = 1; s <= kWedgeScan; ++s) {
+            const uint64_t j = i + s;
+            if (alive) {
+                if (j >= fe || Fnode[j] != node || FT[j] > lim) {
+                    alive = false;
+                } else if ((FN[j] & kNodeMask) != v) {
+                    hits |= 1u << (s - 1);
+                }
+            }
+        }
+        if (alive && i + kWedgeScan + 1 < fe && Fnode[i + kWedgeScan + 1] == node &&
+            FT[i + kWedgeScan + 1] <= lim)
+            is_long = true;
+        nw = is_long ? 0u : (uint32_t)__popc(hits);
+        // reserve nw slots per lane with one atomic per warp
+        uint32_t incl = nw;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t wbase = 0;
+        if (total) {
+            if (lane == 31) wbase = atomicAdd(counters, total);
+            wbase = __shfl_sync(0xffffffffu, wbase, 31);
+        }
+        const bool fits = total == 0 || (uint64_t)wbase + total <= wedge_cap;
+        if (!fits && lane == 31) atomicMin(counters + 2, wbase);  // valid wedges end here
+        if (nw && fits) {
+            uint32_t o = wbase + incl - nw;
+            uint32_t h = hits;
+            while (h) {
+                const int s = __ffs(h);
+                h &= h - 1;
+                wedges[o++] = ((uint64_t)i << 32) | (uint32_t)(i + s);
+            }
+        }
+        warp_append(is_long || (nw && !fits), (uint32_t)i, long_list, counters + 1);
+    }
+}
+
+__device__ __forceinline__ void add_wedge(const GView& G, const int64_t* __restrict__ FT,
+                                          const uint32_t* __restrict__ FN,
+                                          const uint32_t* __restrict__ FO, uint32_t i, uint32_t j,
+                                          int64_t delta, TriAcc& acc) {
+    const uint32_t ni = FN[i], nj = FN[j];
+    const int64_t ti = FT[i], tj = FT[j];
+    uint32_t c[6];
+    closing_counts(G, ni & kNodeMask, nj & kNodeMask, sat_sub(tj, delta), sat_add(ti, delta), ti,
+                   FO[i], tj, FO[j], c);
+    const uint32_t cell0 = (ni >> 31) * 4 + (nj >> 31) * 2;  // di*4 + dj*2
+#pragma unroll
+    for (int ty = 0; ty < 3; ++ty)
+#pragma unroll
+        for (int dk = 0; dk < 2; ++dk)
+#pragma unroll
+            for (int dd = 0; dd < 8; dd += 2) {
+                if (dd == (int)cell0) acc.v[ty * 8 + dd + dk] += c[ty * 2 + dk];
+            }
+}
+
+// one wedge per thread
+__global__ void __launch_bounds__(256) tri_wedge_kernel(GView G, const int64_t* __restrict__ FT,
+                                                        const uint32_t* __restrict__ FN,
+                                                        const uint32_t* __restrict__ FO,
+                                                        int64_t delta,
+                                                        const uint64_t* __restrict__ wedges,
+                                                        uint32_t wedge_cap,
+                                                        const uint32_t* __restrict__ counters,
+                                                        uint64_t* out) {
     TriAcc acc;
 #pragma unroll
     for (int j = 0; j < 24; ++j) acc.v[j] = 0;
-    for (uint64_t ii = (uint64_t)f_begin + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-         ii < f_end; ii += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t i = (uint32_t)ii;
-        const uint32_t end = Foff[Fnode[i] + 1];
-        wedges_from(G, FT, FN, FO, i, end, delta, nullptr, acc);
+    const uint32_t cnt = min(min(counters[0], wedge_cap), counters[2]);
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = wedges[idx];
+        add_wedge(G, FT, FN, FO, (uint32_t)(w >> 32), (uint32_t)w, delta, acc);
+    }
+    flush_tri(acc, out);
+}
+
+// first edges with long windows: the whole wedge loop in one thread
+__global__ void __launch_bounds__(256) tri_long_kernel(GView G, const int64_t* __restrict__ FT,
+                                                       const uint32_t* __restrict__ FN,
+                                                       const uint32_t* __restrict__ FO,
+                                                       const uint32_t* __restrict__ Fnode,
+                                                       const uint32_t* __restrict__ Foff,
+                                                       int64_t delta,
+                                                       const uint32_t* __restrict__ list,
+                                                       const uint32_t* __restrict__ counters,
+                                                       uint64_t* out) {
+    TriAcc acc;
+#pragma unroll
+    for (int j = 0; j < 24; ++j) acc.v[j] = 0;
+    const uint32_t cnt = counters[1];
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = list[idx];
+        wedges_from(G, FT, FN, FO, i, Foff[Fnode[i] + 1], delta, nullptr, acc);
     }
     flush_tri(acc, out);
 }
@@ -211,12 +328,26 @@ __global__ void __launch_bounds__(256) tri_items_kernel(SView S, GView G, int64_
 void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
                   uint32_t f_end, uint64_t* d_out) {
     if (f_end <= f_begin) return;
+    cudaStream_t st = g.stream;
     const uint64_t work = f_end - f_begin;
     const uint64_t cap = (uint64_t)sm_count() * 8;
     uint64_t grid = (work + 255) / 256;
     if (grid > cap) grid = cap;
-    TM_LAUNCH("tri_oriented", g.stream, tri_oriented_kernel, (unsigned)grid, 256, 0, gview(g), f.t,
-              f.nbr, f.ord, f.node, f.off, delta, f_begin, f_end, d_out);
+    const uint64_t wedge_cap64 = work + 1024;  // overflow spills to the long list
+    const uint32_t wedge_cap = (uint32_t)(wedge_cap64 < 0xFFFFFFF0ull ? wedge_cap64 : 0xFFFFFFF0ull);
+    uint64_t* wedges = dalloc<uint64_t>(wedge_cap, st);
+    uint32_t* long_list = dalloc<uint32_t>(work + 3, st);
+    uint32_t* counters = long_list + work;  // [0] wedges reserved, [1] long list, [2] valid end
+    TM_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), st));
+    TM_CUDA(cudaMemsetAsync(counters + 2, 0xFF, sizeof(uint32_t), st));
+    TM_LAUNCH("tri_filter", st, tri_filter_kernel, (unsigned)grid, 256, 0, f.t, f.nbr, f.node, delta,
+              f_begin, f_end, wedges, wedge_cap, long_list, counters);
+    TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, gview(g), f.t, f.nbr, f.ord,
+              delta, wedges, wedge_cap, counters, d_out);
+    TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, gview(g), f.t, f.nbr, f.ord,
+              f.node, f.off, delta, long_list, counters, d_out);
+    dfree(wedges, st);
+    dfree(long_list, st);
 }
 
 void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
