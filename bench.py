@@ -33,24 +33,29 @@ METRIC = "temporal edges/sec, exact 36-motif count (1/2/4/8 B200); % of HBM roof
 
 # Algorithmic bytes per STEP for each kernel family that can dominate a step
 # (DESIGN.md "Roofline"): bytes that must cross HBM at least once.
-#   star_filter   per incident record: G t (8 B) + w2 (4 B), neighbours' t from the same lines
+#   star_filter   per edge: P t (8 B) + w (4 B) + qmin/qmax (8 B), neighbours' t from the same lines
 #   tri_filter    per forward record (one per edge): F t (8 B) + node (4 B)
 #   star_work / tri_work run on the filtered worklists only (random access, no streaming model)
-#   onesweep_pass per key per digit pass: (key + u32 value) read + write
-#                 node sort: u32 keys over 2m records, ceil(nb/8) passes
-#                 G sort:    u64 keys over 2m records, ceil(2nb/8) passes
-#                 t sort:    u64 keys over m edges, ceil(tbits/8) passes (only for unsorted input)
+#   radix_downsweep per key per digit pass: key (+ value) read + write
+#                 node sort: packed u64 keys over 2m records, ceil(nb/8) passes
+#                 pair sort: packed u64 keys over m edges, ceil(2nb/8) passes
+#                 t sort:    packed u64 keys over m edges, ceil(tbits/8) passes (unsorted input only)
 #   scan          per element: predicate inputs read (4 B) + u32 output written (4 B)
 def algo_bytes(n, m, t):
     R = 2 * m
     nb = max(1, int(n - 1).bit_length())
+    pbits = max(1, int(m - 1).bit_length())
     tb = int(int(t.max()) - int(t.min())).bit_length() if m else 0
     unsorted = bool(m > 1 and (np.diff(t) < 0).any())
-    sort = R * 8 * 2 * ((nb + 7) // 8) + R * 12 * 2 * ((2 * nb + 7) // 8)
+    # node sort: packed u64 keys (node << 32 | record), keys only
+    sort = R * 8 * 2 * ((nb + 7) // 8)
+    # pair sort: packed u64 keys when 2nb + pbits <= 64, else u64 key + u32 value
+    pk = 8 if 2 * nb + pbits <= 64 else 12
+    sort += m * pk * 2 * ((2 * nb + 7) // 8)
     if unsorted:
-        sort += m * 12 * 2 * ((tb + 7) // 8)
-    return {"star_filter": R * 12, "tri_filter": m * 12, "onesweep_pass": sort, "radix_downsweep": sort,
-            "scan": 4 * R * 8 + m * 8}
+        sort += m * (8 if tb + pbits <= 64 else 12) * 2 * ((tb + 7) // 8)
+    return {"star_filter": m * 20, "tri_filter": m * 12, "radix_downsweep": sort,
+            "scan": 2 * R * 4 + m * 8}
 
 
 def log(*a):
@@ -263,9 +268,9 @@ def main():
         step(False)
     torch.cuda.synchronize()
     tm.kernel_timing(enable=False)
-    names = ["star_filter", "star_work", "tri_filter", "tri_wedge", "tri_long", "onesweep_pass", "onesweep_hist", "scan", "gather_s", "gather_g",
-             "forward_scatter", "node_keys", "group_keys", "validate", "offsets", "group_table", "max_degree",
-             "node_group", "forward_off", "onesweep_base", "radix_upsweep", "radix_downsweep"]
+    names = ["star_filter", "star_work", "tri_filter", "tri_wedge", "tri_long", "radix_upsweep",
+             "radix_downsweep", "scan", "gather_s", "gather_p", "forward_scatter", "pack_edges", "pair_keys",
+             "time_keys", "perm_from_keys", "validate", "offsets", "pair_offsets", "forward_off"]
     ktimes = {}
     for nm in names:
         tot_ms, cnt = tm.kernel_time(nm)

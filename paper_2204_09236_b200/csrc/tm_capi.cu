@@ -513,31 +513,33 @@ int tm_pair_window(const tm_graph* g, uint32_t v, uint32_t w, int64_t lo, int64_
         auto* G = const_cast<tm_graph*>(g);
         if (v >= G->g.n || w >= G->g.n) throw tm_error(TM_ERR_INVALID, "node out of range");
         if (len) *len = 0;
+        if (v == w || lo > hi) return TM_OK;
         cudaStream_t st = G->g.stream;
-        const uint32_t g0 = read_u32(G->g.node_grp, v, st), g1 = read_u32(G->g.node_grp, v + 1, st);
-        std::vector<uint32_t> nb(g1 - g0);
-        if (g1 > g0) {
-            TM_CUDA(cudaMemcpyAsync(nb.data(), G->g.grp_nbr + g0, (g1 - g0) * 4,
-                                    cudaMemcpyDeviceToHost, st));
+        const uint32_t a = std::min(v, w), b = std::max(v, w);
+        const uint32_t k0 = read_u32(G->g.pofs, a, st), k1 = read_u32(G->g.pofs, a + 1, st);
+        std::vector<uint32_t> mx(k1 - k0);
+        if (k1 > k0) {
+            TM_CUDA(cudaMemcpyAsync(mx.data(), G->g.P_max + k0, (k1 - k0) * 4, cudaMemcpyDeviceToHost, st));
             TM_CUDA(cudaStreamSynchronize(st));
         }
-        auto it = std::lower_bound(nb.begin(), nb.end(), w);
-        if (it == nb.end() || *it != w || lo > hi) return TM_OK;
-        const uint32_t gi = g0 + (uint32_t)(it - nb.begin());
-        const uint32_t kb = read_u32(G->g.grp_off, gi, st), ke = read_u32(G->g.grp_off, gi + 1, st);
+        auto lo_it = std::lower_bound(mx.begin(), mx.end(), b);
+        auto hi_it = std::upper_bound(lo_it, mx.end(), b);
+        const uint32_t kb = k0 + (uint32_t)(lo_it - mx.begin()), ke = k0 + (uint32_t)(hi_it - mx.begin());
+        if (ke == kb) return TM_OK;
         std::vector<int64_t> ht(ke - kb);
         std::vector<uint32_t> ho(ke - kb), hw(ke - kb);
-        TM_CUDA(cudaMemcpyAsync(ht.data(), G->g.G_t + kb, (ke - kb) * 8, cudaMemcpyDeviceToHost, st));
-        TM_CUDA(cudaMemcpyAsync(ho.data(), G->g.G_ord + kb, (ke - kb) * 4, cudaMemcpyDeviceToHost, st));
-        TM_CUDA(cudaMemcpyAsync(hw.data(), G->g.G_w2 + kb, (ke - kb) * 4, cudaMemcpyDeviceToHost, st));
+        TM_CUDA(cudaMemcpyAsync(ht.data(), G->g.P_t + kb, (ke - kb) * 8, cudaMemcpyDeviceToHost, st));
+        TM_CUDA(cudaMemcpyAsync(ho.data(), G->g.P_ord + kb, (ke - kb) * 4, cudaMemcpyDeviceToHost, st));
+        TM_CUDA(cudaMemcpyAsync(hw.data(), G->g.P_w + kb, (ke - kb) * 4, cudaMemcpyDeviceToHost, st));
         TM_CUDA(cudaStreamSynchronize(st));
+        const uint32_t flip = v == a ? 0u : 1u;
         uint64_t k = 0;
         for (uint32_t x = 0; x < ke - kb; ++x) {
             if (ht[x] < lo || ht[x] > hi) continue;
             if (k < cap) {
                 if (t) t[k] = ht[x];
                 if (ordinal) ordinal[k] = ho[x];
-                if (dir_rel_v) dir_rel_v[k] = (uint8_t)(hw[x] >> 31);
+                if (dir_rel_v) dir_rel_v[k] = (uint8_t)((hw[x] >> 31) ^ flip);
             }
             ++k;
         }
@@ -616,6 +618,7 @@ int tm_count_star_pair_items(tm_graph* g, int64_t delta, uint64_t n_items, const
         TM_CUDA(cudaMemcpyAsync(dfo, fo.data(), (n_items + 1) * 8, cudaMemcpyHostToDevice, s));
         TM_CUDA(cudaMemcpyAsync(dto, to.data(), (n_items + 1) * 8, cudaMemcpyHostToDevice, s));
         TM_CUDA(cudaMemsetAsync(dout, 0, n_items * 32 * 8, s));
+        build_s_pidx(g->g);
         star_items(g->g, delta, n_items, dn, db, de, dfo, fo[n_items], to[n_items], dto, dout);
         std::vector<uint64_t> raw(n_items * 32);
         TM_CUDA(cudaMemcpyAsync(raw.data(), dout, n_items * 32 * 8, cudaMemcpyDeviceToHost, s));

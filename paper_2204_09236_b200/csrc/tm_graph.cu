@@ -7,8 +7,10 @@
 //      edge order is the reference's (t, ordinal) total order;
 //   3. stable radix sort of the 2m incident records (emitted in that order)
 //      by node -> S, the per-node time-ordered sequences;
-//   4. stable radix sort of S by (node, other) -> G, the same records grouped
-//      by neighbour; its (v, w) groups are the per-pair time-sorted edge lists.
+//   4. stable radix sort of the edges by unordered pair {min, max} -> P, the
+//      per-pair time-sorted edge lists (PairEdgeIndex), which are also each
+//      endpoint's same-neighbour runs.  Keys carry their payload in the low
+//      bits when it fits (keys-only sorts).
 #include "tm_primitives.cuh"
 
 namespace tmb {
@@ -53,43 +55,68 @@ __global__ void validate_kernel(const uint32_t* __restrict__ src, const uint32_t
     }
 }
 
-__global__ void time_keys_kernel(const int64_t* __restrict__ t, uint64_t m, int64_t tmin,
-                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+// packed (t - tmin) << kbits | k  when it fits 64 bits, else key = t - tmin, val = k
+__global__ void time_keys_kernel(const int64_t* __restrict__ t, uint64_t m, int64_t tmin, int kbits,
+                                 bool packed, uint64_t* __restrict__ keys,
+                                 uint32_t* __restrict__ vals) {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        keys[k] = (uint64_t)t[k] - (uint64_t)tmin;
-        vals[k] = (uint32_t)k;
+        const uint64_t rel = (uint64_t)t[k] - (uint64_t)tmin;
+        if (packed) {
+            keys[k] = (rel << kbits) | k;
+        } else {
+            keys[k] = rel;
+            vals[k] = (uint32_t)k;
+        }
     }
 }
 
-// record r = 2p + side of the p-th edge in (t, ordinal) order
-__global__ void node_keys_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ src,
-                                 const uint32_t* __restrict__ dst, uint64_t R,
-                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R;
-         r += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t p = r >> 1;
+__global__ void perm_from_keys_kernel(const uint64_t* __restrict__ keys, uint64_t m, uint64_t kmask,
+                                      uint32_t* __restrict__ perm) {
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x)
+        perm[p] = (uint32_t)(keys[p] & kmask);
+}
+
+// Edges packed in (t, ordinal) order, 16 B each, so every later random gather
+// touches one sector; node sort keys for both records of each edge.
+struct PackedEdge {
+    int64_t t;
+    uint32_t src;
+    uint32_t dst;
+};
+
+// record r = 2p + side of the p-th edge in (t, ordinal) order: key node << 32 | r
+__global__ void pack_edges_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ src,
+                                  const uint32_t* __restrict__ dst, const int64_t* __restrict__ t,
+                                  uint64_t m, PackedEdge* __restrict__ E,
+                                  uint64_t* __restrict__ keys) {
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t k = perm ? perm[p] : (uint32_t)p;
-        keys[r] = (r & 1) ? dst[k] : src[k];
-        vals[r] = (uint32_t)r;
+        const uint32_t a = src[k], b = dst[k];
+        E[p] = PackedEdge{t[k], a, b};
+        keys[2 * p] = ((uint64_t)a << 32) | (2 * p);
+        keys[2 * p + 1] = ((uint64_t)b << 32) | (2 * p + 1);
     }
 }
 
-__global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ src,
-                                const uint32_t* __restrict__ dst, const int64_t* __restrict__ t,
-                                const uint32_t* __restrict__ skeys,
-                                const uint32_t* __restrict__ svals, uint64_t R,
+__global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedEdge* __restrict__ E,
+                                const uint64_t* __restrict__ skeys, uint64_t R,
                                 int64_t* __restrict__ S_t, uint32_t* __restrict__ S_nbr,
-                                uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node) {
+                                uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
+                                uint32_t* __restrict__ rec2s) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
          q += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t r = svals[q];
+        const uint64_t key = skeys[q];
+        const uint32_t r = (uint32_t)key;
         const uint32_t p = r >> 1, side = r & 1u;
-        const uint32_t k = perm ? perm[p] : p;
-        S_t[q] = t[k];
-        S_ord[q] = k;
-        S_node[q] = skeys[q];
-        S_nbr[q] = (side ? src[k] : dst[k]) | (side << 31);
+        const PackedEdge e = E[p];
+        S_t[q] = e.t;
+        S_ord[q] = perm ? perm[p] : p;
+        S_node[q] = (uint32_t)(key >> 32);
+        S_nbr[q] = (side ? e.src : e.dst) | (side << 31);
+        rec2s[r] = (uint32_t)q;
     }
 }
 
@@ -106,71 +133,71 @@ __global__ void offsets_kernel(const uint32_t* __restrict__ node, uint64_t R, ui
     }
 }
 
-__global__ void max_degree_kernel(const uint32_t* __restrict__ off, uint64_t n, BuildStats* st) {
-    unsigned mx = 0;
-    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-         u += (uint64_t)gridDim.x * blockDim.x)
-        mx = max(mx, off[u + 1] - off[u]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(&st->max_degree, mx);
-}
-
-__global__ void group_keys_kernel(const uint32_t* __restrict__ S_node,
-                                  const uint32_t* __restrict__ S_nbr, uint64_t R, int nb,
-                                  uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
-         q += (uint64_t)gridDim.x * blockDim.x) {
-        keys[q] = ((uint64_t)S_node[q] << nb) | (S_nbr[q] & kNodeMask);
-        vals[q] = (uint32_t)q;
-    }
-}
-
-__global__ void gather_g_kernel(const uint64_t* __restrict__ gkeys,
-                                const uint32_t* __restrict__ gvals, uint64_t R, int nb,
-                                const uint32_t* __restrict__ off, const int64_t* __restrict__ S_t,
-                                const uint32_t* __restrict__ S_ord,
-                                const uint32_t* __restrict__ S_nbr,
-                                const uint32_t* __restrict__ S_pg, int64_t* __restrict__ G_t,
-                                uint32_t* __restrict__ G_ord, uint32_t* __restrict__ G_w2,
-                                uint32_t* __restrict__ G_pg, uint32_t* __restrict__ S_gidx) {
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < R;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t q = gvals[k];
-        const uint64_t key = gkeys[k];
-        const uint32_t node = (uint32_t)(key >> nb);
-        const uint32_t first = (k == 0 || gkeys[k - 1] != key) ? kFirstBit : 0u;
-        const uint32_t last = (k == R - 1 || gkeys[k + 1] != key) ? kLastBit : 0u;
-        const uint32_t pos = q - off[node];
-        G_t[k] = S_t[q];
-        G_ord[k] = S_ord[q];
-        G_pg[k] = S_pg[q];
-        G_w2[k] = pos | first | last | (S_nbr[q] & kDirBit);
-        S_gidx[q] = (uint32_t)k;
-    }
-}
-
-__global__ void group_table_kernel(const uint64_t* __restrict__ gkeys,
-                                   const uint32_t* __restrict__ G_w2,
-                                   const uint32_t* __restrict__ gscan, uint64_t R, uint64_t nmask,
-                                   uint32_t* __restrict__ grp_nbr, uint32_t* __restrict__ grp_off) {
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < R;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        if (G_w2[k] & kFirstBit) {
-            const uint32_t g = gscan[k];
-            grp_off[g] = (uint32_t)k;
-            grp_nbr[g] = (uint32_t)(gkeys[k] & nmask);
+// pair keys of the edges in (t, ordinal) order: (min << nb | max) [<< pbits | p]
+__global__ void pair_keys_kernel(const PackedEdge* __restrict__ E, uint64_t m, int nb, int pbits,
+                                 bool packed, uint64_t* __restrict__ keys,
+                                 uint32_t* __restrict__ vals) {
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = E[p].src, b = E[p].dst;
+        const uint64_t key2 = ((uint64_t)min(a, b) << nb) | max(a, b);
+        if (packed) {
+            keys[p] = (key2 << pbits) | p;
+        } else {
+            keys[p] = key2;
+            vals[p] = (uint32_t)p;
         }
-        if (k == R - 1) grp_off[gscan[R]] = (uint32_t)R;
     }
 }
 
-__global__ void node_group_kernel(const uint32_t* __restrict__ off,
-                                  const uint32_t* __restrict__ gscan, uint64_t n,
-                                  uint32_t* __restrict__ node_grp) {
-    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= n;
-         u += (uint64_t)gridDim.x * blockDim.x)
-        node_grp[u] = gscan[off[u]];
+__global__ void gather_p_kernel(const uint64_t* __restrict__ pkeys, const uint32_t* __restrict__ pvals,
+                                uint64_t m, int nb, int pbits, bool packed,
+                                const uint32_t* __restrict__ perm, const PackedEdge* __restrict__ E,
+                                const uint32_t* __restrict__ rec2s,
+                                int64_t* __restrict__ P_t, uint32_t* __restrict__ P_ord,
+                                uint32_t* __restrict__ P_max, uint32_t* __restrict__ P_w,
+                                uint32_t* __restrict__ P_qmin, uint32_t* __restrict__ P_qmax) {
+    const uint64_t nmask = (1ull << nb) - 1;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = pkeys[k];
+        const uint64_t key2 = packed ? key >> pbits : key;
+        const uint32_t p = packed ? (uint32_t)(key & ((1ull << pbits) - 1)) : pvals[k];
+        const uint32_t a = (uint32_t)(key2 >> nb), b = (uint32_t)(key2 & nmask);
+        const PackedEdge ed = E[p];
+        const uint32_t side_min = ed.src == a ? 0u : 1u;  // record side of the min endpoint
+        const bool first = k == 0 || (packed ? pkeys[k - 1] >> pbits : pkeys[k - 1]) != key2;
+        const bool last = k == m - 1 || (packed ? pkeys[k + 1] >> pbits : pkeys[k + 1]) != key2;
+        const uint2 qq = reinterpret_cast<const uint2*>(rec2s)[p];  // records 2p, 2p+1
+        P_t[k] = ed.t;
+        P_ord[k] = perm ? perm[p] : p;
+        P_max[k] = b;
+        P_w[k] = (side_min << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u);
+        P_qmin[k] = side_min ? qq.y : qq.x;
+        P_qmax[k] = side_min ? qq.x : qq.y;
+    }
+}
+
+__global__ void s_pidx_kernel(const uint32_t* __restrict__ qmin, const uint32_t* __restrict__ qmax,
+                              uint64_t m, uint32_t* __restrict__ S_pidx) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        S_pidx[qmin[k]] = (uint32_t)k;
+        S_pidx[qmax[k]] = (uint32_t)k;
+    }
+}
+
+// pofs[x] = first P position whose min endpoint is x
+__global__ void pair_offsets_kernel(const uint64_t* __restrict__ pkeys, uint64_t m, uint64_t n,
+                                    int shift, uint32_t* __restrict__ pofs) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t cur = (int64_t)(pkeys[k] >> shift);
+        const int64_t prev = k ? (int64_t)(pkeys[k - 1] >> shift) : -1;
+        for (int64_t x = prev + 1; x <= cur; ++x) pofs[x] = (uint32_t)k;
+        if (k == m - 1)
+            for (int64_t x = cur + 1; x <= (int64_t)n; ++x) pofs[x] = (uint32_t)m;
+    }
 }
 
 struct OutwardLoad {
@@ -179,17 +206,6 @@ struct OutwardLoad {
         return (nbr[i] & kDirBit) ? 0u : 1u;
     }
 };
-struct InwardG {
-    const uint32_t* w2;
-    __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return w2[i] >> 31; }
-};
-struct FirstG {
-    const uint32_t* w2;
-    __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
-        return (w2[i] >> 29) & 1u;
-    }
-};
-
 // forward(u -> x): mode 0 degree rank (deg, id), mode 1 node index
 struct ForwardFlag {
     const uint32_t* node;
@@ -257,108 +273,100 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     }
     TM_CUDA(cudaMemcpyAsync(&h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, s));
     TM_CUDA(cudaStreamSynchronize(s));
-    if (h_st.bad) {
-        dfree(d_st, s);
-        throw tm_error(1, "self-loop or out-of-range endpoint in edge list");
-    }
+    dfree(d_st, s);
+    if (h_st.bad) throw tm_error(1, "self-loop or out-of-range endpoint in edge list");
 
     g.off = dalloc<uint32_t>(n + 1, s);
-    g.node_grp = dalloc<uint32_t>(n + 1, s);
+    g.pofs = dalloc<uint32_t>(n + 1, s);
     g.S_t = dalloc<int64_t>(R, s);
     g.S_nbr = dalloc<uint32_t>(R, s);
     g.S_ord = dalloc<uint32_t>(R, s);
     g.S_node = dalloc<uint32_t>(R, s);
     g.S_pg = dalloc<uint32_t>(R + 1, s);
-    g.S_gidx = dalloc<uint32_t>(R, s);
-    g.G_t = dalloc<int64_t>(R, s);
-    g.G_ord = dalloc<uint32_t>(R, s);
-    g.G_w2 = dalloc<uint32_t>(R, s);
-    g.G_pg = dalloc<uint32_t>(R, s);
-    g.G_dscan = dalloc<uint32_t>(R + 1, s);
-    g.grp_nbr = dalloc<uint32_t>(R, s);
-    g.grp_off = dalloc<uint32_t>(R + 1, s);
+    g.P_t = dalloc<int64_t>(m, s);
+    g.P_ord = dalloc<uint32_t>(m, s);
+    g.P_max = dalloc<uint32_t>(m, s);
+    g.P_w = dalloc<uint32_t>(m, s);
+    g.P_qmin = dalloc<uint32_t>(m, s);
+    g.P_qmax = dalloc<uint32_t>(m, s);
 
     if (m == 0) {
         TM_CUDA(cudaMemsetAsync(g.off, 0, (n + 1) * sizeof(uint32_t), s));
-        TM_CUDA(cudaMemsetAsync(g.node_grp, 0, (n + 1) * sizeof(uint32_t), s));
+        TM_CUDA(cudaMemsetAsync(g.pofs, 0, (n + 1) * sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.S_pg, 0, sizeof(uint32_t), s));
-        TM_CUDA(cudaMemsetAsync(g.G_dscan, 0, sizeof(uint32_t), s));
-        TM_CUDA(cudaMemsetAsync(g.grp_off, 0, sizeof(uint32_t), s));
-        g.ng = 0;
         g.max_degree = 0;
-        dfree(d_st, s);
         return;
     }
+    uint32_t* nullv = nullptr;
+    uint32_t* nullv2 = nullptr;
 
-    // 2. (t, ordinal) order of the edges
+    // 1. (t, ordinal) order of the edges (skipped for time-ordered input)
     uint32_t* perm = nullptr;
     if (h_st.unsorted) {
+        const int tbits = bit_width_u64((uint64_t)h_st.tmax - (uint64_t)h_st.tmin);
+        const int kbits = bit_width_u64(m - 1 ? m - 1 : 1);
+        const bool packed = tbits + kbits <= 64;
         uint64_t* k0 = dalloc<uint64_t>(m, s);
         uint64_t* k1 = dalloc<uint64_t>(m, s);
-        uint32_t* v0 = dalloc<uint32_t>(m, s);
-        uint32_t* v1 = dalloc<uint32_t>(m, s);
-        TM_LAUNCH("time_keys", s, time_keys_kernel, grid_for(m), 256, 0, d_t, m,
-                  (int64_t)h_st.tmin, k0, v0);
-        const int tbits = bit_width_u64((uint64_t)h_st.tmax - (uint64_t)h_st.tmin);
-        radix_sort_pairs<uint64_t>(k0, v0, k1, v1, m, tbits, s);
-        perm = v0;
+        uint32_t* v0 = packed ? nullptr : dalloc<uint32_t>(m, s);
+        uint32_t* v1 = packed ? nullptr : dalloc<uint32_t>(m, s);
+        TM_LAUNCH("time_keys", s, time_keys_kernel, grid_for(m), 256, 0, d_t, m, (int64_t)h_st.tmin,
+                  kbits, packed, k0, v0);
+        if (packed) {
+            radix_sort<uint64_t>(k0, nullv, k1, nullv2, m, kbits, kbits + tbits, s);
+            perm = dalloc<uint32_t>(m, s);
+            TM_LAUNCH("perm_from_keys", s, perm_from_keys_kernel, grid_for(m), 256, 0, k0, m,
+                      (1ull << kbits) - 1, perm);
+        } else {
+            radix_sort<uint64_t>(k0, v0, k1, v1, m, 0, tbits, s);
+            perm = v0;
+            dfree(v1, s);
+        }
         dfree(k0, s);
         dfree(k1, s);
-        dfree(v1, s);
     }
 
-    // 3. S: stable sort of incident records by node
+    // 2. S: stable sort of the incident records by node (key node << 32 | r)
     const int nb = bit_width_u64(n > 1 ? n - 1 : 1);
-    uint32_t* nk0 = dalloc<uint32_t>(R, s);
-    uint32_t* nk1 = dalloc<uint32_t>(R, s);
-    uint32_t* nv0 = dalloc<uint32_t>(R, s);
-    uint32_t* nv1 = dalloc<uint32_t>(R, s);
-    TM_LAUNCH("node_keys", s, node_keys_kernel, grid_for(R), 256, 0, perm, d_src, d_dst, R, nk0,
-              nv0);
-    radix_sort_pairs<uint32_t>(nk0, nv0, nk1, nv1, R, nb, s);
-    TM_LAUNCH("gather_s", s, gather_s_kernel, grid_for(R), 256, 0, perm, d_src, d_dst, d_t, nk0,
-              nv0, R, g.S_t, g.S_nbr, g.S_ord, g.S_node);
-    dfree(nk0, s);
-    dfree(nk1, s);
-    dfree(nv0, s);
-    dfree(nv1, s);
+    {
+        uint64_t* nk0 = dalloc<uint64_t>(R, s);
+        uint64_t* nk1 = dalloc<uint64_t>(R, s);
+        uint32_t* rec2s = dalloc<uint32_t>(R, s);
+        PackedEdge* E = dalloc<PackedEdge>(m, s);
+        TM_LAUNCH("pack_edges", s, pack_edges_kernel, grid_for(m), 256, 0, perm, d_src, d_dst, d_t, m, E,
+                  nk0);
+        radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s);
+        TM_LAUNCH("gather_s", s, gather_s_kernel, grid_for(R), 256, 0, perm, E, nk0, R, g.S_t, g.S_nbr,
+                  g.S_ord, g.S_node, rec2s);
+        dfree(nk0, s);
+        dfree(nk1, s);
+        TM_LAUNCH("offsets", s, offsets_kernel, grid_for(R), 256, 0, g.S_node, R, n, g.off);
+        exclusive_scan<uint32_t>(OutwardLoad{g.S_nbr}, R, g.S_pg, s);
+
+        // 3. P: stable sort of the edges by unordered pair {min, max}
+        const int pbits = bit_width_u64(m - 1 ? m - 1 : 1);
+        const bool packed = 2 * nb + pbits <= 64;
+        uint64_t* pk0 = dalloc<uint64_t>(m, s);
+        uint64_t* pk1 = dalloc<uint64_t>(m, s);
+        uint32_t* pv0 = packed ? nullptr : dalloc<uint32_t>(m, s);
+        uint32_t* pv1 = packed ? nullptr : dalloc<uint32_t>(m, s);
+        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(m), 256, 0, E, m, nb, pbits, packed, pk0,
+                  pv0);
+        if (packed) radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, pbits, pbits + 2 * nb, s);
+        else radix_sort<uint64_t>(pk0, pv0, pk1, pv1, m, 0, 2 * nb, s);
+        TM_LAUNCH("gather_p", s, gather_p_kernel, grid_for(m), 256, 0, pk0, pv0, m, nb, pbits, packed,
+                  perm, E, rec2s, g.P_t, g.P_ord, g.P_max, g.P_w, g.P_qmin, g.P_qmax);
+        TM_LAUNCH("pair_offsets", s, pair_offsets_kernel, grid_for(m), 256, 0, pk0, m, n,
+                  packed ? pbits + nb : nb, g.pofs);
+        dfree(pk0, s);
+        dfree(pk1, s);
+        dfree(pv0, s);
+        dfree(pv1, s);
+        dfree(rec2s, s);
+        dfree(E, s);
+    }
     if (perm) dfree(perm, s);
-
-    TM_LAUNCH("offsets", s, offsets_kernel, grid_for(R), 256, 0, g.S_node, R, n, g.off);
-    TM_LAUNCH("max_degree", s, max_degree_kernel, grid_for(n), 256, 0, g.off, n, d_st);
-    exclusive_scan<uint32_t>(OutwardLoad{g.S_nbr}, R, g.S_pg, s);
-
-    // 4. G: stable sort of S by (node, other)
-    uint64_t* gk0 = dalloc<uint64_t>(R, s);
-    uint64_t* gk1 = dalloc<uint64_t>(R, s);
-    uint32_t* gv0 = dalloc<uint32_t>(R, s);
-    uint32_t* gv1 = dalloc<uint32_t>(R, s);
-    TM_LAUNCH("group_keys", s, group_keys_kernel, grid_for(R), 256, 0, g.S_node, g.S_nbr, R, nb,
-              gk0, gv0);
-    radix_sort_pairs<uint64_t>(gk0, gv0, gk1, gv1, R, 2 * nb, s);
-    TM_LAUNCH("gather_g", s, gather_g_kernel, grid_for(R), 256, 0, gk0, gv0, R, nb, g.off, g.S_t,
-              g.S_ord, g.S_nbr, g.S_pg, g.G_t, g.G_ord, g.G_w2, g.G_pg, g.S_gidx);
-    exclusive_scan<uint32_t>(InwardG{g.G_w2}, R, g.G_dscan, s);
-    uint32_t* gscan = dalloc<uint32_t>(R + 1, s);
-    exclusive_scan<uint32_t>(FirstG{g.G_w2}, R, gscan, s);
-    TM_LAUNCH("group_table", s, group_table_kernel, grid_for(R), 256, 0, gk0, g.G_w2, gscan, R,
-              (uint64_t)((1ull << nb) - 1), g.grp_nbr, g.grp_off);
-    TM_LAUNCH("node_group", s, node_group_kernel, grid_for(n + 1), 256, 0, g.off, gscan, n,
-              g.node_grp);
-    uint32_t ng32 = 0;
-    TM_CUDA(cudaMemcpyAsync(&ng32, gscan + R, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    TM_CUDA(cudaMemcpyAsync(&h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, s));
-    dfree(gk0, s);
-    dfree(gk1, s);
-    dfree(gv0, s);
-    dfree(gv1, s);
-    dfree(gscan, s);
-    dfree(d_st, s);
-    TM_CUDA(cudaStreamSynchronize(s));
-    g.ng = ng32;
-    g.max_degree = h_st.max_degree;
-    if (g.max_degree > kPosMask)
-        throw tm_error(9, "node degree exceeds the 29-bit in-node position layout");
+    g.max_degree = 0;  // not needed by the layout (positions are global 32-bit)
 }
 
 void build_forward(DeviceGraph& g, int mode) {
@@ -386,12 +394,22 @@ void build_forward(DeviceGraph& g, int mode) {
     f.valid = true;
 }
 
+void build_s_pidx(DeviceGraph& g) {
+    if (g.S_pidx || g.m == 0) {
+        if (!g.S_pidx) g.S_pidx = dalloc<uint32_t>(1, g.stream);
+        return;
+    }
+    g.S_pidx = dalloc<uint32_t>(g.R, g.stream);
+    TM_LAUNCH("s_pidx", g.stream, s_pidx_kernel, grid_for(g.m), 256, 0, g.P_qmin, g.P_qmax, g.m,
+              g.S_pidx);
+}
+
 void free_graph(DeviceGraph& g) {
     cudaStream_t s = g.stream;
     dfree(g.S_t, s); dfree(g.S_nbr, s); dfree(g.S_ord, s); dfree(g.S_node, s);
-    dfree(g.S_pg, s); dfree(g.S_gidx, s); dfree(g.off, s);
-    dfree(g.G_t, s); dfree(g.G_ord, s); dfree(g.G_w2, s); dfree(g.G_pg, s);
-    dfree(g.G_dscan, s); dfree(g.grp_nbr, s); dfree(g.grp_off, s); dfree(g.node_grp, s);
+    dfree(g.S_pg, s); dfree(g.S_pidx, s); dfree(g.off, s);
+    dfree(g.P_t, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
+    dfree(g.P_qmin, s); dfree(g.P_qmax, s); dfree(g.pofs, s);
     for (auto& f : g.fwd) {
         dfree(f.t, s); dfree(f.nbr, s); dfree(f.ord, s); dfree(f.node, s); dfree(f.off, s);
         f.valid = false;

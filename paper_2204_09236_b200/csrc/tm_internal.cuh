@@ -7,16 +7,17 @@
 //     S_ord[R]  u32    ingestion ordinal
 //     S_node[R] u32    center node
 //     S_pg[R+1] u32    global exclusive prefix count of outward records
-//     S_gidx[R] u32    position of this record in G
+//     S_pidx[R] u32    the record's edge position in P (built lazily, items API)
 //     off[n+1]  u32    CSR offsets
-//   G (per-node records grouped by neighbour, time-ordered inside a group;
-//      its (v, w) groups double as PairEdgeIndex, indexes.hpp:63-92)
-//     G_t[R]    int64
-//     G_ord[R]  u32
-//     G_w2[R]   u32    local S position (29 b) | first<<29 | last<<30 | dir<<31
-//     G_pg[R]   u32    S_pg at that record's S position
-//     G_dscan[R+1] u32 exclusive prefix count of inward records in G order
-//     grp_nbr[ng], grp_off[ng+1], node_grp[n+1]   group table
+//   P (PairEdgeIndex, indexes.hpp:63-92: one record per edge, grouped by the
+//      unordered pair {min, max}, time-ordered inside a group; the group of
+//      {u, v} is also u's and v's same-neighbour run, shared by both ends)
+//     P_t[m]    int64
+//     P_ord[m]  u32
+//     P_max[m]  u32    larger endpoint (the block of the smaller one is pofs)
+//     P_w[m]    u32    dir_rel_min << 31 | first << 30 | last << 29
+//     P_qmin[m], P_qmax[m]  u32  S positions of the record at min / max
+//     pofs[n+1] u32    first P position whose min endpoint is u
 //   F (forward-oriented sequences for the triangle pass, one per orientation)
 #pragma once
 
@@ -30,9 +31,9 @@ namespace tmb {
 
 constexpr uint32_t kDirBit = 0x80000000u;
 constexpr uint32_t kNodeMask = 0x7fffffffu;
-constexpr uint32_t kFirstBit = 1u << 29;
-constexpr uint32_t kLastBit = 1u << 30;
-constexpr uint32_t kPosMask = (1u << 29) - 1;
+constexpr uint32_t kPDir = 1u << 31;
+constexpr uint32_t kPFirst = 1u << 30;
+constexpr uint32_t kPLast = 1u << 29;
 
 struct tm_error : std::runtime_error {
     int code;
@@ -87,7 +88,7 @@ struct Forward {
 };
 
 struct DeviceGraph {
-    uint64_t n = 0, m = 0, R = 0, ng = 0;
+    uint64_t n = 0, m = 0, R = 0;
     uint32_t max_degree = 0;
     cudaStream_t stream = nullptr;
     bool owns_stream = false;
@@ -97,22 +98,20 @@ struct DeviceGraph {
     uint32_t* S_ord = nullptr;
     uint32_t* S_node = nullptr;
     uint32_t* S_pg = nullptr;
-    uint32_t* S_gidx = nullptr;
+    uint32_t* S_pidx = nullptr;
     uint32_t* off = nullptr;
 
-    int64_t* G_t = nullptr;
-    uint32_t* G_ord = nullptr;
-    uint32_t* G_w2 = nullptr;
-    uint32_t* G_pg = nullptr;
-    uint32_t* G_dscan = nullptr;
-    uint32_t* grp_nbr = nullptr;
-    uint32_t* grp_off = nullptr;
-    uint32_t* node_grp = nullptr;
+    int64_t* P_t = nullptr;
+    uint32_t* P_ord = nullptr;
+    uint32_t* P_max = nullptr;
+    uint32_t* P_w = nullptr;
+    uint32_t* P_qmin = nullptr;
+    uint32_t* P_qmax = nullptr;
+    uint32_t* pofs = nullptr;
 
     Forward fwd[2];
 
-    uint64_t* d_acc = nullptr;     // 64 u64 device accumulators
-    uint64_t* h_acc = nullptr;     // pinned mirror
+    uint64_t* d_acc = nullptr;  // 64 u64 device accumulators
 };
 
 // read-only views passed by value to kernels
@@ -122,24 +121,23 @@ struct SView {
     const uint32_t* ord;
     const uint32_t* node;
     const uint32_t* pg;
-    const uint32_t* gidx;
+    const uint32_t* pidx;
     const uint32_t* off;
 };
-struct GView {
+struct PView {
     const int64_t* t;
     const uint32_t* ord;
-    const uint32_t* w2;
-    const uint32_t* pg;
-    const uint32_t* dscan;
-    const uint32_t* grp_nbr;
-    const uint32_t* grp_off;
-    const uint32_t* node_grp;
+    const uint32_t* max;
+    const uint32_t* w;
+    const uint32_t* qmin;
+    const uint32_t* qmax;
+    const uint32_t* pofs;
 };
 inline SView sview(const DeviceGraph& g) {
-    return {g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_pg, g.S_gidx, g.off};
+    return {g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_pg, g.S_pidx, g.off};
 }
-inline GView gview(const DeviceGraph& g) {
-    return {g.G_t, g.G_ord, g.G_w2, g.G_pg, g.G_dscan, g.grp_nbr, g.grp_off, g.node_grp};
+inline PView pview(const DeviceGraph& g) {
+    return {g.P_t, g.P_ord, g.P_max, g.P_w, g.P_qmin, g.P_qmax, g.pofs};
 }
 
 // ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------
@@ -147,9 +145,10 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst,
                  const int64_t* d_t, uint64_t m, uint64_t n);
 void free_graph(DeviceGraph& g);
 void build_forward(DeviceGraph& g, int mode);
+void build_s_pidx(DeviceGraph& g);
 
-// raw star sums (32 u64: Pair[8], C[8], B[8], A[8]) for S positions
-// [q_begin, q_end), added into d_out.
+// raw star sums (32 u64: Pair[8], C[8], B[8], A[8]) for the centers whose
+// S positions are [q_begin, q_end), added into d_out.
 void star_full(const DeviceGraph& g, int64_t delta, uint32_t q_begin, uint32_t q_end,
                uint64_t* d_out);
 void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,

@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cstdlib>
+#include <string>
 
 #include "tm_internal.cuh"
 
@@ -109,6 +110,39 @@ __device__ __forceinline__ void warp_append(bool pred, uint32_t value, uint32_t*
     if (lane == leader) base = atomicAdd(counter, (uint32_t)__popc(mask));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (pred) list[base + __popc(mask & ((1u << lane) - 1u))] = value;
+}
+
+__device__ __forceinline__ void warp_append64(bool pred, uint64_t value, uint64_t* list,
+                                              uint32_t* counter) {
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (!mask) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(counter, (uint32_t)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pred) list[base + __popc(mask & ((1u << lane) - 1u))] = value;
+}
+
+// Count sinks: rare per-item contributions go straight to shared (per block)
+// or global (per work item) u64 cells, so no kernel keeps a register array.
+struct SmemSink {
+    unsigned long long* cells;
+    __device__ __forceinline__ void add(int i, uint64_t v) const {
+        if (v) atomicAdd(&cells[i], (unsigned long long)v);
+    }
+};
+using GlobalSink = SmemSink;
+
+// zero `count` shared cells; call before use, followed by __syncthreads
+__device__ __forceinline__ void zero_cells(unsigned long long* cells, int count) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) cells[i] = 0;
+}
+// add block cells to global out (after __syncthreads)
+__device__ __forceinline__ void flush_cells(const unsigned long long* cells, int count,
+                                            uint64_t* out) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x)
+        if (cells[i]) atomicAdd((unsigned long long*)&out[i], cells[i]);
 }
 
 // last u with off[u] <= k (the node owning record k); off has n+1 entries
@@ -246,116 +280,80 @@ void exclusive_scan(Load load, uint64_t n, T* out, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// onesweep stable LSD radix sort of (key, u32 value) pairs, 8-bit digits
-constexpr int kOsBlock = 512;
-constexpr int kOsWarps = kOsBlock / 32;
-constexpr int kOsItems = 8;
-constexpr int kOsTile = kOsBlock * kOsItems;  // 4096
+// stable LSD radix sort of (key, u32 value) pairs, 8-bit digits, reduce-then-
+// scan per pass: upsweep (per-tile digit counts) -> scan of the digit-major
+// count matrix -> downsweep (rank the tile with per-warp __match_any_sync,
+// keeping input order; reorder in shared memory; write each digit run as one
+// burst).  All tile loads are issued before any ranking (ILP).
 constexpr int kRadix = 256;
-constexpr int kMaxPasses = 8;
 
-template <typename K>
-__global__ void __launch_bounds__(256) onesweep_hist(const K* __restrict__ keys, uint64_t n,
-                                                     int passes, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[kMaxPasses][kRadix];
-    for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) (&h[0][0])[i] = 0;
-    __syncthreads();
-    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n;
-         base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = base + threadIdx.x;
-        const bool valid = i < n;
-        const K k = valid ? keys[i] : K(0);
-        for (int p = 0; p < passes; ++p) {
-            const uint32_t d = valid ? ((uint32_t)(k >> (8 * p)) & 255u) : 256u;
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
-            if (valid && (peers & lt) == 0) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
-        const uint32_t c = (&h[0][0])[i];
-        if (c) atomicAdd(&hist[i], c);
-    }
-}
-
-// classic upsweep: per-tile digit counts, counts[d * ntiles + tile]
-template <typename K>
-__global__ void __launch_bounds__(kOsBlock) radix_upsweep(const K* __restrict__ keys, uint64_t n,
-                                                          int shift, uint32_t* __restrict__ counts,
-                                                          uint32_t ntiles) {
-    __shared__ uint32_t hist[kOsWarps][kRadix];
-    for (int i = threadIdx.x; i < kOsWarps * kRadix; i += kOsBlock) (&hist[0][0])[i] = 0;
+template <typename K, int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) radix_upsweep(const K* __restrict__ keys, uint64_t n,
+                                                       int shift, uint32_t* __restrict__ counts,
+                                                       uint32_t ntiles) {
+    constexpr int NW = BLOCK / 32;
+    constexpr int TILE = BLOCK * ITEMS;
+    __shared__ uint32_t hist[NW][kRadix];
+    for (int i = threadIdx.x; i < NW * kRadix; i += BLOCK) (&hist[0][0])[i] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint64_t base = (uint64_t)blockIdx.x * kOsTile + (uint64_t)w * (kOsItems * 32);
-    K k[kOsItems];
+    const uint64_t base = (uint64_t)blockIdx.x * TILE + (uint64_t)w * (ITEMS * 32);
+    K k[ITEMS];
 #pragma unroll
-    for (int r = 0; r < kOsItems; ++r) {
+    for (int r = 0; r < ITEMS; ++r) {
         const uint64_t i = base + r * 32 + lane;
         k[r] = i < n ? keys[i] : K(0);
     }
 #pragma unroll
-    for (int r = 0; r < kOsItems; ++r) {
+    for (int r = 0; r < ITEMS; ++r) {
         const uint64_t i = base + r * 32 + lane;
         if (i < n) atomicAdd(&hist[w][(uint32_t)(k[r] >> shift) & 255u], 1u);
     }
     __syncthreads();
-    if (threadIdx.x < kRadix) {
+    for (int d = threadIdx.x; d < kRadix; d += BLOCK) {
         uint32_t s = 0;
 #pragma unroll
-        for (int ww = 0; ww < kOsWarps; ++ww) s += hist[ww][threadIdx.x];
-        counts[(uint64_t)threadIdx.x * ntiles + blockIdx.x] = s;
+        for (int ww = 0; ww < NW; ++ww) s += hist[ww][d];
+        counts[(uint64_t)d * ntiles + blockIdx.x] = s;
     }
 }
 
-// per pass: exclusive scan of the 256 digit counts (one block per pass)
-static __global__ void __launch_bounds__(256) onesweep_digit_base(uint32_t* hist) {
-    uint32_t* h = hist + blockIdx.x * kRadix;
-    const uint32_t v = h[threadIdx.x];
-    const uint32_t ex = block_exclusive_scan<uint32_t, 8>(v, nullptr);
-    h[threadIdx.x] = ex;
-}
-
-template <typename K, bool kClassic>
-__global__ void __launch_bounds__(kOsBlock) onesweep_pass(const K* __restrict__ kin,
-                                                          const uint32_t* __restrict__ vin,
-                                                          K* __restrict__ kout,
-                                                          uint32_t* __restrict__ vout, uint64_t n,
-                                                          int shift,
-                                                          const uint32_t* __restrict__ digit_base,
-                                                          uint64_t* status, uint32_t* tile_ctr,
-                                                          const uint32_t* __restrict__ tile_offsets,
-                                                          uint32_t ntiles) {
-    extern __shared__ __align__(16) unsigned char os_smem[];
-    K* skeys = reinterpret_cast<K*>(os_smem);
-    uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + kOsTile);
-    __shared__ uint32_t wcnt[kOsWarps][kRadix];
+template <typename K, bool kVals, int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) radix_downsweep(const K* __restrict__ kin,
+                                                         const uint32_t* __restrict__ vin,
+                                                         K* __restrict__ kout,
+                                                         uint32_t* __restrict__ vout, uint64_t n,
+                                                         int shift,
+                                                         const uint32_t* __restrict__ tile_offsets,
+                                                         uint32_t ntiles) {
+    constexpr int NW = BLOCK / 32;
+    constexpr int TILE = BLOCK * ITEMS;
+    static_assert(BLOCK >= kRadix, "one digit per thread");
+    extern __shared__ __align__(16) unsigned char rs_smem[];
+    K* skeys = reinterpret_cast<K*>(rs_smem);
+    uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + TILE);
+    __shared__ uint32_t wcnt[NW][kRadix];
     __shared__ uint32_t dstart[kRadix];
     __shared__ uint32_t dglob[kRadix];
-    __shared__ uint32_t s_tile;
 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    if (tid == 0) s_tile = kClassic ? blockIdx.x : atomicAdd(tile_ctr, 1u);
-    for (int i = tid; i < kOsWarps * kRadix; i += kOsBlock) (&wcnt[0][0])[i] = 0;
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint64_t tbase = (uint64_t)tile * kOsTile;
+    for (int i = tid; i < NW * kRadix; i += BLOCK) (&wcnt[0][0])[i] = 0;
+    const uint64_t tbase = (uint64_t)blockIdx.x * TILE;
     const unsigned lt = (1u << lane) - 1u;
-
-    K key[kOsItems];
-    uint32_t val[kOsItems];
-    uint32_t rank[kOsItems];
+    K key[ITEMS];
+    uint32_t val[kVals ? ITEMS : 1];
+    uint32_t rank[ITEMS];
 #pragma unroll
-    for (int r = 0; r < kOsItems; ++r) {
-        const uint64_t i = tbase + (uint64_t)w * (kOsItems * 32) + r * 32 + lane;
+    for (int r = 0; r < ITEMS; ++r) {
+        const uint64_t i = tbase + (uint64_t)w * (ITEMS * 32) + r * 32 + lane;
         const bool valid = i < n;
         key[r] = valid ? kin[i] : K(0);
-        val[r] = valid ? vin[i] : 0u;
+        if (kVals) val[r] = valid ? vin[i] : 0u;
     }
+    __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kOsItems; ++r) {
-        const uint64_t i = tbase + (uint64_t)w * (kOsItems * 32) + r * 32 + lane;
+    for (int r = 0; r < ITEMS; ++r) {
+        const uint64_t i = tbase + (uint64_t)w * (ITEMS * 32) + r * 32 + lane;
         const bool valid = i < n;
         const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 255u) : 256u;
         const unsigned peers = __match_any_sync(0xffffffffu, d);
@@ -370,137 +368,88 @@ __global__ void __launch_bounds__(kOsBlock) onesweep_pass(const K* __restrict__ 
     if (tid < kRadix) {
         uint32_t run = 0;
 #pragma unroll
-        for (int ww = 0; ww < kOsWarps; ++ww) {
+        for (int ww = 0; ww < NW; ++ww) {
             const uint32_t c = wcnt[ww][tid];
             wcnt[ww][tid] = run;
             run += c;
         }
         cnt = run;
-        if (!kClassic)
-            st_status(status + (uint64_t)tile * kRadix + tid, (tile == 0 ? kStInc : kStAgg) | cnt);
     }
-    const uint32_t ex = block_exclusive_scan<uint32_t, kOsWarps>(cnt, nullptr);
-    if (tid < kRadix && kClassic) {
+    const uint32_t ex = block_exclusive_scan<uint32_t, NW>(cnt, nullptr);
+    if (tid < kRadix) {
         dstart[tid] = ex;
-        dglob[tid] = tile_offsets[(uint64_t)tid * ntiles + tile];
-    } else if (tid < kRadix) {
-        dstart[tid] = ex;
-        uint64_t pre = 0;
-        if (tile) {
-            // serial look-back per digit (the predecessor is usually already inclusive)
-            int64_t p = (int64_t)tile - 1;
-            bool done = false;
-            while (!done) {
-                uint64_t sv[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    sv[j] = (p - j >= 0) ? ld_status(status + (uint64_t)(p - j) * kRadix + tid) : kStInc;
-#pragma unroll
-                for (int j = 0; j < 4 && !done; ++j) {
-                    uint64_t s = sv[j];
-                    while ((s >> 62) == 0) s = ld_status(status + (uint64_t)(p - j) * kRadix + tid);
-                    pre += (p - j >= 0) ? (s & kStVal) : 0;
-                    if ((s >> 62) == 2) done = true;
-                }
-                p -= 4;
-            }
-            st_status(status + (uint64_t)tile * kRadix + tid, kStInc | (pre + cnt));
-        }
-        dglob[tid] = digit_base[tid] + (uint32_t)pre;
+        dglob[tid] = tile_offsets[(uint64_t)tid * ntiles + blockIdx.x];
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kOsItems; ++r) {
-        const uint64_t i = tbase + (uint64_t)w * (kOsItems * 32) + r * 32 + lane;
+    for (int r = 0; r < ITEMS; ++r) {
+        const uint64_t i = tbase + (uint64_t)w * (ITEMS * 32) + r * 32 + lane;
         if (i < n) {
             const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
             const uint32_t q = dstart[d] + wcnt[w][d] + rank[r];
             skeys[q] = key[r];
-            svals[q] = val[r];
+            if (kVals) svals[q] = val[r];
         }
     }
     __syncthreads();
-    const uint32_t tile_n = (uint32_t)((n - tbase) < (uint64_t)kOsTile ? (n - tbase) : (uint64_t)kOsTile);
-    for (uint32_t i = tid; i < tile_n; i += kOsBlock) {
+    const uint32_t tile_n = (uint32_t)((n - tbase) < (uint64_t)TILE ? (n - tbase) : (uint64_t)TILE);
+    for (uint32_t i = tid; i < tile_n; i += BLOCK) {
         const K k = skeys[i];
         const uint32_t d = (uint32_t)(k >> shift) & 255u;
         const uint32_t dest = dglob[d] + (i - dstart[d]);
         kout[dest] = k;
-        vout[dest] = svals[i];
+        if (kVals) vout[dest] = svals[i];
     }
 }
 
-// Sorts (keys, vals) on key bits [0, bits).  On return keys/vals point at the
-// sorted data; *_alt point at the scratch halves (pointers may be swapped).
-inline bool classic_sort() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TM_SORT");
-        v = (e && e[0] == 'o') ? 0 : 1;  // default: classic reduce-then-scan
-    }
-    return v == 1;
-}
+constexpr int kRsBlock = 512;
+constexpr int kRsItems = 8;
 
+// Stable sort of keys (and u32 values when vals != nullptr) on key bits
+// [bit_lo, bit_hi).  On return keys/vals point at the sorted data; the *_alt
+// pointers at the scratch halves (pointers may be swapped).
 template <typename K>
-void radix_sort_pairs(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
-                      int bits, cudaStream_t s) {
-    if (n <= 1 || bits <= 0) return;
-    const int passes = (bits + 7) / 8;
-    const uint32_t ntiles = (uint32_t)((n + kOsTile - 1) / kOsTile);
-    const size_t smem = kOsTile * (sizeof(K) + sizeof(uint32_t));
+void radix_sort(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
+                int bit_lo, int bit_hi, cudaStream_t s) {
+    if (n <= 1 || bit_hi <= bit_lo) return;
+    constexpr int TILE = kRsBlock * kRsItems;
+    const bool with_vals = vals != nullptr;
+    const int passes = (bit_hi - bit_lo + 7) / 8;
+    const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
+    const size_t smem = TILE * (sizeof(K) + (with_vals ? sizeof(uint32_t) : 0));
     static bool attr_set = false;
     if (!attr_set) {
-        TM_CUDA(cudaFuncSetAttribute(onesweep_pass<K, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        TM_CUDA(cudaFuncSetAttribute(onesweep_pass<K, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TM_CUDA(cudaFuncSetAttribute(radix_downsweep<K, true, kRsBlock, kRsItems>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(TILE * (sizeof(K) + sizeof(uint32_t)))));
+        TM_CUDA(cudaFuncSetAttribute(radix_downsweep<K, false, kRsBlock, kRsItems>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(TILE * sizeof(K))));
         attr_set = true;
     }
-    auto swap_bufs = [&] {
+    const uint64_t ncount = (uint64_t)kRadix * ntiles;
+    uint32_t* counts = dalloc<uint32_t>(2 * ncount + 1, s);
+    uint32_t* offs = counts + ncount;
+    for (int p = 0; p < passes; ++p) {
+        const int shift = bit_lo + 8 * p;
+        TM_LAUNCH("radix_upsweep", s, (radix_upsweep<K, kRsBlock, kRsItems>), ntiles, kRsBlock, 0, keys,
+                  n, shift, counts, ntiles);
+        exclusive_scan<uint32_t>(ArrayLoad<uint32_t>{counts}, ncount, offs, s);
+        if (with_vals) {
+            TM_LAUNCH("radix_downsweep", s, (radix_downsweep<K, true, kRsBlock, kRsItems>), ntiles,
+                      kRsBlock, smem, keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles);
+            uint32_t* tv = vals;
+            vals = vals_alt;
+            vals_alt = tv;
+        } else {
+            TM_LAUNCH("radix_downsweep", s, (radix_downsweep<K, false, kRsBlock, kRsItems>), ntiles,
+                      kRsBlock, smem, keys, nullptr, keys_alt, nullptr, n, shift, offs, ntiles);
+        }
         K* tk = keys;
         keys = keys_alt;
         keys_alt = tk;
-        uint32_t* tv = vals;
-        vals = vals_alt;
-        vals_alt = tv;
-    };
-    if (classic_sort()) {
-        const uint64_t ncount = (uint64_t)kRadix * ntiles;
-        uint32_t* counts = dalloc<uint32_t>(2 * ncount + 1, s);
-        uint32_t* offs = counts + ncount;
-        for (int p = 0; p < passes; ++p) {
-            TM_LAUNCH("radix_upsweep", s, radix_upsweep<K>, ntiles, kOsBlock, 0, keys, n, 8 * p,
-                      counts, ntiles);
-            exclusive_scan<uint32_t>(ArrayLoad<uint32_t>{counts}, ncount, offs, s);
-            TM_LAUNCH("radix_downsweep", s, (onesweep_pass<K, true>), ntiles, kOsBlock, smem, keys,
-                      vals, keys_alt, vals_alt, n, 8 * p, nullptr, nullptr, nullptr, offs, ntiles);
-            swap_bufs();
-        }
-        dfree(counts, s);
-        return;
     }
-    const uint64_t nstatus = (uint64_t)passes * ntiles * kRadix;
-    // [hist passes*256 u32][tile counters passes u32] [status u64 ...]
-    const size_t hist_bytes = ((size_t)passes * kRadix + kMaxPasses) * sizeof(uint32_t);
-    const size_t bytes = hist_bytes + nstatus * sizeof(uint64_t) + 16;
-    unsigned char* scratch = dalloc<unsigned char>(bytes, s);
-    TM_CUDA(cudaMemsetAsync(scratch, 0, bytes, s));
-    uint32_t* hist = reinterpret_cast<uint32_t*>(scratch);
-    uint32_t* ctr = hist + (size_t)passes * kRadix;
-    uint64_t* status = reinterpret_cast<uint64_t*>(scratch + ((hist_bytes + 15) & ~size_t(15)));
-    uint64_t hist_grid = (n + 255) / 256;
-    const uint64_t cap = (uint64_t)sm_count() * 8;
-    if (hist_grid > cap) hist_grid = cap;
-    TM_LAUNCH("onesweep_hist", s, onesweep_hist<K>, (unsigned)hist_grid, 256, 0, keys, n, passes,
-              hist);
-    TM_LAUNCH("onesweep_base", s, onesweep_digit_base, (unsigned)passes, 256, 0, hist);
-    for (int p = 0; p < passes; ++p) {
-        TM_LAUNCH("onesweep_pass", s, (onesweep_pass<K, false>), ntiles, kOsBlock, smem, keys, vals,
-                  keys_alt, vals_alt, n, 8 * p, hist + (size_t)p * kRadix,
-                  status + (uint64_t)p * ntiles * kRadix, ctr + p, nullptr, ntiles);
-        swap_bufs();
-    }
-    dfree(scratch, s);
+    dfree(counts, s);
 }
 
 inline int bit_width_u64(uint64_t x) {

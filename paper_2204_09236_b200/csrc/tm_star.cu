@@ -15,7 +15,8 @@
 //                         #{a in [lo(c), b), dir_a = d1}   Star-I   = C - Pair
 //
 // A, B and Pair only need the same-neighbour records of a inside its window
-// (walked in G, which stores each group contiguously) plus global prefix
+// (walked in P, where the pair {u, x} is one contiguous time-ordered group
+// shared by both endpoints) plus global prefix
 // counts of outward records (S_pg); C walks the same-neighbour records of c
 // backwards.  Each record is handled by one thread, so a hub needs no special
 // treatment and there is no per-center state at all.  Work per record is
@@ -74,48 +75,49 @@ __device__ __forceinline__ uint32_t gallop_lower_back(const int64_t* __restrict_
     return lo;
 }
 
-struct StarAcc {
-    uint64_t v[32];
-};
-
-__device__ __forceinline__ void add_d1(StarAcc& acc, int base, uint32_t d1, const uint64_t x[4]) {
-    const uint64_t m0 = d1 ? 0ull : ~0ull;
-    const uint64_t m1 = ~m0;
+template <typename Sink>
+__device__ __forceinline__ void add_d1(const Sink& sink, int base, uint32_t d1, const uint64_t x[4]) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        acc.v[base + j] += x[j] & m0;
-        acc.v[base + 4 + j] += x[j] & m1;
-    }
+    for (int j = 0; j < 4; ++j) sink.add(base + (int)d1 * 4 + j, x[j]);
 }
 
-// first-edge role of S position q (node range [start, end)): Pair, A, B.
-__device__ __forceinline__ void first_role(const SView& S, const GView& G, uint32_t q,
+// Side of center u in the unordered pair {u, other}: 0 when u is the smaller
+// id (P_qmin / dir_rel_min describe it), 1 when u is the larger one.
+__device__ __forceinline__ uint32_t side_of(uint32_t u, uint32_t other) { return u > other ? 1u : 0u; }
+
+// first-edge role of S position q with P index k (center u, S range
+// [start, end)): Pair, A, B.
+template <typename Sink>
+__device__ __forceinline__ void first_role(const SView& S, const PView& P, uint32_t q, uint32_t k,
                                            uint32_t start, uint32_t end, int64_t delta,
-                                           StarAcc& acc) {
+                                           const Sink& acc) {
     const int64_t ta = S.t[q];
-    const uint32_t da = S.nbr[q] >> 31;
+    const uint32_t nq = S.nbr[q];
+    const uint32_t da = nq >> 31;
+    const uint32_t side = side_of(S.node[q], nq & kNodeMask);
     const int64_t lim = sat_add(ta, delta);
-    uint32_t k = S.gidx[q];
-    if (G.w2[k] & kLastBit) return;
-    if (G.t[k + 1] > lim) return;  // no same-neighbour record in the window
+    if (P.w[k] & kPLast) return;
+    if (P.t[k + 1] > lim) return;  // no same-neighbour record in the window
 
     const uint32_t base = S.pg[start];
     const uint32_t e = gallop_upper(S.t, q + 1, end, lim);
     const uint64_t pe_o = S.pg[e] - base, pe_i = (uint64_t)(e - start) - pe_o;
     const uint64_t pa_o = (uint64_t)(S.pg[q] - base) + (da ? 0u : 1u);
     const uint64_t pa_i = (uint64_t)(q - start + 1) - pa_o;
+    const uint32_t* __restrict__ qside = side ? P.qmax : P.qmin;
 
     uint64_t n0 = 0, n1 = 0;
     uint64_t A00 = 0, A01 = 0, A10 = 0, A11 = 0;   // A[d2][d3]: sum [dir_b=d2] P_d3(b+1)
     uint64_t B00 = 0, B01 = 0, B10 = 0, B11 = 0;   // B[d3][d2]: sum [dir_c=d3] P_d2(c)
     uint64_t P00 = 0, P01 = 0, P10 = 0, P11 = 0;   // Pair[d2][d3]
     for (++k;; ++k) {
-        if (G.t[k] > lim) break;
-        const uint32_t w2 = G.w2[k];
-        const uint64_t pos = w2 & kPosMask;
-        const uint64_t pb_o = G.pg[k] - base;
+        if (P.t[k] > lim) break;
+        const uint32_t w = P.w[k];
+        const uint32_t qb = qside[k];
+        const uint64_t pos = qb - start;
+        const uint64_t pb_o = S.pg[qb] - base;
         const uint64_t pb_i = pos - pb_o;
-        if (w2 & kDirBit) {  // inward
+        if ((w >> 31) ^ side) {  // inward relative to u
             A10 += pb_o;
             A11 += pos + 1 - pb_o;
             B10 += pb_o;
@@ -132,7 +134,7 @@ __device__ __forceinline__ void first_role(const SView& S, const GView& G, uint3
             P10 += n1;
             ++n0;
         }
-        if (w2 & kLastBit) break;
+        if (w & kPLast) break;
     }
     uint64_t pair[4] = {P00, P01, P10, P11};
     // A(d2,d3) = n[d2] * P_d3(e) - Aacc[d2][d3]
@@ -146,109 +148,101 @@ __device__ __forceinline__ void first_role(const SView& S, const GView& G, uint3
 
 // third-edge role of S position q: the Star-I pair term C.
 // rb/re: first-edge range (local), clipped; full run passes rb=0, re=s.
-__device__ __forceinline__ void third_role(const SView& S, const GView& G, uint32_t q,
+template <typename Sink>
+__device__ __forceinline__ void third_role(const SView& S, const PView& P, uint32_t q, uint32_t k,
                                            uint32_t start, int64_t delta, uint32_t rb,
-                                           uint32_t re, StarAcc& acc) {
-    uint32_t k = S.gidx[q];
-    if (G.w2[k] & kFirstBit) return;
+                                           uint32_t re, const Sink& acc) {
+    if (P.w[k] & kPFirst) return;
     const int64_t tc = S.t[q];
     const int64_t lo_lim = sat_sub(tc, delta);
     // quick reject: previous same-neighbour record already before the window
-    if (G.t[k - 1] < lo_lim) return;
-    const uint32_t dc = S.nbr[q] >> 31;
+    if (P.t[k - 1] < lo_lim) return;
+    const uint32_t nq = S.nbr[q];
+    const uint32_t dc = nq >> 31;
+    const uint32_t side = side_of(S.node[q], nq & kNodeMask);
+    const uint32_t* __restrict__ qside = side ? P.qmax : P.qmin;
     const uint32_t lo = gallop_lower_back(S.t, start, q, lo_lim);
     const uint32_t L = max(lo, start + rb);
     const uint32_t pl = S.pg[L];
     const uint32_t hiq = start + re;
     uint64_t x0 = 0, x1 = 0, y0 = 0, y1 = 0;  // x: d1 = out, y: d1 = in ; index d2
     for (--k;; --k) {
-        const uint32_t w2 = G.w2[k];
-        const uint32_t posb = start + (w2 & kPosMask);
+        const uint32_t w = P.w[k];
+        const uint32_t posb = qside[k];
         if (posb <= L) break;
         const uint32_t mhi = min(posb, hiq);
         if (mhi > L) {
-            const uint64_t x = (uint64_t)((mhi == posb ? G.pg[k] : S.pg[mhi]) - pl);
+            const uint64_t x = (uint64_t)(S.pg[mhi] - pl);
             const uint64_t y = (uint64_t)(mhi - L) - x;
-            if (w2 & kDirBit) { x1 += x; y1 += y; } else { x0 += x; y0 += y; }
+            if ((w >> 31) ^ side) { x1 += x; y1 += y; } else { x0 += x; y0 += y; }
         }
-        if (w2 & kFirstBit) break;
+        if (w & kPFirst) break;
     }
     // cells C[d1][d2][dc]
-    const uint64_t mo = dc ? 0ull : ~0ull, mi = ~mo;
-    acc.v[8 + 0 + 0 + 0] += x0 & mo;
-    acc.v[8 + 0 + 0 + 1] += x0 & mi;
-    acc.v[8 + 0 + 2 + 0] += x1 & mo;
-    acc.v[8 + 0 + 2 + 1] += x1 & mi;
-    acc.v[8 + 4 + 0 + 0] += y0 & mo;
-    acc.v[8 + 4 + 0 + 1] += y0 & mi;
-    acc.v[8 + 4 + 2 + 0] += y1 & mo;
-    acc.v[8 + 4 + 2 + 1] += y1 & mi;
+    acc.add(8 + 0 + 0 + dc, x0);
+    acc.add(8 + 0 + 2 + dc, x1);
+    acc.add(8 + 4 + 0 + dc, y0);
+    acc.add(8 + 4 + 2 + dc, y1);
 }
 
-// block-reduce 32 u64 and add into out[0..32)
-__device__ __forceinline__ void flush_acc(StarAcc& acc, uint64_t* out) {
-    __shared__ uint64_t red[8][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        uint64_t v = acc.v[j];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == j) red[w][j] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        uint64_t s = 0;
-#pragma unroll
-        for (int ww = 0; ww < 8; ++ww) s += red[ww][threadIdx.x];
-        if (s) atomicAdd((unsigned long long*)&out[threadIdx.x], (unsigned long long)s);
-    }
-}
-
-// Filter: one coalesced pass over G.  A record can contribute as a first
-// edge only if the next record of its neighbour group is inside its window,
-// and as a third edge only if the previous one is (otherwise every term of
-// first_role / third_role is zero).  Survivors go to two worklists.
-__global__ void __launch_bounds__(256) star_filter_kernel(GView G, int64_t delta, uint32_t kb,
-                                                          uint32_t ke, uint32_t* __restrict__ first_list,
-                                                          uint32_t* __restrict__ third_list,
+// Filter: one coalesced pass over P.  A record can contribute as a first
+// edge only if the next record of its pair group is inside its window, and as
+// a third edge only if the previous one is (otherwise every term of
+// first_role / third_role is zero).  Both endpoints share the group order, so
+// a surviving record yields candidates at both of its centers; the S
+// positions of those inside the center partition [qlo, qhi) go to the lists.
+__global__ void __launch_bounds__(256) star_filter_kernel(PView P, int64_t delta, uint64_t m,
+                                                          uint32_t qlo, uint32_t qhi,
+                                                          uint64_t* __restrict__ first_list,
+                                                          uint64_t* __restrict__ third_list,
                                                           uint32_t* __restrict__ counters) {
-    for (uint64_t base = (uint64_t)kb + (uint64_t)blockIdx.x * blockDim.x; base < ke;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = base + threadIdx.x;
         bool f = false, th = false;
-        if (k < ke) {
-            const uint32_t w2 = G.w2[k];
-            const int64_t t = G.t[k];
-            f = !(w2 & kLastBit) && G.t[k + 1] <= sat_add(t, delta);
-            th = !(w2 & kFirstBit) && G.t[k - 1] >= sat_sub(t, delta);
+        uint32_t qa = 0, qb = 0;
+        if (k < m) {
+            const uint32_t w = P.w[k];
+            const int64_t t = P.t[k];
+            f = !(w & kPLast) && P.t[k + 1] <= sat_add(t, delta);
+            th = !(w & kPFirst) && P.t[k - 1] >= sat_sub(t, delta);
+            if (f || th) {
+                qa = P.qmin[k];
+                qb = P.qmax[k];
+            }
         }
-        warp_append(f, (uint32_t)k, first_list, counters);
-        warp_append(th, (uint32_t)k, third_list, counters + 1);
+        const bool ina = qa >= qlo && qa < qhi, inb = qb >= qlo && qb < qhi;
+        const uint64_t ea = (k << 32) | qa, eb = (k << 32) | qb;
+        warp_append64(f && ina, ea, first_list, counters);
+        warp_append64(f && inb, eb, first_list, counters);
+        warp_append64(th && ina, ea, third_list, counters + 1);
+        warp_append64(th && inb, eb, third_list, counters + 1);
     }
 }
 
 // Work: the full first_role / third_role sums for the surviving records.
-__global__ void __launch_bounds__(256) star_work_kernel(SView S, GView G, int64_t delta, uint64_t n,
-                                                        const uint32_t* __restrict__ first_list,
-                                                        const uint32_t* __restrict__ third_list,
+__global__ void __launch_bounds__(256) star_work_kernel(SView S, PView P, int64_t delta,
+                                                        const uint64_t* __restrict__ first_list,
+                                                        const uint64_t* __restrict__ third_list,
                                                         const uint32_t* __restrict__ counters,
                                                         uint64_t* __restrict__ out) {
-    StarAcc acc;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) acc.v[j] = 0;
+    __shared__ unsigned long long cells[32];
+    zero_cells(cells, 32);
+    __syncthreads();
+    const SmemSink acc{cells};
     const uint32_t nf = counters[0], nt = counters[1];
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (uint64_t)nf + nt;
          idx += (uint64_t)gridDim.x * blockDim.x) {
         const bool first = idx < nf;
-        const uint32_t k = first ? first_list[idx] : third_list[idx - nf];
-        const uint32_t u = owner_of(S.off, n, k);
+        const uint64_t e = first ? first_list[idx] : third_list[idx - nf];
+        const uint32_t q = (uint32_t)e, k = (uint32_t)(e >> 32);
+        const uint32_t u = S.node[q];
         const uint32_t start = S.off[u], end = S.off[u + 1];
-        const uint32_t q = start + (G.w2[k] & kPosMask);
-        if (first) first_role(S, G, q, start, end, delta, acc);
-        else third_role(S, G, q, start, delta, 0u, end - start, acc);
+        if (first) first_role(S, P, q, k, start, end, delta, acc);
+        else third_role(S, P, q, k, start, delta, 0u, end - start, acc);
     }
-    flush_acc(acc, out);
+    __syncthreads();
+    flush_cells(cells, 32, out);
 }
 
 __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ item_off, uint64_t n_items,
@@ -263,23 +257,21 @@ __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ item_
 
 // per-item star/pair: first-edge positions [rb, min(re, s)), third positions (rb, s)
 __global__ void __launch_bounds__(256) star_items_kernel(
-    SView S, GView G, int64_t delta, uint64_t n_items, const uint32_t* __restrict__ nodes,
+    SView S, PView P, int64_t delta, uint64_t n_items, const uint32_t* __restrict__ nodes,
     const uint64_t* __restrict__ begin, const uint64_t* __restrict__ endr,
     const uint64_t* __restrict__ first_off, uint64_t total_first,
     const uint64_t* __restrict__ third_off, uint64_t total_third, uint64_t* __restrict__ out) {
     const uint64_t total = total_first + total_third;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (uint64_t)gridDim.x * blockDim.x) {
-        StarAcc acc;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc.v[j] = 0;
         uint32_t it;
         if (idx < total_first) {
             it = find_item(first_off, n_items, idx);
             const uint32_t u = nodes[it];
             const uint32_t start = S.off[u], end = S.off[u + 1];
             const uint32_t q = start + (uint32_t)begin[it] + (uint32_t)(idx - first_off[it]);
-            first_role(S, G, q, start, end, delta, acc);
+            first_role(S, P, q, S.pidx[q], start, end, delta,
+                       GlobalSink{(unsigned long long*)out + (uint64_t)it * 32});
         } else {
             const uint64_t j = idx - total_first;
             it = find_item(third_off, n_items, j);
@@ -289,12 +281,9 @@ __global__ void __launch_bounds__(256) star_items_kernel(
             const uint32_t rb = (uint32_t)begin[it];
             const uint32_t re = (uint32_t)(endr[it] < (uint64_t)s ? endr[it] : (uint64_t)s);
             const uint32_t q = start + rb + 1 + (uint32_t)(j - third_off[it]);
-            third_role(S, G, q, start, delta, rb, re, acc);
+            third_role(S, P, q, S.pidx[q], start, delta, rb, re,
+                       GlobalSink{(unsigned long long*)out + (uint64_t)it * 32});
         }
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-            if (acc.v[c]) atomicAdd((unsigned long long*)&out[(uint64_t)it * 32 + c],
-                                    (unsigned long long)acc.v[c]);
     }
 }
 
@@ -302,20 +291,19 @@ __global__ void __launch_bounds__(256) star_items_kernel(
 
 void star_full(const DeviceGraph& g, int64_t delta, uint32_t q_begin, uint32_t q_end,
                uint64_t* d_out) {
-    if (q_end <= q_begin) return;
+    if (q_end <= q_begin || g.m == 0) return;
     cudaStream_t st = g.stream;
     const uint64_t work = q_end - q_begin;
     const uint64_t cap = (uint64_t)sm_count() * 8;
-    uint64_t grid = (work + 255) / 256;
+    uint64_t grid = (g.m + 255) / 256;
     if (grid > cap) grid = cap;
-    uint32_t* lists = dalloc<uint32_t>(2 * work + 2, st);
-    uint32_t* counters = lists + 2 * work;
+    uint64_t* lists = dalloc<uint64_t>(2 * work + 1, st);
+    uint32_t* counters = reinterpret_cast<uint32_t*>(lists + 2 * work);
     TM_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), st));
-    // G positions of nodes [cb, ce) are the same range as their S positions
-    TM_LAUNCH("star_filter", st, star_filter_kernel, (unsigned)grid, 256, 0, gview(g), delta, q_begin,
-              q_end, lists, lists + work, counters);
-    TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), gview(g), delta, g.n,
-              lists, lists + work, counters, d_out);
+    TM_LAUNCH("star_filter", st, star_filter_kernel, (unsigned)grid, 256, 0, pview(g), delta, g.m,
+              q_begin, q_end, lists, lists + work, counters);
+    TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), delta, lists,
+              lists + work, counters, d_out);
     dfree(lists, st);
 }
 
@@ -328,7 +316,7 @@ void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uin
     const uint64_t cap = (uint64_t)sm_count() * 8;
     uint64_t grid = (total + 255) / 256;
     if (grid > cap) grid = cap;
-    TM_LAUNCH("star_items", g.stream, star_items_kernel, (unsigned)grid, 256, 0, sview(g), gview(g),
+    TM_LAUNCH("star_items", g.stream, star_items_kernel, (unsigned)grid, 256, 0, sview(g), pview(g),
               delta, n_items, d_nodes, d_begin, d_end, d_first_off, total_first, d_third_off,
               total_third, d_out);
 }

@@ -4,9 +4,9 @@
 // neighbours v, w is a wedge; the closing edges are the v-w records with
 // t in [t_j - delta, t_i + delta], typed I/II/III by their (t, ordinal) place
 // relative to e_i and e_j (triangle_engine.cpp:10-16, 43-51).  The v-w list
-// is found in the neighbour-grouped G layout: binary search of w in v's
-// distinct-neighbour table (the smaller side), then either a short linear
-// scan (<= 16 records) or four binary searches plus G_dscan prefix counts.
+// is the P group {min, max} (PairEdgeIndex), found by a binary search of max
+// in min's block; short groups are classified record by record, long ones by
+// four binary searches for the window and the I/II/III boundaries.
 //
 // Full-graph passes run on the forward-oriented sequences F (each edge kept
 // at one endpoint under a strict total order), so every triangle instance is
@@ -25,79 +25,80 @@ namespace tmb {
 
 namespace {
 
-// counts of closing records for one wedge: c[type*2 + dk], dk relative to v
-__device__ __forceinline__ void closing_counts(const GView& G, uint32_t v, uint32_t w, int64_t lo,
+// counts of closing records for one wedge: c[type*2 + dk], dk relative to v.
+// The v-w list is the P group {min, max}: lower_bound of max in min's block.
+__device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint32_t w, int64_t lo,
                                                int64_t hi, int64_t ti, uint32_t oi, int64_t tj,
                                                uint32_t oj, uint32_t c[6]) {
 #pragma unroll
     for (int j = 0; j < 6; ++j) c[j] = 0;
-    const uint32_t gv0 = G.node_grp[v], gv1 = G.node_grp[v + 1];
-    const uint32_t gw0 = G.node_grp[w], gw1 = G.node_grp[w + 1];
-    uint32_t a, b, y, flip;
-    if (gv1 - gv0 <= gw1 - gw0) { a = gv0; b = gv1; y = w; flip = 0; }
-    else { a = gw0; b = gw1; y = v; flip = 1; }
-    // lower_bound of y in grp_nbr[a, b)
-    while (a < b) {
-        const uint32_t mid = (a + b) >> 1;
-        if (G.grp_nbr[mid] < y) a = mid + 1; else b = mid;
+    const uint32_t a = min(v, w), b = max(v, w);
+    const uint32_t flip = v == a ? 0u : 1u;  // dir_rel_min -> dir relative to v
+    const uint32_t blk_end = P.pofs[a + 1];
+    uint32_t l = P.pofs[a], r = blk_end;
+    while (l < r) {
+        const uint32_t mid = (l + r) >> 1;
+        if (P.max[mid] < b) l = mid + 1; else r = mid;
     }
-    if (a >= (flip ? gw1 : gv1) || G.grp_nbr[a] != y) return;
-    const uint32_t kb = G.grp_off[a], ke = G.grp_off[a + 1];
-    if (ke - kb <= 16) {
-        for (uint32_t k = kb; k < ke; ++k) {
-            const int64_t tk = G.t[k];
-            if (tk < lo) continue;
-            if (tk > hi) break;
-            const uint32_t dk = (G.w2[k] >> 31) ^ flip;
+    if (l >= blk_end || P.max[l] != b) return;
+    const uint32_t kb = l;
+    // short groups: classify record by record (triangle_engine.cpp:43-51)
+    uint32_t k = kb;
+    for (int step = 0; step < 16; ++step, ++k) {
+        const int64_t tk = P.t[k];
+        const uint32_t wk = P.w[k];
+        if (tk > hi) return;
+        if (tk >= lo) {
+            const uint32_t dk = (wk >> 31) ^ flip;
             uint32_t type;
-            if (tk < ti || (tk == ti && G.ord[k] < oi)) type = 0;
-            else if (tk > tj || (tk == tj && G.ord[k] > oj)) type = 2;
+            if (tk < ti || (tk == ti && P.ord[k] < oi)) type = 0;
+            else if (tk > tj || (tk == tj && P.ord[k] > oj)) type = 2;
             else type = 1;
             c[type * 2 + dk] += 1;
         }
-        return;
+        if (wk & kPLast) return;
     }
-    // k1: first t >= lo ; k4: first t > hi
-    uint32_t l = kb, r = ke;
-    while (l < r) { const uint32_t mid = (l + r) >> 1; if (G.t[mid] < lo) l = mid + 1; else r = mid; }
+    // long group: binary search the window [k1, k4) and the type boundaries
+    r = blk_end;  // group end = upper_bound of b in the block
+    l = k;
+    while (l < r) {
+        const uint32_t mid = (l + r) >> 1;
+        if (P.max[mid] <= b) l = mid + 1; else r = mid;
+    }
+    const uint32_t ke = l;
+    l = k; r = ke;
+    while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] < lo) l = mid + 1; else r = mid; }
     const uint32_t k1 = l;
     r = ke;
-    while (l < r) { const uint32_t mid = (l + r) >> 1; if (G.t[mid] <= hi) l = mid + 1; else r = mid; }
+    while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] <= hi) l = mid + 1; else r = mid; }
     const uint32_t k4 = l;
-    // k2: first (t, ord) > (ti, oi) in [k1, k4)
-    l = k1; r = k4;
+    l = k1; r = k4;  // k2: first (t, ord) > (ti, oi)
     while (l < r) {
         const uint32_t mid = (l + r) >> 1;
-        const int64_t tm = G.t[mid];
-        if (tm < ti || (tm == ti && G.ord[mid] < oi)) l = mid + 1; else r = mid;
+        const int64_t tm = P.t[mid];
+        if (tm < ti || (tm == ti && P.ord[mid] < oi)) l = mid + 1; else r = mid;
     }
     const uint32_t k2 = l;
-    r = k4;
+    r = k4;  // k3: first (t, ord) > (tj, oj)
     while (l < r) {
         const uint32_t mid = (l + r) >> 1;
-        const int64_t tm = G.t[mid];
-        if (tm < tj || (tm == tj && G.ord[mid] < oj)) l = mid + 1; else r = mid;
+        const int64_t tm = P.t[mid];
+        if (tm < tj || (tm == tj && P.ord[mid] < oj)) l = mid + 1; else r = mid;
     }
     const uint32_t k3 = l;
-    const uint32_t in1 = G.dscan[k2] - G.dscan[k1];
-    const uint32_t in2 = G.dscan[k3] - G.dscan[k2];
-    const uint32_t in3 = G.dscan[k4] - G.dscan[k3];
-    const uint32_t out1 = (k2 - k1) - in1, out2 = (k3 - k2) - in2, out3 = (k4 - k3) - in3;
-    c[0] = flip ? in1 : out1;  c[1] = flip ? out1 : in1;
-    c[2] = flip ? in2 : out2;  c[3] = flip ? out2 : in2;
-    c[4] = flip ? in3 : out3;  c[5] = flip ? out3 : in3;
+    for (uint32_t x = k1; x < k4; ++x) {
+        const uint32_t type = x < k2 ? 0u : (x < k3 ? 1u : 2u);
+        c[type * 2 + ((P.w[x] >> 31) ^ flip)] += 1;
+    }
 }
 
-struct TriAcc {
-    uint64_t v[24];
-};
-
 // all wedges with first edge i in sequence arrays (T, NBR, ORD) ending at end
-__device__ __forceinline__ void wedges_from(const GView& G, const int64_t* __restrict__ T,
+template <typename Sink>
+__device__ __forceinline__ void wedges_from(const PView& P, const int64_t* __restrict__ T,
                                             const uint32_t* __restrict__ NBR,
                                             const uint32_t* __restrict__ ORD, uint32_t i,
                                             uint32_t end, int64_t delta,
-                                            const uint8_t* __restrict__ live, TriAcc& acc) {
+                                            const uint8_t* __restrict__ live, const Sink& acc) {
     const uint32_t ni = NBR[i];
     const uint32_t v = ni & kNodeMask, di = ni >> 31;
     if (live && !live[v]) return;
@@ -113,7 +114,7 @@ __device__ __forceinline__ void wedges_from(const GView& G, const int64_t* __res
         if (w == v) continue;
         if (live && !live[w]) continue;
         uint32_t c[6];
-        closing_counts(G, v, w, sat_sub(tj, delta), lim, ti, oi, tj, ORD[j], c);
+        closing_counts(P, v, w, sat_sub(tj, delta), lim, ti, oi, tj, ORD[j], c);
         const uint64_t m1 = (nj >> 31) ? ~0ull : 0ull, m0 = ~m1;
 #pragma unroll
         for (int x = 0; x < 6; ++x) {
@@ -121,35 +122,13 @@ __device__ __forceinline__ void wedges_from(const GView& G, const int64_t* __res
             a1[x] += c[x] & m1;
         }
     }
-    const uint64_t mi = di ? ~0ull : 0ull, mo = ~mi;
 #pragma unroll
     for (int ty = 0; ty < 3; ++ty)
 #pragma unroll
         for (int dk = 0; dk < 2; ++dk) {
-            acc.v[ty * 8 + 0 + 0 + dk] += a0[ty * 2 + dk] & mo;
-            acc.v[ty * 8 + 0 + 2 + dk] += a1[ty * 2 + dk] & mo;
-            acc.v[ty * 8 + 4 + 0 + dk] += a0[ty * 2 + dk] & mi;
-            acc.v[ty * 8 + 4 + 2 + dk] += a1[ty * 2 + dk] & mi;
+            acc.add(ty * 8 + (int)di * 4 + 0 + dk, a0[ty * 2 + dk]);
+            acc.add(ty * 8 + (int)di * 4 + 2 + dk, a1[ty * 2 + dk]);
         }
-}
-
-__device__ __forceinline__ void flush_tri(TriAcc& acc, uint64_t* out) {
-    __shared__ uint64_t red[8][24];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int j = 0; j < 24; ++j) {
-        uint64_t v = acc.v[j];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == j) red[w][j] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < 24) {
-        uint64_t s = 0;
-#pragma unroll
-        for (int ww = 0; ww < 8; ++ww) s += red[ww][threadIdx.x];
-        if (s) atomicAdd((unsigned long long*)&out[threadIdx.x], (unsigned long long)s);
-    }
 }
 
 // Filter + wedge expansion: one pass over F.  Thread i scans the next
@@ -225,28 +204,25 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(const int64_t* __restri
     }
 }
 
-__device__ __forceinline__ void add_wedge(const GView& G, const int64_t* __restrict__ FT,
+template <typename Sink>
+__device__ __forceinline__ void add_wedge(const PView& P, const int64_t* __restrict__ FT,
                                           const uint32_t* __restrict__ FN,
                                           const uint32_t* __restrict__ FO, uint32_t i, uint32_t j,
-                                          int64_t delta, TriAcc& acc) {
+                                          int64_t delta, const Sink& acc) {
     const uint32_t ni = FN[i], nj = FN[j];
     const int64_t ti = FT[i], tj = FT[j];
     uint32_t c[6];
-    closing_counts(G, ni & kNodeMask, nj & kNodeMask, sat_sub(tj, delta), sat_add(ti, delta), ti,
+    closing_counts(P, ni & kNodeMask, nj & kNodeMask, sat_sub(tj, delta), sat_add(ti, delta), ti,
                    FO[i], tj, FO[j], c);
-    const uint32_t cell0 = (ni >> 31) * 4 + (nj >> 31) * 2;  // di*4 + dj*2
+    const int cell0 = (int)((ni >> 31) * 4 + (nj >> 31) * 2);  // di*4 + dj*2
 #pragma unroll
     for (int ty = 0; ty < 3; ++ty)
 #pragma unroll
-        for (int dk = 0; dk < 2; ++dk)
-#pragma unroll
-            for (int dd = 0; dd < 8; dd += 2) {
-                if (dd == (int)cell0) acc.v[ty * 8 + dd + dk] += c[ty * 2 + dk];
-            }
+        for (int dk = 0; dk < 2; ++dk) acc.add(ty * 8 + cell0 + dk, c[ty * 2 + dk]);
 }
 
 // one wedge per thread
-__global__ void __launch_bounds__(256) tri_wedge_kernel(GView G, const int64_t* __restrict__ FT,
+__global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, const int64_t* __restrict__ FT,
                                                         const uint32_t* __restrict__ FN,
                                                         const uint32_t* __restrict__ FO,
                                                         int64_t delta,
@@ -254,20 +230,22 @@ __global__ void __launch_bounds__(256) tri_wedge_kernel(GView G, const int64_t* 
                                                         uint32_t wedge_cap,
                                                         const uint32_t* __restrict__ counters,
                                                         uint64_t* out) {
-    TriAcc acc;
-#pragma unroll
-    for (int j = 0; j < 24; ++j) acc.v[j] = 0;
+    __shared__ unsigned long long cells[24];
+    zero_cells(cells, 24);
+    __syncthreads();
+    const SmemSink acc{cells};
     const uint32_t cnt = min(min(counters[0], wedge_cap), counters[2]);
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
          idx += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t w = wedges[idx];
-        add_wedge(G, FT, FN, FO, (uint32_t)(w >> 32), (uint32_t)w, delta, acc);
+        add_wedge(P, FT, FN, FO, (uint32_t)(w >> 32), (uint32_t)w, delta, acc);
     }
-    flush_tri(acc, out);
+    __syncthreads();
+    flush_cells(cells, 24, out);
 }
 
 // first edges with long windows: the whole wedge loop in one thread
-__global__ void __launch_bounds__(256) tri_long_kernel(GView G, const int64_t* __restrict__ FT,
+__global__ void __launch_bounds__(256) tri_long_kernel(PView P, const int64_t* __restrict__ FT,
                                                        const uint32_t* __restrict__ FN,
                                                        const uint32_t* __restrict__ FO,
                                                        const uint32_t* __restrict__ Fnode,
@@ -276,16 +254,18 @@ __global__ void __launch_bounds__(256) tri_long_kernel(GView G, const int64_t* _
                                                        const uint32_t* __restrict__ list,
                                                        const uint32_t* __restrict__ counters,
                                                        uint64_t* out) {
-    TriAcc acc;
-#pragma unroll
-    for (int j = 0; j < 24; ++j) acc.v[j] = 0;
+    __shared__ unsigned long long cells[24];
+    zero_cells(cells, 24);
+    __syncthreads();
+    const SmemSink acc{cells};
     const uint32_t cnt = counters[1];
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
          idx += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t i = list[idx];
-        wedges_from(G, FT, FN, FO, i, Foff[Fnode[i] + 1], delta, nullptr, acc);
+        wedges_from(P, FT, FN, FO, i, Foff[Fnode[i] + 1], delta, nullptr, acc);
     }
-    flush_tri(acc, out);
+    __syncthreads();
+    flush_cells(cells, 24, out);
 }
 
 __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ item_off, uint64_t n_items,
@@ -298,7 +278,7 @@ __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ item_
     return (uint32_t)lo;
 }
 
-__global__ void __launch_bounds__(256) tri_items_kernel(SView S, GView G, int64_t delta,
+__global__ void __launch_bounds__(256) tri_items_kernel(SView S, PView P, int64_t delta,
                                                         uint64_t n_items,
                                                         const uint32_t* __restrict__ nodes,
                                                         const uint64_t* __restrict__ begin,
@@ -312,14 +292,8 @@ __global__ void __launch_bounds__(256) tri_items_kernel(SView S, GView G, int64_
         const uint32_t u = nodes[it];
         const uint32_t start = S.off[u], end = S.off[u + 1];
         const uint32_t i = start + (uint32_t)begin[it] + (uint32_t)(idx - item_off[it]);
-        TriAcc acc;
-#pragma unroll
-        for (int j = 0; j < 24; ++j) acc.v[j] = 0;
-        wedges_from(G, S.t, S.nbr, S.ord, i, end, delta, live, acc);
-#pragma unroll
-        for (int c = 0; c < 24; ++c)
-            if (acc.v[c]) atomicAdd((unsigned long long*)&out[(uint64_t)it * 24 + c],
-                                    (unsigned long long)acc.v[c]);
+        wedges_from(P, S.t, S.nbr, S.ord, i, end, delta, live,
+                    GlobalSink{(unsigned long long*)out + (uint64_t)it * 24});
     }
 }
 
@@ -342,9 +316,9 @@ void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_
     TM_CUDA(cudaMemsetAsync(counters + 2, 0xFF, sizeof(uint32_t), st));
     TM_LAUNCH("tri_filter", st, tri_filter_kernel, (unsigned)grid, 256, 0, f.t, f.nbr, f.node, delta,
               f_begin, f_end, wedges, wedge_cap, long_list, counters);
-    TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, gview(g), f.t, f.nbr, f.ord,
+    TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pview(g), f.t, f.nbr, f.ord,
               delta, wedges, wedge_cap, counters, d_out);
-    TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, gview(g), f.t, f.nbr, f.ord,
+    TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pview(g), f.t, f.nbr, f.ord,
               f.node, f.off, delta, long_list, counters, d_out);
     dfree(wedges, st);
     dfree(long_list, st);
@@ -357,7 +331,7 @@ void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint
     const uint64_t cap = (uint64_t)sm_count() * 8;
     uint64_t grid = (total + 255) / 256;
     if (grid > cap) grid = cap;
-    TM_LAUNCH("tri_items", g.stream, tri_items_kernel, (unsigned)grid, 256, 0, sview(g), gview(g),
+    TM_LAUNCH("tri_items", g.stream, tri_items_kernel, (unsigned)grid, 256, 0, sview(g), pview(g),
               delta, n_items, d_nodes, d_begin, d_item_off, total, d_live, d_out);
 }
 
