@@ -106,17 +106,18 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedE
                                 int64_t* __restrict__ S_t, uint32_t* __restrict__ S_nbr,
                                 uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
                                 uint32_t* __restrict__ rec2s) {
+    const uint64_t keep = l2_policy_evict_last();
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
          q += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t key = skeys[q];
+        const uint64_t key = __ldcs(skeys + q);
         const uint32_t r = (uint32_t)key;
         const uint32_t p = r >> 1, side = r & 1u;
         const PackedEdge e = E[p];
-        S_t[q] = e.t;
-        S_ord[q] = perm ? perm[p] : p;
-        S_node[q] = (uint32_t)(key >> 32);
-        S_nbr[q] = (side ? e.src : e.dst) | (side << 31);
-        rec2s[r] = (uint32_t)q;
+        __stcs(S_t + q, e.t);
+        __stcs(S_ord + q, perm ? perm[p] : p);
+        __stcs(S_node + q, (uint32_t)(key >> 32));
+        __stcs(S_nbr + q, (side ? e.src : e.dst) | (side << 31));
+        st_keep_u32(rec2s + r, (uint32_t)q, keep);  // re-read by gather_p: keep in L2
     }
 }
 

@@ -99,6 +99,16 @@ __device__ __forceinline__ uint64_t warp_lookback(const uint64_t* status, int64_
     return acc;
 }
 
+// L2 eviction-priority hints: keep scatter targets resident, stream the rest
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_keep_u32(uint32_t* p, uint32_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+
 // warp-aggregated append of `value` to list when pred holds (whole warp calls)
 __device__ __forceinline__ void warp_append(bool pred, uint32_t value, uint32_t* list,
                                             uint32_t* counter) {

@@ -244,7 +244,8 @@ __global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, const int64_t* 
     flush_cells(cells, 24, out);
 }
 
-// first edges with long windows: the whole wedge loop in one thread
+// first edges with long windows: one warp per first edge, lanes stride the
+// in-window records (the HARE intra-node split, per first edge)
 __global__ void __launch_bounds__(256) tri_long_kernel(PView P, const int64_t* __restrict__ FT,
                                                        const uint32_t* __restrict__ FN,
                                                        const uint32_t* __restrict__ FO,
@@ -259,10 +260,20 @@ __global__ void __launch_bounds__(256) tri_long_kernel(PView P, const int64_t* _
     __syncthreads();
     const SmemSink acc{cells};
     const uint32_t cnt = counters[1];
-    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
-         idx += (uint64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t idx = warp; idx < cnt; idx += nwarps) {
         const uint32_t i = list[idx];
-        wedges_from(P, FT, FN, FO, i, Foff[Fnode[i] + 1], delta, nullptr, acc);
+        const uint32_t end = Foff[Fnode[i] + 1];
+        const uint32_t v = FN[i] & kNodeMask;
+        const int64_t lim = sat_add(FT[i], delta);
+        for (uint32_t j0 = i + 1; j0 < end; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            const bool in = j < end && FT[j] <= lim;
+            if (in && (FN[j] & kNodeMask) != v) add_wedge(P, FT, FN, FO, i, j, delta, acc);
+            if (!__all_sync(0xffffffffu, in)) break;
+        }
     }
     __syncthreads();
     flush_cells(cells, 24, out);
