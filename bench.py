@@ -62,11 +62,20 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def load_workload(name: str):
+def load_workload(name: str, delta=None):
     from paper_2204_09236_b200 import synth
-    cfg = synth.CONFIGS[name]
+    if name in synth.CONFIGS:
+        cfg = synth.CONFIGS[name]
+        n, src, dst, t = cfg["fn"]()
+        return n, src, dst, t, int(delta if delta is not None else cfg["delta"])
+    cfg = synth.GPU_CONFIGS[name]  # generated on the GPU, copied to host arrays
     n, src, dst, t = cfg["fn"]()
-    return n, src, dst, t, cfg["delta"]
+    d = delta if delta is not None else cfg.get("delta", (cfg.get("deltas") or [3600])[1 if len(cfg.get("deltas", [])) > 1 else 0])
+    out = (src.cpu().numpy().view(np.uint32), dst.cpu().numpy().view(np.uint32), t.cpu().numpy())
+    del src, dst, t
+    import torch
+    torch.cuda.empty_cache()
+    return n, out[0], out[1], out[2], int(d)
 
 
 class ClockSampler:
@@ -156,6 +165,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-edges", type=int, default=1_000_000)
+    ap.add_argument("--delta", type=int, default=None, help="override the config's delta")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="counter all-reduce backend (gloo: CPU tensors, for multi-rank tests on one GPU)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="testing only: every rank uses cuda:0 (independent kernels, gloo reduce)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -164,7 +178,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     threads = os.cpu_count() or 1
 
-    n, src, dst, t, delta = load_workload(args.config)
+    n, src, dst, t, delta = load_workload(args.config, args.delta)
     m = len(src)
     base_cfg = {"workload": args.config, "nodes": int(n), "edges": int(m), "delta": int(delta),
                 "inputs": "time-ordered synthetic edge list (seed 2204), ingestion order = time order",
@@ -187,12 +201,18 @@ def main():
         return
 
     import torch
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    red_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     import paper_2204_09236_b200 as tm
 
     stream = torch.cuda.Stream(device=dev)
@@ -212,7 +232,7 @@ def main():
     b, e = ctx.partition(world, rank)
     ctx.close()
     center = (b, e) if world > 1 else (0, 0)
-    red = torch.zeros(56, dtype=torch.int64, device=dev)
+    red = torch.zeros(56, dtype=torch.int64, device=red_dev)
     raw = np.zeros(56, np.uint64)
 
     def step(host: bool):
@@ -222,7 +242,7 @@ def main():
         else:
             census = tm.count_edges_device(n, m, d_src.data_ptr(), d_dst.data_ptr(), d_t.data_ptr(), cfg,
                                            stream=sptr, center=center, raw_out=raw)
-        if world > 1:
+        if world > 1:  # one all-reduce of the 56 raw u64 counters (exact modulo 2^64)
             with torch.cuda.stream(stream):
                 red.copy_(torch.from_numpy(raw.view(np.int64)), non_blocking=False)
                 dist.all_reduce(red)
@@ -251,7 +271,7 @@ def main():
             dist.barrier()
         ms = ev0.elapsed_time(ev1)
         if dist:
-            x = torch.tensor([ms], dtype=torch.float64, device=dev)
+            x = torch.tensor([ms], dtype=torch.float64, device=red_dev)
             dist.all_reduce(x, op=dist.ReduceOp.MAX)
             ms = float(x.item())
         return ms / steps, census, tm.kernel_launches() - l0

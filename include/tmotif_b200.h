@@ -136,6 +136,10 @@ int tm_generate_random_graph(uint64_t nodes, uint64_t m, int64_t t_max, uint64_t
                              uint32_t* src, uint32_t* dst, int64_t* t);
 
 /* ---- diagnostics -------------------------------------------------------- */
+/* Work counters of the graph's last counting run: [0] star first-edge
+ * candidates, [1] star third-edge candidates, [2] short-window wedges,
+ * [3] long-window first edges, [4] long-window wedges, [5..7] reserved. */
+int tm_run_stats(const tm_graph* g, uint64_t* out8);
 const char* tm_last_error(void);
 /* Number of this library's kernels launched since load. */
 uint64_t tm_kernel_launches(void);

@@ -294,7 +294,7 @@ void run_passes(tm_graph* G, int64_t delta, bool do_star, bool do_tri, int tri_m
             qb = read_u32(g.off, cb, s);
             qe = read_u32(g.off, ce, s);
         }
-        star_full(g, delta, qb, qe, g.d_acc);
+        star_full(g, delta, qb, qe, g.d_acc, g.d_acc + 56);
     }
     if (tm) TM_CUDA(cudaEventRecord(e1, s));
     if (do_tri && g.R) {
@@ -306,7 +306,7 @@ void run_passes(tm_graph* G, int64_t delta, bool do_star, bool do_tri, int tri_m
             fb = read_u32(f.off, cb, s);
             fe = read_u32(f.off, ce, s);
         }
-        tri_oriented(g, f, delta, fb, fe, g.d_acc + 32);
+        tri_oriented(g, f, delta, fb, fe, g.d_acc + 32, g.d_acc + 56);
     }
     if (tm) TM_CUDA(cudaEventRecord(e2, s));
     uint64_t* h = pinned_acc();
@@ -314,6 +314,7 @@ void run_passes(tm_graph* G, int64_t delta, bool do_star, bool do_tri, int tri_m
     TM_CUDA(cudaStreamSynchronize(s));
     std::memcpy(r.star_raw, h, 32 * sizeof(uint64_t));
     std::memcpy(r.tri_once, h + 32, 24 * sizeof(uint64_t));
+    std::memcpy(g.stats, h + 56, 8 * sizeof(uint64_t));
     if (tm) {
         float a = 0, b = 0;
         cudaEventElapsedTime(&a, e0, e1);
@@ -784,6 +785,12 @@ int tm_generate_random_graph(uint64_t nodes, uint64_t m, int64_t t_max, uint64_t
         dst[i] = o + (o >= s ? 1 : 0);
         t[i] = (int64_t)draw((uint64_t)t_max + 1);
     }
+    return TM_OK;
+}
+
+int tm_run_stats(const tm_graph* g, uint64_t* out8) {
+    if (!g || !out8) return TM_ERR_INVALID;
+    std::memcpy(out8, g->g.stats, 8 * sizeof(uint64_t));
     return TM_OK;
 }
 

@@ -111,7 +111,8 @@ struct DeviceGraph {
 
     Forward fwd[2];
 
-    uint64_t* d_acc = nullptr;  // 64 u64 device accumulators
+    uint64_t* d_acc = nullptr;  // 64 u64: star raw [0,32), tri [32,56), work stats [56,64)
+    uint64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // last run's work statistics
 };
 
 // read-only views passed by value to kernels
@@ -150,14 +151,14 @@ void build_s_pidx(DeviceGraph& g);
 // raw star sums (32 u64: Pair[8], C[8], B[8], A[8]) for the centers whose
 // S positions are [q_begin, q_end), added into d_out.
 void star_full(const DeviceGraph& g, int64_t delta, uint32_t q_begin, uint32_t q_end,
-               uint64_t* d_out);
+               uint64_t* d_out, uint64_t* d_stats);
 void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
                 const uint64_t* d_begin, const uint64_t* d_end, const uint64_t* d_item_off,
                 uint64_t total_first, uint64_t total_third, const uint64_t* d_third_off,
                 uint64_t* d_out);
 // once-counted triangle cells (24 u64) over forward positions [f_begin, f_end)
 void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
-                  uint32_t f_end, uint64_t* d_out);
+                  uint32_t f_end, uint64_t* d_out, uint64_t* d_stats);
 void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
                const uint64_t* d_begin, const uint64_t* d_item_off, uint64_t total,
                const uint8_t* d_live, uint64_t* d_out);

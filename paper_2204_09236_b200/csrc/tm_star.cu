@@ -225,9 +225,14 @@ __global__ void __launch_bounds__(256) star_work_kernel(SView S, PView P, int64_
                                                         const uint64_t* __restrict__ first_list,
                                                         const uint64_t* __restrict__ third_list,
                                                         const uint32_t* __restrict__ counters,
-                                                        uint64_t* __restrict__ out) {
+                                                        uint64_t* __restrict__ out,
+                                                        uint64_t* __restrict__ stats) {
     __shared__ unsigned long long cells[32];
     zero_cells(cells, 32);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && stats) {
+        stats[0] = counters[0];
+        stats[1] = counters[1];
+    }
     __syncthreads();
     const SmemSink acc{cells};
     const uint32_t nf = counters[0], nt = counters[1];
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(256) star_items_kernel(
 }  // namespace
 
 void star_full(const DeviceGraph& g, int64_t delta, uint32_t q_begin, uint32_t q_end,
-               uint64_t* d_out) {
+               uint64_t* d_out, uint64_t* d_stats) {
     if (q_end <= q_begin || g.m == 0) return;
     cudaStream_t st = g.stream;
     const uint64_t work = q_end - q_begin;
@@ -303,7 +308,7 @@ void star_full(const DeviceGraph& g, int64_t delta, uint32_t q_begin, uint32_t q
     TM_LAUNCH("star_filter", st, star_filter_kernel, (unsigned)grid, 256, 0, pview(g), delta, g.m,
               q_begin, q_end, lists, lists + work, counters);
     TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), delta, lists,
-              lists + work, counters, d_out);
+              lists + work, counters, d_out, d_stats);
     dfree(lists, st);
 }
 

@@ -229,12 +229,13 @@ __global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, const int64_t* 
                                                         const uint64_t* __restrict__ wedges,
                                                         uint32_t wedge_cap,
                                                         const uint32_t* __restrict__ counters,
-                                                        uint64_t* out) {
+                                                        uint64_t* out, uint64_t* stats) {
     __shared__ unsigned long long cells[24];
     zero_cells(cells, 24);
     __syncthreads();
     const SmemSink acc{cells};
     const uint32_t cnt = min(min(counters[0], wedge_cap), counters[2]);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && stats) stats[2] = cnt;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
          idx += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t w = wedges[idx];
@@ -254,12 +255,14 @@ __global__ void __launch_bounds__(256) tri_long_kernel(PView P, const int64_t* _
                                                        int64_t delta,
                                                        const uint32_t* __restrict__ list,
                                                        const uint32_t* __restrict__ counters,
-                                                       uint64_t* out) {
+                                                       uint64_t* out, uint64_t* stats) {
     __shared__ unsigned long long cells[24];
     zero_cells(cells, 24);
     __syncthreads();
     const SmemSink acc{cells};
     const uint32_t cnt = counters[1];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && stats) stats[3] = cnt;
+    uint32_t my_wedges = 0;
     const int lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -271,10 +274,15 @@ __global__ void __launch_bounds__(256) tri_long_kernel(PView P, const int64_t* _
         for (uint32_t j0 = i + 1; j0 < end; j0 += 32) {
             const uint32_t j = j0 + lane;
             const bool in = j < end && FT[j] <= lim;
-            if (in && (FN[j] & kNodeMask) != v) add_wedge(P, FT, FN, FO, i, j, delta, acc);
+            if (in && (FN[j] & kNodeMask) != v) {
+                add_wedge(P, FT, FN, FO, i, j, delta, acc);
+                ++my_wedges;
+            }
             if (!__all_sync(0xffffffffu, in)) break;
         }
     }
+    my_wedges = warp_sum(my_wedges);
+    if (lane == 0 && my_wedges && stats) atomicAdd((unsigned long long*)&stats[4], (unsigned long long)my_wedges);
     __syncthreads();
     flush_cells(cells, 24, out);
 }
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(256) tri_items_kernel(SView S, PView P, int64_
 }  // namespace
 
 void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
-                  uint32_t f_end, uint64_t* d_out) {
+                  uint32_t f_end, uint64_t* d_out, uint64_t* d_stats) {
     if (f_end <= f_begin) return;
     cudaStream_t st = g.stream;
     const uint64_t work = f_end - f_begin;
@@ -328,9 +336,9 @@ void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_
     TM_LAUNCH("tri_filter", st, tri_filter_kernel, (unsigned)grid, 256, 0, f.t, f.nbr, f.node, delta,
               f_begin, f_end, wedges, wedge_cap, long_list, counters);
     TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pview(g), f.t, f.nbr, f.ord,
-              delta, wedges, wedge_cap, counters, d_out);
+              delta, wedges, wedge_cap, counters, d_out, d_stats);
     TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pview(g), f.t, f.nbr, f.ord,
-              f.node, f.off, delta, long_list, counters, d_out);
+              f.node, f.off, delta, long_list, counters, d_out, d_stats);
     dfree(wedges, st);
     dfree(long_list, st);
 }

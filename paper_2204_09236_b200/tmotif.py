@@ -132,6 +132,7 @@ def lib():
     L.tm_cell_signature.argtypes = [C.c_int, C.c_int]
     L.tm_signature_label.argtypes = [C.c_int, C.c_char_p]
     L.tm_generate_random_graph.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_uint64, VP, VP, VP]
+    L.tm_run_stats.argtypes = [VP, VP]
     L.tm_last_error.restype = C.c_char_p
     L.tm_kernel_launches.restype = C.c_uint64
     L.tm_kernel_timing_enable.argtypes = [C.c_int]
@@ -602,6 +603,14 @@ class GraphContext:
                                         d.ctypes.data, cap, C.byref(n)), self._lib)
         k = int(n.value)
         return [(int(t[i]), int(o[i]), Direction(int(d[i]))) for i in range(k)]
+
+    def run_stats(self) -> Dict[str, int]:
+        """Work counters of the last counting run on this graph."""
+        out = np.zeros(8, np.uint64)
+        _raise(self._lib.tm_run_stats(self._h, out.ctypes.data), self._lib)
+        keys = ["star_first_candidates", "star_third_candidates", "short_wedges", "long_first_edges",
+                "long_wedges"]
+        return {k: int(v) for k, v in zip(keys, out)}
 
     def partition(self, world: int, rank: int) -> Tuple[int, int]:
         b, e = C.c_uint32(0), C.c_uint32(0)
