@@ -500,7 +500,7 @@ int tm_graph_sequence(const tm_graph* g, uint32_t u, int64_t* t, uint64_t* ordin
         }
         for (uint64_t k = 0; k < s; ++k) {
             if (t) t[k] = ht[k];
-            if (ordinal) ordinal[k] = ho[k];
+            if (ordinal) ordinal[k] = ho[k] & kNodeMask;
             if (other) other[k] = hn[k] & kNodeMask;
             if (dir) dir[k] = (uint8_t)(hn[k] >> 31);
         }

@@ -103,6 +103,7 @@ __global__ void pack_edges_kernel(const uint32_t* __restrict__ perm, const uint3
 
 __global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedEdge* __restrict__ E,
                                 const uint64_t* __restrict__ skeys, uint64_t R,
+                                const uint32_t* __restrict__ off,
                                 int64_t* __restrict__ S_t, uint32_t* __restrict__ S_nbr,
                                 uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
                                 uint32_t* __restrict__ rec2s) {
@@ -114,20 +115,25 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedE
         const uint32_t p = r >> 1, side = r & 1u;
         const PackedEdge e = E[p];
         __stcs(S_t + q, e.t);
-        __stcs(S_ord + q, perm ? perm[p] : p);
-        __stcs(S_node + q, (uint32_t)(key >> 32));
-        __stcs(S_nbr + q, (side ? e.src : e.dst) | (side << 31));
+        const uint32_t u = (uint32_t)(key >> 32), x = side ? e.src : e.dst;
+        // degree-rank orientation of the triangle pass: forward iff (deg, id) of the
+        // neighbour exceeds the center's; kept in the spare top bit of S_ord
+        const uint32_t du = off[u + 1] - off[u], dx = off[x + 1] - off[x];
+        const uint32_t fwd = (dx > du || (dx == du && x > u)) ? kDirBit : 0u;
+        __stcs(S_ord + q, (perm ? perm[p] : p) | fwd);
+        __stcs(S_node + q, u);
+        __stcs(S_nbr + q, x | (side << 31));
         st_keep_u32(rec2s + r, (uint32_t)q, keep);  // re-read by gather_p: keep in L2
     }
 }
 
-// off[x] = first position of node x (boundary fill over the sorted node ids)
-__global__ void offsets_kernel(const uint32_t* __restrict__ node, uint64_t R, uint64_t n,
-                               uint32_t* __restrict__ off) {
+// off[x] from the sorted node keys (node << 32 | record)
+__global__ void offsets_from_keys_kernel(const uint64_t* __restrict__ keys, uint64_t R, uint64_t n,
+                                         uint32_t* __restrict__ off) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
          q += (uint64_t)gridDim.x * blockDim.x) {
-        const int64_t cur = node[q];
-        const int64_t prev = q ? (int64_t)node[q - 1] : -1;
+        const int64_t cur = (int64_t)(keys[q] >> 32);
+        const int64_t prev = q ? (int64_t)(keys[q - 1] >> 32) : -1;
         for (int64_t x = prev + 1; x <= cur; ++x) off[x] = (uint32_t)q;
         if (q == R - 1)
             for (int64_t x = cur + 1; x <= (int64_t)n; ++x) off[x] = (uint32_t)R;
@@ -213,11 +219,10 @@ struct ForwardFlag {
     const uint32_t* nbr;
     const uint32_t* off;
     int mode;
+    const uint32_t* ord;
     __device__ __forceinline__ uint32_t operator()(uint64_t q) const {
-        const uint32_t u = node[q], x = nbr[q] & kNodeMask;
-        if (mode == 1) return x > u ? 1u : 0u;
-        const uint32_t du = off[u + 1] - off[u], dx = off[x + 1] - off[x];
-        return (dx > du || (dx == du && x > u)) ? 1u : 0u;
+        if (mode == 0) return ord[q] >> 31;  // degree orientation bit set by gather_s
+        return (nbr[q] & kNodeMask) > node[q] ? 1u : 0u;
     }
 };
 
@@ -232,7 +237,7 @@ __global__ void forward_scatter_kernel(ForwardFlag flag, const uint32_t* __restr
             const uint32_t j = fscan[q];
             F_t[j] = S_t[q];
             F_nbr[j] = flag.nbr[q];
-            F_ord[j] = S_ord[q];
+            F_ord[j] = S_ord[q] & kNodeMask;
             F_node[j] = flag.node[q];
         }
     }
@@ -307,10 +312,10 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         const int tbits = bit_width_u64((uint64_t)h_st.tmax - (uint64_t)h_st.tmin);
         const int kbits = bit_width_u64(m - 1 ? m - 1 : 1);
         const bool packed = tbits + kbits <= 64;
-        uint64_t* k0 = dalloc<uint64_t>(m, s);
-        uint64_t* k1 = dalloc<uint64_t>(m, s);
-        uint32_t* v0 = packed ? nullptr : dalloc<uint32_t>(m, s);
-        uint32_t* v1 = packed ? nullptr : dalloc<uint32_t>(m, s);
+        uint64_t* k0 = dalloc<uint64_t>(m + kSortPad, s);
+        uint64_t* k1 = dalloc<uint64_t>(m + kSortPad, s);
+        uint32_t* v0 = packed ? nullptr : dalloc<uint32_t>(m + kSortPad, s);
+        uint32_t* v1 = packed ? nullptr : dalloc<uint32_t>(m + kSortPad, s);
         TM_LAUNCH("time_keys", s, time_keys_kernel, grid_for(m), 256, 0, d_t, m, (int64_t)h_st.tmin,
                   kbits, packed, k0, v0);
         if (packed) {
@@ -330,27 +335,27 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     // 2. S: stable sort of the incident records by node (key node << 32 | r)
     const int nb = bit_width_u64(n > 1 ? n - 1 : 1);
     {
-        uint64_t* nk0 = dalloc<uint64_t>(R, s);
-        uint64_t* nk1 = dalloc<uint64_t>(R, s);
+        uint64_t* nk0 = dalloc<uint64_t>(R + kSortPad, s);
+        uint64_t* nk1 = dalloc<uint64_t>(R + kSortPad, s);
         uint32_t* rec2s = dalloc<uint32_t>(R, s);
         PackedEdge* E = dalloc<PackedEdge>(m, s);
         TM_LAUNCH("pack_edges", s, pack_edges_kernel, grid_for(m), 256, 0, perm, d_src, d_dst, d_t, m, E,
                   nk0);
         radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s);
-        TM_LAUNCH("gather_s", s, gather_s_kernel, grid_for(R), 256, 0, perm, E, nk0, R, g.S_t, g.S_nbr,
-                  g.S_ord, g.S_node, rec2s);
+        TM_LAUNCH("offsets", s, offsets_from_keys_kernel, grid_for(R), 256, 0, nk0, R, n, g.off);
+        TM_LAUNCH("gather_s", s, gather_s_kernel, grid_for(R), 256, 0, perm, E, nk0, R, g.off, g.S_t,
+                  g.S_nbr, g.S_ord, g.S_node, rec2s);
         dfree(nk0, s);
         dfree(nk1, s);
-        TM_LAUNCH("offsets", s, offsets_kernel, grid_for(R), 256, 0, g.S_node, R, n, g.off);
         exclusive_scan<uint32_t>(OutwardLoad{g.S_nbr}, R, g.S_pg, s);
 
         // 3. P: stable sort of the edges by unordered pair {min, max}
         const int pbits = bit_width_u64(m - 1 ? m - 1 : 1);
         const bool packed = 2 * nb + pbits <= 64;
-        uint64_t* pk0 = dalloc<uint64_t>(m, s);
-        uint64_t* pk1 = dalloc<uint64_t>(m, s);
-        uint32_t* pv0 = packed ? nullptr : dalloc<uint32_t>(m, s);
-        uint32_t* pv1 = packed ? nullptr : dalloc<uint32_t>(m, s);
+        uint64_t* pk0 = dalloc<uint64_t>(m + kSortPad, s);
+        uint64_t* pk1 = dalloc<uint64_t>(m + kSortPad, s);
+        uint32_t* pv0 = packed ? nullptr : dalloc<uint32_t>(m + kSortPad, s);
+        uint32_t* pv1 = packed ? nullptr : dalloc<uint32_t>(m + kSortPad, s);
         TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(m), 256, 0, E, m, nb, pbits, packed, pk0,
                   pv0);
         if (packed) radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, pbits, pbits + 2 * nb, s);
@@ -383,7 +388,7 @@ void build_forward(DeviceGraph& g, int mode) {
     f.node = dalloc<uint32_t>(g.m, s);
     f.off = dalloc<uint32_t>(g.n + 1, s);
     uint32_t* fscan = dalloc<uint32_t>(R + 1, s);
-    ForwardFlag flag{g.S_node, g.S_nbr, g.off, mode};
+    ForwardFlag flag{g.S_node, g.S_nbr, g.off, mode, g.S_ord};
     exclusive_scan<uint32_t>(flag, R, fscan, s);
     if (R) {
         TM_LAUNCH("forward_scatter", s, forward_scatter_kernel, grid_for(R), 256, 0, flag, fscan, R,

@@ -4,7 +4,7 @@
 //   S (time-ordered per-node sequences, NodeSequenceIndex, indexes.hpp:22-40)
 //     S_t[R]    int64  timestamp
 //     S_nbr[R]  u32    other endpoint | dir << 31   (dir 0 = outward)
-//     S_ord[R]  u32    ingestion ordinal
+//     S_ord[R]  u32    ingestion ordinal | forward-in-degree-order << 31
 //     S_node[R] u32    center node
 //     S_pg[R+1] u32    global exclusive prefix count of outward records
 //     S_pidx[R] u32    the record's edge position in P (built lazily, items API)

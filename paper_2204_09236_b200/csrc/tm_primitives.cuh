@@ -15,6 +15,7 @@
 //    memory and writes each digit run as one burst.
 #pragma once
 
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -328,6 +329,39 @@ __global__ void __launch_bounds__(BLOCK) radix_upsweep(const K* __restrict__ key
     }
 }
 
+// One block per digit d: offs[d][t] = sum_{t' < t} counts[d][t'] (row-local),
+// totals[d] = row sum.  The downsweep adds the exclusive scan of totals.
+static __global__ void __launch_bounds__(256) radix_scan_counts(const uint32_t* __restrict__ counts,
+                                                                uint32_t ntiles,
+                                                                uint32_t* __restrict__ offs,
+                                                                uint32_t* __restrict__ totals) {
+    const uint32_t d = blockIdx.x;
+    __shared__ uint32_t s_tot;
+    uint32_t carry = 0;
+    const uint32_t* row = counts + (uint64_t)d * ntiles;
+    uint32_t* orow = offs + (uint64_t)d * ntiles;
+    for (uint32_t base = 0; base < ntiles; base += 256 * 4) {
+        uint32_t v[4];
+        uint32_t ts = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = base + threadIdx.x * 4 + k;
+            v[k] = i < ntiles ? row[i] : 0u;
+            ts += v[k];
+        }
+        uint32_t run = block_exclusive_scan<uint32_t, 8>(ts, &s_tot) + carry;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = base + threadIdx.x * 4 + k;
+            if (i < ntiles) orow[i] = run;
+            run += v[k];
+        }
+        carry += s_tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) totals[d] = carry;
+}
+
 template <typename K, bool kVals, int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK) radix_downsweep(const K* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin,
@@ -335,7 +369,8 @@ __global__ void __launch_bounds__(BLOCK) radix_downsweep(const K* __restrict__ k
                                                          uint32_t* __restrict__ vout, uint64_t n,
                                                          int shift,
                                                          const uint32_t* __restrict__ tile_offsets,
-                                                         uint32_t ntiles) {
+                                                         uint32_t ntiles,
+                                                         const uint32_t* __restrict__ totals) {
     constexpr int NW = BLOCK / 32;
     constexpr int TILE = BLOCK * ITEMS;
     static_assert(BLOCK >= kRadix, "one digit per thread");
@@ -386,9 +421,10 @@ __global__ void __launch_bounds__(BLOCK) radix_downsweep(const K* __restrict__ k
         cnt = run;
     }
     const uint32_t ex = block_exclusive_scan<uint32_t, NW>(cnt, nullptr);
+    const uint32_t dbase = block_exclusive_scan<uint32_t, NW>(tid < kRadix ? totals[tid] : 0u, nullptr);
     if (tid < kRadix) {
         dstart[tid] = ex;
-        dglob[tid] = tile_offsets[(uint64_t)tid * ntiles + blockIdx.x];
+        dglob[tid] = tile_offsets[(uint64_t)tid * ntiles + blockIdx.x] + dbase;
     }
     __syncthreads();
 #pragma unroll
@@ -412,11 +448,189 @@ __global__ void __launch_bounds__(BLOCK) radix_downsweep(const K* __restrict__ k
     }
 }
 
+// ---- TMA-pipelined persistent downsweep ----------------------------------
+// Each block loops over tiles blockIdx.x, +gridDim.x, ...; one elected thread
+// streams tile i+1 into the other shared-memory stage with cp.async.bulk
+// (mbarrier completion) while the block ranks and scatters tile i.  Keys are
+// re-read from shared memory instead of being held in registers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+// lanes of the warp holding the same 8-bit digit (invalid lanes pass 256 and
+// get no peers among valid lanes): bit-sliced ballots instead of MATCH.ANY
+template <bool kBallot>
+__device__ __forceinline__ unsigned digit_peers(uint32_t d) {
+    if (!kBallot) return __match_any_sync(0xffffffffu, d);
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+        const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bal : ~bal;
+    }
+    return peers;
+}
+
+template <typename K, bool kVals, bool kBallot = true>
+__global__ void __launch_bounds__(512, 2) radix_downsweep_tma(const K* __restrict__ kin,
+                                                              const uint32_t* __restrict__ vin,
+                                                              K* __restrict__ kout,
+                                                              uint32_t* __restrict__ vout, uint64_t n,
+                                                              int shift,
+                                                              const uint32_t* __restrict__ tile_offsets,
+                                                              uint32_t ntiles,
+                                                              const uint32_t* __restrict__ totals) {
+    constexpr int BLOCK = 512, NW = BLOCK / 32, ITEMS = 8, TILE = BLOCK * ITEMS;
+    constexpr uint32_t STAGE_BYTES = TILE * (sizeof(K) + (kVals ? 4 : 0));
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    // [stage0][stage1][out]: each TILE keys (+ TILE vals)
+    auto stage_keys = [&](int s) { return reinterpret_cast<K*>(tma_smem + s * STAGE_BYTES); };
+    auto stage_vals = [&](int s) {
+        return reinterpret_cast<uint32_t*>(tma_smem + s * STAGE_BYTES + TILE * sizeof(K));
+    };
+    K* okeys = stage_keys(2);
+    uint32_t* ovals = stage_vals(2);
+    __shared__ uint16_t wcnt[NW][kRadix];  // per-warp counts <= 256, prefixes <= 4096
+    __shared__ uint32_t dstart[kRadix];
+    __shared__ uint32_t dglob[kRadix];
+    __shared__ __align__(8) uint64_t bar[2];
+
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](uint32_t tile, int s) {
+        const uint64_t base = (uint64_t)tile * TILE;
+        const uint64_t cnt = (n - base) < (uint64_t)TILE ? (n - base) : (uint64_t)TILE;
+        const uint32_t kbytes = (uint32_t)((cnt * sizeof(K) + 15) & ~uint64_t(15));
+        const uint32_t vbytes = kVals ? (uint32_t)((cnt * 4 + 15) & ~uint64_t(15)) : 0u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[s], kbytes + vbytes);
+        tma_load_1d(stage_keys(s), kin + base, kbytes, &bar[s]);
+        if (kVals) tma_load_1d(stage_vals(s), vin + base, vbytes, &bar[s]);
+    };
+    const uint32_t dbase = block_exclusive_scan<uint32_t, NW>(tid < kRadix ? totals[tid] : 0u, nullptr);
+    uint32_t tile = blockIdx.x;
+    if (tid == 0 && tile < ntiles) issue(tile, 0);
+    for (uint32_t it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        const int s = it & 1;
+        const uint32_t next = tile + gridDim.x;
+        if (tid == 0 && next < ntiles) issue(next, s ^ 1);
+        for (int i = tid; i < NW * kRadix; i += BLOCK) (&wcnt[0][0])[i] = 0;
+        const uint64_t tbase = (uint64_t)tile * TILE;
+        const uint32_t tile_n = (uint32_t)((n - tbase) < (uint64_t)TILE ? (n - tbase) : (uint64_t)TILE);
+        mbar_wait(&bar[s], (it >> 1) & 1);
+        __syncthreads();
+        const K* sk = stage_keys(s);
+        uint32_t rank[ITEMS];
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const uint32_t i = w * (ITEMS * 32) + r * 32 + lane;
+            const bool valid = i < tile_n;
+            const uint32_t d = valid ? ((uint32_t)(sk[i] >> shift) & 255u) : 256u;
+            const unsigned peers = digit_peers<kBallot>(d);
+            const uint32_t prev = valid ? wcnt[w][d] : 0u;
+            rank[r] = prev + __popc(peers & lt);
+            __syncwarp();
+            if (valid && (peers & lt) == 0) wcnt[w][d] = (uint16_t)(prev + __popc(peers));
+            __syncwarp();
+        }
+        __syncthreads();
+        uint32_t cnt = 0;
+        if (tid < kRadix) {
+            uint32_t run = 0;
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) {
+                const uint32_t c = wcnt[ww][tid];
+                wcnt[ww][tid] = (uint16_t)run;
+                run += c;
+            }
+            cnt = run;
+        }
+        const uint32_t ex = block_exclusive_scan<uint32_t, NW>(cnt, nullptr);
+        if (tid < kRadix) {
+            dstart[tid] = ex;
+            dglob[tid] = tile_offsets[(uint64_t)tid * ntiles + tile] + dbase;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const uint32_t i = w * (ITEMS * 32) + r * 32 + lane;
+            if (i < tile_n) {
+                const K k = sk[i];
+                const uint32_t d = (uint32_t)(k >> shift) & 255u;
+                const uint32_t q = dstart[d] + wcnt[w][d] + rank[r];
+                okeys[q] = k;
+                if (kVals) ovals[q] = stage_vals(s)[i];
+            }
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < tile_n; i += BLOCK) {
+            const K k = okeys[i];
+            const uint32_t d = (uint32_t)(k >> shift) & 255u;
+            const uint32_t dest = dglob[d] + (i - dstart[d]);
+            kout[dest] = k;
+            if (kVals) vout[dest] = ovals[i];
+        }
+        __syncthreads();
+    }
+}
+
 constexpr int kRsBlock = 512;
 constexpr int kRsItems = 8;
 
+constexpr uint64_t kSortPad = 4;
+
+inline bool use_ballot_rank() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TM_RANK");
+        v = (e && e[0] == 'm') ? 0 : 1;  // default: ballot ranking
+    }
+    return v == 1;
+}
+
+inline bool use_tma_sort() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TM_SORT_TMA");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // Stable sort of keys (and u32 values when vals != nullptr) on key bits
-// [bit_lo, bit_hi).  On return keys/vals point at the sorted data; the *_alt
+// [bit_lo, bit_hi).  Buffers need kSortPad elements of slack (TMA tile loads
+// round up to 16 bytes).  On return keys/vals point at the sorted data; the *_alt
 // pointers at the scratch halves (pointers may be swapped).
 template <typename K>
 void radix_sort(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
@@ -427,8 +641,21 @@ void radix_sort(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, ui
     const int passes = (bit_hi - bit_lo + 7) / 8;
     const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
     const size_t smem = TILE * (sizeof(K) + (with_vals ? sizeof(uint32_t) : 0));
+    const size_t tma_smem = 3 * smem;
     static bool attr_set = false;
     if (!attr_set) {
+        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, true, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(3 * TILE * (sizeof(K) + sizeof(uint32_t)))));
+        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(3 * TILE * sizeof(K))));
+        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, true, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(3 * TILE * (sizeof(K) + sizeof(uint32_t)))));
+        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, false, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(3 * TILE * sizeof(K))));
         TM_CUDA(cudaFuncSetAttribute(radix_downsweep<K, true, kRsBlock, kRsItems>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(TILE * (sizeof(K) + sizeof(uint32_t)))));
@@ -438,22 +665,43 @@ void radix_sort(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, ui
         attr_set = true;
     }
     const uint64_t ncount = (uint64_t)kRadix * ntiles;
-    uint32_t* counts = dalloc<uint32_t>(2 * ncount + 1, s);
+    uint32_t* counts = dalloc<uint32_t>(2 * ncount + (uint64_t)kRadix * passes, s);
     uint32_t* offs = counts + ncount;
+    uint32_t* totals = offs + ncount;  // 256 digit totals (per pass, reused)
     for (int p = 0; p < passes; ++p) {
         const int shift = bit_lo + 8 * p;
         TM_LAUNCH("radix_upsweep", s, (radix_upsweep<K, kRsBlock, kRsItems>), ntiles, kRsBlock, 0, keys,
                   n, shift, counts, ntiles);
-        exclusive_scan<uint32_t>(ArrayLoad<uint32_t>{counts}, ncount, offs, s);
-        if (with_vals) {
+        TM_LAUNCH("radix_scan", s, radix_scan_counts, kRadix, 256, 0, counts, ntiles, offs, totals);
+        const bool tma = use_tma_sort();
+        const unsigned pgrid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * 2);
+        const bool ballot = use_ballot_rank();
+        if (with_vals && tma) {
+            if (ballot)
+                TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, true, true>), pgrid, 512, tma_smem,
+                          keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
+            else
+                TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, true, false>), pgrid, 512, tma_smem,
+                          keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
+            uint32_t* tv = vals;
+            vals = vals_alt;
+            vals_alt = tv;
+        } else if (tma) {
+            if (ballot)
+                TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, false, true>), pgrid, 512, tma_smem,
+                          keys, nullptr, keys_alt, nullptr, n, shift, offs, ntiles, totals);
+            else
+                TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, false, false>), pgrid, 512,
+                          tma_smem, keys, nullptr, keys_alt, nullptr, n, shift, offs, ntiles, totals);
+        } else if (with_vals) {
             TM_LAUNCH("radix_downsweep", s, (radix_downsweep<K, true, kRsBlock, kRsItems>), ntiles,
-                      kRsBlock, smem, keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles);
+                      kRsBlock, smem, keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
             uint32_t* tv = vals;
             vals = vals_alt;
             vals_alt = tv;
         } else {
             TM_LAUNCH("radix_downsweep", s, (radix_downsweep<K, false, kRsBlock, kRsItems>), ntiles,
-                      kRsBlock, smem, keys, nullptr, keys_alt, nullptr, n, shift, offs, ntiles);
+                      kRsBlock, smem, keys, nullptr, keys_alt, nullptr, n, shift, offs, ntiles, totals);
         }
         K* tk = keys;
         keys = keys_alt;

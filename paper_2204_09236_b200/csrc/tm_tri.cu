@@ -103,7 +103,7 @@ __device__ __forceinline__ void wedges_from(const PView& P, const int64_t* __res
     const uint32_t v = ni & kNodeMask, di = ni >> 31;
     if (live && !live[v]) return;
     const int64_t ti = T[i];
-    const uint32_t oi = ORD[i];
+    const uint32_t oi = ORD[i] & kNodeMask;  // S_ord carries the orientation bit on top
     const int64_t lim = sat_add(ti, delta);
     uint64_t a0[6] = {0, 0, 0, 0, 0, 0}, a1[6] = {0, 0, 0, 0, 0, 0};
     for (uint32_t j = i + 1; j < end; ++j) {
@@ -114,7 +114,7 @@ __device__ __forceinline__ void wedges_from(const PView& P, const int64_t* __res
         if (w == v) continue;
         if (live && !live[w]) continue;
         uint32_t c[6];
-        closing_counts(P, v, w, sat_sub(tj, delta), lim, ti, oi, tj, ORD[j], c);
+        closing_counts(P, v, w, sat_sub(tj, delta), lim, ti, oi, tj, ORD[j] & kNodeMask, c);
         const uint64_t m1 = (nj >> 31) ? ~0ull : 0ull, m0 = ~m1;
 #pragma unroll
         for (int x = 0; x < 6; ++x) {
