@@ -33,9 +33,9 @@ METRIC = "temporal edges/sec, exact 36-motif count (1/2/4/8 B200); % of HBM roof
 
 # Algorithmic bytes per STEP for each kernel family that can dominate a step
 # (DESIGN.md "Roofline"): bytes that must cross HBM at least once.
-#   star_filter   per edge: P t (8 B) + w (4 B) + qmin/qmax (8 B), neighbours' t from the same lines
-#   gather_s      per incident record: sorted key 8 B + edge record 16 B + S outputs 20 B + rec2s 4 B
-#   gather_p      per edge: sorted key 8 B + edge record 16 B + rec2s pair 8 B + P outputs 28 B
+#   star_filter   per edge: P t (8 B) + w (4 B), neighbours' t from the same lines
+#   gather_s      per incident record: sorted key 8 B + edge record 16 B + S outputs 20 B
+#   gather_p      per edge: sorted key 8 B + edge record 16 B + P outputs 24 B
 #   tri_filter    per forward record (one per edge): F t (8 B) + node (4 B)
 #   star_work / tri_work run on the filtered worklists only (random access, no streaming model)
 #   radix_downsweep per key per digit pass: key (+ value) read + write
@@ -56,8 +56,8 @@ def algo_bytes(n, m, t):
     sort += m * pk * 2 * ((2 * nb + 7) // 8)
     if unsorted:
         sort += m * (8 if tb + pbits <= 64 else 12) * 2 * ((tb + 7) // 8)
-    return {"star_filter": m * 20, "tri_filter": m * 12, "radix_downsweep": sort,
-            "gather_s": R * 48, "gather_p": m * 60, "scan": 2 * R * 4 + m * 8}
+    return {"star_filter": m * 12, "tri_filter": m * 12, "radix_downsweep": sort,
+            "gather_s": R * 44, "gather_p": m * 48, "scan": 2 * R * 4 + m * 8}
 
 
 def log(*a):

@@ -288,14 +288,7 @@ void run_passes(tm_graph* G, int64_t delta, bool do_star, bool do_tri, int tri_m
         TM_CUDA(cudaEventCreate(&e2));
         TM_CUDA(cudaEventRecord(e0, s));
     }
-    if (do_star && g.R) {
-        uint32_t qb = 0, qe = (uint32_t)g.R;
-        if (!full) {
-            qb = read_u32(g.off, cb, s);
-            qe = read_u32(g.off, ce, s);
-        }
-        star_full(g, delta, qb, qe, g.d_acc, g.d_acc + 56);
-    }
+    if (do_star && g.R) star_full(g, delta, cb, ce, g.d_acc, g.d_acc + 56);
     if (tm) TM_CUDA(cudaEventRecord(e1, s));
     if (do_tri && g.R) {
         const int fm = tri_mode == TM_TRI_REMOVAL ? 1 : 0;

@@ -105,9 +105,7 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedE
                                 const uint64_t* __restrict__ skeys, uint64_t R,
                                 const uint32_t* __restrict__ off,
                                 int64_t* __restrict__ S_t, uint32_t* __restrict__ S_nbr,
-                                uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
-                                uint32_t* __restrict__ rec2s) {
-    const uint64_t keep = l2_policy_evict_last();
+                                uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
          q += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t key = __ldcs(skeys + q);
@@ -123,7 +121,6 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedE
         __stcs(S_ord + q, (perm ? perm[p] : p) | fwd);
         __stcs(S_node + q, u);
         __stcs(S_nbr + q, x | (side << 31));
-        st_keep_u32(rec2s + r, (uint32_t)q, keep);  // re-read by gather_p: keep in L2
     }
 }
 
@@ -160,10 +157,9 @@ __global__ void pair_keys_kernel(const PackedEdge* __restrict__ E, uint64_t m, i
 __global__ void gather_p_kernel(const uint64_t* __restrict__ pkeys, const uint32_t* __restrict__ pvals,
                                 uint64_t m, int nb, int pbits, bool packed,
                                 const uint32_t* __restrict__ perm, const PackedEdge* __restrict__ E,
-                                const uint32_t* __restrict__ rec2s,
                                 int64_t* __restrict__ P_t, uint32_t* __restrict__ P_ord,
-                                uint32_t* __restrict__ P_max, uint32_t* __restrict__ P_w,
-                                uint32_t* __restrict__ P_qmin, uint32_t* __restrict__ P_qmax) {
+                                uint32_t* __restrict__ P_min, uint32_t* __restrict__ P_max,
+                                uint32_t* __restrict__ P_w) {
     const uint64_t nmask = (1ull << nb) - 1;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
          k += (uint64_t)gridDim.x * blockDim.x) {
@@ -172,25 +168,41 @@ __global__ void gather_p_kernel(const uint64_t* __restrict__ pkeys, const uint32
         const uint32_t p = packed ? (uint32_t)(key & ((1ull << pbits) - 1)) : pvals[k];
         const uint32_t a = (uint32_t)(key2 >> nb), b = (uint32_t)(key2 & nmask);
         const PackedEdge ed = E[p];
-        const uint32_t side_min = ed.src == a ? 0u : 1u;  // record side of the min endpoint
+        const uint32_t dir_min = ed.src == a ? 0u : 1u;  // 0: min -> max
         const bool first = k == 0 || (packed ? pkeys[k - 1] >> pbits : pkeys[k - 1]) != key2;
         const bool last = k == m - 1 || (packed ? pkeys[k + 1] >> pbits : pkeys[k + 1]) != key2;
-        const uint2 qq = reinterpret_cast<const uint2*>(rec2s)[p];  // records 2p, 2p+1
         P_t[k] = ed.t;
         P_ord[k] = perm ? perm[p] : p;
+        P_min[k] = a;
         P_max[k] = b;
-        P_w[k] = (side_min << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u);
-        P_qmin[k] = side_min ? qq.y : qq.x;
-        P_qmax[k] = side_min ? qq.x : qq.y;
+        P_w[k] = (dir_min << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u);
     }
 }
 
-__global__ void s_pidx_kernel(const uint32_t* __restrict__ qmin, const uint32_t* __restrict__ qmax,
-                              uint64_t m, uint32_t* __restrict__ S_pidx) {
+// S -> P index for the per-center items API: each P record finds its two S
+// positions by binary search of (t, ordinal) in its endpoints' sequences.
+__device__ __forceinline__ uint32_t s_locate(const int64_t* __restrict__ S_t,
+                                             const uint32_t* __restrict__ S_ord, uint32_t lo,
+                                             uint32_t hi, int64_t t, uint32_t ord) {
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const int64_t tm = S_t[mid];
+        if (tm < t || (tm == t && (S_ord[mid] & kNodeMask) < ord)) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void s_pidx_kernel(const int64_t* __restrict__ P_t, const uint32_t* __restrict__ P_ord,
+                              const uint32_t* __restrict__ P_min, const uint32_t* __restrict__ P_max,
+                              const int64_t* __restrict__ S_t, const uint32_t* __restrict__ S_ord,
+                              const uint32_t* __restrict__ off, uint64_t m,
+                              uint32_t* __restrict__ S_pidx) {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        S_pidx[qmin[k]] = (uint32_t)k;
-        S_pidx[qmax[k]] = (uint32_t)k;
+        const int64_t t = P_t[k];
+        const uint32_t o = P_ord[k], a = P_min[k], b = P_max[k];
+        S_pidx[s_locate(S_t, S_ord, off[a], off[a + 1], t, o)] = (uint32_t)k;
+        S_pidx[s_locate(S_t, S_ord, off[b], off[b + 1], t, o)] = (uint32_t)k;
     }
 }
 
@@ -293,8 +305,7 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     g.P_ord = dalloc<uint32_t>(m, s);
     g.P_max = dalloc<uint32_t>(m, s);
     g.P_w = dalloc<uint32_t>(m, s);
-    g.P_qmin = dalloc<uint32_t>(m, s);
-    g.P_qmax = dalloc<uint32_t>(m, s);
+    g.P_min = dalloc<uint32_t>(m, s);
 
     if (m == 0) {
         TM_CUDA(cudaMemsetAsync(g.off, 0, (n + 1) * sizeof(uint32_t), s));
@@ -337,14 +348,13 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     {
         uint64_t* nk0 = dalloc<uint64_t>(R + kSortPad, s);
         uint64_t* nk1 = dalloc<uint64_t>(R + kSortPad, s);
-        uint32_t* rec2s = dalloc<uint32_t>(R, s);
         PackedEdge* E = dalloc<PackedEdge>(m, s);
         TM_LAUNCH("pack_edges", s, pack_edges_kernel, grid_for(m), 256, 0, perm, d_src, d_dst, d_t, m, E,
                   nk0);
         radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s);
         TM_LAUNCH("offsets", s, offsets_from_keys_kernel, grid_for(R), 256, 0, nk0, R, n, g.off);
         TM_LAUNCH("gather_s", s, gather_s_kernel, grid_for(R), 256, 0, perm, E, nk0, R, g.off, g.S_t,
-                  g.S_nbr, g.S_ord, g.S_node, rec2s);
+                  g.S_nbr, g.S_ord, g.S_node);
         dfree(nk0, s);
         dfree(nk1, s);
         exclusive_scan<uint32_t>(OutwardLoad{g.S_nbr}, R, g.S_pg, s);
@@ -361,14 +371,13 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         if (packed) radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, pbits, pbits + 2 * nb, s);
         else radix_sort<uint64_t>(pk0, pv0, pk1, pv1, m, 0, 2 * nb, s);
         TM_LAUNCH("gather_p", s, gather_p_kernel, grid_for(m), 256, 0, pk0, pv0, m, nb, pbits, packed,
-                  perm, E, rec2s, g.P_t, g.P_ord, g.P_max, g.P_w, g.P_qmin, g.P_qmax);
+                  perm, E, g.P_t, g.P_ord, g.P_min, g.P_max, g.P_w);
         TM_LAUNCH("pair_offsets", s, pair_offsets_kernel, grid_for(m), 256, 0, pk0, m, n,
                   packed ? pbits + nb : nb, g.pofs);
         dfree(pk0, s);
         dfree(pk1, s);
         dfree(pv0, s);
         dfree(pv1, s);
-        dfree(rec2s, s);
         dfree(E, s);
     }
     if (perm) dfree(perm, s);
@@ -406,8 +415,8 @@ void build_s_pidx(DeviceGraph& g) {
         return;
     }
     g.S_pidx = dalloc<uint32_t>(g.R, g.stream);
-    TM_LAUNCH("s_pidx", g.stream, s_pidx_kernel, grid_for(g.m), 256, 0, g.P_qmin, g.P_qmax, g.m,
-              g.S_pidx);
+    TM_LAUNCH("s_pidx", g.stream, s_pidx_kernel, grid_for(g.m), 256, 0, g.P_t, g.P_ord, g.P_min,
+              g.P_max, g.S_t, g.S_ord, g.off, g.m, g.S_pidx);
 }
 
 void free_graph(DeviceGraph& g) {
@@ -415,7 +424,7 @@ void free_graph(DeviceGraph& g) {
     dfree(g.S_t, s); dfree(g.S_nbr, s); dfree(g.S_ord, s); dfree(g.S_node, s);
     dfree(g.S_pg, s); dfree(g.S_pidx, s); dfree(g.off, s);
     dfree(g.P_t, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
-    dfree(g.P_qmin, s); dfree(g.P_qmax, s); dfree(g.pofs, s);
+    dfree(g.P_min, s); dfree(g.pofs, s);
     for (auto& f : g.fwd) {
         dfree(f.t, s); dfree(f.nbr, s); dfree(f.ord, s); dfree(f.node, s); dfree(f.off, s);
         f.valid = false;

@@ -14,9 +14,8 @@
 //      {u, v} is also u's and v's same-neighbour run, shared by both ends)
 //     P_t[m]    int64
 //     P_ord[m]  u32
-//     P_max[m]  u32    larger endpoint (the block of the smaller one is pofs)
+//     P_min[m], P_max[m]  u32  endpoints (the block of the smaller one is pofs)
 //     P_w[m]    u32    dir_rel_min << 31 | first << 30 | last << 29
-//     P_qmin[m], P_qmax[m]  u32  S positions of the record at min / max
 //     pofs[n+1] u32    first P position whose min endpoint is u
 //   F (forward-oriented sequences for the triangle pass, one per orientation)
 #pragma once
@@ -105,8 +104,7 @@ struct DeviceGraph {
     uint32_t* P_ord = nullptr;
     uint32_t* P_max = nullptr;
     uint32_t* P_w = nullptr;
-    uint32_t* P_qmin = nullptr;
-    uint32_t* P_qmax = nullptr;
+    uint32_t* P_min = nullptr;
     uint32_t* pofs = nullptr;
 
     Forward fwd[2];
@@ -130,15 +128,14 @@ struct PView {
     const uint32_t* ord;
     const uint32_t* max;
     const uint32_t* w;
-    const uint32_t* qmin;
-    const uint32_t* qmax;
+    const uint32_t* min;
     const uint32_t* pofs;
 };
 inline SView sview(const DeviceGraph& g) {
     return {g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_pg, g.S_pidx, g.off};
 }
 inline PView pview(const DeviceGraph& g) {
-    return {g.P_t, g.P_ord, g.P_max, g.P_w, g.P_qmin, g.P_qmax, g.pofs};
+    return {g.P_t, g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs};
 }
 
 // ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------
@@ -148,9 +145,9 @@ void free_graph(DeviceGraph& g);
 void build_forward(DeviceGraph& g, int mode);
 void build_s_pidx(DeviceGraph& g);
 
-// raw star sums (32 u64: Pair[8], C[8], B[8], A[8]) for the centers whose
-// S positions are [q_begin, q_end), added into d_out.
-void star_full(const DeviceGraph& g, int64_t delta, uint32_t q_begin, uint32_t q_end,
+// raw star sums (32 u64: Pair[8], C[8], B[8], A[8]) for the centers
+// [c_begin, c_end), added into d_out.
+void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end,
                uint64_t* d_out, uint64_t* d_stats);
 void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
                 const uint64_t* d_begin, const uint64_t* d_end, const uint64_t* d_item_off,

@@ -82,19 +82,66 @@ __device__ __forceinline__ void add_d1(const Sink& sink, int base, uint32_t d1, 
 }
 
 // Side of center u in the unordered pair {u, other}: 0 when u is the smaller
-// id (P_qmin / dir_rel_min describe it), 1 when u is the larger one.
+// id (P_min / dir_rel_min describe it), 1 when u is the larger one.
 __device__ __forceinline__ uint32_t side_of(uint32_t u, uint32_t other) { return u > other ? 1u : 0u; }
 
-// first-edge role of S position q with P index k (center u, S range
-// [start, end)): Pair, A, B.
+// (t, ordinal) strict order between S record p and (t, ord); S_ord carries
+// the orientation bit on top, masked here.
+__device__ __forceinline__ bool s_before(const SView& S, uint32_t p, int64_t t, uint32_t ord) {
+    const int64_t tp = S.t[p];
+    return tp < t || (tp == t && (S.ord[p] & kNodeMask) < ord);
+}
+
+// first position in [lo, hi) not before (t, ord): the record itself when it
+// lies in the range.  gallop_locate probes upward from lo, gallop_locate_back
+// downward from hi (members of a group are met in order, close to the last).
+__device__ __forceinline__ uint32_t gallop_locate(const SView& S, uint32_t lo, uint32_t hi, int64_t t,
+                                                  uint32_t ord) {
+    uint32_t a = lo, b = hi, span = 1;
+    while (true) {
+        const uint64_t probe = (uint64_t)a + span - 1;
+        if (probe >= hi) break;
+        if (!s_before(S, (uint32_t)probe, t, ord)) {
+            b = (uint32_t)probe;
+            break;
+        }
+        a = (uint32_t)probe + 1;
+        span <<= 1;
+    }
+    while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (s_before(S, mid, t, ord)) a = mid + 1; else b = mid;
+    }
+    return a;
+}
+__device__ __forceinline__ uint32_t gallop_locate_back(const SView& S, uint32_t lo, uint32_t hi,
+                                                       int64_t t, uint32_t ord) {
+    uint32_t a = lo, b = hi, span = 1;
+    while (true) {
+        if (b - lo < span) break;
+        const uint32_t probe = b - span;
+        if (s_before(S, probe, t, ord)) {
+            a = probe + 1;
+            break;
+        }
+        b = probe;
+        span <<= 1;
+    }
+    while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (s_before(S, mid, t, ord)) a = mid + 1; else b = mid;
+    }
+    return a;
+}
+
+// first-edge role of S position q = P record k seen from center u (side 0:
+// u is the pair's smaller id), S range [start, end): Pair, A, B.
 template <typename Sink>
 __device__ __forceinline__ void first_role(const SView& S, const PView& P, uint32_t q, uint32_t k,
-                                           uint32_t start, uint32_t end, int64_t delta,
-                                           const Sink& acc) {
+                                           uint32_t side, uint32_t start, uint32_t end,
+                                           int64_t delta, const Sink& acc) {
     const int64_t ta = S.t[q];
-    const uint32_t nq = S.nbr[q];
-    const uint32_t da = nq >> 31;
-    const uint32_t side = side_of(S.node[q], nq & kNodeMask);
+    const uint32_t da = S.nbr[q] >> 31;
     const int64_t lim = sat_add(ta, delta);
     if (P.w[k] & kPLast) return;
     if (P.t[k + 1] > lim) return;  // no same-neighbour record in the window
@@ -104,16 +151,17 @@ __device__ __forceinline__ void first_role(const SView& S, const PView& P, uint3
     const uint64_t pe_o = S.pg[e] - base, pe_i = (uint64_t)(e - start) - pe_o;
     const uint64_t pa_o = (uint64_t)(S.pg[q] - base) + (da ? 0u : 1u);
     const uint64_t pa_i = (uint64_t)(q - start + 1) - pa_o;
-    const uint32_t* __restrict__ qside = side ? P.qmax : P.qmin;
 
     uint64_t n0 = 0, n1 = 0;
     uint64_t A00 = 0, A01 = 0, A10 = 0, A11 = 0;   // A[d2][d3]: sum [dir_b=d2] P_d3(b+1)
     uint64_t B00 = 0, B01 = 0, B10 = 0, B11 = 0;   // B[d3][d2]: sum [dir_c=d3] P_d2(c)
     uint64_t P00 = 0, P01 = 0, P10 = 0, P11 = 0;   // Pair[d2][d3]
+    uint32_t qb = q;
     for (++k;; ++k) {
-        if (P.t[k] > lim) break;
+        const int64_t tb = P.t[k];
+        if (tb > lim) break;
         const uint32_t w = P.w[k];
-        const uint32_t qb = qside[k];
+        qb = gallop_locate(S, qb + 1, e, tb, P.ord[k]);  // member's place in S_u
         const uint64_t pos = qb - start;
         const uint64_t pb_o = S.pg[qb] - base;
         const uint64_t pb_i = pos - pb_o;
@@ -146,31 +194,35 @@ __device__ __forceinline__ void first_role(const SView& S, const PView& P, uint3
     add_d1(acc, 16, da, b);
 }
 
-// third-edge role of S position q: the Star-I pair term C.
-// rb/re: first-edge range (local), clipped; full run passes rb=0, re=s.
+// third-edge role of S position q = P record k seen from center u: the
+// Star-I pair term C.  rb/re: first-edge range (local), clipped; the full run
+// passes rb = 0, re = s.
 template <typename Sink>
 __device__ __forceinline__ void third_role(const SView& S, const PView& P, uint32_t q, uint32_t k,
-                                           uint32_t start, int64_t delta, uint32_t rb,
-                                           uint32_t re, const Sink& acc) {
+                                           uint32_t side, uint32_t start, int64_t delta,
+                                           uint32_t rb, uint32_t re, const Sink& acc) {
     if (P.w[k] & kPFirst) return;
     const int64_t tc = S.t[q];
     const int64_t lo_lim = sat_sub(tc, delta);
     // quick reject: previous same-neighbour record already before the window
     if (P.t[k - 1] < lo_lim) return;
-    const uint32_t nq = S.nbr[q];
-    const uint32_t dc = nq >> 31;
-    const uint32_t side = side_of(S.node[q], nq & kNodeMask);
-    const uint32_t* __restrict__ qside = side ? P.qmax : P.qmin;
+    const uint32_t dc = S.nbr[q] >> 31;
     const uint32_t lo = gallop_lower_back(S.t, start, q, lo_lim);
     const uint32_t L = max(lo, start + rb);
+    if (L >= q) return;
     const uint32_t pl = S.pg[L];
+    const int64_t tL = S.t[L];
+    const uint32_t oL = S.ord[L] & kNodeMask;
     const uint32_t hiq = start + re;
     uint64_t x0 = 0, x1 = 0, y0 = 0, y1 = 0;  // x: d1 = out, y: d1 = in ; index d2
+    uint32_t qb = q;
     for (--k;; --k) {
+        const int64_t tb = P.t[k];
+        const uint32_t ob = P.ord[k];
+        if (tb < tL || (tb == tL && ob <= oL)) break;  // member at or before position L
         const uint32_t w = P.w[k];
-        const uint32_t posb = qside[k];
-        if (posb <= L) break;
-        const uint32_t mhi = min(posb, hiq);
+        qb = gallop_locate_back(S, L + 1, qb, tb, ob);
+        const uint32_t mhi = min(qb, hiq);
         if (mhi > L) {
             const uint64_t x = (uint64_t)(S.pg[mhi] - pl);
             const uint64_t y = (uint64_t)(mhi - L) - x;
@@ -189,41 +241,42 @@ __device__ __forceinline__ void third_role(const SView& S, const PView& P, uint3
 // edge only if the next record of its pair group is inside its window, and as
 // a third edge only if the previous one is (otherwise every term of
 // first_role / third_role is zero).  Both endpoints share the group order, so
-// a surviving record yields candidates at both of its centers; the S
-// positions of those inside the center partition [qlo, qhi) go to the lists.
+// a surviving record yields a candidate at each of its centers inside the
+// center partition [cb, ce); entries are 2k + side.
 __global__ void __launch_bounds__(256) star_filter_kernel(PView P, int64_t delta, uint64_t m,
-                                                          uint32_t qlo, uint32_t qhi,
-                                                          uint64_t* __restrict__ first_list,
-                                                          uint64_t* __restrict__ third_list,
+                                                          uint32_t cb, uint32_t ce,
+                                                          uint32_t* __restrict__ first_list,
+                                                          uint32_t* __restrict__ third_list,
                                                           uint32_t* __restrict__ counters) {
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = base + threadIdx.x;
-        bool f = false, th = false;
-        uint32_t qa = 0, qb = 0;
+        bool f = false, th = false, ina = false, inb = false;
         if (k < m) {
             const uint32_t w = P.w[k];
             const int64_t t = P.t[k];
             f = !(w & kPLast) && P.t[k + 1] <= sat_add(t, delta);
             th = !(w & kPFirst) && P.t[k - 1] >= sat_sub(t, delta);
             if (f || th) {
-                qa = P.qmin[k];
-                qb = P.qmax[k];
+                const uint32_t a = P.min[k], b = P.max[k];
+                ina = a >= cb && a < ce;
+                inb = b >= cb && b < ce;
             }
         }
-        const bool ina = qa >= qlo && qa < qhi, inb = qb >= qlo && qb < qhi;
-        const uint64_t ea = (k << 32) | qa, eb = (k << 32) | qb;
-        warp_append64(f && ina, ea, first_list, counters);
-        warp_append64(f && inb, eb, first_list, counters);
-        warp_append64(th && ina, ea, third_list, counters + 1);
-        warp_append64(th && inb, eb, third_list, counters + 1);
+        const uint32_t e0 = (uint32_t)(2 * k), e1 = (uint32_t)(2 * k + 1);
+        warp_append(f && ina, e0, first_list, counters);
+        warp_append(f && inb, e1, first_list, counters);
+        warp_append(th && ina, e0, third_list, counters + 1);
+        warp_append(th && inb, e1, third_list, counters + 1);
     }
 }
 
 // Work: the full first_role / third_role sums for the surviving records.
+// The record's own S position is found by binary search of (t, ordinal) in
+// its center's time-ordered sequence.
 __global__ void __launch_bounds__(256) star_work_kernel(SView S, PView P, int64_t delta,
-                                                        const uint64_t* __restrict__ first_list,
-                                                        const uint64_t* __restrict__ third_list,
+                                                        const uint32_t* __restrict__ first_list,
+                                                        const uint32_t* __restrict__ third_list,
                                                         const uint32_t* __restrict__ counters,
                                                         uint64_t* __restrict__ out,
                                                         uint64_t* __restrict__ stats) {
@@ -239,12 +292,13 @@ __global__ void __launch_bounds__(256) star_work_kernel(SView S, PView P, int64_
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (uint64_t)nf + nt;
          idx += (uint64_t)gridDim.x * blockDim.x) {
         const bool first = idx < nf;
-        const uint64_t e = first ? first_list[idx] : third_list[idx - nf];
-        const uint32_t q = (uint32_t)e, k = (uint32_t)(e >> 32);
-        const uint32_t u = S.node[q];
+        const uint32_t e = first ? first_list[idx] : third_list[idx - nf];
+        const uint32_t k = e >> 1, side = e & 1u;
+        const uint32_t u = side ? P.max[k] : P.min[k];
         const uint32_t start = S.off[u], end = S.off[u + 1];
-        if (first) first_role(S, P, q, k, start, end, delta, acc);
-        else third_role(S, P, q, k, start, delta, 0u, end - start, acc);
+        const uint32_t q = gallop_locate(S, start, end, P.t[k], P.ord[k]);
+        if (first) first_role(S, P, q, k, side, start, end, delta, acc);
+        else third_role(S, P, q, k, side, start, delta, 0u, end - start, acc);
     }
     __syncthreads();
     flush_cells(cells, 32, out);
@@ -275,7 +329,7 @@ __global__ void __launch_bounds__(256) star_items_kernel(
             const uint32_t u = nodes[it];
             const uint32_t start = S.off[u], end = S.off[u + 1];
             const uint32_t q = start + (uint32_t)begin[it] + (uint32_t)(idx - first_off[it]);
-            first_role(S, P, q, S.pidx[q], start, end, delta,
+            first_role(S, P, q, S.pidx[q], side_of(u, S.nbr[q] & kNodeMask), start, end, delta,
                        GlobalSink{(unsigned long long*)out + (uint64_t)it * 32});
         } else {
             const uint64_t j = idx - total_first;
@@ -286,7 +340,7 @@ __global__ void __launch_bounds__(256) star_items_kernel(
             const uint32_t rb = (uint32_t)begin[it];
             const uint32_t re = (uint32_t)(endr[it] < (uint64_t)s ? endr[it] : (uint64_t)s);
             const uint32_t q = start + rb + 1 + (uint32_t)(j - third_off[it]);
-            third_role(S, P, q, S.pidx[q], start, delta, rb, re,
+            third_role(S, P, q, S.pidx[q], side_of(u, S.nbr[q] & kNodeMask), start, delta, rb, re,
                        GlobalSink{(unsigned long long*)out + (uint64_t)it * 32});
         }
     }
@@ -294,19 +348,19 @@ __global__ void __launch_bounds__(256) star_items_kernel(
 
 }  // namespace
 
-void star_full(const DeviceGraph& g, int64_t delta, uint32_t q_begin, uint32_t q_end,
+void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end,
                uint64_t* d_out, uint64_t* d_stats) {
-    if (q_end <= q_begin || g.m == 0) return;
+    if (c_end <= c_begin || g.m == 0) return;
     cudaStream_t st = g.stream;
-    const uint64_t work = q_end - q_begin;
     const uint64_t cap = (uint64_t)sm_count() * 8;
     uint64_t grid = (g.m + 255) / 256;
     if (grid > cap) grid = cap;
-    uint64_t* lists = dalloc<uint64_t>(2 * work + 1, st);
-    uint32_t* counters = reinterpret_cast<uint32_t*>(lists + 2 * work);
+    const uint64_t work = 2 * g.m;
+    uint32_t* lists = dalloc<uint32_t>(2 * work + 2, st);
+    uint32_t* counters = lists + 2 * work;
     TM_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), st));
     TM_LAUNCH("star_filter", st, star_filter_kernel, (unsigned)grid, 256, 0, pview(g), delta, g.m,
-              q_begin, q_end, lists, lists + work, counters);
+              c_begin, c_end, lists, lists + work, counters);
     TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), delta, lists,
               lists + work, counters, d_out, d_stats);
     dfree(lists, st);
