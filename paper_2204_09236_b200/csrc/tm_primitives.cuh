@@ -5,14 +5,14 @@
 // CSR fill does (graph.cpp:37-41, indexes.cpp:7-26): keys are stable-sorted,
 // and records enter the sort in (t, ordinal) order, so ties keep input order.
 //
-// Both primitives are single-pass over HBM per digit / per scan:
-//  * scan: one kernel, tiles claim ids from an atomic counter and chain their
-//    prefixes with decoupled look-back (aggregate / inclusive status words);
-//  * sort ("onesweep"): one histogram kernel reads the keys once for all digit
-//    passes; each pass is then one kernel that ranks its 4096-key tile with
-//    per-warp __match_any_sync (stable), publishes per-digit tile counts,
-//    looks back across earlier tiles per digit, reorders the tile in shared
-//    memory and writes each digit run as one burst.
+// Scan: chunked reduce-then-scan (one contiguous chunk per block, no
+// inter-block waiting).  Sort: LSD, 8-bit digits, 4096-key tiles; per pass an
+// upsweep (per-tile digit counts), a row scan (one block per digit) and a
+// persistent downsweep that streams the next tile into shared memory with TMA
+// (cp.async.bulk + mbarrier) while it ranks the current one with per-warp
+// __match_any_sync (stable), reorders it in shared memory and writes each
+// digit run as one burst.  Keys carry their payload in the low bits when it
+// fits, so most sorts are keys-only.
 #pragma once
 
 #include <algorithm>
@@ -22,21 +22,6 @@
 #include "tm_internal.cuh"
 
 namespace tmb {
-
-// ---------------------------------------------------------------------------
-// decoupled look-back status words: 2-bit flag | 62-bit value
-constexpr uint64_t kStAgg = 1ull << 62;
-constexpr uint64_t kStInc = 2ull << 62;
-constexpr uint64_t kStVal = (1ull << 62) - 1;
-
-__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 template <typename T>
 __device__ __forceinline__ T warp_inclusive_scan(T v) {
@@ -74,40 +59,6 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* total) {
     T r = warp_tot[w] + inc - v;
     __syncthreads();
     return r;
-}
-
-// warp-cooperative look-back: sum of predecessors of `tile` in status[idx(p)]
-template <typename Idx>
-__device__ __forceinline__ uint64_t warp_lookback(const uint64_t* status, int64_t tile, Idx idx) {
-    const int lane = threadIdx.x & 31;
-    uint64_t acc = 0;
-    int64_t p = tile - 1;
-    while (p >= 0) {
-        const int64_t q = p - lane;
-        uint64_t s = kStInc;  // lanes past tile 0 behave as zero-valued inclusive
-        if (q >= 0) {
-            do {
-                s = ld_status(status + idx(q));
-            } while ((s >> 62) == 0);
-        }
-        const unsigned inc_mask = __ballot_sync(0xffffffffu, (s >> 62) == 2);
-        const int first = inc_mask ? __ffs(inc_mask) - 1 : 32;
-        uint64_t v = (lane <= first && q >= 0) ? (s & kStVal) : 0;
-        acc += warp_sum(v);
-        if (inc_mask) break;
-        p -= 32;
-    }
-    return acc;
-}
-
-// L2 eviction-priority hints: keep scatter targets resident, stream the rest
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ void st_keep_u32(uint32_t* p, uint32_t v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
 }
 
 // warp-aggregated append of `value` to list when pred holds (whole warp calls)
@@ -482,21 +433,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
-// lanes of the warp holding the same 8-bit digit (invalid lanes pass 256 and
-// get no peers among valid lanes): bit-sliced ballots instead of MATCH.ANY
-template <bool kBallot>
-__device__ __forceinline__ unsigned digit_peers(uint32_t d) {
-    if (!kBallot) return __match_any_sync(0xffffffffu, d);
-    unsigned peers = 0xffffffffu;
-#pragma unroll
-    for (int b = 0; b < 9; ++b) {
-        const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        peers &= ((d >> b) & 1u) ? bal : ~bal;
-    }
-    return peers;
-}
-
-template <typename K, bool kVals, bool kBallot = true>
+template <typename K, bool kVals>
 __global__ void __launch_bounds__(512, 2) radix_downsweep_tma(const K* __restrict__ kin,
                                                               const uint32_t* __restrict__ vin,
                                                               K* __restrict__ kout,
@@ -557,7 +494,7 @@ __global__ void __launch_bounds__(512, 2) radix_downsweep_tma(const K* __restric
             const uint32_t i = w * (ITEMS * 32) + r * 32 + lane;
             const bool valid = i < tile_n;
             const uint32_t d = valid ? ((uint32_t)(sk[i] >> shift) & 255u) : 256u;
-            const unsigned peers = digit_peers<kBallot>(d);
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
             const uint32_t prev = valid ? wcnt[w][d] : 0u;
             rank[r] = prev + __popc(peers & lt);
             __syncwarp();
@@ -610,15 +547,6 @@ constexpr int kRsItems = 8;
 
 constexpr uint64_t kSortPad = 4;
 
-inline bool use_ballot_rank() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TM_RANK");
-        v = (e && e[0] == 'm') ? 0 : 1;  // default: ballot ranking
-    }
-    return v == 1;
-}
-
 inline bool use_tma_sort() {
     static int v = -1;
     if (v < 0) {
@@ -644,16 +572,10 @@ void radix_sort(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, ui
     const size_t tma_smem = 3 * smem;
     static bool attr_set = false;
     if (!attr_set) {
-        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, true, true>,
+        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(3 * TILE * (sizeof(K) + sizeof(uint32_t)))));
-        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, false, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(3 * TILE * sizeof(K))));
-        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, true, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(3 * TILE * (sizeof(K) + sizeof(uint32_t)))));
-        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, false, false>,
+        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(3 * TILE * sizeof(K))));
         TM_CUDA(cudaFuncSetAttribute(radix_downsweep<K, true, kRsBlock, kRsItems>,
@@ -675,24 +597,15 @@ void radix_sort(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, ui
         TM_LAUNCH("radix_scan", s, radix_scan_counts, kRadix, 256, 0, counts, ntiles, offs, totals);
         const bool tma = use_tma_sort();
         const unsigned pgrid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * 2);
-        const bool ballot = use_ballot_rank();
         if (with_vals && tma) {
-            if (ballot)
-                TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, true, true>), pgrid, 512, tma_smem,
-                          keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
-            else
-                TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, true, false>), pgrid, 512, tma_smem,
-                          keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
+            TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, true>), pgrid, 512, tma_smem, keys,
+                      vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
             uint32_t* tv = vals;
             vals = vals_alt;
             vals_alt = tv;
         } else if (tma) {
-            if (ballot)
-                TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, false, true>), pgrid, 512, tma_smem,
-                          keys, nullptr, keys_alt, nullptr, n, shift, offs, ntiles, totals);
-            else
-                TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, false, false>), pgrid, 512,
-                          tma_smem, keys, nullptr, keys_alt, nullptr, n, shift, offs, ntiles, totals);
+            TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, false>), pgrid, 512, tma_smem, keys,
+                      nullptr, keys_alt, nullptr, n, shift, offs, ntiles, totals);
         } else if (with_vals) {
             TM_LAUNCH("radix_downsweep", s, (radix_downsweep<K, true, kRsBlock, kRsItems>), ntiles,
                       kRsBlock, smem, keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
