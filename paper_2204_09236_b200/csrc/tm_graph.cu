@@ -105,26 +105,37 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedE
                                 const uint64_t* __restrict__ skeys, uint64_t R,
                                 const uint32_t* __restrict__ off,
                                 int64_t* __restrict__ S_t, uint32_t* __restrict__ S_nbr,
-                                uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node) {
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
-         q += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t key = __ldcs(skeys + q);
-        const uint32_t r = (uint32_t)key;
-        const uint32_t p = r >> 1, side = r & 1u;
-        const PackedEdge e = E[p];
-        __stcs(S_t + q, e.t);
-        const uint32_t u = (uint32_t)(key >> 32), x = side ? e.src : e.dst;
-        // degree-rank orientation of the triangle pass: forward iff (deg, id) of the
-        // neighbour exceeds the center's; kept in the spare top bit of S_ord
-        const uint32_t du = off[u + 1] - off[u], dx = off[x + 1] - off[x];
-        const uint32_t fwd = (dx > du || (dx == du && x > u)) ? kDirBit : 0u;
-        __stcs(S_ord + q, (perm ? perm[p] : p) | fwd);
-        __stcs(S_node + q, u);
-        __stcs(S_nbr + q, x | (side << 31));
+                                uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
+                                uint32_t* __restrict__ omask, uint32_t* __restrict__ fmask) {
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = base + threadIdx.x;
+        uint32_t out = 0, fwd = 0;
+        if (q < R) {
+            const uint64_t key = __ldcs(skeys + q);
+            const uint32_t r = (uint32_t)key;
+            const uint32_t p = r >> 1, side = r & 1u;
+            const PackedEdge e = E[p];
+            const uint32_t u = (uint32_t)(key >> 32), x = side ? e.src : e.dst;
+            // degree-rank orientation of the triangle pass: forward iff (deg, id) of the
+            // neighbour exceeds the center's; kept in the spare top bit of S_ord
+            const uint32_t du = off[u + 1] - off[u], dx = off[x + 1] - off[x];
+            fwd = (dx > du || (dx == du && x > u)) ? 1u : 0u;
+            out = side ^ 1u;
+            __stcs(S_t + q, e.t);
+            __stcs(S_ord + q, (perm ? perm[p] : p) | (fwd << 31));
+            __stcs(S_node + q, u);
+            __stcs(S_nbr + q, x | (side << 31));
+        }
+        const unsigned ob = __ballot_sync(0xffffffffu, out), fb = __ballot_sync(0xffffffffu, fwd);
+        if ((threadIdx.x & 31) == 0 && q < R) {
+            omask[q >> 5] = ob;
+            fmask[q >> 5] = fb;
+        }
     }
 }
 
-// off[x] from the sorted node keys (node << 32 | record)
+// off[x] from the sorted node keys (node << 32 | record): boundary fill
 __global__ void offsets_from_keys_kernel(const uint64_t* __restrict__ keys, uint64_t R, uint64_t n,
                                          uint32_t* __restrict__ off) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
@@ -219,48 +230,54 @@ __global__ void pair_offsets_kernel(const uint64_t* __restrict__ pkeys, uint64_t
     }
 }
 
-struct OutwardLoad {
-    const uint32_t* nbr;
-    __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
-        return (nbr[i] & kDirBit) ? 0u : 1u;
-    }
+struct PopcLoad {
+    const uint32_t* mask;
+    __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return __popc(mask[i]); }
 };
-// forward(u -> x): mode 0 degree rank (deg, id), mode 1 node index
-struct ForwardFlag {
-    const uint32_t* node;
-    const uint32_t* nbr;
-    const uint32_t* off;
-    int mode;
-    const uint32_t* ord;
-    __device__ __forceinline__ uint32_t operator()(uint64_t q) const {
-        if (mode == 0) return ord[q] >> 31;  // degree orientation bit set by gather_s
-        return (nbr[q] & kNodeMask) > node[q] ? 1u : 0u;
+// forward(u -> x) bitmask for the node-index orientation (removal mode); the
+// degree orientation's mask is written by gather_s
+__global__ void index_forward_mask_kernel(const uint32_t* __restrict__ node,
+                                          const uint32_t* __restrict__ nbr, uint64_t R,
+                                          uint32_t* __restrict__ fmask) {
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = base + threadIdx.x;
+        const uint32_t f = q < R && (nbr[q] & kNodeMask) > node[q] ? 1u : 0u;
+        const unsigned b = __ballot_sync(0xffffffffu, f);
+        if ((threadIdx.x & 31) == 0 && q < R) fmask[q >> 5] = b;
     }
-};
+}
 
-__global__ void forward_scatter_kernel(ForwardFlag flag, const uint32_t* __restrict__ fscan,
-                                       uint64_t R, const int64_t* __restrict__ S_t,
-                                       const uint32_t* __restrict__ S_ord, int64_t* __restrict__ F_t,
+// F position of forward record q = fpref[q/32] + popc(fmask[q/32] & below)
+__global__ void forward_scatter_kernel(const uint32_t* __restrict__ fmask,
+                                       const uint32_t* __restrict__ fpref, uint64_t R,
+                                       const int64_t* __restrict__ S_t,
+                                       const uint32_t* __restrict__ S_nbr,
+                                       const uint32_t* __restrict__ S_ord,
+                                       const uint32_t* __restrict__ S_node, int64_t* __restrict__ F_t,
                                        uint32_t* __restrict__ F_nbr, uint32_t* __restrict__ F_ord,
                                        uint32_t* __restrict__ F_node) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
          q += (uint64_t)gridDim.x * blockDim.x) {
-        if (flag(q)) {
-            const uint32_t j = fscan[q];
+        const uint32_t word = fmask[q >> 5], bit = 1u << (q & 31);
+        if (word & bit) {
+            const uint32_t j = fpref[q >> 5] + __popc(word & (bit - 1u));
             F_t[j] = S_t[q];
-            F_nbr[j] = flag.nbr[q];
+            F_nbr[j] = S_nbr[q];
             F_ord[j] = S_ord[q] & kNodeMask;
-            F_node[j] = flag.node[q];
+            F_node[j] = S_node[q];
         }
     }
 }
 
-__global__ void forward_off_kernel(const uint32_t* __restrict__ off,
-                                   const uint32_t* __restrict__ fscan, uint64_t n,
+__global__ void forward_off_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ fmask,
+                                   const uint32_t* __restrict__ fpref, uint64_t n,
                                    uint32_t* __restrict__ F_off) {
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= n;
-         u += (uint64_t)gridDim.x * blockDim.x)
-        F_off[u] = fscan[off[u]];
+         u += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t q = off[u];
+        F_off[u] = fpref[q >> 5] + __popc(fmask[q >> 5] & ((1u << (q & 31)) - 1u));
+    }
 }
 
 unsigned grid_for(uint64_t work, int block = 256) {
@@ -300,7 +317,10 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     g.S_nbr = dalloc<uint32_t>(R, s);
     g.S_ord = dalloc<uint32_t>(R, s);
     g.S_node = dalloc<uint32_t>(R, s);
-    g.S_pg = dalloc<uint32_t>(R + 1, s);
+    const uint64_t nw = R / 32 + 1;  // mask words (+1: a zero word past the end)
+    g.S_omask = dalloc<uint32_t>(nw, s);
+    g.S_opref = dalloc<uint32_t>(nw + 1, s);
+    g.S_fmask = dalloc<uint32_t>(nw, s);
     g.P_t = dalloc<int64_t>(m, s);
     g.P_ord = dalloc<uint32_t>(m, s);
     g.P_max = dalloc<uint32_t>(m, s);
@@ -310,7 +330,8 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     if (m == 0) {
         TM_CUDA(cudaMemsetAsync(g.off, 0, (n + 1) * sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.pofs, 0, (n + 1) * sizeof(uint32_t), s));
-        TM_CUDA(cudaMemsetAsync(g.S_pg, 0, sizeof(uint32_t), s));
+        TM_CUDA(cudaMemsetAsync(g.S_omask, 0, nw * sizeof(uint32_t), s));
+        TM_CUDA(cudaMemsetAsync(g.S_opref, 0, (nw + 1) * sizeof(uint32_t), s));
         g.max_degree = 0;
         return;
     }
@@ -353,11 +374,13 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
                   nk0);
         radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s);
         TM_LAUNCH("offsets", s, offsets_from_keys_kernel, grid_for(R), 256, 0, nk0, R, n, g.off);
+        TM_CUDA(cudaMemsetAsync(g.S_omask + (nw - 1), 0, sizeof(uint32_t), s));
+        TM_CUDA(cudaMemsetAsync(g.S_fmask + (nw - 1), 0, sizeof(uint32_t), s));
         TM_LAUNCH("gather_s", s, gather_s_kernel, grid_for(R), 256, 0, perm, E, nk0, R, g.off, g.S_t,
-                  g.S_nbr, g.S_ord, g.S_node);
+                  g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask);
         dfree(nk0, s);
         dfree(nk1, s);
-        exclusive_scan<uint32_t>(OutwardLoad{g.S_nbr}, R, g.S_pg, s);
+        exclusive_scan<uint32_t>(PopcLoad{g.S_omask}, nw, g.S_opref, s);
 
         // 3. P: stable sort of the edges by unordered pair {min, max}
         const int pbits = bit_width_u64(m - 1 ? m - 1 : 1);
@@ -396,16 +419,28 @@ void build_forward(DeviceGraph& g, int mode) {
     f.ord = dalloc<uint32_t>(g.m, s);
     f.node = dalloc<uint32_t>(g.m, s);
     f.off = dalloc<uint32_t>(g.n + 1, s);
-    uint32_t* fscan = dalloc<uint32_t>(R + 1, s);
-    ForwardFlag flag{g.S_node, g.S_nbr, g.off, mode, g.S_ord};
-    exclusive_scan<uint32_t>(flag, R, fscan, s);
-    if (R) {
-        TM_LAUNCH("forward_scatter", s, forward_scatter_kernel, grid_for(R), 256, 0, flag, fscan, R,
-                  g.S_t, g.S_ord, f.t, f.nbr, f.ord, f.node);
+    const uint64_t nw = R / 32 + 1;
+    uint32_t* fmask = g.S_fmask;
+    uint32_t* imask = nullptr;
+    if (mode == 1) {
+        imask = dalloc<uint32_t>(nw, s);
+        TM_CUDA(cudaMemsetAsync(imask + (nw - 1), 0, sizeof(uint32_t), s));
+        if (R) {
+            TM_LAUNCH("forward_mask", s, index_forward_mask_kernel, grid_for(R), 256, 0, g.S_node, g.S_nbr,
+                      R, imask);
+        }
+        fmask = imask;
     }
-    TM_LAUNCH("forward_off", s, forward_off_kernel, grid_for(g.n + 1), 256, 0, g.off, fscan, g.n,
+    uint32_t* fpref = dalloc<uint32_t>(nw + 1, s);
+    exclusive_scan<uint32_t>(PopcLoad{fmask}, nw, fpref, s);
+    if (R) {
+        TM_LAUNCH("forward_scatter", s, forward_scatter_kernel, grid_for(R), 256, 0, fmask, fpref, R, g.S_t,
+                  g.S_nbr, g.S_ord, g.S_node, f.t, f.nbr, f.ord, f.node);
+    }
+    TM_LAUNCH("forward_off", s, forward_off_kernel, grid_for(g.n + 1), 256, 0, g.off, fmask, fpref, g.n,
               f.off);
-    dfree(fscan, s);
+    dfree(fpref, s);
+    dfree(imask, s);
     f.valid = true;
 }
 
@@ -422,7 +457,8 @@ void build_s_pidx(DeviceGraph& g) {
 void free_graph(DeviceGraph& g) {
     cudaStream_t s = g.stream;
     dfree(g.S_t, s); dfree(g.S_nbr, s); dfree(g.S_ord, s); dfree(g.S_node, s);
-    dfree(g.S_pg, s); dfree(g.S_pidx, s); dfree(g.off, s);
+    dfree(g.S_omask, s); dfree(g.S_opref, s); dfree(g.S_fmask, s); dfree(g.S_pidx, s);
+    dfree(g.off, s);
     dfree(g.P_t, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
     dfree(g.P_min, s); dfree(g.pofs, s);
     for (auto& f : g.fwd) {

@@ -6,7 +6,9 @@
 //     S_nbr[R]  u32    other endpoint | dir << 31   (dir 0 = outward)
 //     S_ord[R]  u32    ingestion ordinal | forward-in-degree-order << 31
 //     S_node[R] u32    center node
-//     S_pg[R+1] u32    global exclusive prefix count of outward records
+//     S_omask[R/32+1], S_opref[R/32+2]  u32  outward-record bitmask (one bit per
+//               record, written by warp ballots) + exclusive prefix of its
+//               word popcounts: P_o(q) = opref[q/32] + popc(omask[q/32] & below)
 //     S_pidx[R] u32    the record's edge position in P (built lazily, items API)
 //     off[n+1]  u32    CSR offsets
 //   P (PairEdgeIndex, indexes.hpp:63-92: one record per edge, grouped by the
@@ -96,7 +98,9 @@ struct DeviceGraph {
     uint32_t* S_nbr = nullptr;
     uint32_t* S_ord = nullptr;
     uint32_t* S_node = nullptr;
-    uint32_t* S_pg = nullptr;
+    uint32_t* S_omask = nullptr;
+    uint32_t* S_opref = nullptr;
+    uint32_t* S_fmask = nullptr;  // forward (degree orientation) bitmask, same layout
     uint32_t* S_pidx = nullptr;
     uint32_t* off = nullptr;
 
@@ -119,7 +123,8 @@ struct SView {
     const uint32_t* nbr;
     const uint32_t* ord;
     const uint32_t* node;
-    const uint32_t* pg;
+    const uint32_t* omask;
+    const uint32_t* opref;
     const uint32_t* pidx;
     const uint32_t* off;
 };
@@ -132,8 +137,13 @@ struct PView {
     const uint32_t* pofs;
 };
 inline SView sview(const DeviceGraph& g) {
-    return {g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_pg, g.S_pidx, g.off};
+    return {g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_opref, g.S_pidx, g.off};
 }
+// global exclusive count of outward records before S position q
+__device__ __forceinline__ uint32_t outward_before(const SView& S, uint32_t q) {
+    return S.opref[q >> 5] + __popc(S.omask[q >> 5] & ((1u << (q & 31)) - 1u));
+}
+
 inline PView pview(const DeviceGraph& g) {
     return {g.P_t, g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs};
 }

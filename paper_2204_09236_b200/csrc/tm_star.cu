@@ -146,10 +146,10 @@ __device__ __forceinline__ void first_role(const SView& S, const PView& P, uint3
     if (P.w[k] & kPLast) return;
     if (P.t[k + 1] > lim) return;  // no same-neighbour record in the window
 
-    const uint32_t base = S.pg[start];
+    const uint32_t base = outward_before(S, start);
     const uint32_t e = gallop_upper(S.t, q + 1, end, lim);
-    const uint64_t pe_o = S.pg[e] - base, pe_i = (uint64_t)(e - start) - pe_o;
-    const uint64_t pa_o = (uint64_t)(S.pg[q] - base) + (da ? 0u : 1u);
+    const uint64_t pe_o = outward_before(S, e) - base, pe_i = (uint64_t)(e - start) - pe_o;
+    const uint64_t pa_o = (uint64_t)(outward_before(S, q) - base) + (da ? 0u : 1u);
     const uint64_t pa_i = (uint64_t)(q - start + 1) - pa_o;
 
     uint64_t n0 = 0, n1 = 0;
@@ -163,7 +163,7 @@ __device__ __forceinline__ void first_role(const SView& S, const PView& P, uint3
         const uint32_t w = P.w[k];
         qb = gallop_locate(S, qb + 1, e, tb, P.ord[k]);  // member's place in S_u
         const uint64_t pos = qb - start;
-        const uint64_t pb_o = S.pg[qb] - base;
+        const uint64_t pb_o = outward_before(S, qb) - base;
         const uint64_t pb_i = pos - pb_o;
         if ((w >> 31) ^ side) {  // inward relative to u
             A10 += pb_o;
@@ -210,7 +210,7 @@ __device__ __forceinline__ void third_role(const SView& S, const PView& P, uint3
     const uint32_t lo = gallop_lower_back(S.t, start, q, lo_lim);
     const uint32_t L = max(lo, start + rb);
     if (L >= q) return;
-    const uint32_t pl = S.pg[L];
+    const uint32_t pl = outward_before(S, L);
     const int64_t tL = S.t[L];
     const uint32_t oL = S.ord[L] & kNodeMask;
     const uint32_t hiq = start + re;
@@ -224,7 +224,7 @@ __device__ __forceinline__ void third_role(const SView& S, const PView& P, uint3
         qb = gallop_locate_back(S, L + 1, qb, tb, ob);
         const uint32_t mhi = min(qb, hiq);
         if (mhi > L) {
-            const uint64_t x = (uint64_t)(S.pg[mhi] - pl);
+            const uint64_t x = (uint64_t)(outward_before(S, mhi) - pl);
             const uint64_t y = (uint64_t)(mhi - L) - x;
             if ((w >> 31) ^ side) { x1 += x; y1 += y; } else { x0 += x; y0 += y; }
         }
