@@ -58,6 +58,12 @@ typedef struct tm_run_config {
     uint64_t shard_target;     /* accepted for API parity; semantics-free           */
     uint32_t center_begin;     /* center partition [begin, end); end == 0: all      */
     uint32_t center_end;
+    /* time-slice partition: when nonzero, count only the instances whose
+     * earliest edge (in (t, ordinal) order) has t < first_edge_t_end.  A rank
+     * that builds the edges with t in [lo, hi + delta) and counts with
+     * first_edge_t_end = hi owns exactly the instances starting in [lo, hi). */
+    int32_t has_first_edge_t_end;
+    int64_t first_edge_t_end;
 } tm_run_config;
 
 /* PhaseTimings (executor.hpp:55-65); device-event times in ms. */
@@ -108,15 +114,25 @@ int tm_count_star_pair_items(tm_graph* g, int64_t delta, uint64_t n_items, const
 int tm_count_triangles_items(tm_graph* g, int64_t delta, uint64_t n_items, const uint32_t* nodes,
                              const uint64_t* begin, const uint64_t* end, const uint8_t* live,
                              uint64_t* tri_out);
-/* run_parallel (executor.cpp:149-215).  With a proper center partition the
- * raw counters are partial sums and census is left zeroed (merge after the
- * all-reduce); for the full range census holds merge_census(raw). */
+/* run_parallel (executor.cpp:149-215).  With a center or time-slice partition
+ * the raw counters are partial sums and census is left zeroed (merge after the
+ * all-reduce); for the full graph census holds merge_census(raw). */
 int tm_run_parallel(tm_graph* g, const tm_run_config* cfg, tm_counters* raw, uint64_t* census36,
                     tm_phase_timings* timings);
 /* Whole pipeline for one step: build + run_parallel + free. */
 int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
                    uint64_t n, int device_ptrs, void* stream, const tm_run_config* cfg,
                    tm_counters* raw, uint64_t* census36, tm_phase_timings* timings);
+/* One rank's share of a time-sliced census (multi-GPU without a replicated
+ * index build): the edges with t in [t_lo, t_hi + delta) are compacted on the
+ * GPU (ingestion order kept), indexed, and counted for the instances whose
+ * earliest edge has t in [t_lo, t_hi).  has_lo / has_hi = 0 leave the first /
+ * last slice open.  Summing raw over slices that partition the time axis gives
+ * the whole graph's counters exactly. */
+int tm_count_edges_time_slice(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
+                              uint64_t n, int device_ptrs, void* stream, const tm_run_config* cfg,
+                              int has_lo, int64_t t_lo, int has_hi, int64_t t_hi, tm_counters* raw,
+                              tm_phase_timings* timings);
 /* Degree-cost balanced center partition for rank `rank` of `world`. */
 int tm_partition_centers(const tm_graph* g, uint32_t world, uint32_t rank, uint32_t* begin,
                          uint32_t* end);

@@ -156,6 +156,8 @@ inline tm_run_config to_c(const RunConfig& c, std::uint32_t cb = 0, std::uint32_
     r.shard_target = c.shard_target;
     r.center_begin = cb;
     r.center_end = ce;
+    r.has_first_edge_t_end = 0;
+    r.first_edge_t_end = 0;
     return r;
 }
 

@@ -57,6 +57,7 @@ class Oracle:
         L.orc_count_triangles.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p]
         L.orc_merge_census.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.orc_census_bruteforce.argtypes = [C.c_void_p, C.c_int64, C.c_void_p]
+        L.orc_census_bruteforce_before.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]
         L.orc_signature.argtypes = [C.c_int, C.c_char_p]
         L.orc_cell_signature.argtypes = [C.c_int, C.c_int]
         L.orc_auto_degree_threshold.restype = C.c_uint64
@@ -158,6 +159,13 @@ class Oracle:
     def census_bruteforce(self, g, delta):
         out = np.zeros(36, np.uint64)
         if self.L.orc_census_bruteforce(g.h, delta, out.ctypes.data):
+            raise OverflowError("overflow")
+        return out
+
+    def census_bruteforce_before(self, g, delta, t_end):
+        """Brute-force census of the instances whose earliest edge has t < t_end."""
+        out = np.zeros(36, np.uint64)
+        if self.L.orc_census_bruteforce_before(g.h, delta, t_end, out.ctypes.data):
             raise OverflowError("overflow")
         return out
 

@@ -451,6 +451,38 @@ int orc_census_bruteforce(const orc_graph* g, int64_t delta, uint64_t* census) {
     return g_overflow ? ORC_ERR_OVERFLOW : ORC_OK;
 }
 
+/* Brute force restricted to instances whose earliest edge has t < t_end
+ * (time-slice partitions of the multi-GPU path); same enumeration as above. */
+int orc_census_bruteforce_before(const orc_graph* g, int64_t delta, int64_t t_end, uint64_t* census) {
+    universe();
+    g_overflow = 0;
+    memset(census, 0, 36 * 8);
+    const orc_edge* E = g->edges;
+    uint64_t m = g->m;
+    for (uint64_t i = 0; i + 2 < m; ++i) {
+        if (E[i].t >= t_end) break;
+        int64_t horizon = sat_add(E[i].t, delta);
+        for (uint64_t j = i + 1; j + 1 < m; ++j) {
+            if (E[j].t > horizon) break;
+            for (uint64_t k = j + 1; k < m; ++k) {
+                if (E[k].t > horizon) break;
+                uint32_t nodes[6] = {E[i].src, E[i].dst, E[j].src, E[j].dst, E[k].src, E[k].dst};
+                uint32_t seen[3]; int distinct = 0, ok = 1;
+                for (int q = 0; q < 6 && ok; ++q) {
+                    int f = 0;
+                    for (int z = 0; z < distinct; ++z) if (seen[z] == nodes[q]) f = 1;
+                    if (!f) { if (distinct == 3) ok = 0; else seen[distinct++] = nodes[q]; }
+                }
+                if (!ok) continue;
+                uint32_t e[3][2] = {{E[i].src, E[i].dst}, {E[j].src, E[j].dst}, {E[k].src, E[k].dst}};
+                sig_t sg = canonical(e);
+                inc(&census[sig_index(sg.s)], 1);
+            }
+        }
+    }
+    return g_overflow ? ORC_ERR_OVERFLOW : ORC_OK;
+}
+
 /* ------------------------------------------------------------------ */
 /* generate_random_graph: graph.cpp:140-168 (mt19937_64, rejection      */
 /* sampling bounded draws).  Output in ingestion (ordinal) order.      */

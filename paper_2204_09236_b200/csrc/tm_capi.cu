@@ -274,7 +274,7 @@ struct PassResult {
     uint64_t tri_once[24];
 };
 
-void run_passes(tm_graph* G, int64_t delta, bool do_star, bool do_tri, int tri_mode,
+void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do_tri, int tri_mode,
                 uint32_t cb, uint32_t ce, PassResult& r, tm_phase_timings* tm) {
     DeviceGraph& g = G->g;
     cudaStream_t s = g.stream;
@@ -288,7 +288,7 @@ void run_passes(tm_graph* G, int64_t delta, bool do_star, bool do_tri, int tri_m
         TM_CUDA(cudaEventCreate(&e2));
         TM_CUDA(cudaEventRecord(e0, s));
     }
-    if (do_star && g.R) star_full(g, delta, cb, ce, g.d_acc, g.d_acc + 56);
+    if (do_star && g.R) star_full(g, delta, cb, ce, t_end, g.d_acc, g.d_acc + 56);
     if (tm) TM_CUDA(cudaEventRecord(e1, s));
     if (do_tri && g.R) {
         const int fm = tri_mode == TM_TRI_REMOVAL ? 1 : 0;
@@ -299,7 +299,7 @@ void run_passes(tm_graph* G, int64_t delta, bool do_star, bool do_tri, int tri_m
             fb = read_u32(f.off, cb, s);
             fe = read_u32(f.off, ce, s);
         }
-        tri_oriented(g, f, delta, fb, fe, g.d_acc + 32, g.d_acc + 56);
+        tri_oriented(g, f, delta, fb, fe, t_end, g.d_acc + 32, g.d_acc + 56);
     }
     if (tm) TM_CUDA(cudaEventRecord(e2, s));
     uint64_t* h = pinned_acc();
@@ -333,11 +333,12 @@ int run_parallel_impl(tm_graph* G, const tm_run_config* cfg, tm_counters* raw, u
     const uint32_t cb = cfg->center_begin;
     const uint32_t ce = cfg->center_end ? cfg->center_end : (uint32_t)G->g.n;
     if (cb > ce || ce > G->g.n) throw tm_error(TM_ERR_INVALID, "bad center partition");
-    const bool full = (cb == 0 && ce == G->g.n);
+    const bool full = (cb == 0 && ce == G->g.n) && !cfg->has_first_edge_t_end;
 
     PassResult r;
     auto t0 = std::chrono::steady_clock::now();
-    run_passes(G, cfg->delta, (motifs & 3u) != 0, (motifs & 4u) != 0, cfg->triangle_mode, cb, ce, r,
+    const int64_t t_end = cfg->has_first_edge_t_end ? cfg->first_edge_t_end : INT64_MAX;
+    run_passes(G, cfg->delta, t_end, (motifs & 3u) != 0, (motifs & 4u) != 0, cfg->triangle_mode, cb, ce, r,
                tm);
     tm_counters out;
     std::memset(&out, 0, sizeof(out));
@@ -566,7 +567,7 @@ int tm_count_star_pair(tm_graph* g, int64_t delta, uint64_t* star24, uint64_t* p
     return guarded([&] {
         if (delta < 0) throw tm_error(TM_ERR_CONFIG, "delta must be >= 0");
         PassResult r;
-        run_passes(g, delta, true, false, 0, 0, (uint32_t)g->g.n, r, nullptr);
+        run_passes(g, delta, INT64_MAX, true, false, 0, 0, (uint32_t)g->g.n, r, nullptr);
         finish_star(r.star_raw, star24, pair8);
         return TM_OK;
     });
@@ -578,7 +579,7 @@ int tm_count_triangles(tm_graph* g, int64_t delta, int mode, uint64_t* tri24) {
         if (mode != TM_TRI_COUNT_ALL && mode != TM_TRI_REMOVAL)
             throw tm_error(TM_ERR_CONFIG, "triangle mode must be countall or removal");
         PassResult r;
-        run_passes(g, delta, false, true, mode, 0, (uint32_t)g->g.n, r, nullptr);
+        run_passes(g, delta, INT64_MAX, false, true, mode, 0, (uint32_t)g->g.n, r, nullptr);
         if (mode == TM_TRI_COUNT_ALL) expand_count_all(r.tri_once, tri24);
         else std::memcpy(tri24, r.tri_once, 24 * sizeof(uint64_t));
         return TM_OK;
@@ -681,6 +682,69 @@ int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, u
         }
         free_impl(G);
         if (timings) timings->index_ms = index_ms;
+        return rc;
+    });
+}
+
+int tm_count_edges_time_slice(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
+                              uint64_t n, int device_ptrs, void* stream, const tm_run_config* cfg,
+                              int has_lo, int64_t t_lo, int has_hi, int64_t t_hi, tm_counters* raw,
+                              tm_phase_timings* timings) {
+    return guarded([&] {
+        if (!cfg) throw tm_error(TM_ERR_INVALID, "null config");
+        if (cfg->delta < 0) throw tm_error(TM_ERR_CONFIG, "delta must be >= 0");
+        ensure_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        bool own = false;
+        if (!s) {
+            TM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            own = true;
+        }
+        const uint32_t *ds = src, *dd = dst;
+        const int64_t* dt = t;
+        uint32_t *hs = nullptr, *hd = nullptr, *os = nullptr, *od = nullptr;
+        int64_t *ht = nullptr, *ot = nullptr;
+        tm_graph* G = nullptr;
+        int rc = TM_OK;
+        try {
+            if (!device_ptrs && m) {
+                hs = dalloc<uint32_t>(m, s);
+                hd = dalloc<uint32_t>(m, s);
+                ht = dalloc<int64_t>(m, s);
+                TM_CUDA(cudaMemcpyAsync(hs, src, m * 4, cudaMemcpyHostToDevice, s));
+                TM_CUDA(cudaMemcpyAsync(hd, dst, m * 4, cudaMemcpyHostToDevice, s));
+                TM_CUDA(cudaMemcpyAsync(ht, t, m * 8, cudaMemcpyHostToDevice, s));
+                ds = hs;
+                dd = hd;
+                dt = ht;
+            }
+            // edges of instances whose first edge starts in [t_lo, t_hi): t in [t_lo, t_hi + delta)
+            const int64_t lo = has_lo ? t_lo : INT64_MIN;
+            const int64_t hi = has_hi ? sat_add(t_hi, cfg->delta) : INT64_MAX;
+            uint64_t ms = 0;
+            if (has_lo || has_hi) {
+                ms = slice_edges(ds, dd, dt, m, lo, hi == INT64_MAX ? INT64_MAX : hi, &os, &od, &ot, s);
+            }
+            tm_run_config c = *cfg;
+            c.has_first_edge_t_end = has_hi ? 1 : 0;
+            c.first_edge_t_end = t_hi;
+            double index_ms = 0;
+            if (has_lo || has_hi)
+                G = build_impl(os, od, ot, ms, n, 1, s, timings ? &index_ms : nullptr);
+            else
+                G = build_impl(ds, dd, dt, m, n, 1, s, timings ? &index_ms : nullptr);
+            rc = run_parallel_impl(G, &c, raw, nullptr, timings);
+            if (timings) timings->index_ms = index_ms;
+        } catch (...) {
+            if (G) free_impl(G);
+            dfree(os, s); dfree(od, s); dfree(ot, s); dfree(hs, s); dfree(hd, s); dfree(ht, s);
+            if (own) cudaStreamDestroy(s);
+            throw;
+        }
+        free_impl(G);
+        dfree(os, s); dfree(od, s); dfree(ot, s); dfree(hs, s); dfree(hd, s); dfree(ht, s);
+        TM_CUDA(cudaStreamSynchronize(s));
+        if (own) cudaStreamDestroy(s);
         return rc;
     });
 }

@@ -280,6 +280,35 @@ __global__ void forward_off_kernel(const uint32_t* __restrict__ off, const uint3
     }
 }
 
+// time-slice partition: keep edges with t in [lo, hi) (ingestion order kept)
+__global__ void slice_mask_kernel(const int64_t* __restrict__ t, uint64_t m, int64_t lo, int64_t hi,
+                                  uint32_t* __restrict__ mask) {
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = base + threadIdx.x;
+        const uint32_t keep = k < m && t[k] >= lo && t[k] < hi ? 1u : 0u;
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if ((threadIdx.x & 31) == 0 && k < m) mask[k >> 5] = b;
+    }
+}
+
+__global__ void slice_scatter_kernel(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                                     const int64_t* __restrict__ t, uint64_t m,
+                                     const uint32_t* __restrict__ mask, const uint32_t* __restrict__ pref,
+                                     uint32_t* __restrict__ osrc, uint32_t* __restrict__ odst,
+                                     int64_t* __restrict__ ot) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t word = mask[k >> 5], bit = 1u << (k & 31);
+        if (word & bit) {
+            const uint32_t j = pref[k >> 5] + __popc(word & (bit - 1u));
+            osrc[j] = src[k];
+            odst[j] = dst[k];
+            ot[j] = t[k];
+        }
+    }
+}
+
 unsigned grid_for(uint64_t work, int block = 256) {
     const uint64_t cap = (uint64_t)sm_count() * 8;
     uint64_t g = (work + block - 1) / block;
@@ -442,6 +471,32 @@ void build_forward(DeviceGraph& g, int mode) {
     dfree(fpref, s);
     dfree(imask, s);
     f.valid = true;
+}
+
+uint64_t slice_edges(const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t, uint64_t m,
+                     int64_t lo, int64_t hi, uint32_t** o_src, uint32_t** o_dst, int64_t** o_t,
+                     cudaStream_t s) {
+    const uint64_t nw = m / 32 + 1;
+    uint32_t* mask = dalloc<uint32_t>(nw, s);
+    uint32_t* pref = dalloc<uint32_t>(nw + 1, s);
+    TM_CUDA(cudaMemsetAsync(mask + (nw - 1), 0, sizeof(uint32_t), s));
+    if (m) {
+        TM_LAUNCH("slice_mask", s, slice_mask_kernel, grid_for(m), 256, 0, d_t, m, lo, hi, mask);
+    }
+    exclusive_scan<uint32_t>(PopcLoad{mask}, nw, pref, s);
+    uint32_t cnt = 0;
+    TM_CUDA(cudaMemcpyAsync(&cnt, pref + nw, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TM_CUDA(cudaStreamSynchronize(s));
+    *o_src = dalloc<uint32_t>(cnt, s);
+    *o_dst = dalloc<uint32_t>(cnt, s);
+    *o_t = dalloc<int64_t>(cnt, s);
+    if (m && cnt) {
+        TM_LAUNCH("slice_scatter", s, slice_scatter_kernel, grid_for(m), 256, 0, d_src, d_dst, d_t, m, mask,
+                  pref, *o_src, *o_dst, *o_t);
+    }
+    dfree(mask, s);
+    dfree(pref, s);
+    return cnt;
 }
 
 void build_s_pidx(DeviceGraph& g) {

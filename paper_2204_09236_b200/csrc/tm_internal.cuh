@@ -154,10 +154,14 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst,
 void free_graph(DeviceGraph& g);
 void build_forward(DeviceGraph& g, int mode);
 void build_s_pidx(DeviceGraph& g);
+// compact the edges with t in [lo, hi) (ingestion order kept); returns the count
+uint64_t slice_edges(const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t, uint64_t m,
+                     int64_t lo, int64_t hi, uint32_t** o_src, uint32_t** o_dst, int64_t** o_t,
+                     cudaStream_t s);
 
 // raw star sums (32 u64: Pair[8], C[8], B[8], A[8]) for the centers
-// [c_begin, c_end), added into d_out.
-void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end,
+// [c_begin, c_end) and instances whose first edge has t < t_end, added into d_out.
+void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end, int64_t t_end,
                uint64_t* d_out, uint64_t* d_stats);
 void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
                 const uint64_t* d_begin, const uint64_t* d_end, const uint64_t* d_item_off,
@@ -165,7 +169,7 @@ void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uin
                 uint64_t* d_out);
 // once-counted triangle cells (24 u64) over forward positions [f_begin, f_end)
 void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
-                  uint32_t f_end, uint64_t* d_out, uint64_t* d_stats);
+                  uint32_t f_end, int64_t t_end, uint64_t* d_out, uint64_t* d_stats);
 void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
                const uint64_t* d_begin, const uint64_t* d_item_off, uint64_t total,
                const uint8_t* d_live, uint64_t* d_out);

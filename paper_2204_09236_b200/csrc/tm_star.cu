@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256) star_filter_kernel(PView P, int64_t delta
 // Work: the full first_role / third_role sums for the surviving records.
 // The record's own S position is found by binary search of (t, ordinal) in
 // its center's time-ordered sequence.
-__global__ void __launch_bounds__(256) star_work_kernel(SView S, PView P, int64_t delta,
+__global__ void __launch_bounds__(256) star_work_kernel(SView S, PView P, int64_t delta, int64_t t_end,
                                                         const uint32_t* __restrict__ first_list,
                                                         const uint32_t* __restrict__ third_list,
                                                         const uint32_t* __restrict__ counters,
@@ -296,9 +296,17 @@ __global__ void __launch_bounds__(256) star_work_kernel(SView S, PView P, int64_
         const uint32_t k = e >> 1, side = e & 1u;
         const uint32_t u = side ? P.max[k] : P.min[k];
         const uint32_t start = S.off[u], end = S.off[u + 1];
-        const uint32_t q = gallop_locate(S, start, end, P.t[k], P.ord[k]);
-        if (first) first_role(S, P, q, k, side, start, end, delta, acc);
-        else third_role(S, P, q, k, side, start, delta, 0u, end - start, acc);
+        const int64_t tk = P.t[k];
+        if (first && tk >= t_end) continue;  // instance's first edge outside the time slice
+        const uint32_t q = gallop_locate(S, start, end, tk, P.ord[k]);
+        if (first) {
+            first_role(S, P, q, k, side, start, end, delta, acc);
+        } else {
+            // first edges restricted to t < t_end: a prefix of S_u
+            const uint32_t re = t_end == INT64_MAX ? end - start
+                                                   : gallop_upper(S.t, start, end, t_end - 1) - start;
+            third_role(S, P, q, k, side, start, delta, 0u, re, acc);
+        }
     }
     __syncthreads();
     flush_cells(cells, 32, out);
@@ -348,7 +356,7 @@ __global__ void __launch_bounds__(256) star_items_kernel(
 
 }  // namespace
 
-void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end,
+void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end, int64_t t_end,
                uint64_t* d_out, uint64_t* d_stats) {
     if (c_end <= c_begin || g.m == 0) return;
     cudaStream_t st = g.stream;
@@ -361,7 +369,8 @@ void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c
     TM_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), st));
     TM_LAUNCH("star_filter", st, star_filter_kernel, (unsigned)grid, 256, 0, pview(g), delta, g.m,
               c_begin, c_end, lists, lists + work, counters);
-    TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), delta, lists,
+    TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), delta, t_end,
+              lists,
               lists + work, counters, d_out, d_stats);
     dfree(lists, st);
 }

@@ -27,9 +27,11 @@ namespace {
 
 // counts of closing records for one wedge: c[type*2 + dk], dk relative to v.
 // The v-w list is the P group {min, max}: lower_bound of max in min's block.
+// t_end restricts to instances whose earliest edge has t < t_end (time-slice
+// partitions): the closing edge itself for type I, e_i otherwise.
 __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint32_t w, int64_t lo,
                                                int64_t hi, int64_t ti, uint32_t oi, int64_t tj,
-                                               uint32_t oj, uint32_t c[6]) {
+                                               uint32_t oj, int64_t t_end, uint32_t c[6]) {
 #pragma unroll
     for (int j = 0; j < 6; ++j) c[j] = 0;
     const uint32_t a = min(v, w), b = max(v, w);
@@ -54,7 +56,7 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
             if (tk < ti || (tk == ti && P.ord[k] < oi)) type = 0;
             else if (tk > tj || (tk == tj && P.ord[k] > oj)) type = 2;
             else type = 1;
-            c[type * 2 + dk] += 1;
+            if ((type == 0 ? tk : ti) < t_end) c[type * 2 + dk] += 1;
         }
         if (wk & kPLast) return;
     }
@@ -86,7 +88,15 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         if (tm < tj || (tm == tj && P.ord[mid] < oj)) l = mid + 1; else r = mid;
     }
     const uint32_t k3 = l;
-    for (uint32_t x = k1; x < k4; ++x) {
+    uint32_t k2e = k2;  // type I records whose own t is before t_end
+    if (t_end != INT64_MAX) {
+        l = k1; r = k2;
+        while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] < t_end) l = mid + 1; else r = mid; }
+        k2e = l;
+    }
+    const uint32_t kend = ti < t_end ? k4 : k2;
+    for (uint32_t x = k1; x < kend; ++x) {
+        if (x >= k2e && x < k2) continue;
         const uint32_t type = x < k2 ? 0u : (x < k3 ? 1u : 2u);
         c[type * 2 + ((P.w[x] >> 31) ^ flip)] += 1;
     }
@@ -114,7 +124,7 @@ __device__ __forceinline__ void wedges_from(const PView& P, const int64_t* __res
         if (w == v) continue;
         if (live && !live[w]) continue;
         uint32_t c[6];
-        closing_counts(P, v, w, sat_sub(tj, delta), lim, ti, oi, tj, ORD[j] & kNodeMask, c);
+        closing_counts(P, v, w, sat_sub(tj, delta), lim, ti, oi, tj, ORD[j] & kNodeMask, INT64_MAX, c);
         const uint64_t m1 = (nj >> 31) ? ~0ull : 0ull, m0 = ~m1;
 #pragma unroll
         for (int x = 0; x < 6; ++x) {
@@ -208,12 +218,12 @@ template <typename Sink>
 __device__ __forceinline__ void add_wedge(const PView& P, const int64_t* __restrict__ FT,
                                           const uint32_t* __restrict__ FN,
                                           const uint32_t* __restrict__ FO, uint32_t i, uint32_t j,
-                                          int64_t delta, const Sink& acc) {
+                                          int64_t delta, int64_t t_end, const Sink& acc) {
     const uint32_t ni = FN[i], nj = FN[j];
     const int64_t ti = FT[i], tj = FT[j];
     uint32_t c[6];
     closing_counts(P, ni & kNodeMask, nj & kNodeMask, sat_sub(tj, delta), sat_add(ti, delta), ti,
-                   FO[i], tj, FO[j], c);
+                   FO[i], tj, FO[j], t_end, c);
     const int cell0 = (int)((ni >> 31) * 4 + (nj >> 31) * 2);  // di*4 + dj*2
 #pragma unroll
     for (int ty = 0; ty < 3; ++ty)
@@ -225,7 +235,7 @@ __device__ __forceinline__ void add_wedge(const PView& P, const int64_t* __restr
 __global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, const int64_t* __restrict__ FT,
                                                         const uint32_t* __restrict__ FN,
                                                         const uint32_t* __restrict__ FO,
-                                                        int64_t delta,
+                                                        int64_t delta, int64_t t_end,
                                                         const uint64_t* __restrict__ wedges,
                                                         uint32_t wedge_cap,
                                                         const uint32_t* __restrict__ counters,
@@ -239,7 +249,7 @@ __global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, const int64_t* 
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
          idx += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t w = wedges[idx];
-        add_wedge(P, FT, FN, FO, (uint32_t)(w >> 32), (uint32_t)w, delta, acc);
+        add_wedge(P, FT, FN, FO, (uint32_t)(w >> 32), (uint32_t)w, delta, t_end, acc);
     }
     __syncthreads();
     flush_cells(cells, 24, out);
@@ -252,7 +262,7 @@ __global__ void __launch_bounds__(256) tri_long_kernel(PView P, const int64_t* _
                                                        const uint32_t* __restrict__ FO,
                                                        const uint32_t* __restrict__ Fnode,
                                                        const uint32_t* __restrict__ Foff,
-                                                       int64_t delta,
+                                                       int64_t delta, int64_t t_end,
                                                        const uint32_t* __restrict__ list,
                                                        const uint32_t* __restrict__ counters,
                                                        uint64_t* out, uint64_t* stats) {
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(256) tri_long_kernel(PView P, const int64_t* _
             const uint32_t j = j0 + lane;
             const bool in = j < end && FT[j] <= lim;
             if (in && (FN[j] & kNodeMask) != v) {
-                add_wedge(P, FT, FN, FO, i, j, delta, acc);
+                add_wedge(P, FT, FN, FO, i, j, delta, t_end, acc);
                 ++my_wedges;
             }
             if (!__all_sync(0xffffffffu, in)) break;
@@ -319,7 +329,7 @@ __global__ void __launch_bounds__(256) tri_items_kernel(SView S, PView P, int64_
 }  // namespace
 
 void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
-                  uint32_t f_end, uint64_t* d_out, uint64_t* d_stats) {
+                  uint32_t f_end, int64_t t_end, uint64_t* d_out, uint64_t* d_stats) {
     if (f_end <= f_begin) return;
     cudaStream_t st = g.stream;
     const uint64_t work = f_end - f_begin;
@@ -336,9 +346,9 @@ void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_
     TM_LAUNCH("tri_filter", st, tri_filter_kernel, (unsigned)grid, 256, 0, f.t, f.nbr, f.node, delta,
               f_begin, f_end, wedges, wedge_cap, long_list, counters);
     TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pview(g), f.t, f.nbr, f.ord,
-              delta, wedges, wedge_cap, counters, d_out, d_stats);
+              delta, t_end, wedges, wedge_cap, counters, d_out, d_stats);
     TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pview(g), f.t, f.nbr, f.ord,
-              f.node, f.off, delta, long_list, counters, d_out, d_stats);
+              f.node, f.off, delta, t_end, long_list, counters, d_out, d_stats);
     dfree(wedges, st);
     dfree(long_list, st);
 }

@@ -1,11 +1,17 @@
-"""Multi-GPU plumbing: one process per GPU, graph replicated, centers
-partitioned by a degree-cost prefix sum, the 56 raw u64 counters combined by
-one all-reduce (NCCL over NVLink on GPUs; gloo in the CPU tests), then
-merge_census on every rank.
+"""Multi-GPU plumbing: one process per GPU, the 56 raw u64 counters combined
+by one all-reduce (NCCL over NVLink on GPUs; gloo in the CPU tests), then
+merge_census on every rank.  Two exact partitions of the work:
+
+* time slices (default): rank r holds the edges with t in [tau_r,
+  tau_{r+1} + delta) and counts the instances whose earliest edge has t in
+  [tau_r, tau_{r+1}).  Every instance has exactly one earliest edge, so the
+  slices partition the census; each rank builds only its slice's indexes, so
+  the index build scales too.
+* center ranges (north_star): graph replicated, centers split by a
+  degree-cost prefix sum (tm_partition_centers).
 
 This is the GPU analogue of HARE's inter-node split (executor.cpp:23-52 plan,
-executor.cpp:96-139 worker pool + reduction): center ranges instead of a
-dynamic queue, and an all-reduce instead of the per-worker counter merge.
+executor.cpp:96-139 worker pool + reduction).
 """
 from __future__ import annotations
 
@@ -59,3 +65,27 @@ def run_distributed(ctx, config, rank: int, world: int, group=None, device=None)
     tot = allreduce_counters(arr, group, device)
     rc = tm.RawCounters.from_array(tot)
     return tm.merge_census(rc.star, rc.pair, rc.tri, config.triangle_mode)
+
+
+def time_slice_bounds(t, world: int) -> List[Tuple[object, object]]:
+    """Per-rank [lo, hi) first-edge time bounds balanced by edge count
+    (None = open end).  Deterministic for the same t on every rank."""
+    ts = np.sort(np.asarray(t, np.int64))
+    m = len(ts)
+    cuts = [int(ts[(r * m) // world]) for r in range(1, world)] if m else []
+    lows = [None] + cuts
+    highs = cuts + [None]
+    return list(zip(lows, highs))
+
+
+def time_slice_mask(t, lo, hi, delta: int) -> np.ndarray:
+    """Edges a rank needs: t in [lo, hi + delta) (saturating at the int64 ends)."""
+    t = np.asarray(t, np.int64)
+    keep = np.ones(len(t), bool)
+    if lo is not None:
+        keep &= t >= lo
+    if hi is not None:
+        top = hi + delta if hi <= (2 ** 63 - 1) - delta else None
+        if top is not None:
+            keep &= t < top
+    return keep

@@ -84,7 +84,8 @@ class _Counters(C.Structure):
 class _RunConfig(C.Structure):
     _fields_ = [("delta", C.c_int64), ("workers", C.c_uint32), ("degree_threshold", C.c_int64),
                 ("triangle_mode", C.c_int32), ("motifs", C.c_uint32), ("shard_target", C.c_uint64),
-                ("center_begin", C.c_uint32), ("center_end", C.c_uint32)]
+                ("center_begin", C.c_uint32), ("center_end", C.c_uint32),
+                ("has_first_edge_t_end", C.c_int32), ("first_edge_t_end", C.c_int64)]
 
 
 class _Timings(C.Structure):
@@ -125,6 +126,9 @@ def lib():
                                   C.POINTER(_Timings)]
     L.tm_count_edges.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint64, C.c_int, VP,
                                  C.POINTER(_RunConfig), C.POINTER(_Counters), VP, C.POINTER(_Timings)]
+    L.tm_count_edges_time_slice.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint64, C.c_int, VP,
+                                            C.POINTER(_RunConfig), C.c_int, C.c_int64, C.c_int, C.c_int64,
+                                            C.POINTER(_Counters), C.POINTER(_Timings)]
     L.tm_partition_centers.argtypes = [VP, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32),
                                        C.POINTER(C.c_uint32)]
     L.tm_merge_census.argtypes = [VP, VP, VP, C.c_int, VP]
@@ -705,14 +709,18 @@ class RunConfig:
     motifs: MotifFilter = field(default_factory=MotifFilter)
     shard_target: int = 4096
     light_batch: int = 64
+    # time-slice partition: count only instances whose earliest edge has t < this
+    first_edge_t_end: Optional[int] = None
 
     def to_c(self, center_begin: int = 0, center_end: int = 0) -> _RunConfig:
         thr = -1 if self.degree_threshold is None else min(int(self.degree_threshold), NO_SHARDING)
         m = self.motifs.mask()
         if m == 0:
             raise ValueError("empty motif filter")
+        has_t = 0 if self.first_edge_t_end is None else 1
         return _RunConfig(int(self.delta), int(self.workers), thr, int(self.triangle_mode), m,
-                          int(self.shard_target), center_begin, center_end)
+                          int(self.shard_target), center_begin, center_end, has_t,
+                          int(self.first_edge_t_end or 0))
 
 
 @dataclass
@@ -762,7 +770,8 @@ def run_parallel_raw(ctx: GraphContext, config: RunConfig, center_begin: int = 0
     rc = RawCounters(StarCounter(np.frombuffer(raw.star, np.uint64)),
                      PairCounter(np.frombuffer(raw.pair, np.uint64)),
                      TriCounter(np.frombuffer(raw.tri, np.uint64)))
-    full = center_begin == 0 and (center_end == 0 or center_end == ctx.node_count())
+    full = center_begin == 0 and (center_end == 0 or center_end == ctx.node_count()) \
+        and config.first_edge_t_end is None
     return rc, (census if full else None)
 
 
@@ -821,3 +830,27 @@ def count_edges_device(n: int, m: int, src_ptr: int, dst_ptr: int, t_ptr: int, c
         timings.index_ms, timings.star_pair_ms = tm.index_ms, tm.star_pair_ms
         timings.triangle_ms, timings.merge_ms = tm.triangle_ms, tm.merge_ms
     return census
+
+
+def count_edges_time_slice(n: int, src, dst, t, config: RunConfig, t_lo: Optional[int] = None,
+                           t_hi: Optional[int] = None, m: Optional[int] = None,
+                           stream: Optional[int] = None) -> RawCounters:
+    """One rank's share of a time-sliced census (tm_count_edges_time_slice):
+    the instances whose earliest edge has t in [t_lo, t_hi).  src/dst/t are
+    numpy host arrays, or device pointers (ints) together with `m`."""
+    L = lib()
+    cfg = config.to_c()
+    raw = _Counters()
+    tm_ = _Timings()
+    if m is None:
+        src = np.ascontiguousarray(src, np.uint32)
+        dst = np.ascontiguousarray(dst, np.uint32)
+        t = np.ascontiguousarray(t, np.int64)
+        args = (src.ctypes.data, dst.ctypes.data, t.ctypes.data, len(src), n, 0)
+    else:
+        args = (src, dst, t, m, n, 1)
+    _raise(L.tm_count_edges_time_slice(*args, stream, C.byref(cfg), int(t_lo is not None), int(t_lo or 0),
+                                       int(t_hi is not None), int(t_hi or 0), C.byref(raw), C.byref(tm_)), L)
+    return RawCounters(StarCounter(np.frombuffer(raw.star, np.uint64)),
+                       PairCounter(np.frombuffer(raw.pair, np.uint64)),
+                       TriCounter(np.frombuffer(raw.tri, np.uint64)))

@@ -65,3 +65,46 @@ def test_gloo_partition_allreduce_matches_single(world, oracle):
     assert res[0][1][0] == 0 and res[-1][1][1] == n and res[0][1][1] == res[1][1][0]
     for _, _, census in res:
         assert census == expect
+
+
+def _slice_worker(rank, world, port, out_q, n, src, dst, t, delta):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import Oracle
+    from paper_2204_09236_b200.distributed import allreduce_counters, time_slice_bounds, time_slice_mask
+    O = Oracle()
+    lo, hi = time_slice_bounds(t, world)[rank]
+    keep = time_slice_mask(t, lo, hi, delta)
+    g = O.build_graph(n, src[keep], dst[keep], t[keep])
+    part = O.census_bruteforce_before(g, delta, hi if hi is not None else 2 ** 63 - 1)
+    tot = allreduce_counters(part)
+    out_q.put((rank, (lo, hi), int(keep.sum()), tot.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_time_slices_match_single(world, oracle):
+    """Time-slice partition logic on CPU: each rank keeps t in [lo, hi + delta),
+    counts instances whose earliest edge has t < hi, one all-reduce."""
+    n, m, delta = 30, 1500, 40
+    src, dst, t = oracle.generate_random_graph(n, m, 2000, 777)
+    g = oracle.build_graph(n, src, dst, t)
+    expect = oracle.census_bruteforce(g, delta).tolist()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slice_worker, args=(r, world, port, q, n, src, dst, t, delta))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sum(r[2] for r in res) < m + world * m // 10  # overlap is only the delta margins
+    for r in res:
+        assert r[3] == expect

@@ -44,6 +44,12 @@ def test_bench_contract_and_multirank(cuda):
                 "uniform_10k_200k", "--steps", "3", "--warmup", "3", "--dist-backend", "gloo", "--same-device"])
     assert two["n_gpus"] == 2
     assert two["census_total"] == gold
+    for world, part in ((3, "time"), (2, "centers")):
+        multi = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+                      "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--config",
+                      "uniform_10k_200k", "--steps", "3", "--warmup", "3", "--dist-backend", "gloo",
+                      "--same-device", "--partition", part])
+        assert multi["n_gpus"] == world and multi["census_total"] == gold, (world, part)
     ref = _run([sys.executable, "bench.py", "--impl", "reference", "--config", "uniform_10k_200k", "--steps", "1",
                 "--warmup", "3"]) if os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libtmotif_ref.so")) else None
     if ref is not None:
