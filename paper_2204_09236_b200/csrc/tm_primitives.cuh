@@ -61,6 +61,39 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* total) {
     return r;
 }
 
+// Block-wide reservation in two lists at once: each thread asks for `a` slots
+// of list A and `b` of list B and gets its first slot in each; one global
+// atomic per list per block call (all threads of the block call).  The counts
+// travel packed 16/16 through one u32 scan, so a block's total per list must
+// stay below 65536.  No trailing barrier is needed: the shared words are only
+// rewritten after every warp has passed the next call's first barrier.
+template <int NW, typename CA>
+__device__ __forceinline__ void block_reserve2(uint32_t a, uint32_t b, CA* ca, uint32_t* cb,
+                                               CA& oa, uint32_t& ob) {
+    __shared__ uint32_t s_w[NW];
+    __shared__ CA s_base_a;
+    __shared__ uint32_t s_base_b;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t v = (b << 16) | a;
+    const uint32_t inc = warp_inclusive_scan(v);
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t x = lane < NW ? s_w[lane] : 0u;
+        const uint32_t xi = warp_inclusive_scan(x);
+        if (lane < NW) s_w[lane] = xi - x;
+        if (lane == NW - 1) {
+            const uint32_t ta = xi & 0xffffu, tb = xi >> 16;
+            s_base_a = ta ? atomicAdd(ca, (CA)ta) : (CA)0;
+            s_base_b = tb ? atomicAdd(cb, tb) : 0u;
+        }
+    }
+    __syncthreads();
+    const uint32_t ex = s_w[w] + inc - v;
+    oa = s_base_a + (ex & 0xffffu);
+    ob = s_base_b + (ex >> 16);
+}
+
 // warp-aggregated append of `value` to list when pred holds (whole warp calls)
 __device__ __forceinline__ void warp_append(bool pred, uint32_t value, uint32_t* list,
                                             uint32_t* counter) {

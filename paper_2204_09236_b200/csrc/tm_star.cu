@@ -264,10 +264,14 @@ __global__ void __launch_bounds__(256) star_filter_kernel(PView P, int64_t delta
             }
         }
         const uint32_t e0 = (uint32_t)(2 * k), e1 = (uint32_t)(2 * k + 1);
-        warp_append(f && ina, e0, first_list, counters);
-        warp_append(f && inb, e1, first_list, counters);
-        warp_append(th && ina, e0, third_list, counters + 1);
-        warp_append(th && inb, e1, third_list, counters + 1);
+        const bool fa = f && ina, fb = f && inb, ta = th && ina, tb = th && inb;
+        uint32_t of, ot;
+        block_reserve2<8, uint32_t>((uint32_t)fa + (uint32_t)fb, (uint32_t)ta + (uint32_t)tb, counters,
+                          counters + 1, of, ot);
+        if (fa) first_list[of++] = e0;
+        if (fb) first_list[of] = e1;
+        if (ta) third_list[ot++] = e0;
+        if (tb) third_list[ot] = e1;
     }
 }
 

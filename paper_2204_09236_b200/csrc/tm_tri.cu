@@ -154,10 +154,10 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(const int64_t* __restri
                                                          const uint32_t* __restrict__ Fnode,
                                                          int64_t delta, uint32_t fb, uint32_t fe,
                                                          uint64_t* __restrict__ wedges,
-                                                         uint32_t wedge_cap,
+                                                         uint64_t wedge_cap,
                                                          uint32_t* __restrict__ long_list,
-                                                         uint32_t* __restrict__ counters) {
-    const int lane = threadIdx.x & 31;
+                                                         unsigned long long* __restrict__ wcount,
+                                                         uint32_t* __restrict__ lcount) {
     for (uint64_t base = (uint64_t)fb + (uint64_t)blockIdx.x * blockDim.x; base < fe;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t i = base + threadIdx.x;
@@ -186,31 +186,25 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(const int64_t* __restri
             FT[i + kWedgeScan + 1] <= lim)
             is_long = true;
         nw = is_long ? 0u : (uint32_t)__popc(hits);
-        // reserve nw slots per lane with one atomic per warp
-        uint32_t incl = nw;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        uint32_t wbase = 0;
-        if (total) {
-            if (lane == 31) wbase = atomicAdd(counters, total);
-            wbase = __shfl_sync(0xffffffffu, wbase, 31);
-        }
-        const bool fits = total == 0 || (uint64_t)wbase + total <= wedge_cap;
-        if (!fits && lane == 31) atomicMin(counters + 2, wbase);  // valid wedges end here
+        // one block-wide reservation for the wedge slots and the long list
+        unsigned long long wo;
+        uint32_t lo;
+        block_reserve2<8>(nw, is_long ? 1u : 0u, wcount, lcount, wo, lo);
+        if (is_long) long_list[lo] = (uint32_t)i;
+        // a reservation past the capacity goes to the long list instead; the
+        // lowest such start bounds the valid wedge prefix (every slot below it
+        // belongs to a reservation that fit)
+        const bool fits = wo + nw <= wedge_cap;
+        if (nw && !fits) atomicMin(wcount + 1, wo);
         if (nw && fits) {
-            uint32_t o = wbase + incl - nw;
             uint32_t h = hits;
             while (h) {
                 const int s = __ffs(h);
                 h &= h - 1;
-                wedges[o++] = ((uint64_t)i << 32) | (uint32_t)(i + s);
+                wedges[wo++] = ((uint64_t)i << 32) | (uint32_t)(i + s);
             }
         }
-        warp_append(is_long || (nw && !fits), (uint32_t)i, long_list, counters + 1);
+        warp_append(nw && !fits, (uint32_t)i, long_list, lcount);
     }
 }
 
@@ -237,14 +231,15 @@ __global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, const int64_t* 
                                                         const uint32_t* __restrict__ FO,
                                                         int64_t delta, int64_t t_end,
                                                         const uint64_t* __restrict__ wedges,
-                                                        uint32_t wedge_cap,
-                                                        const uint32_t* __restrict__ counters,
+                                                        uint64_t wedge_cap,
+                                                        const unsigned long long* __restrict__ wcount,
                                                         uint64_t* out, uint64_t* stats) {
     __shared__ unsigned long long cells[24];
     zero_cells(cells, 24);
     __syncthreads();
     const SmemSink acc{cells};
-    const uint32_t cnt = min(min(counters[0], wedge_cap), counters[2]);
+    uint64_t cnt = wcount[0] < wedge_cap ? wcount[0] : wedge_cap;
+    if (wcount[1] < cnt) cnt = wcount[1];
     if (blockIdx.x == 0 && threadIdx.x == 0 && stats) stats[2] = cnt;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
          idx += (uint64_t)gridDim.x * blockDim.x) {
@@ -264,13 +259,13 @@ __global__ void __launch_bounds__(256) tri_long_kernel(PView P, const int64_t* _
                                                        const uint32_t* __restrict__ Foff,
                                                        int64_t delta, int64_t t_end,
                                                        const uint32_t* __restrict__ list,
-                                                       const uint32_t* __restrict__ counters,
+                                                       const uint32_t* __restrict__ lcount,
                                                        uint64_t* out, uint64_t* stats) {
     __shared__ unsigned long long cells[24];
     zero_cells(cells, 24);
     __syncthreads();
     const SmemSink acc{cells};
-    const uint32_t cnt = counters[1];
+    const uint32_t cnt = *lcount;
     if (blockIdx.x == 0 && threadIdx.x == 0 && stats) stats[3] = cnt;
     uint32_t my_wedges = 0;
     const int lane = threadIdx.x & 31;
@@ -336,21 +331,26 @@ void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_
     const uint64_t cap = (uint64_t)sm_count() * 8;
     uint64_t grid = (work + 255) / 256;
     if (grid > cap) grid = cap;
-    const uint64_t wedge_cap64 = work + 1024;  // overflow spills to the long list
-    const uint32_t wedge_cap = (uint32_t)(wedge_cap64 < 0xFFFFFFF0ull ? wedge_cap64 : 0xFFFFFFF0ull);
+    const uint64_t wedge_cap = work + 1024;  // overflow spills to the long list
     uint64_t* wedges = dalloc<uint64_t>(wedge_cap, st);
-    uint32_t* long_list = dalloc<uint32_t>(work + 3, st);
-    uint32_t* counters = long_list + work;  // [0] wedges reserved, [1] long list, [2] valid end
-    TM_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), st));
-    TM_CUDA(cudaMemsetAsync(counters + 2, 0xFF, sizeof(uint32_t), st));
+    // [0] wedge slots reserved (u64: up to kWedgeScan per record), [1] valid
+    // end, then the u32 long-list fill
+    uint64_t* wbuf = dalloc<uint64_t>(3, st);
+    unsigned long long* wcount = reinterpret_cast<unsigned long long*>(wbuf);
+    uint32_t* lcount = reinterpret_cast<uint32_t*>(wbuf + 2);
+    uint32_t* long_list = dalloc<uint32_t>(work + 1, st);
+    TM_CUDA(cudaMemsetAsync(wcount, 0, sizeof(uint64_t), st));
+    TM_CUDA(cudaMemsetAsync(wcount + 1, 0xFF, sizeof(uint64_t), st));
+    TM_CUDA(cudaMemsetAsync(lcount, 0, sizeof(uint32_t), st));
     TM_LAUNCH("tri_filter", st, tri_filter_kernel, (unsigned)grid, 256, 0, f.t, f.nbr, f.node, delta,
-              f_begin, f_end, wedges, wedge_cap, long_list, counters);
+              f_begin, f_end, wedges, wedge_cap, long_list, wcount, lcount);
     TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pview(g), f.t, f.nbr, f.ord,
-              delta, t_end, wedges, wedge_cap, counters, d_out, d_stats);
+              delta, t_end, wedges, wedge_cap, wcount, d_out, d_stats);
     TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pview(g), f.t, f.nbr, f.ord,
-              f.node, f.off, delta, t_end, long_list, counters, d_out, d_stats);
+              f.node, f.off, delta, t_end, long_list, lcount, d_out, d_stats);
     dfree(wedges, st);
     dfree(long_list, st);
+    dfree(wbuf, st);
 }
 
 void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
