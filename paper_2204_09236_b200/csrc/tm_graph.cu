@@ -7,10 +7,11 @@
 //      edge order is the reference's (t, ordinal) total order;
 //   3. stable radix sort of the 2m incident records (emitted in that order)
 //      by node -> S, the per-node time-ordered sequences;
-//   4. stable radix sort of the edges by unordered pair {min, max} -> P, the
-//      per-pair time-sorted edge lists (PairEdgeIndex), which are also each
-//      endpoint's same-neighbour runs.  Keys carry their payload in the low
-//      bits when it fits (keys-only sorts).
+//   4. P, the per-pair time-sorted edge lists (PairEdgeIndex), which are also
+//      each endpoint's same-neighbour runs: the max-side records of S are
+//      already in (max, t, ordinal) order, so a stable sort of them by the min
+//      endpoint alone yields (min, max, t, ordinal) -- nb key bits instead of
+//      2 nb.  Keys carry their payload in the low bits (keys-only sorts).
 #include "tm_primitives.cuh"
 
 namespace tmb {
@@ -106,11 +107,12 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedE
                                 const uint32_t* __restrict__ off,
                                 int64_t* __restrict__ S_t, uint32_t* __restrict__ S_nbr,
                                 uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
-                                uint32_t* __restrict__ omask, uint32_t* __restrict__ fmask) {
+                                uint32_t* __restrict__ omask, uint32_t* __restrict__ fmask,
+                                uint32_t* __restrict__ xmask) {
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t q = base + threadIdx.x;
-        uint32_t out = 0, fwd = 0;
+        uint32_t out = 0, fwd = 0, mx = 0;
         if (q < R) {
             const uint64_t key = __ldcs(skeys + q);
             const uint32_t r = (uint32_t)key;
@@ -122,15 +124,18 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedE
             const uint32_t du = off[u + 1] - off[u], dx = off[x + 1] - off[x];
             fwd = (dx > du || (dx == du && x > u)) ? 1u : 0u;
             out = side ^ 1u;
+            mx = x < u ? 1u : 0u;  // u is the pair's larger endpoint
             __stcs(S_t + q, e.t);
             __stcs(S_ord + q, (perm ? perm[p] : p) | (fwd << 31));
             __stcs(S_node + q, u);
             __stcs(S_nbr + q, x | (side << 31));
         }
         const unsigned ob = __ballot_sync(0xffffffffu, out), fb = __ballot_sync(0xffffffffu, fwd);
+        const unsigned xb = __ballot_sync(0xffffffffu, mx);
         if ((threadIdx.x & 31) == 0 && q < R) {
             omask[q >> 5] = ob;
             fmask[q >> 5] = fb;
+            xmask[q >> 5] = xb;
         }
     }
 }
@@ -148,45 +153,71 @@ __global__ void offsets_from_keys_kernel(const uint64_t* __restrict__ keys, uint
     }
 }
 
-// pair keys of the edges in (t, ordinal) order: (min << nb | max) [<< pbits | p]
-__global__ void pair_keys_kernel(const PackedEdge* __restrict__ E, uint64_t m, int nb, int pbits,
-                                 bool packed, uint64_t* __restrict__ keys,
-                                 uint32_t* __restrict__ vals) {
-    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
-         p += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = E[p].src, b = E[p].dst;
-        const uint64_t key2 = ((uint64_t)min(a, b) << nb) | max(a, b);
-        if (packed) {
-            keys[p] = (key2 << pbits) | p;
-        } else {
-            keys[p] = key2;
-            vals[p] = (uint32_t)p;
+// pair keys from the max-side records of S (in (max, t, ordinal) order):
+// min << 32 | p, compacted by the xmask prefix
+__global__ void pair_keys_kernel(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ S_nbr,
+                                 const uint32_t* __restrict__ xmask, const uint32_t* __restrict__ xpref,
+                                 uint64_t R, uint64_t* __restrict__ pkeys) {
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
+         q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t word = xmask[q >> 5], bit = 1u << (q & 31);
+        if (word & bit) {
+            const uint32_t j = xpref[q >> 5] + __popc(word & (bit - 1u));
+            pkeys[j] = ((uint64_t)(__ldcs(S_nbr + q) & kNodeMask) << 32) | ((uint32_t)__ldcs(skeys + q) >> 1);
         }
     }
 }
 
-__global__ void gather_p_kernel(const uint64_t* __restrict__ pkeys, const uint32_t* __restrict__ pvals,
-                                uint64_t m, int nb, int pbits, bool packed,
-                                const uint32_t* __restrict__ perm, const PackedEdge* __restrict__ E,
-                                int64_t* __restrict__ P_t, uint32_t* __restrict__ P_ord,
-                                uint32_t* __restrict__ P_min, uint32_t* __restrict__ P_max,
-                                uint32_t* __restrict__ P_w) {
-    const uint64_t nmask = (1ull << nb) - 1;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t key = pkeys[k];
-        const uint64_t key2 = packed ? key >> pbits : key;
-        const uint32_t p = packed ? (uint32_t)(key & ((1ull << pbits) - 1)) : pvals[k];
-        const uint32_t a = (uint32_t)(key2 >> nb), b = (uint32_t)(key2 & nmask);
-        const PackedEdge ed = E[p];
-        const uint32_t dir_min = ed.src == a ? 0u : 1u;  // 0: min -> max
-        const bool first = k == 0 || (packed ? pkeys[k - 1] >> pbits : pkeys[k - 1]) != key2;
-        const bool last = k == m - 1 || (packed ? pkeys[k + 1] >> pbits : pkeys[k + 1]) != key2;
-        P_t[k] = ed.t;
-        P_ord[k] = perm ? perm[p] : p;
-        P_min[k] = a;
-        P_max[k] = b;
-        P_w[k] = (dir_min << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u);
+// P records from the sorted pair keys (min << 32 | p): the max endpoint is
+// the edge's other one; group first/last flags compare (min, max) with the
+// neighbours, staged through shared memory (block-edge neighbours re-read).
+__device__ __forceinline__ void pair_of(const uint64_t* __restrict__ pkeys,
+                                        const PackedEdge* __restrict__ E, uint64_t k,
+                                        uint32_t& a, uint32_t& b) {
+    const uint64_t key = pkeys[k];
+    const PackedEdge e = E[(uint32_t)key];
+    a = (uint32_t)(key >> 32);
+    b = e.src ^ e.dst ^ a;
+}
+
+__global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restrict__ pkeys, uint64_t m,
+                                                       const uint32_t* __restrict__ perm,
+                                                       const PackedEdge* __restrict__ E,
+                                                       int64_t* __restrict__ P_t,
+                                                       uint32_t* __restrict__ P_ord,
+                                                       uint32_t* __restrict__ P_min,
+                                                       uint32_t* __restrict__ P_max,
+                                                       uint32_t* __restrict__ P_w) {
+    __shared__ uint32_t s_a[258], s_b[258];
+    const int tid = threadIdx.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = base + tid;
+        uint32_t a = 0, b = 0, p = 0;
+        PackedEdge ed{};
+        if (k < m) {
+            const uint64_t key = pkeys[k];
+            p = (uint32_t)key;
+            ed = E[p];
+            a = (uint32_t)(key >> 32);
+            b = ed.src ^ ed.dst ^ a;
+            s_a[tid + 1] = a;
+            s_b[tid + 1] = b;
+        }
+        if (tid == 0 && k > 0 && k - 1 < m) pair_of(pkeys, E, k - 1, s_a[0], s_b[0]);
+        if (tid == (int)blockDim.x - 1 && k + 1 < m) pair_of(pkeys, E, k + 1, s_a[tid + 2], s_b[tid + 2]);
+        __syncthreads();
+        if (k < m) {
+            const bool first = k == 0 || s_a[tid] != a || s_b[tid] != b;
+            const bool last = k + 1 == m || s_a[tid + 2] != a || s_b[tid + 2] != b;
+            const uint32_t dir_min = ed.src == a ? 0u : 1u;  // 0: min -> max
+            __stcs(P_t + k, ed.t);
+            __stcs(P_ord + k, perm ? perm[p] : p);
+            __stcs(P_min + k, a);
+            __stcs(P_max + k, b);
+            __stcs(P_w + k, (dir_min << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u));
+        }
+        __syncthreads();
     }
 }
 
@@ -405,31 +436,29 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         TM_LAUNCH("offsets", s, offsets_from_keys_kernel, grid_for(R), 256, 0, nk0, R, n, g.off);
         TM_CUDA(cudaMemsetAsync(g.S_omask + (nw - 1), 0, sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.S_fmask + (nw - 1), 0, sizeof(uint32_t), s));
+        uint32_t* xmask = dalloc<uint32_t>(nw, s);
+        uint32_t* xpref = dalloc<uint32_t>(nw + 1, s);
+        TM_CUDA(cudaMemsetAsync(xmask + (nw - 1), 0, sizeof(uint32_t), s));
         TM_LAUNCH("gather_s", s, gather_s_kernel, grid_for(R), 256, 0, perm, E, nk0, R, g.off, g.S_t,
-                  g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask);
-        dfree(nk0, s);
-        dfree(nk1, s);
+                  g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
         exclusive_scan<uint32_t>(PopcLoad{g.S_omask}, nw, g.S_opref, s);
 
-        // 3. P: stable sort of the edges by unordered pair {min, max}
-        const int pbits = bit_width_u64(m - 1 ? m - 1 : 1);
-        const bool packed = 2 * nb + pbits <= 64;
+        // 3. P: the max-side records (one per edge, (max, t, ordinal) order)
+        //    stably sorted by the min endpoint
+        exclusive_scan<uint32_t>(PopcLoad{xmask}, nw, xpref, s);
         uint64_t* pk0 = dalloc<uint64_t>(m + kSortPad, s);
-        uint64_t* pk1 = dalloc<uint64_t>(m + kSortPad, s);
-        uint32_t* pv0 = packed ? nullptr : dalloc<uint32_t>(m + kSortPad, s);
-        uint32_t* pv1 = packed ? nullptr : dalloc<uint32_t>(m + kSortPad, s);
-        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(m), 256, 0, E, m, nb, pbits, packed, pk0,
-                  pv0);
-        if (packed) radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, pbits, pbits + 2 * nb, s);
-        else radix_sort<uint64_t>(pk0, pv0, pk1, pv1, m, 0, 2 * nb, s);
-        TM_LAUNCH("gather_p", s, gather_p_kernel, grid_for(m), 256, 0, pk0, pv0, m, nb, pbits, packed,
-                  perm, E, g.P_t, g.P_ord, g.P_min, g.P_max, g.P_w);
-        TM_LAUNCH("pair_offsets", s, pair_offsets_kernel, grid_for(m), 256, 0, pk0, m, n,
-                  packed ? pbits + nb : nb, g.pofs);
+        uint64_t* pk1 = nk1;  // R + pad >= m + pad
+        nk1 = nullptr;
+        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, xmask, xpref, R, pk0);
+        dfree(nk0, s);
+        dfree(xmask, s);
+        dfree(xpref, s);
+        radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
+        TM_LAUNCH("gather_p", s, gather_p_kernel, grid_for(m), 256, 0, pk0, m, perm, E, g.P_t, g.P_ord,
+                  g.P_min, g.P_max, g.P_w);
+        TM_LAUNCH("pair_offsets", s, pair_offsets_kernel, grid_for(m), 256, 0, pk0, m, n, 32, g.pofs);
         dfree(pk0, s);
-        dfree(pk1, s);
-        dfree(pv0, s);
-        dfree(pv1, s);
+        dfree(pk1, s);  // (the node sort's second buffer)
         dfree(E, s);
     }
     if (perm) dfree(perm, s);
