@@ -40,7 +40,7 @@ METRIC = "temporal edges/sec, exact 36-motif count (1/2/4/8 B200); % of HBM roof
 #   star_work / tri_work run on the filtered worklists only (random access, no streaming model)
 #   radix_downsweep per key per digit pass: key (+ value) read + write
 #                 node sort: packed u64 keys over 2m records, ceil(nb/8) passes
-#                 pair sort: packed u64 keys over m edges, ceil(2nb/8) passes
+#                 pair sort: packed u64 keys (min << 32 | edge) over m edges, ceil(nb/8) passes
 #                 t sort:    packed u64 keys over m edges, ceil(tbits/8) passes (unsorted input only)
 #   scan          per element: predicate inputs read (4 B) + u32 output written (4 B)
 def algo_bytes(n, m, t):
@@ -51,9 +51,8 @@ def algo_bytes(n, m, t):
     unsorted = bool(m > 1 and (np.diff(t) < 0).any())
     # node sort: packed u64 keys (node << 32 | record), keys only
     sort = R * 8 * 2 * ((nb + 7) // 8)
-    # pair sort: packed u64 keys when 2nb + pbits <= 64, else u64 key + u32 value
-    pk = 8 if 2 * nb + pbits <= 64 else 12
-    sort += m * pk * 2 * ((2 * nb + 7) // 8)
+    # pair sort: the max-side records re-sorted by the min endpoint, keys only
+    sort += m * 8 * 2 * ((nb + 7) // 8)
     if unsorted:
         sort += m * (8 if tb + pbits <= 64 else 12) * 2 * ((tb + 7) // 8)
     return {"star_filter": m * 12, "tri_filter": m * 12, "radix_downsweep": sort,

@@ -6,12 +6,14 @@
 // and records enter the sort in (t, ordinal) order, so ties keep input order.
 //
 // Scan: chunked reduce-then-scan (one contiguous chunk per block, no
-// inter-block waiting).  Sort: LSD, 8-bit digits, 4096-key tiles; per pass an
+// inter-block waiting).  Sort: LSD, 8-bit digits, 2048-key tiles; per pass an
 // upsweep (per-tile digit counts), a row scan (one block per digit) and a
 // persistent downsweep that streams the next tile into shared memory with TMA
 // (cp.async.bulk + mbarrier) while it ranks the current one with per-warp
-// __match_any_sync (stable), reorders it in shared memory and writes each
-// digit run as one burst.  Keys carry their payload in the low bits when it
+// __match_any_sync (stable), reorders it in place in shared memory and writes
+// each digit run as one burst.  The per-warp ranking chain is what bounds a
+// pass (profiles/sortbench.cu ablations: the same kernel with ranking removed
+// streams at ~6 TB/s).  Keys carry their payload in the low bits when it
 // fits, so most sorts are keys-only.
 #pragma once
 
@@ -346,92 +348,6 @@ static __global__ void __launch_bounds__(256) radix_scan_counts(const uint32_t* 
     if (threadIdx.x == 0) totals[d] = carry;
 }
 
-template <typename K, bool kVals, int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK) radix_downsweep(const K* __restrict__ kin,
-                                                         const uint32_t* __restrict__ vin,
-                                                         K* __restrict__ kout,
-                                                         uint32_t* __restrict__ vout, uint64_t n,
-                                                         int shift,
-                                                         const uint32_t* __restrict__ tile_offsets,
-                                                         uint32_t ntiles,
-                                                         const uint32_t* __restrict__ totals) {
-    constexpr int NW = BLOCK / 32;
-    constexpr int TILE = BLOCK * ITEMS;
-    static_assert(BLOCK >= kRadix, "one digit per thread");
-    extern __shared__ __align__(16) unsigned char rs_smem[];
-    K* skeys = reinterpret_cast<K*>(rs_smem);
-    uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + TILE);
-    __shared__ uint32_t wcnt[NW][kRadix];
-    __shared__ uint32_t dstart[kRadix];
-    __shared__ uint32_t dglob[kRadix];
-
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    for (int i = tid; i < NW * kRadix; i += BLOCK) (&wcnt[0][0])[i] = 0;
-    const uint64_t tbase = (uint64_t)blockIdx.x * TILE;
-    const unsigned lt = (1u << lane) - 1u;
-    K key[ITEMS];
-    uint32_t val[kVals ? ITEMS : 1];
-    uint32_t rank[ITEMS];
-#pragma unroll
-    for (int r = 0; r < ITEMS; ++r) {
-        const uint64_t i = tbase + (uint64_t)w * (ITEMS * 32) + r * 32 + lane;
-        const bool valid = i < n;
-        key[r] = valid ? kin[i] : K(0);
-        if (kVals) val[r] = valid ? vin[i] : 0u;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < ITEMS; ++r) {
-        const uint64_t i = tbase + (uint64_t)w * (ITEMS * 32) + r * 32 + lane;
-        const bool valid = i < n;
-        const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 255u) : 256u;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t prev = valid ? wcnt[w][d] : 0u;
-        rank[r] = prev + __popc(peers & lt);
-        __syncwarp();
-        if (valid && (peers & lt) == 0) wcnt[w][d] = prev + __popc(peers);
-        __syncwarp();
-    }
-    __syncthreads();
-    uint32_t cnt = 0;
-    if (tid < kRadix) {
-        uint32_t run = 0;
-#pragma unroll
-        for (int ww = 0; ww < NW; ++ww) {
-            const uint32_t c = wcnt[ww][tid];
-            wcnt[ww][tid] = run;
-            run += c;
-        }
-        cnt = run;
-    }
-    const uint32_t ex = block_exclusive_scan<uint32_t, NW>(cnt, nullptr);
-    const uint32_t dbase = block_exclusive_scan<uint32_t, NW>(tid < kRadix ? totals[tid] : 0u, nullptr);
-    if (tid < kRadix) {
-        dstart[tid] = ex;
-        dglob[tid] = tile_offsets[(uint64_t)tid * ntiles + blockIdx.x] + dbase;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < ITEMS; ++r) {
-        const uint64_t i = tbase + (uint64_t)w * (ITEMS * 32) + r * 32 + lane;
-        if (i < n) {
-            const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
-            const uint32_t q = dstart[d] + wcnt[w][d] + rank[r];
-            skeys[q] = key[r];
-            if (kVals) svals[q] = val[r];
-        }
-    }
-    __syncthreads();
-    const uint32_t tile_n = (uint32_t)((n - tbase) < (uint64_t)TILE ? (n - tbase) : (uint64_t)TILE);
-    for (uint32_t i = tid; i < tile_n; i += BLOCK) {
-        const K k = skeys[i];
-        const uint32_t d = (uint32_t)(k >> shift) & 255u;
-        const uint32_t dest = dglob[d] + (i - dstart[d]);
-        kout[dest] = k;
-        if (kVals) vout[dest] = svals[i];
-    }
-}
-
 // ---- TMA-pipelined persistent downsweep ----------------------------------
 // Each block loops over tiles blockIdx.x, +gridDim.x, ...; one elected thread
 // streams tile i+1 into the other shared-memory stage with cp.async.bulk
@@ -466,27 +382,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
-template <typename K, bool kVals>
-__global__ void __launch_bounds__(512, 2) radix_downsweep_tma(const K* __restrict__ kin,
-                                                              const uint32_t* __restrict__ vin,
-                                                              K* __restrict__ kout,
-                                                              uint32_t* __restrict__ vout, uint64_t n,
-                                                              int shift,
-                                                              const uint32_t* __restrict__ tile_offsets,
-                                                              uint32_t ntiles,
-                                                              const uint32_t* __restrict__ totals) {
-    constexpr int BLOCK = 512, NW = BLOCK / 32, ITEMS = 8, TILE = BLOCK * ITEMS;
+template <typename K, bool kVals, int BLOCK, int ITEMS, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __restrict__ kin,
+                                                                   const uint32_t* __restrict__ vin,
+                                                                   K* __restrict__ kout,
+                                                                   uint32_t* __restrict__ vout, uint64_t n,
+                                                                   int shift,
+                                                                   const uint32_t* __restrict__ tile_offsets,
+                                                                   uint32_t ntiles,
+                                                                   const uint32_t* __restrict__ totals) {
+    constexpr int NW = BLOCK / 32, TILE = BLOCK * ITEMS;
+    static_assert(BLOCK >= kRadix, "one digit per thread");
     constexpr uint32_t STAGE_BYTES = TILE * (sizeof(K) + (kVals ? 4 : 0));
     extern __shared__ __align__(128) unsigned char tma_smem[];
-    // [stage0][stage1][out]: each TILE keys (+ TILE vals)
+    // [stage0][stage1]: each TILE keys (+ TILE vals); a tile is reordered in
+    // place in its own stage (its keys are in registers by then)
     auto stage_keys = [&](int s) { return reinterpret_cast<K*>(tma_smem + s * STAGE_BYTES); };
     auto stage_vals = [&](int s) {
         return reinterpret_cast<uint32_t*>(tma_smem + s * STAGE_BYTES + TILE * sizeof(K));
     };
-    K* okeys = stage_keys(2);
-    uint32_t* ovals = stage_vals(2);
-    __shared__ uint16_t wcnt[NW][kRadix];  // per-warp counts <= 256, prefixes <= 4096
-    __shared__ uint32_t dstart[kRadix];
+    __shared__ uint16_t wcnt[NW][kRadix];  // per-warp counts <= 32 * ITEMS, prefixes <= TILE
     __shared__ uint32_t dglob[kRadix];
     __shared__ __align__(8) uint64_t bar[2];
 
@@ -518,75 +433,129 @@ __global__ void __launch_bounds__(512, 2) radix_downsweep_tma(const K* __restric
         for (int i = tid; i < NW * kRadix; i += BLOCK) (&wcnt[0][0])[i] = 0;
         const uint64_t tbase = (uint64_t)tile * TILE;
         const uint32_t tile_n = (uint32_t)((n - tbase) < (uint64_t)TILE ? (n - tbase) : (uint64_t)TILE);
+        // the tile's digit offsets, loaded now and used after the ranking
+        // (keeps the global-load latency off the critical path)
+        const uint32_t toff = tid < kRadix ? __ldg(tile_offsets + (uint64_t)tid * ntiles + tile) : 0u;
         mbar_wait(&bar[s], (it >> 1) & 1);
         __syncthreads();
-        const K* sk = stage_keys(s);
-        uint32_t rank[ITEMS];
+        K* sk = stage_keys(s);
+        uint32_t* sv = stage_vals(s);
+        // digits and match masks of all rounds first (independent, overlapped),
+        // then the warp's sequential per-digit running counts
+        K key[ITEMS];
+        uint32_t val[kVals ? ITEMS : 1];
+        uint32_t dig[ITEMS], rank[ITEMS];
 #pragma unroll
         for (int r = 0; r < ITEMS; ++r) {
             const uint32_t i = w * (ITEMS * 32) + r * 32 + lane;
-            const bool valid = i < tile_n;
-            const uint32_t d = valid ? ((uint32_t)(sk[i] >> shift) & 255u) : 256u;
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
-            const uint32_t prev = valid ? wcnt[w][d] : 0u;
+            key[r] = sk[i];
+            if (kVals) val[r] = sv[i];
+            dig[r] = i < tile_n ? ((uint32_t)(key[r] >> shift) & 255u) : 256u;
+        }
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) rank[r] = __match_any_sync(0xffffffffu, dig[r]);
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const bool valid = dig[r] < 256u;
+            const unsigned peers = rank[r];
+            const uint32_t prev = valid ? wcnt[w][dig[r]] : 0u;
             rank[r] = prev + __popc(peers & lt);
             __syncwarp();
-            if (valid && (peers & lt) == 0) wcnt[w][d] = (uint16_t)(prev + __popc(peers));
+            if (valid && (peers & lt) == 0) wcnt[w][dig[r]] = (uint16_t)(prev + __popc(peers));
             __syncwarp();
         }
         __syncthreads();
         uint32_t cnt = 0;
         if (tid < kRadix) {
-            uint32_t run = 0;
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) cnt += wcnt[ww][tid];
+        }
+        const uint32_t ex = block_exclusive_scan<uint32_t, NW>(cnt, nullptr);
+        if (tid < kRadix) {
+            // tile position of each (warp, digit) run; global minus tile start per digit
+            uint32_t run = ex;
 #pragma unroll
             for (int ww = 0; ww < NW; ++ww) {
                 const uint32_t c = wcnt[ww][tid];
                 wcnt[ww][tid] = (uint16_t)run;
                 run += c;
             }
-            cnt = run;
-        }
-        const uint32_t ex = block_exclusive_scan<uint32_t, NW>(cnt, nullptr);
-        if (tid < kRadix) {
-            dstart[tid] = ex;
-            dglob[tid] = tile_offsets[(uint64_t)tid * ntiles + tile] + dbase;
+            dglob[tid] = toff + dbase - ex;
         }
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < ITEMS; ++r) {
-            const uint32_t i = w * (ITEMS * 32) + r * 32 + lane;
-            if (i < tile_n) {
-                const K k = sk[i];
-                const uint32_t d = (uint32_t)(k >> shift) & 255u;
-                const uint32_t q = dstart[d] + wcnt[w][d] + rank[r];
-                okeys[q] = k;
-                if (kVals) ovals[q] = stage_vals(s)[i];
+            if (dig[r] < 256u) {
+                const uint32_t q = wcnt[w][dig[r]] + rank[r];
+                sk[q] = key[r];
+                if (kVals) sv[q] = val[r];
             }
         }
         __syncthreads();
         for (uint32_t i = tid; i < tile_n; i += BLOCK) {
-            const K k = okeys[i];
-            const uint32_t d = (uint32_t)(k >> shift) & 255u;
-            const uint32_t dest = dglob[d] + (i - dstart[d]);
+            const K k = sk[i];
+            const uint32_t dest = dglob[(uint32_t)(k >> shift) & 255u] + i;
             kout[dest] = k;
-            if (kVals) vout[dest] = ovals[i];
+            if (kVals) vout[dest] = sv[i];
         }
         __syncthreads();
     }
 }
 
-constexpr int kRsBlock = 512;
-constexpr int kRsItems = 8;
-
 constexpr uint64_t kSortPad = 4;
 
-inline bool use_tma_sort() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TM_SORT_TMA");
-        v = (e && e[0] == '0') ? 0 : 1;
+// one pass configuration: tile = BLOCK * ITEMS keys
+template <typename K, int BLOCK, int ITEMS, int MINB>
+void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
+                    int bit_lo, int bit_hi, cudaStream_t s) {
+    constexpr int TILE = BLOCK * ITEMS;
+    const bool with_vals = vals != nullptr;
+    const int passes = (bit_hi - bit_lo + 7) / 8;
+    const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
+    const size_t smem = 2 * TILE * (sizeof(K) + (with_vals ? sizeof(uint32_t) : 0));
+    static bool attr_set = false;
+    if (!attr_set) {
+        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, true, BLOCK, ITEMS, MINB>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(2 * TILE * (sizeof(K) + sizeof(uint32_t)))));
+        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, false, BLOCK, ITEMS, MINB>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(2 * TILE * sizeof(K))));
+        attr_set = true;
     }
-    return v == 1;
+    int per_sm = 0;
+    if (with_vals)
+        TM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, radix_downsweep_tma<K, true, BLOCK, ITEMS, MINB>, BLOCK, smem));
+    else
+        TM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, radix_downsweep_tma<K, false, BLOCK, ITEMS, MINB>, BLOCK, smem));
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t ncount = (uint64_t)kRadix * ntiles;
+    uint32_t* counts = dalloc<uint32_t>(2 * ncount + (uint64_t)kRadix * passes, s);
+    uint32_t* offs = counts + ncount;
+    uint32_t* totals = offs + ncount;  // 256 digit totals (per pass, reused)
+    const unsigned pgrid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * per_sm);
+    for (int p = 0; p < passes; ++p) {
+        const int shift = bit_lo + 8 * p;
+        TM_LAUNCH("radix_upsweep", s, (radix_upsweep<K, BLOCK, ITEMS>), ntiles, BLOCK, 0, keys, n, shift,
+                  counts, ntiles);
+        TM_LAUNCH("radix_scan", s, radix_scan_counts, kRadix, 256, 0, counts, ntiles, offs, totals);
+        if (with_vals) {
+            TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, true, BLOCK, ITEMS, MINB>), pgrid, BLOCK,
+                      smem, keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
+            uint32_t* tv = vals;
+            vals = vals_alt;
+            vals_alt = tv;
+        } else {
+            TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, false, BLOCK, ITEMS, MINB>), pgrid, BLOCK,
+                      smem, keys, nullptr, keys_alt, nullptr, n, shift, offs, ntiles, totals);
+        }
+        K* tk = keys;
+        keys = keys_alt;
+        keys_alt = tk;
+    }
+    dfree(counts, s);
 }
 
 // Stable sort of keys (and u32 values when vals != nullptr) on key bits
@@ -597,63 +566,9 @@ template <typename K>
 void radix_sort(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
                 int bit_lo, int bit_hi, cudaStream_t s) {
     if (n <= 1 || bit_hi <= bit_lo) return;
-    constexpr int TILE = kRsBlock * kRsItems;
-    const bool with_vals = vals != nullptr;
-    const int passes = (bit_hi - bit_lo + 7) / 8;
-    const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
-    const size_t smem = TILE * (sizeof(K) + (with_vals ? sizeof(uint32_t) : 0));
-    const size_t tma_smem = 3 * smem;
-    static bool attr_set = false;
-    if (!attr_set) {
-        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(3 * TILE * (sizeof(K) + sizeof(uint32_t)))));
-        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(3 * TILE * sizeof(K))));
-        TM_CUDA(cudaFuncSetAttribute(radix_downsweep<K, true, kRsBlock, kRsItems>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(TILE * (sizeof(K) + sizeof(uint32_t)))));
-        TM_CUDA(cudaFuncSetAttribute(radix_downsweep<K, false, kRsBlock, kRsItems>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(TILE * sizeof(K))));
-        attr_set = true;
-    }
-    const uint64_t ncount = (uint64_t)kRadix * ntiles;
-    uint32_t* counts = dalloc<uint32_t>(2 * ncount + (uint64_t)kRadix * passes, s);
-    uint32_t* offs = counts + ncount;
-    uint32_t* totals = offs + ncount;  // 256 digit totals (per pass, reused)
-    for (int p = 0; p < passes; ++p) {
-        const int shift = bit_lo + 8 * p;
-        TM_LAUNCH("radix_upsweep", s, (radix_upsweep<K, kRsBlock, kRsItems>), ntiles, kRsBlock, 0, keys,
-                  n, shift, counts, ntiles);
-        TM_LAUNCH("radix_scan", s, radix_scan_counts, kRadix, 256, 0, counts, ntiles, offs, totals);
-        const bool tma = use_tma_sort();
-        const unsigned pgrid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * 2);
-        if (with_vals && tma) {
-            TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, true>), pgrid, 512, tma_smem, keys,
-                      vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
-            uint32_t* tv = vals;
-            vals = vals_alt;
-            vals_alt = tv;
-        } else if (tma) {
-            TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, false>), pgrid, 512, tma_smem, keys,
-                      nullptr, keys_alt, nullptr, n, shift, offs, ntiles, totals);
-        } else if (with_vals) {
-            TM_LAUNCH("radix_downsweep", s, (radix_downsweep<K, true, kRsBlock, kRsItems>), ntiles,
-                      kRsBlock, smem, keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
-            uint32_t* tv = vals;
-            vals = vals_alt;
-            vals_alt = tv;
-        } else {
-            TM_LAUNCH("radix_downsweep", s, (radix_downsweep<K, false, kRsBlock, kRsItems>), ntiles,
-                      kRsBlock, smem, keys, nullptr, keys_alt, nullptr, n, shift, offs, ntiles, totals);
-        }
-        K* tk = keys;
-        keys = keys_alt;
-        keys_alt = tk;
-    }
-    dfree(counts, s);
+    // 256 threads x 8 keys, 4 blocks per SM (measured best of the
+    // 256/512-thread, 4-16 keys/thread variants on B200, profiles/sortbench.cu)
+    radix_sort_cfg<K, 256, 8, 4>(keys, vals, keys_alt, vals_alt, n, bit_lo, bit_hi, s);
 }
 
 inline int bit_width_u64(uint64_t x) {
