@@ -288,11 +288,17 @@ void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do
         TM_CUDA(cudaEventCreate(&e2));
         TM_CUDA(cudaEventRecord(e0, s));
     }
-    if (do_star && g.R) star_full(g, delta, cb, ce, t_end, g.d_acc, g.d_acc + 56);
-    if (tm) TM_CUDA(cudaEventRecord(e1, s));
+    // star pass on a side stream, concurrent with the triangle pass on s
+    // (both mostly latency-bound gathers; they accumulate into disjoint cells)
+    cudaStream_t ss = g.aux[1] ? g.aux[1] : s;
+    if (do_star && g.R) {
+        stream_after(g, ss, s);
+        star_full(g, delta, cb, ce, t_end, g.d_acc, g.d_acc + 56, ss);
+    }
+    if (tm) TM_CUDA(cudaEventRecord(e1, ss));
     if (do_tri && g.R) {
         const int fm = tri_mode == TM_TRI_REMOVAL ? 1 : 0;
-        build_forward(g, fm);
+        build_forward(g, fm, s);
         const Forward& f = g.fwd[fm];
         uint32_t fb = 0, fe = (uint32_t)f.len;
         if (!full) {
@@ -300,6 +306,10 @@ void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do
             fe = read_u32(f.off, ce, s);
         }
         tri_oriented(g, f, delta, fb, fe, t_end, g.d_acc + 32, g.d_acc + 56);
+    }
+    if (ss != s) {
+        TM_CUDA(cudaEventRecord(g.ev_join, ss));
+        TM_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
     }
     if (tm) TM_CUDA(cudaEventRecord(e2, s));
     uint64_t* h = pinned_acc();
@@ -310,8 +320,8 @@ void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do
     std::memcpy(g.stats, h + 56, 8 * sizeof(uint64_t));
     if (tm) {
         float a = 0, b = 0;
-        cudaEventElapsedTime(&a, e0, e1);
-        cudaEventElapsedTime(&b, e1, e2);
+        cudaEventElapsedTime(&a, e0, e1);  // star pass (side stream)
+        cudaEventElapsedTime(&b, e0, e2);  // triangle pass, overlapping it
         tm->star_pair_ms = a;
         tm->triangle_ms = b;
         cudaEventDestroy(e0);
@@ -757,7 +767,7 @@ int tm_partition_centers(const tm_graph* g, uint32_t world, uint32_t rank, uint3
         const uint64_t n = G->g.n;
         const auto& off = host_off(G);
         // cost(u) = |S_u| + |F_u| (star records + forward wedges' first edges)
-        build_forward(G->g, 0);
+        build_forward(G->g, 0, G->g.stream);
         std::vector<uint32_t> foff(n + 1);
         TM_CUDA(cudaMemcpyAsync(foff.data(), G->g.fwd[0].off, (n + 1) * 4, cudaMemcpyDeviceToHost,
                                 G->g.stream));

@@ -353,6 +353,13 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
                  uint64_t m, uint64_t n) {
     cudaStream_t s = g.stream;
     if (2 * m > 0xFFFFFFF0ull) throw tm_error(9, "graph too large: 2m must fit 32-bit positions");
+    for (auto& a : g.aux)
+        if (!a) TM_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+    if (!g.ev_fork) {
+        TM_CUDA(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
+        TM_CUDA(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
+        TM_CUDA(cudaEventCreateWithFlags(&g.fwd_ready, cudaEventDisableTiming));
+    }
     if (n > kNodeMask) throw tm_error(9, "graph too large: node ids must fit 31 bits");
     g.n = n;
     g.m = m;
@@ -443,6 +450,13 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
                   g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
         exclusive_scan<uint32_t>(PopcLoad{g.S_omask}, nw, g.S_opref, s);
 
+        // the forward sequences (degree orientation) only need S: build them
+        // on a side stream while the pair index is sorted
+        stream_after(g, g.aux[0], s);
+        build_forward(g, 0, g.aux[0]);
+        TM_CUDA(cudaEventRecord(g.fwd_ready, g.aux[0]));
+        g.fwd_pending = true;
+
         // 3. P: the max-side records (one per edge, (max, t, ordinal) order)
         //    stably sorted by the min endpoint
         exclusive_scan<uint32_t>(PopcLoad{xmask}, nw, xpref, s);
@@ -465,10 +479,18 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     g.max_degree = 0;  // not needed by the layout (positions are global 32-bit)
 }
 
-void build_forward(DeviceGraph& g, int mode) {
+void stream_after(DeviceGraph& g, cudaStream_t st, cudaStream_t from) {
+    if (st == from) return;
+    TM_CUDA(cudaEventRecord(g.ev_fork, from));
+    TM_CUDA(cudaStreamWaitEvent(st, g.ev_fork, 0));
+}
+
+void build_forward(DeviceGraph& g, int mode, cudaStream_t s) {
     Forward& f = g.fwd[mode];
-    if (f.valid) return;
-    cudaStream_t s = g.stream;
+    if (f.valid) {
+        if (mode == 0 && g.fwd_pending) TM_CUDA(cudaStreamWaitEvent(s, g.fwd_ready, 0));
+        return;
+    }
     const uint64_t R = g.R;
     f.mode = mode;
     f.len = g.m;  // every edge is forward from exactly one endpoint
@@ -540,6 +562,18 @@ void build_s_pidx(DeviceGraph& g) {
 
 void free_graph(DeviceGraph& g) {
     cudaStream_t s = g.stream;
+    for (auto& a : g.aux)
+        if (a) {
+            cudaStreamSynchronize(a);
+            cudaStreamDestroy(a);
+            a = nullptr;
+        }
+    for (cudaEvent_t* e : {&g.ev_fork, &g.ev_join, &g.fwd_ready})
+        if (*e) {
+            cudaEventDestroy(*e);
+            *e = nullptr;
+        }
+    g.fwd_pending = false;
     dfree(g.S_t, s); dfree(g.S_nbr, s); dfree(g.S_ord, s); dfree(g.S_node, s);
     dfree(g.S_omask, s); dfree(g.S_opref, s); dfree(g.S_fmask, s); dfree(g.S_pidx, s);
     dfree(g.off, s);

@@ -93,6 +93,12 @@ struct DeviceGraph {
     uint32_t max_degree = 0;
     cudaStream_t stream = nullptr;
     bool owns_stream = false;
+    // Side streams forked from `stream` with events: aux[0] builds the forward
+    // sequences while the pair index is sorted, aux[1] runs the star pass
+    // while the triangle pass runs on `stream`.  fwd_ready marks fwd[0].
+    cudaStream_t aux[2] = {nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, fwd_ready = nullptr;
+    bool fwd_pending = false;
 
     int64_t* S_t = nullptr;
     uint32_t* S_nbr = nullptr;
@@ -152,7 +158,11 @@ inline PView pview(const DeviceGraph& g) {
 void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst,
                  const int64_t* d_t, uint64_t m, uint64_t n);
 void free_graph(DeviceGraph& g);
-void build_forward(DeviceGraph& g, int mode);
+// builds fwd[mode] on stream st (no-op when built); for fwd[0] started
+// during build_graph, makes st wait for it
+void build_forward(DeviceGraph& g, int mode, cudaStream_t st);
+// st waits for everything issued so far on from
+void stream_after(DeviceGraph& g, cudaStream_t st, cudaStream_t from);
 void build_s_pidx(DeviceGraph& g);
 // compact the edges with t in [lo, hi) (ingestion order kept); returns the count
 uint64_t slice_edges(const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t, uint64_t m,
@@ -162,7 +172,7 @@ uint64_t slice_edges(const uint32_t* d_src, const uint32_t* d_dst, const int64_t
 // raw star sums (32 u64: Pair[8], C[8], B[8], A[8]) for the centers
 // [c_begin, c_end) and instances whose first edge has t < t_end, added into d_out.
 void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end, int64_t t_end,
-               uint64_t* d_out, uint64_t* d_stats);
+               uint64_t* d_out, uint64_t* d_stats, cudaStream_t st);
 void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
                 const uint64_t* d_begin, const uint64_t* d_end, const uint64_t* d_item_off,
                 uint64_t total_first, uint64_t total_third, const uint64_t* d_third_off,

@@ -361,9 +361,8 @@ __global__ void __launch_bounds__(256) star_items_kernel(
 }  // namespace
 
 void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end, int64_t t_end,
-               uint64_t* d_out, uint64_t* d_stats) {
+               uint64_t* d_out, uint64_t* d_stats, cudaStream_t st) {
     if (c_end <= c_begin || g.m == 0) return;
-    cudaStream_t st = g.stream;
     const uint64_t cap = (uint64_t)sm_count() * 8;
     uint64_t grid = (g.m + 255) / 256;
     if (grid > cap) grid = cap;
