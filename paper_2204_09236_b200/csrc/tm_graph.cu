@@ -87,6 +87,12 @@ struct PackedEdge {
     uint32_t dst;
 };
 
+// one-touch random edge record: a single 16-byte streaming load
+__device__ __forceinline__ PackedEdge load_edge_cs(const PackedEdge* ptr) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(ptr));
+    return PackedEdge{(int64_t)(((uint64_t)v.y << 32) | v.x), v.z, v.w};
+}
+
 // record r = 2p + side of the p-th edge in (t, ordinal) order: key node << 32 | r
 __global__ void pack_edges_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ src,
                                   const uint32_t* __restrict__ dst, const int64_t* __restrict__ t,
@@ -198,7 +204,7 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
         if (k < m) {
             const uint64_t key = pkeys[k];
             p = (uint32_t)key;
-            ed = E[p];
+            ed = load_edge_cs(E + p);
             a = (uint32_t)(key >> 32);
             b = ed.src ^ ed.dst ^ a;
             s_a[tid + 1] = a;
