@@ -304,7 +304,7 @@ def main():
     tm.kernel_timing(enable=False)
     names = ["star_filter", "star_work", "tri_filter", "tri_wedge", "tri_long", "radix_upsweep",
              "radix_downsweep", "radix_scan", "scan", "gather_s", "gather_p", "forward_scatter", "pack_edges", "pair_keys",
-             "time_keys", "perm_from_keys", "validate", "offsets", "pair_offsets", "forward_off"]
+             "time_keys", "perm_from_keys", "validate", "offsets", "forward_off"]
     ktimes = {}
     for nm in names:
         tot_ms, cnt = tm.kernel_time(nm)

@@ -93,18 +93,44 @@ __device__ __forceinline__ PackedEdge load_edge_cs(const PackedEdge* ptr) {
     return PackedEdge{(int64_t)(((uint64_t)v.y << 32) | v.x), v.z, v.w};
 }
 
-// record r = 2p + side of the p-th edge in (t, ordinal) order: key node << 32 | r
-__global__ void pack_edges_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ src,
-                                  const uint32_t* __restrict__ dst, const int64_t* __restrict__ t,
-                                  uint64_t m, PackedEdge* __restrict__ E,
-                                  uint64_t* __restrict__ keys) {
-    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
-         p += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t k = perm ? perm[p] : (uint32_t)p;
-        const uint32_t a = src[k], b = dst[k];
-        E[p] = PackedEdge{t[k], a, b};
-        keys[2 * p] = ((uint64_t)a << 32) | (2 * p);
-        keys[2 * p + 1] = ((uint64_t)b << 32) | (2 * p + 1);
+// record r = 2p + side of the p-th edge in (t, ordinal) order: key node << 32 | r.
+// One block per radix-sort tile (kSortTile keys = kSortTile / 2 edges): the
+// tile's histogram of the first digit (node & 255) is written digit-major like
+// radix_upsweep's, so the node sort skips its first counting pass.
+constexpr int kPackBlock = 256;
+constexpr int kPackEdges = kSortTile / 2;
+__global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
+    const uint32_t* __restrict__ perm, const uint32_t* __restrict__ src,
+    const uint32_t* __restrict__ dst, const int64_t* __restrict__ t, uint64_t m,
+    PackedEdge* __restrict__ E, uint64_t* __restrict__ keys, uint32_t* __restrict__ counts,
+    uint32_t ntiles) {
+    constexpr int NW = kPackBlock / 32;
+    __shared__ uint32_t hist[NW][256];
+    const int w = threadIdx.x >> 5;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int i = threadIdx.x; i < NW * 256; i += kPackBlock) (&hist[0][0])[i] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kPackEdges / kPackBlock; ++j) {
+            const uint64_t p = (uint64_t)tile * kPackEdges + j * kPackBlock + threadIdx.x;
+            if (p < m) {
+                const uint32_t k = perm ? perm[p] : (uint32_t)p;
+                const uint32_t a = src[k], b = dst[k];
+                E[p] = PackedEdge{t[k], a, b};
+                reinterpret_cast<ulonglong2*>(keys)[p] =
+                    make_ulonglong2(((uint64_t)a << 32) | (2 * p), ((uint64_t)b << 32) | (2 * p + 1));
+                atomicAdd(&hist[w][a & 255u], 1u);
+                atomicAdd(&hist[w][b & 255u], 1u);
+            }
+        }
+        __syncthreads();
+        for (int d = threadIdx.x; d < 256; d += kPackBlock) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) c += hist[ww][d];
+            counts[(uint64_t)d * ntiles + tile] = c;
+        }
+        __syncthreads();
     }
 }
 
@@ -193,7 +219,8 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
                                                        uint32_t* __restrict__ P_ord,
                                                        uint32_t* __restrict__ P_min,
                                                        uint32_t* __restrict__ P_max,
-                                                       uint32_t* __restrict__ P_w) {
+                                                       uint32_t* __restrict__ P_w, uint64_t n,
+                                                       uint32_t* __restrict__ pofs) {
     __shared__ uint32_t s_a[258], s_b[258];
     const int tid = threadIdx.x;
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m;
@@ -222,6 +249,11 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
             __stcs(P_min + k, a);
             __stcs(P_max + k, b);
             __stcs(P_w + k, (dir_min << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u));
+            // pofs[x] = first P position whose min endpoint is x (block boundaries)
+            const int64_t prev = k == 0 ? -1 : (int64_t)s_a[tid];
+            for (int64_t x = prev + 1; x <= (int64_t)a; ++x) pofs[x] = (uint32_t)k;
+            if (k + 1 == m)
+                for (int64_t x = (int64_t)a + 1; x <= (int64_t)n; ++x) pofs[x] = (uint32_t)m;
         }
         __syncthreads();
     }
@@ -251,19 +283,6 @@ __global__ void s_pidx_kernel(const int64_t* __restrict__ P_t, const uint32_t* _
         const uint32_t o = P_ord[k], a = P_min[k], b = P_max[k];
         S_pidx[s_locate(S_t, S_ord, off[a], off[a + 1], t, o)] = (uint32_t)k;
         S_pidx[s_locate(S_t, S_ord, off[b], off[b + 1], t, o)] = (uint32_t)k;
-    }
-}
-
-// pofs[x] = first P position whose min endpoint is x
-__global__ void pair_offsets_kernel(const uint64_t* __restrict__ pkeys, uint64_t m, uint64_t n,
-                                    int shift, uint32_t* __restrict__ pofs) {
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const int64_t cur = (int64_t)(pkeys[k] >> shift);
-        const int64_t prev = k ? (int64_t)(pkeys[k - 1] >> shift) : -1;
-        for (int64_t x = prev + 1; x <= cur; ++x) pofs[x] = (uint32_t)k;
-        if (k == m - 1)
-            for (int64_t x = cur + 1; x <= (int64_t)n; ++x) pofs[x] = (uint32_t)m;
     }
 }
 
@@ -443,9 +462,12 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         uint64_t* nk0 = dalloc<uint64_t>(R + kSortPad, s);
         uint64_t* nk1 = dalloc<uint64_t>(R + kSortPad, s);
         PackedEdge* E = dalloc<PackedEdge>(m, s);
-        TM_LAUNCH("pack_edges", s, pack_edges_kernel, grid_for(m), 256, 0, perm, d_src, d_dst, d_t, m, E,
-                  nk0);
-        radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s);
+        const uint32_t ntiles = (uint32_t)((R + kSortTile - 1) / kSortTile);
+        uint32_t* c0 = dalloc<uint32_t>((uint64_t)256 * ntiles, s);
+        TM_LAUNCH("pack_edges", s, pack_edges_kernel, grid_for(m, kPackEdges), kPackBlock, 0, perm, d_src,
+                  d_dst, d_t, m, E, nk0, c0, ntiles);
+        radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s, c0);
+        dfree(c0, s);
         TM_LAUNCH("offsets", s, offsets_from_keys_kernel, grid_for(R), 256, 0, nk0, R, n, g.off);
         TM_CUDA(cudaMemsetAsync(g.S_omask + (nw - 1), 0, sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.S_fmask + (nw - 1), 0, sizeof(uint32_t), s));
@@ -475,8 +497,7 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         dfree(xpref, s);
         radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
         TM_LAUNCH("gather_p", s, gather_p_kernel, grid_for(m), 256, 0, pk0, m, perm, E, g.P_t, g.P_ord,
-                  g.P_min, g.P_max, g.P_w);
-        TM_LAUNCH("pair_offsets", s, pair_offsets_kernel, grid_for(m), 256, 0, pk0, m, n, 32, g.pofs);
+                  g.P_min, g.P_max, g.P_w, n, g.pofs);
         dfree(pk0, s);
         dfree(pk1, s);  // (the node sort's second buffer)
         dfree(E, s);

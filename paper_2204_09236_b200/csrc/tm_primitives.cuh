@@ -503,11 +503,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
 }
 
 constexpr uint64_t kSortPad = 4;
+// sort tile: kSortBlock threads x kSortItems keys (a producer that counts the
+// first digit itself must use the same tiles: digit-major counts[d][tile])
+constexpr int kSortBlock = 256, kSortItems = 8, kSortTile = kSortBlock * kSortItems;
 
 // one pass configuration: tile = BLOCK * ITEMS keys
 template <typename K, int BLOCK, int ITEMS, int MINB>
 void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
-                    int bit_lo, int bit_hi, cudaStream_t s) {
+                    int bit_lo, int bit_hi, cudaStream_t s, const uint32_t* first_counts) {
     constexpr int TILE = BLOCK * ITEMS;
     const bool with_vals = vals != nullptr;
     const int passes = (bit_hi - bit_lo + 7) / 8;
@@ -538,9 +541,14 @@ void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt
     const unsigned pgrid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * per_sm);
     for (int p = 0; p < passes; ++p) {
         const int shift = bit_lo + 8 * p;
-        TM_LAUNCH("radix_upsweep", s, (radix_upsweep<K, BLOCK, ITEMS>), ntiles, BLOCK, 0, keys, n, shift,
-                  counts, ntiles);
-        TM_LAUNCH("radix_scan", s, radix_scan_counts, kRadix, 256, 0, counts, ntiles, offs, totals);
+        const uint32_t* cin = counts;
+        if (p == 0 && first_counts) {
+            cin = first_counts;  // the producer of the keys already counted pass 0
+        } else {
+            TM_LAUNCH("radix_upsweep", s, (radix_upsweep<K, BLOCK, ITEMS>), ntiles, BLOCK, 0, keys, n, shift,
+                      counts, ntiles);
+        }
+        TM_LAUNCH("radix_scan", s, radix_scan_counts, kRadix, 256, 0, cin, ntiles, offs, totals);
         if (with_vals) {
             TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, true, BLOCK, ITEMS, MINB>), pgrid, BLOCK,
                       smem, keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
@@ -564,11 +572,12 @@ void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt
 // pointers at the scratch halves (pointers may be swapped).
 template <typename K>
 void radix_sort(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
-                int bit_lo, int bit_hi, cudaStream_t s) {
+                int bit_lo, int bit_hi, cudaStream_t s, const uint32_t* first_counts = nullptr) {
     if (n <= 1 || bit_hi <= bit_lo) return;
     // 256 threads x 8 keys, 4 blocks per SM (measured best of the
     // 256/512-thread, 4-16 keys/thread variants on B200, profiles/sortbench.cu)
-    radix_sort_cfg<K, 256, 8, 4>(keys, vals, keys_alt, vals_alt, n, bit_lo, bit_hi, s);
+    radix_sort_cfg<K, kSortBlock, kSortItems, 4>(keys, vals, keys_alt, vals_alt, n, bit_lo, bit_hi, s,
+                                                 first_counts);
 }
 
 inline int bit_width_u64(uint64_t x) {

@@ -21,7 +21,8 @@ from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtmotif_b200.so")
+# TM_LIB overrides the library path (A/B runs of two builds of the same API)
+LIB_PATH = os.environ.get("TM_LIB") or os.path.join(HERE, "libtmotif_b200.so")
 
 TM_OK = 0
 TM_ERR_INVALID = 1
