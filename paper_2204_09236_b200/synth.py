@@ -104,11 +104,32 @@ def _gpu_gen(seed: int):
     return g
 
 
+_CDF_CACHE = {}
+
+
+def _gpu_cdf(n, exponent):
+    """Chung-Lu CDF computed on the host (sequential, bit-reproducible) and
+    uploaded once: a device float scan is not run-to-run deterministic."""
+    torch = _torch()
+    key = (n, exponent)
+    if key not in _CDF_CACHE:
+        _CDF_CACHE.clear()
+        _CDF_CACHE[key] = torch.from_numpy(np.cumsum(_chung_lu_weights(n, exponent))).cuda()
+    return _CDF_CACHE[key]
+
+
+def _det_cumsum(x):
+    """Deterministic running sum of non-negative float64 values: fixed-point
+    (2^-20) integer prefix sum, since a device float scan may associate
+    differently from run to run."""
+    torch = _torch()
+    q = torch.round(x * float(1 << 20)).to(torch.int64)
+    return torch.cumsum(q, 0).to(torch.float64) / float(1 << 20)
+
+
 def _chung_lu_draw(n, k, exponent, gen, perm):
     torch = _torch()
-    r = torch.arange(1, n + 1, device="cuda", dtype=torch.float64)
-    w = r.pow(-1.0 / exponent)
-    cdf = torch.cumsum(w / w.sum(), 0)
+    cdf = _gpu_cdf(n, exponent)
     u = torch.rand(k, device="cuda", dtype=torch.float64, generator=gen)
     idx = torch.searchsorted(cdf, u, right=True).clamp_(max=n - 1)
     return perm[idx]
@@ -133,7 +154,7 @@ def power_law_gpu(n: int, m: int, mean_gap: float, seed: int = 2204, exponent: f
     src = draw(m)
     dst = _fix_self_loops(src, draw(m), draw)
     gaps = torch.empty(m, device="cuda", dtype=torch.float64).exponential_(1.0 / mean_gap, generator=gen)
-    t = torch.floor(torch.cumsum(gaps, 0)).to(torch.int64)
+    t = torch.floor(_det_cumsum(gaps)).to(torch.int64)
     return n, src.to(torch.int32), dst.to(torch.int32), t
 
 
@@ -155,8 +176,8 @@ def hub_stress_gpu(n: int = 100_000, m: int = 50_000_000, hubs: int = 20, hub_sh
     src = draw(m)
     dst = _fix_self_loops(src, draw(m), draw)
     nb = (m + burst - 1) // burst
-    starts = torch.cumsum(torch.empty(nb, device="cuda", dtype=torch.float64)
-                          .exponential_(1.0 / burst_gap, generator=gen), 0)
+    starts = _det_cumsum(torch.empty(nb, device="cuda", dtype=torch.float64)
+                         .exponential_(1.0 / burst_gap, generator=gen))
     t = starts.repeat_interleave(burst)[:m] + torch.rand(m, device="cuda", dtype=torch.float64,
                                                           generator=gen) * burst_span
     return n, src.to(torch.int32), dst.to(torch.int32), torch.floor(t).to(torch.int64)
@@ -178,7 +199,7 @@ def triadic_gpu(n: int = 25_000_000, m: int = 100_000_000, closure: float = 0.30
     dst = dst.to(torch.int64)
     # out-adjacency of the base edges by (src, t)
     key = src * (t.max() + 1) + t
-    order = torch.argsort(key)
+    order = torch.argsort(key, stable=True)
     s_src, s_t, s_dst = src[order], t[order], dst[order]
     starts = torch.searchsorted(s_src, torch.arange(n + 1, device="cuda"))
     need = m - mb
