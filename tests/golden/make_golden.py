@@ -10,8 +10,10 @@ container, where /root/reference exists).
   uniform_reference.json reference census for BASELINE config 0
                         (10k nodes, 200k edges, t uniform in [0, 1e6), delta 1000)
   powerlaw_reference.json reference census for BASELINE config 1 (optional, slow)
+  hubstress_reference.json reference census for BASELINE config 2 (100k nodes,
+                        50M edges, delta 3600; numpy generator; optional, slow)
 
-Usage: python tests/golden/make_golden.py [--powerlaw]
+Usage: python tests/golden/make_golden.py [--powerlaw] [--hubstress] [--only-extra]
 """
 from __future__ import annotations
 
@@ -59,8 +61,23 @@ def counters(R, g, delta):
             "tri_countall": [int(x) for x in tr], "tri_removal": [int(x) for x in trr]}
 
 
-def main(with_powerlaw: bool):
+def hubstress_golden(R):
+    from paper_2204_09236_b200 import synth
+    n, s, d, tt = synth.hub_stress()
+    delta = 3600
+    g = R.build_graph(n, s, d, tt)
+    out = {"config": "hubstress_100k_50m", "nodes": n, "edges": int(len(s)), "hash": edge_hash(s, d, tt),
+           "delta": delta, "census": [int(x) for x in R.run_parallel(g, delta, os.cpu_count() or 1)]}
+    R.free(g)
+    json.dump(out, open(os.path.join(HERE, "hubstress_reference.json"), "w"))
+
+
+def main(with_powerlaw: bool, with_hubstress: bool = False, only_extra: bool = False):
     R = Reference()
+    if only_extra:
+        if with_hubstress:
+            hubstress_golden(R)
+        return
     sigs = R.signatures()
 
     toy_text = open(os.path.join(REF_TESTS, "data", "toy.txt")).read()
@@ -128,8 +145,10 @@ def main(with_powerlaw: bool):
                "delta": delta, "census": [int(x) for x in R.run_parallel(g, delta, os.cpu_count() or 1)]}
         R.free(g)
         json.dump(out, open(os.path.join(HERE, "powerlaw_reference.json"), "w"))
+    if with_hubstress:
+        hubstress_golden(R)
     print("golden fixtures written to", HERE)
 
 
 if __name__ == "__main__":
-    main("--powerlaw" in sys.argv)
+    main("--powerlaw" in sys.argv, "--hubstress" in sys.argv, "--only-extra" in sys.argv)
