@@ -328,6 +328,39 @@ def test_config1_powerlaw_full_size_properties(cuda, tm):
         assert census.tolist() == ref["census"]
 
 
+def test_config2_hubstress_full_size_vs_reference(cuda, tm):
+    """BASELINE config 2 at full size (100k nodes, 50M edges with 20 hubs on
+    30 % of the edges, bursty unsorted timestamps -> the GPU time sort runs):
+    census == the reference's own run_parallel census on the identical input
+    (tests/golden/hubstress_reference.json, made by make_golden.py --hubstress),
+    for the whole graph and for a 2-way time-slice split summed."""
+    import hashlib
+    import os
+    from paper_2204_09236_b200 import synth
+    from paper_2204_09236_b200.distributed import time_slice_bounds, time_slice_mask
+    path = os.path.join(os.path.dirname(__file__), "golden", "hubstress_reference.json")
+    if not os.path.exists(path):
+        pytest.skip("hubstress golden not generated")
+    ref = load_golden("hubstress_reference.json")
+    n, s, d, t = synth.hub_stress()
+    h = hashlib.sha256()
+    for a in (s, d, t):
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert h.hexdigest()[:16] == ref["hash"]  # same input as the reference saw
+    delta = ref["delta"]
+    census = tm.run_parallel(tm.GraphContext.build(tm.TemporalGraph.from_arrays(n, s, d, t)),
+                             tm.RunConfig(delta=delta))
+    assert census.counts.tolist() == ref["census"]
+    total = np.zeros(56, np.uint64)
+    for lo, hi in time_slice_bounds(t, 2):
+        keep = time_slice_mask(t, lo, hi, delta)
+        raw = tm.count_edges_time_slice(n, s[keep], d[keep], t[keep], tm.RunConfig(delta=delta), lo, hi)
+        total += raw.as_array()
+    rc = tm.RawCounters.from_array(total)
+    merged = tm.merge_census(rc.star, rc.pair, rc.tri, tm.TriangleMode.count_all)
+    assert merged.counts.tolist() == ref["census"]
+
+
 def test_cpp_host_mirror_driver(cuda, tm, oracle):
     """The C++ header mirror (include/tmotif_b200.hpp) used as a reference
     caller would: toy census == frozen vector; random graph == oracle."""
