@@ -79,19 +79,40 @@ __global__ void perm_from_keys_kernel(const uint64_t* __restrict__ keys, uint64_
         perm[p] = (uint32_t)(keys[p] & kmask);
 }
 
-// Edges packed in (t, ordinal) order, 16 B each, so every later random gather
-// touches one sector; node sort keys for both records of each edge.
-struct PackedEdge {
+// Edge records in (t, ordinal) order, read by random gathers in gather_s
+// and gather_p.  Wide (16 B): any int64 timestamps.  Narrow (8 B): t - t_min
+// as u32 and src ^ dst with "src is the smaller endpoint" in the top bit (node
+// ids are < 2^31), used whenever the time span fits 32 bits -- half the bytes
+// per gather, and the whole array (80 MB at 10M edges) mostly stays in L2.
+struct WideEdge {
     int64_t t;
     uint32_t src;
     uint32_t dst;
 };
-
-// one-touch random edge record: a single 16-byte streaming load
-__device__ __forceinline__ PackedEdge load_edge_cs(const PackedEdge* ptr) {
-    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(ptr));
-    return PackedEdge{(int64_t)(((uint64_t)v.y << 32) | v.x), v.z, v.w};
-}
+struct NarrowEdge {
+    uint32_t trel;
+    uint32_t x;
+};
+template <bool kNarrow>
+struct EdgeCodec;
+template <>
+struct EdgeCodec<false> {
+    using Rec = WideEdge;
+    __device__ static Rec make(int64_t t, uint32_t a, uint32_t b, int64_t) { return Rec{t, a, b}; }
+    __device__ static int64_t time(const Rec& e, int64_t) { return e.t; }
+    __device__ static uint32_t other(const Rec& e, uint32_t u) { return e.src ^ e.dst ^ u; }
+    __device__ static uint32_t dir_from_min(const Rec& e, uint32_t mn) { return e.src == mn ? 0u : 1u; }
+};
+template <>
+struct EdgeCodec<true> {
+    using Rec = NarrowEdge;
+    __device__ static Rec make(int64_t t, uint32_t a, uint32_t b, int64_t tmin) {
+        return Rec{(uint32_t)((uint64_t)t - (uint64_t)tmin), (a ^ b) | (a < b ? 0x80000000u : 0u)};
+    }
+    __device__ static int64_t time(const Rec& e, int64_t tmin) { return tmin + (int64_t)e.trel; }
+    __device__ static uint32_t other(const Rec& e, uint32_t u) { return (e.x & kNodeMask) ^ u; }
+    __device__ static uint32_t dir_from_min(const Rec& e, uint32_t) { return (e.x >> 31) ? 0u : 1u; }
+};
 
 // record r = 2p + side of the p-th edge in (t, ordinal) order: key node << 32 | r.
 // One block per radix-sort tile (kSortTile keys = kSortTile / 2 edges): the
@@ -99,11 +120,12 @@ __device__ __forceinline__ PackedEdge load_edge_cs(const PackedEdge* ptr) {
 // radix_upsweep's, so the node sort skips its first counting pass.
 constexpr int kPackBlock = 256;
 constexpr int kPackEdges = kSortTile / 2;
+template <bool kNarrow>
 __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
     const uint32_t* __restrict__ perm, const uint32_t* __restrict__ src,
-    const uint32_t* __restrict__ dst, const int64_t* __restrict__ t, uint64_t m,
-    PackedEdge* __restrict__ E, uint64_t* __restrict__ keys, uint32_t* __restrict__ counts,
-    uint32_t ntiles) {
+    const uint32_t* __restrict__ dst, const int64_t* __restrict__ t, uint64_t m, int64_t tmin,
+    typename EdgeCodec<kNarrow>::Rec* __restrict__ E, uint64_t* __restrict__ keys,
+    uint32_t* __restrict__ counts, uint32_t ntiles) {
     constexpr int NW = kPackBlock / 32;
     __shared__ uint32_t hist[NW][256];
     const int w = threadIdx.x >> 5;
@@ -116,7 +138,7 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
             if (p < m) {
                 const uint32_t k = perm ? perm[p] : (uint32_t)p;
                 const uint32_t a = src[k], b = dst[k];
-                E[p] = PackedEdge{t[k], a, b};
+                E[p] = EdgeCodec<kNarrow>::make(t[k], a, b, tmin);
                 reinterpret_cast<ulonglong2*>(keys)[p] =
                     make_ulonglong2(((uint64_t)a << 32) | (2 * p), ((uint64_t)b << 32) | (2 * p + 1));
                 atomicAdd(&hist[w][a & 255u], 1u);
@@ -134,7 +156,9 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
     }
 }
 
-__global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedEdge* __restrict__ E,
+template <bool kNarrow>
+__global__ void gather_s_kernel(const uint32_t* __restrict__ perm,
+                                const typename EdgeCodec<kNarrow>::Rec* __restrict__ E, int64_t tmin,
                                 const uint64_t* __restrict__ skeys, uint64_t R,
                                 const uint32_t* __restrict__ off,
                                 int64_t* __restrict__ S_t, uint32_t* __restrict__ S_nbr,
@@ -149,15 +173,16 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm, const PackedE
             const uint64_t key = __ldcs(skeys + q);
             const uint32_t r = (uint32_t)key;
             const uint32_t p = r >> 1, side = r & 1u;
-            const PackedEdge e = E[p];
-            const uint32_t u = (uint32_t)(key >> 32), x = side ? e.src : e.dst;
+            using Codec = EdgeCodec<kNarrow>;
+            const typename Codec::Rec e = E[p];
+            const uint32_t u = (uint32_t)(key >> 32), x = Codec::other(e, u);
             // degree-rank orientation of the triangle pass: forward iff (deg, id) of the
             // neighbour exceeds the center's; kept in the spare top bit of S_ord
             const uint32_t du = off[u + 1] - off[u], dx = off[x + 1] - off[x];
             fwd = (dx > du || (dx == du && x > u)) ? 1u : 0u;
             out = side ^ 1u;
             mx = x < u ? 1u : 0u;  // u is the pair's larger endpoint
-            __stcs(S_t + q, e.t);
+            __stcs(S_t + q, Codec::time(e, tmin));
             __stcs(S_ord + q, (perm ? perm[p] : p) | (fwd << 31));
             __stcs(S_node + q, u);
             __stcs(S_nbr + q, x | (side << 31));
@@ -203,48 +228,52 @@ __global__ void pair_keys_kernel(const uint64_t* __restrict__ skeys, const uint3
 // P records from the sorted pair keys (min << 32 | p): the max endpoint is
 // the edge's other one; group first/last flags compare (min, max) with the
 // neighbours, staged through shared memory (block-edge neighbours re-read).
+template <bool kNarrow>
 __device__ __forceinline__ void pair_of(const uint64_t* __restrict__ pkeys,
-                                        const PackedEdge* __restrict__ E, uint64_t k,
+                                        const typename EdgeCodec<kNarrow>::Rec* __restrict__ E, uint64_t k,
                                         uint32_t& a, uint32_t& b) {
     const uint64_t key = pkeys[k];
-    const PackedEdge e = E[(uint32_t)key];
     a = (uint32_t)(key >> 32);
-    b = e.src ^ e.dst ^ a;
+    b = EdgeCodec<kNarrow>::other(E[(uint32_t)key], a);
 }
 
+template <bool kNarrow>
 __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restrict__ pkeys, uint64_t m,
                                                        const uint32_t* __restrict__ perm,
-                                                       const PackedEdge* __restrict__ E,
+                                                       const typename EdgeCodec<kNarrow>::Rec* __restrict__ E,
+                                                       int64_t tmin,
                                                        int64_t* __restrict__ P_t,
                                                        uint32_t* __restrict__ P_ord,
                                                        uint32_t* __restrict__ P_min,
                                                        uint32_t* __restrict__ P_max,
                                                        uint32_t* __restrict__ P_w, uint64_t n,
                                                        uint32_t* __restrict__ pofs) {
+    using Codec = EdgeCodec<kNarrow>;
     __shared__ uint32_t s_a[258], s_b[258];
     const int tid = threadIdx.x;
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = base + tid;
         uint32_t a = 0, b = 0, p = 0;
-        PackedEdge ed{};
+        typename Codec::Rec ed{};
         if (k < m) {
             const uint64_t key = pkeys[k];
             p = (uint32_t)key;
-            ed = load_edge_cs(E + p);
+            ed = E[p];
             a = (uint32_t)(key >> 32);
-            b = ed.src ^ ed.dst ^ a;
+            b = Codec::other(ed, a);
             s_a[tid + 1] = a;
             s_b[tid + 1] = b;
         }
-        if (tid == 0 && k > 0 && k - 1 < m) pair_of(pkeys, E, k - 1, s_a[0], s_b[0]);
-        if (tid == (int)blockDim.x - 1 && k + 1 < m) pair_of(pkeys, E, k + 1, s_a[tid + 2], s_b[tid + 2]);
+        if (tid == 0 && k > 0 && k - 1 < m) pair_of<kNarrow>(pkeys, E, k - 1, s_a[0], s_b[0]);
+        if (tid == (int)blockDim.x - 1 && k + 1 < m)
+            pair_of<kNarrow>(pkeys, E, k + 1, s_a[tid + 2], s_b[tid + 2]);
         __syncthreads();
         if (k < m) {
             const bool first = k == 0 || s_a[tid] != a || s_b[tid] != b;
             const bool last = k + 1 == m || s_a[tid + 2] != a || s_b[tid + 2] != b;
-            const uint32_t dir_min = ed.src == a ? 0u : 1u;  // 0: min -> max
-            __stcs(P_t + k, ed.t);
+            const uint32_t dir_min = Codec::dir_from_min(ed, a);  // 0: min -> max
+            __stcs(P_t + k, Codec::time(ed, tmin));
             __stcs(P_ord + k, perm ? perm[p] : p);
             __stcs(P_min + k, a);
             __stcs(P_max + k, b);
@@ -461,11 +490,20 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     {
         uint64_t* nk0 = dalloc<uint64_t>(R + kSortPad, s);
         uint64_t* nk1 = dalloc<uint64_t>(R + kSortPad, s);
-        PackedEdge* E = dalloc<PackedEdge>(m, s);
+        // narrow 8-byte edge records when the time span fits 32 bits
+        const bool narrow = (uint64_t)h_st.tmax - (uint64_t)h_st.tmin < (1ull << 32);
+        const int64_t tmin = h_st.tmin;
+        uint8_t* E = dalloc<uint8_t>(m * (narrow ? sizeof(NarrowEdge) : sizeof(WideEdge)), s);
+        auto EN = reinterpret_cast<NarrowEdge*>(E);
+        auto EW = reinterpret_cast<WideEdge*>(E);
         const uint32_t ntiles = (uint32_t)((R + kSortTile - 1) / kSortTile);
         uint32_t* c0 = dalloc<uint32_t>((uint64_t)256 * ntiles, s);
-        TM_LAUNCH("pack_edges", s, pack_edges_kernel, grid_for(m, kPackEdges), kPackBlock, 0, perm, d_src,
-                  d_dst, d_t, m, E, nk0, c0, ntiles);
+        if (narrow)
+            TM_LAUNCH("pack_edges", s, pack_edges_kernel<true>, grid_for(m, kPackEdges), kPackBlock, 0, perm,
+                      d_src, d_dst, d_t, m, tmin, EN, nk0, c0, ntiles);
+        else
+            TM_LAUNCH("pack_edges", s, pack_edges_kernel<false>, grid_for(m, kPackEdges), kPackBlock, 0, perm,
+                      d_src, d_dst, d_t, m, tmin, EW, nk0, c0, ntiles);
         radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s, c0);
         dfree(c0, s);
         TM_LAUNCH("offsets", s, offsets_from_keys_kernel, grid_for(R), 256, 0, nk0, R, n, g.off);
@@ -474,8 +512,12 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         uint32_t* xmask = dalloc<uint32_t>(nw, s);
         uint32_t* xpref = dalloc<uint32_t>(nw + 1, s);
         TM_CUDA(cudaMemsetAsync(xmask + (nw - 1), 0, sizeof(uint32_t), s));
-        TM_LAUNCH("gather_s", s, gather_s_kernel, grid_for(R), 256, 0, perm, E, nk0, R, g.off, g.S_t,
-                  g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
+        if (narrow)
+            TM_LAUNCH("gather_s", s, gather_s_kernel<true>, grid_for(R), 256, 0, perm, EN, tmin, nk0, R, g.off,
+                      g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
+        else
+            TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, perm, EW, tmin, nk0, R, g.off,
+                      g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
         exclusive_scan<uint32_t>(PopcLoad{g.S_omask}, nw, g.S_opref, s);
 
         // the forward sequences (degree orientation) only need S: build them
@@ -496,8 +538,12 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         dfree(xmask, s);
         dfree(xpref, s);
         radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
-        TM_LAUNCH("gather_p", s, gather_p_kernel, grid_for(m), 256, 0, pk0, m, perm, E, g.P_t, g.P_ord,
-                  g.P_min, g.P_max, g.P_w, n, g.pofs);
+        if (narrow)
+            TM_LAUNCH("gather_p", s, gather_p_kernel<true>, grid_for(m), 256, 0, pk0, m, perm, EN, tmin, g.P_t,
+                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs);
+        else
+            TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, perm, EW, tmin, g.P_t,
+                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs);
         dfree(pk0, s);
         dfree(pk1, s);  // (the node sort's second buffer)
         dfree(E, s);
