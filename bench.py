@@ -34,8 +34,9 @@ METRIC = "temporal edges/sec, exact 36-motif count (1/2/4/8 B200); % of HBM roof
 # Algorithmic bytes per STEP for each kernel family that can dominate a step
 # (DESIGN.md "Roofline"): bytes that must cross HBM at least once.
 #   star_filter   per edge: P t (8 B) + w (4 B), neighbours' t from the same lines
-#   gather_s      per incident record: sorted key 8 B + edge record 16 B + S outputs 20 B
-#   gather_p      per edge: sorted key 8 B + edge record 16 B + P outputs 24 B
+#   gather_s      per incident record: sorted key 8 B + edge record 8 B (16 B when the
+#                 time span needs more than 32 bits) + S outputs 20 B
+#   gather_p      per edge: sorted key 8 B + edge record 8/16 B + P outputs 24 B
 #   tri_filter    per forward record (one per edge): F t (8 B) + node (4 B)
 #   star_work / tri_work run on the filtered worklists only (random access, no streaming model)
 #   radix_downsweep per key per digit pass: key (+ value) read + write
@@ -55,8 +56,9 @@ def algo_bytes(n, m, t):
     sort += m * 8 * 2 * ((nb + 7) // 8)
     if unsorted:
         sort += m * (8 if tb + pbits <= 64 else 12) * 2 * ((tb + 7) // 8)
+    eb = 8 if tb <= 32 else 16  # narrow / wide edge records (tm_graph.cu EdgeCodec)
     return {"star_filter": m * 12, "tri_filter": m * 12, "radix_downsweep": sort,
-            "gather_s": R * 44, "gather_p": m * 48, "scan": 2 * R * 4 + m * 8}
+            "gather_s": R * (8 + eb + 20), "gather_p": m * (8 + eb + 24), "scan": 2 * R * 4 + m * 8}
 
 
 def log(*a):
