@@ -114,6 +114,14 @@ __device__ __forceinline__ uint32_t gallop_locate(const SView& S, uint32_t lo, u
     }
     return a;
 }
+__device__ __forceinline__ uint32_t bsearch_locate(const SView& S, uint32_t lo, uint32_t hi, int64_t t,
+                                                   uint32_t ord) {
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_before(S, mid, t, ord)) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
 __device__ __forceinline__ uint32_t gallop_locate_back(const SView& S, uint32_t lo, uint32_t hi,
                                                        int64_t t, uint32_t ord) {
     uint32_t a = lo, b = hi, span = 1;
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(256) star_work_kernel(SView S, PView P, int64_
         const uint32_t start = S.off[u], end = S.off[u + 1];
         const int64_t tk = P.t[k];
         if (first && tk >= t_end) continue;  // instance's first edge outside the time slice
-        const uint32_t q = gallop_locate(S, start, end, tk, P.ord[k]);
+        const uint32_t q = bsearch_locate(S, start, end, tk, P.ord[k]);
         if (first) {
             first_role(S, P, q, k, side, start, end, delta, acc);
         } else {

@@ -60,9 +60,19 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         }
         if (wk & kPLast) return;
     }
-    // long group: binary search the window [k1, k4) and the type boundaries
-    r = blk_end;  // group end = upper_bound of b in the block
+    // long group: gallop to the group end (first max > b after k), then
+    // binary search the window [k1, k4) and the type boundaries
     l = k;
+    r = blk_end;
+    for (uint32_t span = 16;; span <<= 1) {
+        const uint64_t probe = (uint64_t)l + span;
+        if (probe >= r) break;
+        if (P.max[probe] > b) {
+            r = (uint32_t)probe;
+            break;
+        }
+        l = (uint32_t)probe + 1;
+    }
     while (l < r) {
         const uint32_t mid = (l + r) >> 1;
         if (P.max[mid] <= b) l = mid + 1; else r = mid;
