@@ -27,35 +27,6 @@ struct BuildStats {
     unsigned int pad;
 };
 
-__global__ void validate_kernel(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
-                                const int64_t* __restrict__ t, uint64_t m, uint64_t n,
-                                BuildStats* st) {
-    long long lo = LLONG_MAX, hi = LLONG_MIN;
-    unsigned bad = 0, uns = 0;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = src[k], b = dst[k];
-        const long long tk = t[k];
-        bad |= (a == b) | (a >= n) | (b >= n) | (a > kNodeMask) | (b > kNodeMask);
-        lo = min(lo, tk);
-        hi = max(hi, tk);
-        if (k + 1 < m) uns |= (t[k + 1] < tk);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
-        uns |= __shfl_xor_sync(0xffffffffu, uns, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&st->tmin, lo);
-        atomicMax(&st->tmax, hi);
-        if (bad) atomicOr(&st->bad, 1u);
-        if (uns) atomicOr(&st->unsorted, 1u);
-    }
-}
-
 // packed (t - tmin) << kbits | k  when it fits 64 bits, else key = t - tmin, val = k
 __global__ void time_keys_kernel(const int64_t* __restrict__ t, uint64_t m, int64_t tmin, int kbits,
                                  bool packed, uint64_t* __restrict__ keys,
@@ -120,15 +91,23 @@ struct EdgeCodec<true> {
 // radix_upsweep's, so the node sort skips its first counting pass.
 constexpr int kPackBlock = 256;
 constexpr int kPackEdges = kSortTile / 2;
+// With `st` set (first pass over the caller's arrays, no permutation) the
+// kernel also validates the edges (endpoint range, self loops), reduces the
+// t range, detects time-unordered input, and -- packing narrow records
+// relative to t[0] -- flags spans that do not fit; the host reads `st` once
+// and re-packs in the rare cases (unordered input, wide span).
 template <bool kNarrow>
 __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
     const uint32_t* __restrict__ perm, const uint32_t* __restrict__ src,
-    const uint32_t* __restrict__ dst, const int64_t* __restrict__ t, uint64_t m, int64_t tmin,
-    typename EdgeCodec<kNarrow>::Rec* __restrict__ E, uint64_t* __restrict__ keys,
-    uint32_t* __restrict__ counts, uint32_t ntiles) {
+    const uint32_t* __restrict__ dst, const int64_t* __restrict__ t, uint64_t m, uint64_t n,
+    int64_t tmin, typename EdgeCodec<kNarrow>::Rec* __restrict__ E, uint64_t* __restrict__ keys,
+    uint32_t* __restrict__ counts, uint32_t ntiles, BuildStats* __restrict__ st) {
     constexpr int NW = kPackBlock / 32;
     __shared__ uint32_t hist[NW][256];
     const int w = threadIdx.x >> 5;
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    unsigned bad = 0, uns = 0;
+    if (st) tmin = t[0];
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int i = threadIdx.x; i < NW * 256; i += kPackBlock) (&hist[0][0])[i] = 0;
         __syncthreads();
@@ -138,7 +117,14 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
             if (p < m) {
                 const uint32_t k = perm ? perm[p] : (uint32_t)p;
                 const uint32_t a = src[k], b = dst[k];
-                E[p] = EdgeCodec<kNarrow>::make(t[k], a, b, tmin);
+                const int64_t tk = t[k];
+                if (st) {
+                    bad |= (a == b) | (a >= n) | (b >= n);
+                    lo = min(lo, (long long)tk);
+                    hi = max(hi, (long long)tk);
+                    if (p + 1 < m) uns |= (t[p + 1] < tk);
+                }
+                E[p] = EdgeCodec<kNarrow>::make(tk, a, b, tmin);
                 reinterpret_cast<ulonglong2*>(keys)[p] =
                     make_ulonglong2(((uint64_t)a << 32) | (2 * p), ((uint64_t)b << 32) | (2 * p + 1));
                 atomicAdd(&hist[w][a & 255u], 1u);
@@ -153,6 +139,21 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
             counts[(uint64_t)d * ntiles + tile] = c;
         }
         __syncthreads();
+    }
+    if (st) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+            uns |= __shfl_xor_sync(0xffffffffu, uns, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&st->tmin, lo);
+            atomicMax(&st->tmax, hi);
+            if (bad) atomicOr(&st->bad, 1u);
+            if (uns) atomicOr(&st->unsorted, 1u);
+        }
     }
 }
 
@@ -420,17 +421,32 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     g.R = 2 * m;
     const uint64_t R = g.R;
 
+    // 1. pack + validate in one pass, assuming time-ordered input and a time
+    //    span that fits narrow records; one 4-word read-back decides whether
+    //    to re-pack (time sort first / wide records)
+    const uint32_t ntiles = (uint32_t)((R + kSortTile - 1) / kSortTile);
+    uint64_t* nk0 = dalloc<uint64_t>(R + kSortPad, s);
+    uint64_t* nk1 = dalloc<uint64_t>(R + kSortPad, s);
+    uint32_t* c0 = dalloc<uint32_t>((uint64_t)256 * ntiles, s);
+    uint8_t* E = dalloc<uint8_t>(m * sizeof(NarrowEdge), s);
     BuildStats* d_st = dalloc<BuildStats>(1, s);
     BuildStats h_st{LLONG_MAX, LLONG_MIN, 0, 0, 0, 0};
     TM_CUDA(cudaMemcpyAsync(d_st, &h_st, sizeof(h_st), cudaMemcpyHostToDevice, s));
     if (m) {
-        TM_LAUNCH("validate", s, validate_kernel, grid_for(m), 256, 0, d_src, d_dst, d_t, m, n,
-                  d_st);
+        TM_LAUNCH("pack_edges", s, pack_edges_kernel<true>, grid_for(m, kPackEdges), kPackBlock, 0, nullptr,
+                  d_src, d_dst, d_t, m, n, (int64_t)0, reinterpret_cast<NarrowEdge*>(E), nk0, c0, ntiles, d_st);
     }
     TM_CUDA(cudaMemcpyAsync(&h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, s));
     TM_CUDA(cudaStreamSynchronize(s));
     dfree(d_st, s);
-    if (h_st.bad) throw tm_error(1, "self-loop or out-of-range endpoint in edge list");
+    if (h_st.bad) {
+        dfree(nk0, s); dfree(nk1, s); dfree(c0, s); dfree(E, s);
+        throw tm_error(1, "self-loop or out-of-range endpoint in edge list");
+    }
+    // narrow 8-byte edge records when the time span fits 32 bits
+    const bool narrow = (uint64_t)h_st.tmax - (uint64_t)h_st.tmin < (1ull << 32);
+    const int64_t tmin = h_st.tmin;
+    const bool repack = m && (h_st.unsorted || !narrow);
 
     g.off = dalloc<uint32_t>(n + 1, s);
     g.pofs = dalloc<uint32_t>(n + 1, s);
@@ -449,6 +465,7 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     g.P_min = dalloc<uint32_t>(m, s);
 
     if (m == 0) {
+        dfree(nk0, s); dfree(nk1, s); dfree(c0, s); dfree(E, s);
         TM_CUDA(cudaMemsetAsync(g.off, 0, (n + 1) * sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.pofs, 0, (n + 1) * sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.S_omask, 0, nw * sizeof(uint32_t), s));
@@ -488,22 +505,22 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     // 2. S: stable sort of the incident records by node (key node << 32 | r)
     const int nb = bit_width_u64(n > 1 ? n - 1 : 1);
     {
-        uint64_t* nk0 = dalloc<uint64_t>(R + kSortPad, s);
-        uint64_t* nk1 = dalloc<uint64_t>(R + kSortPad, s);
-        // narrow 8-byte edge records when the time span fits 32 bits
-        const bool narrow = (uint64_t)h_st.tmax - (uint64_t)h_st.tmin < (1ull << 32);
-        const int64_t tmin = h_st.tmin;
-        uint8_t* E = dalloc<uint8_t>(m * (narrow ? sizeof(NarrowEdge) : sizeof(WideEdge)), s);
+        if (repack) {
+            if (!narrow) {
+                dfree(E, s);
+                E = dalloc<uint8_t>(m * sizeof(WideEdge), s);
+            }
+            if (narrow)
+                TM_LAUNCH("pack_edges", s, pack_edges_kernel<true>, grid_for(m, kPackEdges), kPackBlock, 0, perm,
+                          d_src, d_dst, d_t, m, n, tmin, reinterpret_cast<NarrowEdge*>(E), nk0, c0, ntiles,
+                          nullptr);
+            else
+                TM_LAUNCH("pack_edges", s, pack_edges_kernel<false>, grid_for(m, kPackEdges), kPackBlock, 0, perm,
+                          d_src, d_dst, d_t, m, n, tmin, reinterpret_cast<WideEdge*>(E), nk0, c0, ntiles,
+                          nullptr);
+        }
         auto EN = reinterpret_cast<NarrowEdge*>(E);
         auto EW = reinterpret_cast<WideEdge*>(E);
-        const uint32_t ntiles = (uint32_t)((R + kSortTile - 1) / kSortTile);
-        uint32_t* c0 = dalloc<uint32_t>((uint64_t)256 * ntiles, s);
-        if (narrow)
-            TM_LAUNCH("pack_edges", s, pack_edges_kernel<true>, grid_for(m, kPackEdges), kPackBlock, 0, perm,
-                      d_src, d_dst, d_t, m, tmin, EN, nk0, c0, ntiles);
-        else
-            TM_LAUNCH("pack_edges", s, pack_edges_kernel<false>, grid_for(m, kPackEdges), kPackBlock, 0, perm,
-                      d_src, d_dst, d_t, m, tmin, EW, nk0, c0, ntiles);
         radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s, c0);
         dfree(c0, s);
         TM_LAUNCH("offsets", s, offsets_from_keys_kernel, grid_for(R), 256, 0, nk0, R, n, g.off);

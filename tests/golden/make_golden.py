@@ -13,7 +13,10 @@ container, where /root/reference exists).
   hubstress_reference.json reference census for BASELINE config 2 (100k nodes,
                         50M edges, delta 3600; numpy generator; optional, slow)
 
-Usage: python tests/golden/make_golden.py [--powerlaw] [--hubstress] [--only-extra]
+  powerlaw_deltas_reference.json reference census of config 1's input at delta
+                        600 and 86400 (optional, slow)
+
+Usage: python tests/golden/make_golden.py [--powerlaw] [--hubstress] [--powerlaw-deltas] [--only-extra]
 """
 from __future__ import annotations
 
@@ -72,11 +75,28 @@ def hubstress_golden(R):
     json.dump(out, open(os.path.join(HERE, "hubstress_reference.json"), "w"))
 
 
-def main(with_powerlaw: bool, with_hubstress: bool = False, only_extra: bool = False):
+def powerlaw_deltas_golden(R, deltas=(600, 86400)):
+    """config 1's input at further deltas (the BASELINE delta sweep)."""
+    from paper_2204_09236_b200 import synth
+    n, s, d, tt = synth.power_law()
+    g = R.build_graph(n, s, d, tt)
+    out = {"config": "powerlaw_1m_10m", "nodes": n, "edges": int(len(s)), "hash": edge_hash(s, d, tt),
+           "cases": []}
+    for delta in deltas:
+        out["cases"].append({"delta": delta,
+                             "census": [int(x) for x in R.run_parallel(g, delta, os.cpu_count() or 1)]})
+        json.dump(out, open(os.path.join(HERE, "powerlaw_deltas_reference.json"), "w"))
+    R.free(g)
+
+
+def main(with_powerlaw: bool, with_hubstress: bool = False, only_extra: bool = False,
+         with_pl_deltas: bool = False):
     R = Reference()
     if only_extra:
         if with_hubstress:
             hubstress_golden(R)
+        if with_pl_deltas:
+            powerlaw_deltas_golden(R)
         return
     sigs = R.signatures()
 
@@ -151,4 +171,5 @@ def main(with_powerlaw: bool, with_hubstress: bool = False, only_extra: bool = F
 
 
 if __name__ == "__main__":
-    main("--powerlaw" in sys.argv, "--hubstress" in sys.argv, "--only-extra" in sys.argv)
+    main("--powerlaw" in sys.argv, "--hubstress" in sys.argv, "--only-extra" in sys.argv,
+         "--powerlaw-deltas" in sys.argv)
