@@ -251,35 +251,47 @@ __device__ __forceinline__ void third_role(const SView& S, const PView& P, uint3
 // first_role / third_role is zero).  Both endpoints share the group order, so
 // a surviving record yields a candidate at each of its centers inside the
 // center partition [cb, ce); entries are 2k + side.
+constexpr int kFilterItems = 4;  // edges per thread per block iteration (one reservation)
 __global__ void __launch_bounds__(256) star_filter_kernel(PView P, int64_t delta, uint64_t m,
                                                           uint32_t cb, uint32_t ce,
                                                           uint32_t* __restrict__ first_list,
                                                           uint32_t* __restrict__ third_list,
                                                           uint32_t* __restrict__ counters) {
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m;
-         base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = base + threadIdx.x;
-        bool f = false, th = false, ina = false, inb = false;
-        if (k < m) {
-            const uint32_t w = P.w[k];
-            const int64_t t = P.t[k];
-            f = !(w & kPLast) && P.t[k + 1] <= sat_add(t, delta);
-            th = !(w & kPFirst) && P.t[k - 1] >= sat_sub(t, delta);
-            if (f || th) {
-                const uint32_t a = P.min[k], b = P.max[k];
-                ina = a >= cb && a < ce;
-                inb = b >= cb && b < ce;
+    constexpr uint64_t kStep = 256 * kFilterItems;
+    for (uint64_t base = (uint64_t)blockIdx.x * kStep; base < m; base += (uint64_t)gridDim.x * kStep) {
+        // bit 2j + side: edge j's entry for that center is a first / third candidate
+        uint32_t fbits = 0, tbits = 0;
+#pragma unroll
+        for (int j = 0; j < kFilterItems; ++j) {
+            const uint64_t k = base + (uint64_t)j * 256 + threadIdx.x;
+            if (k < m) {
+                const uint32_t w = P.w[k];
+                const int64_t t = P.t[k];
+                const bool f = !(w & kPLast) && P.t[k + 1] <= sat_add(t, delta);
+                const bool th = !(w & kPFirst) && P.t[k - 1] >= sat_sub(t, delta);
+                if (f || th) {
+                    const uint32_t a = P.min[k], b = P.max[k];
+                    const uint32_t in = (a >= cb && a < ce ? 1u : 0u) | (b >= cb && b < ce ? 2u : 0u);
+                    if (f) fbits |= in << (2 * j);
+                    if (th) tbits |= in << (2 * j);
+                }
             }
         }
-        const uint32_t e0 = (uint32_t)(2 * k), e1 = (uint32_t)(2 * k + 1);
-        const bool fa = f && ina, fb = f && inb, ta = th && ina, tb = th && inb;
         uint32_t of, ot;
-        block_reserve2<8, uint32_t>((uint32_t)fa + (uint32_t)fb, (uint32_t)ta + (uint32_t)tb, counters,
-                          counters + 1, of, ot);
-        if (fa) first_list[of++] = e0;
-        if (fb) first_list[of] = e1;
-        if (ta) third_list[ot++] = e0;
-        if (tb) third_list[ot] = e1;
+        block_reserve2<8, uint32_t>((uint32_t)__popc(fbits), (uint32_t)__popc(tbits), counters, counters + 1,
+                                    of, ot);
+        while (fbits) {
+            const int b = __ffs(fbits) - 1;
+            fbits &= fbits - 1;
+            const uint64_t k = base + (uint64_t)(b >> 1) * 256 + threadIdx.x;
+            first_list[of++] = (uint32_t)(2 * k + (b & 1));
+        }
+        while (tbits) {
+            const int b = __ffs(tbits) - 1;
+            tbits &= tbits - 1;
+            const uint64_t k = base + (uint64_t)(b >> 1) * 256 + threadIdx.x;
+            third_list[ot++] = (uint32_t)(2 * k + (b & 1));
+        }
     }
 }
 
@@ -372,7 +384,7 @@ void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c
                uint64_t* d_out, uint64_t* d_stats, cudaStream_t st) {
     if (c_end <= c_begin || g.m == 0) return;
     const uint64_t cap = (uint64_t)sm_count() * 8;
-    uint64_t grid = (g.m + 255) / 256;
+    uint64_t grid = (g.m + 256 * kFilterItems - 1) / (256 * kFilterItems);
     if (grid > cap) grid = cap;
     const uint64_t work = 2 * g.m;
     uint32_t* lists = dalloc<uint32_t>(2 * work + 2, st);

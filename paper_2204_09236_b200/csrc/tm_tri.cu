@@ -159,6 +159,7 @@ __device__ __forceinline__ void wedges_from(const PView& P, const int64_t* __res
 // the long list instead and is enumerated by tri_long_kernel.
 constexpr int kWedgeScan = 8;
 
+constexpr int kFilterItems = 4;  // first edges per thread per block iteration (one reservation)
 __global__ void __launch_bounds__(256) tri_filter_kernel(const int64_t* __restrict__ FT,
                                                          const uint32_t* __restrict__ FN,
                                                          const uint32_t* __restrict__ Fnode,
@@ -168,53 +169,65 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(const int64_t* __restri
                                                          uint32_t* __restrict__ long_list,
                                                          unsigned long long* __restrict__ wcount,
                                                          uint32_t* __restrict__ lcount) {
-    for (uint64_t base = (uint64_t)fb + (uint64_t)blockIdx.x * blockDim.x; base < fe;
-         base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = base + threadIdx.x;
-        uint32_t node = 0, v = 0, nw = 0;
-        int64_t lim = 0;
-        bool alive = false, is_long = false;
-        if (i + 1 < fe) {
-            node = Fnode[i];
-            v = FN[i] & kNodeMask;
-            lim = sat_add(FT[i], delta);
-            alive = true;
-        }
-        uint32_t hits = 0;  // bit s-1: record i+s is a wedge partner
+    constexpr uint64_t kStep = 256 * kFilterItems;
+    for (uint64_t base = (uint64_t)fb + (uint64_t)blockIdx.x * kStep; base < fe;
+         base += (uint64_t)gridDim.x * kStep) {
+        uint32_t hits4 = 0;   // byte j: partners (bit s-1 = record i+s) of first edge j
+        uint32_t longs = 0;   // bit j: first edge j goes to the long list
 #pragma unroll
-        for (int s = 1; s <= kWedgeScan; ++s) {
-            const uint64_t j = i + s;
-            if (alive) {
-                if (j >= fe || Fnode[j] != node || FT[j] > lim) {
-                    alive = false;
-                } else if ((FN[j] & kNodeMask) != v) {
-                    hits |= 1u << (s - 1);
+        for (int jj = 0; jj < kFilterItems; ++jj) {
+            const uint64_t i = base + (uint64_t)jj * 256 + threadIdx.x;
+            if (i + 1 >= fe) continue;
+            const uint32_t node = Fnode[i];
+            const uint32_t v = FN[i] & kNodeMask;
+            const int64_t lim = sat_add(FT[i], delta);
+            bool alive = true;
+            uint32_t hits = 0;
+#pragma unroll
+            for (int s = 1; s <= kWedgeScan; ++s) {
+                const uint64_t j = i + s;
+                if (alive) {
+                    if (j >= fe || Fnode[j] != node || FT[j] > lim) {
+                        alive = false;
+                    } else if ((FN[j] & kNodeMask) != v) {
+                        hits |= 1u << (s - 1);
+                    }
                 }
             }
+            if (alive && i + kWedgeScan + 1 < fe && Fnode[i + kWedgeScan + 1] == node &&
+                FT[i + kWedgeScan + 1] <= lim)
+                longs |= 1u << jj;
+            else
+                hits4 |= hits << (8 * jj);
         }
-        if (alive && i + kWedgeScan + 1 < fe && Fnode[i + kWedgeScan + 1] == node &&
-            FT[i + kWedgeScan + 1] <= lim)
-            is_long = true;
-        nw = is_long ? 0u : (uint32_t)__popc(hits);
+        const uint32_t nw = (uint32_t)__popc(hits4);
         // one block-wide reservation for the wedge slots and the long list
         unsigned long long wo;
         uint32_t lo;
-        block_reserve2<8>(nw, is_long ? 1u : 0u, wcount, lcount, wo, lo);
-        if (is_long) long_list[lo] = (uint32_t)i;
+        block_reserve2<8>(nw, (uint32_t)__popc(longs), wcount, lcount, wo, lo);
+        for (uint32_t lb = longs; lb; lb &= lb - 1)
+            long_list[lo++] = (uint32_t)(base + (uint64_t)(__ffs(lb) - 1) * 256 + threadIdx.x);
         // a reservation past the capacity goes to the long list instead; the
         // lowest such start bounds the valid wedge prefix (every slot below it
         // belongs to a reservation that fit)
         const bool fits = wo + nw <= wedge_cap;
         if (nw && !fits) atomicMin(wcount + 1, wo);
         if (nw && fits) {
-            uint32_t h = hits;
-            while (h) {
-                const int s = __ffs(h);
-                h &= h - 1;
-                wedges[wo++] = ((uint64_t)i << 32) | (uint32_t)(i + s);
+            for (uint32_t h = hits4; h; h &= h - 1) {
+                const int bit = __ffs(h) - 1;
+                const uint64_t i = base + (uint64_t)(bit >> 3) * 256 + threadIdx.x;
+                wedges[wo++] = (i << 32) | (uint32_t)(i + (bit & 7) + 1);
             }
         }
-        warp_append(nw && !fits, (uint32_t)i, long_list, lcount);
+        if (nw && !fits) {
+            uint32_t firsts = 0;  // first edges with wedges, spilled to the long list
+            for (int jj = 0; jj < kFilterItems; ++jj)
+                if ((hits4 >> (8 * jj)) & 0xffu) firsts |= 1u << jj;
+            const uint32_t o = atomicAdd(lcount, (uint32_t)__popc(firsts));
+            uint32_t x = 0;
+            for (uint32_t fbits = firsts; fbits; fbits &= fbits - 1)
+                long_list[o + x++] = (uint32_t)(base + (uint64_t)(__ffs(fbits) - 1) * 256 + threadIdx.x);
+        }
     }
 }
 
@@ -339,7 +352,7 @@ void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_
     cudaStream_t st = g.stream;
     const uint64_t work = f_end - f_begin;
     const uint64_t cap = (uint64_t)sm_count() * 8;
-    uint64_t grid = (work + 255) / 256;
+    uint64_t grid = (work + 256 * kFilterItems - 1) / (256 * kFilterItems);
     if (grid > cap) grid = cap;
     const uint64_t wedge_cap = work + 1024;  // overflow spills to the long list
     uint64_t* wedges = dalloc<uint64_t>(wedge_cap, st);
