@@ -484,6 +484,21 @@ int tm_graph_degrees(const tm_graph* g, uint64_t* out) {
     });
 }
 
+namespace {
+// host copy of timestamps [b, b + cnt) of a TimeBuf as absolute int64
+void copy_times(const TimeBuf& tb, int64_t base, uint64_t b, uint64_t cnt, int64_t* out, cudaStream_t st) {
+    if (!cnt) return;
+    if (tb.n) {
+        std::vector<uint32_t> tmp(cnt);
+        TM_CUDA(cudaMemcpyAsync(tmp.data(), tb.n + b, cnt * 4, cudaMemcpyDeviceToHost, st));
+        TM_CUDA(cudaStreamSynchronize(st));
+        for (uint64_t i = 0; i < cnt; ++i) out[i] = base + (int64_t)tmp[i];
+    } else {
+        TM_CUDA(cudaMemcpyAsync(out, tb.w + b, cnt * 8, cudaMemcpyDeviceToHost, st));
+    }
+}
+}  // namespace
+
 int tm_graph_sequence(const tm_graph* g, uint32_t u, int64_t* t, uint64_t* ordinal, uint32_t* other,
                       uint8_t* dir, uint64_t cap, uint64_t* len) {
     return guarded([&] {
@@ -497,7 +512,7 @@ int tm_graph_sequence(const tm_graph* g, uint32_t u, int64_t* t, uint64_t* ordin
         std::vector<uint32_t> hn(s), ho(s);
         cudaStream_t st = G->g.stream;
         if (s) {
-            TM_CUDA(cudaMemcpyAsync(ht.data(), G->g.S_t + b, s * 8, cudaMemcpyDeviceToHost, st));
+            copy_times(G->g.S_t, G->g.tbase, b, s, ht.data(), st);
             TM_CUDA(cudaMemcpyAsync(hn.data(), G->g.S_nbr + b, s * 4, cudaMemcpyDeviceToHost, st));
             TM_CUDA(cudaMemcpyAsync(ho.data(), G->g.S_ord + b, s * 4, cudaMemcpyDeviceToHost, st));
             TM_CUDA(cudaStreamSynchronize(st));
@@ -533,7 +548,7 @@ int tm_pair_window(const tm_graph* g, uint32_t v, uint32_t w, int64_t lo, int64_
         if (ke == kb) return TM_OK;
         std::vector<int64_t> ht(ke - kb);
         std::vector<uint32_t> ho(ke - kb), hw(ke - kb);
-        TM_CUDA(cudaMemcpyAsync(ht.data(), G->g.P_t + kb, (ke - kb) * 8, cudaMemcpyDeviceToHost, st));
+        copy_times(G->g.P_t, G->g.tbase, kb, ke - kb, ht.data(), st);
         TM_CUDA(cudaMemcpyAsync(ho.data(), G->g.P_ord + kb, (ke - kb) * 4, cudaMemcpyDeviceToHost, st));
         TM_CUDA(cudaMemcpyAsync(hw.data(), G->g.P_w + kb, (ke - kb) * 4, cudaMemcpyDeviceToHost, st));
         TM_CUDA(cudaStreamSynchronize(st));

@@ -71,6 +71,7 @@ struct EdgeCodec<false> {
     using Rec = WideEdge;
     __device__ static Rec make(int64_t t, uint32_t a, uint32_t b, int64_t) { return Rec{t, a, b}; }
     __device__ static int64_t time(const Rec& e, int64_t) { return e.t; }
+    __device__ static uint32_t rel(const Rec&) { return 0u; }
     __device__ static uint32_t other(const Rec& e, uint32_t u) { return e.src ^ e.dst ^ u; }
     __device__ static uint32_t dir_from_min(const Rec& e, uint32_t mn) { return e.src == mn ? 0u : 1u; }
 };
@@ -81,6 +82,7 @@ struct EdgeCodec<true> {
         return Rec{(uint32_t)((uint64_t)t - (uint64_t)tmin), (a ^ b) | (a < b ? 0x80000000u : 0u)};
     }
     __device__ static int64_t time(const Rec& e, int64_t tmin) { return tmin + (int64_t)e.trel; }
+    __device__ static uint32_t rel(const Rec& e) { return e.trel; }
     __device__ static uint32_t other(const Rec& e, uint32_t u) { return (e.x & kNodeMask) ^ u; }
     __device__ static uint32_t dir_from_min(const Rec& e, uint32_t) { return (e.x >> 31) ? 0u : 1u; }
 };
@@ -162,7 +164,8 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm,
                                 const typename EdgeCodec<kNarrow>::Rec* __restrict__ E, int64_t tmin,
                                 const uint64_t* __restrict__ skeys, uint64_t R,
                                 const uint32_t* __restrict__ off,
-                                int64_t* __restrict__ S_t, uint32_t* __restrict__ S_nbr,
+                                int64_t* __restrict__ S_tw, uint32_t* __restrict__ S_tn,
+                                uint32_t* __restrict__ S_nbr,
                                 uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
                                 uint32_t* __restrict__ omask, uint32_t* __restrict__ fmask,
                                 uint32_t* __restrict__ xmask) {
@@ -183,7 +186,8 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm,
             fwd = (dx > du || (dx == du && x > u)) ? 1u : 0u;
             out = side ^ 1u;
             mx = x < u ? 1u : 0u;  // u is the pair's larger endpoint
-            __stcs(S_t + q, Codec::time(e, tmin));
+            if (kNarrow) __stcs(S_tn + q, Codec::rel(e));
+            else __stcs(S_tw + q, Codec::time(e, tmin));
             __stcs(S_ord + q, (perm ? perm[p] : p) | (fwd << 31));
             __stcs(S_node + q, u);
             __stcs(S_nbr + q, x | (side << 31));
@@ -243,7 +247,8 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
                                                        const uint32_t* __restrict__ perm,
                                                        const typename EdgeCodec<kNarrow>::Rec* __restrict__ E,
                                                        int64_t tmin,
-                                                       int64_t* __restrict__ P_t,
+                                                       int64_t* __restrict__ P_tw,
+                                                       uint32_t* __restrict__ P_tn,
                                                        uint32_t* __restrict__ P_ord,
                                                        uint32_t* __restrict__ P_min,
                                                        uint32_t* __restrict__ P_max,
@@ -274,7 +279,8 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
             const bool first = k == 0 || s_a[tid] != a || s_b[tid] != b;
             const bool last = k + 1 == m || s_a[tid + 2] != a || s_b[tid + 2] != b;
             const uint32_t dir_min = Codec::dir_from_min(ed, a);  // 0: min -> max
-            __stcs(P_t + k, Codec::time(ed, tmin));
+            if (kNarrow) __stcs(P_tn + k, Codec::rel(ed));
+            else __stcs(P_tw + k, Codec::time(ed, tmin));
             __stcs(P_ord + k, perm ? perm[p] : p);
             __stcs(P_min + k, a);
             __stcs(P_max + k, b);
@@ -291,7 +297,7 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
 
 // S -> P index for the per-center items API: each P record finds its two S
 // positions by binary search of (t, ordinal) in its endpoints' sequences.
-__device__ __forceinline__ uint32_t s_locate(const int64_t* __restrict__ S_t,
+__device__ __forceinline__ uint32_t s_locate(const TimeArr& S_t,
                                              const uint32_t* __restrict__ S_ord, uint32_t lo,
                                              uint32_t hi, int64_t t, uint32_t ord) {
     while (lo < hi) {
@@ -302,9 +308,9 @@ __device__ __forceinline__ uint32_t s_locate(const int64_t* __restrict__ S_t,
     return lo;
 }
 
-__global__ void s_pidx_kernel(const int64_t* __restrict__ P_t, const uint32_t* __restrict__ P_ord,
+__global__ void s_pidx_kernel(TimeArr P_t, const uint32_t* __restrict__ P_ord,
                               const uint32_t* __restrict__ P_min, const uint32_t* __restrict__ P_max,
-                              const int64_t* __restrict__ S_t, const uint32_t* __restrict__ S_ord,
+                              TimeArr S_t, const uint32_t* __restrict__ S_ord,
                               const uint32_t* __restrict__ off, uint64_t m,
                               uint32_t* __restrict__ S_pidx) {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
@@ -337,10 +343,12 @@ __global__ void index_forward_mask_kernel(const uint32_t* __restrict__ node,
 // F position of forward record q = fpref[q/32] + popc(fmask[q/32] & below)
 __global__ void forward_scatter_kernel(const uint32_t* __restrict__ fmask,
                                        const uint32_t* __restrict__ fpref, uint64_t R,
-                                       const int64_t* __restrict__ S_t,
+                                       const int64_t* __restrict__ S_tw,
+                                       const uint32_t* __restrict__ S_tn,
                                        const uint32_t* __restrict__ S_nbr,
                                        const uint32_t* __restrict__ S_ord,
-                                       const uint32_t* __restrict__ S_node, int64_t* __restrict__ F_t,
+                                       const uint32_t* __restrict__ S_node, int64_t* __restrict__ F_tw,
+                                       uint32_t* __restrict__ F_tn,
                                        uint32_t* __restrict__ F_nbr, uint32_t* __restrict__ F_ord,
                                        uint32_t* __restrict__ F_node) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
@@ -348,7 +356,8 @@ __global__ void forward_scatter_kernel(const uint32_t* __restrict__ fmask,
         const uint32_t word = fmask[q >> 5], bit = 1u << (q & 31);
         if (word & bit) {
             const uint32_t j = fpref[q >> 5] + __popc(word & (bit - 1u));
-            F_t[j] = S_t[q];
+            if (S_tn) F_tn[j] = S_tn[q];
+            else F_tw[j] = S_tw[q];
             F_nbr[j] = S_nbr[q];
             F_ord[j] = S_ord[q] & kNodeMask;
             F_node[j] = S_node[q];
@@ -450,7 +459,9 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
 
     g.off = dalloc<uint32_t>(n + 1, s);
     g.pofs = dalloc<uint32_t>(n + 1, s);
-    g.S_t = dalloc<int64_t>(R, s);
+    g.tbase = narrow ? tmin : 0;
+    if (narrow) g.S_t.n = dalloc<uint32_t>(R, s);
+    else g.S_t.w = dalloc<int64_t>(R, s);
     g.S_nbr = dalloc<uint32_t>(R, s);
     g.S_ord = dalloc<uint32_t>(R, s);
     g.S_node = dalloc<uint32_t>(R, s);
@@ -458,7 +469,8 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     g.S_omask = dalloc<uint32_t>(nw, s);
     g.S_opref = dalloc<uint32_t>(nw + 1, s);
     g.S_fmask = dalloc<uint32_t>(nw, s);
-    g.P_t = dalloc<int64_t>(m, s);
+    if (narrow) g.P_t.n = dalloc<uint32_t>(m, s);
+    else g.P_t.w = dalloc<int64_t>(m, s);
     g.P_ord = dalloc<uint32_t>(m, s);
     g.P_max = dalloc<uint32_t>(m, s);
     g.P_w = dalloc<uint32_t>(m, s);
@@ -531,10 +543,10 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         TM_CUDA(cudaMemsetAsync(xmask + (nw - 1), 0, sizeof(uint32_t), s));
         if (narrow)
             TM_LAUNCH("gather_s", s, gather_s_kernel<true>, grid_for(R), 256, 0, perm, EN, tmin, nk0, R, g.off,
-                      g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
+                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
         else
             TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, perm, EW, tmin, nk0, R, g.off,
-                      g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
+                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
         exclusive_scan<uint32_t>(PopcLoad{g.S_omask}, nw, g.S_opref, s);
 
         // the forward sequences (degree orientation) only need S: build them
@@ -556,10 +568,10 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         dfree(xpref, s);
         radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
         if (narrow)
-            TM_LAUNCH("gather_p", s, gather_p_kernel<true>, grid_for(m), 256, 0, pk0, m, perm, EN, tmin, g.P_t,
+            TM_LAUNCH("gather_p", s, gather_p_kernel<true>, grid_for(m), 256, 0, pk0, m, perm, EN, tmin, g.P_t.w, g.P_t.n,
                       g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs);
         else
-            TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, perm, EW, tmin, g.P_t,
+            TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, perm, EW, tmin, g.P_t.w, g.P_t.n,
                       g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs);
         dfree(pk0, s);
         dfree(pk1, s);  // (the node sort's second buffer)
@@ -584,7 +596,8 @@ void build_forward(DeviceGraph& g, int mode, cudaStream_t s) {
     const uint64_t R = g.R;
     f.mode = mode;
     f.len = g.m;  // every edge is forward from exactly one endpoint
-    f.t = dalloc<int64_t>(g.m, s);
+    if (g.S_t.n) f.t.n = dalloc<uint32_t>(g.m, s);
+    else f.t.w = dalloc<int64_t>(g.m, s);
     f.nbr = dalloc<uint32_t>(g.m, s);
     f.ord = dalloc<uint32_t>(g.m, s);
     f.node = dalloc<uint32_t>(g.m, s);
@@ -604,8 +617,8 @@ void build_forward(DeviceGraph& g, int mode, cudaStream_t s) {
     uint32_t* fpref = dalloc<uint32_t>(nw + 1, s);
     exclusive_scan<uint32_t>(PopcLoad{fmask}, nw, fpref, s);
     if (R) {
-        TM_LAUNCH("forward_scatter", s, forward_scatter_kernel, grid_for(R), 256, 0, fmask, fpref, R, g.S_t,
-                  g.S_nbr, g.S_ord, g.S_node, f.t, f.nbr, f.ord, f.node);
+        TM_LAUNCH("forward_scatter", s, forward_scatter_kernel, grid_for(R), 256, 0, fmask, fpref, R, g.S_t.w,
+                  g.S_t.n, g.S_nbr, g.S_ord, g.S_node, f.t.w, f.t.n, f.nbr, f.ord, f.node);
     }
     TM_LAUNCH("forward_off", s, forward_off_kernel, grid_for(g.n + 1), 256, 0, g.off, fmask, fpref, g.n,
               f.off);
@@ -646,8 +659,8 @@ void build_s_pidx(DeviceGraph& g) {
         return;
     }
     g.S_pidx = dalloc<uint32_t>(g.R, g.stream);
-    TM_LAUNCH("s_pidx", g.stream, s_pidx_kernel, grid_for(g.m), 256, 0, g.P_t, g.P_ord, g.P_min,
-              g.P_max, g.S_t, g.S_ord, g.off, g.m, g.S_pidx);
+    TM_LAUNCH("s_pidx", g.stream, s_pidx_kernel, grid_for(g.m), 256, 0, g.P_t.view(g.tbase), g.P_ord, g.P_min,
+              g.P_max, g.S_t.view(g.tbase), g.S_ord, g.off, g.m, g.S_pidx);
 }
 
 void free_graph(DeviceGraph& g) {
@@ -664,13 +677,13 @@ void free_graph(DeviceGraph& g) {
             *e = nullptr;
         }
     g.fwd_pending = false;
-    dfree(g.S_t, s); dfree(g.S_nbr, s); dfree(g.S_ord, s); dfree(g.S_node, s);
+    dfree(g.S_t.w, s); dfree(g.S_t.n, s); dfree(g.S_nbr, s); dfree(g.S_ord, s); dfree(g.S_node, s);
     dfree(g.S_omask, s); dfree(g.S_opref, s); dfree(g.S_fmask, s); dfree(g.S_pidx, s);
     dfree(g.off, s);
-    dfree(g.P_t, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
+    dfree(g.P_t.w, s); dfree(g.P_t.n, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
     dfree(g.P_min, s); dfree(g.pofs, s);
     for (auto& f : g.fwd) {
-        dfree(f.t, s); dfree(f.nbr, s); dfree(f.ord, s); dfree(f.node, s); dfree(f.off, s);
+        dfree(f.t.w, s); dfree(f.t.n, s); dfree(f.nbr, s); dfree(f.ord, s); dfree(f.node, s); dfree(f.off, s);
         f.valid = false;
     }
     dfree(g.d_acc, s);

@@ -2,7 +2,8 @@
 //
 // HBM layout (all positions are 32-bit; R = 2m incident records):
 //   S (time-ordered per-node sequences, NodeSequenceIndex, indexes.hpp:22-40)
-//     S_t[R]    int64  timestamp
+//     S_t[R]    timestamp: int64, or u32 offset from tbase when the time
+//               span fits 32 bits (TimeArr; same for P_t and F.t)
 //     S_nbr[R]  u32    other endpoint | dir << 31   (dir 0 = outward)
 //     S_ord[R]  u32    ingestion ordinal | forward-in-degree-order << 31
 //     S_node[R] u32    center node
@@ -77,11 +78,28 @@ void dfree(T*& p, cudaStream_t s) {
     p = nullptr;
 }
 
+// A timestamp array of an index (S, P or F): int64, or -- when the graph's
+// time span fits 32 bits -- u32 offsets from `base`: half the bytes in every
+// window search, group walk and gather.  Reads return absolute times.
+struct TimeArr {
+    const int64_t* w;
+    const uint32_t* n;
+    int64_t base;
+    __device__ __forceinline__ int64_t operator[](uint64_t i) const {
+        return n ? base + (int64_t)n[i] : w[i];
+    }
+};
+struct TimeBuf {
+    int64_t* w = nullptr;
+    uint32_t* n = nullptr;
+    TimeArr view(int64_t base) const { return TimeArr{w, n, base}; }
+};
+
 struct Forward {
     bool valid = false;
     int mode = 0;  // 0: degree rank (count_all), 1: node index (removal)
     uint64_t len = 0;
-    int64_t* t = nullptr;
+    TimeBuf t;
     uint32_t* nbr = nullptr;
     uint32_t* ord = nullptr;
     uint32_t* node = nullptr;
@@ -100,7 +118,8 @@ struct DeviceGraph {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, fwd_ready = nullptr;
     bool fwd_pending = false;
 
-    int64_t* S_t = nullptr;
+    int64_t tbase = 0;  // t_min: base of the narrow (u32) timestamp arrays
+    TimeBuf S_t;
     uint32_t* S_nbr = nullptr;
     uint32_t* S_ord = nullptr;
     uint32_t* S_node = nullptr;
@@ -110,7 +129,7 @@ struct DeviceGraph {
     uint32_t* S_pidx = nullptr;
     uint32_t* off = nullptr;
 
-    int64_t* P_t = nullptr;
+    TimeBuf P_t;
     uint32_t* P_ord = nullptr;
     uint32_t* P_max = nullptr;
     uint32_t* P_w = nullptr;
@@ -125,7 +144,7 @@ struct DeviceGraph {
 
 // read-only views passed by value to kernels
 struct SView {
-    const int64_t* t;
+    TimeArr t;
     const uint32_t* nbr;
     const uint32_t* ord;
     const uint32_t* node;
@@ -135,7 +154,7 @@ struct SView {
     const uint32_t* off;
 };
 struct PView {
-    const int64_t* t;
+    TimeArr t;
     const uint32_t* ord;
     const uint32_t* max;
     const uint32_t* w;
@@ -143,7 +162,7 @@ struct PView {
     const uint32_t* pofs;
 };
 inline SView sview(const DeviceGraph& g) {
-    return {g.S_t, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_opref, g.S_pidx, g.off};
+    return {g.S_t.view(g.tbase), g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_opref, g.S_pidx, g.off};
 }
 // global exclusive count of outward records before S position q
 __device__ __forceinline__ uint32_t outward_before(const SView& S, uint32_t q) {
@@ -151,7 +170,7 @@ __device__ __forceinline__ uint32_t outward_before(const SView& S, uint32_t q) {
 }
 
 inline PView pview(const DeviceGraph& g) {
-    return {g.P_t, g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs};
+    return {g.P_t.view(g.tbase), g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs};
 }
 
 // ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------

@@ -32,7 +32,7 @@ namespace tmb {
 namespace {
 
 // first index in [beg, end) with T[idx] > lim (end if none); T ascending
-__device__ __forceinline__ uint32_t gallop_upper(const int64_t* __restrict__ T, uint32_t beg,
+__device__ __forceinline__ uint32_t gallop_upper(const TimeArr& T, uint32_t beg,
                                                  uint32_t end, int64_t lim) {
     uint32_t lo = beg, hi = end;
     uint32_t span = 1;
@@ -54,7 +54,7 @@ __device__ __forceinline__ uint32_t gallop_upper(const int64_t* __restrict__ T, 
 }
 
 // first index in [beg, from] with T[idx] >= lim, given T[from] >= lim
-__device__ __forceinline__ uint32_t gallop_lower_back(const int64_t* __restrict__ T, uint32_t beg,
+__device__ __forceinline__ uint32_t gallop_lower_back(const TimeArr& T, uint32_t beg,
                                                       uint32_t from, int64_t lim) {
     uint32_t hi = from, lo = beg;
     uint32_t span = 1;

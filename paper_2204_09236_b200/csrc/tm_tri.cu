@@ -114,7 +114,7 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
 
 // all wedges with first edge i in sequence arrays (T, NBR, ORD) ending at end
 template <typename Sink>
-__device__ __forceinline__ void wedges_from(const PView& P, const int64_t* __restrict__ T,
+__device__ __forceinline__ void wedges_from(const PView& P, const TimeArr& T,
                                             const uint32_t* __restrict__ NBR,
                                             const uint32_t* __restrict__ ORD, uint32_t i,
                                             uint32_t end, int64_t delta,
@@ -160,7 +160,7 @@ __device__ __forceinline__ void wedges_from(const PView& P, const int64_t* __res
 constexpr int kWedgeScan = 8;
 
 constexpr int kFilterItems = 4;  // first edges per thread per block iteration (one reservation)
-__global__ void __launch_bounds__(256) tri_filter_kernel(const int64_t* __restrict__ FT,
+__global__ void __launch_bounds__(256) tri_filter_kernel(TimeArr FT,
                                                          const uint32_t* __restrict__ FN,
                                                          const uint32_t* __restrict__ Fnode,
                                                          int64_t delta, uint32_t fb, uint32_t fe,
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(const int64_t* __restri
 }
 
 template <typename Sink>
-__device__ __forceinline__ void add_wedge(const PView& P, const int64_t* __restrict__ FT,
+__device__ __forceinline__ void add_wedge(const PView& P, TimeArr FT,
                                           const uint32_t* __restrict__ FN,
                                           const uint32_t* __restrict__ FO, uint32_t i, uint32_t j,
                                           int64_t delta, int64_t t_end, const Sink& acc) {
@@ -249,7 +249,7 @@ __device__ __forceinline__ void add_wedge(const PView& P, const int64_t* __restr
 }
 
 // one wedge per thread
-__global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, const int64_t* __restrict__ FT,
+__global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, TimeArr FT,
                                                         const uint32_t* __restrict__ FN,
                                                         const uint32_t* __restrict__ FO,
                                                         int64_t delta, int64_t t_end,
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, const int64_t* 
 
 // first edges with long windows: one warp per first edge, lanes stride the
 // in-window records (the HARE intra-node split, per first edge)
-__global__ void __launch_bounds__(256) tri_long_kernel(PView P, const int64_t* __restrict__ FT,
+__global__ void __launch_bounds__(256) tri_long_kernel(PView P, TimeArr FT,
                                                        const uint32_t* __restrict__ FN,
                                                        const uint32_t* __restrict__ FO,
                                                        const uint32_t* __restrict__ Fnode,
@@ -365,11 +365,11 @@ void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_
     TM_CUDA(cudaMemsetAsync(wcount, 0, sizeof(uint64_t), st));
     TM_CUDA(cudaMemsetAsync(wcount + 1, 0xFF, sizeof(uint64_t), st));
     TM_CUDA(cudaMemsetAsync(lcount, 0, sizeof(uint32_t), st));
-    TM_LAUNCH("tri_filter", st, tri_filter_kernel, (unsigned)grid, 256, 0, f.t, f.nbr, f.node, delta,
+    TM_LAUNCH("tri_filter", st, tri_filter_kernel, (unsigned)grid, 256, 0, f.t.view(g.tbase), f.nbr, f.node, delta,
               f_begin, f_end, wedges, wedge_cap, long_list, wcount, lcount);
-    TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pview(g), f.t, f.nbr, f.ord,
+    TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pview(g), f.t.view(g.tbase), f.nbr, f.ord,
               delta, t_end, wedges, wedge_cap, wcount, d_out, d_stats);
-    TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pview(g), f.t, f.nbr, f.ord,
+    TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pview(g), f.t.view(g.tbase), f.nbr, f.ord,
               f.node, f.off, delta, t_end, long_list, lcount, d_out, d_stats);
     dfree(wedges, st);
     dfree(long_list, st);
