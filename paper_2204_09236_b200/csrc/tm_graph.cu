@@ -322,6 +322,22 @@ __global__ void s_pidx_kernel(TimeArr P_t, const uint32_t* __restrict__ P_ord,
     }
 }
 
+// two word-popcount prefixes in one scan: low / high 32 bits of a u64
+struct PopcLoad2 {
+    const uint32_t* a;
+    const uint32_t* b;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+        return (uint64_t)__popc(a[i]) | ((uint64_t)__popc(b[i]) << 32);
+    }
+};
+struct SplitStore2 {
+    uint32_t* a;
+    uint32_t* b;
+    __device__ __forceinline__ void operator()(uint64_t i, uint64_t v) const {
+        a[i] = (uint32_t)v;
+        b[i] = (uint32_t)(v >> 32);
+    }
+};
 struct PopcLoad {
     const uint32_t* mask;
     __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return __popc(mask[i]); }
@@ -547,7 +563,8 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         else
             TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, perm, EW, tmin, nk0, R, g.off,
                       g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
-        exclusive_scan<uint32_t>(PopcLoad{g.S_omask}, nw, g.S_opref, s);
+        // outward prefix (stars) and max-side prefix (pair keys) in one scan
+        exclusive_scan_to<uint64_t>(PopcLoad2{g.S_omask, xmask}, nw, SplitStore2{g.S_opref, xpref}, s);
 
         // the forward sequences (degree orientation) only need S: build them
         // on a side stream while the pair index is sorted
@@ -558,7 +575,6 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
 
         // 3. P: the max-side records (one per edge, (max, t, ordinal) order)
         //    stably sorted by the min endpoint
-        exclusive_scan<uint32_t>(PopcLoad{xmask}, nw, xpref, s);
         uint64_t* pk0 = dalloc<uint64_t>(m + kSortPad, s);
         uint64_t* pk1 = nk1;  // R + pad >= m + pad
         nk1 = nullptr;

@@ -204,9 +204,15 @@ __global__ void __launch_bounds__(1024) scan_partials(T* partials, uint32_t g) {
     if (threadIdx.x == 0) partials[g] = total;
 }
 
-template <typename T, typename Load>
+template <typename T>
+struct ArrayStore {
+    T* p;
+    __device__ __forceinline__ void operator()(uint64_t i, T v) const { p[i] = v; }
+};
+
+template <typename T, typename Load, typename Store>
 __global__ void __launch_bounds__(kScanBlock) scan_chunk_down(Load load, uint64_t n, uint64_t chunk,
-                                                              const T* __restrict__ partials, T* out) {
+                                                              const T* __restrict__ partials, Store out) {
     __shared__ T stage[kScanTile + kScanTile / 32];
     __shared__ T s_tot;
     const uint64_t b0 = (uint64_t)blockIdx.x * chunk;
@@ -247,21 +253,17 @@ __global__ void __launch_bounds__(kScanBlock) scan_chunk_down(Load load, uint64_
         for (int k = 0; k < kScanItems; ++k) {
             const uint64_t i = base + (uint64_t)k * kScanBlock + threadIdx.x;
             const uint32_t j = k * kScanBlock + threadIdx.x;
-            if (i < b1) out[i] = stage[j + (j >> 5)];
+            if (i < b1) out(i, stage[j + (j >> 5)]);
         }
         carry += s_tot;
         __syncthreads();
     }
-    if (b1 == n && b0 < b1 && threadIdx.x == 0) out[n] = carry;
+    if (b1 == n && b0 < b1 && threadIdx.x == 0) out(n, carry);
 }
 
-// out[0..n] = exclusive prefix of load(0..n-1); out[n] = total.
-template <typename T, typename Load>
-void exclusive_scan(Load load, uint64_t n, T* out, cudaStream_t s) {
-    if (n == 0) {
-        TM_CUDA(cudaMemsetAsync(out, 0, sizeof(T), s));
-        return;
-    }
+// out(i, exclusive prefix of load(0..i-1)) for i in [0, n]; out(n, .) = total.
+template <typename T, typename Load, typename Store>
+void exclusive_scan_to(Load load, uint64_t n, Store out, cudaStream_t s) {
     uint64_t g = (uint64_t)sm_count() * 4;
     if (g > 1024) g = 1024;
     uint64_t chunk = (n + g - 1) / g;
@@ -271,9 +273,19 @@ void exclusive_scan(Load load, uint64_t n, T* out, cudaStream_t s) {
     TM_LAUNCH("scan", s, (scan_chunk_reduce<T, Load>), (unsigned)g, kScanBlock, 0, load, n, chunk,
               partials);
     TM_LAUNCH("scan", s, scan_partials<T>, 1, 1024, 0, partials, (uint32_t)g);
-    TM_LAUNCH("scan", s, (scan_chunk_down<T, Load>), (unsigned)g, kScanBlock, 0, load, n, chunk,
+    TM_LAUNCH("scan", s, (scan_chunk_down<T, Load, Store>), (unsigned)g, kScanBlock, 0, load, n, chunk,
               partials, out);
     dfree(partials, s);
+}
+
+// out[0..n] = exclusive prefix of load(0..n-1); out[n] = total.
+template <typename T, typename Load>
+void exclusive_scan(Load load, uint64_t n, T* out, cudaStream_t s) {
+    if (n == 0) {
+        TM_CUDA(cudaMemsetAsync(out, 0, sizeof(T), s));
+        return;
+    }
+    exclusive_scan_to<T>(load, n, ArrayStore<T>{out}, s);
 }
 
 // ---------------------------------------------------------------------------
