@@ -326,6 +326,13 @@ def test_config1_powerlaw_full_size_properties(cuda, tm):
     if os.path.exists(path):
         ref = load_golden("powerlaw_reference.json")
         assert census.tolist() == ref["census"]
+    # the BASELINE delta sweep on the same input, vs the reference's census
+    path = os.path.join(os.path.dirname(__file__), "golden", "powerlaw_deltas_reference.json")
+    if os.path.exists(path):
+        ref = load_golden("powerlaw_deltas_reference.json")
+        for case in ref["cases"]:
+            got = tm.run_parallel(ctx, tm.RunConfig(delta=case["delta"]))
+            assert got.counts.tolist() == case["census"], case["delta"]
 
 
 def test_config2_hubstress_full_size_vs_reference(cuda, tm):
