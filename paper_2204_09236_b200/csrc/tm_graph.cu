@@ -12,6 +12,8 @@
 //      already in (max, t, ordinal) order, so a stable sort of them by the min
 //      endpoint alone yields (min, max, t, ordinal) -- nb key bits instead of
 //      2 nb.  Keys carry their payload in the low bits (keys-only sorts).
+#include <vector>
+
 #include "tm_primitives.cuh"
 
 namespace tmb {
@@ -427,19 +429,52 @@ unsigned grid_for(uint64_t work, int block = 256) {
     return (unsigned)(g < cap ? g : cap);
 }
 
+// Side streams and events, recycled per host thread (creating and
+// destroying them per graph costs tens of microseconds of host time).
+struct SideSet {
+    cudaStream_t aux[2];
+    cudaEvent_t ev[3];
+};
+struct SidePool {
+    std::vector<SideSet> free_sets;
+    ~SidePool() {
+        for (auto& x : free_sets) {
+            for (auto a : x.aux) cudaStreamDestroy(a);
+            for (auto e : x.ev) cudaEventDestroy(e);
+        }
+    }
+};
+thread_local SidePool g_side_pool;
+
+void acquire_side(DeviceGraph& g) {
+    SideSet x;
+    if (!g_side_pool.free_sets.empty()) {
+        x = g_side_pool.free_sets.back();
+        g_side_pool.free_sets.pop_back();
+    } else {
+        for (auto& a : x.aux) TM_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+        for (auto& e : x.ev) TM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    g.aux[0] = x.aux[0];
+    g.aux[1] = x.aux[1];
+    g.ev_fork = x.ev[0];
+    g.ev_join = x.ev[1];
+    g.fwd_ready = x.ev[2];
+}
+
+void release_side(DeviceGraph& g) {
+    g_side_pool.free_sets.push_back(SideSet{{g.aux[0], g.aux[1]}, {g.ev_fork, g.ev_join, g.fwd_ready}});
+    g.aux[0] = g.aux[1] = nullptr;
+    g.ev_fork = g.ev_join = g.fwd_ready = nullptr;
+}
+
 }  // namespace
 
 void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
                  uint64_t m, uint64_t n) {
     cudaStream_t s = g.stream;
     if (2 * m > 0xFFFFFFF0ull) throw tm_error(9, "graph too large: 2m must fit 32-bit positions");
-    for (auto& a : g.aux)
-        if (!a) TM_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
-    if (!g.ev_fork) {
-        TM_CUDA(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
-        TM_CUDA(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
-        TM_CUDA(cudaEventCreateWithFlags(&g.fwd_ready, cudaEventDisableTiming));
-    }
+    if (!g.aux[0]) acquire_side(g);
     if (n > kNodeMask) throw tm_error(9, "graph too large: node ids must fit 31 bits");
     g.n = n;
     g.m = m;
@@ -681,17 +716,11 @@ void build_s_pidx(DeviceGraph& g) {
 
 void free_graph(DeviceGraph& g) {
     cudaStream_t s = g.stream;
-    for (auto& a : g.aux)
-        if (a) {
-            cudaStreamSynchronize(a);
-            cudaStreamDestroy(a);
-            a = nullptr;
-        }
-    for (cudaEvent_t* e : {&g.ev_fork, &g.ev_join, &g.fwd_ready})
-        if (*e) {
-            cudaEventDestroy(*e);
-            *e = nullptr;
-        }
+    if (g.aux[0]) {
+        // the frees below are ordered after everything the side streams did
+        for (auto& a : g.aux) stream_after(g, s, a);
+        release_side(g);
+    }
     g.fwd_pending = false;
     dfree(g.S_t.w, s); dfree(g.S_t.n, s); dfree(g.S_nbr, s); dfree(g.S_ord, s); dfree(g.S_node, s);
     dfree(g.S_omask, s); dfree(g.S_opref, s); dfree(g.S_fmask, s); dfree(g.S_pidx, s);

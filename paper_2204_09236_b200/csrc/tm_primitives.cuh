@@ -538,14 +538,17 @@ void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt
                                      (int)(2 * TILE * sizeof(K))));
         attr_set = true;
     }
-    int per_sm = 0;
-    if (with_vals)
-        TM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, radix_downsweep_tma<K, true, BLOCK, ITEMS, MINB>, BLOCK, smem));
-    else
-        TM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, radix_downsweep_tma<K, false, BLOCK, ITEMS, MINB>, BLOCK, smem));
-    if (per_sm < 1) per_sm = 1;
+    static int occ[2] = {0, 0};  // resident downsweep blocks per SM (keys-only, with values)
+    int& per_sm = occ[with_vals ? 1 : 0];
+    if (per_sm == 0) {
+        if (with_vals)
+            TM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, radix_downsweep_tma<K, true, BLOCK, ITEMS, MINB>, BLOCK, smem));
+        else
+            TM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, radix_downsweep_tma<K, false, BLOCK, ITEMS, MINB>, BLOCK, smem));
+        if (per_sm < 1) per_sm = 1;
+    }
     const uint64_t ncount = (uint64_t)kRadix * ntiles;
     uint32_t* counts = dalloc<uint32_t>(2 * ncount + (uint64_t)kRadix * passes, s);
     uint32_t* offs = counts + ncount;
