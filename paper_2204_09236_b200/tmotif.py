@@ -798,8 +798,10 @@ def count_edges(n: int, src, dst, t, config: RunConfig, stream: Optional[int] = 
     raw = _Counters()
     census = np.zeros(36, np.uint64)
     tm = _Timings()
+    # phase timings only when asked for: they add events and a host sync
     rc = L.tm_count_edges(src.ctypes.data, dst.ctypes.data, t.ctypes.data, len(src), n, 0, stream,
-                          C.byref(cfg), C.byref(raw), census.ctypes.data, C.byref(tm))
+                          C.byref(cfg), C.byref(raw), census.ctypes.data,
+                          C.byref(tm) if timings is not None else None)
     _raise(rc, L)
     if raw_out is not None:
         raw_out[:24] = np.frombuffer(raw.star, np.uint64)
@@ -821,7 +823,7 @@ def count_edges_device(n: int, m: int, src_ptr: int, dst_ptr: int, t_ptr: int, c
     census = np.zeros(36, np.uint64)
     tm = _Timings()
     rc = L.tm_count_edges(src_ptr, dst_ptr, t_ptr, m, n, 1, stream, C.byref(cfg), C.byref(raw),
-                          census.ctypes.data, C.byref(tm))
+                          census.ctypes.data, C.byref(tm) if timings is not None else None)
     _raise(rc, L)
     if raw_out is not None:
         raw_out[:24] = np.frombuffer(raw.star, np.uint64)
@@ -851,7 +853,7 @@ def count_edges_time_slice(n: int, src, dst, t, config: RunConfig, t_lo: Optiona
     else:
         args = (src, dst, t, m, n, 1)
     _raise(L.tm_count_edges_time_slice(*args, stream, C.byref(cfg), int(t_lo is not None), int(t_lo or 0),
-                                       int(t_hi is not None), int(t_hi or 0), C.byref(raw), C.byref(tm_)), L)
+                                       int(t_hi is not None), int(t_hi or 0), C.byref(raw), None), L)
     return RawCounters(StarCounter(np.frombuffer(raw.star, np.uint64)),
                        PairCounter(np.frombuffer(raw.pair, np.uint64)),
                        TriCounter(np.frombuffer(raw.tri, np.uint64)))
