@@ -470,8 +470,8 @@ void release_side(DeviceGraph& g) {
 
 }  // namespace
 
-void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
-                 uint64_t m, uint64_t n) {
+BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
+                        uint64_t m, uint64_t n, BuildWorkspace* ws) {
     cudaStream_t s = g.stream;
     if (2 * m > 0xFFFFFFF0ull) throw tm_error(9, "graph too large: 2m must fit 32-bit positions");
     if (!g.aux[0]) acquire_side(g);
@@ -484,29 +484,79 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     // 1. pack + validate in one pass, assuming time-ordered input and a time
     //    span that fits narrow records; one 4-word read-back decides whether
     //    to re-pack (time sort first / wide records)
-    const uint32_t ntiles = (uint32_t)((R + kSortTile - 1) / kSortTile);
-    uint64_t* nk0 = dalloc<uint64_t>(R + kSortPad, s);
-    uint64_t* nk1 = dalloc<uint64_t>(R + kSortPad, s);
-    uint32_t* c0 = dalloc<uint32_t>((uint64_t)256 * ntiles, s);
-    uint8_t* E = dalloc<uint8_t>(m * sizeof(NarrowEdge), s);
-    BuildStats* d_st = dalloc<BuildStats>(1, s);
+    BuildPlan pl;
+    pl.ntiles = (uint32_t)((R + kSortTile - 1) / kSortTile);
+    pl.owned = ws == nullptr;
+    BuildStats* d_st;
+    if (ws) {  // persistent buffers (graph replay): sized for wide records
+        if (!ws->nk0) {
+            ws->nk0 = dalloc<uint64_t>(R + kSortPad, s);
+            ws->nk1 = dalloc<uint64_t>(R + kSortPad, s);
+            ws->c0 = dalloc<uint32_t>((uint64_t)256 * pl.ntiles, s);
+            ws->E = dalloc<uint8_t>(m * sizeof(WideEdge), s);
+            ws->st = dalloc<uint8_t>(sizeof(BuildStats), s);
+        }
+        pl.nk0 = ws->nk0;
+        pl.nk1 = ws->nk1;
+        pl.c0 = ws->c0;
+        pl.E = ws->E;
+        pl.E_bytes = m * sizeof(WideEdge);
+        d_st = reinterpret_cast<BuildStats*>(ws->st);
+    } else {
+        pl.nk0 = dalloc<uint64_t>(R + kSortPad, s);
+        pl.nk1 = dalloc<uint64_t>(R + kSortPad, s);
+        pl.c0 = dalloc<uint32_t>((uint64_t)256 * pl.ntiles, s);
+        pl.E = dalloc<uint8_t>(m * sizeof(NarrowEdge), s);
+        pl.E_bytes = m * sizeof(NarrowEdge);
+        d_st = dalloc<BuildStats>(1, s);
+    }
     BuildStats h_st{LLONG_MAX, LLONG_MIN, 0, 0, 0, 0};
     TM_CUDA(cudaMemcpyAsync(d_st, &h_st, sizeof(h_st), cudaMemcpyHostToDevice, s));
     if (m) {
         TM_LAUNCH("pack_edges", s, pack_edges_kernel<true>, grid_for(m, kPackEdges), kPackBlock, 0, nullptr,
-                  d_src, d_dst, d_t, m, n, (int64_t)0, reinterpret_cast<NarrowEdge*>(E), nk0, c0, ntiles, d_st);
+                  d_src, d_dst, d_t, m, n, (int64_t)0, reinterpret_cast<NarrowEdge*>(pl.E), pl.nk0, pl.c0,
+                  pl.ntiles, d_st);
     }
     TM_CUDA(cudaMemcpyAsync(&h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, s));
     TM_CUDA(cudaStreamSynchronize(s));
-    dfree(d_st, s);
+    if (!ws) dfree(d_st, s);
     if (h_st.bad) {
-        dfree(nk0, s); dfree(nk1, s); dfree(c0, s); dfree(E, s);
+        release_plan(g, pl);
         throw tm_error(1, "self-loop or out-of-range endpoint in edge list");
     }
     // narrow 8-byte edge records when the time span fits 32 bits
-    const bool narrow = (uint64_t)h_st.tmax - (uint64_t)h_st.tmin < (1ull << 32);
-    const int64_t tmin = h_st.tmin;
-    const bool repack = m && (h_st.unsorted || !narrow);
+    pl.narrow = (uint64_t)h_st.tmax - (uint64_t)h_st.tmin < (1ull << 32);
+    pl.unsorted = h_st.unsorted != 0;
+    pl.tmin = h_st.tmin;
+    pl.tmax = h_st.tmax;
+    return pl;
+}
+
+void release_plan(DeviceGraph& g, BuildPlan& pl) {
+    if (!pl.owned) return;
+    cudaStream_t s = g.stream;
+    dfree(pl.nk0, s); dfree(pl.nk1, s); dfree(pl.c0, s); dfree(pl.E, s);
+}
+
+void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
+                 uint64_t m, uint64_t n) {
+    BuildPlan pl = build_prepare(g, d_src, d_dst, d_t, m, n, nullptr);
+    build_finish(g, pl, d_src, d_dst, d_t);
+}
+
+void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const uint32_t* d_dst,
+                  const int64_t* d_t) {
+    cudaStream_t s = g.stream;
+    const uint64_t m = g.m, n = g.n, R = g.R;
+    const bool narrow = pl.narrow;
+    const int64_t tmin = pl.tmin;
+    const bool repack = m && (pl.unsorted || !narrow);
+    BuildStats h_st{pl.tmin, pl.tmax, 0, pl.unsorted ? 1u : 0u, 0, 0};
+    uint64_t* nk0 = pl.nk0;
+    uint64_t* nk1 = pl.nk1;
+    uint32_t* c0 = pl.c0;
+    uint8_t* E = pl.E;
+    const uint32_t ntiles = pl.ntiles;
 
     g.off = dalloc<uint32_t>(n + 1, s);
     g.pofs = dalloc<uint32_t>(n + 1, s);
@@ -528,7 +578,7 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     g.P_min = dalloc<uint32_t>(m, s);
 
     if (m == 0) {
-        dfree(nk0, s); dfree(nk1, s); dfree(c0, s); dfree(E, s);
+        release_plan(g, pl);
         TM_CUDA(cudaMemsetAsync(g.off, 0, (n + 1) * sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.pofs, 0, (n + 1) * sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.S_omask, 0, nw * sizeof(uint32_t), s));
@@ -569,9 +619,11 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
     const int nb = bit_width_u64(n > 1 ? n - 1 : 1);
     {
         if (repack) {
-            if (!narrow) {
+            if (!narrow && pl.E_bytes < m * sizeof(WideEdge)) {
                 dfree(E, s);
                 E = dalloc<uint8_t>(m * sizeof(WideEdge), s);
+                pl.E = E;
+                pl.E_bytes = m * sizeof(WideEdge);
             }
             if (narrow)
                 TM_LAUNCH("pack_edges", s, pack_edges_kernel<true>, grid_for(m, kPackEdges), kPackBlock, 0, perm,
@@ -585,7 +637,7 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         auto EN = reinterpret_cast<NarrowEdge*>(E);
         auto EW = reinterpret_cast<WideEdge*>(E);
         radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s, c0);
-        dfree(c0, s);
+        if (pl.owned) dfree(c0, s);
         TM_LAUNCH("offsets", s, offsets_from_keys_kernel, grid_for(R), 256, 0, nk0, R, n, g.off);
         TM_CUDA(cudaMemsetAsync(g.S_omask + (nw - 1), 0, sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.S_fmask + (nw - 1), 0, sizeof(uint32_t), s));
@@ -611,10 +663,12 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         // 3. P: the max-side records (one per edge, (max, t, ordinal) order)
         //    stably sorted by the min endpoint
         uint64_t* pk0 = dalloc<uint64_t>(m + kSortPad, s);
+        uint64_t* pk0_alloc = pk0;
         uint64_t* pk1 = nk1;  // R + pad >= m + pad
+        uint64_t* spare = nk1;  // the node sort's second buffer (plan-owned)
         nk1 = nullptr;
         TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, xmask, xpref, R, pk0);
-        dfree(nk0, s);
+        if (pl.owned) dfree(nk0, s);
         dfree(xmask, s);
         dfree(xpref, s);
         radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
@@ -624,9 +678,11 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
         else
             TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, perm, EW, tmin, g.P_t.w, g.P_t.n,
                       g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs);
-        dfree(pk0, s);
-        dfree(pk1, s);  // (the node sort's second buffer)
-        dfree(E, s);
+        dfree(pk0_alloc, s);
+        if (pl.owned) {
+            dfree(spare, s);
+            dfree(E, s);
+        }
     }
     if (perm) dfree(perm, s);
     g.max_degree = 0;  // not needed by the layout (positions are global 32-bit)

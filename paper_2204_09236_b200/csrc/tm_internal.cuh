@@ -176,6 +176,32 @@ inline PView pview(const DeviceGraph& g) {
 // ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------
 void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst,
                  const int64_t* d_t, uint64_t m, uint64_t n);
+// build_graph in two halves: build_prepare packs + validates and reads the
+// 4-word verdict back (the only host sync); build_finish issues the rest with
+// no host synchronisation, so it can be captured into a CUDA graph.  With a
+// workspace, the prepare buffers are persistent (replayed graphs reuse them).
+struct BuildWorkspace {
+    uint64_t* nk0 = nullptr;
+    uint64_t* nk1 = nullptr;
+    uint32_t* c0 = nullptr;
+    uint8_t* E = nullptr;
+    uint8_t* st = nullptr;
+};
+struct BuildPlan {
+    uint64_t* nk0 = nullptr;
+    uint64_t* nk1 = nullptr;
+    uint32_t* c0 = nullptr;
+    uint8_t* E = nullptr;
+    uint64_t E_bytes = 0;
+    uint32_t ntiles = 0;
+    bool narrow = true, unsorted = false, owned = true;
+    int64_t tmin = 0, tmax = 0;
+};
+BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
+                        uint64_t m, uint64_t n, BuildWorkspace* ws);
+void build_finish(DeviceGraph& g, BuildPlan& plan, const uint32_t* d_src, const uint32_t* d_dst,
+                  const int64_t* d_t);
+void release_plan(DeviceGraph& g, BuildPlan& plan);
 void free_graph(DeviceGraph& g);
 // builds fwd[mode] on stream st (no-op when built); for fwd[0] started
 // during build_graph, makes st wait for it

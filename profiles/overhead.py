@@ -18,4 +18,10 @@ for m in (1000, 200000, 2000000):
             tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg, stream=st.cuda_stream, timings=tmg)
         torch.cuda.synchronize()
         dtm = (time.perf_counter() - t0) / 10
-    print(m, "wall ms/step", round(dtm * 1e3, 3), "phases", tmg.index_ms if tmg else None, tmg.star_pair_ms if tmg else None, tmg.triangle_ms if tmg else None, tmg.merge_ms if tmg else None, flush=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg, stream=st.cuda_stream)
+    torch.cuda.synchronize()
+    dtn = (time.perf_counter() - t0) / 10
+    print(m, "wall ms/step", round(dtm * 1e3, 3), "no-timings", round(dtn * 1e3, 3), "phases", tmg.index_ms if tmg else None, tmg.star_pair_ms if tmg else None, tmg.triangle_ms if tmg else None, tmg.merge_ms if tmg else None, flush=True)
