@@ -294,7 +294,7 @@ def main():
 
     with ClockSampler(local) as clk:
         ms_step, census, launches = timed(False, args.steps, args.warmup)
-    ms_e2e, census_e2e, _ = timed(True, max(2, args.steps // 2), 1)
+    ms_e2e, census_e2e, _ = timed(True, max(2, args.steps // 2), args.warmup)
     assert (census == census_e2e).all(), "device and host paths disagree"
 
     # per-kernel device time with CUDA events on the launching stream (separate instrumented pass)

@@ -274,8 +274,17 @@ struct PassResult {
     uint64_t tri_once[24];
 };
 
+// host side of a pass: wait for the counter copy and unpack it
+void collect_passes(tm_graph* G, PassResult& r) {
+    TM_CUDA(cudaStreamSynchronize(G->g.stream));
+    const uint64_t* h = pinned_acc();
+    std::memcpy(r.star_raw, h, 32 * sizeof(uint64_t));
+    std::memcpy(r.tri_once, h + 32, 24 * sizeof(uint64_t));
+    std::memcpy(G->g.stats, h + 56, 8 * sizeof(uint64_t));
+}
+
 void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do_tri, int tri_mode,
-                uint32_t cb, uint32_t ce, PassResult& r, tm_phase_timings* tm) {
+                uint32_t cb, uint32_t ce, PassResult& r, tm_phase_timings* tm, bool collect = true) {
     DeviceGraph& g = G->g;
     cudaStream_t s = g.stream;
     if (!g.d_acc) g.d_acc = dalloc<uint64_t>(64, s);
@@ -314,10 +323,8 @@ void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do
     if (tm) TM_CUDA(cudaEventRecord(e2, s));
     uint64_t* h = pinned_acc();
     TM_CUDA(cudaMemcpyAsync(h, g.d_acc, 64 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    TM_CUDA(cudaStreamSynchronize(s));
-    std::memcpy(r.star_raw, h, 32 * sizeof(uint64_t));
-    std::memcpy(r.tri_once, h + 32, 24 * sizeof(uint64_t));
-    std::memcpy(g.stats, h + 56, 8 * sizeof(uint64_t));
+    if (!collect) return;  // (graph capture: the caller launches, synchronises and collects)
+    collect_passes(G, r);
     if (tm) {
         float a = 0, b = 0;
         cudaEventElapsedTime(&a, e0, e1);  // star pass (side stream)
@@ -328,6 +335,41 @@ void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do
         cudaEventDestroy(e1);
         cudaEventDestroy(e2);
     }
+}
+
+void check_config(const tm_run_config* cfg) {
+    if (!cfg) throw tm_error(TM_ERR_INVALID, "null graph or config");
+    if (cfg->workers < 1) throw tm_error(TM_ERR_CONFIG, "workers must be >= 1");
+    if (cfg->delta < 0) throw tm_error(TM_ERR_CONFIG, "delta must be >= 0");
+    if (cfg->triangle_mode == TM_TRI_REMOVAL && cfg->workers > 1)
+        throw tm_error(TM_ERR_CONFIG, "removal triangle mode requires a single worker");
+    if (cfg->triangle_mode != TM_TRI_REMOVAL && cfg->triangle_mode != TM_TRI_COUNT_ALL)
+        throw tm_error(TM_ERR_CONFIG, "triangle mode must be countall or removal");
+}
+
+// raw pass sums -> the reference's counters (+ census for full runs)
+void finish_counts(const PassResult& r, const tm_run_config* cfg, bool full, tm_counters* raw,
+                   uint64_t* census, tm_phase_timings* tm) {
+    const uint32_t motifs = cfg->motifs ? cfg->motifs : 7u;
+    tm_counters out;
+    std::memset(&out, 0, sizeof(out));
+    finish_star(r.star_raw, out.star, out.pair);
+    if (cfg->triangle_mode == TM_TRI_COUNT_ALL) expand_count_all(r.tri_once, out.tri);
+    else std::memcpy(out.tri, r.tri_once, sizeof(out.tri));
+    if (!(motifs & TM_MOTIF_STAR)) std::memset(out.star, 0, sizeof(out.star));
+    if (!(motifs & TM_MOTIF_PAIR)) std::memset(out.pair, 0, sizeof(out.pair));
+    if (!(motifs & TM_MOTIF_TRIANGLE)) std::memset(out.tri, 0, sizeof(out.tri));
+    if (raw) *raw = out;
+    auto t1 = std::chrono::steady_clock::now();
+    if (census) {
+        std::memset(census, 0, 36 * sizeof(uint64_t));
+        if (full) {
+            int rc = merge_census_impl(out.star, out.pair, out.tri, cfg->triangle_mode, census);
+            if (rc) throw tm_error(rc, g_last_error.empty() ? "merge failed" : g_last_error);
+        }
+    }
+    if (tm) tm->merge_ms = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t1).count();
 }
 
 int run_parallel_impl(tm_graph* G, const tm_run_config* cfg, tm_counters* raw, uint64_t* census,
@@ -350,25 +392,7 @@ int run_parallel_impl(tm_graph* G, const tm_run_config* cfg, tm_counters* raw, u
     const int64_t t_end = cfg->has_first_edge_t_end ? cfg->first_edge_t_end : INT64_MAX;
     run_passes(G, cfg->delta, t_end, (motifs & 3u) != 0, (motifs & 4u) != 0, cfg->triangle_mode, cb, ce, r,
                tm);
-    tm_counters out;
-    std::memset(&out, 0, sizeof(out));
-    finish_star(r.star_raw, out.star, out.pair);
-    if (cfg->triangle_mode == TM_TRI_COUNT_ALL) expand_count_all(r.tri_once, out.tri);
-    else std::memcpy(out.tri, r.tri_once, sizeof(out.tri));
-    if (!(motifs & TM_MOTIF_STAR)) std::memset(out.star, 0, sizeof(out.star));
-    if (!(motifs & TM_MOTIF_PAIR)) std::memset(out.pair, 0, sizeof(out.pair));
-    if (!(motifs & TM_MOTIF_TRIANGLE)) std::memset(out.tri, 0, sizeof(out.tri));
-    if (raw) *raw = out;
-    auto t1 = std::chrono::steady_clock::now();
-    if (census) {
-        std::memset(census, 0, 36 * sizeof(uint64_t));
-        if (full) {
-            int rc = merge_census_impl(out.star, out.pair, out.tri, cfg->triangle_mode, census);
-            if (rc) throw tm_error(rc, g_last_error.empty() ? "merge failed" : g_last_error);
-        }
-    }
-    if (tm) tm->merge_ms = std::chrono::duration<double, std::milli>(
-                              std::chrono::steady_clock::now() - t1).count();
+    finish_counts(r, cfg, full, raw, census, tm);
     (void)t0;
     return TM_OK;
 }
@@ -438,6 +462,184 @@ tm_graph* build_impl(const uint32_t* src, const uint32_t* dst, const int64_t* t,
         throw;
     }
     return G;
+}
+
+// ---------------------------------------------------------------------------
+// Graph replay for repeated one-shot counts (tm_count_edges with the same
+// arrays, sizes, stream and config -- a caller streaming batches into fixed
+// buffers, or a benchmark loop).  Everything after the pack/validate read-back
+// is issued without host synchronisation (build_finish, the counting passes,
+// the counter copy and all frees), so it is captured once per (narrow,
+// unsorted) variant into a CUDA graph and replayed with one launch: ~40
+// kernel launches, ~30 stream-ordered allocations and the side-stream
+// fork/joins collapse into cudaGraphLaunch.  The prepare buffers live in a
+// per-entry workspace so the replayed graph sees the same addresses.
+struct ReplayKey {
+    const void* src;
+    const void* dst;
+    const void* t;
+    uint64_t m, n;
+    int device_ptrs;
+    cudaStream_t stream;
+    tm_run_config cfg;
+    bool operator==(const ReplayKey& o) const {
+        return src == o.src && dst == o.dst && t == o.t && m == o.m && n == o.n &&
+               device_ptrs == o.device_ptrs && stream == o.stream &&
+               std::memcmp(&cfg, &o.cfg, sizeof(cfg)) == 0;
+    }
+};
+struct ReplayEntry {
+    ReplayKey key;
+    BuildWorkspace ws;
+    uint32_t* hs = nullptr;  // device staging of host arrays
+    uint32_t* hd = nullptr;
+    int64_t* ht = nullptr;
+    cudaGraphExec_t exec[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint64_t kernels[4] = {0, 0, 0, 0};  // kernel launches captured in each graph
+    int eager_runs[4] = {0, 0, 0, 0};
+    void release() {
+        for (auto& e : exec)
+            if (e) {
+                cudaGraphExecDestroy(e);
+                e = nullptr;
+            }
+        cudaStream_t s = key.stream;
+        cudaStreamSynchronize(s);
+        dfree(ws.nk0, s); dfree(ws.nk1, s); dfree(ws.c0, s); dfree(ws.E, s); dfree(ws.st, s);
+        dfree(hs, s); dfree(hd, s); dfree(ht, s);
+        cudaStreamSynchronize(s);
+    }
+};
+struct ReplayCache {
+    std::vector<ReplayEntry*> entries;  // most recent last
+    cudaStream_t own = nullptr;
+    ~ReplayCache() {
+        for (auto* e : entries) {
+            e->release();
+            delete e;
+        }
+    }
+};
+thread_local ReplayCache g_replay;
+constexpr size_t kReplayEntries = 2;
+
+bool replay_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TM_GRAPHS");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1 && !g_timing.load(std::memory_order_relaxed);
+}
+
+int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m, uint64_t n,
+                       int device_ptrs, void* stream, const tm_run_config* cfg, tm_counters* raw,
+                       uint64_t* census36) {
+    ensure_device();
+    check_config(cfg);
+    if (!src || !dst || !t) throw tm_error(TM_ERR_INVALID, "null edge arrays");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!s) {
+        if (!g_replay.own) TM_CUDA(cudaStreamCreateWithFlags(&g_replay.own, cudaStreamNonBlocking));
+        s = g_replay.own;
+    }
+    ReplayKey key{src, dst, t, m, n, device_ptrs, s, *cfg};
+    ReplayEntry* E = nullptr;
+    for (size_t i = 0; i < g_replay.entries.size(); ++i)
+        if (g_replay.entries[i]->key == key) {
+            E = g_replay.entries[i];
+            g_replay.entries.erase(g_replay.entries.begin() + i);
+            break;
+        }
+    if (!E) {
+        if (g_replay.entries.size() >= kReplayEntries) {
+            g_replay.entries.front()->release();
+            delete g_replay.entries.front();
+            g_replay.entries.erase(g_replay.entries.begin());
+        }
+        E = new ReplayEntry();
+        E->key = key;
+    }
+    g_replay.entries.push_back(E);
+
+    const uint32_t* ds = src;
+    const uint32_t* dd = dst;
+    const int64_t* dt = t;
+    if (!device_ptrs) {
+        if (!E->hs) {
+            E->hs = dalloc<uint32_t>(m, s);
+            E->hd = dalloc<uint32_t>(m, s);
+            E->ht = dalloc<int64_t>(m, s);
+        }
+        TM_CUDA(cudaMemcpyAsync(E->hs, src, m * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaMemcpyAsync(E->hd, dst, m * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaMemcpyAsync(E->ht, t, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        ds = E->hs;
+        dd = E->hd;
+        dt = E->ht;
+    }
+    tm_graph G;
+    G.g.stream = s;
+    BuildPlan plan;
+    try {
+        plan = build_prepare(G.g, ds, dd, dt, m, n, &E->ws);
+    } catch (...) {
+        free_graph(G.g);
+        throw;
+    }
+    const int variant = (plan.narrow ? 2 : 0) | (plan.unsorted ? 1 : 0);
+    const uint32_t motifs = cfg->motifs ? cfg->motifs : 7u;
+    const int64_t t_end = cfg->has_first_edge_t_end ? cfg->first_edge_t_end : INT64_MAX;
+    const bool full = !cfg->has_first_edge_t_end;
+    PassResult r;
+    auto issue = [&](bool collect) {
+        build_finish(G.g, plan, ds, dd, dt);
+        run_passes(&G, cfg->delta, t_end, (motifs & 3u) != 0, (motifs & 4u) != 0, cfg->triangle_mode, 0,
+                   (uint32_t)n, r, nullptr, collect);
+    };
+    if (!E->exec[variant] && E->eager_runs[variant] == 0) {
+        // first run of this shape: eager (also initialises every lazy static)
+        ++E->eager_runs[variant];
+        try {
+            issue(true);
+        } catch (...) {
+            free_graph(G.g);
+            throw;
+        }
+        free_graph(G.g);
+        TM_CUDA(cudaStreamSynchronize(s));
+        finish_counts(r, cfg, full, raw, census36, nullptr);
+        return TM_OK;
+    }
+    if (!E->exec[variant]) {
+        cudaGraph_t graph = nullptr;
+        const uint64_t l0 = g_launches.load();
+        TM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            issue(false);
+            free_graph(G.g);
+        } catch (...) {
+            cudaStreamEndCapture(s, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            free_graph(G.g);
+            throw;
+        }
+        TM_CUDA(cudaStreamEndCapture(s, &graph));
+        E->kernels[variant] = g_launches.load() - l0;
+        g_launches.fetch_sub(E->kernels[variant]);  // counted when launched, below
+        cudaGraphExec_t ex = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&ex, graph, 0);
+        cudaGraphDestroy(graph);
+        TM_CUDA(ie);
+        E->exec[variant] = ex;
+    } else {
+        free_graph(G.g);  // (only returns the side streams: nothing was allocated)
+    }
+    TM_CUDA(cudaGraphLaunch(E->exec[variant], s));
+    g_launches.fetch_add(E->kernels[variant]);  // the graph's kernels, launched from the device queue
+    collect_passes(&G, r);
+    finish_counts(r, cfg, full, raw, census36, nullptr);
+    return TM_OK;
 }
 
 void free_impl(tm_graph* G) {
@@ -696,6 +898,9 @@ int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, u
                    uint64_t n, int device_ptrs, void* stream, const tm_run_config* cfg,
                    tm_counters* raw, uint64_t* census36, tm_phase_timings* timings) {
     return guarded([&] {
+        if (!timings && m && cfg && cfg->center_begin == 0 && (cfg->center_end == 0 || cfg->center_end == n) &&
+            replay_enabled())
+            return count_edges_replay(src, dst, t, m, n, device_ptrs, stream, cfg, raw, census36);
         double index_ms = 0;
         tm_graph* G = build_impl(src, dst, t, m, n, device_ptrs, stream, timings ? &index_ms : nullptr);
         int rc;

@@ -416,3 +416,40 @@ def test_time_slices_partition_the_census(cuda, tm, oracle):
                     assert (acc_pre == full.as_array()).all(), (delta, mode, world)
                 merged = tm.merge_census(full.star, full.pair, full.tri, mode)
                 assert (merged.counts == census).all()
+
+
+def test_repeated_one_shot_counts_graph_replay(cuda, tm, oracle):
+    """tm_count_edges called repeatedly with the same buffers runs eagerly once,
+    then captures the sync-free half of the step into a CUDA graph and replays
+    it.  Every call must equal the oracle, in place data changes must be seen
+    by the replay, and both input modes (device pointers, host arrays) and the
+    unsorted-input variant must replay correctly."""
+    import torch
+    n, m, delta = 70, 5000, 200
+    s, d, t = oracle.generate_random_graph(n, m, 30000, 99)
+    og = oracle.build_graph(n, s, d, t)
+    want = oracle.census(og, delta).tolist()
+    cfg = tm.RunConfig(delta=delta)
+    ds = torch.from_numpy(s.view(np.int32)).cuda()
+    dd = torch.from_numpy(d.view(np.int32)).cuda()
+    dt = torch.from_numpy(t).cuda()
+    st = torch.cuda.Stream()
+    for _ in range(4):  # eager, capture + launch, replay, replay
+        got = tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg, stream=st.cuda_stream)
+        assert got.tolist() == want
+    # same buffers, new contents (reversed time order -> the unsorted variant)
+    rev = np.ascontiguousarray(t[::-1])
+    dt.copy_(torch.from_numpy(rev))
+    og2 = oracle.build_graph(n, s, d, rev)
+    want2 = oracle.census(og2, delta).tolist()
+    for _ in range(3):
+        got = tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg, stream=st.cuda_stream)
+        assert got.tolist() == want2
+    # host arrays (the e2e path)
+    hs = torch.from_numpy(s.view(np.int32)).pin_memory()
+    hd = torch.from_numpy(d.view(np.int32)).pin_memory()
+    ht = torch.from_numpy(t).pin_memory()
+    for _ in range(3):
+        got = tm.count_edges(n, hs.numpy().view(np.uint32), hd.numpy().view(np.uint32), ht.numpy(), cfg,
+                             stream=st.cuda_stream)
+        assert got.tolist() == want
