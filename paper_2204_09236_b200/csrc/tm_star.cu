@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(256) star_filter_kernel(PView P, int64_t delta
 // Work: the full first_role / third_role sums for the surviving records.
 // The record's own S position is found by binary search of (t, ordinal) in
 // its center's time-ordered sequence.
-__global__ void __launch_bounds__(256) star_work_kernel(SView S, PView P, int64_t delta, int64_t t_end,
+__global__ void __launch_bounds__(256, 5) star_work_kernel(SView S, PView P, int64_t delta, int64_t t_end,
                                                         const uint32_t* __restrict__ first_list,
                                                         const uint32_t* __restrict__ third_list,
                                                         const uint32_t* __restrict__ counters,

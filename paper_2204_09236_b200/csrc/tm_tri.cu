@@ -249,7 +249,7 @@ __device__ __forceinline__ void add_wedge(const PView& P, TimeArr FT,
 }
 
 // one wedge per thread
-__global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, TimeArr FT,
+__global__ void __launch_bounds__(256, 6) tri_wedge_kernel(PView P, TimeArr FT,
                                                         const uint32_t* __restrict__ FN,
                                                         const uint32_t* __restrict__ FO,
                                                         int64_t delta, int64_t t_end,
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(256) tri_wedge_kernel(PView P, TimeArr FT,
 
 // first edges with long windows: one warp per first edge, lanes stride the
 // in-window records (the HARE intra-node split, per first edge)
-__global__ void __launch_bounds__(256) tri_long_kernel(PView P, TimeArr FT,
+__global__ void __launch_bounds__(256, 6) tri_long_kernel(PView P, TimeArr FT,
                                                        const uint32_t* __restrict__ FN,
                                                        const uint32_t* __restrict__ FO,
                                                        const uint32_t* __restrict__ Fnode,
