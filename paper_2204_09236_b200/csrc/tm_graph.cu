@@ -164,56 +164,41 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
 template <bool kNarrow>
 __global__ void gather_s_kernel(const uint32_t* __restrict__ perm,
                                 const typename EdgeCodec<kNarrow>::Rec* __restrict__ E, int64_t tmin,
-                                const uint64_t* __restrict__ skeys, uint64_t R,
-                                const uint32_t* __restrict__ off,
+                                const uint64_t* __restrict__ skeys, uint64_t R, uint64_t n,
+                                uint32_t* __restrict__ off,
                                 int64_t* __restrict__ S_tw, uint32_t* __restrict__ S_tn,
                                 uint32_t* __restrict__ S_nbr,
                                 uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
-                                uint32_t* __restrict__ omask, uint32_t* __restrict__ fmask,
-                                uint32_t* __restrict__ xmask) {
+                                uint32_t* __restrict__ omask, uint32_t* __restrict__ xmask) {
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t q = base + threadIdx.x;
-        uint32_t out = 0, fwd = 0, mx = 0;
+        uint32_t out = 0, mx = 0;
         if (q < R) {
-            const uint64_t key = __ldcs(skeys + q);
+            const uint64_t key = skeys[q];
             const uint32_t r = (uint32_t)key;
             const uint32_t p = r >> 1, side = r & 1u;
             using Codec = EdgeCodec<kNarrow>;
             const typename Codec::Rec e = E[p];
             const uint32_t u = (uint32_t)(key >> 32), x = Codec::other(e, u);
-            // degree-rank orientation of the triangle pass: forward iff (deg, id) of the
-            // neighbour exceeds the center's; kept in the spare top bit of S_ord
-            const uint32_t du = off[u + 1] - off[u], dx = off[x + 1] - off[x];
-            fwd = (dx > du || (dx == du && x > u)) ? 1u : 0u;
+            // CSR offsets from the node boundaries of the sorted keys
+            const int64_t prev = q ? (int64_t)(skeys[q - 1] >> 32) : -1;
+            for (int64_t y = prev + 1; y <= (int64_t)u; ++y) off[y] = (uint32_t)q;
+            if (q == R - 1)
+                for (int64_t y = (int64_t)u + 1; y <= (int64_t)n; ++y) off[y] = (uint32_t)R;
             out = side ^ 1u;
             mx = x < u ? 1u : 0u;  // u is the pair's larger endpoint
             if (kNarrow) __stcs(S_tn + q, Codec::rel(e));
             else __stcs(S_tw + q, Codec::time(e, tmin));
-            __stcs(S_ord + q, (perm ? perm[p] : p) | (fwd << 31));
+            __stcs(S_ord + q, perm ? perm[p] : p);
             __stcs(S_node + q, u);
             __stcs(S_nbr + q, x | (side << 31));
         }
-        const unsigned ob = __ballot_sync(0xffffffffu, out), fb = __ballot_sync(0xffffffffu, fwd);
-        const unsigned xb = __ballot_sync(0xffffffffu, mx);
+        const unsigned ob = __ballot_sync(0xffffffffu, out), xb = __ballot_sync(0xffffffffu, mx);
         if ((threadIdx.x & 31) == 0 && q < R) {
             omask[q >> 5] = ob;
-            fmask[q >> 5] = fb;
             xmask[q >> 5] = xb;
         }
-    }
-}
-
-// off[x] from the sorted node keys (node << 32 | record): boundary fill
-__global__ void offsets_from_keys_kernel(const uint64_t* __restrict__ keys, uint64_t R, uint64_t n,
-                                         uint32_t* __restrict__ off) {
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
-         q += (uint64_t)gridDim.x * blockDim.x) {
-        const int64_t cur = (int64_t)(keys[q] >> 32);
-        const int64_t prev = q ? (int64_t)(keys[q - 1] >> 32) : -1;
-        for (int64_t x = prev + 1; x <= cur; ++x) off[x] = (uint32_t)q;
-        if (q == R - 1)
-            for (int64_t x = cur + 1; x <= (int64_t)n; ++x) off[x] = (uint32_t)R;
     }
 }
 
@@ -221,14 +206,27 @@ __global__ void offsets_from_keys_kernel(const uint64_t* __restrict__ keys, uint
 // min << 32 | p, compacted by the xmask prefix
 __global__ void pair_keys_kernel(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ S_nbr,
                                  const uint32_t* __restrict__ xmask, const uint32_t* __restrict__ xpref,
-                                 uint64_t R, uint64_t* __restrict__ pkeys) {
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R;
-         q += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t word = xmask[q >> 5], bit = 1u << (q & 31);
-        if (word & bit) {
-            const uint32_t j = xpref[q >> 5] + __popc(word & (bit - 1u));
-            pkeys[j] = ((uint64_t)(__ldcs(S_nbr + q) & kNodeMask) << 32) | ((uint32_t)__ldcs(skeys + q) >> 1);
+                                 const uint32_t* __restrict__ off, uint64_t R, uint64_t* __restrict__ pkeys,
+                                 uint32_t* __restrict__ fmask) {
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = base + threadIdx.x;
+        uint32_t fwd = 0;
+        if (q < R) {
+            const uint64_t key = __ldcs(skeys + q);
+            const uint32_t u = (uint32_t)(key >> 32), x = __ldcs(S_nbr + q) & kNodeMask;
+            // degree-rank orientation of the triangle pass: forward iff (deg, id) of
+            // the neighbour exceeds the center's
+            const uint32_t du = off[u + 1] - off[u], dx = off[x + 1] - off[x];
+            fwd = (dx > du || (dx == du && x > u)) ? 1u : 0u;
+            const uint32_t word = xmask[q >> 5], bit = 1u << (q & 31);
+            if (word & bit) {
+                const uint32_t j = xpref[q >> 5] + __popc(word & (bit - 1u));
+                pkeys[j] = ((uint64_t)x << 32) | ((uint32_t)key >> 1);
+            }
         }
+        const unsigned fb = __ballot_sync(0xffffffffu, fwd);
+        if ((threadIdx.x & 31) == 0 && q < R) fmask[q >> 5] = fb;
     }
 }
 
@@ -638,27 +636,19 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         auto EW = reinterpret_cast<WideEdge*>(E);
         radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s, c0);
         if (pl.owned) dfree(c0, s);
-        TM_LAUNCH("offsets", s, offsets_from_keys_kernel, grid_for(R), 256, 0, nk0, R, n, g.off);
         TM_CUDA(cudaMemsetAsync(g.S_omask + (nw - 1), 0, sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.S_fmask + (nw - 1), 0, sizeof(uint32_t), s));
         uint32_t* xmask = dalloc<uint32_t>(nw, s);
         uint32_t* xpref = dalloc<uint32_t>(nw + 1, s);
         TM_CUDA(cudaMemsetAsync(xmask + (nw - 1), 0, sizeof(uint32_t), s));
         if (narrow)
-            TM_LAUNCH("gather_s", s, gather_s_kernel<true>, grid_for(R), 256, 0, perm, EN, tmin, nk0, R, g.off,
-                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
+            TM_LAUNCH("gather_s", s, gather_s_kernel<true>, grid_for(R), 256, 0, perm, EN, tmin, nk0, R, n, g.off,
+                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask);
         else
-            TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, perm, EW, tmin, nk0, R, g.off,
-                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_fmask, xmask);
+            TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, perm, EW, tmin, nk0, R, n, g.off,
+                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask);
         // outward prefix (stars) and max-side prefix (pair keys) in one scan
         exclusive_scan_to<uint64_t>(PopcLoad2{g.S_omask, xmask}, nw, SplitStore2{g.S_opref, xpref}, s);
-
-        // the forward sequences (degree orientation) only need S: build them
-        // on a side stream while the pair index is sorted
-        stream_after(g, g.aux[0], s);
-        build_forward(g, 0, g.aux[0]);
-        TM_CUDA(cudaEventRecord(g.fwd_ready, g.aux[0]));
-        g.fwd_pending = true;
 
         // 3. P: the max-side records (one per edge, (max, t, ordinal) order)
         //    stably sorted by the min endpoint
@@ -667,7 +657,15 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         uint64_t* pk1 = nk1;  // R + pad >= m + pad
         uint64_t* spare = nk1;  // the node sort's second buffer (plan-owned)
         nk1 = nullptr;
-        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, xmask, xpref, R, pk0);
+        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, xmask, xpref, g.off, R,
+                  pk0, g.S_fmask);
+
+        // the forward sequences (degree orientation) only need S and the
+        // forward mask: build them on a side stream while the pair index sorts
+        stream_after(g, g.aux[0], s);
+        build_forward(g, 0, g.aux[0]);
+        TM_CUDA(cudaEventRecord(g.fwd_ready, g.aux[0]));
+        g.fwd_pending = true;
         if (pl.owned) dfree(nk0, s);
         dfree(xmask, s);
         dfree(xpref, s);

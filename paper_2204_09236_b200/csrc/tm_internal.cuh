@@ -5,7 +5,7 @@
 //     S_t[R]    timestamp: int64, or u32 offset from tbase when the time
 //               span fits 32 bits (TimeArr; same for P_t and F.t)
 //     S_nbr[R]  u32    other endpoint | dir << 31   (dir 0 = outward)
-//     S_ord[R]  u32    ingestion ordinal | forward-in-degree-order << 31
+//     S_ord[R]  u32    ingestion ordinal
 //     S_node[R] u32    center node
 //     S_omask[R/32+1], S_opref[R/32+2]  u32  outward-record bitmask (one bit per
 //               record, written by warp ballots) + exclusive prefix of its
