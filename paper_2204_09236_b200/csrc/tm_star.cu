@@ -85,8 +85,7 @@ __device__ __forceinline__ void add_d1(const Sink& sink, int base, uint32_t d1, 
 // id (P_min / dir_rel_min describe it), 1 when u is the larger one.
 __device__ __forceinline__ uint32_t side_of(uint32_t u, uint32_t other) { return u > other ? 1u : 0u; }
 
-// (t, ordinal) strict order between S record p and (t, ord); S_ord carries
-// the orientation bit on top, masked here.
+// (t, ordinal) strict order between S record p and (t, ord)
 __device__ __forceinline__ bool s_before(const SView& S, uint32_t p, int64_t t, uint32_t ord) {
     const int64_t tp = S.t[p];
     return tp < t || (tp == t && (S.ord[p] & kNodeMask) < ord);

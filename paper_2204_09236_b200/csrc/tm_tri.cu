@@ -123,7 +123,7 @@ __device__ __forceinline__ void wedges_from(const PView& P, const TimeArr& T,
     const uint32_t v = ni & kNodeMask, di = ni >> 31;
     if (live && !live[v]) return;
     const int64_t ti = T[i];
-    const uint32_t oi = ORD[i] & kNodeMask;  // S_ord carries the orientation bit on top
+    const uint32_t oi = ORD[i] & kNodeMask;
     const int64_t lim = sat_add(ti, delta);
     uint64_t a0[6] = {0, 0, 0, 0, 0, 0}, a1[6] = {0, 0, 0, 0, 0, 0};
     for (uint32_t j = i + 1; j < end; ++j) {
