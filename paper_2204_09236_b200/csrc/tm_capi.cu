@@ -314,7 +314,11 @@ void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do
             fb = read_u32(f.off, cb, s);
             fe = read_u32(f.off, ce, s);
         }
-        tri_oriented(g, f, delta, fb, fe, t_end, g.d_acc + 32, g.d_acc + 56);
+        if (fm == 0 && full && g.pre_tri.valid && g.pre_tri.delta == delta && g.pre_tri.f_begin == fb &&
+            g.pre_tri.f_end == fe)
+            tri_work_stage(g, f, g.pre_tri, t_end, g.d_acc + 32, g.d_acc + 56);  // filter ran during the build
+        else
+            tri_oriented(g, f, delta, fb, fe, t_end, g.d_acc + 32, g.d_acc + 56);
     }
     if (ss != s) {
         TM_CUDA(cudaEventRecord(g.ev_join, ss));
@@ -398,7 +402,8 @@ int run_parallel_impl(tm_graph* G, const tm_run_config* cfg, tm_counters* raw, u
 }
 
 tm_graph* build_impl(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
-                     uint64_t n, int device_ptrs, void* stream, double* index_ms) {
+                     uint64_t n, int device_ptrs, void* stream, double* index_ms,
+                     const RunHint* hint = nullptr) {
     ensure_device();
     if (m && (!src || !dst || !t)) throw tm_error(TM_ERR_INVALID, "null edge arrays");
     auto* G = new tm_graph();
@@ -442,7 +447,7 @@ tm_graph* build_impl(const uint32_t* src, const uint32_t* dst, const int64_t* t,
             dd = hd;
             dt = ht;
         }
-        build_graph(G->g, ds, dd, dt, m, n);
+        build_graph(G->g, ds, dd, dt, m, n, hint);
         dfree(hs, s);
         dfree(hd, s);
         dfree(ht, s);
@@ -523,6 +528,16 @@ struct ReplayCache {
 thread_local ReplayCache g_replay;
 constexpr size_t kReplayEntries = 2;
 
+// the triangle filter of a one-shot count can run while the index builds
+RunHint hint_for(const tm_run_config* cfg, uint64_t n) {
+    RunHint h;
+    const uint32_t motifs = cfg->motifs ? cfg->motifs : 7u;
+    h.early_tri = (motifs & TM_MOTIF_TRIANGLE) && cfg->triangle_mode == TM_TRI_COUNT_ALL &&
+                  cfg->center_begin == 0 && (cfg->center_end == 0 || cfg->center_end == n) && cfg->delta >= 0;
+    h.delta = cfg->delta;
+    return h;
+}
+
 bool replay_enabled() {
     static int v = -1;
     if (v < 0) {
@@ -592,8 +607,9 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
     const int64_t t_end = cfg->has_first_edge_t_end ? cfg->first_edge_t_end : INT64_MAX;
     const bool full = !cfg->has_first_edge_t_end;
     PassResult r;
+    const RunHint hint = hint_for(cfg, n);
     auto issue = [&](bool collect) {
-        build_finish(G.g, plan, ds, dd, dt);
+        build_finish(G.g, plan, ds, dd, dt, &hint);
         run_passes(&G, cfg->delta, t_end, (motifs & 3u) != 0, (motifs & 4u) != 0, cfg->triangle_mode, 0,
                    (uint32_t)n, r, nullptr, collect);
     };
@@ -902,7 +918,10 @@ int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, u
             replay_enabled())
             return count_edges_replay(src, dst, t, m, n, device_ptrs, stream, cfg, raw, census36);
         double index_ms = 0;
-        tm_graph* G = build_impl(src, dst, t, m, n, device_ptrs, stream, timings ? &index_ms : nullptr);
+        RunHint hint;
+        if (cfg) hint = hint_for(cfg, n);
+        tm_graph* G = build_impl(src, dst, t, m, n, device_ptrs, stream, timings ? &index_ms : nullptr,
+                                 cfg ? &hint : nullptr);
         int rc;
         try {
             rc = run_parallel_impl(G, cfg, raw, census36, timings);

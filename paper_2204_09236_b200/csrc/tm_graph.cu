@@ -537,13 +537,13 @@ void release_plan(DeviceGraph& g, BuildPlan& pl) {
 }
 
 void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
-                 uint64_t m, uint64_t n) {
+                 uint64_t m, uint64_t n, const RunHint* hint) {
     BuildPlan pl = build_prepare(g, d_src, d_dst, d_t, m, n, nullptr);
-    build_finish(g, pl, d_src, d_dst, d_t);
+    build_finish(g, pl, d_src, d_dst, d_t, hint);
 }
 
 void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const uint32_t* d_dst,
-                  const int64_t* d_t) {
+                  const int64_t* d_t, const RunHint* hint) {
     cudaStream_t s = g.stream;
     const uint64_t m = g.m, n = g.n, R = g.R;
     const bool narrow = pl.narrow;
@@ -664,6 +664,8 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         // forward mask: build them on a side stream while the pair index sorts
         stream_after(g, g.aux[0], s);
         build_forward(g, 0, g.aux[0]);
+        if (hint && hint->early_tri)  // the one-shot count's triangle filter needs F only
+            tri_filter_stage(g, g.fwd[0], hint->delta, 0, (uint32_t)g.fwd[0].len, g.aux[0], g.pre_tri);
         TM_CUDA(cudaEventRecord(g.fwd_ready, g.aux[0]));
         g.fwd_pending = true;
         if (pl.owned) dfree(nk0, s);
@@ -781,6 +783,8 @@ void free_graph(DeviceGraph& g) {
     dfree(g.off, s);
     dfree(g.P_t.w, s); dfree(g.P_t.n, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
     dfree(g.P_min, s); dfree(g.pofs, s);
+    dfree(g.pre_tri.wedges, s); dfree(g.pre_tri.long_list, s); dfree(g.pre_tri.wbuf, s);
+    g.pre_tri.valid = false;
     for (auto& f : g.fwd) {
         dfree(f.t.w, s); dfree(f.t.n, s); dfree(f.nbr, s); dfree(f.ord, s); dfree(f.node, s); dfree(f.off, s);
         f.valid = false;

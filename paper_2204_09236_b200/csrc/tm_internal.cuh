@@ -106,6 +106,25 @@ struct Forward {
     uint32_t* off = nullptr;  // n+1
 };
 
+// triangle pass split in two: the filter over F (wedge list + long list)
+// and the closing-edge work over P.  A one-shot count (build + run in one
+// call) issues the filter on the side stream right after F is built, while
+// the pair index is still sorting.
+struct TriStage {
+    bool valid = false;
+    int64_t delta = 0;
+    uint32_t f_begin = 0, f_end = 0;
+    uint64_t* wedges = nullptr;
+    uint64_t wedge_cap = 0;
+    uint32_t* long_list = nullptr;
+    uint64_t* wbuf = nullptr;
+};
+// what a one-shot count will run, known while the index is being built
+struct RunHint {
+    bool early_tri = false;  // count_all triangles over the full range
+    int64_t delta = 0;
+};
+
 struct DeviceGraph {
     uint64_t n = 0, m = 0, R = 0;
     uint32_t max_degree = 0;
@@ -137,6 +156,7 @@ struct DeviceGraph {
     uint32_t* pofs = nullptr;
 
     Forward fwd[2];
+    TriStage pre_tri;  // filter issued early for a one-shot count (RunHint)
 
     uint64_t* d_acc = nullptr;  // 64 u64: star raw [0,32), tri [32,56), work stats [56,64)
     uint64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // last run's work statistics
@@ -175,7 +195,7 @@ inline PView pview(const DeviceGraph& g) {
 
 // ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------
 void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst,
-                 const int64_t* d_t, uint64_t m, uint64_t n);
+                 const int64_t* d_t, uint64_t m, uint64_t n, const RunHint* hint = nullptr);
 // build_graph in two halves: build_prepare packs + validates and reads the
 // 4-word verdict back (the only host sync); build_finish issues the rest with
 // no host synchronisation, so it can be captured into a CUDA graph.  With a
@@ -200,7 +220,7 @@ struct BuildPlan {
 BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
                         uint64_t m, uint64_t n, BuildWorkspace* ws);
 void build_finish(DeviceGraph& g, BuildPlan& plan, const uint32_t* d_src, const uint32_t* d_dst,
-                  const int64_t* d_t);
+                  const int64_t* d_t, const RunHint* hint = nullptr);
 void release_plan(DeviceGraph& g, BuildPlan& plan);
 void free_graph(DeviceGraph& g);
 // builds fwd[mode] on stream st (no-op when built); for fwd[0] started
@@ -225,6 +245,10 @@ void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uin
 // once-counted triangle cells (24 u64) over forward positions [f_begin, f_end)
 void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
                   uint32_t f_end, int64_t t_end, uint64_t* d_out, uint64_t* d_stats);
+void tri_filter_stage(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin, uint32_t f_end,
+                      cudaStream_t st, TriStage& ts);
+void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_t t_end, uint64_t* d_out,
+                    uint64_t* d_stats);
 void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
                const uint64_t* d_begin, const uint64_t* d_item_off, uint64_t total,
                const uint8_t* d_live, uint64_t* d_out);

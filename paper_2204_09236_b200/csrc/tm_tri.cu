@@ -346,34 +346,55 @@ __global__ void __launch_bounds__(256) tri_items_kernel(SView S, PView P, int64_
 
 }  // namespace
 
-void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
-                  uint32_t f_end, int64_t t_end, uint64_t* d_out, uint64_t* d_stats) {
+void tri_filter_stage(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin, uint32_t f_end,
+                      cudaStream_t st, TriStage& ts) {
+    ts = TriStage{};
+    ts.delta = delta;
+    ts.f_begin = f_begin;
+    ts.f_end = f_end;
     if (f_end <= f_begin) return;
-    cudaStream_t st = g.stream;
     const uint64_t work = f_end - f_begin;
     const uint64_t cap = (uint64_t)sm_count() * 8;
     uint64_t grid = (work + 256 * kFilterItems - 1) / (256 * kFilterItems);
     if (grid > cap) grid = cap;
-    const uint64_t wedge_cap = work + 1024;  // overflow spills to the long list
-    uint64_t* wedges = dalloc<uint64_t>(wedge_cap, st);
+    ts.wedge_cap = work + 1024;  // overflow spills to the long list
+    ts.wedges = dalloc<uint64_t>(ts.wedge_cap, st);
     // [0] wedge slots reserved (u64: up to kWedgeScan per record), [1] valid
     // end, then the u32 long-list fill
-    uint64_t* wbuf = dalloc<uint64_t>(3, st);
-    unsigned long long* wcount = reinterpret_cast<unsigned long long*>(wbuf);
-    uint32_t* lcount = reinterpret_cast<uint32_t*>(wbuf + 2);
-    uint32_t* long_list = dalloc<uint32_t>(work + 1, st);
+    ts.wbuf = dalloc<uint64_t>(3, st);
+    unsigned long long* wcount = reinterpret_cast<unsigned long long*>(ts.wbuf);
+    uint32_t* lcount = reinterpret_cast<uint32_t*>(ts.wbuf + 2);
+    ts.long_list = dalloc<uint32_t>(work + 1, st);
     TM_CUDA(cudaMemsetAsync(wcount, 0, sizeof(uint64_t), st));
     TM_CUDA(cudaMemsetAsync(wcount + 1, 0xFF, sizeof(uint64_t), st));
     TM_CUDA(cudaMemsetAsync(lcount, 0, sizeof(uint32_t), st));
     TM_LAUNCH("tri_filter", st, tri_filter_kernel, (unsigned)grid, 256, 0, f.t.view(g.tbase), f.nbr, f.node, delta,
-              f_begin, f_end, wedges, wedge_cap, long_list, wcount, lcount);
+              f_begin, f_end, ts.wedges, ts.wedge_cap, ts.long_list, wcount, lcount);
+    ts.valid = true;
+}
+
+void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_t t_end, uint64_t* d_out,
+                    uint64_t* d_stats) {
+    if (!ts.valid) return;
+    cudaStream_t st = g.stream;
+    const uint64_t cap = (uint64_t)sm_count() * 8;
+    unsigned long long* wcount = reinterpret_cast<unsigned long long*>(ts.wbuf);
+    uint32_t* lcount = reinterpret_cast<uint32_t*>(ts.wbuf + 2);
     TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pview(g), f.t.view(g.tbase), f.nbr, f.ord,
-              delta, t_end, wedges, wedge_cap, wcount, d_out, d_stats);
+              ts.delta, t_end, ts.wedges, ts.wedge_cap, wcount, d_out, d_stats);
     TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pview(g), f.t.view(g.tbase), f.nbr, f.ord,
-              f.node, f.off, delta, t_end, long_list, lcount, d_out, d_stats);
-    dfree(wedges, st);
-    dfree(long_list, st);
-    dfree(wbuf, st);
+              f.node, f.off, ts.delta, t_end, ts.long_list, lcount, d_out, d_stats);
+    dfree(ts.wedges, st);
+    dfree(ts.long_list, st);
+    dfree(ts.wbuf, st);
+    ts.valid = false;
+}
+
+void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
+                  uint32_t f_end, int64_t t_end, uint64_t* d_out, uint64_t* d_stats) {
+    TriStage ts;
+    tri_filter_stage(g, f, delta, f_begin, f_end, g.stream, ts);
+    tri_work_stage(g, f, ts, t_end, d_out, d_stats);
 }
 
 void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
