@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
                                                        uint32_t* __restrict__ P_min,
                                                        uint32_t* __restrict__ P_max,
                                                        uint32_t* __restrict__ P_w, uint64_t n,
-                                                       uint32_t* __restrict__ pofs) {
+                                                       uint32_t* __restrict__ pofs,
+                                                       uint32_t* __restrict__ dmask) {
     using Codec = EdgeCodec<kNarrow>;
     __shared__ uint32_t s_a[258], s_b[258];
     const int tid = threadIdx.x;
@@ -291,6 +292,8 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
             if (k + 1 == m)
                 for (int64_t x = (int64_t)a + 1; x <= (int64_t)n; ++x) pofs[x] = (uint32_t)m;
         }
+        const unsigned db = __ballot_sync(0xffffffffu, k < m && Codec::dir_from_min(ed, a));
+        if ((tid & 31) == 0 && k < m) dmask[k >> 5] = db;
         __syncthreads();
     }
 }
@@ -574,6 +577,9 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
     g.P_max = dalloc<uint32_t>(m, s);
     g.P_w = dalloc<uint32_t>(m, s);
     g.P_min = dalloc<uint32_t>(m, s);
+    g.P_dmask = dalloc<uint32_t>(m / 32 + 1, s);
+    g.P_dpref = dalloc<uint32_t>(m / 32 + 2, s);
+    TM_CUDA(cudaMemsetAsync(g.P_dmask + m / 32, 0, sizeof(uint32_t), s));
 
     if (m == 0) {
         release_plan(g, pl);
@@ -674,11 +680,12 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
         if (narrow)
             TM_LAUNCH("gather_p", s, gather_p_kernel<true>, grid_for(m), 256, 0, pk0, m, perm, EN, tmin, g.P_t.w, g.P_t.n,
-                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs);
+                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask);
         else
             TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, perm, EW, tmin, g.P_t.w, g.P_t.n,
-                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs);
+                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask);
         dfree(pk0_alloc, s);
+        exclusive_scan<uint32_t>(PopcLoad{g.P_dmask}, m / 32 + 1, g.P_dpref, s);
         if (pl.owned) {
             dfree(spare, s);
             dfree(E, s);
@@ -782,7 +789,7 @@ void free_graph(DeviceGraph& g) {
     dfree(g.S_omask, s); dfree(g.S_opref, s); dfree(g.S_fmask, s); dfree(g.S_pidx, s);
     dfree(g.off, s);
     dfree(g.P_t.w, s); dfree(g.P_t.n, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
-    dfree(g.P_min, s); dfree(g.pofs, s);
+    dfree(g.P_min, s); dfree(g.pofs, s); dfree(g.P_dmask, s); dfree(g.P_dpref, s);
     dfree(g.pre_tri.wedges, s); dfree(g.pre_tri.long_list, s); dfree(g.pre_tri.wbuf, s);
     g.pre_tri.valid = false;
     for (auto& f : g.fwd) {

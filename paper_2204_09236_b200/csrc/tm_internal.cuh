@@ -20,6 +20,9 @@
 //     P_min[m], P_max[m]  u32  endpoints (the block of the smaller one is pofs)
 //     P_w[m]    u32    dir_rel_min << 31 | first << 30 | last << 29
 //     pofs[n+1] u32    first P position whose min endpoint is u
+//     P_dmask[m/32+1], P_dpref[m/32+2]  bitmask of dir_rel_min = 1 records and
+//               the prefix of its word popcounts: the direction split of any P
+//               range in four loads (long closing groups)
 //   F (forward-oriented sequences for the triangle pass, one per orientation)
 #pragma once
 
@@ -154,6 +157,8 @@ struct DeviceGraph {
     uint32_t* P_w = nullptr;
     uint32_t* P_min = nullptr;
     uint32_t* pofs = nullptr;
+    uint32_t* P_dmask = nullptr;
+    uint32_t* P_dpref = nullptr;
 
     Forward fwd[2];
     TriStage pre_tri;  // filter issued early for a one-shot count (RunHint)
@@ -180,7 +185,13 @@ struct PView {
     const uint32_t* w;
     const uint32_t* min;
     const uint32_t* pofs;
+    const uint32_t* dmask;
+    const uint32_t* dpref;
 };
+// P records with dir_rel_min = 1 before position x
+__device__ __forceinline__ uint32_t p_dir_before(const PView& P, uint32_t x) {
+    return P.dpref[x >> 5] + __popc(P.dmask[x >> 5] & ((1u << (x & 31)) - 1u));
+}
 inline SView sview(const DeviceGraph& g) {
     return {g.S_t.view(g.tbase), g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_opref, g.S_pidx, g.off};
 }
@@ -190,7 +201,7 @@ __device__ __forceinline__ uint32_t outward_before(const SView& S, uint32_t q) {
 }
 
 inline PView pview(const DeviceGraph& g) {
-    return {g.P_t.view(g.tbase), g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs};
+    return {g.P_t.view(g.tbase), g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs, g.P_dmask, g.P_dpref};
 }
 
 // ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------

@@ -104,11 +104,18 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] < t_end) l = mid + 1; else r = mid; }
         k2e = l;
     }
-    const uint32_t kend = ti < t_end ? k4 : k2;
-    for (uint32_t x = k1; x < kend; ++x) {
-        if (x >= k2e && x < k2) continue;
-        const uint32_t type = x < k2 ? 0u : (x < k3 ? 1u : 2u);
-        c[type * 2 + ((P.w[x] >> 31) ^ flip)] += 1;
+    // direction split of each type range from the P direction prefix
+    auto add_range = [&](int type, uint32_t x0, uint32_t x1) {
+        if (x1 <= x0) return;
+        const uint32_t n1 = p_dir_before(P, x1) - p_dir_before(P, x0);  // dir_rel_min = 1
+        const uint32_t n0 = (x1 - x0) - n1;
+        c[type * 2 + flip] += n0;
+        c[type * 2 + (flip ^ 1u)] += n1;
+    };
+    add_range(0, k1, k2e);
+    if (ti < t_end) {
+        add_range(1, k2, k3);
+        add_range(2, k3, k4);
     }
 }
 
