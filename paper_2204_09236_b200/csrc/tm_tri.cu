@@ -44,9 +44,11 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
     }
     if (l >= blk_end || P.max[l] != b) return;
     const uint32_t kb = l;
-    // short groups: classify record by record (triangle_engine.cpp:43-51)
+    // short groups: classify record by record (triangle_engine.cpp:43-51);
+    // a group still running 16 records on goes straight to the searches
     uint32_t k = kb;
-    for (int step = 0; step < 16; ++step, ++k) {
+    const bool is_long = kb + 16 < blk_end && P.max[kb + 16] == b;
+    for (int step = 0; step < 16 && !is_long; ++step, ++k) {
         const int64_t tk = P.t[k];
         const uint32_t wk = P.w[k];
         if (tk > hi) return;
