@@ -502,6 +502,10 @@ struct ReplayEntry {
     cudaGraphExec_t exec[4] = {nullptr, nullptr, nullptr, nullptr};
     uint64_t kernels[4] = {0, 0, 0, 0};  // kernel launches captured in each graph
     int eager_runs[4] = {0, 0, 0, 0};
+    // the t range a graph was captured for: its time base (narrow records) and
+    // time-sort key width are baked in, so different data re-captures it
+    int64_t cap_tmin[4] = {0, 0, 0, 0}, cap_tmax[4] = {0, 0, 0, 0};
+    int recaptures = 0;  // data keeps changing under the same buffers: stay eager
     void release() {
         for (auto& e : exec)
             if (e) {
@@ -613,7 +617,13 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
         run_passes(&G, cfg->delta, t_end, (motifs & 3u) != 0, (motifs & 4u) != 0, cfg->triangle_mode, 0,
                    (uint32_t)n, r, nullptr, collect);
     };
-    if (!E->exec[variant] && E->eager_runs[variant] == 0) {
+    if (E->exec[variant] && (E->cap_tmin[variant] != plan.tmin || E->cap_tmax[variant] != plan.tmax)) {
+        cudaGraphExecDestroy(E->exec[variant]);
+        E->exec[variant] = nullptr;
+        E->eager_runs[variant] = 0;
+        ++E->recaptures;
+    }
+    if (!E->exec[variant] && (E->eager_runs[variant] == 0 || E->recaptures > 2)) {
         // first run of this shape: eager (also initialises every lazy static)
         ++E->eager_runs[variant];
         try {
@@ -648,6 +658,8 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
         cudaGraphDestroy(graph);
         TM_CUDA(ie);
         E->exec[variant] = ex;
+        E->cap_tmin[variant] = plan.tmin;
+        E->cap_tmax[variant] = plan.tmax;
     } else {
         free_graph(G.g);  // (only returns the side streams: nothing was allocated)
     }

@@ -445,6 +445,32 @@ def test_repeated_one_shot_counts_graph_replay(cuda, tm, oracle):
     for _ in range(3):
         got = tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg, stream=st.cuda_stream)
         assert got.tolist() == want2
+    # same buffers, a shifted time range (the captured time base must follow)
+    for shift in (12345, 10 ** 9, 12345):
+        sh = np.ascontiguousarray(t + shift)
+        dt.copy_(torch.from_numpy(sh))
+        og3 = oracle.build_graph(n, s, d, sh)
+        want3 = oracle.census(og3, delta).tolist()
+        for _ in range(3):
+            got = tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg,
+                                        stream=st.cuda_stream)
+            assert got.tolist() == want3
+    # a time slice through the replay path (t_end is part of the config); then
+    # the same buffers with every time shifted and t_end shifted alike: the
+    # count must not change (a stale captured time base would move all times
+    # against t_end)
+    hi = int(np.sort(t)[m // 2])
+    ref = oracle.census_bruteforce_before(og, delta, hi).tolist()
+    for shift in (0, 0, 0, 10 ** 6, 10 ** 6, 10 ** 6):
+        dt.copy_(torch.from_numpy(np.ascontiguousarray(t + shift)))
+        raw = np.zeros(56, np.uint64)
+        tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(),
+                              tm.RunConfig(delta=delta, first_edge_t_end=hi + shift), stream=st.cuda_stream,
+                              raw_out=raw)
+        rc = tm.RawCounters.from_array(raw)
+        got = tm.merge_census(rc.star, rc.pair, rc.tri, tm.TriangleMode.count_all)
+        assert got.counts.tolist() == ref, shift
+    dt.copy_(torch.from_numpy(t))
     # host arrays (the e2e path)
     hs = torch.from_numpy(s.view(np.int32)).pin_memory()
     hd = torch.from_numpy(d.view(np.int32)).pin_memory()
