@@ -506,6 +506,8 @@ struct ReplayEntry {
     // time-sort key width are baked in, so different data re-captures it
     int64_t cap_tmin[4] = {0, 0, 0, 0}, cap_tmax[4] = {0, 0, 0, 0};
     int recaptures = 0;  // data keeps changing under the same buffers: stay eager
+    int last_variant = -1;  // replayed by the previous call (speculation target)
+    BuildVerdict* verdict = nullptr;  // pinned
     void release() {
         for (auto& e : exec)
             if (e) {
@@ -517,6 +519,8 @@ struct ReplayEntry {
         dfree(ws.nk0, s); dfree(ws.nk1, s); dfree(ws.c0, s); dfree(ws.E, s); dfree(ws.st, s);
         dfree(hs, s); dfree(hd, s); dfree(ht, s);
         cudaStreamSynchronize(s);
+        if (verdict) cudaFreeHost(verdict);
+        verdict = nullptr;
     }
 };
 struct ReplayCache {
@@ -597,6 +601,40 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
         dd = E->hd;
         dt = E->ht;
     }
+    const uint32_t motifs = cfg->motifs ? cfg->motifs : 7u;
+    const int64_t t_end = cfg->has_first_edge_t_end ? cfg->first_edge_t_end : INT64_MAX;
+    const bool full = !cfg->has_first_edge_t_end;
+    PassResult r;
+    if (!E->verdict) TM_CUDA(cudaMallocHost(&E->verdict, sizeof(BuildVerdict)));
+    // Speculative replay: when the previous call of this entry replayed a
+    // graph, pack + validate and launch that graph back to back without the
+    // verdict read-back in between; the verdict is checked afterwards (the
+    // pack clamps invalid ids, so even rejected input stays in bounds) and a
+    // call whose data changed variant or t range falls through to the
+    // checked path below.
+    if (E->last_variant >= 0 && E->exec[E->last_variant]) {
+        const int lv = E->last_variant;
+        tm_graph G;
+        G.g.stream = s;
+        BuildPlan plan;
+        try {
+            plan = build_prepare(G.g, ds, dd, dt, m, n, &E->ws, E->verdict);
+            TM_CUDA(cudaGraphLaunch(E->exec[lv], s));
+            collect_passes(&G, r);
+            plan_from_verdict(G.g, plan, *E->verdict);
+        } catch (...) {
+            free_graph(G.g);
+            throw;
+        }
+        free_graph(G.g);
+        const int v = (plan.narrow ? 2 : 0) | (plan.unsorted ? 1 : 0);
+        if (v == lv && E->cap_tmin[lv] == plan.tmin && E->cap_tmax[lv] == plan.tmax) {
+            g_launches.fetch_add(E->kernels[lv]);
+            finish_counts(r, cfg, full, raw, census36, nullptr);
+            return TM_OK;
+        }
+        E->last_variant = -1;  // the data moved: redo with the verdict first
+    }
     tm_graph G;
     G.g.stream = s;
     BuildPlan plan;
@@ -607,10 +645,6 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
         throw;
     }
     const int variant = (plan.narrow ? 2 : 0) | (plan.unsorted ? 1 : 0);
-    const uint32_t motifs = cfg->motifs ? cfg->motifs : 7u;
-    const int64_t t_end = cfg->has_first_edge_t_end ? cfg->first_edge_t_end : INT64_MAX;
-    const bool full = !cfg->has_first_edge_t_end;
-    PassResult r;
     const RunHint hint = hint_for(cfg, n);
     auto issue = [&](bool collect) {
         build_finish(G.g, plan, ds, dd, dt, &hint);
@@ -667,6 +701,7 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
     g_launches.fetch_add(E->kernels[variant]);  // the graph's kernels, launched from the device queue
     collect_passes(&G, r);
     finish_counts(r, cfg, full, raw, census36, nullptr);
+    E->last_variant = variant;
     return TM_OK;
 }
 

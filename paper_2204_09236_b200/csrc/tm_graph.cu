@@ -20,14 +20,7 @@ namespace tmb {
 
 namespace {
 
-struct BuildStats {
-    long long tmin;
-    long long tmax;
-    unsigned int bad;
-    unsigned int unsorted;
-    unsigned int max_degree;
-    unsigned int pad;
-};
+using BuildStats = BuildVerdict;
 
 // packed (t - tmin) << kbits | k  when it fits 64 bits, else key = t - tmin, val = k
 __global__ void time_keys_kernel(const int64_t* __restrict__ t, uint64_t m, int64_t tmin, int kbits,
@@ -120,10 +113,14 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
             const uint64_t p = (uint64_t)tile * kPackEdges + j * kPackBlock + threadIdx.x;
             if (p < m) {
                 const uint32_t k = perm ? perm[p] : (uint32_t)p;
-                const uint32_t a = src[k], b = dst[k];
+                uint32_t a = src[k], b = dst[k];
                 const int64_t tk = t[k];
                 if (st) {
                     bad |= (a == b) | (a >= n) | (b >= n);
+                    // keep a speculative build of invalid input in bounds
+                    // (the verdict rejects it afterwards)
+                    a = a < n ? a : 0u;
+                    b = b < n ? b : 0u;
                     lo = min(lo, (long long)tk);
                     hi = max(hi, (long long)tk);
                     if (p + 1 < m) uns |= (t[p + 1] < tk);
@@ -472,7 +469,7 @@ void release_side(DeviceGraph& g) {
 }  // namespace
 
 BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
-                        uint64_t m, uint64_t n, BuildWorkspace* ws) {
+                        uint64_t m, uint64_t n, BuildWorkspace* ws, BuildVerdict* h_async) {
     cudaStream_t s = g.stream;
     if (2 * m > 0xFFFFFFF0ull) throw tm_error(9, "graph too large: 2m must fit 32-bit positions");
     if (!g.aux[0]) acquire_side(g);
@@ -512,25 +509,32 @@ BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d
         d_st = dalloc<BuildStats>(1, s);
     }
     BuildStats h_st{LLONG_MAX, LLONG_MIN, 0, 0, 0, 0};
-    TM_CUDA(cudaMemcpyAsync(d_st, &h_st, sizeof(h_st), cudaMemcpyHostToDevice, s));
+    BuildStats* hv = h_async ? h_async : &h_st;
+    *hv = h_st;
+    TM_CUDA(cudaMemcpyAsync(d_st, hv, sizeof(h_st), cudaMemcpyHostToDevice, s));
     if (m) {
         TM_LAUNCH("pack_edges", s, pack_edges_kernel<true>, grid_for(m, kPackEdges), kPackBlock, 0, nullptr,
                   d_src, d_dst, d_t, m, n, (int64_t)0, reinterpret_cast<NarrowEdge*>(pl.E), pl.nk0, pl.c0,
                   pl.ntiles, d_st);
     }
-    TM_CUDA(cudaMemcpyAsync(&h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, s));
+    TM_CUDA(cudaMemcpyAsync(hv, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, s));
+    if (h_async) return pl;  // verdict read later (plan_from_verdict)
     TM_CUDA(cudaStreamSynchronize(s));
     if (!ws) dfree(d_st, s);
-    if (h_st.bad) {
+    plan_from_verdict(g, pl, h_st);
+    return pl;
+}
+
+void plan_from_verdict(DeviceGraph& g, BuildPlan& pl, const BuildVerdict& v) {
+    if (v.bad) {
         release_plan(g, pl);
         throw tm_error(1, "self-loop or out-of-range endpoint in edge list");
     }
     // narrow 8-byte edge records when the time span fits 32 bits
-    pl.narrow = (uint64_t)h_st.tmax - (uint64_t)h_st.tmin < (1ull << 32);
-    pl.unsorted = h_st.unsorted != 0;
-    pl.tmin = h_st.tmin;
-    pl.tmax = h_st.tmax;
-    return pl;
+    pl.narrow = (uint64_t)v.tmax - (uint64_t)v.tmin < (1ull << 32);
+    pl.unsorted = v.unsorted != 0;
+    pl.tmin = v.tmin;
+    pl.tmax = v.tmax;
 }
 
 void release_plan(DeviceGraph& g, BuildPlan& pl) {
@@ -541,7 +545,7 @@ void release_plan(DeviceGraph& g, BuildPlan& pl) {
 
 void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
                  uint64_t m, uint64_t n, const RunHint* hint) {
-    BuildPlan pl = build_prepare(g, d_src, d_dst, d_t, m, n, nullptr);
+    BuildPlan pl = build_prepare(g, d_src, d_dst, d_t, m, n, nullptr, nullptr);
     build_finish(g, pl, d_src, d_dst, d_t, hint);
 }
 

@@ -211,6 +211,15 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst,
 // 4-word verdict back (the only host sync); build_finish issues the rest with
 // no host synchronisation, so it can be captured into a CUDA graph.  With a
 // workspace, the prepare buffers are persistent (replayed graphs reuse them).
+// the pack kernel's 4-word verdict on the input
+struct BuildVerdict {
+    long long tmin;
+    long long tmax;
+    unsigned int bad;
+    unsigned int unsorted;
+    unsigned int max_degree;
+    unsigned int pad;
+};
 struct BuildWorkspace {
     uint64_t* nk0 = nullptr;
     uint64_t* nk1 = nullptr;
@@ -228,8 +237,11 @@ struct BuildPlan {
     bool narrow = true, unsorted = false, owned = true;
     int64_t tmin = 0, tmax = 0;
 };
+// h_async (pinned) set: the verdict is copied there without waiting and the
+// caller completes the plan with plan_from_verdict after synchronising
 BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
-                        uint64_t m, uint64_t n, BuildWorkspace* ws);
+                        uint64_t m, uint64_t n, BuildWorkspace* ws, BuildVerdict* h_async = nullptr);
+void plan_from_verdict(DeviceGraph& g, BuildPlan& plan, const BuildVerdict& v);
 void build_finish(DeviceGraph& g, BuildPlan& plan, const uint32_t* d_src, const uint32_t* d_dst,
                   const int64_t* d_t, const RunHint* hint = nullptr);
 void release_plan(DeviceGraph& g, BuildPlan& plan);

@@ -471,6 +471,17 @@ def test_repeated_one_shot_counts_graph_replay(cuda, tm, oracle):
         got = tm.merge_census(rc.star, rc.pair, rc.tri, tm.TriangleMode.count_all)
         assert got.counts.tolist() == ref, shift
     dt.copy_(torch.from_numpy(t))
+    # an invalid edge under a replaying entry: rejected (the speculative replay
+    # runs on clamped ids and is discarded), then valid data counts again
+    bad = s.copy()
+    bad[m // 3] = n + 5
+    ds.copy_(torch.from_numpy(bad.view(np.int32)))
+    with pytest.raises(ValueError):
+        tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg, stream=st.cuda_stream)
+    ds.copy_(torch.from_numpy(s.view(np.int32)))
+    for _ in range(2):
+        got = tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg, stream=st.cuda_stream)
+        assert got.tolist() == want
     # host arrays (the e2e path)
     hs = torch.from_numpy(s.view(np.int32)).pin_memory()
     hd = torch.from_numpy(d.view(np.int32)).pin_memory()
