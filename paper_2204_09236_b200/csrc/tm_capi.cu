@@ -299,8 +299,9 @@ void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do
     }
     // star pass on a side stream, concurrent with the triangle pass on s
     // (both mostly latency-bound gathers; they accumulate into disjoint cells)
-    cudaStream_t ss = g.aux[1] ? g.aux[1] : s;
-    if (do_star && g.R) {
+    const bool star_on = do_star && g.R;
+    cudaStream_t ss = (star_on && g.aux[1]) ? g.aux[1] : s;  // side stream only when used
+    if (star_on) {
         stream_after(g, ss, s);
         star_full(g, delta, cb, ce, t_end, g.d_acc, g.d_acc + 56, ss);
     }

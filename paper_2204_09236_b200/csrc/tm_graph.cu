@@ -701,6 +701,8 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
 
 void stream_after(DeviceGraph& g, cudaStream_t st, cudaStream_t from) {
     if (st == from) return;
+    for (int i = 0; i < 2; ++i)
+        if (st == g.aux[i]) g.aux_used[i] = true;
     TM_CUDA(cudaEventRecord(g.ev_fork, from));
     TM_CUDA(cudaStreamWaitEvent(st, g.ev_fork, 0));
 }
@@ -785,7 +787,11 @@ void free_graph(DeviceGraph& g) {
     cudaStream_t s = g.stream;
     if (g.aux[0]) {
         // the frees below are ordered after everything the side streams did
-        for (auto& a : g.aux) stream_after(g, s, a);
+        // (only streams that were forked: joining an unused one would tie a
+        // captured stream to uncaptured work)
+        for (int i = 0; i < 2; ++i)
+            if (g.aux_used[i]) stream_after(g, s, g.aux[i]);
+        g.aux_used[0] = g.aux_used[1] = false;
         release_side(g);
     }
     g.fwd_pending = false;

@@ -138,6 +138,7 @@ struct DeviceGraph {
     // while the triangle pass runs on `stream`.  fwd_ready marks fwd[0].
     cudaStream_t aux[2] = {nullptr, nullptr};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, fwd_ready = nullptr;
+    bool aux_used[2] = {false, false};  // forked from `stream` (must be joined back)
     bool fwd_pending = false;
 
     int64_t tbase = 0;  // t_min: base of the narrow (u32) timestamp arrays

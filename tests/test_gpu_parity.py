@@ -482,6 +482,14 @@ def test_repeated_one_shot_counts_graph_replay(cuda, tm, oracle):
     for _ in range(2):
         got = tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg, stream=st.cuda_stream)
         assert got.tolist() == want
+    # motif filters through the replay (the star side stream unused)
+    for mf in (tm.MotifFilter(star=False, pair=False), tm.MotifFilter(triangle=False)):
+        cfg_m = tm.RunConfig(delta=delta, motifs=mf)
+        base = tm.run_parallel(tm.GraphContext.build(tm.TemporalGraph.from_arrays(n, s, d, t)), cfg_m).counts.tolist()
+        for _ in range(3):
+            got = tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg_m,
+                                        stream=st.cuda_stream)
+            assert got.tolist() == base
     # host arrays (the e2e path)
     hs = torch.from_numpy(s.view(np.int32)).pin_memory()
     hd = torch.from_numpy(d.view(np.int32)).pin_memory()
