@@ -483,8 +483,9 @@ def test_repeated_one_shot_counts_graph_replay(cuda, tm, oracle):
         got = tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg, stream=st.cuda_stream)
         assert got.tolist() == want
     # motif filters through the replay (the star side stream unused)
-    for mf in (tm.MotifFilter(star=False, pair=False), tm.MotifFilter(triangle=False)):
-        cfg_m = tm.RunConfig(delta=delta, motifs=mf)
+    for cfg_m in (tm.RunConfig(delta=delta, motifs=tm.MotifFilter(star=False, pair=False)),
+                  tm.RunConfig(delta=delta, motifs=tm.MotifFilter(triangle=False)),
+                  tm.RunConfig(delta=delta, triangle_mode=tm.TriangleMode.removal)):
         base = tm.run_parallel(tm.GraphContext.build(tm.TemporalGraph.from_arrays(n, s, d, t)), cfg_m).counts.tolist()
         for _ in range(3):
             got = tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg_m,
