@@ -9,11 +9,12 @@
 // inter-block waiting).  Sort: LSD, 8-bit digits, 2048-key tiles; per pass an
 // upsweep (per-tile digit counts), a row scan (one block per digit) and a
 // persistent downsweep that streams the next tile into shared memory with TMA
-// (cp.async.bulk + mbarrier) while it ranks the current one with per-warp
-// __match_any_sync (stable), reorders it in place in shared memory and writes
-// each digit run as one burst.  The per-warp ranking chain is what bounds a
-// pass (profiles/sortbench.cu ablations: the same kernel with ranking removed
-// streams at ~6 TB/s).  Keys carry their payload in the low bits when it
+// (cp.async.bulk + mbarrier) while it ranks the current one (peer masks from
+// __match_any_sync for two of the eight rounds and a ballot multi-split for the
+// rest, so the ADU and ALU pipes share the work; per-warp running counts keep
+// input order), reorders it in place in shared memory and writes each digit
+// run as one burst.  Ranking, not HBM, bounds a pass (profiles/sortbench.cu,
+// profiles/rankbench.cu).  Keys carry their payload in the low bits when it
 // fits, so most sorts are keys-only.
 #pragma once
 
@@ -22,6 +23,10 @@
 #include <string>
 
 #include "tm_internal.cuh"
+
+#ifndef TM_RANK_MATCH_ROUNDS
+#define TM_RANK_MATCH_ROUNDS 4  // of the 8 ranking rounds per tile, how many use match.any
+#endif
 
 namespace tmb {
 
@@ -298,8 +303,8 @@ constexpr int kRadix = 256;
 
 template <typename K, int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK) radix_upsweep(const K* __restrict__ keys, uint64_t n,
-                                                       int shift, uint32_t* __restrict__ counts,
-                                                       uint32_t ntiles) {
+                                                       int shift, uint32_t dmask,
+                                                       uint32_t* __restrict__ counts, uint32_t ntiles) {
     constexpr int NW = BLOCK / 32;
     constexpr int TILE = BLOCK * ITEMS;
     __shared__ uint32_t hist[NW][kRadix];
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(BLOCK) radix_upsweep(const K* __restrict__ key
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
         const uint64_t i = base + r * 32 + lane;
-        if (i < n) atomicAdd(&hist[w][(uint32_t)(k[r] >> shift) & 255u], 1u);
+        if (i < n) atomicAdd(&hist[w][(uint32_t)(k[r] >> shift) & dmask], 1u);
     }
     __syncthreads();
     for (int d = threadIdx.x; d < kRadix; d += BLOCK) {
@@ -394,16 +399,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
-template <typename K, bool kVals, int BLOCK, int ITEMS, int MINB>
+#ifndef TM_RANK_MATCH_ROUNDS_NARROW
+#define TM_RANK_MATCH_ROUNDS_NARROW 2  // the same for passes of <= 4 digit bits
+#endif
+
+// NBITS: digit bits of this pass (8, or 4 for a short last pass); digits are
+// (key >> shift) & dmask with dmask < 2^NBITS
+template <typename K, bool kVals, int BLOCK, int ITEMS, int MINB, int NBITS>
 __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __restrict__ kin,
                                                                    const uint32_t* __restrict__ vin,
                                                                    K* __restrict__ kout,
                                                                    uint32_t* __restrict__ vout, uint64_t n,
-                                                                   int shift,
+                                                                   int shift, uint32_t dmask,
                                                                    const uint32_t* __restrict__ tile_offsets,
                                                                    uint32_t ntiles,
                                                                    const uint32_t* __restrict__ totals) {
     constexpr int NW = BLOCK / 32, TILE = BLOCK * ITEMS;
+    constexpr int kMatchRounds = NBITS >= 8 ? TM_RANK_MATCH_ROUNDS : TM_RANK_MATCH_ROUNDS_NARROW;
     static_assert(BLOCK >= kRadix, "one digit per thread");
     constexpr uint32_t STAGE_BYTES = TILE * (sizeof(K) + (kVals ? 4 : 0));
     extern __shared__ __align__(128) unsigned char tma_smem[];
@@ -413,7 +425,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
     auto stage_vals = [&](int s) {
         return reinterpret_cast<uint32_t*>(tma_smem + s * STAGE_BYTES + TILE * sizeof(K));
     };
-    __shared__ uint16_t wcnt[NW][kRadix];  // per-warp counts <= 32 * ITEMS, prefixes <= TILE
+    __shared__ __align__(16) uint16_t wcnt[NW][kRadix];  // per-warp digit counts, then (warp, digit) run starts
     __shared__ uint32_t dglob[kRadix];
     __shared__ __align__(8) uint64_t bar[2];
 
@@ -442,7 +454,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
         const int s = it & 1;
         const uint32_t next = tile + gridDim.x;
         if (tid == 0 && next < ntiles) issue(next, s ^ 1);
-        for (int i = tid; i < NW * kRadix; i += BLOCK) (&wcnt[0][0])[i] = 0;
+        for (int i = tid; i < NW * kRadix / 8; i += BLOCK) reinterpret_cast<uint4*>(&wcnt[0][0])[i] = make_uint4(0, 0, 0, 0);
         const uint64_t tbase = (uint64_t)tile * TILE;
         const uint32_t tile_n = (uint32_t)((n - tbase) < (uint64_t)TILE ? (n - tbase) : (uint64_t)TILE);
         // the tile's digit offsets, loaded now and used after the ranking
@@ -462,10 +474,31 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
             const uint32_t i = w * (ITEMS * 32) + r * 32 + lane;
             key[r] = sk[i];
             if (kVals) val[r] = sv[i];
-            dig[r] = i < tile_n ? ((uint32_t)(key[r] >> shift) & 255u) : 256u;
+            dig[r] = i < tile_n ? ((uint32_t)(key[r] >> shift) & dmask) : 256u;
         }
+        // Peer masks (lanes holding the same digit).  match.any costs ~60 clocks
+        // per warp-instruction per SM on 8-bit random digits (ADU pipe,
+        // profiles/rankbench.cu); a ballot multi-split costs ~4 ALU
+        // instructions per digit bit.  The first kMatchRounds rounds use
+        // match.any and the rest ballots, so the two pipes share the ranking.
+        const bool full_tile = tile_n == (uint32_t)TILE;
 #pragma unroll
-        for (int r = 0; r < ITEMS; ++r) rank[r] = __match_any_sync(0xffffffffu, dig[r]);
+        for (int r = 0; r < ITEMS; ++r) {
+            if (r < kMatchRounds) {
+                rank[r] = __match_any_sync(0xffffffffu, dig[r]);
+            } else {
+                uint32_t peers = full_tile ? 0xffffffffu : __ballot_sync(0xffffffffu, dig[r] < 256u);
+                if (dig[r] >= 256u) peers = ~peers;
+#pragma unroll
+                for (int b = 0; b < NBITS; ++b) {
+                    const bool bit = (dig[r] >> b) & 1u;
+                    const uint32_t v = __ballot_sync(0xffffffffu, bit);
+                    peers &= v ^ (bit ? 0u : 0xffffffffu);
+                }
+                rank[r] = peers;
+            }
+        }
+        // running per-warp digit counts, one load -> store step per round
 #pragma unroll
         for (int r = 0; r < ITEMS; ++r) {
             const bool valid = dig[r] < 256u;
@@ -504,11 +537,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
             }
         }
         __syncthreads();
-        for (uint32_t i = tid; i < tile_n; i += BLOCK) {
-            const K k = sk[i];
-            const uint32_t dest = dglob[(uint32_t)(k >> shift) & 255u] + i;
-            kout[dest] = k;
-            if (kVals) vout[dest] = sv[i];
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const uint32_t i = r * BLOCK + tid;
+            if (i < tile_n) {
+                const K k = sk[i];
+                const uint32_t dest = dglob[(uint32_t)(k >> shift) & dmask] + i;
+                kout[dest] = k;
+                if (kVals) vout[dest] = sv[i];
+            }
         }
         __syncthreads();
     }
@@ -519,6 +556,26 @@ constexpr uint64_t kSortPad = 4;
 // first digit itself must use the same tiles: digit-major counts[d][tile])
 constexpr int kSortBlock = 256, kSortItems = 8, kSortTile = kSortBlock * kSortItems;
 
+// one downsweep instantiation: sets its shared-memory limit and caches its
+// occupancy on first use, then launches a persistent grid
+template <typename K, bool kVals, int BLOCK, int ITEMS, int MINB, int NBITS>
+void launch_downsweep(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint64_t n, int shift,
+                      uint32_t dmask, const uint32_t* offs, uint32_t ntiles, const uint32_t* totals,
+                      cudaStream_t s) {
+    constexpr int TILE = BLOCK * ITEMS;
+    constexpr size_t smem = 2 * TILE * (sizeof(K) + (kVals ? sizeof(uint32_t) : 0));
+    auto kern = radix_downsweep_tma<K, kVals, BLOCK, ITEMS, MINB, NBITS>;
+    static int per_sm = 0;  // resident blocks per SM
+    if (per_sm == 0) {
+        TM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem));
+        if (per_sm < 1) per_sm = 1;
+    }
+    const unsigned pgrid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * per_sm);
+    TM_LAUNCH("radix_downsweep", s, kern, pgrid, BLOCK, smem, kin, vin, kout, vout, n, shift, dmask, offs,
+              ntiles, totals);
+}
+
 // one pass configuration: tile = BLOCK * ITEMS keys
 template <typename K, int BLOCK, int ITEMS, int MINB>
 void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
@@ -527,52 +584,39 @@ void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt
     const bool with_vals = vals != nullptr;
     const int passes = (bit_hi - bit_lo + 7) / 8;
     const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
-    const size_t smem = 2 * TILE * (sizeof(K) + (with_vals ? sizeof(uint32_t) : 0));
-    static bool attr_set = false;
-    if (!attr_set) {
-        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, true, BLOCK, ITEMS, MINB>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(2 * TILE * (sizeof(K) + sizeof(uint32_t)))));
-        TM_CUDA(cudaFuncSetAttribute(radix_downsweep_tma<K, false, BLOCK, ITEMS, MINB>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(2 * TILE * sizeof(K))));
-        attr_set = true;
-    }
-    static int occ[2] = {0, 0};  // resident downsweep blocks per SM (keys-only, with values)
-    int& per_sm = occ[with_vals ? 1 : 0];
-    if (per_sm == 0) {
-        if (with_vals)
-            TM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, radix_downsweep_tma<K, true, BLOCK, ITEMS, MINB>, BLOCK, smem));
-        else
-            TM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, radix_downsweep_tma<K, false, BLOCK, ITEMS, MINB>, BLOCK, smem));
-        if (per_sm < 1) per_sm = 1;
-    }
     const uint64_t ncount = (uint64_t)kRadix * ntiles;
     uint32_t* counts = dalloc<uint32_t>(2 * ncount + (uint64_t)kRadix * passes, s);
     uint32_t* offs = counts + ncount;
     uint32_t* totals = offs + ncount;  // 256 digit totals (per pass, reused)
-    const unsigned pgrid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * per_sm);
     for (int p = 0; p < passes; ++p) {
         const int shift = bit_lo + 8 * p;
+        const int width = std::min(8, bit_hi - shift);
+        const uint32_t dmask = (1u << width) - 1u;
         const uint32_t* cin = counts;
         if (p == 0 && first_counts) {
             cin = first_counts;  // the producer of the keys already counted pass 0
         } else {
             TM_LAUNCH("radix_upsweep", s, (radix_upsweep<K, BLOCK, ITEMS>), ntiles, BLOCK, 0, keys, n, shift,
-                      counts, ntiles);
+                      dmask, counts, ntiles);
         }
         TM_LAUNCH("radix_scan", s, radix_scan_counts, kRadix, 256, 0, cin, ntiles, offs, totals);
         if (with_vals) {
-            TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, true, BLOCK, ITEMS, MINB>), pgrid, BLOCK,
-                      smem, keys, vals, keys_alt, vals_alt, n, shift, offs, ntiles, totals);
+            if (width <= 4)
+                launch_downsweep<K, true, BLOCK, ITEMS, MINB, 4>(keys, vals, keys_alt, vals_alt, n, shift, dmask,
+                                                                 offs, ntiles, totals, s);
+            else
+                launch_downsweep<K, true, BLOCK, ITEMS, MINB, 8>(keys, vals, keys_alt, vals_alt, n, shift, dmask,
+                                                                 offs, ntiles, totals, s);
             uint32_t* tv = vals;
             vals = vals_alt;
             vals_alt = tv;
         } else {
-            TM_LAUNCH("radix_downsweep", s, (radix_downsweep_tma<K, false, BLOCK, ITEMS, MINB>), pgrid, BLOCK,
-                      smem, keys, nullptr, keys_alt, nullptr, n, shift, offs, ntiles, totals);
+            if (width <= 4)
+                launch_downsweep<K, false, BLOCK, ITEMS, MINB, 4>(keys, nullptr, keys_alt, nullptr, n, shift,
+                                                                  dmask, offs, ntiles, totals, s);
+            else
+                launch_downsweep<K, false, BLOCK, ITEMS, MINB, 8>(keys, nullptr, keys_alt, nullptr, n, shift,
+                                                                  dmask, offs, ntiles, totals, s);
         }
         K* tk = keys;
         keys = keys_alt;
