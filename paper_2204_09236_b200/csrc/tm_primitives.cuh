@@ -10,7 +10,7 @@
 // upsweep (per-tile digit counts), a row scan (one block per digit) and a
 // persistent downsweep that streams the next tile into shared memory with TMA
 // (cp.async.bulk + mbarrier) while it ranks the current one (peer masks from
-// __match_any_sync for two of the eight rounds and a ballot multi-split for the
+// __match_any_sync for one of the eight rounds and a ballot multi-split for the
 // rest, so the ADU and ALU pipes share the work; per-warp running counts keep
 // input order), reorders it in place in shared memory and writes each digit
 // run as one burst.  Ranking, not HBM, bounds a pass (profiles/sortbench.cu,
@@ -25,7 +25,7 @@
 #include "tm_internal.cuh"
 
 #ifndef TM_RANK_MATCH_ROUNDS
-#define TM_RANK_MATCH_ROUNDS 4  // of the 8 ranking rounds per tile, how many use match.any
+#define TM_RANK_MATCH_ROUNDS 1  // of the 8 ranking rounds per tile, how many use match.any
 #endif
 
 namespace tmb {
@@ -399,8 +399,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// one digit bit of the ballot multi-split: the lanes whose bit equals ours
+// (and-test with predicate out, vote, select, xor: four instructions)
+__device__ __forceinline__ uint32_t wlms_bit(uint32_t d, uint32_t bit) {
+    uint32_t r;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 v, s, a;\n\t"
+        "and.b32 a, %1, %2;\n\t"
+        "setp.ne.u32 p, a, 0;\n\t"
+        "vote.sync.ballot.b32 v, p, 0xffffffff;\n\t"
+        "selp.b32 s, 0, -1, p;\n\t"
+        "xor.b32 %0, v, s;\n\t}"
+        : "=r"(r)
+        : "r"(d), "r"(bit));
+    return r;
+}
+
 #ifndef TM_RANK_MATCH_ROUNDS_NARROW
-#define TM_RANK_MATCH_ROUNDS_NARROW 2  // the same for passes of <= 4 digit bits
+#define TM_RANK_MATCH_ROUNDS_NARROW 1  // the same for passes of <= 4 digit bits
 #endif
 
 // NBITS: digit bits of this pass (8, or 4 for a short last pass); digits are
@@ -490,11 +505,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
                 uint32_t peers = full_tile ? 0xffffffffu : __ballot_sync(0xffffffffu, dig[r] < 256u);
                 if (dig[r] >= 256u) peers = ~peers;
 #pragma unroll
-                for (int b = 0; b < NBITS; ++b) {
-                    const bool bit = (dig[r] >> b) & 1u;
-                    const uint32_t v = __ballot_sync(0xffffffffu, bit);
-                    peers &= v ^ (bit ? 0u : 0xffffffffu);
-                }
+                for (int b = 0; b < NBITS; ++b) peers &= wlms_bit(dig[r], 1u << b);
                 rank[r] = peers;
             }
         }
