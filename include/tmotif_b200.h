@@ -123,6 +123,19 @@ int tm_run_parallel(tm_graph* g, const tm_run_config* cfg, tm_counters* raw, uin
 int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
                    uint64_t n, int device_ptrs, void* stream, const tm_run_config* cfg,
                    tm_counters* raw, uint64_t* census36, tm_phase_timings* timings);
+/* Pipelined variant of tm_count_edges for callers that stream batches from
+ * host memory (serving): enqueues the host->device copy of the edge arrays on
+ * a copy stream, the census on `stream` once its copy has landed, and the
+ * counter read-back, then returns a ticket without waiting, so the copy of
+ * the next batch overlaps this batch's census.  Host arrays should be pinned
+ * for the copy to be asynchronous.  At most two batches per host thread are
+ * staged at a time (a third call first completes the oldest, whose result is
+ * kept for its tm_count_edges_wait).  Results are those of tm_count_edges on
+ * the same arrays; errors (invalid edges, ...) are reported by the wait. */
+int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
+                         uint64_t n, void* stream, const tm_run_config* cfg, uint64_t* ticket);
+/* Blocks until the ticket's census is done and returns it (once per ticket). */
+int tm_count_edges_wait(uint64_t ticket, tm_counters* raw, uint64_t* census36);
 /* One rank's share of a time-sliced census (multi-GPU without a replicated
  * index build): the edges with t in [t_lo, t_hi + delta) are compacted on the
  * GPU (ingestion order kept), indexed, and counted for the instances whose

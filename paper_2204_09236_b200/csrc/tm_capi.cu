@@ -226,11 +226,21 @@ struct PinnedAcc {
         if (cudaMallocHost(&h, 64 * sizeof(uint64_t)) != cudaSuccess) h = nullptr;
     }
 };
+// replayed graphs copy their counters into their own entry's pinned buffer
+// (two asynchronous censuses can be in flight), everything else into the
+// thread's buffer
+thread_local uint64_t* g_acc_override = nullptr;
 uint64_t* pinned_acc() {
+    if (g_acc_override) return g_acc_override;
     static thread_local PinnedAcc p;
     if (!p.h) throw tm_error(TM_ERR_CUDA, "cannot allocate pinned host buffer");
     return p.h;
 }
+struct AccOverride {
+    uint64_t* prev;
+    explicit AccOverride(uint64_t* p) : prev(g_acc_override) { g_acc_override = p; }
+    ~AccOverride() { g_acc_override = prev; }
+};
 
 template <typename F>
 int guarded(F&& f) {
@@ -274,9 +284,11 @@ struct PassResult {
     uint64_t tri_once[24];
 };
 
-// host side of a pass: wait for the counter copy and unpack it
-void collect_passes(tm_graph* G, PassResult& r) {
-    TM_CUDA(cudaStreamSynchronize(G->g.stream));
+// host side of a pass: wait for the counter copy (the whole stream, or just
+// up to `done` when later work is already queued behind it) and unpack it
+void collect_passes(tm_graph* G, PassResult& r, cudaEvent_t done = nullptr) {
+    if (done) TM_CUDA(cudaEventSynchronize(done));
+    else TM_CUDA(cudaStreamSynchronize(G->g.stream));
     const uint64_t* h = pinned_acc();
     std::memcpy(r.star_raw, h, 32 * sizeof(uint64_t));
     std::memcpy(r.tri_once, h + 32, 24 * sizeof(uint64_t));
@@ -509,6 +521,7 @@ struct ReplayEntry {
     int recaptures = 0;  // data keeps changing under the same buffers: stay eager
     int last_variant = -1;  // replayed by the previous call (speculation target)
     BuildVerdict* verdict = nullptr;  // pinned
+    uint64_t* acc = nullptr;          // pinned: the graph's counter read-back
     void release() {
         for (auto& e : exec)
             if (e) {
@@ -522,7 +535,22 @@ struct ReplayEntry {
         cudaStreamSynchronize(s);
         if (verdict) cudaFreeHost(verdict);
         verdict = nullptr;
+        if (acc) cudaFreeHost(acc);
+        acc = nullptr;
     }
+};
+
+constexpr int kPending = 100;  // count_edges_replay left a speculative replay in flight
+
+// A speculative replay launched but not yet collected (asynchronous API):
+// completing it synchronises, checks the verdict against the replayed
+// variant and unpacks the counters.
+struct ReplayPending {
+    ReplayEntry* E = nullptr;
+    tm_graph G;
+    BuildPlan plan;
+    int lv = -1;
+    bool full = true;
 };
 struct ReplayCache {
     std::vector<ReplayEntry*> entries;  // most recent last
@@ -558,7 +586,7 @@ bool replay_enabled() {
 
 int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m, uint64_t n,
                        int device_ptrs, void* stream, const tm_run_config* cfg, tm_counters* raw,
-                       uint64_t* census36) {
+                       uint64_t* census36, ReplayPending* pend = nullptr) {
     ensure_device();
     check_config(cfg);
     if (!src || !dst || !t) throw tm_error(TM_ERR_INVALID, "null edge arrays");
@@ -607,6 +635,8 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
     const bool full = !cfg->has_first_edge_t_end;
     PassResult r;
     if (!E->verdict) TM_CUDA(cudaMallocHost(&E->verdict, sizeof(BuildVerdict)));
+    if (!E->acc) TM_CUDA(cudaMallocHost(&E->acc, 64 * sizeof(uint64_t)));
+    AccOverride acc_scope(E->acc);
     // Speculative replay: when the previous call of this entry replayed a
     // graph, pack + validate and launch that graph back to back without the
     // verdict read-back in between; the verdict is checked afterwards (the
@@ -621,6 +651,16 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
         try {
             plan = build_prepare(G.g, ds, dd, dt, m, n, &E->ws, E->verdict);
             TM_CUDA(cudaGraphLaunch(E->exec[lv], s));
+            if (pend) {  // asynchronous: collected by complete_pending
+                g_launches.fetch_add(E->kernels[lv]);
+                pend->E = E;
+                pend->G.g = G.g;
+                G.g = DeviceGraph();
+                pend->plan = plan;
+                pend->lv = lv;
+                pend->full = full;
+                return kPending;
+            }
             collect_passes(&G, r);
             plan_from_verdict(G.g, plan, *E->verdict);
         } catch (...) {
@@ -704,6 +744,97 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
     finish_counts(r, cfg, full, raw, census36, nullptr);
     E->last_variant = variant;
     return TM_OK;
+}
+
+// Finish a speculative replay: wait, check the verdict against the replayed
+// variant and t range, unpack.  Returns false when the data did not match the
+// graph (the caller re-runs the checked path on the same device arrays).
+bool complete_pending(ReplayPending& P, cudaEvent_t done, const tm_run_config* cfg, tm_counters* raw,
+                      uint64_t* census36) {
+    ReplayEntry* E = P.E;
+    PassResult r;
+    bool ok = false;
+    try {
+        AccOverride acc_scope(E->acc);
+        collect_passes(&P.G, r, done);
+        plan_from_verdict(P.G.g, P.plan, *E->verdict);
+        const int v = (P.plan.narrow ? 2 : 0) | (P.plan.unsorted ? 1 : 0);
+        ok = v == P.lv && E->cap_tmin[v] == P.plan.tmin && E->cap_tmax[v] == P.plan.tmax;
+    } catch (...) {
+        free_graph(P.G.g);
+        throw;
+    }
+    free_graph(P.G.g);
+    if (!ok) {
+        E->last_variant = -1;
+        return false;
+    }
+    finish_counts(r, cfg, P.full, raw, census36, nullptr);
+    return true;
+}
+
+// Per-host-thread pipeline of the asynchronous API: two staging slots of
+// device input buffers, filled on a copy stream while the other slot's
+// census runs.
+struct AsyncResult {
+    int rc = TM_OK;
+    std::string err;
+    tm_counters raw;
+    uint64_t census[36];
+};
+struct AsyncSlot {
+    uint32_t* ds = nullptr;
+    uint32_t* dd = nullptr;
+    int64_t* dt = nullptr;
+    uint64_t cap = 0;
+    cudaEvent_t copied = nullptr, done = nullptr;
+    bool busy = false, pending = false;
+    uint64_t ticket = 0, m = 0, n = 0;
+    cudaStream_t s = nullptr;
+    tm_run_config cfg;
+    ReplayPending P;
+    AsyncResult res;  // when !pending
+};
+struct AsyncPipe {
+    cudaStream_t copy = nullptr;
+    AsyncSlot slot[2];
+    uint64_t next = 1;
+    std::vector<std::pair<uint64_t, AsyncResult>> finished;  // completed, not yet waited
+    ~AsyncPipe() {
+        for (auto& sl : slot) {
+            if (sl.copied) cudaEventDestroy(sl.copied);
+            if (sl.done) cudaEventDestroy(sl.done);
+            if (sl.ds) {
+                cudaFree(sl.ds);
+                cudaFree(sl.dd);
+                cudaFree(sl.dt);
+            }
+        }
+        if (copy) cudaStreamDestroy(copy);
+    }
+};
+thread_local AsyncPipe g_async;
+
+// run the slot's census to completion (speculation checked, re-run if needed)
+AsyncResult finish_slot(AsyncSlot& sl) {
+    AsyncResult out;
+    try {
+        if (sl.pending) {
+            sl.pending = false;
+            if (!complete_pending(sl.P, sl.done, &sl.cfg, &out.raw, out.census))
+                count_edges_replay(sl.ds, sl.dd, sl.dt, sl.m, sl.n, 1, sl.s, &sl.cfg, &out.raw, out.census);
+        } else {
+            out = sl.res;
+        }
+    } catch (const tm_error& e) {
+        out.rc = e.code;
+        out.err = e.what();
+    } catch (const std::exception& e) {
+        out.rc = TM_ERR_CUDA;
+        out.err = e.what();
+    }
+    sl.busy = false;
+    return out;
 }
 
 void free_impl(tm_graph* G) {
@@ -980,6 +1111,100 @@ int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, u
         free_impl(G);
         if (timings) timings->index_ms = index_ms;
         return rc;
+    });
+}
+
+int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
+                         uint64_t n, void* stream, const tm_run_config* cfg, uint64_t* ticket) {
+    return guarded([&] {
+        ensure_device();
+        check_config(cfg);
+        if (!ticket || (m && (!src || !dst || !t))) throw tm_error(TM_ERR_INVALID, "null argument");
+        if (cfg->center_begin != 0 || (cfg->center_end != 0 && cfg->center_end != n))
+            throw tm_error(TM_ERR_CONFIG, "asynchronous census: whole-graph runs only");
+        AsyncPipe& A = g_async;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (!s) {
+            if (!g_replay.own) TM_CUDA(cudaStreamCreateWithFlags(&g_replay.own, cudaStreamNonBlocking));
+            s = g_replay.own;
+        }
+        if (!A.copy) TM_CUDA(cudaStreamCreateWithFlags(&A.copy, cudaStreamNonBlocking));
+        const uint64_t tk = A.next++;
+        AsyncSlot& sl = A.slot[tk & 1];
+        if (sl.busy) A.finished.emplace_back(sl.ticket, finish_slot(sl));  // oldest batch first
+        if (!sl.copied) {
+            TM_CUDA(cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming));
+            TM_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+            TM_CUDA(cudaEventRecord(sl.done, s));
+        }
+        if (sl.cap < m) {  // (re)size the staging buffers once the slot is idle
+            TM_CUDA(cudaEventSynchronize(sl.done));
+            if (sl.ds) {
+                cudaFree(sl.ds);
+                cudaFree(sl.dd);
+                cudaFree(sl.dt);
+            }
+            TM_CUDA(cudaMalloc(&sl.ds, m * sizeof(uint32_t)));
+            TM_CUDA(cudaMalloc(&sl.dd, m * sizeof(uint32_t)));
+            TM_CUDA(cudaMalloc(&sl.dt, m * sizeof(int64_t)));
+            sl.cap = m;
+        }
+        sl.busy = true;
+        sl.ticket = tk;
+        sl.m = m;
+        sl.n = n;
+        sl.s = s;
+        sl.cfg = *cfg;
+        sl.pending = false;
+        sl.res = AsyncResult();
+        // copy stream: wait until the slot's previous census stopped reading it
+        TM_CUDA(cudaStreamWaitEvent(A.copy, sl.done, 0));
+        if (m) {
+            TM_CUDA(cudaMemcpyAsync(sl.ds, src, m * sizeof(uint32_t), cudaMemcpyHostToDevice, A.copy));
+            TM_CUDA(cudaMemcpyAsync(sl.dd, dst, m * sizeof(uint32_t), cudaMemcpyHostToDevice, A.copy));
+            TM_CUDA(cudaMemcpyAsync(sl.dt, t, m * sizeof(int64_t), cudaMemcpyHostToDevice, A.copy));
+        }
+        TM_CUDA(cudaEventRecord(sl.copied, A.copy));
+        TM_CUDA(cudaStreamWaitEvent(s, sl.copied, 0));
+        try {
+            int rc;
+            if (m)
+                rc = count_edges_replay(sl.ds, sl.dd, sl.dt, m, n, 1, s, cfg, &sl.res.raw, sl.res.census, &sl.P);
+            else
+                rc = tm_count_edges(sl.ds, sl.dd, sl.dt, 0, n, 1, s, cfg, &sl.res.raw, sl.res.census, nullptr);
+            sl.pending = rc == kPending;
+            if (!sl.pending) sl.res.rc = rc;
+        } catch (const tm_error& e) {
+            sl.res.rc = e.code;
+            sl.res.err = e.what();
+        }
+        TM_CUDA(cudaEventRecord(sl.done, s));
+        *ticket = tk;
+        return TM_OK;
+    });
+}
+
+int tm_count_edges_wait(uint64_t ticket, tm_counters* raw, uint64_t* census36) {
+    return guarded([&] {
+        AsyncPipe& A = g_async;
+        AsyncResult res;
+        bool found = false;
+        for (size_t i = 0; i < A.finished.size(); ++i)
+            if (A.finished[i].first == ticket) {
+                res = A.finished[i].second;
+                A.finished.erase(A.finished.begin() + i);
+                found = true;
+                break;
+            }
+        if (!found) {
+            AsyncSlot& sl = A.slot[ticket & 1];
+            if (!sl.busy || sl.ticket != ticket) throw tm_error(TM_ERR_INVALID, "unknown or already collected ticket");
+            res = finish_slot(sl);
+        }
+        if (res.rc != TM_OK) throw tm_error(res.rc, res.err.empty() ? "census failed" : res.err);
+        if (raw) *raw = res.raw;
+        if (census36) std::memcpy(census36, res.census, sizeof(res.census));
+        return TM_OK;
     });
 }
 

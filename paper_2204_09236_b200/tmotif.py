@@ -127,6 +127,9 @@ def lib():
                                   C.POINTER(_Timings)]
     L.tm_count_edges.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint64, C.c_int, VP,
                                  C.POINTER(_RunConfig), C.POINTER(_Counters), VP, C.POINTER(_Timings)]
+    L.tm_count_edges_async.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint64, VP, C.POINTER(_RunConfig),
+                                       C.POINTER(C.c_uint64)]
+    L.tm_count_edges_wait.argtypes = [C.c_uint64, C.POINTER(_Counters), VP]
     L.tm_count_edges_time_slice.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint64, C.c_int, VP,
                                             C.POINTER(_RunConfig), C.c_int, C.c_int64, C.c_int, C.c_int64,
                                             C.POINTER(_Counters), C.POINTER(_Timings)]
@@ -811,6 +814,45 @@ def count_edges(n: int, src, dst, t, config: RunConfig, stream: Optional[int] = 
         timings.index_ms, timings.star_pair_ms = tm.index_ms, tm.star_pair_ms
         timings.triangle_ms, timings.merge_ms = tm.triangle_ms, tm.merge_ms
     return census
+
+
+class PendingCensus:
+    """A census submitted with count_edges_async; result() waits for it.  Keeps
+    the host arrays alive until their copy to the device has been waited for."""
+
+    def __init__(self, ticket: int, arrays):
+        self.ticket = ticket
+        self._arrays = arrays
+        self._census = None
+
+    def result(self, raw_out: Optional[np.ndarray] = None) -> np.ndarray:
+        if self._census is None:
+            L = lib()
+            raw = _Counters()
+            census = np.zeros(36, np.uint64)
+            _raise(L.tm_count_edges_wait(self.ticket, C.byref(raw), census.ctypes.data), L)
+            self._raw = np.concatenate([np.frombuffer(raw.star, np.uint64), np.frombuffer(raw.pair, np.uint64),
+                                        np.frombuffer(raw.tri, np.uint64)])
+            self._census = census
+            self._arrays = None
+        if raw_out is not None:
+            raw_out[:56] = self._raw
+        return self._census
+
+
+def count_edges_async(n: int, src, dst, t, config: RunConfig, stream: Optional[int] = None) -> PendingCensus:
+    """Pipelined count_edges for batches streamed from host memory
+    (tm_count_edges_async): the copy of this batch overlaps the previous
+    batch's census.  src/dst/t should live in pinned memory."""
+    L = lib()
+    src = np.ascontiguousarray(src, np.uint32)
+    dst = np.ascontiguousarray(dst, np.uint32)
+    t = np.ascontiguousarray(t, np.int64)
+    cfg = config.to_c()
+    ticket = C.c_uint64(0)
+    _raise(L.tm_count_edges_async(src.ctypes.data, dst.ctypes.data, t.ctypes.data, len(src), n, stream,
+                                  C.byref(cfg), C.byref(ticket)), L)
+    return PendingCensus(ticket.value, (src, dst, t))
 
 
 def count_edges_device(n: int, m: int, src_ptr: int, dst_ptr: int, t_ptr: int, config: RunConfig,

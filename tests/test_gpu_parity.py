@@ -499,3 +499,62 @@ def test_repeated_one_shot_counts_graph_replay(cuda, tm, oracle):
         got = tm.count_edges(n, hs.numpy().view(np.uint32), hd.numpy().view(np.uint32), ht.numpy(), cfg,
                              stream=st.cuda_stream)
         assert got.tolist() == want
+
+
+def test_async_pipelined_counts(cuda, tm, oracle):
+    """tm_count_edges_async / tm_count_edges_wait: batches streamed from pinned
+    host memory with two in flight must each equal the oracle's census of the
+    batch they were submitted with -- through the staging slots' eager run,
+    capture and speculative replay, with data that switches variant (reversed
+    time order) or t range under a replaying slot, an invalid batch (reported
+    by its wait, neighbours unaffected) and more submissions than slots before
+    any wait."""
+    import torch
+    n, m, delta = 60, 4000, 150
+    batches = []
+    for seed in range(3):
+        s, d, t = oracle.generate_random_graph(n, m, 20000, 300 + seed)
+        batches.append((s, d, t))
+    s0, d0, t0 = batches[0]
+    batches.append((s0, d0, np.ascontiguousarray(t0[::-1])))   # unsorted variant
+    batches.append((s0, d0, np.ascontiguousarray(t0 + 10 ** 7)))  # shifted t range
+    want = []
+    for s, d, t in batches:
+        og = oracle.build_graph(n, s, d, t)
+        want.append(oracle.census(og, delta).tolist())
+        oracle.free(og)
+    pinned = [tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).pin_memory() for a in b)
+              for b in batches]
+
+    def host(i):
+        ps, pd, pt = pinned[i]
+        return ps.numpy().view(np.uint32), pd.numpy().view(np.uint32), pt.numpy()
+
+    cfg = tm.RunConfig(delta=delta)
+    st = torch.cuda.Stream()
+    order = [0, 1, 0, 1, 2, 0, 3, 1, 4, 4, 2, 3, 0, 0, 1]
+    pend = []
+    for i in order:
+        pend.append((i, tm.count_edges_async(n, *host(i), cfg, stream=st.cuda_stream)))
+        if len(pend) > 1:
+            j, p = pend.pop(0)
+            assert p.result().tolist() == want[j], j
+    for j, p in pend:
+        assert p.result().tolist() == want[j], j
+    # three submissions before the first wait (the oldest completes internally)
+    ps = [(i, tm.count_edges_async(n, *host(i), cfg, stream=st.cuda_stream)) for i in (1, 2, 0)]
+    for j, p in reversed(ps):
+        assert p.result().tolist() == want[j], j
+    # an invalid batch: its wait raises, the next batch is unaffected
+    s, d, t = batches[0]
+    bad = s.copy()
+    bad[m // 2] = n + 3
+    pb = torch.from_numpy(bad.view(np.int32)).pin_memory()
+    p_bad = tm.count_edges_async(n, pb.numpy().view(np.uint32), host(0)[1], host(0)[2], cfg, stream=st.cuda_stream)
+    p_ok = tm.count_edges_async(n, *host(1), cfg, stream=st.cuda_stream)
+    with pytest.raises(ValueError):
+        p_bad.result()
+    assert p_ok.result().tolist() == want[1]
+    # a second collection of the same ticket is rejected by the C-ABI
+    L = tm.lib()
+    assert L.tm_count_edges_wait(p_ok.ticket, None, None) != 0
