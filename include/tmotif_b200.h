@@ -27,6 +27,7 @@ extern "C" {
 
 #define TM_OK 0
 #define TM_ERR_INVALID 1     /* std::invalid_argument (graph.cpp:20,29,32)      */
+#define TM_ERR_PARSE 2       /* ParseError (types.hpp:35), CLI exit_parse        */
 #define TM_ERR_OVERFLOW 3    /* CounterOverflowError (types.hpp:50)             */
 #define TM_ERR_CONFIG 4      /* ConfigError (types.hpp:46, executor.cpp:151-156)  */
 #define TM_ERR_CONSISTENCY 5 /* ConsistencyError (types.hpp:55, motifs.cpp:254) */
@@ -149,6 +150,31 @@ int tm_count_edges_time_slice(const uint32_t* src, const uint32_t* dst, const in
 /* Degree-cost balanced center partition for rank `rank` of `world`. */
 int tm_partition_centers(const tm_graph* g, uint32_t world, uint32_t rank, uint32_t* begin,
                          uint32_t* end);
+
+/* ---- edge-list text (the reader in front of the path) -------------------
+ * parse_edge_list (graph.cpp:73-116) on the GPU: whitespace-separated
+ * "SRC DST T" lines, '#'-prefixed and blank lines skipped, CRLF accepted,
+ * fields past the third ignored, node ids = arbitrary tokens mapped to dense
+ * indices in order of first appearance among retained edges, self-loops
+ * dropped and tallied (drop_self_loops = 1) or rejected.  Errors return
+ * TM_ERR_PARSE with the reference's ParseError text ("line N: ...") in
+ * tm_last_error and N in tm_parse_error_line.  The edge arrays stay on the
+ * device in ingestion order, ready for tm_graph_build / tm_count_edges with
+ * device_ptrs = 1 (TemporalGraph::build's (t, ordinal) sort happens there). */
+typedef struct tm_edge_list tm_edge_list;
+int tm_parse_edge_list(const char* text, uint64_t bytes, int device_text, int drop_self_loops, void* stream,
+                       tm_edge_list** out);
+/* node_count, edge_count, dropped_self_loops (graph.hpp:44-54) and the size
+ * of the '\n'-joined node-id tokens in id order. */
+int tm_edge_list_info(const tm_edge_list* el, uint64_t* nodes, uint64_t* edges, uint64_t* dropped_self_loops,
+                      uint64_t* id_bytes);
+int tm_edge_list_device_arrays(const tm_edge_list* el, const uint32_t** src, const uint32_t** dst,
+                               const int64_t** t);
+/* host copies; any NULL output is skipped.  ids: id_bytes bytes, tokens in
+ * id order joined by '\n' (TemporalGraph::node_id, graph.hpp:46). */
+int tm_edge_list_copy(const tm_edge_list* el, uint32_t* src, uint32_t* dst, int64_t* t, char* ids);
+uint64_t tm_parse_error_line(void);
+void tm_edge_list_free(tm_edge_list* el);
 
 /* ---- taxonomy (host only) ----------------------------------------------- */
 /* merge_census (motifs.cpp:233-281). */

@@ -218,6 +218,8 @@ class Reference:
                                    C.POINTER(C.c_double)]
         L.ref_generate_random_graph.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_uint64,
                                                 C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_parse_edge_list.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p, C.c_char_p]
         self.L = L
 
     def build_graph(self, n, src, dst, t):
@@ -291,3 +293,22 @@ class Reference:
                                             t.ctypes.data):
             raise ValueError("bad generator parameters")
         return src, dst, t
+
+    def parse_edge_list(self, text: bytes, drop_self_loops: bool = True):
+        """The reference's parse_edge_list: (node_ids, src, dst, t, dropped)
+        in ingestion order, or raises ValueError((line, message))."""
+        lines = text.count(b"\n") + 1
+        counts = np.zeros(3, np.uint64)
+        src = np.zeros(lines, np.uint32); dst = np.zeros(lines, np.uint32); t = np.zeros(lines, np.int64)
+        ids = C.create_string_buffer(len(text) + 1)
+        ids_len = np.zeros(1, np.uint64)
+        err_line = np.zeros(1, np.uint64)
+        err = C.create_string_buffer(512)
+        rc = self.L.ref_parse_edge_list(text, len(text), int(drop_self_loops), counts.ctypes.data,
+                                        src.ctypes.data, dst.ctypes.data, t.ctypes.data, ids,
+                                        ids_len.ctypes.data, err_line.ctypes.data, err)
+        if rc:
+            raise ValueError((int(err_line[0]), err.value.decode("utf-8", "surrogateescape")))
+        n, m, dropped = (int(x) for x in counts)
+        names = ids.raw[:int(ids_len[0])].decode("utf-8", "surrogateescape").split("\n") if n else []
+        return names, src[:m], dst[:m], t[:m], dropped

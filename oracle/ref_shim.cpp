@@ -8,6 +8,7 @@
 // reference's own std::thread HARE path as bench.py's CPU baseline / reference
 // arm.  Nothing here is on the product path.
 #include <chrono>
+#include <sstream>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -58,6 +59,43 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
 }  // namespace
 
 extern "C" {
+
+// parse_edge_list (graph.cpp:73) over a text buffer.  Edges are returned in
+// ingestion order (edge i at index ordinal); ids joined by '\n'.  Outputs:
+// counts[0..3) = n, m, dropped; the arrays must hold one entry per line and
+// `ids` len + 1 bytes.  Returns 0, or 2 with err_line / err_msg (<= 511
+// chars) for a ParseError.
+int ref_parse_edge_list(const char* text, uint64_t len, int drop_self_loops, uint64_t* counts,
+                        uint32_t* src, uint32_t* dst, int64_t* t, char* ids, uint64_t* ids_len,
+                        uint64_t* err_line, char* err_msg) {
+    try {
+        std::istringstream in(std::string(text, len));
+        ParseOptions opt;
+        opt.drop_self_loops = drop_self_loops != 0;
+        TemporalGraph g = parse_edge_list(in, opt);
+        counts[0] = g.node_count();
+        counts[1] = g.edge_count();
+        counts[2] = g.dropped_self_loops();
+        for (const TemporalEdge& e : g.edges()) {
+            src[e.ordinal] = e.src;
+            dst[e.ordinal] = e.dst;
+            t[e.ordinal] = e.t;
+        }
+        std::string joined;
+        for (std::size_t u = 0; u < g.node_count(); ++u) {
+            if (u) joined += '\n';
+            joined += g.node_id(static_cast<NodeId>(u));
+        }
+        std::memcpy(ids, joined.data(), joined.size());
+        *ids_len = joined.size();
+        return 0;
+    } catch (const ParseError& e) {
+        *err_line = e.line();
+        std::strncpy(err_msg, e.what(), 511);
+        err_msg[511] = 0;
+        return 2;
+    }
+}
 
 struct ref_ctx {
     GraphContext ctx;

@@ -21,6 +21,11 @@ struct tm_graph {
     tmb::DeviceGraph g;
     std::vector<uint32_t> h_off;  // lazily mirrored CSR offsets
 };
+struct tm_edge_list {
+    tmb::ParsedEdges P;
+    uint64_t id_bytes = 0;
+    bool own_stream = false;
+};
 
 namespace tmb {
 
@@ -746,6 +751,23 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
     return TM_OK;
 }
 
+// node-id tokens joined by '\n' in id order
+struct IdLenLoad {
+    const uint32_t* len;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return (uint64_t)len[i] + 1; }
+};
+__global__ void gather_ids_kernel(const unsigned char* __restrict__ text, const uint64_t* __restrict__ off,
+                                  const uint32_t* __restrict__ len, const uint64_t* __restrict__ pos, uint64_t n,
+                                  char* __restrict__ out) {
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+         u += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = pos[u];
+        for (uint32_t k = 0; k < len[u]; ++k) out[p + k] = (char)text[off[u] + k];
+        if (u + 1 < n) out[p + len[u]] = '\n';
+    }
+}
+thread_local uint64_t g_parse_line = 0;
+
 // Finish a speculative replay: wait, check the verdict against the replayed
 // variant and t range, unpack.  Returns false when the data did not match the
 // graph (the caller re-runs the checked path on the same device arrays).
@@ -1112,6 +1134,113 @@ int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, u
         if (timings) timings->index_ms = index_ms;
         return rc;
     });
+}
+
+int tm_parse_edge_list(const char* text, uint64_t bytes, int device_text, int drop_self_loops, void* stream,
+                       tm_edge_list** out) {
+    return guarded([&] {
+        if (!out || (bytes && !text)) throw tm_error(TM_ERR_INVALID, "null argument");
+        ensure_device();
+        auto* el = new tm_edge_list();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (!s) {
+            TM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            el->own_stream = true;
+        }
+        el->P.stream = s;
+        try {
+            // a private copy of the text: the node-id tokens point into it
+            unsigned char* d_text = dalloc<unsigned char>(bytes + 16, s);
+            if (bytes)
+                TM_CUDA(cudaMemcpyAsync(d_text, text, bytes,
+                                        device_text ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+            try {
+                el->P = parse_edge_list_device(d_text, bytes, drop_self_loops != 0, s);
+            } catch (...) {
+                dfree(d_text, s);
+                throw;
+            }
+            el->P.text = d_text;
+            el->P.bytes = bytes;
+            el->P.stream = s;
+            if (el->P.n) {  // sum of token lengths + separators
+                uint64_t ib = 0;
+                uint64_t* pos = dalloc<uint64_t>(el->P.n + 1, s);
+                exclusive_scan<uint64_t>(IdLenLoad{el->P.node_len}, el->P.n, pos, s);
+                TM_CUDA(cudaMemcpyAsync(&ib, pos + el->P.n, 8, cudaMemcpyDeviceToHost, s));
+                dfree(pos, s);
+                TM_CUDA(cudaStreamSynchronize(s));
+                el->id_bytes = ib - 1;
+            }
+        } catch (const parse_error& e) {
+            g_parse_line = e.line;
+            cudaStreamSynchronize(s);
+            if (el->own_stream) cudaStreamDestroy(s);
+            delete el;
+            throw;
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            if (el->own_stream) cudaStreamDestroy(s);
+            delete el;
+            throw;
+        }
+        *out = el;
+        return TM_OK;
+    });
+}
+
+int tm_edge_list_info(const tm_edge_list* el, uint64_t* nodes, uint64_t* edges, uint64_t* dropped,
+                      uint64_t* id_bytes) {
+    if (!el) return TM_ERR_INVALID;
+    if (nodes) *nodes = el->P.n;
+    if (edges) *edges = el->P.m;
+    if (dropped) *dropped = el->P.dropped;
+    if (id_bytes) *id_bytes = el->id_bytes;
+    return TM_OK;
+}
+
+int tm_edge_list_device_arrays(const tm_edge_list* el, const uint32_t** src, const uint32_t** dst,
+                               const int64_t** t) {
+    if (!el) return TM_ERR_INVALID;
+    if (src) *src = el->P.src;
+    if (dst) *dst = el->P.dst;
+    if (t) *t = el->P.t;
+    return TM_OK;
+}
+
+int tm_edge_list_copy(const tm_edge_list* el, uint32_t* src, uint32_t* dst, int64_t* t, char* ids) {
+    return guarded([&] {
+        if (!el) throw tm_error(TM_ERR_INVALID, "null edge list");
+        const ParsedEdges& P = el->P;
+        cudaStream_t s = P.stream;
+        if (src && P.m) TM_CUDA(cudaMemcpyAsync(src, P.src, P.m * 4, cudaMemcpyDeviceToHost, s));
+        if (dst && P.m) TM_CUDA(cudaMemcpyAsync(dst, P.dst, P.m * 4, cudaMemcpyDeviceToHost, s));
+        if (t && P.m) TM_CUDA(cudaMemcpyAsync(t, P.t, P.m * 8, cudaMemcpyDeviceToHost, s));
+        if (ids && P.n) {
+            uint64_t* pos = dalloc<uint64_t>(P.n + 1, s);
+            exclusive_scan<uint64_t>(IdLenLoad{P.node_len}, P.n, pos, s);
+            char* d_ids = dalloc<char>(el->id_bytes + 1, s);
+            const unsigned g = (unsigned)std::min<uint64_t>((P.n + 255) / 256, (uint64_t)sm_count() * 8);
+            TM_LAUNCH("parse_gather_ids", s, gather_ids_kernel, g, 256, 0, P.text, P.node_off, P.node_len, pos, P.n,
+                      d_ids);
+            TM_CUDA(cudaMemcpyAsync(ids, d_ids, el->id_bytes, cudaMemcpyDeviceToHost, s));
+            dfree(d_ids, s);
+            dfree(pos, s);
+        }
+        TM_CUDA(cudaStreamSynchronize(s));
+        return TM_OK;
+    });
+}
+
+uint64_t tm_parse_error_line(void) { return g_parse_line; }
+
+void tm_edge_list_free(tm_edge_list* el) {
+    if (!el) return;
+    cudaStream_t s = el->P.stream;
+    free_parsed(el->P);
+    cudaStreamSynchronize(s);
+    if (el->own_stream) cudaStreamDestroy(s);
+    delete el;
 }
 
 int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,

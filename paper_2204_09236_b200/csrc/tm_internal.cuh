@@ -45,6 +45,28 @@ struct tm_error : std::runtime_error {
     tm_error(int c, const std::string& w) : std::runtime_error(w), code(c) {}
 };
 
+// ParseError (types.hpp:35): code 2 = the reference CLI's exit_parse
+struct parse_error : tm_error {
+    uint64_t line;
+    parse_error(uint64_t l, const std::string& w) : tm_error(2, w), line(l) {}
+};
+
+// parse_edge_list on the GPU (tm_parse.cu): ingestion-order edges + node-id
+// tokens (offsets into the device text) in id order
+struct ParsedEdges {
+    cudaStream_t stream = nullptr;
+    uint64_t n = 0, m = 0, dropped = 0, bytes = 0;
+    unsigned char* text = nullptr;  // device copy of the text (owned)
+    uint32_t* src = nullptr;
+    uint32_t* dst = nullptr;
+    int64_t* t = nullptr;
+    uint64_t* node_off = nullptr;
+    uint32_t* node_len = nullptr;
+};
+ParsedEdges parse_edge_list_device(const unsigned char* d_text, uint64_t bytes, bool drop_self_loops,
+                                   cudaStream_t s);
+void free_parsed(ParsedEdges& P);
+
 void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 #define TM_CUDA(x) ::tmb::check_cuda((x), #x, __FILE__, __LINE__)
 

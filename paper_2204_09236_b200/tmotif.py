@@ -26,6 +26,7 @@ LIB_PATH = os.environ.get("TM_LIB") or os.path.join(HERE, "libtmotif_b200.so")
 
 TM_OK = 0
 TM_ERR_INVALID = 1
+TM_ERR_PARSE = 2
 TM_ERR_OVERFLOW = 3
 TM_ERR_CONFIG = 4
 TM_ERR_CONSISTENCY = 5
@@ -66,6 +67,10 @@ def _raise(rc: int, lib) -> None:
     msg = lib.tm_last_error().decode() if lib is not None else ""
     if rc == TM_ERR_INVALID:
         raise ValueError(msg)
+    if rc == TM_ERR_PARSE:
+        line = int(lib.tm_parse_error_line())
+        prefix = f"line {line}: "
+        raise ParseError(line, msg[len(prefix):] if msg.startswith(prefix) else msg)
     if rc == TM_ERR_OVERFLOW:
         raise CounterOverflowError(msg or "motif counter overflow")
     if rc == TM_ERR_CONFIG:
@@ -127,6 +132,13 @@ def lib():
                                   C.POINTER(_Timings)]
     L.tm_count_edges.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint64, C.c_int, VP,
                                  C.POINTER(_RunConfig), C.POINTER(_Counters), VP, C.POINTER(_Timings)]
+    L.tm_parse_edge_list.argtypes = [VP, C.c_uint64, C.c_int, C.c_int, VP, C.POINTER(VP)]
+    L.tm_edge_list_info.argtypes = [VP, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                    C.POINTER(C.c_uint64)]
+    L.tm_edge_list_device_arrays.argtypes = [VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)]
+    L.tm_edge_list_copy.argtypes = [VP, VP, VP, VP, VP]
+    L.tm_parse_error_line.restype = C.c_uint64
+    L.tm_edge_list_free.argtypes = [VP]
     L.tm_count_edges_async.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint64, VP, C.POINTER(_RunConfig),
                                        C.POINTER(C.c_uint64)]
     L.tm_count_edges_wait.argtypes = [C.c_uint64, C.POINTER(_Counters), VP]
@@ -484,7 +496,9 @@ def parse_edge_list(text: str, drop_self_loops: bool = True) -> TemporalGraph:
             raise ParseError(line_no, "expected 3 tokens: SRC DST T")
         tok = f[2]
         try:
-            if not tok.lstrip("-").isdigit() or tok.startswith("+"):
+            # std::from_chars<int64_t>: optional '-', ASCII digits, whole field
+            body = tok[1:] if tok.startswith("-") else tok
+            if not body or any(c not in "0123456789" for c in body):
                 raise ValueError
             tv = int(tok)
             if not -(2 ** 63) <= tv < 2 ** 63:
@@ -503,6 +517,59 @@ def parse_edge_list(text: str, drop_self_loops: bool = True) -> TemporalGraph:
         ts.append(tv)
     return TemporalGraph(node_ids, np.array(src, np.uint32), np.array(dst, np.uint32),
                          np.array(ts, np.int64), dropped)
+
+
+class EdgeList:
+    """A parsed edge list resident on the GPU (tm_parse_edge_list): the
+    reference's parse_edge_list output -- ingestion-order edges, dense node
+    ids by first appearance, dropped self-loop tally -- with the edge arrays
+    left in device memory for GraphContext.build_device / count_edges_device."""
+
+    def __init__(self, handle, lib_):
+        self._h = handle
+        self._L = lib_
+        n, m, dr, ib = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _raise(lib_.tm_edge_list_info(handle, C.byref(n), C.byref(m), C.byref(dr), C.byref(ib)), lib_)
+        self.n, self.m, self.dropped_self_loops, self._id_bytes = n.value, m.value, dr.value, ib.value
+
+    def device_arrays(self) -> Tuple[int, int, int]:
+        s, d, t = VP(), VP(), VP()
+        _raise(self._L.tm_edge_list_device_arrays(self._h, C.byref(s), C.byref(d), C.byref(t)), self._L)
+        return s.value or 0, d.value or 0, t.value or 0
+
+    def to_graph(self) -> TemporalGraph:
+        src = np.zeros(self.m, np.uint32)
+        dst = np.zeros(self.m, np.uint32)
+        t = np.zeros(self.m, np.int64)
+        ids = C.create_string_buffer(self._id_bytes + 1)
+        _raise(self._L.tm_edge_list_copy(self._h, src.ctypes.data, dst.ctypes.data, t.ctypes.data, ids), self._L)
+        names = ids.raw[:self._id_bytes].decode("utf-8", "surrogateescape").split("\n") if self.n else []
+        return TemporalGraph(names, src, dst, t, self.dropped_self_loops)
+
+    def close(self):
+        if self._h:
+            self._L.tm_edge_list_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def parse_edge_list_gpu(text, drop_self_loops: bool = True, stream: Optional[int] = None) -> EdgeList:
+    """parse_edge_list (graph.cpp:73-116) on the GPU; `text` is str or bytes
+    (host), or (device_pointer, nbytes).  Raises ParseError like the reference."""
+    L = lib()
+    h = VP()
+    if isinstance(text, tuple):
+        ptr, nbytes = text
+        _raise(L.tm_parse_edge_list(ptr, nbytes, 1, int(drop_self_loops), stream, C.byref(h)), L)
+    else:
+        buf = text.encode("utf-8", "surrogateescape") if isinstance(text, str) else bytes(text)
+        _raise(L.tm_parse_edge_list(buf, len(buf), 0, int(drop_self_loops), stream, C.byref(h)), L)
+    return EdgeList(h, L)
 
 
 def load_edge_list(path: str, drop_self_loops: bool = True) -> TemporalGraph:

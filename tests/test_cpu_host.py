@@ -177,3 +177,30 @@ def test_partition_bounds_host_logic():
         assert b[0][0] == 0 and b[-1][1] == 10 and len(b) == world
         for (x, y), (x2, _) in zip(b, b[1:]):
             assert y == x2 and x <= y
+
+
+def test_parse_mirror_matches_reference_parser(tm):
+    """The host mirror of parse_edge_list against the reference's own parser
+    (oracle/_ref) on seeded fuzz texts, valid and with one planted error."""
+    from oracle import Reference
+    if not Reference.available():
+        pytest.skip("reference build absent")
+    from edgelist_fuzz import fuzz_text
+    R = Reference()
+    for seed in range(12):
+        for err in ("", "short", "time", "loop"):
+            text = fuzz_text(seed, 200, err)
+            for drop in (True, False):
+                try:
+                    want = R.parse_edge_list(text.encode(), drop)
+                except ValueError as e:
+                    line, msg = e.args[0]
+                    with pytest.raises(tm.ParseError) as got:
+                        tm.parse_edge_list(text, drop)
+                    assert got.value.line == line and str(got.value) == msg
+                    continue
+                g = tm.parse_edge_list(text, drop)
+                names, s, d, t, dropped = want
+                assert g.node_ids == names
+                assert (g.src == s).all() and (g.dst == d).all() and (g.t == t).all()
+                assert g.dropped_self_loops() == dropped
