@@ -167,6 +167,7 @@ def main():
     ap.add_argument("--config", default="powerlaw_1m_10m")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-reader", action="store_true", help="skip the edge-list reader measurement")
     ap.add_argument("--cpu-sample-edges", type=int, default=1_000_000)
     ap.add_argument("--delta", type=int, default=None, help="override the config's delta")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -389,6 +390,50 @@ def main():
         if k in abytes:
             v["algo_GBps"] = abytes[k] / (v["ms_per_step"] * 1e-3) / 1e9
 
+    # the edge-list reader in front of the path (N = 1): the same edges as
+    # "SRC DST T" text, parsed on the GPU from device memory and from host
+    # memory; the parsed arrays are counted once and must give the same census
+    reader = None
+    if world == 1 and not args.no_reader:
+        nbytes = tm.write_edge_list_device(m_local, d_src.data_ptr(), d_dst.data_ptr(), d_t.data_ptr(), stream=sptr)
+        d_text = torch.empty(nbytes + 16, dtype=torch.uint8, device=dev)
+        tm.write_edge_list_device(m_local, d_src.data_ptr(), d_dst.data_ptr(), d_t.data_ptr(), d_text.data_ptr(),
+                                  stream=sptr)
+        h_text = d_text[:nbytes].cpu().pin_memory()
+        torch.cuda.synchronize()
+        el = tm.parse_edge_list_gpu((d_text.data_ptr(), nbytes), stream=sptr)
+        assert el.m == m_local
+        ps, pd, pt = el.device_arrays()
+        census_txt = tm.count_edges_device(el.n, el.m, ps, pd, pt, cfg, stream=sptr)
+        assert (census_txt == census).all(), "census of the parsed text differs"
+        el.close()
+
+        def time_parse(src_arg, reps=5):
+            for _ in range(2):
+                tm.parse_edge_list_gpu(src_arg, stream=sptr).close()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+            for _ in range(reps):
+                tm.parse_edge_list_gpu(src_arg, stream=sptr).close()
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / reps
+
+        ms_dev = time_parse((d_text.data_ptr(), nbytes))
+        ms_host = time_parse((h_text.data_ptr(), nbytes, False))
+        reader = {"what": "tm_parse_edge_list: the reference's parse_edge_list (graph.cpp:73) on the GPU",
+                  "text_bytes": int(nbytes), "lines": int(m_local),
+                  "device_text": {"ms": ms_dev, "GB_per_s": nbytes / (ms_dev * 1e-3) / 1e9,
+                                  "lines_per_s": m_local / (ms_dev * 1e-3)},
+                  "host_text": {"ms": ms_host, "GB_per_s": nbytes / (ms_host * 1e-3) / 1e9,
+                                "lines_per_s": m_local / (ms_host * 1e-3),
+                                "note": "pinned host text, host->device copy inside the timed call"}}
+        del d_text
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -406,6 +451,22 @@ def main():
                                  f"build + run_parallel, {threads} std::threads)"}
         except Exception as ex:  # pragma: no cover
             log("cpu baseline failed:", ex)
+        if reader is not None:
+            try:  # the reference's own reader on a prefix of the same text
+                from oracle import Reference
+                if Reference.available():
+                    k = min(args.cpu_sample_edges, m)
+                    arr = h_text.numpy()[:nbytes]
+                    cut = int(np.flatnonzero(arr == 10)[k - 1]) + 1
+                    sample = bytes(arr[:cut])
+                    t0 = time.perf_counter()
+                    Reference().parse_edge_list(sample)
+                    sec = time.perf_counter() - t0
+                    reader["cpu_reference"] = {"lines_per_s": k / sec, "GB_per_s": len(sample) / sec / 1e9,
+                                               "cores": 1, "kind": "reference",
+                                               "sample": f"first {k} lines (parse_edge_list incl. TemporalGraph::build)"}
+            except Exception as ex:  # pragma: no cover
+                log("reader cpu baseline failed:", ex)
 
     value = m / (ms_step * 1e-3)
     line = {
@@ -430,6 +491,7 @@ def main():
         "kernels": ktimes,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
+        "reader": reader,
     }
     print(json.dumps(line), flush=True)
     if dist:

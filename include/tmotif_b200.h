@@ -174,6 +174,13 @@ int tm_edge_list_device_arrays(const tm_edge_list* el, const uint32_t** src, con
  * id order joined by '\n' (TemporalGraph::node_id, graph.hpp:46). */
 int tm_edge_list_copy(const tm_edge_list* el, uint32_t* src, uint32_t* dst, int64_t* t, char* ids);
 uint64_t tm_parse_error_line(void);
+/* write_edge_list (graph.cpp:170-175) for graphs whose node ids are their
+ * decimal indices (generate_random_graph's naming): "SRC DST T\n" per edge
+ * in the order given (the reference writes graph.edges(), i.e. (t, ordinal)
+ * order: pass time-ordered edges for byte-identical output).  With out == NULL only *bytes is set; otherwise out
+ * (host, or device when device_out) receives *bytes bytes. */
+int tm_write_edge_list(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m, int device_ptrs,
+                       void* stream, char* out, int device_out, uint64_t* bytes);
 void tm_edge_list_free(tm_edge_list* el);
 
 /* ---- taxonomy (host only) ----------------------------------------------- */

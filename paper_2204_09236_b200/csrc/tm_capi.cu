@@ -1234,6 +1234,51 @@ int tm_edge_list_copy(const tm_edge_list* el, uint32_t* src, uint32_t* dst, int6
 
 uint64_t tm_parse_error_line(void) { return g_parse_line; }
 
+int tm_write_edge_list(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m, int device_ptrs,
+                       void* stream, char* out, int device_out, uint64_t* bytes) {
+    return guarded([&] {
+        if (!bytes || (m && (!src || !dst || !t))) throw tm_error(TM_ERR_INVALID, "null argument");
+        ensure_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        bool own = false;
+        if (!s) {
+            TM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            own = true;
+        }
+        const uint32_t *ds = src, *dd = dst;
+        const int64_t* dt = t;
+        uint32_t *hs = nullptr, *hd = nullptr;
+        int64_t* ht = nullptr;
+        if (!device_ptrs && m) {
+            hs = dalloc<uint32_t>(m, s);
+            hd = dalloc<uint32_t>(m, s);
+            ht = dalloc<int64_t>(m, s);
+            TM_CUDA(cudaMemcpyAsync(hs, src, m * 4, cudaMemcpyHostToDevice, s));
+            TM_CUDA(cudaMemcpyAsync(hd, dst, m * 4, cudaMemcpyHostToDevice, s));
+            TM_CUDA(cudaMemcpyAsync(ht, t, m * 8, cudaMemcpyHostToDevice, s));
+            ds = hs;
+            dd = hd;
+            dt = ht;
+        }
+        const uint64_t nb = edge_list_text_bytes(ds, dd, dt, m, s);
+        *bytes = nb;
+        if (out && nb) {
+            char* d_out = device_out ? out : dalloc<char>(nb, s);
+            write_edge_list_device(ds, dd, dt, m, d_out, s);
+            if (!device_out) {
+                TM_CUDA(cudaMemcpyAsync(out, d_out, nb, cudaMemcpyDeviceToHost, s));
+                dfree(d_out, s);
+            }
+        }
+        dfree(hs, s);
+        dfree(hd, s);
+        dfree(ht, s);
+        TM_CUDA(cudaStreamSynchronize(s));
+        if (own) cudaStreamDestroy(s);
+        return TM_OK;
+    });
+}
+
 void tm_edge_list_free(tm_edge_list* el) {
     if (!el) return;
     cudaStream_t s = el->P.stream;

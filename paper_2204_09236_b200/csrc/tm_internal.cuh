@@ -66,6 +66,11 @@ struct ParsedEdges {
 ParsedEdges parse_edge_list_device(const unsigned char* d_text, uint64_t bytes, bool drop_self_loops,
                                    cudaStream_t s);
 void free_parsed(ParsedEdges& P);
+// write_edge_list with decimal node ids: "SRC DST T\n" per edge
+uint64_t edge_list_text_bytes(const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t, uint64_t m,
+                              cudaStream_t s);
+void write_edge_list_device(const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t, uint64_t m,
+                            char* d_out, cudaStream_t s);
 
 void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 #define TM_CUDA(x) ::tmb::check_cuda((x), #x, __FILE__, __LINE__)

@@ -19,12 +19,14 @@
 //   1. newline bitmask (one 32-byte word per thread) + word-popcount scan ->
 //      line starts;
 //   2. one thread per line over a shared-memory stage of the block's 256
-//      lines: field bounds, timestamp, 64-bit token hashes, line kind; the
-//      first error line by atomicMin;
+//      lines: field bounds, timestamp, token keys (the bytes themselves for
+//      tokens of <= 7 bytes, else a 64-bit hash), line kind; the first error
+//      line by atomicMin;
 //   3. scan of the edge lines -> ingestion index e; occurrences 2e / 2e+1;
-//   4. interning: open-addressing table keyed by (hash tag, representative
-//      occurrence) with byte compares on tag hits; atomicMin of the
-//      occurrence index per slot = the token's first appearance;
+//   4. interning: open-addressing table of exact short keys and (hash tag,
+//      representative occurrence) long keys with byte compares on tag hits,
+//      sized for the expected distinct count and regrown when half full;
+//      atomicMin of the occurrence index per slot = first appearance;
 //   5. ids = rank of each first appearance (scan of "is first" flags).
 #include "tm_primitives.cuh"
 
@@ -95,8 +97,8 @@ struct LineOut {
     uint32_t* s_len;
     uint32_t* d_len;
     uint32_t* t_len;
-    uint64_t* s_hash;
-    uint64_t* d_hash;
+    uint64_t* s_key;  // token key: exact bytes | len << 56 (<= 7 bytes) or a 64-bit hash
+    uint64_t* d_key;
     int64_t* tv;
 };
 
@@ -147,12 +149,15 @@ __global__ void __launch_bounds__(kLineBlock) parse_lines_kernel(const unsigned 
                 fo[nf] = i;
                 const uint64_t s0 = i;
                 if (nf < 2) {
-                    uint64_t h = fh[nf];
+                    uint64_t h = fh[nf], pk = 0;
                     while (i < end && !is_space(at(i))) {
-                        h = (h ^ at(i)) * 0x100000001b3ull;  // FNV-1a
+                        const unsigned char c = at(i);
+                        h = (h ^ c) * 0x100000001b3ull;  // FNV-1a
+                        if (i - s0 < 7) pk |= (uint64_t)c << (8 * (i - s0));
                         ++i;
                     }
-                    fh[nf] = mix64(h ^ (i - s0));
+                    // token key: exact (bytes | len << 56) up to 7 bytes, else a hash
+                    fh[nf] = i - s0 <= 7 ? (pk | ((uint64_t)(i - s0) << 56)) : mix64(h ^ (i - s0));
                 } else {
                     // std::from_chars<int64_t> over the whole field
                     neg = at(i) == '-';
@@ -196,8 +201,8 @@ __global__ void __launch_bounds__(kLineBlock) parse_lines_kernel(const unsigned 
                 out.d_off[l] = fo[1];
                 out.s_len[l] = fl[0];
                 out.d_len[l] = fl[1];
-                out.s_hash[l] = fh[0];
-                out.d_hash[l] = fh[1];
+                out.s_key[l] = fh[0];
+                out.d_key[l] = fh[1];
                 out.tv[l] = neg ? (int64_t)(0 - tval) : (int64_t)tval;
             } else if (kind >= kErrShort) {
                 out.s_off[l] = fo[0];
@@ -220,54 +225,63 @@ struct EdgeFlagLoad {
     __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return kind[i] == kEdge ? 1u : 0u; }
 };
 
-// edge lines -> ingestion-order timestamps and the 2m token occurrences
-__global__ void emit_edges_kernel(LineOut in, const uint64_t* __restrict__ eidx, uint64_t L,
-                                  int64_t* __restrict__ t, uint64_t* __restrict__ occ_off,
-                                  uint32_t* __restrict__ occ_len, uint64_t* __restrict__ occ_hash) {
-    for (uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; l < L;
-         l += (uint64_t)gridDim.x * blockDim.x) {
-        if (in.kind[l] != kEdge) continue;
-        const uint64_t e = eidx[l];
-        t[e] = in.tv[l];
-        occ_off[2 * e] = in.s_off[l];
-        occ_len[2 * e] = in.s_len[l];
-        occ_hash[2 * e] = in.s_hash[l];
-        occ_off[2 * e + 1] = in.d_off[l];
-        occ_len[2 * e + 1] = in.d_len[l];
-        occ_hash[2 * e + 1] = in.d_hash[l];
-    }
-}
-
 constexpr unsigned long long kEmpty = ~0ull;
 
-__device__ __forceinline__ bool same_token(const unsigned char* __restrict__ text, const uint64_t* occ_off,
-                                           const uint32_t* occ_len, uint32_t a, uint32_t b) {
-    const uint32_t n = occ_len[a];
-    if (occ_len[b] != n) return false;
-    const unsigned char* p = text + occ_off[a];
-    const unsigned char* q = text + occ_off[b];
+// occurrence o = 2 * line + side (side 0: SRC, 1: DST) of an edge line
+__device__ __forceinline__ uint64_t occ_off(const LineOut& in, uint64_t o) {
+    return (o & 1) ? in.d_off[o >> 1] : in.s_off[o >> 1];
+}
+__device__ __forceinline__ uint32_t occ_len(const LineOut& in, uint64_t o) {
+    return (o & 1) ? in.d_len[o >> 1] : in.s_len[o >> 1];
+}
+__device__ __forceinline__ bool same_token(const unsigned char* __restrict__ text, const LineOut& in, uint32_t a,
+                                           uint32_t b) {
+    const uint32_t n = occ_len(in, a);
+    if (occ_len(in, b) != n) return false;
+    const unsigned char* p = text + occ_off(in, a);
+    const unsigned char* q = text + occ_off(in, b);
     for (uint32_t k = 0; k < n; ++k)
         if (p[k] != q[k]) return false;
     return true;
 }
 
-// slot key: hash tag (high 32 bits) | representative occurrence (low 32)
-__global__ void intern_kernel(const unsigned char* __restrict__ text, const uint64_t* __restrict__ occ_off,
-                              const uint32_t* __restrict__ occ_len, const uint64_t* __restrict__ occ_hash,
-                              uint64_t occs, unsigned long long* __restrict__ table, uint64_t mask,
-                              uint32_t* __restrict__ first, uint32_t* __restrict__ occ_slot) {
+constexpr uint32_t kNoSlot = 0xffffffffu;
+
+// Table entries: tokens of <= 7 bytes by their exact key (top byte = length
+// <= 7: no text access at all); longer ones as 0x80 << 56 | 24-bit hash tag
+// << 32 | representative occurrence, confirmed by a byte compare on a tag
+// hit.  Sized for the expected distinct count (L2-resident when it is small);
+// a probe run longer than kMaxProbe means the table is too full: the thread
+// flags it and stops, and the host retries with a 4x larger table.
+__global__ void intern_kernel(const unsigned char* __restrict__ text, LineOut in, uint64_t occs,
+                              unsigned long long* __restrict__ table, uint64_t mask,
+                              uint32_t* __restrict__ first, uint32_t* __restrict__ occ_slot,
+                              uint32_t* __restrict__ overflow, int bounded) {
+    constexpr uint32_t kMaxProbe = 512;
     for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < occs;
          o += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t h = occ_hash[o];
-        const unsigned long long key = (h & 0xffffffff00000000ull) | o;
+        if (in.kind[o >> 1] != kEdge) {
+            occ_slot[o] = kNoSlot;
+            continue;
+        }
+        const uint64_t k = (o & 1) ? in.d_key[o >> 1] : in.s_key[o >> 1];
+        const bool exact = occ_len(in, o) <= 7;
+        const uint64_t h = exact ? mix64(k) : k;
+        const unsigned long long key = exact ? k : (0x80ull << 56) | ((h >> 40) << 32) | o;
         uint64_t slot = h & mask;
-        for (;;) {
+        for (uint32_t probe = 0;; ++probe) {
+            if (bounded && probe > kMaxProbe) {
+                atomicExch(overflow, 1u);
+                return;
+            }
             unsigned long long cur = table[slot];
             if (cur == kEmpty) {
                 cur = atomicCAS(&table[slot], kEmpty, key);
-                if (cur == kEmpty) break;  // inserted: this occurrence represents the token
+                if (cur == kEmpty) break;
             }
-            if ((cur >> 32) == (key >> 32) && same_token(text, occ_off, occ_len, (uint32_t)cur, (uint32_t)o))
+            if (exact ? cur == key
+                      : ((cur >> 32) == (key >> 32) &&
+                         same_token(text, in, (uint32_t)cur, (uint32_t)o)))
                 break;
             slot = (slot + 1) & mask;
         }
@@ -280,25 +294,78 @@ struct FirstFlagLoad {
     const uint32_t* occ_slot;
     const uint32_t* first;
     __device__ __forceinline__ uint32_t operator()(uint64_t o) const {
-        return first[occ_slot[o]] == (uint32_t)o ? 1u : 0u;
+        const uint32_t sl = occ_slot[o];
+        return sl != kNoSlot && first[sl] == (uint32_t)o ? 1u : 0u;
     }
 };
 
-// ids: the rank of the token's first appearance; node tokens in id order
-__global__ void assign_ids_kernel(const uint32_t* __restrict__ occ_slot, const uint32_t* __restrict__ first,
-                                  const uint32_t* __restrict__ rank, const uint64_t* __restrict__ occ_off,
-                                  const uint32_t* __restrict__ occ_len, uint64_t m, uint32_t* __restrict__ src,
-                                  uint32_t* __restrict__ dst, uint64_t* __restrict__ node_off,
-                                  uint32_t* __restrict__ node_len) {
-    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < 2 * m;
+// ids: the rank of the token's first appearance; edges to their ingestion
+// index; node tokens in id order
+__global__ void assign_ids_kernel(LineOut in, const uint64_t* __restrict__ eidx,
+                                  const uint32_t* __restrict__ occ_slot, const uint32_t* __restrict__ first,
+                                  const uint32_t* __restrict__ rank, uint64_t occs, uint32_t* __restrict__ src,
+                                  uint32_t* __restrict__ dst, int64_t* __restrict__ t,
+                                  uint64_t* __restrict__ node_off, uint32_t* __restrict__ node_len) {
+    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < occs;
          o += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t f = first[occ_slot[o]];
+        const uint32_t sl = occ_slot[o];
+        if (sl == kNoSlot) continue;
+        const uint32_t f = first[sl];
         const uint32_t id = rank[f];
-        if (o & 1) dst[o >> 1] = id; else src[o >> 1] = id;
-        if (f == (uint32_t)o) {
-            node_off[id] = occ_off[o];
-            node_len[id] = occ_len[o];
+        const uint64_t e = eidx[o >> 1];
+        if (o & 1) {
+            dst[e] = id;
+        } else {
+            src[e] = id;
+            t[e] = in.tv[o >> 1];
         }
+        if (f == (uint32_t)o) {
+            node_off[id] = occ_off(in, o);
+            node_len[id] = occ_len(in, o);
+        }
+    }
+}
+
+// ---- write_edge_list (graph.cpp:170-175) for decimal node ids ------------
+__device__ __forceinline__ uint32_t dec_digits(uint64_t v) {
+    uint32_t d = 1;
+    while (v >= 10) {
+        v /= 10;
+        ++d;
+    }
+    return d;
+}
+__device__ __forceinline__ uint64_t abs_t(int64_t t) { return t < 0 ? 0ull - (uint64_t)t : (uint64_t)t; }
+__device__ __forceinline__ uint32_t line_bytes(uint32_t a, uint32_t b, int64_t t) {
+    return dec_digits(a) + 1 + dec_digits(b) + 1 + (t < 0 ? 1 : 0) + dec_digits(abs_t(t)) + 1;
+}
+struct LineLenLoad {
+    const uint32_t* src;
+    const uint32_t* dst;
+    const int64_t* t;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return line_bytes(src[i], dst[i], t[i]); }
+};
+__device__ __forceinline__ char* put_dec(char* p, uint64_t v, uint32_t nd) {
+    for (uint32_t k = nd; k > 0; --k) {
+        p[k - 1] = (char)('0' + v % 10);
+        v /= 10;
+    }
+    return p + nd;
+}
+__global__ void write_lines_kernel(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                                   const int64_t* __restrict__ t, const uint64_t* __restrict__ pos, uint64_t m,
+                                   char* __restrict__ out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        char* p = out + pos[i];
+        p = put_dec(p, src[i], dec_digits(src[i]));
+        *p++ = ' ';
+        p = put_dec(p, dst[i], dec_digits(dst[i]));
+        *p++ = ' ';
+        if (t[i] < 0) *p++ = '-';
+        const uint64_t a = abs_t(t[i]);
+        p = put_dec(p, a, dec_digits(a));
+        *p = '\n';
     }
 }
 
@@ -344,8 +411,8 @@ ParsedEdges parse_edge_list_device(const unsigned char* d_text, uint64_t N, bool
     lo.s_len = dalloc<uint32_t>(L, s);
     lo.d_len = dalloc<uint32_t>(L, s);
     lo.t_len = dalloc<uint32_t>(L, s);
-    lo.s_hash = dalloc<uint64_t>(L, s);
-    lo.d_hash = dalloc<uint64_t>(L, s);
+    lo.s_key = dalloc<uint64_t>(L, s);
+    lo.d_key = dalloc<uint64_t>(L, s);
     lo.tv = dalloc<int64_t>(L, s);
     unsigned long long* flags = dalloc<unsigned long long>(2, s);  // [0] first error line, [1] dropped
     const unsigned long long init[2] = {~0ull, 0ull};
@@ -366,7 +433,7 @@ ParsedEdges parse_edge_list_device(const unsigned char* d_text, uint64_t N, bool
     TM_CUDA(cudaStreamSynchronize(s));
     auto release_lines = [&] {
         dfree(lo.kind, s); dfree(lo.s_off, s); dfree(lo.d_off, s); dfree(lo.t_off, s); dfree(lo.s_len, s);
-        dfree(lo.d_len, s); dfree(lo.t_len, s); dfree(lo.s_hash, s); dfree(lo.d_hash, s); dfree(lo.tv, s);
+        dfree(lo.d_len, s); dfree(lo.t_len, s); dfree(lo.s_key, s); dfree(lo.d_key, s); dfree(lo.tv, s);
         dfree(flags, s); dfree(eidx, s); dfree(ls, s);
     };
     if (hflags[0] != ~0ull) {
@@ -398,50 +465,83 @@ ParsedEdges parse_edge_list_device(const unsigned char* d_text, uint64_t N, bool
     P.m = m;
     P.dropped = hflags[1];
 
-    // 3. occurrences
+    // 3. occurrences o = 2 * line + side (non-edge lines are holes)
     P.t = dalloc<int64_t>(m, s);
     P.src = dalloc<uint32_t>(m, s);
     P.dst = dalloc<uint32_t>(m, s);
-    const uint64_t occs = 2 * m;
-    uint64_t* occ_off = dalloc<uint64_t>(occs, s);
-    uint32_t* occ_len = dalloc<uint32_t>(occs, s);
-    uint64_t* occ_hash = dalloc<uint64_t>(occs, s);
-    if (m)
-        TM_LAUNCH("parse_emit", s, emit_edges_kernel, grid_of(L), 256, 0, lo, eidx, L, P.t, occ_off, occ_len,
-                  occ_hash);
-    release_lines();
+    const uint64_t occs = 2 * L;
+    const uint64_t toks = 2 * m;  // tokens actually present
 
-    // 4. interning (table at most 5/8 full even when every token is distinct)
+    // 4. interning: first a table for max(2^20, tokens / 16) distinct tokens
+    //    at load <= 1/2, 4x larger whenever a probe run overflows
+    uint64_t want = std::max<uint64_t>(1ull << 20, toks / 16);
+    uint64_t cap_max = 1024;
+    while (cap_max < toks + toks / 2 + 1) cap_max <<= 1;
     uint64_t cap = 1024;
-    while (cap < occs + occs / 2 + 1) cap <<= 1;
-    unsigned long long* table = dalloc<unsigned long long>(cap, s);
-    uint32_t* first = dalloc<uint32_t>(cap, s);
+    while (cap < 2 * want) cap <<= 1;
+    cap = std::min(cap, cap_max);
     uint32_t* occ_slot = dalloc<uint32_t>(occs, s);
-    TM_CUDA(cudaMemsetAsync(table, 0xff, cap * sizeof(unsigned long long), s));
-    TM_CUDA(cudaMemsetAsync(first, 0xff, cap * sizeof(uint32_t), s));
-    if (occs)
-        TM_LAUNCH("parse_intern", s, intern_kernel, grid_of(occs), 256, 0, d_text, occ_off, occ_len, occ_hash,
-                  occs, table, cap - 1, first, occ_slot);
-    dfree(table, s);
-    dfree(occ_hash, s);
+    uint32_t* first = nullptr;
+    uint32_t* overflow = dalloc<uint32_t>(1, s);
+    for (;;) {
+        unsigned long long* table = dalloc<unsigned long long>(cap, s);
+        first = dalloc<uint32_t>(cap, s);
+        TM_CUDA(cudaMemsetAsync(table, 0xff, cap * sizeof(unsigned long long), s));
+        TM_CUDA(cudaMemsetAsync(first, 0xff, cap * sizeof(uint32_t), s));
+        TM_CUDA(cudaMemsetAsync(overflow, 0, sizeof(uint32_t), s));
+        const int bounded = cap < cap_max;  // the largest table holds every token at load <= 2/3
+        if (toks)
+            TM_LAUNCH("parse_intern", s, intern_kernel, grid_of(occs), 256, 0, d_text, lo, occs, table, cap - 1,
+                      first, occ_slot, overflow, bounded);
+        uint32_t hov = 0;
+        TM_CUDA(cudaMemcpyAsync(&hov, overflow, sizeof(hov), cudaMemcpyDeviceToHost, s));
+        dfree(table, s);
+        TM_CUDA(cudaStreamSynchronize(s));
+        if (!hov) break;
+        dfree(first, s);
+        cap = std::min(cap * 4, cap_max);
+    }
+    dfree(overflow, s);
     // 5. ids by first appearance
     uint32_t* rank = dalloc<uint32_t>(occs + 1, s);
-    exclusive_scan<uint32_t>(FirstFlagLoad{occ_slot, first}, occs, rank, s);
     uint32_t n32 = 0;
-    TM_CUDA(cudaMemcpyAsync(&n32, rank + occs, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    TM_CUDA(cudaStreamSynchronize(s));
+    if (toks) {
+        exclusive_scan<uint32_t>(FirstFlagLoad{occ_slot, first}, occs, rank, s);
+        TM_CUDA(cudaMemcpyAsync(&n32, rank + occs, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        TM_CUDA(cudaStreamSynchronize(s));
+    }
     P.n = n32;
     P.node_off = dalloc<uint64_t>(P.n, s);
     P.node_len = dalloc<uint32_t>(P.n, s);
-    if (occs)
-        TM_LAUNCH("parse_ids", s, assign_ids_kernel, grid_of(occs), 256, 0, occ_slot, first, rank, occ_off, occ_len,
-                  m, P.src, P.dst, P.node_off, P.node_len);
+    if (toks)
+        TM_LAUNCH("parse_ids", s, assign_ids_kernel, grid_of(occs), 256, 0, lo, eidx, occ_slot, first, rank, occs,
+                  P.src, P.dst, P.t, P.node_off, P.node_len);
     dfree(first, s);
     dfree(occ_slot, s);
     dfree(rank, s);
-    dfree(occ_off, s);
-    dfree(occ_len, s);
+    release_lines();
     return P;
+}
+
+uint64_t edge_list_text_bytes(const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t, uint64_t m,
+                              cudaStream_t s) {
+    if (m == 0) return 0;
+    uint64_t* pos = dalloc<uint64_t>(m + 1, s);
+    exclusive_scan<uint64_t>(LineLenLoad{d_src, d_dst, d_t}, m, pos, s);
+    uint64_t bytes = 0;
+    TM_CUDA(cudaMemcpyAsync(&bytes, pos + m, 8, cudaMemcpyDeviceToHost, s));
+    dfree(pos, s);
+    TM_CUDA(cudaStreamSynchronize(s));
+    return bytes;
+}
+
+void write_edge_list_device(const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t, uint64_t m,
+                            char* d_out, cudaStream_t s) {
+    if (m == 0) return;
+    uint64_t* pos = dalloc<uint64_t>(m + 1, s);
+    exclusive_scan<uint64_t>(LineLenLoad{d_src, d_dst, d_t}, m, pos, s);
+    TM_LAUNCH("write_lines", s, write_lines_kernel, grid_of(m), 256, 0, d_src, d_dst, d_t, pos, m, d_out);
+    dfree(pos, s);
 }
 
 void free_parsed(ParsedEdges& P) {

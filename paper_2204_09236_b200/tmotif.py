@@ -139,6 +139,7 @@ def lib():
     L.tm_edge_list_copy.argtypes = [VP, VP, VP, VP, VP]
     L.tm_parse_error_line.restype = C.c_uint64
     L.tm_edge_list_free.argtypes = [VP]
+    L.tm_write_edge_list.argtypes = [VP, VP, VP, C.c_uint64, C.c_int, VP, VP, C.c_int, C.POINTER(C.c_uint64)]
     L.tm_count_edges_async.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint64, VP, C.POINTER(_RunConfig),
                                        C.POINTER(C.c_uint64)]
     L.tm_count_edges_wait.argtypes = [C.c_uint64, C.POINTER(_Counters), VP]
@@ -560,16 +561,43 @@ class EdgeList:
 
 def parse_edge_list_gpu(text, drop_self_loops: bool = True, stream: Optional[int] = None) -> EdgeList:
     """parse_edge_list (graph.cpp:73-116) on the GPU; `text` is str or bytes
-    (host), or (device_pointer, nbytes).  Raises ParseError like the reference."""
+    (host), or (pointer, nbytes[, is_device=True]).  Raises ParseError like
+    the reference."""
     L = lib()
     h = VP()
     if isinstance(text, tuple):
-        ptr, nbytes = text
-        _raise(L.tm_parse_edge_list(ptr, nbytes, 1, int(drop_self_loops), stream, C.byref(h)), L)
+        ptr, nbytes = text[0], text[1]
+        on_dev = text[2] if len(text) > 2 else True
+        _raise(L.tm_parse_edge_list(ptr, nbytes, int(on_dev), int(drop_self_loops), stream, C.byref(h)), L)
     else:
         buf = text.encode("utf-8", "surrogateescape") if isinstance(text, str) else bytes(text)
         _raise(L.tm_parse_edge_list(buf, len(buf), 0, int(drop_self_loops), stream, C.byref(h)), L)
     return EdgeList(h, L)
+
+
+def write_edge_list_gpu(src, dst, t, stream: Optional[int] = None) -> bytes:
+    """write_edge_list (graph.cpp:170) on the GPU for decimal node ids."""
+    L = lib()
+    src = np.ascontiguousarray(src, np.uint32)
+    dst = np.ascontiguousarray(dst, np.uint32)
+    t = np.ascontiguousarray(t, np.int64)
+    nb = C.c_uint64(0)
+    _raise(L.tm_write_edge_list(src.ctypes.data, dst.ctypes.data, t.ctypes.data, len(src), 0, stream, None, 0,
+                                C.byref(nb)), L)
+    buf = C.create_string_buffer(nb.value + 1)
+    _raise(L.tm_write_edge_list(src.ctypes.data, dst.ctypes.data, t.ctypes.data, len(src), 0, stream, buf, 0,
+                                C.byref(nb)), L)
+    return buf.raw[:nb.value]
+
+
+def write_edge_list_device(n_edges: int, src_ptr: int, dst_ptr: int, t_ptr: int, out_ptr: Optional[int] = None,
+                           stream: Optional[int] = None) -> int:
+    """Device-to-device write_edge_list: returns the byte count; writes into
+    out_ptr (device) when given."""
+    L = lib()
+    nb = C.c_uint64(0)
+    _raise(L.tm_write_edge_list(src_ptr, dst_ptr, t_ptr, n_edges, 1, stream, out_ptr, 1, C.byref(nb)), L)
+    return nb.value
 
 
 def load_edge_list(path: str, drop_self_loops: bool = True) -> TemporalGraph:

@@ -128,3 +128,44 @@ def test_device_text_and_census_from_parsed_arrays(cuda, tm, oracle):
     want = tm.count_edges_device(n, m, ds.data_ptr(), dd.data_ptr(), dt.data_ptr(), cfg)
     assert got.tolist() == want.tolist()
     el.close()
+
+
+def test_write_edge_list_round_trip(cuda, tm, oracle):
+    """write_edge_list (graph.cpp:170) on the GPU for decimal ids equals the
+    host writer byte for byte, and parses back to the same edges
+    (test_graph.cpp 'write/parse round trip')."""
+    s, d, t = oracle.generate_random_graph(20, 200, 1000, 3)
+    t = t.copy()
+    t[::7] = -t[::7]  # negative times format with a sign
+    t[3] = -(2 ** 63)
+    t[4] = 2 ** 63 - 1
+    # the reference writes graph.edges(), i.e. (t, ordinal) order; the GPU
+    # writer keeps the given order, so hand it the edges in that order
+    o = np.argsort(t, kind="stable")
+    s, d, t = s[o], d[o], t[o]
+    g = tm.TemporalGraph([str(u) for u in range(20)], s, d, t)
+    text = tm.write_edge_list_gpu(s, d, t)
+    assert text.decode() == tm.write_edge_list(g)
+    back = tm.parse_edge_list_gpu(text).to_graph()
+    assert [back.node_ids[u] for u in back.src] == [str(u) for u in s]
+    assert [back.node_ids[u] for u in back.dst] == [str(u) for u in d]
+    assert (back.t == t).all()
+    assert tm.write_edge_list_gpu(s[:0], d[:0], t[:0]) == b""
+
+
+def test_many_distinct_tokens_regrow_table(cuda, tm):
+    """3M distinct tokens: more than the first interning table takes, so the
+    table is regrown; ids stay in first-appearance order (u0 v0 u1 v1 ...)."""
+    k = 1_500_000
+    text = "".join(f"u{i} v{i} {i}\n" for i in range(k))
+    g = tm.parse_edge_list_gpu(text).to_graph()
+    assert g.node_count() == 2 * k and g.edge_count() == k
+    assert (g.src == np.arange(0, 2 * k, 2)).all() and (g.dst == np.arange(1, 2 * k, 2)).all()
+    assert g.node_ids[:4] == ["u0", "v0", "u1", "v1"] and g.node_ids[-1] == f"v{k - 1}"
+    assert (g.t == np.arange(k)).all()
+    # long tokens (> 7 bytes: hashed keys with byte compares), repeated
+    text = "".join(f"longnode-{i % 1000:06d} other-node-{i % 777:05d} {i}\n" for i in range(200_000))
+    g = tm.parse_edge_list_gpu(text).to_graph()
+    assert g.node_count() == 1777
+    assert g.node_ids[g.src[12345]] == f"longnode-{12345 % 1000:06d}"
+    assert g.node_ids[g.dst[12345]] == f"other-node-{12345 % 777:05d}"
