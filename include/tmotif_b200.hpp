@@ -30,10 +30,19 @@ struct CounterOverflowError : std::runtime_error {
 };
 struct ConsistencyError : std::logic_error { using std::logic_error::logic_error; };
 struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
+// types.hpp:35-44: "line N: what", line() = N
+struct ParseError : std::runtime_error {
+    ParseError(std::size_t line, const std::string& what_full) : std::runtime_error(what_full), line_(line) {}
+    std::size_t line() const { return line_; }
+
+private:
+    std::size_t line_;
+};
 
 inline void check(int rc) {
     switch (rc) {
         case TM_OK: return;
+        case TM_ERR_PARSE: throw ParseError(tm_parse_error_line(), tm_last_error());
         case TM_ERR_INVALID: throw std::invalid_argument(tm_last_error());
         case TM_ERR_OVERFLOW: throw CounterOverflowError();
         case TM_ERR_CONFIG: throw ConfigError(tm_last_error());
@@ -80,10 +89,52 @@ struct RunConfig {
     std::size_t light_batch = 64;
 };
 
+// parse_edge_list / load_edge_list (graph.hpp:60-70) on the GPU: the parsed
+// edges stay in device memory (ingestion order) for GraphContext below.
+struct ParseOptions { bool drop_self_loops = true; };
+class EdgeList {
+public:
+    explicit EdgeList(const std::string& text, const ParseOptions& o = {}) {
+        check(tm_parse_edge_list(text.data(), text.size(), 0, o.drop_self_loops ? 1 : 0, nullptr, &el_));
+        check(tm_edge_list_info(el_, &n_, &m_, &dropped_, &id_bytes_));
+    }
+    ~EdgeList() { tm_edge_list_free(el_); }
+    EdgeList(const EdgeList&) = delete;
+    EdgeList& operator=(const EdgeList&) = delete;
+    std::size_t node_count() const { return n_; }
+    std::size_t edge_count() const { return m_; }
+    std::size_t dropped_self_loops() const { return dropped_; }
+    // node_id(u) for every u (graph.hpp:46), in id order
+    std::vector<std::string> node_ids() const {
+        std::string all(id_bytes_, '\0');
+        check(tm_edge_list_copy(el_, nullptr, nullptr, nullptr, all.data()));
+        std::vector<std::string> out;
+        std::size_t b = 0;
+        for (std::size_t u = 0; u < n_; ++u) {
+            const std::size_t e = all.find('\n', b);
+            out.push_back(all.substr(b, e == std::string::npos ? std::string::npos : e - b));
+            b = e + 1;
+        }
+        return out;
+    }
+    const tm_edge_list* handle() const { return el_; }
+
+private:
+    tm_edge_list* el_ = nullptr;
+    std::uint64_t n_ = 0, m_ = 0, dropped_ = 0, id_bytes_ = 0;
+};
+inline EdgeList parse_edge_list(const std::string& text, const ParseOptions& o = {}) { return EdgeList(text, o); }
+
 // Device-resident GraphContext (indexes.hpp:95-105): built from edges in
 // ingestion order; the (t, ordinal) sort and all indexes are built on the GPU.
 class GraphContext {
 public:
+    explicit GraphContext(const EdgeList& el) {
+        const std::uint32_t *s, *d;
+        const std::int64_t* t;
+        check(tm_edge_list_device_arrays(el.handle(), &s, &d, &t));
+        check(tm_graph_build(s, d, t, el.edge_count(), el.node_count(), 1, nullptr, &g_));
+    }
     GraphContext(const std::vector<NodeId>& src, const std::vector<NodeId>& dst,
                  const std::vector<Timestamp>& t, std::size_t node_count) {
         check(tm_graph_build(src.data(), dst.data(), t.data(), src.size(), node_count, 0, nullptr,

@@ -3,6 +3,7 @@
 // toy graph and a seeded random graph, and prints the census so the gpu test
 // can compare it with the oracle.  Mirrors test_executor.cpp:135-163.
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #include "tmotif_b200.hpp"
@@ -10,6 +11,30 @@
 using namespace tmotif::b200;
 
 int main(int argc, char** argv) {
+    if (argc > 3 && std::string(argv[1]) == "parse") {  // "parse <delta> <file>": the GPU reader
+        try {
+            std::FILE* f = std::fopen(argv[3], "rb");
+            if (!f) return 4;
+            std::string text;
+            char buf[65536];
+            std::size_t got;
+            while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) text.append(buf, got);
+            std::fclose(f);
+            EdgeList el = parse_edge_list(text);
+            GraphContext ctx(el);
+            RunConfig cfg;
+            cfg.delta = std::stoll(argv[2]);
+            MotifCensus a = run_parallel(ctx, cfg);
+            std::printf("NODES %zu EDGES %zu DROPPED %zu FIRST %s\n", el.node_count(), el.edge_count(),
+                        el.dropped_self_loops(), el.node_count() ? el.node_ids()[0].c_str() : "-");
+            for (int k = 0; k < 36; ++k) std::printf("%s %llu\n", signature(k).c_str(),
+                                                     (unsigned long long)a.count_at(k));
+        } catch (const ParseError& e) {
+            std::printf("PARSE_ERROR %zu %s\n", e.line(), e.what());
+            return 5;
+        }
+        return 0;
+    }
     std::size_t n = 0;
     std::vector<NodeId> src, dst;
     std::vector<Timestamp> t;

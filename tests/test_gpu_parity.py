@@ -386,6 +386,26 @@ def test_cpp_host_mirror_driver(cuda, tm, oracle):
     counts = [int(l.split()[1]) for l in out.stdout.splitlines()]
     og = oracle.build_graph(n, s, d, t)
     assert counts == oracle.census(og, delta).tolist()
+    # the same graph as an edge-list file read by the GPU reader through the
+    # mirror's parse_edge_list / GraphContext(EdgeList) (ids renamed; comment,
+    # blank and self-loop lines mixed in)
+    import tempfile
+    lines = ["# header", ""] + [f"n{a} n{b} {c}" for a, b, c in zip(s, d, t)] + ["n1 n1 5", "# end"]
+    with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False) as f:
+        f.write("\r\n".join(lines))
+        path = f.name
+    out = subprocess.run([exe, "parse", str(delta), path], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    head, *rest = out.stdout.splitlines()
+    assert head.split()[:6] == ["NODES", str(len(set(s) | set(d))), "EDGES", str(m), "DROPPED", "1"]
+    assert head.split()[7] == f"n{s[0]}"
+    assert [int(l.split()[1]) for l in rest] == oracle.census(og, delta).tolist()
+    with open(path, "a") as f:
+        f.write("\nn1 n2 notatime\n")
+    out = subprocess.run([exe, "parse", str(delta), path], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 5 and out.stdout.startswith(f"PARSE_ERROR {len(lines) + 1} line {len(lines) + 1}: "
+                                                           "malformed timestamp 'notatime'"), out.stdout
+    os.unlink(path)
 
 
 def test_time_slices_partition_the_census(cuda, tm, oracle):
