@@ -580,6 +580,12 @@ RunHint hint_for(const tm_run_config* cfg, uint64_t n) {
     return h;
 }
 
+// Graph replay pays off where launch overhead matters; a captured graph also
+// keeps its stream-ordered allocations reserved between launches (tens of GB
+// at hundreds of millions of edges, per cached entry), so very large inputs
+// run eagerly.
+constexpr uint64_t kReplayMaxEdges = 128ull << 20;
+
 bool replay_enabled() {
     static int v = -1;
     if (v < 0) {
@@ -1115,8 +1121,8 @@ int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, u
                    uint64_t n, int device_ptrs, void* stream, const tm_run_config* cfg,
                    tm_counters* raw, uint64_t* census36, tm_phase_timings* timings) {
     return guarded([&] {
-        if (!timings && m && cfg && cfg->center_begin == 0 && (cfg->center_end == 0 || cfg->center_end == n) &&
-            replay_enabled())
+        if (!timings && m && m <= kReplayMaxEdges && cfg && cfg->center_begin == 0 &&
+            (cfg->center_end == 0 || cfg->center_end == n) && replay_enabled())
             return count_edges_replay(src, dst, t, m, n, device_ptrs, stream, cfg, raw, census36);
         double index_ms = 0;
         RunHint hint;
@@ -1342,12 +1348,15 @@ int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t
         TM_CUDA(cudaStreamWaitEvent(s, sl.copied, 0));
         try {
             int rc;
-            if (m)
+            if (m && m <= kReplayMaxEdges && replay_enabled())
                 rc = count_edges_replay(sl.ds, sl.dd, sl.dt, m, n, 1, s, cfg, &sl.res.raw, sl.res.census, &sl.P);
-            else
-                rc = tm_count_edges(sl.ds, sl.dd, sl.dt, 0, n, 1, s, cfg, &sl.res.raw, sl.res.census, nullptr);
+            else  // eager (and synchronous) for very large batches
+                rc = tm_count_edges(sl.ds, sl.dd, sl.dt, m, n, 1, s, cfg, &sl.res.raw, sl.res.census, nullptr);
             sl.pending = rc == kPending;
-            if (!sl.pending) sl.res.rc = rc;
+            if (!sl.pending) {
+                sl.res.rc = rc;
+                if (rc != TM_OK) sl.res.err = g_last_error;
+            }
         } catch (const tm_error& e) {
             sl.res.rc = e.code;
             sl.res.err = e.what();
