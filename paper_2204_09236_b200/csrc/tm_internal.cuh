@@ -148,6 +148,8 @@ struct TriStage {
     uint64_t wedge_cap = 0;
     uint32_t* long_list = nullptr;
     uint64_t* wbuf = nullptr;
+    unsigned long long* pt = nullptr;  // pair table for the long windows (keys, then values)
+    uint64_t pt_cap = 0;
 };
 // what a one-shot count will run, known while the index is being built
 struct RunHint {
@@ -215,7 +217,22 @@ struct PView {
     const uint32_t* pofs;
     const uint32_t* dmask;
     const uint32_t* dpref;
+    // optional pair table: (min << 32 | max) -> group start << 32 | length,
+    // replacing the binary search of max in min's block (hub blocks are long)
+    const unsigned long long* pt_keys;
+    const unsigned long long* pt_vals;
+    uint64_t pt_mask;
 };
+constexpr unsigned long long kPairEmpty = ~0ull;
+__device__ __forceinline__ uint64_t pair_slot(uint32_t a, uint32_t b) {
+    uint64_t h = ((uint64_t)a << 32) | b;
+    h ^= h >> 33;
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
+    h *= 0xc4ceb9fe1a85ec53ull;
+    h ^= h >> 33;
+    return h;
+}
 // P records with dir_rel_min = 1 before position x
 __device__ __forceinline__ uint32_t p_dir_before(const PView& P, uint32_t x) {
     return P.dpref[x >> 5] + __popc(P.dmask[x >> 5] & ((1u << (x & 31)) - 1u));
@@ -229,7 +246,8 @@ __device__ __forceinline__ uint32_t outward_before(const SView& S, uint32_t q) {
 }
 
 inline PView pview(const DeviceGraph& g) {
-    return {g.P_t.view(g.tbase), g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs, g.P_dmask, g.P_dpref};
+    return {g.P_t.view(g.tbase), g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs, g.P_dmask, g.P_dpref, nullptr,
+            nullptr, 0};
 }
 
 // ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------

@@ -36,18 +36,36 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
     for (int j = 0; j < 6; ++j) c[j] = 0;
     const uint32_t a = min(v, w), b = max(v, w);
     const uint32_t flip = v == a ? 0u : 1u;  // dir_rel_min -> dir relative to v
-    const uint32_t blk_end = P.pofs[a + 1];
-    uint32_t l = P.pofs[a], r = blk_end;
-    while (l < r) {
-        const uint32_t mid = (l + r) >> 1;
-        if (P.max[mid] < b) l = mid + 1; else r = mid;
+    uint32_t blk_end, kb, l, r;
+    uint32_t known_end = 0;  // group end from the pair table (0: unknown)
+    if (P.pt_keys) {
+        const unsigned long long key = ((unsigned long long)a << 32) | b;
+        uint64_t slot = pair_slot(a, b) & P.pt_mask;
+        for (;;) {
+            const unsigned long long kk = P.pt_keys[slot];
+            if (kk == key) break;
+            if (kk == kPairEmpty) return;  // no v-w record
+            slot = (slot + 1) & P.pt_mask;
+        }
+        const unsigned long long val = P.pt_vals[slot];
+        kb = (uint32_t)(val >> 32);
+        known_end = kb + (uint32_t)val;
+        blk_end = known_end;
+    } else {
+        blk_end = P.pofs[a + 1];
+        l = P.pofs[a];
+        r = blk_end;
+        while (l < r) {
+            const uint32_t mid = (l + r) >> 1;
+            if (P.max[mid] < b) l = mid + 1; else r = mid;
+        }
+        if (l >= blk_end || P.max[l] != b) return;
+        kb = l;
     }
-    if (l >= blk_end || P.max[l] != b) return;
-    const uint32_t kb = l;
     // short groups: classify record by record (triangle_engine.cpp:43-51);
     // a group still running 16 records on goes straight to the searches
     uint32_t k = kb;
-    const bool is_long = kb + 16 < blk_end && P.max[kb + 16] == b;
+    const bool is_long = known_end ? known_end - kb > 16 : (kb + 16 < blk_end && P.max[kb + 16] == b);
     for (int step = 0; step < 16 && !is_long; ++step, ++k) {
         const int64_t tk = P.t[k];
         const uint32_t wk = P.w[k];
@@ -66,7 +84,7 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
     // binary search the window [k1, k4) and the type boundaries
     l = k;
     r = blk_end;
-    for (uint32_t span = 16;; span <<= 1) {
+    for (uint32_t span = 16; !known_end; span <<= 1) {
         const uint64_t probe = (uint64_t)l + span;
         if (probe >= r) break;
         if (P.max[probe] > b) {
@@ -75,11 +93,11 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         }
         l = (uint32_t)probe + 1;
     }
-    while (l < r) {
+    while (!known_end && l < r) {
         const uint32_t mid = (l + r) >> 1;
         if (P.max[mid] <= b) l = mid + 1; else r = mid;
     }
-    const uint32_t ke = l;
+    const uint32_t ke = known_end ? known_end : l;
     l = k; r = ke;
     while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] < lo) l = mid + 1; else r = mid; }
     const uint32_t k1 = l;
@@ -292,13 +310,16 @@ __global__ void __launch_bounds__(256, 6) tri_long_kernel(PView P, TimeArr FT,
                                                        int64_t delta, int64_t t_end,
                                                        const uint32_t* __restrict__ list,
                                                        const uint32_t* __restrict__ lcount,
-                                                       uint64_t* out, uint64_t* stats) {
+                                                       const unsigned long long* __restrict__ pt_wsum,
+                                                       uint64_t pt_min_wedges, uint64_t* out,
+                                                       uint64_t* stats) {
     __shared__ unsigned long long cells[24];
     zero_cells(cells, 24);
     __syncthreads();
     const SmemSink acc{cells};
     const uint32_t cnt = *lcount;
     if (blockIdx.x == 0 && threadIdx.x == 0 && stats) stats[3] = cnt;
+    if (!P.pt_keys || *pt_wsum < pt_min_wedges) P.pt_keys = nullptr;  // the table was not built
     uint32_t my_wedges = 0;
     const int lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -353,6 +374,78 @@ __global__ void __launch_bounds__(256) tri_items_kernel(SView S, PView P, int64_
     }
 }
 
+// Pair table for the long windows, built only when their wedges are many
+// (decided on the device from long_window_sum_kernel's bound: no host sync):
+// clear, one insert per P group (its first record), then the group lengths
+// (its last record).
+// upper bound of the long-window wedges: the in-window records after every
+// long first edge (one gallop per first edge, warp-aggregated sum)
+__global__ void long_window_sum_kernel(TimeArr FT, const uint32_t* __restrict__ Fnode,
+                                       const uint32_t* __restrict__ Foff, int64_t delta,
+                                       const uint32_t* __restrict__ list, const uint32_t* __restrict__ lcount,
+                                       unsigned long long* __restrict__ sum) {
+    const uint32_t cnt = *lcount;
+    unsigned long long acc = 0;
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = list[idx];
+        const uint32_t end = Foff[Fnode[i] + 1];
+        const int64_t lim = sat_add(FT[i], delta);
+        uint32_t lo = i + 1, hi = end, span = 8;
+        while (true) {  // gallop: windows are long here
+            const uint64_t probe = (uint64_t)lo + span;
+            if (probe >= hi) break;
+            if (FT[probe] > lim) {
+                hi = (uint32_t)probe;
+                break;
+            }
+            lo = (uint32_t)probe + 1;
+            span <<= 1;
+        }
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (FT[mid] > lim) hi = mid; else lo = mid + 1;
+        }
+        acc += lo - i - 1;
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(sum, acc);
+}
+
+__device__ __forceinline__ bool pair_table_wanted(const unsigned long long* wsum, uint64_t min_wedges) {
+    return *wsum >= min_wedges;
+}
+
+__global__ void pair_table_clear_kernel(unsigned long long* __restrict__ keys, uint64_t cap,
+                                        const unsigned long long* __restrict__ wsum, uint64_t min_wedges) {
+    if (!pair_table_wanted(wsum, min_wedges)) return;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < cap;
+         x += (uint64_t)gridDim.x * blockDim.x)
+        keys[x] = kPairEmpty;
+}
+__global__ void pair_table_insert_kernel(const uint32_t* __restrict__ P_min, const uint32_t* __restrict__ P_max,
+                                         const uint32_t* __restrict__ P_w, uint64_t m,
+                                         unsigned long long* __restrict__ keys, unsigned long long* __restrict__ vals,
+                                         uint64_t mask, const unsigned long long* __restrict__ wsum,
+                                         uint64_t min_wedges, int pass) {
+    if (!pair_table_wanted(wsum, min_wedges)) return;
+    const uint32_t flag = pass == 0 ? kPFirst : kPLast;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        if (!(P_w[k] & flag)) continue;
+        const uint32_t a = P_min[k], b = P_max[k];
+        const unsigned long long key = ((unsigned long long)a << 32) | b;
+        uint64_t slot = pair_slot(a, b) & mask;
+        if (pass == 0) {  // each pair is one group: a free slot is always found
+            while (atomicCAS(&keys[slot], kPairEmpty, key) != kPairEmpty) slot = (slot + 1) & mask;
+            vals[slot] = (unsigned long long)k << 32;
+        } else {
+            while (keys[slot] != key) slot = (slot + 1) & mask;
+            vals[slot] |= (uint32_t)(k + 1 - (uint32_t)(vals[slot] >> 32));
+        }
+    }
+}
+
 }  // namespace
 
 void tri_filter_stage(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin, uint32_t f_end,
@@ -382,6 +475,19 @@ void tri_filter_stage(const DeviceGraph& g, const Forward& f, int64_t delta, uin
     ts.valid = true;
 }
 
+// long-window wedges (upper bound) at which the pair table pays for its
+// build: ~4 per edge, measured (config 1 at delta 86400 has 2.6 per edge and
+// loses, config 4 at 86400 has 9.6 and gains a third of its triangle pass).
+// TM_PAIR_TABLE=0 disables it, another number overrides the per-edge factor.
+uint64_t pair_table_min_wedges(const DeviceGraph& g) {
+    static const long long env = [] {
+        const char* e = std::getenv("TM_PAIR_TABLE");
+        return e ? std::atoll(e) : -1ll;
+    }();
+    if (env == 0) return ~0ull;
+    return (env > 0 ? (uint64_t)env : 4ull) * std::max<uint64_t>(g.m, 1024);
+}
+
 void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_t t_end, uint64_t* d_out,
                     uint64_t* d_stats) {
     if (!ts.valid) return;
@@ -391,8 +497,36 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
     uint32_t* lcount = reinterpret_cast<uint32_t*>(ts.wbuf + 2);
     TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pview(g), f.t.view(g.tbase), f.nbr, f.ord,
               ts.delta, t_end, ts.wedges, ts.wedge_cap, wcount, d_out, d_stats);
-    TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pview(g), f.t.view(g.tbase), f.nbr, f.ord,
-              f.node, f.off, ts.delta, t_end, ts.long_list, lcount, d_out, d_stats);
+    // pair table for the long windows when they hold many wedges: the
+    // table costs ~one random insert per P group, and replaces the block
+    // search of each long-window wedge (decided on the device: no host sync)
+    PView pv = pview(g);
+    const uint64_t min_wedges = pair_table_min_wedges(g);
+    unsigned long long* wsum = nullptr;
+    if (min_wedges != ~0ull && g.m) {
+        uint64_t pc = 1024;
+        while (pc < g.m + g.m / 4) pc <<= 1;
+        ts.pt = dalloc<unsigned long long>(2 * pc + 1, st);
+        ts.pt_cap = pc;
+        wsum = ts.pt + 2 * pc;
+        TM_CUDA(cudaMemsetAsync(wsum, 0, sizeof(unsigned long long), st));
+        TM_LAUNCH("pair_table", st, long_window_sum_kernel, (unsigned)cap, 256, 0, f.t.view(g.tbase), f.node, f.off,
+                  ts.delta, ts.long_list, lcount, wsum);
+        uint64_t grid = (pc + 255) / 256;
+        if (grid > cap) grid = cap;
+        TM_LAUNCH("pair_table", st, pair_table_clear_kernel, (unsigned)grid, 256, 0, ts.pt, pc, wsum, min_wedges);
+        grid = (g.m + 255) / 256;
+        if (grid > cap) grid = cap;
+        for (int pass = 0; pass < 2; ++pass)
+            TM_LAUNCH("pair_table", st, pair_table_insert_kernel, (unsigned)grid, 256, 0, g.P_min, g.P_max, g.P_w,
+                      g.m, ts.pt, ts.pt + pc, pc - 1, wsum, min_wedges, pass);
+        pv.pt_keys = ts.pt;
+        pv.pt_vals = ts.pt + pc;
+        pv.pt_mask = pc - 1;
+    }
+    TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
+              f.node, f.off, ts.delta, t_end, ts.long_list, lcount, wsum, min_wedges, d_out, d_stats);
+    dfree(ts.pt, st);
     dfree(ts.wedges, st);
     dfree(ts.long_list, st);
     dfree(ts.wbuf, st);
