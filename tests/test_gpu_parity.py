@@ -578,3 +578,49 @@ def test_async_pipelined_counts(cuda, tm, oracle):
     # a second collection of the same ticket is rejected by the C-ABI
     L = tm.lib()
     assert L.tm_count_edges_wait(p_ok.ticket, None, None) != 0
+
+
+def test_pair_table_paths_agree(cuda, tm, oracle):
+    """The long-window pair table (built when the long windows hold many
+    wedges) against the oracle: the same dense graphs counted with the table
+    forced on for every long window (TM_PAIR_TABLE=1 -> threshold m wedges)
+    and off (TM_PAIR_TABLE=0), including a time slice (first_edge_t_end)."""
+    import json
+    import subprocess
+    import sys
+    script = r'''
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2204_09236_b200 as tm
+out = []
+for n, m, tmax, seed, delta in [(30, 4000, 600, 3, 150), (60, 6000, 3000, 8, 400), (12, 2500, 300, 5, 60)]:
+    g = tm.generate_random_graph(n, m, tmax, seed)
+    raw = np.zeros(56, np.uint64)
+    c = tm.count_edges(n, g.src, g.dst, g.t, tm.RunConfig(delta=delta))
+    hi = int(np.sort(g.t)[m // 2])
+    tm.count_edges(n, g.src, g.dst, g.t, tm.RunConfig(delta=delta, first_edge_t_end=hi), raw_out=raw)
+    out.append([c.tolist(), raw.tolist(), hi])
+print(json.dumps(out))
+'''
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("1", "0"):
+        env = dict(os.environ, TM_PAIR_TABLE=mode)
+        r = subprocess.run([sys.executable, "-c", script, root], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[mode] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["1"] == res["0"]
+    for (n, m, tmax, seed, delta), (census, raw, hi) in zip(
+            [(30, 4000, 600, 3, 150), (60, 6000, 3000, 8, 400), (12, 2500, 300, 5, 60)], res["1"]):
+        s, d, t = oracle.generate_random_graph(n, m, tmax, seed)
+        og = oracle.build_graph(n, s, d, t)
+        assert census == oracle.census(og, delta).tolist()
+        assert sum(raw[32:56]) > 0
+        want = oracle.census_bruteforce_before(og, delta, hi).tolist() if m <= 3000 else None
+        if want is not None:
+            rc = tm.RawCounters.from_array(np.array(raw, np.uint64))
+            assert tm.merge_census(rc.star, rc.pair, rc.tri, tm.TriangleMode.count_all).counts.tolist() == want
+        oracle.free(og)
