@@ -29,6 +29,8 @@ namespace {
 // The v-w list is the P group {min, max}: lower_bound of max in min's block.
 // t_end restricts to instances whose earliest edge has t < t_end (time-slice
 // partitions): the closing edge itself for type I, e_i otherwise.
+constexpr uint32_t kTableMinBlock = 256;
+
 __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint32_t w, int64_t lo,
                                                int64_t hi, int64_t ti, uint32_t oi, int64_t tj,
                                                uint32_t oj, int64_t t_end, uint32_t c[6]) {
@@ -36,9 +38,11 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
     for (int j = 0; j < 6; ++j) c[j] = 0;
     const uint32_t a = min(v, w), b = max(v, w);
     const uint32_t flip = v == a ? 0u : 1u;  // dir_rel_min -> dir relative to v
-    uint32_t blk_end, kb, l, r;
+    uint32_t blk_end = P.pofs[a + 1], kb, l = P.pofs[a], r;
     uint32_t known_end = 0;  // group end from the pair table (0: unknown)
-    if (P.pt_keys) {
+    // the table only for long blocks (a hub's), where the binary search is
+    // ~17 dependent probes; short blocks are cheaper to search in L2
+    if (P.pt_keys && blk_end - l > kTableMinBlock) {
         const unsigned long long key = ((unsigned long long)a << 32) | b;
         uint64_t slot = pair_slot(a, b) & P.pt_mask;
         for (;;) {
@@ -52,8 +56,6 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         known_end = kb + (uint32_t)val;
         blk_end = known_end;
     } else {
-        blk_end = P.pofs[a + 1];
-        l = P.pofs[a];
         r = blk_end;
         while (l < r) {
             const uint32_t mid = (l + r) >> 1;
