@@ -38,15 +38,8 @@ __global__ void time_keys_kernel(const int64_t* __restrict__ t, uint64_t m, int6
     }
 }
 
-__global__ void perm_from_keys_kernel(const uint64_t* __restrict__ keys, uint64_t m, uint64_t kmask,
-                                      uint32_t* __restrict__ perm) {
-    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
-         p += (uint64_t)gridDim.x * blockDim.x)
-        perm[p] = (uint32_t)(keys[p] & kmask);
-}
-
-// Edge records in (t, ordinal) order, read by random gathers in gather_s
-// and gather_p.  Wide (16 B): any int64 timestamps.  Narrow (8 B): t - t_min
+// Edge records in input order (indexed by ordinal), read by random gathers in
+// gather_s and gather_p.  Wide (16 B): any int64 timestamps.  Narrow (8 B): t - t_min
 // as u32 and src ^ dst with "src is the smaller endpoint" in the top bit (node
 // ids are < 2^31), used whenever the time span fits 32 bits -- half the bytes
 // per gather, and the whole array (80 MB at 10M edges) mostly stays in L2.
@@ -82,7 +75,11 @@ struct EdgeCodec<true> {
     __device__ static uint32_t dir_from_min(const Rec& e, uint32_t) { return (e.x >> 31) ? 0u : 1u; }
 };
 
-// record r = 2p + side of the p-th edge in (t, ordinal) order: key node << 32 | r.
+// record r = 2k + side of the p-th edge in (t, ordinal) order, k its input
+// index: key node << 32 | r.  The stable node sort keeps (t, ordinal) order
+// inside each node because the keys are emitted in that order; the payload
+// names the input edge, so the edge records E are indexed by input position
+// (written coalesced here) and S / P read their ordinals straight from the key.
 // One block per radix-sort tile (kSortTile keys = kSortTile / 2 edges): the
 // tile's histogram of the first digit (node & 255) is written digit-major like
 // radix_upsweep's, so the node sort skips its first counting pass.
@@ -92,13 +89,17 @@ constexpr int kPackEdges = kSortTile / 2;
 // kernel also validates the edges (endpoint range, self loops), reduces the
 // t range, detects time-unordered input, and -- packing narrow records
 // relative to t[0] -- flags spans that do not fit; the host reads `st` once
-// and re-packs in the rare cases (unordered input, wide span).
-template <bool kNarrow>
+// and re-packs in the rare cases (unordered input, wide span).  The (t,
+// ordinal) order of unordered input comes as perm[p] or as the low kmask bits
+// of the time sort's packed keys tkeys[p].  Endpoints are clamped into range
+// in every pass: a speculatively replayed build of input the verdict later
+// rejects stays in bounds.
+template <bool kNarrow, bool kPermuted>
 __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
-    const uint32_t* __restrict__ perm, const uint32_t* __restrict__ src,
-    const uint32_t* __restrict__ dst, const int64_t* __restrict__ t, uint64_t m, uint64_t n,
-    int64_t tmin, typename EdgeCodec<kNarrow>::Rec* __restrict__ E, uint64_t* __restrict__ keys,
-    uint32_t* __restrict__ counts, uint32_t ntiles, BuildStats* __restrict__ st) {
+    const uint32_t* __restrict__ perm, const uint64_t* __restrict__ tkeys, uint64_t kmask,
+    const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, const int64_t* __restrict__ t,
+    uint64_t m, uint64_t n, int64_t tmin, typename EdgeCodec<kNarrow>::Rec* __restrict__ E,
+    uint64_t* __restrict__ keys, uint32_t* __restrict__ counts, uint32_t ntiles, BuildStats* __restrict__ st) {
     constexpr int NW = kPackBlock / 32;
     __shared__ uint32_t hist[NW][256];
     const int w = threadIdx.x >> 5;
@@ -112,22 +113,27 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
         for (int j = 0; j < kPackEdges / kPackBlock; ++j) {
             const uint64_t p = (uint64_t)tile * kPackEdges + j * kPackBlock + threadIdx.x;
             if (p < m) {
-                const uint32_t k = perm ? perm[p] : (uint32_t)p;
+                const uint32_t k = !kPermuted ? (uint32_t)p : perm ? perm[p] : (uint32_t)(tkeys[p] & kmask);
                 uint32_t a = src[k], b = dst[k];
-                const int64_t tk = t[k];
+                const int64_t tp = t[p];
                 if (st) {
                     bad |= (a == b) | (a >= n) | (b >= n);
-                    // keep a speculative build of invalid input in bounds
-                    // (the verdict rejects it afterwards)
-                    a = a < n ? a : 0u;
-                    b = b < n ? b : 0u;
-                    lo = min(lo, (long long)tk);
-                    hi = max(hi, (long long)tk);
-                    if (p + 1 < m) uns |= (t[p + 1] < tk);
+                    lo = min(lo, (long long)tp);
+                    hi = max(hi, (long long)tp);
+                    if (p + 1 < m) uns |= (t[p + 1] < tp);
                 }
-                E[p] = EdgeCodec<kNarrow>::make(tk, a, b, tmin);
+                a = a < n ? a : 0u;
+                b = b < n ? b : 0u;
+                uint32_t ea = a, eb = b;  // edge p in input order
+                if (kPermuted) {
+                    ea = src[p];
+                    eb = dst[p];
+                    ea = ea < n ? ea : 0u;
+                    eb = eb < n ? eb : 0u;
+                }
+                E[p] = EdgeCodec<kNarrow>::make(tp, ea, eb, tmin);
                 reinterpret_cast<ulonglong2*>(keys)[p] =
-                    make_ulonglong2(((uint64_t)a << 32) | (2 * p), ((uint64_t)b << 32) | (2 * p + 1));
+                    make_ulonglong2(((uint64_t)a << 32) | (2 * k), ((uint64_t)b << 32) | (2 * k + 1));
                 atomicAdd(&hist[w][a & 255u], 1u);
                 atomicAdd(&hist[w][b & 255u], 1u);
             }
@@ -159,8 +165,7 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
 }
 
 template <bool kNarrow>
-__global__ void gather_s_kernel(const uint32_t* __restrict__ perm,
-                                const typename EdgeCodec<kNarrow>::Rec* __restrict__ E, int64_t tmin,
+__global__ void gather_s_kernel(const typename EdgeCodec<kNarrow>::Rec* __restrict__ E, int64_t tmin,
                                 const uint64_t* __restrict__ skeys, uint64_t R, uint64_t n,
                                 uint32_t* __restrict__ off,
                                 int64_t* __restrict__ S_tw, uint32_t* __restrict__ S_tn,
@@ -172,7 +177,7 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm,
         const uint64_t q = base + threadIdx.x;
         uint32_t out = 0, mx = 0;
         if (q < R) {
-            const uint64_t key = skeys[q];
+            const uint64_t key = __ldcs(skeys + q);  // streamed: leave L2 to the edge records
             const uint32_t r = (uint32_t)key;
             const uint32_t p = r >> 1, side = r & 1u;
             using Codec = EdgeCodec<kNarrow>;
@@ -187,7 +192,7 @@ __global__ void gather_s_kernel(const uint32_t* __restrict__ perm,
             mx = x < u ? 1u : 0u;  // u is the pair's larger endpoint
             if (kNarrow) __stcs(S_tn + q, Codec::rel(e));
             else __stcs(S_tw + q, Codec::time(e, tmin));
-            __stcs(S_ord + q, perm ? perm[p] : p);
+            __stcs(S_ord + q, p);
             __stcs(S_node + q, u);
             __stcs(S_nbr + q, x | (side << 31));
         }
@@ -241,7 +246,6 @@ __device__ __forceinline__ void pair_of(const uint64_t* __restrict__ pkeys,
 
 template <bool kNarrow>
 __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restrict__ pkeys, uint64_t m,
-                                                       const uint32_t* __restrict__ perm,
                                                        const typename EdgeCodec<kNarrow>::Rec* __restrict__ E,
                                                        int64_t tmin,
                                                        int64_t* __restrict__ P_tw,
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
         uint32_t a = 0, b = 0, p = 0;
         typename Codec::Rec ed{};
         if (k < m) {
-            const uint64_t key = pkeys[k];
+            const uint64_t key = __ldcs(pkeys + k);
             p = (uint32_t)key;
             ed = E[p];
             a = (uint32_t)(key >> 32);
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
             const uint32_t dir_min = Codec::dir_from_min(ed, a);  // 0: min -> max
             if (kNarrow) __stcs(P_tn + k, Codec::rel(ed));
             else __stcs(P_tw + k, Codec::time(ed, tmin));
-            __stcs(P_ord + k, perm ? perm[p] : p);
+            __stcs(P_ord + k, p);
             __stcs(P_min + k, a);
             __stcs(P_max + k, b);
             __stcs(P_w + k, (dir_min << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u));
@@ -513,8 +517,8 @@ BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d
     *hv = h_st;
     TM_CUDA(cudaMemcpyAsync(d_st, hv, sizeof(h_st), cudaMemcpyHostToDevice, s));
     if (m) {
-        TM_LAUNCH("pack_edges", s, pack_edges_kernel<true>, grid_for(m, kPackEdges), kPackBlock, 0, nullptr,
-                  d_src, d_dst, d_t, m, n, (int64_t)0, reinterpret_cast<NarrowEdge*>(pl.E), pl.nk0, pl.c0,
+        TM_LAUNCH("pack_edges", s, (pack_edges_kernel<true, false>), grid_for(m, kPackEdges), kPackBlock, 0, nullptr,
+                  nullptr, 0ull, d_src, d_dst, d_t, m, n, (int64_t)0, reinterpret_cast<NarrowEdge*>(pl.E), pl.nk0, pl.c0,
                   pl.ntiles, d_st);
     }
     TM_CUDA(cudaMemcpyAsync(hv, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, s));
@@ -547,6 +551,15 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
                  uint64_t m, uint64_t n, const RunHint* hint) {
     BuildPlan pl = build_prepare(g, d_src, d_dst, d_t, m, n, nullptr, nullptr);
     build_finish(g, pl, d_src, d_dst, d_t, hint);
+}
+
+template <bool kNarrow, bool kPermuted>
+void launch_repack(const uint32_t* perm, const uint64_t* tkeys, uint64_t kmask, const uint32_t* d_src,
+                   const uint32_t* d_dst, const int64_t* d_t, uint64_t m, uint64_t n, int64_t tmin, uint8_t* E,
+                   uint64_t* keys, uint32_t* counts, uint32_t ntiles, cudaStream_t s) {
+    TM_LAUNCH("pack_edges", s, (pack_edges_kernel<kNarrow, kPermuted>), grid_for(m, kPackEdges), kPackBlock, 0, perm,
+              tkeys, kmask, d_src, d_dst, d_t, m, n, tmin,
+              reinterpret_cast<typename EdgeCodec<kNarrow>::Rec*>(E), keys, counts, ntiles, nullptr);
 }
 
 void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const uint32_t* d_dst,
@@ -597,8 +610,12 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
     uint32_t* nullv = nullptr;
     uint32_t* nullv2 = nullptr;
 
-    // 1. (t, ordinal) order of the edges (skipped for time-ordered input)
+    // 1. (t, ordinal) order of the edges (skipped for time-ordered input):
+    //    input indices in the low kbits of the sorted packed keys, or the
+    //    sorted values when (t - tmin, index) does not fit 64 bits
     uint32_t* perm = nullptr;
+    uint64_t* tkeys = nullptr;
+    uint64_t kmask = 0;
     if (h_st.unsorted) {
         const int tbits = bit_width_u64((uint64_t)h_st.tmax - (uint64_t)h_st.tmin);
         const int kbits = bit_width_u64(m - 1 ? m - 1 : 1);
@@ -611,16 +628,16 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
                   kbits, packed, k0, v0);
         if (packed) {
             radix_sort<uint64_t>(k0, nullv, k1, nullv2, m, kbits, kbits + tbits, s);
-            perm = dalloc<uint32_t>(m, s);
-            TM_LAUNCH("perm_from_keys", s, perm_from_keys_kernel, grid_for(m), 256, 0, k0, m,
-                      (1ull << kbits) - 1, perm);
+            tkeys = k0;
+            kmask = (1ull << kbits) - 1;
+            dfree(k1, s);
         } else {
             radix_sort<uint64_t>(k0, v0, k1, v1, m, 0, tbits, s);
             perm = v0;
             dfree(v1, s);
+            dfree(k0, s);
+            dfree(k1, s);
         }
-        dfree(k0, s);
-        dfree(k1, s);
     }
 
     // 2. S: stable sort of the incident records by node (key node << 32 | r)
@@ -633,14 +650,14 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
                 pl.E = E;
                 pl.E_bytes = m * sizeof(WideEdge);
             }
-            if (narrow)
-                TM_LAUNCH("pack_edges", s, pack_edges_kernel<true>, grid_for(m, kPackEdges), kPackBlock, 0, perm,
-                          d_src, d_dst, d_t, m, n, tmin, reinterpret_cast<NarrowEdge*>(E), nk0, c0, ntiles,
-                          nullptr);
-            else
-                TM_LAUNCH("pack_edges", s, pack_edges_kernel<false>, grid_for(m, kPackEdges), kPackBlock, 0, perm,
-                          d_src, d_dst, d_t, m, n, tmin, reinterpret_cast<WideEdge*>(E), nk0, c0, ntiles,
-                          nullptr);
+            const bool permuted = perm || tkeys;
+            if (narrow && permuted) launch_repack<true, true>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, c0, ntiles, s);
+            else if (narrow) launch_repack<true, false>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, c0, ntiles, s);
+            else if (permuted) launch_repack<false, true>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, c0, ntiles, s);
+            else launch_repack<false, false>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, c0, ntiles, s);
+            // the gathers read ordinals from the keys: the order is no longer needed
+            if (perm) dfree(perm, s);
+            if (tkeys) dfree(tkeys, s);
         }
         auto EN = reinterpret_cast<NarrowEdge*>(E);
         auto EW = reinterpret_cast<WideEdge*>(E);
@@ -652,10 +669,10 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         uint32_t* xpref = dalloc<uint32_t>(nw + 1, s);
         TM_CUDA(cudaMemsetAsync(xmask + (nw - 1), 0, sizeof(uint32_t), s));
         if (narrow)
-            TM_LAUNCH("gather_s", s, gather_s_kernel<true>, grid_for(R), 256, 0, perm, EN, tmin, nk0, R, n, g.off,
+            TM_LAUNCH("gather_s", s, gather_s_kernel<true>, grid_for(R), 256, 0, EN, tmin, nk0, R, n, g.off,
                       g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask);
         else
-            TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, perm, EW, tmin, nk0, R, n, g.off,
+            TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, EW, tmin, nk0, R, n, g.off,
                       g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask);
         // outward prefix (stars) and max-side prefix (pair keys) in one scan
         exclusive_scan_to<uint64_t>(PopcLoad2{g.S_omask, xmask}, nw, SplitStore2{g.S_opref, xpref}, s);
@@ -683,10 +700,10 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         dfree(xpref, s);
         radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
         if (narrow)
-            TM_LAUNCH("gather_p", s, gather_p_kernel<true>, grid_for(m), 256, 0, pk0, m, perm, EN, tmin, g.P_t.w, g.P_t.n,
+            TM_LAUNCH("gather_p", s, gather_p_kernel<true>, grid_for(m), 256, 0, pk0, m, EN, tmin, g.P_t.w, g.P_t.n,
                       g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask);
         else
-            TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, perm, EW, tmin, g.P_t.w, g.P_t.n,
+            TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, EW, tmin, g.P_t.w, g.P_t.n,
                       g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask);
         dfree(pk0_alloc, s);
         exclusive_scan<uint32_t>(PopcLoad{g.P_dmask}, m / 32 + 1, g.P_dpref, s);
@@ -695,7 +712,6 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
             dfree(E, s);
         }
     }
-    if (perm) dfree(perm, s);
     g.max_degree = 0;  // not needed by the layout (positions are global 32-bit)
 }
 
