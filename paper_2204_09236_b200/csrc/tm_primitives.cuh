@@ -136,6 +136,51 @@ struct SmemSink {
 };
 using GlobalSink = SmemSink;
 
+// Warp-held triangle cells: lane L (< 24) keeps the warp's running sum of
+// cell L.  add6() folds six per-lane counts bound for cells ty * 8 + base + dk
+// (c[ty * 2 + dk], base in {0, 2, 4, 6}) into them with one warp reduction per
+// value and distinct base present in the warp.  A u64 shared-memory atomicAdd
+// compiles to a CAS loop that serialises every lane of a warp adding to the
+// same cell -- the lanes of a long triangle window all share the first edge,
+// so most of their adds collide.  Reductions are 32-bit: a warp whose counts
+// reach 2^27 (32 of them could wrap) takes the per-lane atomics instead.
+struct WarpCells {
+    uint64_t mine = 0;
+    __device__ __forceinline__ void add6(bool active, int base, const uint32_t c[6],
+                                         unsigned long long* cells) {
+        uint32_t big = 0, nz = 0;
+#pragma unroll
+        for (int x = 0; x < 6; ++x) {
+            const uint32_t v = active ? c[x] : 0u;
+            big |= v >> 27;
+            nz |= v;
+        }
+        if (__any_sync(0xffffffffu, big)) {
+            if (active)
+#pragma unroll
+                for (int x = 0; x < 6; ++x)
+                    if (c[x]) atomicAdd(&cells[(x >> 1) * 8 + base + (x & 1)], (unsigned long long)c[x]);
+            return;
+        }
+        const uint32_t present = __reduce_or_sync(0xffffffffu, nz ? 1u << (base >> 1) : 0u);
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (!((present >> q) & 1u)) continue;  // warp-uniform
+            const bool mine_q = active && base == 2 * q;
+#pragma unroll
+            for (int x = 0; x < 6; ++x) {
+                const uint32_t sum = __reduce_add_sync(0xffffffffu, mine_q ? c[x] : 0u);
+                if (lane == (x >> 1) * 8 + 2 * q + (x & 1)) mine += sum;
+            }
+        }
+    }
+    // each lane's cell into the block's shared cells (whole warp, before the block flush)
+    __device__ __forceinline__ void flush(unsigned long long* cells) const {
+        if (mine) atomicAdd(&cells[threadIdx.x & 31], (unsigned long long)mine);
+    }
+};
+
 // zero `count` shared cells; call before use, followed by __syncthreads
 __device__ __forceinline__ void zero_cells(unsigned long long* cells, int count) {
     for (int i = threadIdx.x; i < count; i += blockDim.x) cells[i] = 0;

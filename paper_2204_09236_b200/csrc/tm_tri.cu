@@ -260,25 +260,20 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(TimeArr FT,
     }
 }
 
-template <typename Sink>
-__device__ __forceinline__ void add_wedge(const PView& P, TimeArr FT,
-                                          const uint32_t* __restrict__ FN,
-                                          const uint32_t* __restrict__ FO, uint32_t i, uint32_t j,
-                                          int64_t delta, int64_t t_end, const Sink& acc) {
+// closing counts of wedge (i, j) in F: c[type * 2 + dk]; returns the cell
+// base di * 4 + dj * 2 (cells type * 8 + base + dk)
+__device__ __forceinline__ int wedge_counts(const PView& P, TimeArr FT, const uint32_t* __restrict__ FN,
+                                            const uint32_t* __restrict__ FO, uint32_t i, uint32_t j,
+                                            int64_t delta, int64_t t_end, uint32_t c[6]) {
     const uint32_t ni = FN[i], nj = FN[j];
     const int64_t ti = FT[i], tj = FT[j];
-    uint32_t c[6];
     closing_counts(P, ni & kNodeMask, nj & kNodeMask, sat_sub(tj, delta), sat_add(ti, delta), ti,
                    FO[i], tj, FO[j], t_end, c);
-    const int cell0 = (int)((ni >> 31) * 4 + (nj >> 31) * 2);  // di*4 + dj*2
-#pragma unroll
-    for (int ty = 0; ty < 3; ++ty)
-#pragma unroll
-        for (int dk = 0; dk < 2; ++dk) acc.add(ty * 8 + cell0 + dk, c[ty * 2 + dk]);
+    return (int)((ni >> 31) * 4 + (nj >> 31) * 2);
 }
 
 // one wedge per thread
-__global__ void __launch_bounds__(256, 6) tri_wedge_kernel(PView P, TimeArr FT,
+__global__ void __launch_bounds__(256, 5) tri_wedge_kernel(PView P, TimeArr FT,
                                                         const uint32_t* __restrict__ FN,
                                                         const uint32_t* __restrict__ FO,
                                                         int64_t delta, int64_t t_end,
@@ -289,22 +284,30 @@ __global__ void __launch_bounds__(256, 6) tri_wedge_kernel(PView P, TimeArr FT,
     __shared__ unsigned long long cells[24];
     zero_cells(cells, 24);
     __syncthreads();
-    const SmemSink acc{cells};
+    WarpCells wc;
     uint64_t cnt = wcount[0] < wedge_cap ? wcount[0] : wedge_cap;
     if (wcount[1] < cnt) cnt = wcount[1];
     if (blockIdx.x == 0 && threadIdx.x == 0 && stats) stats[2] = cnt;
-    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
-         idx += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t w = wedges[idx];
-        add_wedge(P, FT, FN, FO, (uint32_t)(w >> 32), (uint32_t)w, delta, t_end, acc);
+    // warp-uniform trip count (the cells are reduced across the warp)
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < cnt;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t idx = base + (threadIdx.x & 31);
+        uint32_t c[6] = {0, 0, 0, 0, 0, 0};
+        int cb = 0;
+        if (idx < cnt) {
+            const uint64_t w = wedges[idx];
+            cb = wedge_counts(P, FT, FN, FO, (uint32_t)(w >> 32), (uint32_t)w, delta, t_end, c);
+        }
+        wc.add6(idx < cnt, cb, c, cells);
     }
+    wc.flush(cells);
     __syncthreads();
     flush_cells(cells, 24, out);
 }
 
 // first edges with long windows: one warp per first edge, lanes stride the
 // in-window records (the HARE intra-node split, per first edge)
-__global__ void __launch_bounds__(256, 6) tri_long_kernel(PView P, TimeArr FT,
+__global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
                                                        const uint32_t* __restrict__ FN,
                                                        const uint32_t* __restrict__ FO,
                                                        const uint32_t* __restrict__ Fnode,
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(256, 6) tri_long_kernel(PView P, TimeArr FT,
     __shared__ unsigned long long cells[24];
     zero_cells(cells, 24);
     __syncthreads();
-    const SmemSink acc{cells};
+    WarpCells wc;
     const uint32_t cnt = *lcount;
     if (blockIdx.x == 0 && threadIdx.x == 0 && stats) stats[3] = cnt;
     if (!P.pt_keys || *pt_wsum < pt_min_wedges) P.pt_keys = nullptr;  // the table was not built
@@ -334,13 +337,18 @@ __global__ void __launch_bounds__(256, 6) tri_long_kernel(PView P, TimeArr FT,
         for (uint32_t j0 = i + 1; j0 < end; j0 += 32) {
             const uint32_t j = j0 + lane;
             const bool in = j < end && FT[j] <= lim;
-            if (in && (FN[j] & kNodeMask) != v) {
-                add_wedge(P, FT, FN, FO, i, j, delta, t_end, acc);
+            const bool wedge = in && (FN[j] & kNodeMask) != v;
+            uint32_t c[6] = {0, 0, 0, 0, 0, 0};
+            int cb = 0;
+            if (wedge) {
+                cb = wedge_counts(P, FT, FN, FO, i, j, delta, t_end, c);
                 ++my_wedges;
             }
+            wc.add6(wedge, cb, c, cells);
             if (!__all_sync(0xffffffffu, in)) break;
         }
     }
+    wc.flush(cells);
     my_wedges = warp_sum(my_wedges);
     if (lane == 0 && my_wedges && stats) atomicAdd((unsigned long long*)&stats[4], (unsigned long long)my_wedges);
     __syncthreads();
