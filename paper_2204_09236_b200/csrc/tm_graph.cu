@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
                                                        uint32_t* __restrict__ P_max,
                                                        uint32_t* __restrict__ P_w, uint64_t n,
                                                        uint32_t* __restrict__ pofs,
-                                                       uint32_t* __restrict__ dmask) {
+                                                       uint32_t* __restrict__ dmask,
+                                                       uint32_t* __restrict__ gmask) {
     using Codec = EdgeCodec<kNarrow>;
     __shared__ uint32_t s_a[258], s_b[258];
     const int tid = threadIdx.x;
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = base + tid;
         uint32_t a = 0, b = 0, p = 0;
+        bool first = false;
         typename Codec::Rec ed{};
         if (k < m) {
             const uint64_t key = __ldcs(pkeys + k);
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
             pair_of<kNarrow>(pkeys, E, k + 1, s_a[tid + 2], s_b[tid + 2]);
         __syncthreads();
         if (k < m) {
-            const bool first = k == 0 || s_a[tid] != a || s_b[tid] != b;
+            first = k == 0 || s_a[tid] != a || s_b[tid] != b;
             const bool last = k + 1 == m || s_a[tid + 2] != a || s_b[tid + 2] != b;
             const uint32_t dir_min = Codec::dir_from_min(ed, a);  // 0: min -> max
             if (kNarrow) __stcs(P_tn + k, Codec::rel(ed));
@@ -294,7 +296,11 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
                 for (int64_t x = (int64_t)a + 1; x <= (int64_t)n; ++x) pofs[x] = (uint32_t)m;
         }
         const unsigned db = __ballot_sync(0xffffffffu, k < m && Codec::dir_from_min(ed, a));
-        if ((tid & 31) == 0 && k < m) dmask[k >> 5] = db;
+        const unsigned gb = __ballot_sync(0xffffffffu, first);
+        if ((tid & 31) == 0 && k < m) {
+            dmask[k >> 5] = db;
+            gmask[k >> 5] = gb;
+        }
         __syncthreads();
     }
 }
@@ -596,7 +602,10 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
     g.P_min = dalloc<uint32_t>(m, s);
     g.P_dmask = dalloc<uint32_t>(m / 32 + 1, s);
     g.P_dpref = dalloc<uint32_t>(m / 32 + 2, s);
+    g.P_gmask = dalloc<uint32_t>(m / 32 + 1, s);
+    g.P_gpref = dalloc<uint32_t>(m / 32 + 2, s);
     TM_CUDA(cudaMemsetAsync(g.P_dmask + m / 32, 0, sizeof(uint32_t), s));
+    TM_CUDA(cudaMemsetAsync(g.P_gmask + m / 32, 0, sizeof(uint32_t), s));
 
     if (m == 0) {
         release_plan(g, pl);
@@ -701,12 +710,14 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
         if (narrow)
             TM_LAUNCH("gather_p", s, gather_p_kernel<true>, grid_for(m), 256, 0, pk0, m, EN, tmin, g.P_t.w, g.P_t.n,
-                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask);
+                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask, g.P_gmask);
         else
             TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, EW, tmin, g.P_t.w, g.P_t.n,
-                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask);
+                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask, g.P_gmask);
         dfree(pk0_alloc, s);
-        exclusive_scan<uint32_t>(PopcLoad{g.P_dmask}, m / 32 + 1, g.P_dpref, s);
+        // direction prefix and group-first prefix in one scan
+        exclusive_scan_to<uint64_t>(PopcLoad2{g.P_dmask, g.P_gmask}, m / 32 + 1, SplitStore2{g.P_dpref, g.P_gpref},
+                                    s);
         if (pl.owned) {
             dfree(spare, s);
             dfree(E, s);
@@ -816,6 +827,7 @@ void free_graph(DeviceGraph& g) {
     dfree(g.off, s);
     dfree(g.P_t.w, s); dfree(g.P_t.n, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
     dfree(g.P_min, s); dfree(g.pofs, s); dfree(g.P_dmask, s); dfree(g.P_dpref, s);
+    dfree(g.P_gmask, s); dfree(g.P_gpref, s);
     dfree(g.pre_tri.wedges, s); dfree(g.pre_tri.long_list, s); dfree(g.pre_tri.wbuf, s);
     g.pre_tri.valid = false;
     for (auto& f : g.fwd) {

@@ -23,6 +23,9 @@
 //     P_dmask[m/32+1], P_dpref[m/32+2]  bitmask of dir_rel_min = 1 records and
 //               the prefix of its word popcounts: the direction split of any P
 //               range in four loads (long closing groups)
+//     P_gmask[m/32+1], P_gpref[m/32+2]  bitmask of group-first records and
+//               its word-popcount prefix: the group index of a record in two
+//               loads (the triangle pass's group ends, tm_tri.cu)
 //   F (forward-oriented sequences for the triangle pass, one per orientation)
 #pragma once
 
@@ -150,6 +153,8 @@ struct TriStage {
     uint64_t* wbuf = nullptr;
     unsigned long long* pt = nullptr;  // pair table for the long windows (keys, then values)
     uint64_t pt_cap = 0;
+    unsigned long long* wsum = nullptr;  // long-window wedge bound (device)
+    uint32_t* gend = nullptr;           // P group ends, built when the long windows are many
 };
 // what a one-shot count will run, known while the index is being built
 struct RunHint {
@@ -189,6 +194,8 @@ struct DeviceGraph {
     uint32_t* pofs = nullptr;
     uint32_t* P_dmask = nullptr;
     uint32_t* P_dpref = nullptr;
+    uint32_t* P_gmask = nullptr;
+    uint32_t* P_gpref = nullptr;
 
     Forward fwd[2];
     TriStage pre_tri;  // filter issued early for a one-shot count (RunHint)
@@ -217,6 +224,9 @@ struct PView {
     const uint32_t* pofs;
     const uint32_t* dmask;
     const uint32_t* dpref;
+    const uint32_t* gmask;
+    const uint32_t* gpref;
+    const uint32_t* gend;  // group ends by group index (triangle pass only; else null)
     // optional pair table: (min << 32 | max) -> group start << 32 | length,
     // replacing the binary search of max in min's block (hub blocks are long)
     const unsigned long long* pt_keys;
@@ -234,6 +244,10 @@ __device__ __forceinline__ uint64_t pair_slot(uint32_t a, uint32_t b) {
     return h;
 }
 // P records with dir_rel_min = 1 before position x
+// end (one past the last record) of the P group starting at record x
+__device__ __forceinline__ uint32_t p_group_end(const PView& P, uint32_t x) {
+    return P.gend[P.gpref[x >> 5] + __popc(P.gmask[x >> 5] & ((1u << (x & 31)) - 1u))];
+}
 __device__ __forceinline__ uint32_t p_dir_before(const PView& P, uint32_t x) {
     return P.dpref[x >> 5] + __popc(P.dmask[x >> 5] & ((1u << (x & 31)) - 1u));
 }
@@ -246,8 +260,8 @@ __device__ __forceinline__ uint32_t outward_before(const SView& S, uint32_t q) {
 }
 
 inline PView pview(const DeviceGraph& g) {
-    return {g.P_t.view(g.tbase), g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs, g.P_dmask, g.P_dpref, nullptr,
-            nullptr, 0};
+    return {g.P_t.view(g.tbase), g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs, g.P_dmask, g.P_dpref,
+            g.P_gmask, g.P_gpref, nullptr, nullptr, nullptr, 0};
 }
 
 // ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------

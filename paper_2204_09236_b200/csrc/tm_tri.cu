@@ -82,11 +82,12 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         }
         if (wk & kPLast) return;
     }
-    // long group: gallop to the group end (first max > b after k), then
-    // binary search the window [k1, k4) and the type boundaries
+    // long group: its end (pair table, group index, or a gallop over P_max),
+    // then binary searches of the window [k1, k4) and the type boundaries
+    if (!known_end && P.gend) known_end = p_group_end(P, kb);
     l = k;
     r = blk_end;
-    for (uint32_t span = 16; !known_end; span <<= 1) {
+    for (uint32_t span = 16; !known_end; span <<= 1) {  // else gallop to the group end
         const uint64_t probe = (uint64_t)l + span;
         if (probe >= r) break;
         if (P.max[probe] > b) {
@@ -99,7 +100,8 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         const uint32_t mid = (l + r) >> 1;
         if (P.max[mid] <= b) l = mid + 1; else r = mid;
     }
-    const uint32_t ke = known_end ? known_end : l;
+    if (!known_end) known_end = l;
+    const uint32_t ke = known_end;
     l = k; r = ke;
     while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] < lo) l = mid + 1; else r = mid; }
     const uint32_t k1 = l;
@@ -280,8 +282,10 @@ __global__ void __launch_bounds__(256, 5) tri_wedge_kernel(PView P, TimeArr FT,
                                                         const uint64_t* __restrict__ wedges,
                                                         uint64_t wedge_cap,
                                                         const unsigned long long* __restrict__ wcount,
-                                                        uint64_t* out, uint64_t* stats) {
+                                                        const unsigned long long* __restrict__ wsum,
+                                                        uint64_t gend_min, uint64_t* out, uint64_t* stats) {
     __shared__ unsigned long long cells[24];
+    if (!P.gend || *wsum < gend_min) P.gend = nullptr;  // group ends not built
     zero_cells(cells, 24);
     __syncthreads();
     WarpCells wc;
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
                                                        const uint32_t* __restrict__ list,
                                                        const uint32_t* __restrict__ lcount,
                                                        const unsigned long long* __restrict__ pt_wsum,
-                                                       uint64_t pt_min_wedges, uint64_t* out,
+                                                       uint64_t pt_min_wedges, uint64_t gend_min, uint64_t* out,
                                                        uint64_t* stats) {
     __shared__ unsigned long long cells[24];
     zero_cells(cells, 24);
@@ -325,6 +329,7 @@ __global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
     const uint32_t cnt = *lcount;
     if (blockIdx.x == 0 && threadIdx.x == 0 && stats) stats[3] = cnt;
     if (!P.pt_keys || *pt_wsum < pt_min_wedges) P.pt_keys = nullptr;  // the table was not built
+    if (!P.gend || *pt_wsum < gend_min) P.gend = nullptr;               // nor the group ends
     uint32_t my_wedges = 0;
     const int lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -422,6 +427,21 @@ __global__ void long_window_sum_kernel(TimeArr FT, const uint32_t* __restrict__ 
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(sum, acc);
 }
 
+// gend[group index] = one past the group's last record, written by that
+// record (only when the long windows are many enough: device-side gate)
+__global__ void group_end_kernel(const uint32_t* __restrict__ P_w, const uint32_t* __restrict__ gmask,
+                                 const uint32_t* __restrict__ gpref, uint64_t m, uint32_t* __restrict__ gend,
+                                 const unsigned long long* __restrict__ wsum, uint64_t min_wedges) {
+    if (*wsum < min_wedges) return;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        if (!(__ldcs(P_w + k) & kPLast)) continue;
+        const uint32_t x = (uint32_t)k;
+        // inclusive count of group starts up to k, minus one
+        gend[gpref[x >> 5] + __popc(gmask[x >> 5] & ((2u << (x & 31)) - 1u)) - 1] = x + 1;
+    }
+}
+
 __device__ __forceinline__ bool pair_table_wanted(const unsigned long long* wsum, uint64_t min_wedges) {
     return *wsum >= min_wedges;
 }
@@ -482,6 +502,12 @@ void tri_filter_stage(const DeviceGraph& g, const Forward& f, int64_t delta, uin
     TM_CUDA(cudaMemsetAsync(lcount, 0, sizeof(uint32_t), st));
     TM_LAUNCH("tri_filter", st, tri_filter_kernel, (unsigned)grid, 256, 0, f.t.view(g.tbase), f.nbr, f.node, delta,
               f_begin, f_end, ts.wedges, ts.wedge_cap, ts.long_list, wcount, lcount);
+    // the long windows' wedge bound gates the group ends (both counting
+    // kernels) and the pair table (long windows) on the device: no host sync
+    ts.wsum = dalloc<unsigned long long>(1, st);
+    TM_CUDA(cudaMemsetAsync(ts.wsum, 0, sizeof(unsigned long long), st));
+    TM_LAUNCH("tri_gate", st, long_window_sum_kernel, (unsigned)cap, 256, 0, f.t.view(g.tbase), f.node, f.off,
+              delta, ts.long_list, lcount, ts.wsum);
     ts.valid = true;
 }
 
@@ -498,6 +524,20 @@ uint64_t pair_table_min_wedges(const DeviceGraph& g) {
     return (env > 0 ? (uint64_t)env : 4ull) * std::max<uint64_t>(g.m, 1024);
 }
 
+// long-window wedges (upper bound) at which the group ends pay for their
+// pass over P: one per 16 edges (config 1 at delta 3600 has 0.003 per edge
+// and would lose ~1 %, at 86400 2.6 per edge and gains 12 %).
+// TM_GROUP_ENDS=0 disables them, 1 builds them always.
+uint64_t group_end_min_wedges(const DeviceGraph& g) {
+    static const long long env = [] {
+        const char* e = std::getenv("TM_GROUP_ENDS");
+        return e ? std::atoll(e) : -1ll;
+    }();
+    if (env == 0) return ~0ull;
+    if (env == 1) return 0;
+    return std::max<uint64_t>(g.m / 16, 1024);
+}
+
 void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_t t_end, uint64_t* d_out,
                     uint64_t* d_stats) {
     if (!ts.valid) return;
@@ -505,38 +545,45 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
     const uint64_t cap = (uint64_t)sm_count() * 8;
     unsigned long long* wcount = reinterpret_cast<unsigned long long*>(ts.wbuf);
     uint32_t* lcount = reinterpret_cast<uint32_t*>(ts.wbuf + 2);
-    TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pview(g), f.t.view(g.tbase), f.nbr, f.ord,
-              ts.delta, t_end, ts.wedges, ts.wedge_cap, wcount, d_out, d_stats);
+    PView pv = pview(g);
+    const uint64_t gend_min = group_end_min_wedges(g);
+    if (gend_min != ~0ull && g.m) {
+        ts.gend = dalloc<uint32_t>(g.m, st);
+        uint64_t grid = (g.m + 255) / 256;
+        if (grid > cap) grid = cap;
+        TM_LAUNCH("group_end", st, group_end_kernel, (unsigned)grid, 256, 0, g.P_w, g.P_gmask, g.P_gpref, g.m,
+                  ts.gend, ts.wsum, gend_min);
+        pv.gend = ts.gend;
+    }
+    TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
+              ts.delta, t_end, ts.wedges, ts.wedge_cap, wcount, ts.wsum, gend_min, d_out, d_stats);
     // pair table for the long windows when they hold many wedges: the
     // table costs ~one random insert per P group, and replaces the block
-    // search of each long-window wedge (decided on the device: no host sync)
-    PView pv = pview(g);
+    // search of each long-window wedge
     const uint64_t min_wedges = pair_table_min_wedges(g);
-    unsigned long long* wsum = nullptr;
     if (min_wedges != ~0ull && g.m) {
         uint64_t pc = 1024;
         while (pc < g.m + g.m / 4) pc <<= 1;
-        ts.pt = dalloc<unsigned long long>(2 * pc + 1, st);
+        ts.pt = dalloc<unsigned long long>(2 * pc, st);
         ts.pt_cap = pc;
-        wsum = ts.pt + 2 * pc;
-        TM_CUDA(cudaMemsetAsync(wsum, 0, sizeof(unsigned long long), st));
-        TM_LAUNCH("pair_table", st, long_window_sum_kernel, (unsigned)cap, 256, 0, f.t.view(g.tbase), f.node, f.off,
-                  ts.delta, ts.long_list, lcount, wsum);
         uint64_t grid = (pc + 255) / 256;
         if (grid > cap) grid = cap;
-        TM_LAUNCH("pair_table", st, pair_table_clear_kernel, (unsigned)grid, 256, 0, ts.pt, pc, wsum, min_wedges);
+        TM_LAUNCH("pair_table", st, pair_table_clear_kernel, (unsigned)grid, 256, 0, ts.pt, pc, ts.wsum,
+                  min_wedges);
         grid = (g.m + 255) / 256;
         if (grid > cap) grid = cap;
         for (int pass = 0; pass < 2; ++pass)
             TM_LAUNCH("pair_table", st, pair_table_insert_kernel, (unsigned)grid, 256, 0, g.P_min, g.P_max, g.P_w,
-                      g.m, ts.pt, ts.pt + pc, pc - 1, wsum, min_wedges, pass);
+                      g.m, ts.pt, ts.pt + pc, pc - 1, ts.wsum, min_wedges, pass);
         pv.pt_keys = ts.pt;
         pv.pt_vals = ts.pt + pc;
         pv.pt_mask = pc - 1;
     }
     TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
-              f.node, f.off, ts.delta, t_end, ts.long_list, lcount, wsum, min_wedges, d_out, d_stats);
+              f.node, f.off, ts.delta, t_end, ts.long_list, lcount, ts.wsum, min_wedges, gend_min, d_out, d_stats);
     dfree(ts.pt, st);
+    dfree(ts.gend, st);
+    dfree(ts.wsum, st);
     dfree(ts.wedges, st);
     dfree(ts.long_list, st);
     dfree(ts.wbuf, st);

@@ -581,10 +581,11 @@ def test_async_pipelined_counts(cuda, tm, oracle):
 
 
 def test_pair_table_paths_agree(cuda, tm, oracle):
-    """The long-window pair table (built when the long windows hold many
-    wedges) against the oracle: the same dense graphs counted with the table
-    forced on for every long window (TM_PAIR_TABLE=1 -> threshold m wedges)
-    and off (TM_PAIR_TABLE=0), including a time slice (first_edge_t_end)."""
+    """The long-window pair table and the P group ends (both built when the
+    long windows hold many wedges) against the oracle: the same dense graphs
+    counted with each forced on (TM_PAIR_TABLE=1 -> threshold m wedges,
+    TM_GROUP_ENDS=1 -> always) and off (=0) in all four combinations,
+    including a time slice (first_edge_t_end)."""
     import json
     import subprocess
     import sys
@@ -606,13 +607,14 @@ print(json.dumps(out))
     import os
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for mode in ("1", "0"):
-        env = dict(os.environ, TM_PAIR_TABLE=mode)
+    for mode in ("11", "00", "10", "01"):
+        env = dict(os.environ, TM_PAIR_TABLE=mode[0], TM_GROUP_ENDS=mode[1])
         r = subprocess.run([sys.executable, "-c", script, root], env=env, capture_output=True, text=True,
                            timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         res[mode] = json.loads(r.stdout.strip().splitlines()[-1])
-    assert res["1"] == res["0"]
+    assert res["11"] == res["00"] == res["10"] == res["01"]
+    res["1"] = res["11"]
     for (n, m, tmax, seed, delta), (census, raw, hi) in zip(
             [(30, 4000, 600, 3, 150), (60, 6000, 3000, 8, 400), (12, 2500, 300, 5, 60)], res["1"]):
         s, d, t = oracle.generate_random_graph(n, m, tmax, seed)
