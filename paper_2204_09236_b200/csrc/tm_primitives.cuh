@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
 constexpr uint64_t kSortPad = 4;
 // sort tile: kSortBlock threads x kSortItems keys (a producer that counts the
 // first digit itself must use the same tiles: digit-major counts[d][tile])
-constexpr int kSortBlock = 256, kSortItems = 8, kSortTile = kSortBlock * kSortItems;
+constexpr int kSortBlock = 256, kSortItems = 12, kSortMinBlocks = 3, kSortTile = kSortBlock * kSortItems;
 
 // one downsweep instantiation: sets its shared-memory limit and caches its
 // occupancy on first use, then launches a persistent grid
@@ -689,9 +689,11 @@ template <typename K>
 void radix_sort(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
                 int bit_lo, int bit_hi, cudaStream_t s, const uint32_t* first_counts = nullptr) {
     if (n <= 1 || bit_hi <= bit_lo) return;
-    // 256 threads x 8 keys, 4 blocks per SM (measured best of the
-    // 256/512-thread, 4-16 keys/thread variants on B200, profiles/sortbench.cu)
-    radix_sort_cfg<K, kSortBlock, kSortItems, 4>(keys, vals, keys_alt, vals_alt, n, bit_lo, bit_hi, s,
+    // 256 threads x 12 keys, 3 blocks per SM: the same downsweep time as 8
+    // keys x 4 blocks with a third fewer tiles, so the count matrix's upsweep
+    // and row scan shrink (profiles/sortbench.cu sweeps 256/512 threads x
+    // 4-16 keys on B200: 20M node keys 0.457 -> 0.448 ms)
+    radix_sort_cfg<K, kSortBlock, kSortItems, kSortMinBlocks>(keys, vals, keys_alt, vals_alt, n, bit_lo, bit_hi, s,
                                                  first_counts);
 }
 

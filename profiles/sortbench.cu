@@ -14,6 +14,7 @@
 
 using namespace tmb;
 
+template <int BLOCK, int ITEMS, int MINB>
 static void run(const char* label, std::vector<uint64_t>& h, int bit_lo, int bit_hi, int reps) {
     const uint64_t n = h.size();
     uint64_t *k0, *k1;
@@ -34,7 +35,7 @@ static void run(const char* label, std::vector<uint64_t>& h, int bit_lo, int bit
         uint64_t* a = k0;
         uint64_t* b = k1;
         cudaEventRecord(e0, s);
-        radix_sort<uint64_t>(a, v0, b, v1, n, bit_lo, bit_hi, s);
+        radix_sort_cfg<uint64_t, BLOCK, ITEMS, MINB>(a, v0, b, v1, n, bit_lo, bit_hi, s, nullptr);
         cudaEventRecord(e1, s);
         cudaEventSynchronize(e1);
         float ms = 0;
@@ -83,7 +84,17 @@ int main(int argc, char** argv) {
     std::vector<uint64_t> node(2 * m), pair(m);
     for (uint64_t r = 0; r < 2 * m; ++r) node[r] = (draw() << 32) | r;
     for (uint64_t p = 0; p < m; ++p) pair[p] = (draw() << 32) | p;
-    run("node keys", node, 32, 32 + nb, 5);
-    run("pair keys", pair, 32, 32 + nb, 5);
+    // tile shapes (BLOCK threads x ITEMS keys, MINB blocks per SM); the product uses 256 x 8, 4
+    run<256, 8, 4>("node keys 256x8/4", node, 32, 32 + nb, 5);
+    run<256, 8, 4>("pair keys 256x8/4", pair, 32, 32 + nb, 5);
+    if (argc > 3) {
+        run<256, 8, 5>("node keys 256x8/5", node, 32, 32 + nb, 5);
+        run<256, 8, 6>("node keys 256x8/6", node, 32, 32 + nb, 5);
+        run<256, 12, 3>("node keys 256x12/3", node, 32, 32 + nb, 5);
+        run<256, 16, 2>("node keys 256x16/2", node, 32, 32 + nb, 5);
+        run<512, 8, 2>("node keys 512x8/2", node, 32, 32 + nb, 5);
+        run<512, 4, 4>("node keys 512x4/4", node, 32, 32 + nb, 5);
+        run<256, 4, 8>("node keys 256x4/8", node, 32, 32 + nb, 5);
+    }
     return 0;
 }
