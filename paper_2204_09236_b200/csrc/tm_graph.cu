@@ -81,7 +81,8 @@ struct EdgeCodec<true> {
 // names the input edge, so the edge records E are indexed by input position
 // (written coalesced here) and S / P read their ordinals straight from the key.
 // One block per radix-sort tile (kSortTile keys = kSortTile / 2 edges): the
-// tile's histogram of the first digit (node & 255) is written digit-major like
+// tile's histogram of the first digit (node & dmask0, the node sort's first
+// digit width: radix_digit_width) is written digit-major like
 // radix_upsweep's, so the node sort skips its first counting pass.
 constexpr int kPackBlock = 256;
 constexpr int kPackEdges = kSortTile / 2;
@@ -103,6 +104,9 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
     constexpr int NW = kPackBlock / 32;
     __shared__ uint32_t hist[NW][256];
     const int w = threadIdx.x >> 5;
+    int nbits = 1;
+    while (nbits < 32 && ((n > 1 ? n - 1 : 1) >> nbits)) ++nbits;
+    const uint32_t dmask0 = (1u << radix_digit_width(nbits, radix_passes(nbits))) - 1u;
     long long lo = LLONG_MAX, hi = LLONG_MIN;
     unsigned bad = 0, uns = 0;
     if (st) tmin = t[0];
@@ -134,8 +138,8 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
                 E[p] = EdgeCodec<kNarrow>::make(tp, ea, eb, tmin);
                 reinterpret_cast<ulonglong2*>(keys)[p] =
                     make_ulonglong2(((uint64_t)a << 32) | (2 * k), ((uint64_t)b << 32) | (2 * k + 1));
-                atomicAdd(&hist[w][a & 255u], 1u);
-                atomicAdd(&hist[w][b & 255u], 1u);
+                atomicAdd(&hist[w][a & dmask0], 1u);
+                atomicAdd(&hist[w][b & dmask0], 1u);
             }
         }
         __syncthreads();
