@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
             }
         }
         __syncthreads();
-        for (int d = threadIdx.x; d < 256; d += kPackBlock) {
+        for (int d = threadIdx.x; d <= (int)dmask0; d += kPackBlock) {
             uint32_t c = 0;
 #pragma unroll
             for (int ww = 0; ww < NW; ++ww) c += hist[ww][d];

@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(BLOCK) radix_upsweep(const K* __restrict__ key
         if (i < n) atomicAdd(&hist[w][(uint32_t)(k[r] >> shift) & dmask], 1u);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < kRadix; d += BLOCK) {
+    for (int d = threadIdx.x; d <= (int)dmask; d += BLOCK) {  // rows of this pass's digits only
         uint32_t s = 0;
 #pragma unroll
         for (int ww = 0; ww < NW; ++ww) s += hist[ww][d];
@@ -517,7 +517,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
         tma_load_1d(stage_keys(s), kin + base, kbytes, &bar[s]);
         if (kVals) tma_load_1d(stage_vals(s), vin + base, vbytes, &bar[s]);
     };
-    const uint32_t dbase = block_exclusive_scan<uint32_t, NW>(tid < kRadix ? totals[tid] : 0u, nullptr);
+    // count rows exist for this pass's digits only (<= dmask)
+    const uint32_t dbase = block_exclusive_scan<uint32_t, NW>(tid <= (int)dmask ? totals[tid] : 0u, nullptr);
     uint32_t tile = blockIdx.x;
     if (tid == 0 && tile < ntiles) issue(tile, 0);
     for (uint32_t it = 0; tile < ntiles; ++it, tile += gridDim.x) {
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
         const uint32_t tile_n = (uint32_t)((n - tbase) < (uint64_t)TILE ? (n - tbase) : (uint64_t)TILE);
         // the tile's digit offsets, loaded now and used after the ranking
         // (keeps the global-load latency off the critical path)
-        const uint32_t toff = tid < kRadix ? __ldg(tile_offsets + (uint64_t)tid * ntiles + tile) : 0u;
+        const uint32_t toff = tid <= (int)dmask ? __ldg(tile_offsets + (uint64_t)tid * ntiles + tile) : 0u;
         mbar_wait(&bar[s], (it >> 1) & 1);
         __syncthreads();
         K* sk = stage_keys(s);
@@ -667,7 +668,7 @@ void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt
             TM_LAUNCH("radix_upsweep", s, (radix_upsweep<K, BLOCK, ITEMS>), ntiles, BLOCK, 0, keys, n, shift,
                       dmask, counts, ntiles);
         }
-        TM_LAUNCH("radix_scan", s, radix_scan_counts, kRadix, 256, 0, cin, ntiles, offs, totals);
+        TM_LAUNCH("radix_scan", s, radix_scan_counts, dmask + 1, 256, 0, cin, ntiles, offs, totals);
         uint32_t* vin = with_vals ? vals : nullptr;
         uint32_t* vout = with_vals ? vals_alt : nullptr;
 #define TM_DOWNSWEEP(V, NB)                                                                                    \
