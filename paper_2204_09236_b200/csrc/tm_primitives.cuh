@@ -387,32 +387,48 @@ __global__ void __launch_bounds__(BLOCK) radix_upsweep(const K* __restrict__ key
     }
 }
 
-// One block per digit d: offs[d][t] = sum_{t' < t} counts[d][t'] (row-local),
-// totals[d] = row sum.  The downsweep adds the exclusive scan of totals.
-static __global__ void __launch_bounds__(256) radix_scan_counts(const uint32_t* __restrict__ counts,
-                                                                uint32_t ntiles,
-                                                                uint32_t* __restrict__ offs,
-                                                                uint32_t* __restrict__ totals) {
+constexpr int kRowBlock = 512, kRowItems = 16, kRowChunk = kRowBlock * kRowItems;
+// offs[d][t] = sum_{t' < t} counts[d][t'] (row-local), totals[d] = row sum;
+// the downsweep adds the exclusive scan of totals.  One block per digit row,
+// kRowChunk counts per step: loaded coalesced into
+// shared memory, each thread scans its 16 contiguous counts, the block scans
+// the thread sums, results go back through shared memory to coalesced stores.
+static __global__ void __launch_bounds__(kRowBlock) radix_scan_counts(const uint32_t* __restrict__ counts,
+                                                                      uint32_t ntiles,
+                                                                      uint32_t* __restrict__ offs,
+                                                                      uint32_t* __restrict__ totals) {
     const uint32_t d = blockIdx.x;
+    __shared__ uint32_t s_row[kRowChunk + kRowChunk / 32];  // +1 word per 32: no bank conflicts
     __shared__ uint32_t s_tot;
+    auto at = [](uint32_t i) { return i + (i >> 5); };
     uint32_t carry = 0;
     const uint32_t* row = counts + (uint64_t)d * ntiles;
     uint32_t* orow = offs + (uint64_t)d * ntiles;
-    for (uint32_t base = 0; base < ntiles; base += 256 * 4) {
-        uint32_t v[4];
+    for (uint32_t base = 0; base < ntiles; base += kRowChunk) {
+#pragma unroll
+        for (int k = 0; k < kRowItems; ++k) {
+            const uint32_t i = k * kRowBlock + threadIdx.x;
+            s_row[at(i)] = base + i < ntiles ? __ldcs(row + base + i) : 0u;
+        }
+        __syncthreads();
+        uint32_t v[kRowItems];
         uint32_t ts = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t i = base + threadIdx.x * 4 + k;
-            v[k] = i < ntiles ? row[i] : 0u;
+        for (int k = 0; k < kRowItems; ++k) {
+            v[k] = s_row[at(threadIdx.x * kRowItems + k)];
             ts += v[k];
         }
-        uint32_t run = block_exclusive_scan<uint32_t, 8>(ts, &s_tot) + carry;
+        uint32_t run = block_exclusive_scan<uint32_t, kRowBlock / 32>(ts, &s_tot) + carry;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t i = base + threadIdx.x * 4 + k;
-            if (i < ntiles) orow[i] = run;
+        for (int k = 0; k < kRowItems; ++k) {
+            s_row[at(threadIdx.x * kRowItems + k)] = run;
             run += v[k];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kRowItems; ++k) {
+            const uint32_t i = k * kRowBlock + threadIdx.x;
+            if (base + i < ntiles) orow[base + i] = s_row[at(i)];
         }
         carry += s_tot;
         __syncthreads();
@@ -668,7 +684,8 @@ void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt
             TM_LAUNCH("radix_upsweep", s, (radix_upsweep<K, BLOCK, ITEMS>), ntiles, BLOCK, 0, keys, n, shift,
                       dmask, counts, ntiles);
         }
-        TM_LAUNCH("radix_scan", s, radix_scan_counts, dmask + 1, 256, 0, cin, ntiles, offs, totals);
+        TM_LAUNCH("radix_scan", s, radix_scan_counts, dmask + 1, kRowBlock, 0, cin, ntiles,
+                  offs, totals);
         uint32_t* vin = with_vals ? vals : nullptr;
         uint32_t* vout = with_vals ? vals_alt : nullptr;
 #define TM_DOWNSWEEP(V, NB)                                                                                    \
