@@ -245,16 +245,6 @@ __global__ void __launch_bounds__(kScanBlock) scan_chunk_reduce(Load load, uint6
 }
 
 template <typename T>
-__global__ void __launch_bounds__(1024) scan_partials(T* partials, uint32_t g) {
-    // g <= 1024: one element per thread, exclusive in place, total at [g]
-    T v = threadIdx.x < g ? partials[threadIdx.x] : T(0);
-    __shared__ T total;
-    T ex = block_exclusive_scan<T, 32>(v, &total);
-    if (threadIdx.x < g) partials[threadIdx.x] = ex;
-    if (threadIdx.x == 0) partials[g] = total;
-}
-
-template <typename T>
 struct ArrayStore {
     T* p;
     __device__ __forceinline__ void operator()(uint64_t i, T v) const { p[i] = v; }
@@ -267,7 +257,19 @@ __global__ void __launch_bounds__(kScanBlock) scan_chunk_down(Load load, uint64_
     __shared__ T s_tot;
     const uint64_t b0 = (uint64_t)blockIdx.x * chunk;
     const uint64_t b1 = b0 + chunk < n ? b0 + chunk : n;
-    T carry = partials[blockIdx.x];
+    // this chunk's offset: the sum of the chunk totals before it (<= 1024 of
+    // them, reduced in-block instead of a separate scan launch)
+    T carry = 0;
+    {
+        T p = 0;
+        for (uint32_t c = threadIdx.x; c < blockIdx.x; c += kScanBlock) p += partials[c];
+        p = warp_sum(p);
+        __shared__ T ws[kScanBlock / 32];
+        if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = p;
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < kScanBlock / 32; ++w) carry += ws[w];
+    }
     for (uint64_t base = b0; base < b1; base += kScanTile) {
         {
             T x[kScanItems];
@@ -319,10 +321,9 @@ void exclusive_scan_to(Load load, uint64_t n, Store out, cudaStream_t s) {
     uint64_t chunk = (n + g - 1) / g;
     chunk = (chunk + kScanTile - 1) / kScanTile * kScanTile;
     g = (n + chunk - 1) / chunk;
-    T* partials = dalloc<T>(g + 1, s);
+    T* partials = dalloc<T>(g, s);
     TM_LAUNCH("scan", s, (scan_chunk_reduce<T, Load>), (unsigned)g, kScanBlock, 0, load, n, chunk,
               partials);
-    TM_LAUNCH("scan", s, scan_partials<T>, 1, 1024, 0, partials, (uint32_t)g);
     TM_LAUNCH("scan", s, (scan_chunk_down<T, Load, Store>), (unsigned)g, kScanBlock, 0, load, n, chunk,
               partials, out);
     dfree(partials, s);
