@@ -85,8 +85,8 @@ int main(int argc, char** argv) {
     for (uint64_t r = 0; r < 2 * m; ++r) node[r] = (draw() << 32) | r;
     for (uint64_t p = 0; p < m; ++p) pair[p] = (draw() << 32) | p;
     // tile shapes (BLOCK threads x ITEMS keys, MINB blocks per SM); the product uses 256 x 8, 4
-    run<256, 8, 4>("node keys 256x8/4", node, 32, 32 + nb, 5);
-    run<256, 8, 4>("pair keys 256x8/4", pair, 32, 32 + nb, 5);
+    run<kSortBlock, kSortItems, kSortMinBlocks>("node keys (product tiles)", node, 32, 32 + nb, 5);
+    run<kSortBlock, kSortItems, kSortMinBlocks>("pair keys (product tiles)", pair, 32, 32 + nb, 5);
     if (argc > 3) {
         run<256, 8, 5>("node keys 256x8/5", node, 32, 32 + nb, 5);
         run<256, 8, 6>("node keys 256x8/6", node, 32, 32 + nb, 5);
