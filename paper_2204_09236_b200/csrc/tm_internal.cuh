@@ -155,6 +155,7 @@ struct TriStage {
     uint64_t pt_cap = 0;
     unsigned long long* wsum = nullptr;  // long-window wedge bound (device)
     uint32_t* gend = nullptr;           // P group ends, built when the long windows are many
+    unsigned long long* queue = nullptr;  // work queues of tri_wedge / tri_long
 };
 // what a one-shot count will run, known while the index is being built
 struct RunHint {

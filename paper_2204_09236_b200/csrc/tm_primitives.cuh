@@ -101,6 +101,16 @@ __device__ __forceinline__ void block_reserve2(uint32_t a, uint32_t b, CA* ca, u
     ob = s_base_b + (ex >> 16);
 }
 
+// Dynamic work queue: the warp's next `n` items (lane 0 takes them, all
+// lanes get the base).  Work kernels with heavy-tailed items (hub windows,
+// long same-neighbour walks) pull chunks instead of striding a fixed share,
+// so no warp idles while another still holds a long tail.
+__device__ __forceinline__ unsigned long long warp_take(unsigned long long* queue, unsigned n) {
+    unsigned long long b = 0;
+    if ((threadIdx.x & 31) == 0) b = atomicAdd(queue, (unsigned long long)n);
+    return __shfl_sync(0xffffffffu, b, 0);
+}
+
 // warp-aggregated append of `value` to list when pred holds (whole warp calls)
 __device__ __forceinline__ void warp_append(bool pred, uint32_t value, uint32_t* list,
                                             uint32_t* counter) {

@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(256, 5) star_work_kernel(SView S, PView P, int
                                                         const uint32_t* __restrict__ first_list,
                                                         const uint32_t* __restrict__ third_list,
                                                         const uint32_t* __restrict__ counters,
+                                                        unsigned long long* __restrict__ queue,
                                                         uint64_t* __restrict__ out,
                                                         uint64_t* __restrict__ stats) {
     __shared__ unsigned long long cells[32];
@@ -312,23 +313,30 @@ __global__ void __launch_bounds__(256, 5) star_work_kernel(SView S, PView P, int
     __syncthreads();
     const SmemSink acc{cells};
     const uint32_t nf = counters[0], nt = counters[1];
-    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (uint64_t)nf + nt;
-         idx += (uint64_t)gridDim.x * blockDim.x) {
-        const bool first = idx < nf;
-        const uint32_t e = first ? first_list[idx] : third_list[idx - nf];
-        const uint32_t k = e >> 1, side = e & 1u;
-        const uint32_t u = side ? P.max[k] : P.min[k];
-        const uint32_t start = S.off[u], end = S.off[u + 1];
-        const int64_t tk = P.t[k];
-        if (first && tk >= t_end) continue;  // instance's first edge outside the time slice
-        const uint32_t q = bsearch_locate(S, start, end, tk, P.ord[k]);
-        if (first) {
-            first_role(S, P, q, k, side, start, end, delta, acc);
-        } else {
-            // first edges restricted to t < t_end: a prefix of S_u
-            const uint32_t re = t_end == INT64_MAX ? end - start
-                                                   : gallop_upper(S.t, start, end, t_end - 1) - start;
-            third_role(S, P, q, k, side, start, delta, 0u, re, acc);
+    const uint64_t total = (uint64_t)nf + nt;
+    for (;;) {  // 32 items per warp from the queue (hub items are heavy-tailed)
+        const uint64_t base = warp_take(queue, 32);
+        if (base >= total) break;
+        const uint64_t idx = base + (threadIdx.x & 31);
+        // no early continue: the warp reconverges at the next warp_take
+        if (idx < total) {
+            const bool first = idx < nf;
+            const uint32_t e = first ? first_list[idx] : third_list[idx - nf];
+            const uint32_t k = e >> 1, side = e & 1u;
+            const uint32_t u = side ? P.max[k] : P.min[k];
+            const uint32_t start = S.off[u], end = S.off[u + 1];
+            const int64_t tk = P.t[k];
+            if (!(first && tk >= t_end)) {  // else: the instance's first edge is outside the time slice
+                const uint32_t q = bsearch_locate(S, start, end, tk, P.ord[k]);
+                if (first) {
+                    first_role(S, P, q, k, side, start, end, delta, acc);
+                } else {
+                    // first edges restricted to t < t_end: a prefix of S_u
+                    const uint32_t re = t_end == INT64_MAX ? end - start
+                                                           : gallop_upper(S.t, start, end, t_end - 1) - start;
+                    third_role(S, P, q, k, side, start, delta, 0u, re, acc);
+                }
+            }
         }
     }
     __syncthreads();
@@ -386,14 +394,15 @@ void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c
     uint64_t grid = (g.m + 256 * kFilterItems - 1) / (256 * kFilterItems);
     if (grid > cap) grid = cap;
     const uint64_t work = 2 * g.m;
-    uint32_t* lists = dalloc<uint32_t>(2 * work + 2, st);
-    uint32_t* counters = lists + 2 * work;
-    TM_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), st));
+    uint32_t* lists = dalloc<uint32_t>(2 * work + 4, st);
+    uint32_t* counters = lists + 2 * work;  // 2 list fills, then (8-byte aligned) the work queue
+    unsigned long long* queue = reinterpret_cast<unsigned long long*>(lists + 2 * work + 2);
+    TM_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(uint32_t), st));
     TM_LAUNCH("star_filter", st, star_filter_kernel, (unsigned)grid, 256, 0, pview(g), delta, g.m,
               c_begin, c_end, lists, lists + work, counters);
     TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), delta, t_end,
               lists,
-              lists + work, counters, d_out, d_stats);
+              lists + work, counters, queue, d_out, d_stats);
     dfree(lists, st);
 }
 

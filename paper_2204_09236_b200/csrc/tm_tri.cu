@@ -283,7 +283,8 @@ __global__ void __launch_bounds__(256, 5) tri_wedge_kernel(PView P, TimeArr FT,
                                                         uint64_t wedge_cap,
                                                         const unsigned long long* __restrict__ wcount,
                                                         const unsigned long long* __restrict__ wsum,
-                                                        uint64_t gend_min, uint64_t* out, uint64_t* stats) {
+                                                        uint64_t gend_min, unsigned long long* queue,
+                                                        uint64_t* out, uint64_t* stats) {
     __shared__ unsigned long long cells[24];
     if (!P.gend || *wsum < gend_min) P.gend = nullptr;  // group ends not built
     zero_cells(cells, 24);
@@ -292,9 +293,10 @@ __global__ void __launch_bounds__(256, 5) tri_wedge_kernel(PView P, TimeArr FT,
     uint64_t cnt = wcount[0] < wedge_cap ? wcount[0] : wedge_cap;
     if (wcount[1] < cnt) cnt = wcount[1];
     if (blockIdx.x == 0 && threadIdx.x == 0 && stats) stats[2] = cnt;
-    // warp-uniform trip count (the cells are reduced across the warp)
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < cnt;
-         base += (uint64_t)gridDim.x * blockDim.x) {
+    // 32 wedges per warp from the queue (warp-uniform: the cells are reduced across the warp)
+    for (;;) {
+        const uint64_t base = warp_take(queue, 32);
+        if (base >= cnt) break;
         const uint64_t idx = base + (threadIdx.x & 31);
         uint32_t c[6] = {0, 0, 0, 0, 0, 0};
         int cb = 0;
@@ -320,7 +322,8 @@ __global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
                                                        const uint32_t* __restrict__ list,
                                                        const uint32_t* __restrict__ lcount,
                                                        const unsigned long long* __restrict__ pt_wsum,
-                                                       uint64_t pt_min_wedges, uint64_t gend_min, uint64_t* out,
+                                                       uint64_t pt_min_wedges, uint64_t gend_min,
+                                                       unsigned long long* queue, uint64_t* out,
                                                        uint64_t* stats) {
     __shared__ unsigned long long cells[24];
     zero_cells(cells, 24);
@@ -332,9 +335,9 @@ __global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
     if (!P.gend || *pt_wsum < gend_min) P.gend = nullptr;               // nor the group ends
     uint32_t my_wedges = 0;
     const int lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t idx = warp; idx < cnt; idx += nwarps) {
+    for (;;) {  // one first edge per warp from the queue
+        const uint64_t idx = warp_take(queue, 1);
+        if (idx >= cnt) break;
         const uint32_t i = list[idx];
         const uint32_t end = Foff[Fnode[i] + 1];
         const uint32_t v = FN[i] & kNodeMask;
@@ -545,6 +548,8 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
     const uint64_t cap = (uint64_t)sm_count() * 8;
     unsigned long long* wcount = reinterpret_cast<unsigned long long*>(ts.wbuf);
     uint32_t* lcount = reinterpret_cast<uint32_t*>(ts.wbuf + 2);
+    ts.queue = dalloc<unsigned long long>(2, st);
+    TM_CUDA(cudaMemsetAsync(ts.queue, 0, 2 * sizeof(unsigned long long), st));
     PView pv = pview(g);
     const uint64_t gend_min = group_end_min_wedges(g);
     if (gend_min != ~0ull && g.m) {
@@ -556,7 +561,7 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
         pv.gend = ts.gend;
     }
     TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
-              ts.delta, t_end, ts.wedges, ts.wedge_cap, wcount, ts.wsum, gend_min, d_out, d_stats);
+              ts.delta, t_end, ts.wedges, ts.wedge_cap, wcount, ts.wsum, gend_min, ts.queue, d_out, d_stats);
     // pair table for the long windows when they hold many wedges: the
     // table costs ~one random insert per P group, and replaces the block
     // search of each long-window wedge
@@ -580,9 +585,11 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
         pv.pt_mask = pc - 1;
     }
     TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
-              f.node, f.off, ts.delta, t_end, ts.long_list, lcount, ts.wsum, min_wedges, gend_min, d_out, d_stats);
+              f.node, f.off, ts.delta, t_end, ts.long_list, lcount, ts.wsum, min_wedges, gend_min, ts.queue + 1, d_out,
+              d_stats);
     dfree(ts.pt, st);
     dfree(ts.gend, st);
+    dfree(ts.queue, st);
     dfree(ts.wsum, st);
     dfree(ts.wedges, st);
     dfree(ts.long_list, st);
