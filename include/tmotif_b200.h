@@ -13,8 +13,14 @@
  *   census[36] in lexicographic signature order      (motifs.hpp:159-161)
  * with Direction outward = 0, inward = 1 (types.hpp:15).
  *
- * Error codes mirror the reference CLI's exit codes (tmotif_main.cpp:20-30)
- * so that a binding can map them 1:1 onto the reference's exception types.
+ * Error codes: 2 / 3 / 4 are the reference CLI's exit codes for the same
+ * exception (exit_parse, exit_overflow, exit_config; tmotif_main.cpp:20-30,
+ * 283-294).  The CLI folds std::invalid_argument and ConsistencyError (a
+ * std::logic_error) into exit_usage = 1 through its std::exception catch; the
+ * C-ABI keeps them apart (1 and 10) so a binding raises the precise type.
+ * Codes 5-7 are the CLI's exit_too_large / exit_mismatch /
+ * exit_nondeterministic (oracle, verify and bench subcommands, not on this
+ * path) and are never returned; 8+ are this library's own.
  */
 #ifndef TMOTIF_B200_H
 #define TMOTIF_B200_H
@@ -28,9 +34,11 @@ extern "C" {
 #define TM_OK 0
 #define TM_ERR_INVALID 1     /* std::invalid_argument (graph.cpp:20,29,32)      */
 #define TM_ERR_PARSE 2       /* ParseError (types.hpp:35), CLI exit_parse        */
-#define TM_ERR_OVERFLOW 3    /* CounterOverflowError (types.hpp:50)             */
+#define TM_ERR_OVERFLOW 3    /* CounterOverflowError (types.hpp:50): any counter
+                                cell, class sum or census cell above 2^64 - 1
+                                (cells are summed exactly on the device)      */
 #define TM_ERR_CONFIG 4      /* ConfigError (types.hpp:46, executor.cpp:151-156)  */
-#define TM_ERR_CONSISTENCY 5 /* ConsistencyError (types.hpp:55, motifs.cpp:254) */
+#define TM_ERR_CONSISTENCY 10 /* ConsistencyError (types.hpp:55, motifs.cpp:254)  */
 #define TM_ERR_CUDA 8        /* no device / CUDA failure: the path never falls back */
 #define TM_ERR_LIMIT 9       /* graph exceeds the 32-bit position layout         */
 
@@ -55,7 +63,9 @@ typedef struct tm_run_config {
     uint32_t workers;          /* kept for the removal-mode check only            */
     int64_t degree_threshold;  /* < 0: auto top-20 rule (executor.cpp:15)          */
     int32_t triangle_mode;     /* TM_TRI_COUNT_ALL | TM_TRI_REMOVAL                */
-    uint32_t motifs;           /* TM_MOTIF_* bit set; 0 means all                   */
+    uint32_t motifs;           /* TM_MOTIF_* bit set (MotifFilter); 0 = the empty
+                                  filter: nothing runs, the census is all zero
+                                  (executor.cpp:28-29)                             */
     uint64_t shard_target;     /* accepted for API parity; semantics-free           */
     uint32_t center_begin;     /* center partition [begin, end); end == 0: all      */
     uint32_t center_end;
@@ -67,8 +77,10 @@ typedef struct tm_run_config {
     int64_t first_edge_t_end;
 } tm_run_config;
 
-/* PhaseTimings (executor.hpp:55-65); device-event times in ms. */
+/* PhaseTimings (executor.hpp:55-65); device-event times in ms.  ingest_ms is
+ * the host->device copy of the edge arrays (0 for device pointers). */
 typedef struct tm_phase_timings {
+    double ingest_ms;
     double index_ms;
     double star_pair_ms;
     double triangle_ms;
@@ -203,6 +215,10 @@ int tm_generate_random_graph(uint64_t nodes, uint64_t m, int64_t t_max, uint64_t
  * [3] long-window first edges, [4] long-window wedges, [5..7] reserved. */
 int tm_run_stats(const tm_graph* g, uint64_t* out8);
 const char* tm_last_error(void);
+/* Test hook (this host thread, eager runs): every raw star/pair accumulator
+ * cell starts at `bias` instead of 0, so Pair = bias + count while Star is
+ * unchanged -- exercises the exact 2^64 overflow detection.  0 = off. */
+void tm_debug_acc_bias(uint64_t bias);
 /* Number of this library's kernels launched since load. */
 uint64_t tm_kernel_launches(void);
 /* Per-kernel CUDA-event timing on the launching stream. */

@@ -7,8 +7,10 @@
 // exception types (ConfigError, CounterOverflowError, ConsistencyError).
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
+#include <limits>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -29,6 +31,7 @@ struct CounterOverflowError : std::runtime_error {
     CounterOverflowError() : std::runtime_error("motif counter overflow") {}
 };
 struct ConsistencyError : std::logic_error { using std::logic_error::logic_error; };
+struct ClassificationError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
 // types.hpp:35-44: "line N: what", line() = N
 struct ParseError : std::runtime_error {
@@ -57,26 +60,63 @@ struct PairCounter { std::array<std::uint64_t, 8> cells{}; };
 struct TriCounter { std::array<std::uint64_t, 24> cells{}; };
 struct CenterStarResult { StarCounter star; PairCounter pair; };
 
-// MotifCensus over the 36 signatures in lexicographic order (motifs.hpp:168).
-struct MotifCensus {
-    std::array<std::uint64_t, 36> counts{};
-    Timestamp delta = 0;
-    std::uint64_t count_at(std::size_t k) const { return counts[k]; }
-    std::uint64_t total() const {
-        std::uint64_t s = 0;
-        for (auto c : counts) s += c;
-        return s;
-    }
-    bool same_counts(const MotifCensus& o) const { return counts == o.counts; }
-};
-
 inline std::string signature(int idx) {
     char buf[9];
     check(tm_signature(idx, buf));
     return buf;
 }
 
-struct MotifFilter { bool star = true, pair = true, triangle = true; };
+// signature_index (motifs.hpp:164): position of "sd|sd|sd" in all_signatures()
+inline std::optional<std::size_t> signature_index(const std::string& sig) {
+    for (int k = 0; k < 36; ++k)
+        if (signature(k) == sig) return static_cast<std::size_t>(k);
+    return std::nullopt;
+}
+
+// CensusMeta (motifs.hpp:172-177)
+struct CensusMeta {
+    std::string input;
+    std::size_t edge_count = 0;
+    std::string triangle_mode;
+    unsigned workers = 0;
+};
+
+// MotifCensus over the 36 signatures in lexicographic order (motifs.hpp:179-201).
+struct MotifCensus {
+    std::array<std::uint64_t, 36> counts{};
+    Timestamp delta = 0;
+    CensusMeta meta;
+    std::uint64_t count_at(std::size_t k) const { return counts[k]; }
+    // count(sig) (motifs.cpp:221-225): ClassificationError for an unknown signature
+    std::uint64_t count(const std::string& sig) const {
+        const auto k = signature_index(sig);
+        if (!k) throw ClassificationError("unknown signature: " + sig);
+        return counts[*k];
+    }
+    // total() (motifs.cpp:239-243): checked sum
+    std::uint64_t total() const {
+        std::uint64_t s = 0;
+        for (auto c : counts) {
+            if (s > std::numeric_limits<std::uint64_t>::max() - c) throw CounterOverflowError();
+            s += c;
+        }
+        return s;
+    }
+    bool same_counts(const MotifCensus& o) const { return counts == o.counts; }
+};
+
+struct MotifFilter {
+    bool star = true, pair = true, triangle = true;
+    bool any_star_pair() const { return star || pair; }
+};
+
+// PhaseTimings (executor.hpp:55-65); ingest_ms = host->device copy of the edges
+struct PhaseTimings {
+    double ingest_ms = 0, index_ms = 0, star_pair_ms = 0, triangle_ms = 0, merge_ms = 0;
+    double total_ms() const { return ingest_ms + index_ms + star_pair_ms + triangle_ms + merge_ms; }
+};
+
+inline const char* triangle_mode_name(TriangleMode m) { return m == TriangleMode::count_all ? "countall" : "removal"; }
 
 // RunConfig (executor.hpp:36-46).
 struct RunConfig {
@@ -196,6 +236,64 @@ inline std::size_t auto_degree_threshold(const GraphContext& ctx) {
     return v;
 }
 
+// TemporalGraph::degrees (graph.cpp:52-59)
+inline std::vector<std::size_t> degrees(const GraphContext& ctx) {
+    std::vector<std::uint64_t> d(ctx.node_count());
+    if (!d.empty()) check(tm_graph_degrees(ctx.handle(), d.data()));
+    return {d.begin(), d.end()};
+}
+
+// IndexRange / full_star_range / full_triangle_range (types.hpp:25-33,
+// star_engine.hpp:36-38, triangle_engine.hpp:27-29)
+struct IndexRange {
+    std::size_t begin = 0, end = 0;
+    std::size_t size() const { return end > begin ? end - begin : 0; }
+    bool empty() const { return end <= begin; }
+    bool operator==(const IndexRange& o) const { return begin == o.begin && end == o.end; }
+};
+inline IndexRange full_star_range(std::size_t s) { return {0, s >= 3 ? s - 2 : 0}; }
+inline IndexRange full_triangle_range(std::size_t s) { return {0, s >= 2 ? s - 1 : 0}; }
+
+// SchedulePlan / plan_schedule (executor.hpp:20-33, executor.cpp:23-52): the
+// reference's CPU work plan, for callers that drive the per-center API
+// (count_*_at_center) themselves.  The device passes do not need it: they
+// parallelise over records / wedges, and route the long windows of every
+// node, heavy or not, to the cooperative path.
+struct SchedulePlan {
+    struct HeavyNode {
+        NodeId node;
+        std::vector<IndexRange> shards;
+    };
+    std::vector<HeavyNode> heavy;
+    std::vector<NodeId> light;
+    std::size_t thr_d = 0;
+    std::size_t shard_target = 0;
+    bool run_star_pair = true;
+    bool run_triangle = true;
+};
+inline SchedulePlan plan_schedule(const GraphContext& ctx, std::size_t thr_d, std::size_t shard_target,
+                                  const MotifFilter& motifs) {
+    if (shard_target < 1) throw ConfigError("shard_target must be >= 1");
+    SchedulePlan plan;
+    plan.thr_d = thr_d;
+    plan.shard_target = shard_target;
+    plan.run_star_pair = motifs.any_star_pair();
+    plan.run_triangle = motifs.triangle;
+    const auto deg = degrees(ctx);
+    for (NodeId u = 0; u < deg.size(); ++u) {
+        if (deg[u] > thr_d) {
+            SchedulePlan::HeavyNode h{u, {}};
+            const IndexRange full = full_star_range(deg[u]);
+            for (std::size_t b = full.begin; b < full.end; b += shard_target)
+                h.shards.push_back({b, std::min(b + shard_target, full.end)});
+            plan.heavy.push_back(std::move(h));
+        } else {
+            plan.light.push_back(u);
+        }
+    }
+    return plan;
+}
+
 inline tm_run_config to_c(const RunConfig& c, std::uint32_t cb = 0, std::uint32_t ce = 0) {
     tm_run_config r{};
     r.delta = c.delta;
@@ -212,15 +310,49 @@ inline tm_run_config to_c(const RunConfig& c, std::uint32_t cb = 0, std::uint32_
     return r;
 }
 
-// run_parallel (executor.cpp:149-215).
+// run_parallel (executor.cpp:149-215).  An empty motif filter yields the
+// all-zero census, as in the reference.
 inline MotifCensus run_parallel(const GraphContext& ctx, const RunConfig& config,
-                                tm_phase_timings* timings = nullptr) {
-    if (!config.motifs.star && !config.motifs.pair && !config.motifs.triangle)
-        throw std::invalid_argument("empty motif filter");
+                                PhaseTimings* timings = nullptr) {
     const tm_run_config c = to_c(config);
     MotifCensus out;
-    check(tm_run_parallel(ctx.handle(), &c, nullptr, out.counts.data(), timings));
+    tm_phase_timings t{};
+    check(tm_run_parallel(ctx.handle(), &c, nullptr, out.counts.data(), timings ? &t : nullptr));
+    if (timings) {
+        timings->star_pair_ms = t.star_pair_ms;
+        timings->triangle_ms = t.triangle_ms;
+        timings->merge_ms = t.merge_ms;
+    }
     out.delta = config.delta;
+    out.meta.edge_count = ctx.edge_count();
+    out.meta.triangle_mode = triangle_mode_name(config.triangle_mode);
+    out.meta.workers = config.workers;
+    return out;
+}
+
+// The whole pipeline for one batch of ingestion-order HOST edges (the
+// reference's TemporalGraph::build + GraphContext::build + run_parallel):
+// copy-in (ingest_ms), index build (index_ms), both passes and the merge.
+inline MotifCensus count_edges(const std::vector<NodeId>& src, const std::vector<NodeId>& dst,
+                               const std::vector<Timestamp>& t, std::size_t node_count, const RunConfig& config,
+                               PhaseTimings* timings = nullptr) {
+    if (src.size() != dst.size() || src.size() != t.size()) throw std::invalid_argument("edge arrays differ in length");
+    const tm_run_config c = to_c(config);
+    MotifCensus out;
+    tm_phase_timings tt{};
+    check(tm_count_edges(src.data(), dst.data(), t.data(), src.size(), node_count, 0, nullptr, &c, nullptr,
+                         out.counts.data(), timings ? &tt : nullptr));
+    if (timings) {
+        timings->ingest_ms = tt.ingest_ms;
+        timings->index_ms = tt.index_ms;
+        timings->star_pair_ms = tt.star_pair_ms;
+        timings->triangle_ms = tt.triangle_ms;
+        timings->merge_ms = tt.merge_ms;
+    }
+    out.delta = config.delta;
+    out.meta.edge_count = src.size();
+    out.meta.triangle_mode = triangle_mode_name(config.triangle_mode);
+    out.meta.workers = config.workers;
     return out;
 }
 

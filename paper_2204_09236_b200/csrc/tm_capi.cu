@@ -203,32 +203,48 @@ int merge_census_impl(const uint64_t* star, const uint64_t* pair, const uint64_t
     return TM_OK;
 }
 
-// raw star sums (Pair, C, B, A) -> reference Star / Pair cells
-void finish_star(const uint64_t* raw, uint64_t* star, uint64_t* pair) {
+// A device cell is exact to 128 bits: its u64 sum plus the number of times
+// the sum wrapped (tm_primitives.cuh cell_add).  A reference cell that would
+// exceed 2^64 - 1 throws CounterOverflowError (checked_increment,
+// types.hpp:65-70, via motifs.cpp:131-147 and the merges in executor.cpp:173-179).
+using u128 = unsigned __int128;
+inline u128 wide(uint64_t lo, uint64_t wraps) { return ((u128)wraps << 64) | lo; }
+inline uint64_t narrow_checked(u128 v) {
+    if (v >> 64) throw tm_error(TM_ERR_OVERFLOW, "motif counter overflow");
+    return (uint64_t)v;
+}
+
+// raw star sums (Pair, C, B, A) -> reference Star / Pair cells; wraps: the
+// raw cells' wrap counters (nullptr: none)
+void finish_star(const uint64_t* raw, uint64_t* star, uint64_t* pair, const uint64_t* wraps = nullptr) {
+    auto at = [&](int i) { return wide(raw[i], wraps ? wraps[i] : 0); };
     for (int c = 0; c < 8; ++c) {
-        const uint64_t p = raw[c];
-        if (pair) pair[c] = p;
+        const u128 p = at(c);
+        if (pair) pair[c] = narrow_checked(p);
         if (star) {
-            star[0 * 8 + c] = raw[8 + c] - p;   // isolated_first  = C - Pair
-            star[1 * 8 + c] = raw[16 + c] - p;  // isolated_second = B - Pair
-            star[2 * 8 + c] = raw[24 + c] - p;  // isolated_third  = A - Pair
+            star[0 * 8 + c] = narrow_checked(at(8 + c) - p);   // isolated_first  = C - Pair
+            star[1 * 8 + c] = narrow_checked(at(16 + c) - p);  // isolated_second = B - Pair
+            star[2 * 8 + c] = narrow_checked(at(24 + c) - p);  // isolated_third  = A - Pair
         }
     }
 }
 
 // once-counted cells -> count_all cells: every instance lands once in each
 // cell of its class (triangle_engine.hpp:57-60)
-void expand_count_all(const uint64_t* once, uint64_t* tri) {
+void expand_count_all(const uint64_t* once, uint64_t* tri, const uint64_t* wraps = nullptr) {
     const Universe& u = universe();
-    uint64_t cls[36] = {0};
-    for (int c = 0; c < 24; ++c) cls[u.tri_sig[c]] += once[c];
-    for (int c = 0; c < 24; ++c) tri[c] = cls[u.tri_sig[c]];
+    u128 cls[36] = {0};
+    for (int c = 0; c < 24; ++c) cls[u.tri_sig[c]] += wide(once[c], wraps ? wraps[c] : 0);
+    for (int c = 0; c < 24; ++c) tri[c] = narrow_checked(cls[u.tri_sig[c]]);
+}
+void copy_tri_checked(const uint64_t* once, uint64_t* tri, const uint64_t* wraps) {
+    for (int c = 0; c < 24; ++c) tri[c] = narrow_checked(wide(once[c], wraps ? wraps[c] : 0));
 }
 
 struct PinnedAcc {
     uint64_t* h = nullptr;
     PinnedAcc() {
-        if (cudaMallocHost(&h, 64 * sizeof(uint64_t)) != cudaSuccess) h = nullptr;
+        if (cudaMallocHost(&h, kAccWords * sizeof(uint64_t)) != cudaSuccess) h = nullptr;
     }
 };
 // replayed graphs copy their counters into their own entry's pinned buffer
@@ -283,10 +299,17 @@ uint32_t read_u32(const uint32_t* d, uint64_t idx, cudaStream_t s) {
     return v;
 }
 
-// one counting pass into the 64-entry device accumulator; returns raw on host
+// test hook: every star raw cell starts at this value instead of 0 (Star =
+// raw - Pair is unchanged, Pair = bias + count), so the device wrap counters
+// and the host's overflow check can be exercised at the 2^64 boundary
+thread_local uint64_t g_acc_bias = 0;
+
+// one counting pass into the device accumulator; returns raw on host
 struct PassResult {
     uint64_t star_raw[32];
     uint64_t tri_once[24];
+    uint64_t star_wraps[32];
+    uint64_t tri_wraps[24];
 };
 
 // host side of a pass: wait for the counter copy (the whole stream, or just
@@ -298,14 +321,22 @@ void collect_passes(tm_graph* G, PassResult& r, cudaEvent_t done = nullptr) {
     std::memcpy(r.star_raw, h, 32 * sizeof(uint64_t));
     std::memcpy(r.tri_once, h + 32, 24 * sizeof(uint64_t));
     std::memcpy(G->g.stats, h + 56, 8 * sizeof(uint64_t));
+    std::memcpy(r.star_wraps, h + kAccCarry, 32 * sizeof(uint64_t));
+    std::memcpy(r.tri_wraps, h + kAccCarry + 32, 24 * sizeof(uint64_t));
 }
 
 void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do_tri, int tri_mode,
                 uint32_t cb, uint32_t ce, PassResult& r, tm_phase_timings* tm, bool collect = true) {
     DeviceGraph& g = G->g;
     cudaStream_t s = g.stream;
-    if (!g.d_acc) g.d_acc = dalloc<uint64_t>(64, s);
-    TM_CUDA(cudaMemsetAsync(g.d_acc, 0, 64 * sizeof(uint64_t), s));
+    if (!g.d_acc) g.d_acc = dalloc<uint64_t>(kAccWords, s);
+    TM_CUDA(cudaMemsetAsync(g.d_acc, 0, kAccWords * sizeof(uint64_t), s));
+    if (g_acc_bias && collect) {  // test hook (tm_debug_acc_bias): start the 32 star raw cells at the bias
+        static thread_local uint64_t bias[32];
+        for (auto& b : bias) b = g_acc_bias;
+        TM_CUDA(cudaMemcpyAsync(g.d_acc, bias, sizeof(bias), cudaMemcpyHostToDevice, s));
+        TM_CUDA(cudaStreamSynchronize(s));
+    }
     const bool full = (cb == 0 && ce == g.n);
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
     if (tm) {
@@ -344,7 +375,7 @@ void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do
     }
     if (tm) TM_CUDA(cudaEventRecord(e2, s));
     uint64_t* h = pinned_acc();
-    TM_CUDA(cudaMemcpyAsync(h, g.d_acc, 64 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    TM_CUDA(cudaMemcpyAsync(h, g.d_acc, kAccWords * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     if (!collect) return;  // (graph capture: the caller launches, synchronises and collects)
     collect_passes(G, r);
     if (tm) {
@@ -372,12 +403,17 @@ void check_config(const tm_run_config* cfg) {
 // raw pass sums -> the reference's counters (+ census for full runs)
 void finish_counts(const PassResult& r, const tm_run_config* cfg, bool full, tm_counters* raw,
                    uint64_t* census, tm_phase_timings* tm) {
-    const uint32_t motifs = cfg->motifs ? cfg->motifs : 7u;
+    const uint32_t motifs = cfg->motifs;
     tm_counters out;
     std::memset(&out, 0, sizeof(out));
-    finish_star(r.star_raw, out.star, out.pair);
-    if (cfg->triangle_mode == TM_TRI_COUNT_ALL) expand_count_all(r.tri_once, out.tri);
-    else std::memcpy(out.tri, r.tri_once, sizeof(out.tri));
+    // filtered-out kinds were not counted (their cells are zero, not checked)
+    if (motifs & (TM_MOTIF_STAR | TM_MOTIF_PAIR)) finish_star(r.star_raw, out.star, out.pair, r.star_wraps);
+    if (!(motifs & TM_MOTIF_TRIANGLE)) {
+    } else if (cfg->triangle_mode == TM_TRI_COUNT_ALL) {
+        expand_count_all(r.tri_once, out.tri, r.tri_wraps);
+    } else {
+        copy_tri_checked(r.tri_once, out.tri, r.tri_wraps);
+    }
     if (!(motifs & TM_MOTIF_STAR)) std::memset(out.star, 0, sizeof(out.star));
     if (!(motifs & TM_MOTIF_PAIR)) std::memset(out.pair, 0, sizeof(out.pair));
     if (!(motifs & TM_MOTIF_TRIANGLE)) std::memset(out.tri, 0, sizeof(out.tri));
@@ -403,7 +439,9 @@ int run_parallel_impl(tm_graph* G, const tm_run_config* cfg, tm_counters* raw, u
         throw tm_error(TM_ERR_CONFIG, "removal triangle mode requires a single worker");
     if (cfg->triangle_mode != TM_TRI_REMOVAL && cfg->triangle_mode != TM_TRI_COUNT_ALL)
         throw tm_error(TM_ERR_CONFIG, "triangle mode must be countall or removal");
-    const uint32_t motifs = cfg->motifs ? cfg->motifs : 7u;
+    // an empty filter runs nothing and yields the all-zero census
+    // (executor.cpp:28-29, 161-163, 204-206)
+    const uint32_t motifs = cfg->motifs;
     const uint32_t cb = cfg->center_begin;
     const uint32_t ce = cfg->center_end ? cfg->center_end : (uint32_t)G->g.n;
     if (cb > ce || ce > G->g.n) throw tm_error(TM_ERR_INVALID, "bad center partition");
@@ -421,7 +459,7 @@ int run_parallel_impl(tm_graph* G, const tm_run_config* cfg, tm_counters* raw, u
 
 tm_graph* build_impl(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
                      uint64_t n, int device_ptrs, void* stream, double* index_ms,
-                     const RunHint* hint = nullptr) {
+                     const RunHint* hint = nullptr, double* ingest_ms = nullptr) {
     ensure_device();
     if (m && (!src || !dst || !t)) throw tm_error(TM_ERR_INVALID, "null edge arrays");
     auto* G = new tm_graph();
@@ -444,10 +482,11 @@ tm_graph* build_impl(const uint32_t* src, const uint32_t* dst, const int64_t* t,
             }
             pool_set = true;
         }
-        cudaEvent_t e0, e1;
+        cudaEvent_t e0, e1, ec;
         if (index_ms) {
             TM_CUDA(cudaEventCreate(&e0));
             TM_CUDA(cudaEventCreate(&e1));
+            TM_CUDA(cudaEventCreate(&ec));
             TM_CUDA(cudaEventRecord(e0, s));
         }
         const uint32_t *ds = src, *dd = dst;
@@ -465,6 +504,7 @@ tm_graph* build_impl(const uint32_t* src, const uint32_t* dst, const int64_t* t,
             dd = hd;
             dt = ht;
         }
+        if (index_ms) TM_CUDA(cudaEventRecord(ec, s));  // ingest (host->device copy) | index build
         build_graph(G->g, ds, dd, dt, m, n, hint);
         dfree(hs, s);
         dfree(hd, s);
@@ -472,11 +512,14 @@ tm_graph* build_impl(const uint32_t* src, const uint32_t* dst, const int64_t* t,
         if (index_ms) {
             TM_CUDA(cudaEventRecord(e1, s));
             TM_CUDA(cudaEventSynchronize(e1));
-            float ms = 0;
-            cudaEventElapsedTime(&ms, e0, e1);
+            float ms = 0, ms_in = 0;
+            cudaEventElapsedTime(&ms_in, e0, ec);
+            cudaEventElapsedTime(&ms, ec, e1);
             *index_ms = ms;
+            if (ingest_ms) *ingest_ms = ms_in;
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);
+            cudaEventDestroy(ec);
         }
     } catch (...) {
         free_graph(G->g);
@@ -527,6 +570,9 @@ struct ReplayEntry {
     int last_variant = -1;  // replayed by the previous call (speculation target)
     BuildVerdict* verdict = nullptr;  // pinned
     uint64_t* acc = nullptr;          // pinned: the graph's counter read-back
+    // speculative replays of this entry launched by the asynchronous API and
+    // not yet collected (ReplayPending::E): the entry must outlive them
+    int inflight = 0;
     void release() {
         for (auto& e : exec)
             if (e) {
@@ -573,7 +619,7 @@ constexpr size_t kReplayEntries = 2;
 // the triangle filter of a one-shot count can run while the index builds
 RunHint hint_for(const tm_run_config* cfg, uint64_t n) {
     RunHint h;
-    const uint32_t motifs = cfg->motifs ? cfg->motifs : 7u;
+    const uint32_t motifs = cfg->motifs;
     h.early_tri = (motifs & TM_MOTIF_TRIANGLE) && cfg->triangle_mode == TM_TRI_COUNT_ALL &&
                   cfg->center_begin == 0 && (cfg->center_end == 0 || cfg->center_end == n) && cfg->delta >= 0;
     h.delta = cfg->delta;
@@ -615,10 +661,17 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
             break;
         }
     if (!E) {
+        // evict the least recently used entry that no pending asynchronous
+        // batch still reads (the cache may exceed kReplayEntries while all
+        // entries are in flight: at most two per host thread)
         if (g_replay.entries.size() >= kReplayEntries) {
-            g_replay.entries.front()->release();
-            delete g_replay.entries.front();
-            g_replay.entries.erase(g_replay.entries.begin());
+            for (size_t i = 0; i < g_replay.entries.size(); ++i)
+                if (g_replay.entries[i]->inflight == 0) {
+                    g_replay.entries[i]->release();
+                    delete g_replay.entries[i];
+                    g_replay.entries.erase(g_replay.entries.begin() + i);
+                    break;
+                }
         }
         E = new ReplayEntry();
         E->key = key;
@@ -641,12 +694,12 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
         dd = E->hd;
         dt = E->ht;
     }
-    const uint32_t motifs = cfg->motifs ? cfg->motifs : 7u;
+    const uint32_t motifs = cfg->motifs;
     const int64_t t_end = cfg->has_first_edge_t_end ? cfg->first_edge_t_end : INT64_MAX;
     const bool full = !cfg->has_first_edge_t_end;
     PassResult r;
     if (!E->verdict) TM_CUDA(cudaMallocHost(&E->verdict, sizeof(BuildVerdict)));
-    if (!E->acc) TM_CUDA(cudaMallocHost(&E->acc, 64 * sizeof(uint64_t)));
+    if (!E->acc) TM_CUDA(cudaMallocHost(&E->acc, kAccWords * sizeof(uint64_t)));
     AccOverride acc_scope(E->acc);
     // Speculative replay: when the previous call of this entry replayed a
     // graph, pack + validate and launch that graph back to back without the
@@ -664,6 +717,7 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
             TM_CUDA(cudaGraphLaunch(E->exec[lv], s));
             if (pend) {  // asynchronous: collected by complete_pending
                 g_launches.fetch_add(E->kernels[lv]);
+                ++E->inflight;
                 pend->E = E;
                 pend->G.g = G.g;
                 G.g = DeviceGraph();
@@ -780,6 +834,7 @@ thread_local uint64_t g_parse_line = 0;
 bool complete_pending(ReplayPending& P, cudaEvent_t done, const tm_run_config* cfg, tm_counters* raw,
                       uint64_t* census36) {
     ReplayEntry* E = P.E;
+    --E->inflight;  // (the entry stays cached; it is only pinned while pending)
     PassResult r;
     bool ok = false;
     try {
@@ -1018,7 +1073,7 @@ int tm_count_star_pair(tm_graph* g, int64_t delta, uint64_t* star24, uint64_t* p
         if (delta < 0) throw tm_error(TM_ERR_CONFIG, "delta must be >= 0");
         PassResult r;
         run_passes(g, delta, INT64_MAX, true, false, 0, 0, (uint32_t)g->g.n, r, nullptr);
-        finish_star(r.star_raw, star24, pair8);
+        finish_star(r.star_raw, star24, pair8, r.star_wraps);
         return TM_OK;
     });
 }
@@ -1030,8 +1085,8 @@ int tm_count_triangles(tm_graph* g, int64_t delta, int mode, uint64_t* tri24) {
             throw tm_error(TM_ERR_CONFIG, "triangle mode must be countall or removal");
         PassResult r;
         run_passes(g, delta, INT64_MAX, false, true, mode, 0, (uint32_t)g->g.n, r, nullptr);
-        if (mode == TM_TRI_COUNT_ALL) expand_count_all(r.tri_once, tri24);
-        else std::memcpy(tri24, r.tri_once, 24 * sizeof(uint64_t));
+        if (mode == TM_TRI_COUNT_ALL) expand_count_all(r.tri_once, tri24, r.tri_wraps);
+        else copy_tri_checked(r.tri_once, tri24, r.tri_wraps);
         return TM_OK;
     });
 }
@@ -1056,22 +1111,22 @@ int tm_count_star_pair_items(tm_graph* g, int64_t delta, uint64_t n_items, const
         uint32_t* dn = dalloc<uint32_t>(n_items, s);
         uint64_t *db = dalloc<uint64_t>(n_items, s), *de = dalloc<uint64_t>(n_items, s);
         uint64_t *dfo = dalloc<uint64_t>(n_items + 1, s), *dto = dalloc<uint64_t>(n_items + 1, s);
-        uint64_t* dout = dalloc<uint64_t>(n_items * 32, s);
+        uint64_t* dout = dalloc<uint64_t>(n_items * 64, s);  // per item: 32 cells + 32 wrap counters
         TM_CUDA(cudaMemcpyAsync(dn, nodes, n_items * 4, cudaMemcpyHostToDevice, s));
         TM_CUDA(cudaMemcpyAsync(db, b.data(), n_items * 8, cudaMemcpyHostToDevice, s));
         TM_CUDA(cudaMemcpyAsync(de, e.data(), n_items * 8, cudaMemcpyHostToDevice, s));
         TM_CUDA(cudaMemcpyAsync(dfo, fo.data(), (n_items + 1) * 8, cudaMemcpyHostToDevice, s));
         TM_CUDA(cudaMemcpyAsync(dto, to.data(), (n_items + 1) * 8, cudaMemcpyHostToDevice, s));
-        TM_CUDA(cudaMemsetAsync(dout, 0, n_items * 32 * 8, s));
+        TM_CUDA(cudaMemsetAsync(dout, 0, n_items * 64 * 8, s));
         build_s_pidx(g->g);
         star_items(g->g, delta, n_items, dn, db, de, dfo, fo[n_items], to[n_items], dto, dout);
-        std::vector<uint64_t> raw(n_items * 32);
-        TM_CUDA(cudaMemcpyAsync(raw.data(), dout, n_items * 32 * 8, cudaMemcpyDeviceToHost, s));
+        std::vector<uint64_t> raw(n_items * 64);
+        TM_CUDA(cudaMemcpyAsync(raw.data(), dout, n_items * 64 * 8, cudaMemcpyDeviceToHost, s));
         dfree(dn, s); dfree(db, s); dfree(de, s); dfree(dfo, s); dfree(dto, s); dfree(dout, s);
         TM_CUDA(cudaStreamSynchronize(s));
         for (uint64_t it = 0; it < n_items; ++it)
-            finish_star(&raw[it * 32], star_out ? star_out + it * 24 : nullptr,
-                        pair_out ? pair_out + it * 8 : nullptr);
+            finish_star(&raw[it * 64], star_out ? star_out + it * 24 : nullptr,
+                        pair_out ? pair_out + it * 8 : nullptr, &raw[it * 64 + 32]);
         return TM_OK;
     });
 }
@@ -1094,20 +1149,22 @@ int tm_count_triangles_items(tm_graph* g, int64_t delta, uint64_t n_items, const
         cudaStream_t s = g->g.stream;
         uint32_t* dn = dalloc<uint32_t>(n_items, s);
         uint64_t *db = dalloc<uint64_t>(n_items, s), *dio = dalloc<uint64_t>(n_items + 1, s);
-        uint64_t* dout = dalloc<uint64_t>(n_items * 24, s);
+        uint64_t* dout = dalloc<uint64_t>(n_items * 48, s);  // per item: 24 cells + 24 wrap counters
         uint8_t* dl = nullptr;
         TM_CUDA(cudaMemcpyAsync(dn, nodes, n_items * 4, cudaMemcpyHostToDevice, s));
         TM_CUDA(cudaMemcpyAsync(db, b.data(), n_items * 8, cudaMemcpyHostToDevice, s));
         TM_CUDA(cudaMemcpyAsync(dio, io.data(), (n_items + 1) * 8, cudaMemcpyHostToDevice, s));
-        TM_CUDA(cudaMemsetAsync(dout, 0, n_items * 24 * 8, s));
+        TM_CUDA(cudaMemsetAsync(dout, 0, n_items * 48 * 8, s));
         if (live) {
             dl = dalloc<uint8_t>(g->g.n, s);
             TM_CUDA(cudaMemcpyAsync(dl, live, g->g.n, cudaMemcpyHostToDevice, s));
         }
         tri_items(g->g, delta, n_items, dn, db, dio, io[n_items], dl, dout);
-        TM_CUDA(cudaMemcpyAsync(tri_out, dout, n_items * 24 * 8, cudaMemcpyDeviceToHost, s));
+        std::vector<uint64_t> raw(n_items * 48);
+        TM_CUDA(cudaMemcpyAsync(raw.data(), dout, n_items * 48 * 8, cudaMemcpyDeviceToHost, s));
         dfree(dn, s); dfree(db, s); dfree(dio, s); dfree(dout, s); dfree(dl, s);
         TM_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t it = 0; it < n_items; ++it) copy_tri_checked(&raw[it * 48], tri_out + it * 24, &raw[it * 48 + 24]);
         return TM_OK;
     });
 }
@@ -1124,11 +1181,11 @@ int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, u
         if (!timings && m && m <= kReplayMaxEdges && cfg && cfg->center_begin == 0 &&
             (cfg->center_end == 0 || cfg->center_end == n) && replay_enabled())
             return count_edges_replay(src, dst, t, m, n, device_ptrs, stream, cfg, raw, census36);
-        double index_ms = 0;
+        double index_ms = 0, ingest_ms = 0;
         RunHint hint;
         if (cfg) hint = hint_for(cfg, n);
         tm_graph* G = build_impl(src, dst, t, m, n, device_ptrs, stream, timings ? &index_ms : nullptr,
-                                 cfg ? &hint : nullptr);
+                                 cfg ? &hint : nullptr, &ingest_ms);
         int rc;
         try {
             rc = run_parallel_impl(G, cfg, raw, census36, timings);
@@ -1137,7 +1194,10 @@ int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, u
             throw;
         }
         free_impl(G);
-        if (timings) timings->index_ms = index_ms;
+        if (timings) {
+            timings->index_ms = index_ms;
+            timings->ingest_ms = ingest_ms;
+        }
         return rc;
     });
 }
@@ -1423,13 +1483,12 @@ int tm_count_edges_time_slice(const uint32_t* src, const uint32_t* dst, const in
                 dd = hd;
                 dt = ht;
             }
-            // edges of instances whose first edge starts in [t_lo, t_hi): t in [t_lo, t_hi + delta)
+            // edges of instances whose first edge starts in [t_lo, t_hi):
+            // t_lo <= t <= t_hi - 1 + delta (saturating; an open end keeps every t)
             const int64_t lo = has_lo ? t_lo : INT64_MIN;
-            const int64_t hi = has_hi ? sat_add(t_hi, cfg->delta) : INT64_MAX;
+            const int64_t hi = !has_hi ? INT64_MAX : t_hi == INT64_MIN ? INT64_MIN : sat_add(t_hi - 1, cfg->delta);
             uint64_t ms = 0;
-            if (has_lo || has_hi) {
-                ms = slice_edges(ds, dd, dt, m, lo, hi == INT64_MAX ? INT64_MAX : hi, &os, &od, &ot, s);
-            }
+            if (has_lo || has_hi) ms = slice_edges(ds, dd, dt, m, lo, hi, &os, &od, &ot, s);
             tm_run_config c = *cfg;
             c.has_first_edge_t_end = has_hi ? 1 : 0;
             c.first_edge_t_end = t_hi;
@@ -1484,6 +1543,8 @@ int tm_partition_centers(const tm_graph* g, uint32_t world, uint32_t rank, uint3
         return TM_OK;
     });
 }
+
+void tm_debug_acc_bias(uint64_t bias) { g_acc_bias = bias; }
 
 int tm_merge_census(const uint64_t* star24, const uint64_t* pair8, const uint64_t* tri24, int mode,
                     uint64_t* census36) {

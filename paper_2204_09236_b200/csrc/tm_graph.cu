@@ -406,12 +406,14 @@ __global__ void forward_off_kernel(const uint32_t* __restrict__ off, const uint3
 }
 
 // time-slice partition: keep edges with t in [lo, hi) (ingestion order kept)
+// keep lo <= t <= hi (both inclusive: an open end is INT64_MIN / INT64_MAX
+// and keeps every timestamp)
 __global__ void slice_mask_kernel(const int64_t* __restrict__ t, uint64_t m, int64_t lo, int64_t hi,
                                   uint32_t* __restrict__ mask) {
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = base + threadIdx.x;
-        const uint32_t keep = k < m && t[k] >= lo && t[k] < hi ? 1u : 0u;
+        const uint32_t keep = k < m && t[k] >= lo && t[k] <= hi ? 1u : 0u;
         const unsigned b = __ballot_sync(0xffffffffu, keep);
         if ((threadIdx.x & 31) == 0 && k < m) mask[k >> 5] = b;
     }

@@ -42,6 +42,8 @@ constexpr uint32_t kNodeMask = 0x7fffffffu;
 constexpr uint32_t kPDir = 1u << 31;
 constexpr uint32_t kPFirst = 1u << 30;
 constexpr uint32_t kPLast = 1u << 29;
+constexpr int kAccWords = 128;
+constexpr int kAccCarry = 64;  // wrap counter of accumulator cell i at d_acc[i + kAccCarry]
 
 struct tm_error : std::runtime_error {
     int code;
@@ -201,7 +203,9 @@ struct DeviceGraph {
     Forward fwd[2];
     TriStage pre_tri;  // filter issued early for a one-shot count (RunHint)
 
-    uint64_t* d_acc = nullptr;  // 64 u64: star raw [0,32), tri [32,56), work stats [56,64)
+    // kAccWords u64: star raw [0,32), tri [32,56), work stats [56,64), then the
+    // wrap counters of cells [0,56) at [64,120) (cell i's at i + kAccCarry)
+    uint64_t* d_acc = nullptr;
     uint64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // last run's work statistics
 };
 
@@ -313,7 +317,7 @@ void build_forward(DeviceGraph& g, int mode, cudaStream_t st);
 // st waits for everything issued so far on from
 void stream_after(DeviceGraph& g, cudaStream_t st, cudaStream_t from);
 void build_s_pidx(DeviceGraph& g);
-// compact the edges with t in [lo, hi) (ingestion order kept); returns the count
+// compact the edges with lo <= t <= hi (ingestion order kept); returns the count
 uint64_t slice_edges(const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t, uint64_t m,
                      int64_t lo, int64_t hi, uint32_t** o_src, uint32_t** o_dst, int64_t** o_t,
                      cudaStream_t s);

@@ -136,28 +136,45 @@ __device__ __forceinline__ void warp_append64(bool pred, uint64_t value, uint64_
     if (pred) list[base + __popc(mask & ((1u << lane) - 1u))] = value;
 }
 
+// Counter cells are exact to 128 bits: every u64 cell has a wrap counter
+// `cstride` words after it, bumped whenever an add wraps the cell, so the host
+// sees the true total and raises CounterOverflowError exactly when the
+// reference's checked_increment would (types.hpp:65-70) -- including for
+// cells formed by a difference of two raw sums (Star = raw - Pair).
+__device__ __forceinline__ void cell_add(unsigned long long* cell, int cstride, uint64_t v) {
+    if (!v) return;
+    const unsigned long long old = atomicAdd(cell, (unsigned long long)v);
+    if (old + v < old) atomicAdd(cell + cstride, 1ull);
+}
+
 // Count sinks: rare per-item contributions go straight to shared (per block)
 // or global (per work item) u64 cells, so no kernel keeps a register array.
 struct SmemSink {
     unsigned long long* cells;
-    __device__ __forceinline__ void add(int i, uint64_t v) const {
-        if (v) atomicAdd(&cells[i], (unsigned long long)v);
-    }
+    int cstride;  // wrap counter of cells[i] at cells[i + cstride]
+    __device__ __forceinline__ void add(int i, uint64_t v) const { cell_add(&cells[i], cstride, v); }
 };
 using GlobalSink = SmemSink;
 
-// Warp-held triangle cells: lane L (< 24) keeps the warp's running sum of
-// cell L.  add6() folds six per-lane counts bound for cells ty * 8 + base + dk
-// (c[ty * 2 + dk], base in {0, 2, 4, 6}) into them with one warp reduction per
-// value and distinct base present in the warp.  A u64 shared-memory atomicAdd
-// compiles to a CAS loop that serialises every lane of a warp adding to the
-// same cell -- the lanes of a long triangle window all share the first edge,
-// so most of their adds collide.  Reductions are 32-bit: a warp whose counts
-// reach 2^27 (32 of them could wrap) takes the per-lane atomics instead.
+// Warp-held cells: lane L keeps the warp's running sum of cell L (up to 32
+// cells).  A u64 shared-memory atomicAdd compiles to a CAS loop that
+// serialises every lane of a warp adding to the same cell, so hot cells are
+// summed across the warp with __reduce_add_sync (32-bit) instead.
+//   add6(): six per-lane counts bound for cells ty * 8 + base + dk (c[ty * 2 +
+//   dk], base in {0, 2, 4, 6}) -- the triangle kernels, whose long-window lanes
+//   share the first edge; one reduction per value and distinct base present.
+// A warp whose counts reach 2^27 (32 of them could wrap) takes the per-lane
+// atomics instead.  `wraps` counts wraps of the lane's u64 (exactness).
 struct WarpCells {
     uint64_t mine = 0;
+    uint32_t wraps = 0;
+    __device__ __forceinline__ void fold(uint64_t sum) {
+        const uint64_t nm = mine + sum;
+        wraps += nm < mine ? 1u : 0u;
+        mine = nm;
+    }
     __device__ __forceinline__ void add6(bool active, int base, const uint32_t c[6],
-                                         unsigned long long* cells) {
+                                         unsigned long long* cells, int cstride) {
         uint32_t big = 0, nz = 0;
 #pragma unroll
         for (int x = 0; x < 6; ++x) {
@@ -168,8 +185,7 @@ struct WarpCells {
         if (__any_sync(0xffffffffu, big)) {
             if (active)
 #pragma unroll
-                for (int x = 0; x < 6; ++x)
-                    if (c[x]) atomicAdd(&cells[(x >> 1) * 8 + base + (x & 1)], (unsigned long long)c[x]);
+                for (int x = 0; x < 6; ++x) cell_add(&cells[(x >> 1) * 8 + base + (x & 1)], cstride, c[x]);
             return;
         }
         const uint32_t present = __reduce_or_sync(0xffffffffu, nz ? 1u << (base >> 1) : 0u);
@@ -181,25 +197,38 @@ struct WarpCells {
 #pragma unroll
             for (int x = 0; x < 6; ++x) {
                 const uint32_t sum = __reduce_add_sync(0xffffffffu, mine_q ? c[x] : 0u);
-                if (lane == (x >> 1) * 8 + 2 * q + (x & 1)) mine += sum;
+                if (lane == (x >> 1) * 8 + 2 * q + (x & 1)) fold(sum);
             }
         }
     }
     // each lane's cell into the block's shared cells (whole warp, before the block flush)
-    __device__ __forceinline__ void flush(unsigned long long* cells) const {
-        if (mine) atomicAdd(&cells[threadIdx.x & 31], (unsigned long long)mine);
+    __device__ __forceinline__ void flush(unsigned long long* cells, int ncells, int cstride) const {
+        const int lane = threadIdx.x & 31;
+        if (lane < ncells) {
+            cell_add(&cells[lane], cstride, mine);
+            if (wraps) atomicAdd(&cells[lane + cstride], (unsigned long long)wraps);
+        }
     }
 };
 
-// zero `count` shared cells; call before use, followed by __syncthreads
+// zero `count` shared cells and their wrap counters (2 * count words); call
+// before use, followed by __syncthreads
 __device__ __forceinline__ void zero_cells(unsigned long long* cells, int count) {
-    for (int i = threadIdx.x; i < count; i += blockDim.x) cells[i] = 0;
+    for (int i = threadIdx.x; i < 2 * count; i += blockDim.x) cells[i] = 0;
 }
-// add block cells to global out (after __syncthreads)
-__device__ __forceinline__ void flush_cells(const unsigned long long* cells, int count,
-                                            uint64_t* out) {
-    for (int i = threadIdx.x; i < count; i += blockDim.x)
-        if (cells[i]) atomicAdd((unsigned long long*)&out[i], cells[i]);
+// add block cells (wrap counters at cells[i + count]) to global out (wrap
+// counters at out[i + ostride]), after __syncthreads
+__device__ __forceinline__ void flush_cells(const unsigned long long* cells, int count, uint64_t* out,
+                                            int ostride) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
+        const unsigned long long v = cells[i];
+        unsigned long long c = cells[i + count];
+        if (v) {
+            const unsigned long long old = atomicAdd((unsigned long long*)&out[i], v);
+            if (old + v < old) ++c;
+        }
+        if (c) atomicAdd((unsigned long long*)&out[i + ostride], c);
+    }
 }
 
 // last u with off[u] <= k (the node owning record k); off has n+1 entries

@@ -304,14 +304,14 @@ __global__ void __launch_bounds__(256, 5) star_work_kernel(SView S, PView P, int
                                                         unsigned long long* __restrict__ queue,
                                                         uint64_t* __restrict__ out,
                                                         uint64_t* __restrict__ stats) {
-    __shared__ unsigned long long cells[32];
+    __shared__ unsigned long long cells[64];
     zero_cells(cells, 32);
     if (blockIdx.x == 0 && threadIdx.x == 0 && stats) {
         stats[0] = counters[0];
         stats[1] = counters[1];
     }
     __syncthreads();
-    const SmemSink acc{cells};
+    const SmemSink acc{cells, 32};
     const uint32_t nf = counters[0], nt = counters[1];
     const uint64_t total = (uint64_t)nf + nt;
     for (;;) {  // 32 items per warp from the queue (hub items are heavy-tailed)
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(256, 5) star_work_kernel(SView S, PView P, int
         }
     }
     __syncthreads();
-    flush_cells(cells, 32, out);
+    flush_cells(cells, 32, out, kAccCarry);
 }
 
 __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ item_off, uint64_t n_items,
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(256) star_items_kernel(
             const uint32_t start = S.off[u], end = S.off[u + 1];
             const uint32_t q = start + (uint32_t)begin[it] + (uint32_t)(idx - first_off[it]);
             first_role(S, P, q, S.pidx[q], side_of(u, S.nbr[q] & kNodeMask), start, end, delta,
-                       GlobalSink{(unsigned long long*)out + (uint64_t)it * 32});
+                       GlobalSink{(unsigned long long*)out + (uint64_t)it * 64, 32});
         } else {
             const uint64_t j = idx - total_first;
             it = find_item(third_off, n_items, j);
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(256) star_items_kernel(
             const uint32_t re = (uint32_t)(endr[it] < (uint64_t)s ? endr[it] : (uint64_t)s);
             const uint32_t q = start + rb + 1 + (uint32_t)(j - third_off[it]);
             third_role(S, P, q, S.pidx[q], side_of(u, S.nbr[q] & kNodeMask), start, delta, rb, re,
-                       GlobalSink{(unsigned long long*)out + (uint64_t)it * 32});
+                       GlobalSink{(unsigned long long*)out + (uint64_t)it * 64, 32});
         }
     }
 }

@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(256, 5) tri_wedge_kernel(PView P, TimeArr FT,
                                                         const unsigned long long* __restrict__ wsum,
                                                         uint64_t gend_min, unsigned long long* queue,
                                                         uint64_t* out, uint64_t* stats) {
-    __shared__ unsigned long long cells[24];
+    __shared__ unsigned long long cells[48];
     if (!P.gend || *wsum < gend_min) P.gend = nullptr;  // group ends not built
     zero_cells(cells, 24);
     __syncthreads();
@@ -309,11 +309,11 @@ __global__ void __launch_bounds__(256, 5) tri_wedge_kernel(PView P, TimeArr FT,
             const uint64_t w = wedges[idx];
             cb = wedge_counts(P, FT, FN, FO, (uint32_t)(w >> 32), (uint32_t)w, delta, t_end, c);
         }
-        wc.add6(idx < cnt, cb, c, cells);
+        wc.add6(idx < cnt, cb, c, cells, 24);
     }
-    wc.flush(cells);
+    wc.flush(cells, 24, 24);
     __syncthreads();
-    flush_cells(cells, 24, out);
+    flush_cells(cells, 24, out, kAccCarry);
 }
 
 // first edges with long windows: one warp per first edge, lanes stride the
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
                                                        uint64_t pt_min_wedges, uint64_t gend_min,
                                                        unsigned long long* queue, uint64_t* out,
                                                        uint64_t* stats) {
-    __shared__ unsigned long long cells[24];
+    __shared__ unsigned long long cells[48];
     zero_cells(cells, 24);
     __syncthreads();
     WarpCells wc;
@@ -357,15 +357,15 @@ __global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
                 cb = wedge_counts(P, FT, FN, FO, i, j, delta, t_end, c);
                 ++my_wedges;
             }
-            wc.add6(wedge, cb, c, cells);
+            wc.add6(wedge, cb, c, cells, 24);
             if (!__all_sync(0xffffffffu, in)) break;
         }
     }
-    wc.flush(cells);
+    wc.flush(cells, 24, 24);
     my_wedges = warp_sum(my_wedges);
     if (lane == 0 && my_wedges && stats) atomicAdd((unsigned long long*)&stats[4], (unsigned long long)my_wedges);
     __syncthreads();
-    flush_cells(cells, 24, out);
+    flush_cells(cells, 24, out, kAccCarry);
 }
 
 __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ item_off, uint64_t n_items,
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(256) tri_items_kernel(SView S, PView P, int64_
         const uint32_t start = S.off[u], end = S.off[u + 1];
         const uint32_t i = start + (uint32_t)begin[it] + (uint32_t)(idx - item_off[it]);
         wedges_from(P, S.t, S.nbr, S.ord, i, end, delta, live,
-                    GlobalSink{(unsigned long long*)out + (uint64_t)it * 24});
+                    GlobalSink{(unsigned long long*)out + (uint64_t)it * 48, 24});
     }
 }
 

@@ -29,7 +29,7 @@ TM_ERR_INVALID = 1
 TM_ERR_PARSE = 2
 TM_ERR_OVERFLOW = 3
 TM_ERR_CONFIG = 4
-TM_ERR_CONSISTENCY = 5
+TM_ERR_CONSISTENCY = 10
 TM_ERR_CUDA = 8
 TM_ERR_LIMIT = 9
 
@@ -95,7 +95,7 @@ class _RunConfig(C.Structure):
 
 
 class _Timings(C.Structure):
-    _fields_ = [("index_ms", C.c_double), ("star_pair_ms", C.c_double),
+    _fields_ = [("ingest_ms", C.c_double), ("index_ms", C.c_double), ("star_pair_ms", C.c_double),
                 ("triangle_ms", C.c_double), ("merge_ms", C.c_double)]
 
 
@@ -155,6 +155,7 @@ def lib():
     L.tm_generate_random_graph.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_uint64, VP, VP, VP]
     L.tm_run_stats.argtypes = [VP, VP]
     L.tm_last_error.restype = C.c_char_p
+    L.tm_debug_acc_bias.argtypes = [C.c_uint64]
     L.tm_kernel_launches.restype = C.c_uint64
     L.tm_kernel_timing_enable.argtypes = [C.c_int]
     L.tm_kernel_timing_get.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
@@ -381,7 +382,11 @@ class MotifCensus:
         return int(self.counts[k])
 
     def total(self) -> int:
-        return int(sum(int(c) for c in self.counts))
+        """checked sum (motifs.cpp:239-243)."""
+        s = int(sum(int(c) for c in self.counts))
+        if s >= 1 << 64:
+            raise CounterOverflowError("motif counter overflow")
+        return s
 
     def same_counts(self, other: "MotifCensus") -> bool:
         return bool((self.counts == other.counts).all())
@@ -813,9 +818,7 @@ class RunConfig:
 
     def to_c(self, center_begin: int = 0, center_end: int = 0) -> _RunConfig:
         thr = -1 if self.degree_threshold is None else min(int(self.degree_threshold), NO_SHARDING)
-        m = self.motifs.mask()
-        if m == 0:
-            raise ValueError("empty motif filter")
+        m = self.motifs.mask()  # 0 = the empty filter: an all-zero census (executor.cpp:28-29)
         has_t = 0 if self.first_edge_t_end is None else 1
         return _RunConfig(int(self.delta), int(self.workers), thr, int(self.triangle_mode), m,
                           int(self.shard_target), center_begin, center_end, has_t,
@@ -838,6 +841,41 @@ def auto_degree_threshold(ctx: GraphContext) -> int:
     v = C.c_uint64(0)
     _raise(ctx._lib.tm_auto_degree_threshold(ctx._h, C.byref(v)), ctx._lib)
     return int(v.value)
+
+
+@dataclass
+class HeavyNode:
+    node: int
+    shards: List[Tuple[int, int]]
+
+
+@dataclass
+class SchedulePlan:
+    """executor.hpp:20-33."""
+    heavy: List[HeavyNode] = field(default_factory=list)
+    light: List[int] = field(default_factory=list)
+    thr_d: int = 0
+    shard_target: int = 0
+    run_star_pair: bool = True
+    run_triangle: bool = True
+
+
+def plan_schedule(ctx: GraphContext, thr_d: int, shard_target: int, motifs: MotifFilter) -> SchedulePlan:
+    """plan_schedule (executor.cpp:23-52): heavy centers (degree > thr_d)
+    sharded over their star first-edge range, the rest light.  The reference's
+    CPU work plan, for callers that drive the per-center API themselves; the
+    device passes parallelise over records and wedges instead."""
+    if shard_target < 1:
+        raise ConfigError("shard_target must be >= 1")
+    plan = SchedulePlan(thr_d=thr_d, shard_target=shard_target,
+                        run_star_pair=motifs.star or motifs.pair, run_triangle=motifs.triangle)
+    deg = ctx.degrees()
+    heavy = np.nonzero(deg > thr_d)[0]
+    plan.light = [int(u) for u in np.nonzero(deg <= thr_d)[0]]
+    for u in heavy:
+        b, e = full_star_range(int(deg[u]))
+        plan.heavy.append(HeavyNode(int(u), [(x, min(x + shard_target, e)) for x in range(b, e, shard_target)]))
+    return plan
 
 
 @dataclass
@@ -906,7 +944,7 @@ def count_edges(n: int, src, dst, t, config: RunConfig, stream: Optional[int] = 
         raw_out[24:32] = np.frombuffer(raw.pair, np.uint64)
         raw_out[32:56] = np.frombuffer(raw.tri, np.uint64)
     if timings is not None:
-        timings.index_ms, timings.star_pair_ms = tm.index_ms, tm.star_pair_ms
+        timings.ingest_ms, timings.index_ms, timings.star_pair_ms = tm.ingest_ms, tm.index_ms, tm.star_pair_ms
         timings.triangle_ms, timings.merge_ms = tm.triangle_ms, tm.merge_ms
     return census
 
@@ -967,7 +1005,7 @@ def count_edges_device(n: int, m: int, src_ptr: int, dst_ptr: int, t_ptr: int, c
         raw_out[24:32] = np.frombuffer(raw.pair, np.uint64)
         raw_out[32:56] = np.frombuffer(raw.tri, np.uint64)
     if timings is not None:
-        timings.index_ms, timings.star_pair_ms = tm.index_ms, tm.star_pair_ms
+        timings.ingest_ms, timings.index_ms, timings.star_pair_ms = tm.ingest_ms, tm.index_ms, tm.star_pair_ms
         timings.triangle_ms, timings.merge_ms = tm.triangle_ms, tm.merge_ms
     return census
 

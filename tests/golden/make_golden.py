@@ -15,8 +15,15 @@ container, where /root/reference exists).
 
   powerlaw_deltas_reference.json reference census of config 1's input at delta
                         600 and 86400 (optional, slow)
+  config4_slices_reference.json reference census of contiguous 10M-edge index
+                        (= time) slices of config 4 (powerlaw_50m_600m, counter-based
+                        generator synth.power_law_hashed, one early and one
+                        mid-stream) at delta 600 / 3600 / 86400 (optional, slow)
+  triadic_reference.json reference census of config 3 (triadic_25m_100m, synth.
+                        triadic_hashed) at FULL size, delta 3600 and 86400 (optional, slow)
 
-Usage: python tests/golden/make_golden.py [--powerlaw] [--hubstress] [--powerlaw-deltas] [--only-extra]
+Usage: python tests/golden/make_golden.py [--powerlaw] [--hubstress] [--powerlaw-deltas]
+          [--config4-slices] [--triadic] [--only-extra]
 """
 from __future__ import annotations
 
@@ -89,6 +96,78 @@ def powerlaw_deltas_golden(R, deltas=(600, 86400)):
     R.free(g)
 
 
+CONFIG4 = dict(n=50_000_000, m=600_000_000, mean_gap=0.05, seed=2204)
+CONFIG4_SLICES = ((0, 10_000_000), (300_000_000, 310_000_000))
+CONFIG3 = dict(n=25_000_000, m=100_000_000, closure=0.30, delta=86_400, mean_gap=1.0, seed=2204)
+
+
+def _dump(out, name):
+    tmp = os.path.join(HERE, name + ".tmp")
+    json.dump(out, open(tmp, "w"))
+    os.replace(tmp, os.path.join(HERE, name))
+
+
+def config4_slices_golden(R, deltas=(600, 3600, 86400)):
+    """Reference run_parallel (all host threads) on contiguous edge-index
+    slices of config 4; the input is time-ordered, so an index slice is a
+    time slice.  Node ids are kept (n = 50M)."""
+    import time
+    from paper_2204_09236_b200 import synth
+    name = "config4_slices_reference.json"
+    path = os.path.join(HERE, name)
+    out = json.load(open(path)) if os.path.exists(path) else {
+        "config": "powerlaw_50m_600m", "generator": "synth.power_law_hashed", **CONFIG4, "slices": []}
+    for lo, hi in CONFIG4_SLICES:
+        have = [s for s in out["slices"] if s["lo"] == lo and s["hi"] == hi]
+        entry = have[0] if have else None
+        done = {c["delta"] for c in entry["cases"]} if entry else set()
+        if done >= set(deltas):
+            continue
+        n, s, d, tt = synth.power_law_hashed(CONFIG4["n"], CONFIG4["m"], CONFIG4["mean_gap"], CONFIG4["seed"],
+                                             lo=lo, hi=hi)
+        if entry is None:
+            entry = {"lo": lo, "hi": hi, "hash": edge_hash(s, d, tt), "cases": []}
+            out["slices"].append(entry)
+        g = R.build_graph(n, s, d, tt)
+        for delta in deltas:
+            if delta in done:
+                continue
+            t0 = time.time()
+            census = R.run_parallel(g, delta, os.cpu_count() or 1)
+            entry["cases"].append({"delta": delta, "census": [int(x) for x in census],
+                                   "cpu_s": round(time.time() - t0, 1), "threads": os.cpu_count()})
+            _dump(out, name)
+            print("config4 slice", lo, hi, "delta", delta, "done in", round(time.time() - t0, 1), "s", flush=True)
+        R.free(g)
+
+
+def triadic_golden(R, deltas=(3600, 86400)):
+    """Reference run_parallel on the whole of config 3 (100M edges)."""
+    import time
+    from paper_2204_09236_b200 import synth
+    name = "triadic_reference.json"
+    path = os.path.join(HERE, name)
+    n, s, d, tt = synth.triadic_hashed(**CONFIG3)
+    h = edge_hash(s, d, tt)
+    out = json.load(open(path)) if os.path.exists(path) else {
+        "config": "triadic_25m_100m", "generator": "synth.triadic_hashed", **CONFIG3, "edges": int(len(s)),
+        "hash": h, "cases": []}
+    assert out["hash"] == h
+    done = {c["delta"] for c in out["cases"]}
+    g = R.build_graph(n, s, d, tt)
+    del s, d, tt
+    for delta in deltas:
+        if delta in done:
+            continue
+        t0 = time.time()
+        census = R.run_parallel(g, delta, os.cpu_count() or 1)
+        out["cases"].append({"delta": delta, "census": [int(x) for x in census],
+                             "cpu_s": round(time.time() - t0, 1), "threads": os.cpu_count()})
+        _dump(out, name)
+        print("triadic delta", delta, "done in", round(time.time() - t0, 1), "s", flush=True)
+    R.free(g)
+
+
 def main(with_powerlaw: bool, with_hubstress: bool = False, only_extra: bool = False,
          with_pl_deltas: bool = False):
     R = Reference()
@@ -97,6 +176,10 @@ def main(with_powerlaw: bool, with_hubstress: bool = False, only_extra: bool = F
             hubstress_golden(R)
         if with_pl_deltas:
             powerlaw_deltas_golden(R)
+        if "--config4-slices" in sys.argv:
+            config4_slices_golden(R)
+        if "--triadic" in sys.argv:
+            triadic_golden(R)
         return
     sigs = R.signatures()
 

@@ -626,3 +626,149 @@ print(json.dumps(out))
             rc = tm.RawCounters.from_array(np.array(raw, np.uint64))
             assert tm.merge_census(rc.star, rc.pair, rc.tri, tm.TriangleMode.count_all).counts.tolist() == want
         oracle.free(og)
+
+
+# --- boundary semantics (round 2) ---------------------------------------------------
+def test_empty_motif_filter_is_all_zero(cuda, tm):
+    """executor.cpp:28-29, 161-163, 204-206: an all-false MotifFilter runs no
+    pass and merges to the all-zero census (no error)."""
+    g = tm.generate_random_graph(25, 300, 150, 19)
+    ctx = ctx_of(tm, g)
+    assert tm.run_parallel(ctx, tm.RunConfig(delta=40)).total() > 0
+    empty = tm.run_parallel(ctx, tm.RunConfig(delta=40, motifs=tm.MotifFilter(False, False, False)))
+    assert empty.total() == 0 and not empty.counts.any()
+    raw, census = tm.run_parallel_raw(ctx, tm.RunConfig(delta=40, motifs=tm.MotifFilter(False, False, False)))
+    assert not raw.as_array().any()
+    assert tm.count_edges(g.node_count(), g.src, g.dst, g.t,
+                          tm.RunConfig(delta=40, motifs=tm.MotifFilter(False, False, False))).sum() == 0
+
+
+def test_counter_overflow_detected_exactly_at_2_64(cuda, tm):
+    """CounterOverflowError (types.hpp:65-70) exactly when a cell exceeds
+    2^64 - 1.  The test hook starts every raw star/pair accumulator cell at
+    `bias` on the device, so Pair = bias + count wraps on the GPU at the
+    boundary while Star = raw - Pair stays exact: the device wrap counters and
+    the host's 128-bit finish must report overflow for bias = 2^64 - max(Pair)
+    and not for one less."""
+    L = tm.lib()
+    g = tm.generate_random_graph(20, 600, 100, 5)
+    ctx = ctx_of(tm, g)
+    cfg = tm.RunConfig(delta=30)
+    raw0, census0 = tm.run_parallel_raw(ctx, cfg)
+    pmax = int(raw0.pair.cells.max())
+    assert pmax > 0
+    try:
+        L.tm_debug_acc_bias((1 << 64) - 1 - pmax)  # max cell lands on 2^64 - 1: fine
+        raw1, _ = tm.run_parallel_raw(ctx, tm.RunConfig(delta=30, motifs=tm.MotifFilter(True, True, False)))
+        assert (raw1.star.cells == raw0.star.cells).all()
+        assert int(raw1.pair.cells.max()) == (1 << 64) - 1
+        L.tm_debug_acc_bias((1 << 64) - pmax)  # max cell lands on 2^64: overflow
+        with pytest.raises(tm.CounterOverflowError):
+            tm.run_parallel_raw(ctx, tm.RunConfig(delta=30, motifs=tm.MotifFilter(True, True, False)))
+        with pytest.raises(tm.CounterOverflowError):
+            tm.count_star_pair(ctx, 30)
+        # star-only filter: the pass still runs (executor.cpp:161), so it still throws
+        with pytest.raises(tm.CounterOverflowError):
+            tm.run_parallel(ctx, tm.RunConfig(delta=30, motifs=tm.MotifFilter(True, False, False)))
+        # triangles only: the star pass does not run, nothing overflows
+        tri = tm.run_parallel(ctx, tm.RunConfig(delta=30, motifs=tm.MotifFilter(False, False, True)))
+        assert tri.total() == sum(int(c) for k, c in enumerate(census0.counts)
+                                  if tm.signature_category(tm.all_signatures()[k]) == "triangle")
+    finally:
+        L.tm_debug_acc_bias(0)
+    assert (tm.run_parallel(ctx, cfg).counts == census0).all()
+
+
+def test_plan_schedule_mirrors_reference(cuda, tm):
+    """plan_schedule (executor.cpp:23-52): heavy = degree > thr_d, sharded over
+    full_star_range in shard_target steps; every other node light."""
+    g = tm.generate_random_graph(40, 2000, 1000, 3)
+    ctx = ctx_of(tm, g)
+    deg = np.asarray(g.degrees())
+    thr = tm.auto_degree_threshold(ctx)
+    assert thr == sorted(deg.tolist(), reverse=True)[19]
+    plan = tm.plan_schedule(ctx, thr, 7, tm.MotifFilter())
+    assert sorted([h.node for h in plan.heavy] + plan.light) == list(range(40))
+    for h in plan.heavy:
+        assert deg[h.node] > thr
+        b, e = tm.full_star_range(int(deg[h.node]))
+        assert h.shards[0][0] == b and h.shards[-1][1] == e
+        assert all(y - x <= 7 for x, y in h.shards)
+        assert all(a[1] == b2[0] for a, b2 in zip(h.shards, h.shards[1:]))
+    assert all(deg[u] <= thr for u in plan.light)
+    with pytest.raises(tm.ConfigError):
+        tm.plan_schedule(ctx, thr, 0, tm.MotifFilter())
+    # the plan's items, counted through the per-center API, sum to the full run
+    items = [(h.node, r) for h in plan.heavy for r in h.shards] + \
+            [(u, tm.full_star_range(int(deg[u]))) for u in plan.light]
+    res = tm.count_star_pair_items(ctx, 60, [u for u, _ in items], [r for _, r in items])
+    star = sum(r.star.cells.astype(object) for r in res)
+    full = tm.count_star_pair(ctx, 60)
+    assert [int(x) for x in star] == [int(x) for x in full.star.cells]
+
+
+def test_time_slice_open_end_keeps_int64_max(cuda, tm, oracle):
+    """A last (open) time slice keeps edges with t == INT64_MAX, and a bounded
+    slice whose t_hi + delta saturates keeps them too: sliced == unsliced."""
+    top = 2 ** 63 - 1
+    rng = np.random.default_rng(4)
+    n, m = 12, 400
+    s = rng.integers(0, n, m).astype(np.uint32)
+    d = ((s + 1 + rng.integers(0, n - 1, m)) % n).astype(np.uint32)
+    t = (top - rng.integers(0, 60, m)).astype(np.int64)
+    t[:40] = top
+    for delta in (5, 100, 2 ** 62):
+        cfg = tm.RunConfig(delta=delta)
+        full = tm.count_edges_time_slice(n, s, d, t, cfg).as_array()
+        og = oracle.build_graph(n, s, d, t)
+        assert (tm.RawCounters.from_array(full).as_array() ==
+                tm.run_parallel_raw(tm.GraphContext.build(tm.TemporalGraph.from_arrays(n, s, d, t)),
+                                    cfg)[0].as_array()).all()
+        oracle.free(og)
+        for cut in (top - 30, top - 1, top):
+            acc = tm.count_edges_time_slice(n, s, d, t, cfg, None, cut).as_array() + \
+                tm.count_edges_time_slice(n, s, d, t, cfg, cut, None).as_array()
+            assert (acc == full).all(), (delta, cut)
+
+
+def test_async_then_sync_other_key_keeps_pending_entry(cuda, tm, oracle):
+    """with both async slots holding speculative replays, a sync
+    count on other arrays must not evict (free) the replay entries the pending
+    batches still read; every result equals the oracle."""
+    import torch
+    n, m, delta = 50, 3000, 120
+    batches = [oracle.generate_random_graph(n, m, 20000, 900 + k) for k in range(4)]
+    want = []
+    for s, d, t in batches:
+        og = oracle.build_graph(n, s, d, t)
+        want.append(oracle.census(og, delta).tolist())
+        oracle.free(og)
+    pinned = [tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).pin_memory() for a in b)
+              for b in batches]
+
+    def host(i):
+        ps, pd, pt = pinned[i]
+        return ps.numpy().view(np.uint32), pd.numpy().view(np.uint32), pt.numpy()
+
+    cfg = tm.RunConfig(delta=delta)
+    st = torch.cuda.Stream()
+    # warm both slots into speculative replay (eager, capture, replay per slot)
+    for k in range(6):
+        tm.count_edges_async(n, *host(k % 2), cfg, stream=st.cuda_stream).result()
+    p0 = tm.count_edges_async(n, *host(0), cfg, stream=st.cuda_stream)
+    p1 = tm.count_edges_async(n, *host(1), cfg, stream=st.cuda_stream)
+    for k in (2, 3, 2, 3):  # sync calls with other keys: replay-cache churn
+        got = tm.count_edges(n, *batches[k], tm.RunConfig(delta=delta))
+        assert got.tolist() == want[k]
+    assert p1.result().tolist() == want[1]
+    assert p0.result().tolist() == want[0]
+
+
+def test_error_codes_distinct(cuda, tm):
+    """C-ABI codes: ConsistencyError is 10 (the CLI folds it into exit_usage),
+    ConfigError 4, CounterOverflowError 3, ParseError 2 (tmotif_main.cpp:20-30)."""
+    assert (tm.TM_ERR_PARSE, tm.TM_ERR_OVERFLOW, tm.TM_ERR_CONFIG, tm.TM_ERR_CONSISTENCY) == (2, 3, 4, 10)
+    bad_pair = np.zeros(8, np.uint64)
+    bad_pair[0] = 1
+    with pytest.raises(tm.ConsistencyError):
+        tm.merge_census(tm.StarCounter(), tm.PairCounter(bad_pair), tm.TriCounter())
