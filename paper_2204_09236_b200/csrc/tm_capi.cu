@@ -325,7 +325,19 @@ void collect_passes(tm_graph* G, PassResult& r, cudaEvent_t done = nullptr) {
     std::memcpy(r.tri_wraps, h + kAccCarry + 32, 24 * sizeof(uint64_t));
 }
 
-void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do_tri, int tri_mode,
+// inclusive bound on the first edge's t for a time-slice share (INT64_MAX:
+// unbounded); `none` when the exclusive end admits no t at all
+int64_t first_edge_t_last(const tm_run_config* cfg, bool& none) {
+    none = false;
+    if (!cfg->has_first_edge_t_end) return INT64_MAX;
+    if (cfg->first_edge_t_end == INT64_MIN) {
+        none = true;
+        return INT64_MIN;
+    }
+    return cfg->first_edge_t_end - 1;
+}
+
+void run_passes(tm_graph* G, int64_t delta, int64_t t_last, bool do_star, bool do_tri, int tri_mode,
                 uint32_t cb, uint32_t ce, PassResult& r, tm_phase_timings* tm, bool collect = true) {
     DeviceGraph& g = G->g;
     cudaStream_t s = g.stream;
@@ -351,7 +363,7 @@ void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do
     cudaStream_t ss = (star_on && g.aux[1]) ? g.aux[1] : s;  // side stream only when used
     if (star_on) {
         stream_after(g, ss, s);
-        star_full(g, delta, cb, ce, t_end, g.d_acc, g.d_acc + 56, ss);
+        star_full(g, delta, cb, ce, t_last, g.d_acc, g.d_acc + 56, ss);
     }
     if (tm) TM_CUDA(cudaEventRecord(e1, ss));
     if (do_tri && g.R) {
@@ -365,9 +377,9 @@ void run_passes(tm_graph* G, int64_t delta, int64_t t_end, bool do_star, bool do
         }
         if (fm == 0 && full && g.pre_tri.valid && g.pre_tri.delta == delta && g.pre_tri.f_begin == fb &&
             g.pre_tri.f_end == fe)
-            tri_work_stage(g, f, g.pre_tri, t_end, g.d_acc + 32, g.d_acc + 56);  // filter ran during the build
+            tri_work_stage(g, f, g.pre_tri, t_last, g.d_acc + 32, g.d_acc + 56);  // filter ran during the build
         else
-            tri_oriented(g, f, delta, fb, fe, t_end, g.d_acc + 32, g.d_acc + 56);
+            tri_oriented(g, f, delta, fb, fe, t_last, g.d_acc + 32, g.d_acc + 56);
     }
     if (ss != s) {
         TM_CUDA(cudaEventRecord(g.ev_join, ss));
@@ -449,8 +461,10 @@ int run_parallel_impl(tm_graph* G, const tm_run_config* cfg, tm_counters* raw, u
 
     PassResult r;
     auto t0 = std::chrono::steady_clock::now();
-    const int64_t t_end = cfg->has_first_edge_t_end ? cfg->first_edge_t_end : INT64_MAX;
-    run_passes(G, cfg->delta, t_end, (motifs & 3u) != 0, (motifs & 4u) != 0, cfg->triangle_mode, cb, ce, r,
+    bool none = false;
+    const int64_t t_last = first_edge_t_last(cfg, none);
+    run_passes(G, cfg->delta, t_last, !none && (motifs & 3u) != 0, !none && (motifs & 4u) != 0, cfg->triangle_mode,
+               cb, ce, r,
                tm);
     finish_counts(r, cfg, full, raw, census, tm);
     (void)t0;
@@ -695,7 +709,8 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
         dt = E->ht;
     }
     const uint32_t motifs = cfg->motifs;
-    const int64_t t_end = cfg->has_first_edge_t_end ? cfg->first_edge_t_end : INT64_MAX;
+    bool none = false;
+    const int64_t t_last = first_edge_t_last(cfg, none);
     const bool full = !cfg->has_first_edge_t_end;
     PassResult r;
     if (!E->verdict) TM_CUDA(cudaMallocHost(&E->verdict, sizeof(BuildVerdict)));
@@ -754,7 +769,8 @@ int count_edges_replay(const uint32_t* src, const uint32_t* dst, const int64_t* 
     const RunHint hint = hint_for(cfg, n);
     auto issue = [&](bool collect) {
         build_finish(G.g, plan, ds, dd, dt, &hint);
-        run_passes(&G, cfg->delta, t_end, (motifs & 3u) != 0, (motifs & 4u) != 0, cfg->triangle_mode, 0,
+        run_passes(&G, cfg->delta, t_last, !none && (motifs & 3u) != 0, !none && (motifs & 4u) != 0,
+                   cfg->triangle_mode, 0,
                    (uint32_t)n, r, nullptr, collect);
     };
     if (E->exec[variant] && (E->cap_tmin[variant] != plan.tmin || E->cap_tmax[variant] != plan.tmax)) {

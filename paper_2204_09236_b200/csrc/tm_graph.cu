@@ -260,7 +260,10 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
                                                        uint32_t* __restrict__ P_w, uint64_t n,
                                                        uint32_t* __restrict__ pofs,
                                                        uint32_t* __restrict__ dmask,
-                                                       uint32_t* __restrict__ gmask) {
+                                                       uint32_t* __restrict__ gmask,
+                                                       uint32_t* __restrict__ max32, uint32_t* __restrict__ max1k,
+                                                       int64_t* __restrict__ t32w, uint32_t* __restrict__ t32n,
+                                                       int64_t* __restrict__ t1kw, uint32_t* __restrict__ t1kn) {
     using Codec = EdgeCodec<kNarrow>;
     __shared__ uint32_t s_a[258], s_b[258];
     const int tid = threadIdx.x;
@@ -293,6 +296,16 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
             __stcs(P_min + k, a);
             __stcs(P_max + k, b);
             __stcs(P_w + k, (dir_min << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u));
+            if ((k & 31) == 0) {  // the fences (tm_internal.cuh fenced_lower_bound)
+                max32[k >> 5] = b;
+                if (kNarrow) t32n[k >> 5] = Codec::rel(ed);
+                else t32w[k >> 5] = Codec::time(ed, tmin);
+                if ((k & 1023) == 0) {
+                    max1k[k >> 10] = b;
+                    if (kNarrow) t1kn[k >> 10] = Codec::rel(ed);
+                    else t1kw[k >> 10] = Codec::time(ed, tmin);
+                }
+            }
             // pofs[x] = first P position whose min endpoint is x (block boundaries)
             const int64_t prev = k == 0 ? -1 : (int64_t)s_a[tid];
             for (int64_t x = prev + 1; x <= (int64_t)a; ++x) pofs[x] = (uint32_t)k;
@@ -610,6 +623,15 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
     g.P_dpref = dalloc<uint32_t>(m / 32 + 2, s);
     g.P_gmask = dalloc<uint32_t>(m / 32 + 1, s);
     g.P_gpref = dalloc<uint32_t>(m / 32 + 2, s);
+    g.P_max32 = dalloc<uint32_t>(m / 32 + 1, s);
+    g.P_max1k = dalloc<uint32_t>(m / 1024 + 1, s);
+    if (narrow) {
+        g.P_t32.n = dalloc<uint32_t>(m / 32 + 1, s);
+        g.P_t1k.n = dalloc<uint32_t>(m / 1024 + 1, s);
+    } else {
+        g.P_t32.w = dalloc<int64_t>(m / 32 + 1, s);
+        g.P_t1k.w = dalloc<int64_t>(m / 1024 + 1, s);
+    }
     TM_CUDA(cudaMemsetAsync(g.P_dmask + m / 32, 0, sizeof(uint32_t), s));
     TM_CUDA(cudaMemsetAsync(g.P_gmask + m / 32, 0, sizeof(uint32_t), s));
 
@@ -716,10 +738,12 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
         if (narrow)
             TM_LAUNCH("gather_p", s, gather_p_kernel<true>, grid_for(m), 256, 0, pk0, m, EN, tmin, g.P_t.w, g.P_t.n,
-                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask, g.P_gmask);
+                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask, g.P_gmask, g.P_max32, g.P_max1k,
+                      g.P_t32.w, g.P_t32.n, g.P_t1k.w, g.P_t1k.n);
         else
             TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, EW, tmin, g.P_t.w, g.P_t.n,
-                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask, g.P_gmask);
+                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask, g.P_gmask, g.P_max32, g.P_max1k,
+                      g.P_t32.w, g.P_t32.n, g.P_t1k.w, g.P_t1k.n);
         dfree(pk0_alloc, s);
         // direction prefix and group-first prefix in one scan
         exclusive_scan_to<uint64_t>(PopcLoad2{g.P_dmask, g.P_gmask}, m / 32 + 1, SplitStore2{g.P_dpref, g.P_gpref},
@@ -834,6 +858,8 @@ void free_graph(DeviceGraph& g) {
     dfree(g.P_t.w, s); dfree(g.P_t.n, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
     dfree(g.P_min, s); dfree(g.pofs, s); dfree(g.P_dmask, s); dfree(g.P_dpref, s);
     dfree(g.P_gmask, s); dfree(g.P_gpref, s);
+    dfree(g.P_max32, s); dfree(g.P_max1k, s); dfree(g.P_t32.w, s); dfree(g.P_t32.n, s); dfree(g.P_t1k.w, s);
+    dfree(g.P_t1k.n, s);
     dfree(g.pre_tri.wedges, s); dfree(g.pre_tri.long_list, s); dfree(g.pre_tri.wbuf, s);
     g.pre_tri.valid = false;
     for (auto& f : g.fwd) {

@@ -26,6 +26,13 @@
 //     P_gmask[m/32+1], P_gpref[m/32+2]  bitmask of group-first records and
 //               its word-popcount prefix: the group index of a record in two
 //               loads (the triangle pass's group ends, tm_tri.cu)
+//     P_max32[m/32+1], P_max1k[m/1024+1], P_t32, P_t1k: fences -- P_max and
+//               P_t at every 32nd / 1024th record.  (min, max, t) is sorted
+//               over all of P, so a block or group search narrows over the
+//               1024-fence (2.3 MB at 600M edges: L2-resident), then one
+//               128-byte line of the 32-fence, then one line of P itself:
+//               B200's L2 fills a whole 128-byte line from HBM on every miss,
+//               so a plain binary search pays a line per level
 //   F (forward-oriented sequences for the triangle pass, one per orientation)
 #pragma once
 
@@ -199,6 +206,10 @@ struct DeviceGraph {
     uint32_t* P_dpref = nullptr;
     uint32_t* P_gmask = nullptr;
     uint32_t* P_gpref = nullptr;
+    uint32_t* P_max32 = nullptr;  // fences (P_max / P_t every 32nd and 1024th record)
+    uint32_t* P_max1k = nullptr;
+    TimeBuf P_t32;
+    TimeBuf P_t1k;
 
     Forward fwd[2];
     TriStage pre_tri;  // filter issued early for a one-shot count (RunHint)
@@ -232,6 +243,10 @@ struct PView {
     const uint32_t* gmask;
     const uint32_t* gpref;
     const uint32_t* gend;  // group ends by group index (triangle pass only; else null)
+    const uint32_t* max32;  // fences: P_max / P_t at every 32nd and 1024th record
+    const uint32_t* max1k;
+    TimeArr t32;
+    TimeArr t1k;
     // optional pair table: (min << 32 | max) -> group start << 32 | length,
     // replacing the binary search of max in min's block (hub blocks are long)
     const unsigned long long* pt_keys;
@@ -256,6 +271,73 @@ __device__ __forceinline__ uint32_t p_group_end(const PView& P, uint32_t x) {
 __device__ __forceinline__ uint32_t p_dir_before(const PView& P, uint32_t x) {
     return P.dpref[x >> 5] + __popc(P.dmask[x >> 5] & ((1u << (x & 31)) - 1u));
 }
+// Fenced lower bound: the first k in [lo, hi) with !less(A[k]) (hi if none),
+// A sorted w.r.t. `less` over [lo, hi).  The search narrows over the
+// 1024-fence (A at every 1024th position), then the 32-fence, then A: at most
+// ~2 HBM lines per search instead of one per binary-search level.
+template <class Arr, class F32, class F1K, class Less>
+__device__ __forceinline__ uint32_t fenced_lower_bound(uint32_t lo, uint32_t hi, const Arr& a, const F32& f32,
+                                                       const F1K& f1k, const Less& less) {
+    if (hi - lo > 2048) {
+        const uint32_t y0 = (lo + 1023) >> 10, y1 = ((hi - 1) >> 10) + 1;  // fence entries inside [lo, hi)
+        uint32_t l = y0, r = y1;
+        while (l < r) {
+            const uint32_t mid = (l + r) >> 1;
+            if (less(f1k(mid))) l = mid + 1; else r = mid;
+        }
+        if (l > y0) lo = ((l - 1) << 10) + 1;  // A[1024 (l-1)] is below the key
+        if (l < y1) hi = l << 10;              // A[1024 l] is not
+    }
+    if (hi - lo > 64) {
+        const uint32_t x0 = (lo + 31) >> 5, x1 = ((hi - 1) >> 5) + 1;
+        uint32_t l = x0, r = x1;
+        while (l < r) {
+            const uint32_t mid = (l + r) >> 1;
+            if (less(f32(mid))) l = mid + 1; else r = mid;
+        }
+        if (l > x0) lo = ((l - 1) << 5) + 1;
+        if (l < x1) hi = l << 5;
+    }
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (less(a(mid))) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+struct U32At {
+    const uint32_t* p;
+    __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return p[i]; }
+};
+struct TAt {
+    TimeArr t;
+    __device__ __forceinline__ int64_t operator()(uint32_t i) const { return t[i]; }
+};
+template <class V>
+struct Below {  // v < key
+    V key;
+    __device__ __forceinline__ bool operator()(V v) const { return v < key; }
+};
+template <class V>
+struct AtMost {  // v <= key
+    V key;
+    __device__ __forceinline__ bool operator()(V v) const { return v <= key; }
+};
+// first P position in [lo, hi) with P_max >= b (a block of one min endpoint)
+__device__ __forceinline__ uint32_t p_max_lower(const PView& P, uint32_t lo, uint32_t hi, uint32_t b) {
+    return fenced_lower_bound(lo, hi, U32At{P.max}, U32At{P.max32}, U32At{P.max1k}, Below<uint32_t>{b});
+}
+// first P position in [lo, hi) with P_max > b
+__device__ __forceinline__ uint32_t p_max_upper(const PView& P, uint32_t lo, uint32_t hi, uint32_t b) {
+    return fenced_lower_bound(lo, hi, U32At{P.max}, U32At{P.max32}, U32At{P.max1k}, AtMost<uint32_t>{b});
+}
+// first P position in [lo, hi) (one group) with t >= x
+__device__ __forceinline__ uint32_t p_t_lower(const PView& P, uint32_t lo, uint32_t hi, int64_t x) {
+    return fenced_lower_bound(lo, hi, TAt{P.t}, TAt{P.t32}, TAt{P.t1k}, Below<int64_t>{x});
+}
+// first P position in [lo, hi) (one group) with t > x
+__device__ __forceinline__ uint32_t p_t_upper(const PView& P, uint32_t lo, uint32_t hi, int64_t x) {
+    return fenced_lower_bound(lo, hi, TAt{P.t}, TAt{P.t32}, TAt{P.t1k}, AtMost<int64_t>{x});
+}
 inline SView sview(const DeviceGraph& g) {
     return {g.S_t.view(g.tbase), g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_opref, g.S_pidx, g.off};
 }
@@ -266,7 +348,8 @@ __device__ __forceinline__ uint32_t outward_before(const SView& S, uint32_t q) {
 
 inline PView pview(const DeviceGraph& g) {
     return {g.P_t.view(g.tbase), g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs, g.P_dmask, g.P_dpref,
-            g.P_gmask, g.P_gpref, nullptr, nullptr, nullptr, 0};
+            g.P_gmask, g.P_gpref, nullptr, g.P_max32, g.P_max1k, g.P_t32.view(g.tbase), g.P_t1k.view(g.tbase),
+            nullptr, nullptr, 0};
 }
 
 // ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------
@@ -323,8 +406,8 @@ uint64_t slice_edges(const uint32_t* d_src, const uint32_t* d_dst, const int64_t
                      cudaStream_t s);
 
 // raw star sums (32 u64: Pair[8], C[8], B[8], A[8]) for the centers
-// [c_begin, c_end) and instances whose first edge has t < t_end, added into d_out.
-void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end, int64_t t_end,
+// [c_begin, c_end) and instances whose first edge has t <= t_last (INT64_MAX: all), added into d_out.
+void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end, int64_t t_last,
                uint64_t* d_out, uint64_t* d_stats, cudaStream_t st);
 void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
                 const uint64_t* d_begin, const uint64_t* d_end, const uint64_t* d_item_off,
@@ -332,10 +415,10 @@ void star_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uin
                 uint64_t* d_out);
 // once-counted triangle cells (24 u64) over forward positions [f_begin, f_end)
 void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
-                  uint32_t f_end, int64_t t_end, uint64_t* d_out, uint64_t* d_stats);
+                  uint32_t f_end, int64_t t_last, uint64_t* d_out, uint64_t* d_stats);
 void tri_filter_stage(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin, uint32_t f_end,
                       cudaStream_t st, TriStage& ts);
-void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_t t_end, uint64_t* d_out,
+void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_t t_last, uint64_t* d_out,
                     uint64_t* d_stats);
 void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,
                const uint64_t* d_begin, const uint64_t* d_item_off, uint64_t total,

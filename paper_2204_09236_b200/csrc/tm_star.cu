@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256) star_filter_kernel(PView P, int64_t delta
 // Work: the full first_role / third_role sums for the surviving records.
 // The record's own S position is found by binary search of (t, ordinal) in
 // its center's time-ordered sequence.
-__global__ void __launch_bounds__(256, 5) star_work_kernel(SView S, PView P, int64_t delta, int64_t t_end,
+__global__ void __launch_bounds__(256, 5) star_work_kernel(SView S, PView P, int64_t delta, int64_t t_last,
                                                         const uint32_t* __restrict__ first_list,
                                                         const uint32_t* __restrict__ third_list,
                                                         const uint32_t* __restrict__ counters,
@@ -326,14 +326,14 @@ __global__ void __launch_bounds__(256, 5) star_work_kernel(SView S, PView P, int
             const uint32_t u = side ? P.max[k] : P.min[k];
             const uint32_t start = S.off[u], end = S.off[u + 1];
             const int64_t tk = P.t[k];
-            if (!(first && tk >= t_end)) {  // else: the instance's first edge is outside the time slice
+            if (!(first && tk > t_last)) {  // else: the instance's first edge is outside the time slice
                 const uint32_t q = bsearch_locate(S, start, end, tk, P.ord[k]);
                 if (first) {
                     first_role(S, P, q, k, side, start, end, delta, acc);
                 } else {
-                    // first edges restricted to t < t_end: a prefix of S_u
-                    const uint32_t re = t_end == INT64_MAX ? end - start
-                                                           : gallop_upper(S.t, start, end, t_end - 1) - start;
+                    // first edges restricted to t <= t_last: a prefix of S_u
+                    const uint32_t re = t_last == INT64_MAX ? end - start
+                                                            : gallop_upper(S.t, start, end, t_last) - start;
                     third_role(S, P, q, k, side, start, delta, 0u, re, acc);
                 }
             }
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(256) star_items_kernel(
 
 }  // namespace
 
-void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end, int64_t t_end,
+void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c_end, int64_t t_last,
                uint64_t* d_out, uint64_t* d_stats, cudaStream_t st) {
     if (c_end <= c_begin || g.m == 0) return;
     const uint64_t cap = (uint64_t)sm_count() * 8;
@@ -400,7 +400,7 @@ void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c
     TM_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(uint32_t), st));
     TM_LAUNCH("star_filter", st, star_filter_kernel, (unsigned)grid, 256, 0, pview(g), delta, g.m,
               c_begin, c_end, lists, lists + work, counters);
-    TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), delta, t_end,
+    TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), delta, t_last,
               lists,
               lists + work, counters, queue, d_out, d_stats);
     dfree(lists, st);

@@ -27,13 +27,14 @@ namespace {
 
 // counts of closing records for one wedge: c[type*2 + dk], dk relative to v.
 // The v-w list is the P group {min, max}: lower_bound of max in min's block.
-// t_end restricts to instances whose earliest edge has t < t_end (time-slice
-// partitions): the closing edge itself for type I, e_i otherwise.
+// t_last restricts to instances whose earliest edge has t <= t_last (time-slice
+// partitions; INT64_MAX = no bound): the closing edge itself for type I, e_i
+// otherwise.
 constexpr uint32_t kTableMinBlock = 256;
 
 __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint32_t w, int64_t lo,
                                                int64_t hi, int64_t ti, uint32_t oi, int64_t tj,
-                                               uint32_t oj, int64_t t_end, uint32_t c[6]) {
+                                               uint32_t oj, int64_t t_last, uint32_t c[6]) {
 #pragma unroll
     for (int j = 0; j < 6; ++j) c[j] = 0;
     const uint32_t a = min(v, w), b = max(v, w);
@@ -56,11 +57,7 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         known_end = kb + (uint32_t)val;
         blk_end = known_end;
     } else {
-        r = blk_end;
-        while (l < r) {
-            const uint32_t mid = (l + r) >> 1;
-            if (P.max[mid] < b) l = mid + 1; else r = mid;
-        }
+        l = p_max_lower(P, l, blk_end, b);
         if (l >= blk_end || P.max[l] != b) return;
         kb = l;
     }
@@ -78,34 +75,29 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
             if (tk < ti || (tk == ti && P.ord[k] < oi)) type = 0;
             else if (tk > tj || (tk == tj && P.ord[k] > oj)) type = 2;
             else type = 1;
-            if ((type == 0 ? tk : ti) < t_end) c[type * 2 + dk] += 1;
+            if ((type == 0 ? tk : ti) <= t_last) c[type * 2 + dk] += 1;
         }
         if (wk & kPLast) return;
     }
     // long group: its end (pair table, group index, or a gallop over P_max),
     // then binary searches of the window [k1, k4) and the type boundaries
     if (!known_end && P.gend) known_end = p_group_end(P, kb);
-    l = k;
-    r = blk_end;
-    for (uint32_t span = 16; !known_end; span <<= 1) {  // else gallop to the group end
-        const uint64_t probe = (uint64_t)l + span;
+    if (!known_end) known_end = p_max_upper(P, k, blk_end, b);
+    const uint32_t ke = known_end;
+    // window [k1, k4): the lower end by the fenced search, the upper end by a
+    // gallop from it (a window of a long group is short next to the group)
+    const uint32_t k1 = p_t_lower(P, k, ke, lo);
+    l = k1;
+    r = ke;
+    for (uint32_t span = 1;; span <<= 1) {
+        const uint64_t probe = (uint64_t)l + span - 1;
         if (probe >= r) break;
-        if (P.max[probe] > b) {
+        if (P.t[probe] > hi) {
             r = (uint32_t)probe;
             break;
         }
         l = (uint32_t)probe + 1;
     }
-    while (!known_end && l < r) {
-        const uint32_t mid = (l + r) >> 1;
-        if (P.max[mid] <= b) l = mid + 1; else r = mid;
-    }
-    if (!known_end) known_end = l;
-    const uint32_t ke = known_end;
-    l = k; r = ke;
-    while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] < lo) l = mid + 1; else r = mid; }
-    const uint32_t k1 = l;
-    r = ke;
     while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] <= hi) l = mid + 1; else r = mid; }
     const uint32_t k4 = l;
     l = k1; r = k4;  // k2: first (t, ord) > (ti, oi)
@@ -122,10 +114,10 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         if (tm < tj || (tm == tj && P.ord[mid] < oj)) l = mid + 1; else r = mid;
     }
     const uint32_t k3 = l;
-    uint32_t k2e = k2;  // type I records whose own t is before t_end
-    if (t_end != INT64_MAX) {
+    uint32_t k2e = k2;  // type I records whose own t is at most t_last
+    if (t_last != INT64_MAX) {
         l = k1; r = k2;
-        while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] < t_end) l = mid + 1; else r = mid; }
+        while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] <= t_last) l = mid + 1; else r = mid; }
         k2e = l;
     }
     // direction split of each type range from the P direction prefix
@@ -137,7 +129,7 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         c[type * 2 + (flip ^ 1u)] += n1;
     };
     add_range(0, k1, k2e);
-    if (ti < t_end) {
+    if (ti <= t_last) {
         add_range(1, k2, k3);
         add_range(2, k3, k4);
     }
@@ -266,11 +258,11 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(TimeArr FT,
 // base di * 4 + dj * 2 (cells type * 8 + base + dk)
 __device__ __forceinline__ int wedge_counts(const PView& P, TimeArr FT, const uint32_t* __restrict__ FN,
                                             const uint32_t* __restrict__ FO, uint32_t i, uint32_t j,
-                                            int64_t delta, int64_t t_end, uint32_t c[6]) {
+                                            int64_t delta, int64_t t_last, uint32_t c[6]) {
     const uint32_t ni = FN[i], nj = FN[j];
     const int64_t ti = FT[i], tj = FT[j];
     closing_counts(P, ni & kNodeMask, nj & kNodeMask, sat_sub(tj, delta), sat_add(ti, delta), ti,
-                   FO[i], tj, FO[j], t_end, c);
+                   FO[i], tj, FO[j], t_last, c);
     return (int)((ni >> 31) * 4 + (nj >> 31) * 2);
 }
 
@@ -278,7 +270,7 @@ __device__ __forceinline__ int wedge_counts(const PView& P, TimeArr FT, const ui
 __global__ void __launch_bounds__(256, 5) tri_wedge_kernel(PView P, TimeArr FT,
                                                         const uint32_t* __restrict__ FN,
                                                         const uint32_t* __restrict__ FO,
-                                                        int64_t delta, int64_t t_end,
+                                                        int64_t delta, int64_t t_last,
                                                         const uint64_t* __restrict__ wedges,
                                                         uint64_t wedge_cap,
                                                         const unsigned long long* __restrict__ wcount,
@@ -307,7 +299,7 @@ __global__ void __launch_bounds__(256, 5) tri_wedge_kernel(PView P, TimeArr FT,
         int cb = 0;
         if (idx < cnt) {
             const uint64_t w = wedges[idx];
-            cb = wedge_counts(P, FT, FN, FO, (uint32_t)(w >> 32), (uint32_t)w, delta, t_end, c);
+            cb = wedge_counts(P, FT, FN, FO, (uint32_t)(w >> 32), (uint32_t)w, delta, t_last, c);
         }
         wc.add6(idx < cnt, cb, c, cells, 24);
     }
@@ -323,7 +315,7 @@ __global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
                                                        const uint32_t* __restrict__ FO,
                                                        const uint32_t* __restrict__ Fnode,
                                                        const uint32_t* __restrict__ Foff,
-                                                       int64_t delta, int64_t t_end,
+                                                       int64_t delta, int64_t t_last,
                                                        const uint32_t* __restrict__ list,
                                                        const uint32_t* __restrict__ lcount,
                                                        const unsigned long long* __restrict__ pt_wsum,
@@ -354,7 +346,7 @@ __global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
             uint32_t c[6] = {0, 0, 0, 0, 0, 0};
             int cb = 0;
             if (wedge) {
-                cb = wedge_counts(P, FT, FN, FO, i, j, delta, t_end, c);
+                cb = wedge_counts(P, FT, FN, FO, i, j, delta, t_last, c);
                 ++my_wedges;
             }
             wc.add6(wedge, cb, c, cells, 24);
@@ -546,7 +538,7 @@ uint64_t group_end_min_wedges(const DeviceGraph& g) {
     return std::max<uint64_t>(g.m / 16, 1024);
 }
 
-void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_t t_end, uint64_t* d_out,
+void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_t t_last, uint64_t* d_out,
                     uint64_t* d_stats) {
     if (!ts.valid) return;
     cudaStream_t st = g.stream;
@@ -566,7 +558,7 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
         pv.gend = ts.gend;
     }
     TM_LAUNCH("tri_wedge", st, tri_wedge_kernel, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
-              ts.delta, t_end, ts.wedges, ts.wedge_cap, wcount, ts.wsum, gend_min, ts.queue, d_out, d_stats);
+              ts.delta, t_last, ts.wedges, ts.wedge_cap, wcount, ts.wsum, gend_min, ts.queue, d_out, d_stats);
     // pair table for the long windows when they hold many wedges: the
     // table costs ~one random insert per P group, and replaces the block
     // search of each long-window wedge
@@ -590,7 +582,7 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
         pv.pt_mask = pc - 1;
     }
     TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
-              f.node, f.off, ts.delta, t_end, ts.long_list, lcount, ts.wsum, min_wedges, gend_min, ts.queue + 1, d_out,
+              f.node, f.off, ts.delta, t_last, ts.long_list, lcount, ts.wsum, min_wedges, gend_min, ts.queue + 1, d_out,
               d_stats);
     dfree(ts.pt, st);
     dfree(ts.gend, st);
@@ -603,10 +595,10 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
 }
 
 void tri_oriented(const DeviceGraph& g, const Forward& f, int64_t delta, uint32_t f_begin,
-                  uint32_t f_end, int64_t t_end, uint64_t* d_out, uint64_t* d_stats) {
+                  uint32_t f_end, int64_t t_last, uint64_t* d_out, uint64_t* d_stats) {
     TriStage ts;
     tri_filter_stage(g, f, delta, f_begin, f_end, g.stream, ts);
-    tri_work_stage(g, f, ts, t_end, d_out, d_stats);
+    tri_work_stage(g, f, ts, t_last, d_out, d_stats);
 }
 
 void tri_items(const DeviceGraph& g, int64_t delta, uint64_t n_items, const uint32_t* d_nodes,

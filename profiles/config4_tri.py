@@ -11,7 +11,7 @@ import torch  # noqa: E402
 import paper_2204_09236_b200 as tm  # noqa: E402
 from paper_2204_09236_b200 import synth  # noqa: E402
 
-n, s, d, t = synth.power_law_gpu(50_000_000, 600_000_000, 0.05)
+n, s, d, t = synth.power_law_hashed(device="cuda")
 torch.cuda.synchronize()
 ctx = tm.GraphContext.build_device(n, s.data_ptr(), d.data_ptr(), t.data_ptr(), s.numel())
 t0 = time.time()

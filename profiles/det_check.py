@@ -6,7 +6,7 @@ sys.path.insert(0, os.getcwd())
 import torch, numpy as np
 import paper_2204_09236_b200 as tm
 from paper_2204_09236_b200 import synth
-n, src, dst, t = synth.power_law_gpu(50_000_000, 600_000_000, 0.05)
+n, src, dst, t = synth.power_law_hashed(device="cuda")
 torch.cuda.synchronize()
 h = hashlib.sha1()
 for a in (src, dst, t):

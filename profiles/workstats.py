@@ -31,5 +31,5 @@ def run(name, n, src, dst, t, deltas):
 if __name__ == "__main__":
     run("powerlaw_1m_10m", *synth.power_law(), [600, 3600, 86400])
     run("hubstress_100k_50m", *synth.hub_stress_gpu(), [600, 3600])
-    run("triadic_25m_100m", *synth.triadic_gpu(), [3600, 86400])
-    run("powerlaw_50m_600m", *synth.power_law_gpu(50_000_000, 600_000_000, 0.05), [600, 3600, 86400])
+    run("triadic_25m_100m", *synth.triadic_hashed(device="cuda"), [3600, 86400])
+    run("powerlaw_50m_600m", *synth.power_law_hashed(device="cuda"), [600, 3600, 86400])
