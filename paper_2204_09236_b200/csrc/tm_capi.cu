@@ -51,8 +51,11 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// With timing on, every launch runs alone (device synchronised on both
+// sides), so a kernel's time is its own and not shared with side-stream work.
 KernelScope::KernelScope(const char* n, cudaStream_t s) : name(n), stream(s), ev0(nullptr) {
     if (g_timing.load(std::memory_order_relaxed)) {
+        cudaDeviceSynchronize();
         cudaEvent_t e;
         if (cudaEventCreate(&e) == cudaSuccess) {
             cudaEventRecord(e, s);
@@ -65,6 +68,7 @@ KernelScope::~KernelScope() {
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) return;
     cudaEventRecord(e, stream);
+    cudaDeviceSynchronize();
     std::lock_guard<std::mutex> lk(g_timing_mu);
     g_pending.push_back({name, static_cast<cudaEvent_t>(ev0), e});
 }
@@ -888,6 +892,7 @@ struct AsyncSlot {
     uint64_t cap = 0;
     cudaEvent_t copied = nullptr, done = nullptr;
     bool busy = false, pending = false;
+    bool deferred = false;  // large batch: census not yet issued (runs when the next batch is submitted)
     uint64_t ticket = 0, m = 0, n = 0;
     cudaStream_t s = nullptr;
     tm_run_config cfg;
@@ -914,9 +919,30 @@ struct AsyncPipe {
 };
 thread_local AsyncPipe g_async;
 
+// A batch above the replay size is counted eagerly, and an eager count syncs
+// the host (the build verdict).  Its census is therefore issued only when the
+// next batch has been submitted -- after that batch's host->device copy is
+// queued on the copy stream -- so the copy of batch i+1 overlaps the census of
+// batch i.
+void run_deferred(AsyncSlot& sl) {
+    if (!sl.deferred) return;
+    sl.deferred = false;
+    const int rc = tm_count_edges(sl.ds, sl.dd, sl.dt, sl.m, sl.n, 1, sl.s, &sl.cfg, &sl.res.raw, sl.res.census,
+                                  nullptr);
+    sl.res.rc = rc;
+    if (rc != TM_OK) sl.res.err = g_last_error;
+    TM_CUDA(cudaEventRecord(sl.done, sl.s));
+}
+
 // run the slot's census to completion (speculation checked, re-run if needed)
 AsyncResult finish_slot(AsyncSlot& sl) {
     AsyncResult out;
+    try {
+        run_deferred(sl);
+    } catch (const tm_error& e) {
+        sl.res.rc = e.code;
+        sl.res.err = e.what();
+    }
     try {
         if (sl.pending) {
             sl.pending = false;
@@ -1412,6 +1438,7 @@ int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t
         sl.s = s;
         sl.cfg = *cfg;
         sl.pending = false;
+        sl.deferred = false;
         sl.res = AsyncResult();
         // copy stream: wait until the slot's previous census stopped reading it
         TM_CUDA(cudaStreamWaitEvent(A.copy, sl.done, 0));
@@ -1422,12 +1449,26 @@ int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t
         }
         TM_CUDA(cudaEventRecord(sl.copied, A.copy));
         TM_CUDA(cudaStreamWaitEvent(s, sl.copied, 0));
+        // the previous batch's deferred census runs now, behind this copy
+        AsyncSlot& prev = A.slot[(tk & 1) ^ 1];
+        if (prev.busy && prev.deferred) {
+            try {
+                run_deferred(prev);
+            } catch (const tm_error& e) {
+                prev.res.rc = e.code;
+                prev.res.err = e.what();
+            }
+        }
+        if (m && !(m <= kReplayMaxEdges && replay_enabled())) {
+            sl.deferred = true;  // eager (host-synchronous) count: issued with the next submission or the wait
+            *ticket = tk;
+            return TM_OK;
+        }
         try {
-            int rc;
-            if (m && m <= kReplayMaxEdges && replay_enabled())
-                rc = count_edges_replay(sl.ds, sl.dd, sl.dt, m, n, 1, s, cfg, &sl.res.raw, sl.res.census, &sl.P);
-            else  // eager (and synchronous) for very large batches
-                rc = tm_count_edges(sl.ds, sl.dd, sl.dt, m, n, 1, s, cfg, &sl.res.raw, sl.res.census, nullptr);
+            const int rc = m ? count_edges_replay(sl.ds, sl.dd, sl.dt, m, n, 1, s, cfg, &sl.res.raw, sl.res.census,
+                                                  &sl.P)
+                             : tm_count_edges(sl.ds, sl.dd, sl.dt, m, n, 1, s, cfg, &sl.res.raw, sl.res.census,
+                                              nullptr);
             sl.pending = rc == kPending;
             if (!sl.pending) {
                 sl.res.rc = rc;

@@ -175,7 +175,9 @@ __global__ void gather_s_kernel(const typename EdgeCodec<kNarrow>::Rec* __restri
                                 int64_t* __restrict__ S_tw, uint32_t* __restrict__ S_tn,
                                 uint32_t* __restrict__ S_nbr,
                                 uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
-                                uint32_t* __restrict__ omask, uint32_t* __restrict__ xmask) {
+                                uint32_t* __restrict__ omask, uint32_t* __restrict__ xmask,
+                                int64_t* __restrict__ t32w, uint32_t* __restrict__ t32n,
+                                int64_t* __restrict__ t1kw, uint32_t* __restrict__ t1kn) {
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t q = base + threadIdx.x;
@@ -196,6 +198,14 @@ __global__ void gather_s_kernel(const typename EdgeCodec<kNarrow>::Rec* __restri
             mx = x < u ? 1u : 0u;  // u is the pair's larger endpoint
             if (kNarrow) __stcs(S_tn + q, Codec::rel(e));
             else __stcs(S_tw + q, Codec::time(e, tmin));
+            if ((q & 31) == 0) {  // the fences (tm_internal.cuh fenced_lower_bound)
+                if (kNarrow) t32n[q >> 5] = Codec::rel(e);
+                else t32w[q >> 5] = Codec::time(e, tmin);
+                if ((q & 1023) == 0) {
+                    if (kNarrow) t1kn[q >> 10] = Codec::rel(e);
+                    else t1kw[q >> 10] = Codec::time(e, tmin);
+                }
+            }
             __stcs(S_ord + q, p);
             __stcs(S_node + q, u);
             __stcs(S_nbr + q, x | (side << 31));
@@ -606,6 +616,13 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
     g.tbase = narrow ? tmin : 0;
     if (narrow) g.S_t.n = dalloc<uint32_t>(R, s);
     else g.S_t.w = dalloc<int64_t>(R, s);
+    if (narrow) {
+        g.S_t32.n = dalloc<uint32_t>(R / 32 + 1, s);
+        g.S_t1k.n = dalloc<uint32_t>(R / 1024 + 1, s);
+    } else {
+        g.S_t32.w = dalloc<int64_t>(R / 32 + 1, s);
+        g.S_t1k.w = dalloc<int64_t>(R / 1024 + 1, s);
+    }
     g.S_nbr = dalloc<uint32_t>(R, s);
     g.S_ord = dalloc<uint32_t>(R, s);
     g.S_node = dalloc<uint32_t>(R, s);
@@ -707,10 +724,12 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         TM_CUDA(cudaMemsetAsync(xmask + (nw - 1), 0, sizeof(uint32_t), s));
         if (narrow)
             TM_LAUNCH("gather_s", s, gather_s_kernel<true>, grid_for(R), 256, 0, EN, tmin, nk0, R, n, g.off,
-                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask);
+                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask, g.S_t32.w, g.S_t32.n,
+                      g.S_t1k.w, g.S_t1k.n);
         else
             TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, EW, tmin, nk0, R, n, g.off,
-                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask);
+                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask, g.S_t32.w, g.S_t32.n,
+                      g.S_t1k.w, g.S_t1k.n);
         // outward prefix (stars) and max-side prefix (pair keys) in one scan
         exclusive_scan_to<uint64_t>(PopcLoad2{g.S_omask, xmask}, nw, SplitStore2{g.S_opref, xpref}, s);
 
@@ -855,6 +874,7 @@ void free_graph(DeviceGraph& g) {
     dfree(g.S_t.w, s); dfree(g.S_t.n, s); dfree(g.S_nbr, s); dfree(g.S_ord, s); dfree(g.S_node, s);
     dfree(g.S_omask, s); dfree(g.S_opref, s); dfree(g.S_fmask, s); dfree(g.S_pidx, s);
     dfree(g.off, s);
+    dfree(g.S_t32.w, s); dfree(g.S_t32.n, s); dfree(g.S_t1k.w, s); dfree(g.S_t1k.n, s);
     dfree(g.P_t.w, s); dfree(g.P_t.n, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
     dfree(g.P_min, s); dfree(g.pofs, s); dfree(g.P_dmask, s); dfree(g.P_dpref, s);
     dfree(g.P_gmask, s); dfree(g.P_gpref, s);

@@ -195,6 +195,8 @@ struct DeviceGraph {
     uint32_t* S_fmask = nullptr;  // forward (degree orientation) bitmask, same layout
     uint32_t* S_pidx = nullptr;
     uint32_t* off = nullptr;
+    TimeBuf S_t32;  // fences: S_t at every 32nd / 1024th record (fenced_lower_bound)
+    TimeBuf S_t1k;
 
     TimeBuf P_t;
     uint32_t* P_ord = nullptr;
@@ -230,6 +232,8 @@ struct SView {
     const uint32_t* opref;
     const uint32_t* pidx;
     const uint32_t* off;
+    TimeArr t32;  // fences: S_t at every 32nd and 1024th record
+    TimeArr t1k;
 };
 struct PView {
     TimeArr t;
@@ -271,75 +275,106 @@ __device__ __forceinline__ uint32_t p_group_end(const PView& P, uint32_t x) {
 __device__ __forceinline__ uint32_t p_dir_before(const PView& P, uint32_t x) {
     return P.dpref[x >> 5] + __popc(P.dmask[x >> 5] & ((1u << (x & 31)) - 1u));
 }
-// Fenced lower bound: the first k in [lo, hi) with !less(A[k]) (hi if none),
-// A sorted w.r.t. `less` over [lo, hi).  The search narrows over the
-// 1024-fence (A at every 1024th position), then the 32-fence, then A: at most
-// ~2 HBM lines per search instead of one per binary-search level.
-template <class Arr, class F32, class F1K, class Less>
-__device__ __forceinline__ uint32_t fenced_lower_bound(uint32_t lo, uint32_t hi, const Arr& a, const F32& f32,
-                                                       const F1K& f1k, const Less& less) {
+// Fenced lower bound: the first k in [lo, hi) with !below(k) (hi if none),
+// for keys sorted over [lo, hi).  The probe answers "is the key at position
+// k below the target" at three levels: the array itself (below0(k)), its
+// 32-fence (below32(x): the key at 32x) and its 1024-fence (below1k(y): the
+// key at 1024y).  The search narrows over the 1024-fence (L2-resident), then
+// the 32-fence, then the array: about two HBM lines per search instead of
+// one per binary-search level.
+template <class Probe>
+__device__ __forceinline__ uint32_t fenced_lower_bound(uint32_t lo, uint32_t hi, const Probe& pr) {
     if (hi - lo > 2048) {
         const uint32_t y0 = (lo + 1023) >> 10, y1 = ((hi - 1) >> 10) + 1;  // fence entries inside [lo, hi)
         uint32_t l = y0, r = y1;
         while (l < r) {
             const uint32_t mid = (l + r) >> 1;
-            if (less(f1k(mid))) l = mid + 1; else r = mid;
+            if (pr.below1k(mid)) l = mid + 1; else r = mid;
         }
-        if (l > y0) lo = ((l - 1) << 10) + 1;  // A[1024 (l-1)] is below the key
-        if (l < y1) hi = l << 10;              // A[1024 l] is not
+        if (l > y0) lo = ((l - 1) << 10) + 1;  // the key at 1024 (l-1) is below the target
+        if (l < y1) hi = l << 10;              // the key at 1024 l is not
     }
     if (hi - lo > 64) {
         const uint32_t x0 = (lo + 31) >> 5, x1 = ((hi - 1) >> 5) + 1;
         uint32_t l = x0, r = x1;
         while (l < r) {
             const uint32_t mid = (l + r) >> 1;
-            if (less(f32(mid))) l = mid + 1; else r = mid;
+            if (pr.below32(mid)) l = mid + 1; else r = mid;
         }
         if (l > x0) lo = ((l - 1) << 5) + 1;
         if (l < x1) hi = l << 5;
     }
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (less(a(mid))) lo = mid + 1; else hi = mid;
+        if (pr.below0(mid)) lo = mid + 1; else hi = mid;
     }
     return lo;
 }
-struct U32At {
-    const uint32_t* p;
-    __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return p[i]; }
+// keys of one u32 array + its fences: v < key (kStrict) or v <= key
+template <bool kStrict>
+struct U32Probe {
+    const uint32_t* a;
+    const uint32_t* f32;
+    const uint32_t* f1k;
+    uint32_t key;
+    __device__ __forceinline__ bool cmp(uint32_t v) const { return kStrict ? v < key : v <= key; }
+    __device__ __forceinline__ bool below0(uint32_t k) const { return cmp(a[k]); }
+    __device__ __forceinline__ bool below32(uint32_t x) const { return cmp(f32[x]); }
+    __device__ __forceinline__ bool below1k(uint32_t y) const { return cmp(f1k[y]); }
 };
-struct TAt {
-    TimeArr t;
-    __device__ __forceinline__ int64_t operator()(uint32_t i) const { return t[i]; }
-};
-template <class V>
-struct Below {  // v < key
-    V key;
-    __device__ __forceinline__ bool operator()(V v) const { return v < key; }
-};
-template <class V>
-struct AtMost {  // v <= key
-    V key;
-    __device__ __forceinline__ bool operator()(V v) const { return v <= key; }
+template <bool kStrict>
+struct TProbe {
+    TimeArr a, f32, f1k;
+    int64_t key;
+    __device__ __forceinline__ bool cmp(int64_t v) const { return kStrict ? v < key : v <= key; }
+    __device__ __forceinline__ bool below0(uint32_t k) const { return cmp(a[k]); }
+    __device__ __forceinline__ bool below32(uint32_t x) const { return cmp(f32[x]); }
+    __device__ __forceinline__ bool below1k(uint32_t y) const { return cmp(f1k[y]); }
 };
 // first P position in [lo, hi) with P_max >= b (a block of one min endpoint)
 __device__ __forceinline__ uint32_t p_max_lower(const PView& P, uint32_t lo, uint32_t hi, uint32_t b) {
-    return fenced_lower_bound(lo, hi, U32At{P.max}, U32At{P.max32}, U32At{P.max1k}, Below<uint32_t>{b});
+    return fenced_lower_bound(lo, hi, U32Probe<true>{P.max, P.max32, P.max1k, b});
 }
 // first P position in [lo, hi) with P_max > b
 __device__ __forceinline__ uint32_t p_max_upper(const PView& P, uint32_t lo, uint32_t hi, uint32_t b) {
-    return fenced_lower_bound(lo, hi, U32At{P.max}, U32At{P.max32}, U32At{P.max1k}, AtMost<uint32_t>{b});
+    return fenced_lower_bound(lo, hi, U32Probe<false>{P.max, P.max32, P.max1k, b});
 }
 // first P position in [lo, hi) (one group) with t >= x
 __device__ __forceinline__ uint32_t p_t_lower(const PView& P, uint32_t lo, uint32_t hi, int64_t x) {
-    return fenced_lower_bound(lo, hi, TAt{P.t}, TAt{P.t32}, TAt{P.t1k}, Below<int64_t>{x});
+    return fenced_lower_bound(lo, hi, TProbe<true>{P.t, P.t32, P.t1k, x});
 }
 // first P position in [lo, hi) (one group) with t > x
 __device__ __forceinline__ uint32_t p_t_upper(const PView& P, uint32_t lo, uint32_t hi, int64_t x) {
-    return fenced_lower_bound(lo, hi, TAt{P.t}, TAt{P.t32}, TAt{P.t1k}, AtMost<int64_t>{x});
+    return fenced_lower_bound(lo, hi, TProbe<false>{P.t, P.t32, P.t1k, x});
+}
+// S positions in one node's sequence [lo, hi): first with t >= x / t > x
+__device__ __forceinline__ uint32_t s_t_lower(const SView& S, uint32_t lo, uint32_t hi, int64_t x) {
+    return fenced_lower_bound(lo, hi, TProbe<true>{S.t, S.t32, S.t1k, x});
+}
+__device__ __forceinline__ uint32_t s_t_upper(const SView& S, uint32_t lo, uint32_t hi, int64_t x) {
+    return fenced_lower_bound(lo, hi, TProbe<false>{S.t, S.t32, S.t1k, x});
+}
+// the S position of record (t, ord) in one node's sequence [lo, hi): first
+// (t', ord') >= (t, ord); a fence key equal in t reads the ordinal at its
+// position (ties are rare but unbounded: a tie-heavy sequence stays O(log))
+struct SRecProbe {
+    SView S;
+    int64_t t;
+    uint32_t ord;
+    __device__ __forceinline__ bool at(int64_t tp, uint32_t p) const {
+        return tp < t || (tp == t && (S.ord[p] & kNodeMask) < ord);
+    }
+    __device__ __forceinline__ bool below0(uint32_t k) const { return at(S.t[k], k); }
+    __device__ __forceinline__ bool below32(uint32_t x) const { return at(S.t32[x], x << 5); }
+    __device__ __forceinline__ bool below1k(uint32_t y) const { return at(S.t1k[y], y << 10); }
+};
+__device__ __forceinline__ uint32_t s_locate_fenced(const SView& S, uint32_t lo, uint32_t hi, int64_t t,
+                                                    uint32_t ord) {
+    return fenced_lower_bound(lo, hi, SRecProbe{S, t, ord});
 }
 inline SView sview(const DeviceGraph& g) {
-    return {g.S_t.view(g.tbase), g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_opref, g.S_pidx, g.off};
+    return {g.S_t.view(g.tbase), g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_opref, g.S_pidx, g.off,
+            g.S_t32.view(g.tbase), g.S_t1k.view(g.tbase)};
 }
 // global exclusive count of outward records before S position q
 __device__ __forceinline__ uint32_t outward_before(const SView& S, uint32_t q) {

@@ -113,14 +113,6 @@ __device__ __forceinline__ uint32_t gallop_locate(const SView& S, uint32_t lo, u
     }
     return a;
 }
-__device__ __forceinline__ uint32_t bsearch_locate(const SView& S, uint32_t lo, uint32_t hi, int64_t t,
-                                                   uint32_t ord) {
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s_before(S, mid, t, ord)) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
 __device__ __forceinline__ uint32_t gallop_locate_back(const SView& S, uint32_t lo, uint32_t hi,
                                                        int64_t t, uint32_t ord) {
     uint32_t a = lo, b = hi, span = 1;
@@ -294,10 +286,182 @@ __global__ void __launch_bounds__(256) star_filter_kernel(PView P, int64_t delta
     }
 }
 
-// Work: the full first_role / third_role sums for the surviving records.
-// The record's own S position is found by binary search of (t, ordinal) in
-// its center's time-ordered sequence.
-__global__ void __launch_bounds__(256, 5) star_work_kernel(SView S, PView P, int64_t delta, int64_t t_last,
+// ---- full pass: the candidates' S positions first, then the sums --------
+//
+// Every member of a candidate's window is itself a candidate: a record after
+// first edge a inside its window has its predecessor within delta (so it is a
+// third-edge candidate), and a record before third edge c inside c's window
+// has its successor within delta (a first-edge candidate).  star_locate
+// therefore finds the S position q (and the outward count before it) of every
+// candidate once -- a fenced search in its center's sequence -- into the
+// P-indexed planes PS[side][k]; star_work then walks each window's members
+// through PS (contiguous 8-byte reads) instead of locating every member in
+// S_u again, which cost a gallop of scattered 128-byte lines per member.
+
+// S position of the first record after q with t > lim (end if none): a
+// short gallop (the window is usually a few lines), then the fenced search
+__device__ __forceinline__ uint32_t s_window_end(const SView& S, uint32_t q, uint32_t end, int64_t lim) {
+    uint32_t lo = q + 1;
+    for (uint32_t span = 1; span <= 32; span <<= 1) {
+        const uint64_t probe = (uint64_t)lo + span - 1;
+        if (probe >= end) return fenced_lower_bound(lo, end, TProbe<false>{S.t, S.t32, S.t1k, lim});
+        if (S.t[probe] > lim) return fenced_lower_bound(lo, (uint32_t)probe, TProbe<false>{S.t, S.t32, S.t1k, lim});
+        lo = (uint32_t)probe + 1;
+    }
+    return fenced_lower_bound(lo, end, TProbe<false>{S.t, S.t32, S.t1k, lim});
+}
+// first S position in [start, q] with t >= lim (q itself when none before)
+__device__ __forceinline__ uint32_t s_window_begin(const SView& S, uint32_t start, uint32_t q, int64_t lim) {
+    uint32_t hi = q;
+    for (uint32_t span = 1; span <= 32; span <<= 1) {
+        if (hi - start < span) return fenced_lower_bound(start, hi, TProbe<true>{S.t, S.t32, S.t1k, lim});
+        const uint32_t probe = hi - span;
+        if (S.t[probe] < lim) return fenced_lower_bound(probe + 1, hi, TProbe<true>{S.t, S.t32, S.t1k, lim});
+        hi = probe;
+    }
+    return fenced_lower_bound(start, hi, TProbe<true>{S.t, S.t32, S.t1k, lim});
+}
+
+__global__ void __launch_bounds__(256) star_locate_kernel(SView S, PView P, uint64_t m,
+                                                          const uint32_t* __restrict__ first_list,
+                                                          const uint32_t* __restrict__ third_list,
+                                                          const uint32_t* __restrict__ counters,
+                                                          uint2* __restrict__ PS) {
+    const uint32_t nf = counters[0], nt = counters[1];
+    const uint64_t total = (uint64_t)nf + nt;
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = idx < nf ? first_list[idx] : third_list[idx - nf];
+        const uint32_t k = e >> 1, side = e & 1u;
+        const uint32_t u = side ? P.max[k] : P.min[k];
+        const uint32_t q = s_locate_fenced(S, S.off[u], S.off[u + 1], P.t[k], P.ord[k]);
+        PS[(uint64_t)side * m + k] = make_uint2(q, outward_before(S, q));
+    }
+}
+
+// first-edge role of candidate k at center u (side), S position q = PS: Pair, A, B
+__device__ __forceinline__ void first_role_ps(const SView& S, const PView& P, const uint2* __restrict__ PSs,
+                                              uint32_t q, uint32_t ob_q, uint32_t k, uint32_t side,
+                                              uint32_t start, uint32_t end, int64_t delta, uint64_t pair[4],
+                                              uint64_t a[4], uint64_t b[4], uint32_t& da) {
+    const uint32_t wa = P.w[k];
+    const int64_t ta = P.t[k];
+    da = (wa >> 31) ^ side;  // 0: outward from u
+    const int64_t lim = sat_add(ta, delta);
+    if ((wa & kPLast) || P.t[k + 1] > lim) return;  // no same-neighbour record in the window
+    const uint32_t base = outward_before(S, start);
+    const uint32_t e = s_window_end(S, q, end, lim);
+    const uint64_t pe_o = outward_before(S, e) - base, pe_i = (uint64_t)(e - start) - pe_o;
+    const uint64_t pa_o = (uint64_t)(ob_q - base) + (da ? 0u : 1u);
+    const uint64_t pa_i = (uint64_t)(q - start + 1) - pa_o;
+    uint64_t n0 = 0, n1 = 0;
+    uint64_t A00 = 0, A01 = 0, A10 = 0, A11 = 0;   // A[d2][d3]: sum [dir_b=d2] P_d3(b+1)
+    uint64_t B00 = 0, B01 = 0, B10 = 0, B11 = 0;   // B[d3][d2]: sum [dir_c=d3] P_d2(c)
+    uint64_t P00 = 0, P01 = 0, P10 = 0, P11 = 0;   // Pair[d2][d3]
+    for (uint32_t j = k + 1;; ++j) {
+        if (P.t[j] > lim) break;
+        const uint32_t w = P.w[j];
+        const uint2 ps = PSs[j];
+        const uint64_t pos = ps.x - start;
+        const uint64_t pb_o = ps.y - base;
+        const uint64_t pb_i = pos - pb_o;
+        if ((w >> 31) ^ side) {  // inward relative to u
+            A10 += pb_o;
+            A11 += pos + 1 - pb_o;
+            B10 += pb_o;
+            B11 += pb_i;
+            P01 += n0;
+            P11 += n1;
+            ++n1;
+        } else {
+            A00 += pb_o + 1;
+            A01 += pos - pb_o;
+            B00 += pb_o;
+            B01 += pb_i;
+            P00 += n0;
+            P10 += n1;
+            ++n0;
+        }
+        if (w & kPLast) break;
+    }
+    pair[0] = P00; pair[1] = P01; pair[2] = P10; pair[3] = P11;
+    // A(d2,d3) = n[d2] * P_d3(e) - Aacc[d2][d3]
+    a[0] = n0 * pe_o - A00; a[1] = n0 * pe_i - A01; a[2] = n1 * pe_o - A10; a[3] = n1 * pe_i - A11;
+    // B(d2,d3) = Bacc[d3][d2] - n[d3] * P_d2(a+1)
+    b[0] = B00 - n0 * pa_o; b[1] = B10 - n1 * pa_o; b[2] = B01 - n0 * pa_i; b[3] = B11 - n1 * pa_i;
+}
+
+// third-edge role of candidate k at center u (side), S position q = PS: the
+// Star-I pair term C, x[d1*2 + d2]; first edges restricted to the local
+// prefix [0, re) of S_u (time slices), dc = the third edge's direction
+__device__ __forceinline__ void third_role_ps(const SView& S, const PView& P, const uint2* __restrict__ PSs,
+                                              uint32_t q, uint32_t k, uint32_t side, uint32_t start,
+                                              int64_t delta, uint32_t re, uint64_t x[4], uint32_t& dc) {
+    const uint32_t wc = P.w[k];
+    dc = (wc >> 31) ^ side;
+    if (wc & kPFirst) return;
+    const int64_t lo_lim = sat_sub(P.t[k], delta);
+    if (P.t[k - 1] < lo_lim) return;  // previous same-neighbour record already before the window
+    const uint32_t lo = s_window_begin(S, start, q, lo_lim);
+    if (lo >= q) return;
+    const uint32_t pl = outward_before(S, lo);
+    const uint32_t hiq = start + re;
+    const uint32_t o_hiq = hiq < q ? outward_before(S, hiq) : 0u;
+    for (uint32_t j = k - 1;; --j) {
+        // a record before the window is no candidate (its PS entry is not
+        // written): stop on its time first; in-window members are candidates
+        if (P.t[j] < lo_lim) break;
+        const uint2 ps = PSs[j];
+        if (ps.x <= lo) break;  // the member at the window start itself
+        const uint32_t w = P.w[j];
+        const uint32_t mhi = min(ps.x, hiq);
+        if (mhi > lo) {
+            const uint64_t xo = (uint64_t)((mhi == ps.x ? ps.y : o_hiq) - pl);
+            const uint64_t yi = (uint64_t)(mhi - lo) - xo;
+            const int d2 = (int)(((w >> 31) ^ side));
+            x[d2] += xo;      // d1 = out
+            x[2 + d2] += yi;  // d1 = in
+        }
+        if (w & kPFirst) break;
+    }
+}
+
+// exact warp sum of a u64 (three 22-bit chunks through redux.sync): the
+// total as a 128-bit (lo, hi) pair
+__device__ __forceinline__ void warp_sum_u64(uint64_t v, uint64_t& lo, uint32_t& hi) {
+    const uint32_t a = __reduce_add_sync(0xffffffffu, (uint32_t)v & 0x3fffffu);
+    const uint32_t b = __reduce_add_sync(0xffffffffu, (uint32_t)(v >> 22) & 0x3fffffu);
+    const uint32_t c = __reduce_add_sync(0xffffffffu, (uint32_t)(v >> 44));
+    const unsigned __int128 t = (unsigned __int128)a + ((unsigned __int128)b << 22) + ((unsigned __int128)c << 44);
+    lo = (uint64_t)t;
+    hi = (uint32_t)(t >> 64);
+}
+
+// lane L holds star raw cell L (32 cells) with its wrap count
+struct StarLaneCell {
+    uint64_t mine = 0;
+    uint32_t wraps = 0;
+    // warp-wide: add v (per lane) into cell `cell` (per lane; -1 = none)
+    __device__ __forceinline__ void add(int cell, uint64_t v, int c0, int c1) {
+        // the lanes' cells are one of {c0, c1} (or none): one exact sum each
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = h ? c1 : c0;
+            if (!__any_sync(0xffffffffu, cell == c && v)) continue;
+            uint64_t lo;
+            uint32_t hi;
+            warp_sum_u64(cell == c ? v : 0ull, lo, hi);
+            if ((int)(threadIdx.x & 31) == c) {
+                const uint64_t nm = mine + lo;
+                wraps += hi + (nm < mine ? 1u : 0u);
+                mine = nm;
+            }
+        }
+    }
+};
+
+__global__ void __launch_bounds__(256, 4) star_work_kernel(SView S, PView P, int64_t delta, int64_t t_last,
+                                                        uint64_t m, const uint2* __restrict__ PS,
                                                         const uint32_t* __restrict__ first_list,
                                                         const uint32_t* __restrict__ third_list,
                                                         const uint32_t* __restrict__ counters,
@@ -311,34 +475,53 @@ __global__ void __launch_bounds__(256, 5) star_work_kernel(SView S, PView P, int
         stats[1] = counters[1];
     }
     __syncthreads();
-    const SmemSink acc{cells, 32};
+    StarLaneCell lc;
     const uint32_t nf = counters[0], nt = counters[1];
     const uint64_t total = (uint64_t)nf + nt;
     for (;;) {  // 32 items per warp from the queue (hub items are heavy-tailed)
         const uint64_t base = warp_take(queue, 32);
         if (base >= total) break;
         const uint64_t idx = base + (threadIdx.x & 31);
-        // no early continue: the warp reconverges at the next warp_take
+        uint64_t pr[4] = {0, 0, 0, 0}, av[4] = {0, 0, 0, 0}, bv[4] = {0, 0, 0, 0}, xv[4] = {0, 0, 0, 0};
+        uint32_t d1 = 0, dc = 0;
+        bool is_first = false, is_third = false;
         if (idx < total) {
             const bool first = idx < nf;
             const uint32_t e = first ? first_list[idx] : third_list[idx - nf];
             const uint32_t k = e >> 1, side = e & 1u;
             const uint32_t u = side ? P.max[k] : P.min[k];
             const uint32_t start = S.off[u], end = S.off[u + 1];
-            const int64_t tk = P.t[k];
-            if (!(first && tk > t_last)) {  // else: the instance's first edge is outside the time slice
-                const uint32_t q = bsearch_locate(S, start, end, tk, P.ord[k]);
-                if (first) {
-                    first_role(S, P, q, k, side, start, end, delta, acc);
-                } else {
-                    // first edges restricted to t <= t_last: a prefix of S_u
-                    const uint32_t re = t_last == INT64_MAX ? end - start
-                                                            : gallop_upper(S.t, start, end, t_last) - start;
-                    third_role(S, P, q, k, side, start, delta, 0u, re, acc);
+            const uint2* PSs = PS + (uint64_t)side * m;
+            const uint2 me = PSs[k];
+            if (first) {
+                if (P.t[k] <= t_last) {  // else: the instance's first edge is outside the time slice
+                    first_role_ps(S, P, PSs, me.x, me.y, k, side, start, end, delta, pr, av, bv, d1);
+                    is_first = true;
                 }
+            } else {
+                // first edges restricted to t <= t_last: a prefix of S_u
+                const uint32_t re = t_last == INT64_MAX ? end - start : s_t_upper(S, start, end, t_last) - start;
+                third_role_ps(S, P, PSs, me.x, k, side, start, delta, re, xv, dc);
+                is_third = true;
             }
         }
+        // warp reductions into the lane-held cells: Pair [0,8), C [8,16), B [16,24), A [24,32)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = is_first ? (int)d1 * 4 + j : -1;
+            lc.add(c, pr[j], j, 4 + j);
+            lc.add(c < 0 ? -1 : 24 + c, av[j], 24 + j, 28 + j);
+            lc.add(c < 0 ? -1 : 16 + c, bv[j], 16 + j, 20 + j);
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {  // C[d1][d2][dc]: x = d1 * 2 + d2
+            const int c = is_third ? 8 + x * 2 + (int)dc : -1;
+            lc.add(c, xv[x], 8 + x * 2, 9 + x * 2);
+        }
     }
+    const int lane = threadIdx.x & 31;
+    cell_add(&cells[lane], 32, lc.mine);
+    if (lc.wraps) atomicAdd(&cells[lane + 32], (unsigned long long)lc.wraps);
     __syncthreads();
     flush_cells(cells, 32, out, kAccCarry);
 }
@@ -400,9 +583,14 @@ void star_full(const DeviceGraph& g, int64_t delta, uint32_t c_begin, uint32_t c
     TM_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(uint32_t), st));
     TM_LAUNCH("star_filter", st, star_filter_kernel, (unsigned)grid, 256, 0, pview(g), delta, g.m,
               c_begin, c_end, lists, lists + work, counters);
-    TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), delta, t_last,
-              lists,
-              lists + work, counters, queue, d_out, d_stats);
+    // candidates' S positions (P-indexed planes, one per side; only candidate
+    // entries are written), then the sums
+    uint2* PS = dalloc<uint2>(2 * g.m, st);
+    TM_LAUNCH("star_locate", st, star_locate_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), g.m, lists,
+              lists + work, counters, PS);
+    TM_LAUNCH("star_work", st, star_work_kernel, (unsigned)cap, 256, 0, sview(g), pview(g), delta, t_last, g.m,
+              PS, lists, lists + work, counters, queue, d_out, d_stats);
+    dfree(PS, st);
     dfree(lists, st);
 }
 

@@ -511,17 +511,17 @@ void tri_filter_stage(const DeviceGraph& g, const Forward& f, int64_t delta, uin
     ts.valid = true;
 }
 
-// long-window wedges (upper bound) at which the pair table pays for its
-// build: ~4 per edge, measured (config 1 at delta 86400 has 2.6 per edge and
-// loses, config 4 at 86400 has 9.6 and gains a third of its triangle pass).
-// TM_PAIR_TABLE=0 disables it, another number overrides the per-edge factor.
+// The pair table is off by default since the fenced block search: at config
+// 4, delta 86400 its build (clear + two CAS insert passes over 600M records,
+// every insert a full 128-byte line) took 497 ms to save 155 ms of tri_long.
+// TM_PAIR_TABLE=<k> builds it when the long windows hold >= k wedges per edge.
 uint64_t pair_table_min_wedges(const DeviceGraph& g) {
     static const long long env = [] {
         const char* e = std::getenv("TM_PAIR_TABLE");
-        return e ? std::atoll(e) : -1ll;
+        return e ? std::atoll(e) : 0ll;
     }();
-    if (env == 0) return ~0ull;
-    return (env > 0 ? (uint64_t)env : 4ull) * std::max<uint64_t>(g.m, 1024);
+    if (env <= 0) return ~0ull;
+    return (uint64_t)env * std::max<uint64_t>(g.m, 1024);
 }
 
 // long-window wedges (upper bound) at which the group ends pay for their

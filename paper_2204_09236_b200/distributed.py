@@ -70,7 +70,9 @@ def run_distributed(ctx, config, rank: int, world: int, group=None, device=None)
 def time_slice_bounds(t, world: int) -> List[Tuple[object, object]]:
     """Per-rank [lo, hi) first-edge time bounds balanced by edge count
     (None = open end).  Deterministic for the same t on every rank."""
-    ts = np.sort(np.asarray(t, np.int64))
+    ts = np.asarray(t, np.int64)
+    if len(ts) > 1 and not bool(np.all(ts[1:] >= ts[:-1])):
+        ts = np.sort(ts)
     m = len(ts)
     cuts = [int(ts[(r * m) // world]) for r in range(1, world)] if m else []
     lows = [None] + cuts

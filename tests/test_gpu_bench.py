@@ -31,25 +31,26 @@ def _port():
 
 
 def test_bench_contract_and_multirank(cuda):
-    gold = sum(load_golden("uniform_reference.json")["census"])
+    """N=1 contract on config 0, then config 1 (non-zero census, the
+    reference's golden) through 2 ranks, 3 time-slice ranks and 2 center-range
+    ranks: every cell must equal the reference's census."""
     one = _run([sys.executable, "bench.py", "--config", "uniform_10k_200k", "--steps", "3", "--warmup", "3",
                 "--no-cpu-baseline"])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "clocks"):
         assert key in one, key
-    assert one["census_total"] == gold
-    assert one["gpu_launches"] > 0 and one["roofline"]["frac"] > 0
-    two = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--config",
-                "uniform_10k_200k", "--steps", "3", "--warmup", "3", "--dist-backend", "gloo", "--same-device"])
-    assert two["n_gpus"] == 2
-    assert two["census_total"] == gold
-    for world, part in ((3, "time"), (2, "centers")):
+    assert one["census"] == load_golden("uniform_reference.json")["census"]
+    assert one["gpu_launches"] > 0 and one["roofline"]["kernel"] in one["kernels"]
+    top = max(one["kernels"], key=lambda k: one["kernels"][k]["ms_per_step"])
+    assert one["roofline"]["kernel"] == top
+    gold = load_golden("powerlaw_reference.json")["census"]
+    assert sum(gold) > 0
+    for world, part in ((2, "time"), (3, "time"), (2, "centers")):
         multi = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
                       "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--config",
-                      "uniform_10k_200k", "--steps", "3", "--warmup", "3", "--dist-backend", "gloo",
+                      "powerlaw_1m_10m", "--steps", "3", "--warmup", "3", "--dist-backend", "gloo",
                       "--same-device", "--partition", part])
-        assert multi["n_gpus"] == world and multi["census_total"] == gold, (world, part)
+        assert multi["n_gpus"] == world and multi["census"] == gold, (world, part)
     ref = _run([sys.executable, "bench.py", "--impl", "reference", "--config", "uniform_10k_200k", "--steps", "1",
                 "--warmup", "3"]) if os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libtmotif_ref.so")) else None
     if ref is not None:

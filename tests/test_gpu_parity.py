@@ -772,3 +772,52 @@ def test_error_codes_distinct(cuda, tm):
     bad_pair[0] = 1
     with pytest.raises(tm.ConsistencyError):
         tm.merge_census(tm.StarCounter(), tm.PairCounter(bad_pair), tm.TriCounter())
+
+
+def test_async_eager_batches_overlap_copy(cuda, tm, oracle):
+    """Batches counted eagerly by the asynchronous API (replay off: what every
+    batch above the replay size takes) run their census when the next batch is
+    submitted, behind its host->device copy: each result must still be its own
+    batch's census, through waits in order, out of order and a slot reuse."""
+    import json
+    import os
+    import subprocess
+    import sys
+    script = r'''
+import json, sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+import paper_2204_09236_b200 as tm
+n, delta = 50, 120
+gs = [tm.generate_random_graph(n, 3000, 20000, 40 + k) for k in range(4)]
+pin = [tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).pin_memory()
+             for a in (g.src, g.dst, g.t)) for g in gs]
+host = lambda i: (pin[i][0].numpy().view(np.uint32), pin[i][1].numpy().view(np.uint32), pin[i][2].numpy())
+cfg = tm.RunConfig(delta=delta)
+st = torch.cuda.Stream()
+out = []
+p = [tm.count_edges_async(n, *host(i), cfg, stream=st.cuda_stream) for i in (0, 1)]
+out.append([0, p[0].result().tolist()])
+p.append(tm.count_edges_async(n, *host(2), cfg, stream=st.cuda_stream))
+out.append([2, p[2].result().tolist()])   # waits out of order: batch 1 still pending
+out.append([1, p[1].result().tolist()])
+q = [tm.count_edges_async(n, *host(i), cfg, stream=st.cuda_stream) for i in (3, 0, 1)]  # slot reuse before waits
+for i, r in zip((3, 0, 1), q):
+    out.append([i, r.result().tolist()])
+print(json.dumps(out))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", script, root], env=dict(os.environ, TM_GRAPHS="0"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    want = {}
+    for k in range(4):
+        g = tm.generate_random_graph(50, 3000, 20000, 40 + k)
+        og = oracle.build_graph(50, g.src, g.dst, g.t)
+        want[k] = oracle.census(og, 120).tolist()
+        oracle.free(og)
+    assert len(got) == 6
+    for i, c in got:
+        assert c == want[i], i
