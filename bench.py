@@ -284,7 +284,7 @@ def main():
         # each rank holds the edges with t in [lo, hi + delta) and owns the
         # instances whose earliest edge has t in [lo, hi): exact partition
         from paper_2204_09236_b200.distributed import time_slice_bounds, time_slice_mask
-        lo, hi = time_slice_bounds(t, world)[rank]
+        lo, hi = time_slice_bounds(t, world, delta)[rank]  # balanced by estimated work
         keep = time_slice_mask(t, lo, hi, delta)
         src, dst, t = src[keep], dst[keep], t[keep]
         dev_arrays = None
@@ -315,15 +315,13 @@ def main():
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
 
-    red = torch.zeros(56, dtype=torch.int64, device=red_dev)
     raw = np.zeros(56, np.uint64)
+    from paper_2204_09236_b200.distributed import allreduce_counters
 
     def reduce_raw(census):
-        if world > 1:  # one all-reduce of the 56 raw u64 counters (exact modulo 2^64)
+        if world > 1:  # one all-reduce of the 56 counters, exact (32-bit halves), checked on merge
             with torch.cuda.stream(stream):
-                red.copy_(torch.from_numpy(raw.view(np.int64)), non_blocking=False)
-                dist.all_reduce(red)
-                tot = red.cpu().numpy().view(np.uint64)
+                tot = allreduce_counters(raw, device=red_dev)
             census = tm.merge_census(tm.StarCounter(tot[:24]), tm.PairCounter(tot[24:32]), tm.TriCounter(tot[32:]),
                                      cfg.triangle_mode).counts
         return census

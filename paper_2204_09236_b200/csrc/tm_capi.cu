@@ -599,7 +599,7 @@ struct ReplayEntry {
             }
         cudaStream_t s = key.stream;
         cudaStreamSynchronize(s);
-        dfree(ws.nk0, s); dfree(ws.nk1, s); dfree(ws.c0, s); dfree(ws.E, s); dfree(ws.st, s);
+        dfree(ws.nk0, s); dfree(ws.nk1, s); dfree(ws.nv0, s); dfree(ws.nv1, s); dfree(ws.c0, s); dfree(ws.E, s); dfree(ws.st, s);
         dfree(hs, s); dfree(hd, s); dfree(ht, s);
         cudaStreamSynchronize(s);
         if (verdict) cudaFreeHost(verdict);

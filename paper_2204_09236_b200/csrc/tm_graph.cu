@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
     const uint32_t* __restrict__ perm, const uint64_t* __restrict__ tkeys, uint64_t kmask,
     const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, const int64_t* __restrict__ t,
     uint64_t m, uint64_t n, int64_t tmin, typename EdgeCodec<kNarrow>::Rec* __restrict__ E,
-    uint64_t* __restrict__ keys, uint32_t* __restrict__ counts, uint32_t ntiles, BuildStats* __restrict__ st) {
+    uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, uint32_t* __restrict__ counts, uint32_t ntiles,
+    BuildStats* __restrict__ st) {
     constexpr int NW = kPackBlock / 32;
     __shared__ uint32_t hist[NW][256];
     const int w = threadIdx.x >> 5;
@@ -135,9 +136,14 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
                     ea = ea < n ? ea : 0u;
                     eb = eb < n ? eb : 0u;
                 }
-                E[p] = EdgeCodec<kNarrow>::make(tp, ea, eb, tmin);
+                if (!(kNarrow && vals)) E[p] = EdgeCodec<kNarrow>::make(tp, ea, eb, tmin);  // gathered (wide only)
                 reinterpret_cast<ulonglong2*>(keys)[p] =
                     make_ulonglong2(((uint64_t)a << 32) | (2 * k), ((uint64_t)b << 32) | (2 * k + 1));
+                if (kNarrow && vals) {  // the gathers' payload travels with the node sort
+                    const uint64_t rel = (uint64_t)(kPermuted ? t[k] : tp) - (uint64_t)tmin;
+                    reinterpret_cast<ulonglong2*>(vals)[p] =
+                        make_ulonglong2((rel << 32) | b, (rel << 32) | a | kDirBit);
+                }
                 atomicAdd(&hist[w][a & dmask0], 1u);
                 atomicAdd(&hist[w][b & dmask0], 1u);
             }
@@ -218,19 +224,69 @@ __global__ void gather_s_kernel(const typename EdgeCodec<kNarrow>::Rec* __restri
     }
 }
 
+// gather_s for narrow records whose payload travelled with the node sort
+// (pack_edges vals: (t - tmin) << 32 | other | side << 31): a streaming pass,
+// no random read of the edge records.  A random 8-byte read costs a whole
+// 128-byte line from HBM on B200 (profiles/gatherbench.cu: 1.2G gathers of a
+// 4.8 GB array = 155 GB of DRAM reads), so carrying 8 more bytes through each
+// sort pass is cheaper than gathering them once.
+__global__ void gather_s_pay_kernel(const uint64_t* __restrict__ skeys, const uint64_t* __restrict__ svals,
+                                    uint64_t R, uint64_t n, uint32_t* __restrict__ off,
+                                    uint32_t* __restrict__ S_tn, uint32_t* __restrict__ S_nbr,
+                                    uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
+                                    uint32_t* __restrict__ omask, uint32_t* __restrict__ xmask,
+                                    uint32_t* __restrict__ t32n, uint32_t* __restrict__ t1kn) {
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = base + threadIdx.x;
+        uint32_t out = 0, mx = 0;
+        if (q < R) {
+            const uint64_t key = __ldcs(skeys + q);
+            const uint64_t val = __ldcs(svals + q);
+            const uint32_t r = (uint32_t)key;
+            const uint32_t p = r >> 1, side = r & 1u;
+            const uint32_t u = (uint32_t)(key >> 32), x = (uint32_t)val & kNodeMask;
+            const uint32_t trel = (uint32_t)(val >> 32);
+            const int64_t prev = q ? (int64_t)(skeys[q - 1] >> 32) : -1;
+            for (int64_t y = prev + 1; y <= (int64_t)u; ++y) off[y] = (uint32_t)q;
+            if (q == R - 1)
+                for (int64_t y = (int64_t)u + 1; y <= (int64_t)n; ++y) off[y] = (uint32_t)R;
+            out = side ^ 1u;
+            mx = x < u ? 1u : 0u;
+            __stcs(S_tn + q, trel);
+            __stcs(S_ord + q, p);
+            __stcs(S_node + q, u);
+            __stcs(S_nbr + q, x | (side << 31));
+            if ((q & 31) == 0) {
+                t32n[q >> 5] = trel;
+                if ((q & 1023) == 0) t1kn[q >> 10] = trel;
+            }
+        }
+        const unsigned ob = __ballot_sync(0xffffffffu, out), xb = __ballot_sync(0xffffffffu, mx);
+        if ((threadIdx.x & 31) == 0 && q < R) {
+            omask[q >> 5] = ob;
+            xmask[q >> 5] = xb;
+        }
+    }
+}
+
 // pair keys from the max-side records of S (in (max, t, ordinal) order):
 // min << 32 | p, compacted by the xmask prefix
+// (narrow records: also the payload (t - tmin) << 32 | max | dir_rel_min << 31
+// for gather_p_pay, read from S_t / S_nbr)
 __global__ void pair_keys_kernel(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ S_nbr,
+                                 const uint32_t* __restrict__ S_tn,
                                  const uint32_t* __restrict__ xmask, const uint32_t* __restrict__ xpref,
                                  const uint32_t* __restrict__ off, uint64_t R, uint64_t* __restrict__ pkeys,
-                                 uint32_t* __restrict__ fmask) {
+                                 uint64_t* __restrict__ pvals, uint32_t* __restrict__ fmask) {
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t q = base + threadIdx.x;
         uint32_t fwd = 0;
         if (q < R) {
             const uint64_t key = __ldcs(skeys + q);
-            const uint32_t u = (uint32_t)(key >> 32), x = __ldcs(S_nbr + q) & kNodeMask;
+            const uint32_t nbr = __ldcs(S_nbr + q);
+            const uint32_t u = (uint32_t)(key >> 32), x = nbr & kNodeMask;
             // degree-rank orientation of the triangle pass: forward iff (deg, id) of
             // the neighbour exceeds the center's
             const uint32_t du = off[u + 1] - off[u], dx = off[x + 1] - off[x];
@@ -239,6 +295,8 @@ __global__ void pair_keys_kernel(const uint64_t* __restrict__ skeys, const uint3
             if (word & bit) {
                 const uint32_t j = xpref[q >> 5] + __popc(word & (bit - 1u));
                 pkeys[j] = ((uint64_t)x << 32) | ((uint32_t)key >> 1);
+                // u is the max endpoint; the min x is the source iff u's record is inward
+                if (pvals) pvals[j] = ((uint64_t)__ldcs(S_tn + q) << 32) | u | ((~nbr) & kDirBit);
             }
         }
         const unsigned fb = __ballot_sync(0xffffffffu, fwd);
@@ -323,6 +381,74 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
                 for (int64_t x = (int64_t)a + 1; x <= (int64_t)n; ++x) pofs[x] = (uint32_t)m;
         }
         const unsigned db = __ballot_sync(0xffffffffu, k < m && Codec::dir_from_min(ed, a));
+        const unsigned gb = __ballot_sync(0xffffffffu, first);
+        if ((tid & 31) == 0 && k < m) {
+            dmask[k >> 5] = db;
+            gmask[k >> 5] = gb;
+        }
+        __syncthreads();
+    }
+}
+
+// gather_p for narrow records: the payload (t - tmin) << 32 | max |
+// dir_rel_min << 31 came through the pair sort with the keys (min << 32 | p)
+__global__ void __launch_bounds__(256) gather_p_pay_kernel(const uint64_t* __restrict__ pkeys,
+                                                           const uint64_t* __restrict__ pvals, uint64_t m,
+                                                           uint32_t* __restrict__ P_tn, uint32_t* __restrict__ P_ord,
+                                                           uint32_t* __restrict__ P_min, uint32_t* __restrict__ P_max,
+                                                           uint32_t* __restrict__ P_w, uint64_t n,
+                                                           uint32_t* __restrict__ pofs, uint32_t* __restrict__ dmask,
+                                                           uint32_t* __restrict__ gmask, uint32_t* __restrict__ max32,
+                                                           uint32_t* __restrict__ max1k, uint32_t* __restrict__ t32n,
+                                                           uint32_t* __restrict__ t1kn) {
+    __shared__ uint32_t s_a[258], s_b[258];
+    const int tid = threadIdx.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = base + tid;
+        uint32_t a = 0, b = 0, p = 0, dir = 0, trel = 0;
+        bool first = false;
+        if (k < m) {
+            const uint64_t key = __ldcs(pkeys + k), val = __ldcs(pvals + k);
+            p = (uint32_t)key;
+            a = (uint32_t)(key >> 32);
+            b = (uint32_t)val & kNodeMask;
+            dir = ((uint32_t)val) >> 31;
+            trel = (uint32_t)(val >> 32);
+            s_a[tid + 1] = a;
+            s_b[tid + 1] = b;
+        }
+        if (tid == 0 && k > 0 && k - 1 < m) {
+            s_a[0] = (uint32_t)(pkeys[k - 1] >> 32);
+            s_b[0] = (uint32_t)pvals[k - 1] & kNodeMask;
+        }
+        if (tid == (int)blockDim.x - 1 && k + 1 < m) {
+            s_a[tid + 2] = (uint32_t)(pkeys[k + 1] >> 32);
+            s_b[tid + 2] = (uint32_t)pvals[k + 1] & kNodeMask;
+        }
+        __syncthreads();
+        if (k < m) {
+            first = k == 0 || s_a[tid] != a || s_b[tid] != b;
+            const bool last = k + 1 == m || s_a[tid + 2] != a || s_b[tid + 2] != b;
+            __stcs(P_tn + k, trel);
+            __stcs(P_ord + k, p);
+            __stcs(P_min + k, a);
+            __stcs(P_max + k, b);
+            __stcs(P_w + k, (dir << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u));
+            if ((k & 31) == 0) {
+                max32[k >> 5] = b;
+                t32n[k >> 5] = trel;
+                if ((k & 1023) == 0) {
+                    max1k[k >> 10] = b;
+                    t1kn[k >> 10] = trel;
+                }
+            }
+            const int64_t prev = k == 0 ? -1 : (int64_t)s_a[tid];
+            for (int64_t x = prev + 1; x <= (int64_t)a; ++x) pofs[x] = (uint32_t)k;
+            if (k + 1 == m)
+                for (int64_t x = (int64_t)a + 1; x <= (int64_t)n; ++x) pofs[x] = (uint32_t)m;
+        }
+        const unsigned db = __ballot_sync(0xffffffffu, k < m && dir);
         const unsigned gb = __ballot_sync(0xffffffffu, first);
         if ((tid & 31) == 0 && k < m) {
             dmask[k >> 5] = db;
@@ -529,12 +655,16 @@ BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d
         if (!ws->nk0) {
             ws->nk0 = dalloc<uint64_t>(R + kSortPad, s);
             ws->nk1 = dalloc<uint64_t>(R + kSortPad, s);
+            ws->nv0 = dalloc<uint64_t>(R + kSortPad, s);
+            ws->nv1 = dalloc<uint64_t>(R + kSortPad, s);
             ws->c0 = dalloc<uint32_t>((uint64_t)256 * pl.ntiles, s);
             ws->E = dalloc<uint8_t>(m * sizeof(WideEdge), s);
             ws->st = dalloc<uint8_t>(sizeof(BuildStats), s);
         }
         pl.nk0 = ws->nk0;
         pl.nk1 = ws->nk1;
+        pl.nv0 = ws->nv0;
+        pl.nv1 = ws->nv1;
         pl.c0 = ws->c0;
         pl.E = ws->E;
         pl.E_bytes = m * sizeof(WideEdge);
@@ -542,6 +672,8 @@ BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d
     } else {
         pl.nk0 = dalloc<uint64_t>(R + kSortPad, s);
         pl.nk1 = dalloc<uint64_t>(R + kSortPad, s);
+        pl.nv0 = dalloc<uint64_t>(R + kSortPad, s);
+        pl.nv1 = dalloc<uint64_t>(R + kSortPad, s);
         pl.c0 = dalloc<uint32_t>((uint64_t)256 * pl.ntiles, s);
         pl.E = dalloc<uint8_t>(m * sizeof(NarrowEdge), s);
         pl.E_bytes = m * sizeof(NarrowEdge);
@@ -553,8 +685,8 @@ BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d
     TM_CUDA(cudaMemcpyAsync(d_st, hv, sizeof(h_st), cudaMemcpyHostToDevice, s));
     if (m) {
         TM_LAUNCH("pack_edges", s, (pack_edges_kernel<true, false>), grid_for(m, kPackEdges), kPackBlock, 0, nullptr,
-                  nullptr, 0ull, d_src, d_dst, d_t, m, n, (int64_t)0, reinterpret_cast<NarrowEdge*>(pl.E), pl.nk0, pl.c0,
-                  pl.ntiles, d_st);
+                  nullptr, 0ull, d_src, d_dst, d_t, m, n, (int64_t)0, reinterpret_cast<NarrowEdge*>(pl.E), pl.nk0,
+                  pl.nv0, pl.c0, pl.ntiles, d_st);
     }
     TM_CUDA(cudaMemcpyAsync(hv, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, s));
     if (h_async) return pl;  // verdict read later (plan_from_verdict)
@@ -579,7 +711,7 @@ void plan_from_verdict(DeviceGraph& g, BuildPlan& pl, const BuildVerdict& v) {
 void release_plan(DeviceGraph& g, BuildPlan& pl) {
     if (!pl.owned) return;
     cudaStream_t s = g.stream;
-    dfree(pl.nk0, s); dfree(pl.nk1, s); dfree(pl.c0, s); dfree(pl.E, s);
+    dfree(pl.nk0, s); dfree(pl.nk1, s); dfree(pl.nv0, s); dfree(pl.nv1, s); dfree(pl.c0, s); dfree(pl.E, s);
 }
 
 void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
@@ -591,10 +723,10 @@ void build_graph(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, c
 template <bool kNarrow, bool kPermuted>
 void launch_repack(const uint32_t* perm, const uint64_t* tkeys, uint64_t kmask, const uint32_t* d_src,
                    const uint32_t* d_dst, const int64_t* d_t, uint64_t m, uint64_t n, int64_t tmin, uint8_t* E,
-                   uint64_t* keys, uint32_t* counts, uint32_t ntiles, cudaStream_t s) {
+                   uint64_t* keys, uint64_t* vals, uint32_t* counts, uint32_t ntiles, cudaStream_t s) {
     TM_LAUNCH("pack_edges", s, (pack_edges_kernel<kNarrow, kPermuted>), grid_for(m, kPackEdges), kPackBlock, 0, perm,
               tkeys, kmask, d_src, d_dst, d_t, m, n, tmin,
-              reinterpret_cast<typename EdgeCodec<kNarrow>::Rec*>(E), keys, counts, ntiles, nullptr);
+              reinterpret_cast<typename EdgeCodec<kNarrow>::Rec*>(E), keys, vals, counts, ntiles, nullptr);
 }
 
 void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const uint32_t* d_dst,
@@ -607,6 +739,8 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
     BuildStats h_st{pl.tmin, pl.tmax, 0, pl.unsorted ? 1u : 0u, 0, 0};
     uint64_t* nk0 = pl.nk0;
     uint64_t* nk1 = pl.nk1;
+    uint64_t* nv0 = pl.nv0;
+    uint64_t* nv1 = pl.nv1;
     uint32_t* c0 = pl.c0;
     uint8_t* E = pl.E;
     const uint32_t ntiles = pl.ntiles;
@@ -705,17 +839,18 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
                 pl.E_bytes = m * sizeof(WideEdge);
             }
             const bool permuted = perm || tkeys;
-            if (narrow && permuted) launch_repack<true, true>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, c0, ntiles, s);
-            else if (narrow) launch_repack<true, false>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, c0, ntiles, s);
-            else if (permuted) launch_repack<false, true>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, c0, ntiles, s);
-            else launch_repack<false, false>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, c0, ntiles, s);
+            if (narrow && permuted) launch_repack<true, true>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, nv0, c0, ntiles, s);
+            else if (narrow) launch_repack<true, false>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, nv0, c0, ntiles, s);
+            else if (permuted) launch_repack<false, true>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, nullptr, c0, ntiles, s);
+            else launch_repack<false, false>(perm, tkeys, kmask, d_src, d_dst, d_t, m, n, tmin, E, nk0, nullptr, c0, ntiles, s);
             // the gathers read ordinals from the keys: the order is no longer needed
             if (perm) dfree(perm, s);
             if (tkeys) dfree(tkeys, s);
         }
-        auto EN = reinterpret_cast<NarrowEdge*>(E);
         auto EW = reinterpret_cast<WideEdge*>(E);
-        radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s, c0);
+        // narrow records: the S payload travels with the keys (no gather)
+        if (narrow) radix_sort<uint64_t, uint64_t>(nk0, nv0, nk1, nv1, R, 32, 32 + nb, s, c0);
+        else radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s, c0);
         if (pl.owned) dfree(c0, s);
         TM_CUDA(cudaMemsetAsync(g.S_omask + (nw - 1), 0, sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.S_fmask + (nw - 1), 0, sizeof(uint32_t), s));
@@ -723,9 +858,8 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         uint32_t* xpref = dalloc<uint32_t>(nw + 1, s);
         TM_CUDA(cudaMemsetAsync(xmask + (nw - 1), 0, sizeof(uint32_t), s));
         if (narrow)
-            TM_LAUNCH("gather_s", s, gather_s_kernel<true>, grid_for(R), 256, 0, EN, tmin, nk0, R, n, g.off,
-                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask, g.S_t32.w, g.S_t32.n,
-                      g.S_t1k.w, g.S_t1k.n);
+            TM_LAUNCH("gather_s", s, gather_s_pay_kernel, grid_for(R), 256, 0, nk0, nv0, R, n, g.off, g.S_t.n,
+                      g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask, g.S_t32.n, g.S_t1k.n);
         else
             TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, EW, tmin, nk0, R, n, g.off,
                       g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask, g.S_t32.w, g.S_t32.n,
@@ -740,8 +874,11 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         uint64_t* pk1 = nk1;  // R + pad >= m + pad
         uint64_t* spare = nk1;  // the node sort's second buffer (plan-owned)
         nk1 = nullptr;
-        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, xmask, xpref, g.off, R,
-                  pk0, g.S_fmask);
+        uint64_t* pv0 = narrow ? dalloc<uint64_t>(m + kSortPad, s) : nullptr;
+        uint64_t* pv0_alloc = pv0;
+        uint64_t* pv1 = nv1;  // the node sort's second value buffer
+        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, g.S_t.n, xmask, xpref, g.off,
+                  R, pk0, pv0, g.S_fmask);
 
         // the forward sequences (degree orientation) only need S and the
         // forward mask: build them on a side stream while the pair index sorts
@@ -751,24 +888,30 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
             tri_filter_stage(g, g.fwd[0], hint->delta, 0, (uint32_t)g.fwd[0].len, g.aux[0], g.pre_tri);
         TM_CUDA(cudaEventRecord(g.fwd_ready, g.aux[0]));
         g.fwd_pending = true;
-        if (pl.owned) dfree(nk0, s);
+        if (pl.owned) {
+            dfree(nk0, s);
+            dfree(nv0, s);
+        }
         dfree(xmask, s);
         dfree(xpref, s);
-        radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
-        if (narrow)
-            TM_LAUNCH("gather_p", s, gather_p_kernel<true>, grid_for(m), 256, 0, pk0, m, EN, tmin, g.P_t.w, g.P_t.n,
-                      g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask, g.P_gmask, g.P_max32, g.P_max1k,
-                      g.P_t32.w, g.P_t32.n, g.P_t1k.w, g.P_t1k.n);
-        else
+        if (narrow) {
+            radix_sort<uint64_t, uint64_t>(pk0, pv0, pk1, pv1, m, 32, 32 + nb, s);
+            TM_LAUNCH("gather_p", s, gather_p_pay_kernel, grid_for(m), 256, 0, pk0, pv0, m, g.P_t.n, g.P_ord, g.P_min,
+                      g.P_max, g.P_w, n, g.pofs, g.P_dmask, g.P_gmask, g.P_max32, g.P_max1k, g.P_t32.n, g.P_t1k.n);
+        } else {
+            radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
             TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, EW, tmin, g.P_t.w, g.P_t.n,
                       g.P_ord, g.P_min, g.P_max, g.P_w, n, g.pofs, g.P_dmask, g.P_gmask, g.P_max32, g.P_max1k,
                       g.P_t32.w, g.P_t32.n, g.P_t1k.w, g.P_t1k.n);
+        }
         dfree(pk0_alloc, s);
+        dfree(pv0_alloc, s);
         // direction prefix and group-first prefix in one scan
         exclusive_scan_to<uint64_t>(PopcLoad2{g.P_dmask, g.P_gmask}, m / 32 + 1, SplitStore2{g.P_dpref, g.P_gpref},
                                     s);
         if (pl.owned) {
             dfree(spare, s);
+            dfree(nv1, s);
             dfree(E, s);
         }
     }

@@ -406,6 +406,8 @@ struct BuildVerdict {
 struct BuildWorkspace {
     uint64_t* nk0 = nullptr;
     uint64_t* nk1 = nullptr;
+    uint64_t* nv0 = nullptr;  // node-sort payloads (narrow records)
+    uint64_t* nv1 = nullptr;
     uint32_t* c0 = nullptr;
     uint8_t* E = nullptr;
     uint8_t* st = nullptr;
@@ -413,6 +415,8 @@ struct BuildWorkspace {
 struct BuildPlan {
     uint64_t* nk0 = nullptr;
     uint64_t* nk1 = nullptr;
+    uint64_t* nv0 = nullptr;  // node-sort payloads: (t - tmin) << 32 | other | side << 31
+    uint64_t* nv1 = nullptr;
     uint32_t* c0 = nullptr;
     uint8_t* E = nullptr;
     uint64_t E_bytes = 0;

@@ -531,11 +531,11 @@ __device__ __forceinline__ uint32_t wlms_bit(uint32_t d, uint32_t bit) {
 
 // NBITS: digit bits of this pass (8, or 4 for a short last pass); digits are
 // (key >> shift) & dmask with dmask < 2^NBITS
-template <typename K, bool kVals, int BLOCK, int ITEMS, int MINB, int NBITS>
+template <typename K, typename V, bool kVals, int BLOCK, int ITEMS, int MINB, int NBITS>
 __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __restrict__ kin,
-                                                                   const uint32_t* __restrict__ vin,
+                                                                   const V* __restrict__ vin,
                                                                    K* __restrict__ kout,
-                                                                   uint32_t* __restrict__ vout, uint64_t n,
+                                                                   V* __restrict__ vout, uint64_t n,
                                                                    int shift, uint32_t dmask,
                                                                    const uint32_t* __restrict__ tile_offsets,
                                                                    uint32_t ntiles,
@@ -543,13 +543,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
     constexpr int NW = BLOCK / 32, TILE = BLOCK * ITEMS;
     constexpr int kMatchRounds = NBITS >= 8 ? TM_RANK_MATCH_ROUNDS : TM_RANK_MATCH_ROUNDS_NARROW;
     static_assert(BLOCK >= kRadix, "one digit per thread");
-    constexpr uint32_t STAGE_BYTES = TILE * (sizeof(K) + (kVals ? 4 : 0));
+    constexpr uint32_t STAGE_BYTES = TILE * (sizeof(K) + (kVals ? sizeof(V) : 0));
     extern __shared__ __align__(128) unsigned char tma_smem[];
     // [stage0][stage1]: each TILE keys (+ TILE vals); a tile is reordered in
     // place in its own stage (its keys are in registers by then)
     auto stage_keys = [&](int s) { return reinterpret_cast<K*>(tma_smem + s * STAGE_BYTES); };
     auto stage_vals = [&](int s) {
-        return reinterpret_cast<uint32_t*>(tma_smem + s * STAGE_BYTES + TILE * sizeof(K));
+        return reinterpret_cast<V*>(tma_smem + s * STAGE_BYTES + TILE * sizeof(K));
     };
     __shared__ __align__(16) uint16_t wcnt[NW][kRadix];  // per-warp digit counts, then (warp, digit) run starts
     __shared__ uint32_t dglob[kRadix];
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
         const uint64_t base = (uint64_t)tile * TILE;
         const uint64_t cnt = (n - base) < (uint64_t)TILE ? (n - base) : (uint64_t)TILE;
         const uint32_t kbytes = (uint32_t)((cnt * sizeof(K) + 15) & ~uint64_t(15));
-        const uint32_t vbytes = kVals ? (uint32_t)((cnt * 4 + 15) & ~uint64_t(15)) : 0u;
+        const uint32_t vbytes = kVals ? (uint32_t)((cnt * sizeof(V) + 15) & ~uint64_t(15)) : 0u;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], kbytes + vbytes);
         tma_load_1d(stage_keys(s), kin + base, kbytes, &bar[s]);
@@ -590,11 +590,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
         mbar_wait(&bar[s], (it >> 1) & 1);
         __syncthreads();
         K* sk = stage_keys(s);
-        uint32_t* sv = stage_vals(s);
+        V* sv = stage_vals(s);
         // digits and match masks of all rounds first (independent, overlapped),
         // then the warp's sequential per-digit running counts
         K key[ITEMS];
-        uint32_t val[kVals ? ITEMS : 1];
+        V val[kVals ? ITEMS : 1];
         uint32_t dig[ITEMS], rank[ITEMS];
 #pragma unroll
         for (int r = 0; r < ITEMS; ++r) {
@@ -681,13 +681,13 @@ constexpr int kSortBlock = 256, kSortItems = 12, kSortMinBlocks = 3, kSortTile =
 
 // one downsweep instantiation: sets its shared-memory limit and caches its
 // occupancy on first use, then launches a persistent grid
-template <typename K, bool kVals, int BLOCK, int ITEMS, int MINB, int NBITS>
-void launch_downsweep(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint64_t n, int shift,
+template <typename K, typename V, bool kVals, int BLOCK, int ITEMS, int MINB, int NBITS>
+void launch_downsweep(const K* kin, const V* vin, K* kout, V* vout, uint64_t n, int shift,
                       uint32_t dmask, const uint32_t* offs, uint32_t ntiles, const uint32_t* totals,
                       cudaStream_t s) {
     constexpr int TILE = BLOCK * ITEMS;
-    constexpr size_t smem = 2 * TILE * (sizeof(K) + (kVals ? sizeof(uint32_t) : 0));
-    auto kern = radix_downsweep_tma<K, kVals, BLOCK, ITEMS, MINB, NBITS>;
+    constexpr size_t smem = 2 * TILE * (sizeof(K) + (kVals ? sizeof(V) : 0));
+    auto kern = radix_downsweep_tma<K, V, kVals, BLOCK, ITEMS, MINB, NBITS>;
     static int per_sm = 0;  // resident blocks per SM
     if (per_sm == 0) {
         TM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -700,8 +700,8 @@ void launch_downsweep(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout
 }
 
 // one pass configuration: tile = BLOCK * ITEMS keys
-template <typename K, int BLOCK, int ITEMS, int MINB>
-void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
+template <typename K, typename V, int BLOCK, int ITEMS, int MINB>
+void radix_sort_cfg(K*& keys, V*& vals, K*& keys_alt, V*& vals_alt, uint64_t n,
                     int bit_lo, int bit_hi, cudaStream_t s, const uint32_t* first_counts) {
     constexpr int TILE = BLOCK * ITEMS;
     const bool with_vals = vals != nullptr;
@@ -726,17 +726,17 @@ void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt
         }
         TM_LAUNCH("radix_scan", s, radix_scan_counts, dmask + 1, kRowBlock, 0, cin, ntiles,
                   offs, totals);
-        uint32_t* vin = with_vals ? vals : nullptr;
-        uint32_t* vout = with_vals ? vals_alt : nullptr;
-#define TM_DOWNSWEEP(V, NB)                                                                                    \
-    launch_downsweep<K, V, BLOCK, ITEMS, MINB, NB>(keys, vin, keys_alt, vout, n, shift, dmask, offs, ntiles, \
-                                                   totals, s)
+        V* vin = with_vals ? vals : nullptr;
+        V* vout = with_vals ? vals_alt : nullptr;
+#define TM_DOWNSWEEP(HV, NB)                                                                                    \
+    launch_downsweep<K, V, HV, BLOCK, ITEMS, MINB, NB>(keys, vin, keys_alt, vout, n, shift, dmask, offs, ntiles, \
+                                                       totals, s)
         if (with_vals) {
             if (width <= 4) TM_DOWNSWEEP(true, 4);
             else if (width <= 6) TM_DOWNSWEEP(true, 6);
             else if (width <= 7) TM_DOWNSWEEP(true, 7);
             else TM_DOWNSWEEP(true, 8);
-            uint32_t* tv = vals;
+            V* tv = vals;
             vals = vals_alt;
             vals_alt = tv;
         } else {
@@ -754,19 +754,19 @@ void radix_sort_cfg(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt
     dfree(counts, s);
 }
 
-// Stable sort of keys (and u32 values when vals != nullptr) on key bits
+// Stable sort of keys (and u32 or u64 values when vals != nullptr) on key bits
 // [bit_lo, bit_hi).  Buffers need kSortPad elements of slack (TMA tile loads
 // round up to 16 bytes).  On return keys/vals point at the sorted data; the *_alt
 // pointers at the scratch halves (pointers may be swapped).
-template <typename K>
-void radix_sort(K*& keys, uint32_t*& vals, K*& keys_alt, uint32_t*& vals_alt, uint64_t n,
+template <typename K, typename V = uint32_t>
+void radix_sort(K*& keys, V*& vals, K*& keys_alt, V*& vals_alt, uint64_t n,
                 int bit_lo, int bit_hi, cudaStream_t s, const uint32_t* first_counts = nullptr) {
     if (n <= 1 || bit_hi <= bit_lo) return;
     // 256 threads x 12 keys, 3 blocks per SM: the same downsweep time as 8
     // keys x 4 blocks with a third fewer tiles, so the count matrix's upsweep
     // and row scan shrink (profiles/sortbench.cu sweeps 256/512 threads x
     // 4-16 keys on B200: 20M node keys 0.457 -> 0.448 ms)
-    radix_sort_cfg<K, kSortBlock, kSortItems, kSortMinBlocks>(keys, vals, keys_alt, vals_alt, n, bit_lo, bit_hi, s,
+    radix_sort_cfg<K, V, kSortBlock, kSortItems, kSortMinBlocks>(keys, vals, keys_alt, vals_alt, n, bit_lo, bit_hi, s,
                                                  first_counts);
 }
 

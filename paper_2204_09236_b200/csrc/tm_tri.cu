@@ -32,6 +32,57 @@ namespace {
 // otherwise.
 constexpr uint32_t kTableMinBlock = 256;
 
+// (t, ordinal) strict order of P record k before (t, ord)
+__device__ __forceinline__ bool p_before(const PView& P, uint32_t k, int64_t t, uint32_t ord) {
+    const int64_t tk = P.t[k];
+    return tk < t || (tk == t && P.ord[k] < ord);
+}
+// first k in [from, end) with (t, ord) >= (t0, o0), galloping up from `from`
+// (the boundaries of one window are close together)
+__device__ __forceinline__ uint32_t p_gallop_rec(const PView& P, uint32_t from, uint32_t end, int64_t t0,
+                                                 uint32_t o0) {
+    uint32_t lo = from, hi = end;
+    for (uint32_t span = 1;; span <<= 1) {
+        const uint64_t probe = (uint64_t)lo + span - 1;
+        if (probe >= end) break;
+        if (!p_before(P, (uint32_t)probe, t0, o0)) {
+            hi = (uint32_t)probe;
+            break;
+        }
+        lo = (uint32_t)probe + 1;
+    }
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (p_before(P, mid, t0, o0)) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+// first k in [from, end) with t > x, galloping up from `from`
+__device__ __forceinline__ uint32_t p_gallop_tupper(const PView& P, uint32_t from, uint32_t end, int64_t x) {
+    uint32_t lo = from, hi = end;
+    for (uint32_t span = 1;; span <<= 1) {
+        const uint64_t probe = (uint64_t)lo + span - 1;
+        if (probe >= end) break;
+        if (P.t[probe] > x) {
+            hi = (uint32_t)probe;
+            break;
+        }
+        lo = (uint32_t)probe + 1;
+    }
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (P.t[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// One path for every group, short or long: the lanes of a warp hold wedges
+// whose closing groups range from one record to hundreds of thousands (hub
+// pairs), and a per-length special case made the warp execute both paths.
+// Group [kb, ke) by the fenced block search and the group end; then the
+// window [k1, k4) = [t_j - delta, t_i + delta] and the type boundaries k2 =
+// (t_i, o_i), k3 = (t_j, o_j) (triangle_engine.cpp:43-51): k1 by the fenced
+// search, k2, k3, k4 each by a gallop from the previous boundary.
 __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint32_t w, int64_t lo,
                                                int64_t hi, int64_t ti, uint32_t oi, int64_t tj,
                                                uint32_t oj, int64_t t_last, uint32_t c[6]) {
@@ -39,11 +90,8 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
     for (int j = 0; j < 6; ++j) c[j] = 0;
     const uint32_t a = min(v, w), b = max(v, w);
     const uint32_t flip = v == a ? 0u : 1u;  // dir_rel_min -> dir relative to v
-    uint32_t blk_end = P.pofs[a + 1], kb, l = P.pofs[a], r;
-    uint32_t known_end = 0;  // group end from the pair table (0: unknown)
-    // the table only for long blocks (a hub's), where the binary search is
-    // ~17 dependent probes; short blocks are cheaper to search in L2
-    if (P.pt_keys && blk_end - l > kTableMinBlock) {
+    uint32_t blk_end = P.pofs[a + 1], kb, ke = 0;
+    if (P.pt_keys && blk_end - P.pofs[a] > kTableMinBlock) {  // optional pair table (TM_PAIR_TABLE)
         const unsigned long long key = ((unsigned long long)a << 32) | b;
         uint64_t slot = pair_slot(a, b) & P.pt_mask;
         for (;;) {
@@ -54,69 +102,19 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         }
         const unsigned long long val = P.pt_vals[slot];
         kb = (uint32_t)(val >> 32);
-        known_end = kb + (uint32_t)val;
-        blk_end = known_end;
+        ke = kb + (uint32_t)val;
     } else {
-        l = p_max_lower(P, l, blk_end, b);
-        if (l >= blk_end || P.max[l] != b) return;
-        kb = l;
+        kb = p_max_lower(P, P.pofs[a], blk_end, b);
+        if (kb >= blk_end || P.max[kb] != b) return;
+        ke = P.gend ? p_group_end(P, kb) : p_max_upper(P, kb, blk_end, b);
     }
-    // short groups: classify record by record (triangle_engine.cpp:43-51);
-    // a group still running 16 records on goes straight to the searches
-    uint32_t k = kb;
-    const bool is_long = known_end ? known_end - kb > 16 : (kb + 16 < blk_end && P.max[kb + 16] == b);
-    for (int step = 0; step < 16 && !is_long; ++step, ++k) {
-        const int64_t tk = P.t[k];
-        const uint32_t wk = P.w[k];
-        if (tk > hi) return;
-        if (tk >= lo) {
-            const uint32_t dk = (wk >> 31) ^ flip;
-            uint32_t type;
-            if (tk < ti || (tk == ti && P.ord[k] < oi)) type = 0;
-            else if (tk > tj || (tk == tj && P.ord[k] > oj)) type = 2;
-            else type = 1;
-            if ((type == 0 ? tk : ti) <= t_last) c[type * 2 + dk] += 1;
-        }
-        if (wk & kPLast) return;
-    }
-    // long group: its end (pair table, group index, or a gallop over P_max),
-    // then binary searches of the window [k1, k4) and the type boundaries
-    if (!known_end && P.gend) known_end = p_group_end(P, kb);
-    if (!known_end) known_end = p_max_upper(P, k, blk_end, b);
-    const uint32_t ke = known_end;
-    // window [k1, k4): the lower end by the fenced search, the upper end by a
-    // gallop from it (a window of a long group is short next to the group)
-    const uint32_t k1 = p_t_lower(P, k, ke, lo);
-    l = k1;
-    r = ke;
-    for (uint32_t span = 1;; span <<= 1) {
-        const uint64_t probe = (uint64_t)l + span - 1;
-        if (probe >= r) break;
-        if (P.t[probe] > hi) {
-            r = (uint32_t)probe;
-            break;
-        }
-        l = (uint32_t)probe + 1;
-    }
-    while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] <= hi) l = mid + 1; else r = mid; }
-    const uint32_t k4 = l;
-    l = k1; r = k4;  // k2: first (t, ord) > (ti, oi)
-    while (l < r) {
-        const uint32_t mid = (l + r) >> 1;
-        const int64_t tm = P.t[mid];
-        if (tm < ti || (tm == ti && P.ord[mid] < oi)) l = mid + 1; else r = mid;
-    }
-    const uint32_t k2 = l;
-    r = k4;  // k3: first (t, ord) > (tj, oj)
-    while (l < r) {
-        const uint32_t mid = (l + r) >> 1;
-        const int64_t tm = P.t[mid];
-        if (tm < tj || (tm == tj && P.ord[mid] < oj)) l = mid + 1; else r = mid;
-    }
-    const uint32_t k3 = l;
+    const uint32_t k1 = p_t_lower(P, kb, ke, lo);
+    const uint32_t k2 = p_gallop_rec(P, k1, ke, ti, oi);
+    const uint32_t k3 = p_gallop_rec(P, k2, ke, tj, oj);
+    const uint32_t k4 = p_gallop_tupper(P, k3, ke, hi);
     uint32_t k2e = k2;  // type I records whose own t is at most t_last
     if (t_last != INT64_MAX) {
-        l = k1; r = k2;
+        uint32_t l = k1, r = k2;
         while (l < r) { const uint32_t mid = (l + r) >> 1; if (P.t[mid] <= t_last) l = mid + 1; else r = mid; }
         k2e = l;
     }

@@ -41,16 +41,27 @@ def partition_bounds(cost_prefix: np.ndarray, world: int) -> List[Tuple[int, int
 
 
 def allreduce_counters(raw: np.ndarray, group=None, device=None) -> np.ndarray:
-    """Sum 56 u64 counters across ranks.  u64 -> i64 reinterpretation keeps the
-    sum exact modulo 2^64, which is the counters' own arithmetic."""
+    """Exact cross-rank sum of 56 u64 counters.  Each counter travels as two
+    32-bit halves in int64 words (a sum over <= 2^31 ranks cannot wrap), and
+    the totals are recombined with Python integers: a total past 2^64 - 1
+    raises CounterOverflowError, as the reference's checked merge of worker
+    partials does (executor.cpp:173-179, types.hpp:65-70)."""
     import torch
     import torch.distributed as dist
-    a = np.ascontiguousarray(raw, np.uint64).view(np.int64)
-    t = torch.from_numpy(a.copy())
+    from .tmotif import CounterOverflowError
+    a = np.ascontiguousarray(raw, np.uint64)
+    halves = np.empty(2 * len(a), np.int64)
+    halves[0::2] = (a & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    halves[1::2] = (a >> np.uint64(32)).astype(np.int64)
+    t = torch.from_numpy(halves)
     if device is not None:
         t = t.to(device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return t.cpu().numpy().view(np.uint64).copy()
+    h = t.cpu().numpy()
+    tot = [int(lo) + (int(hi) << 32) for lo, hi in zip(h[0::2], h[1::2])]
+    if any(x >> 64 for x in tot):
+        raise CounterOverflowError("motif counter overflow in the cross-rank merge")
+    return np.array(tot, dtype=np.uint64)
 
 
 def run_distributed(ctx, config, rank: int, world: int, group=None, device=None):
@@ -67,14 +78,26 @@ def run_distributed(ctx, config, rank: int, world: int, group=None, device=None)
     return tm.merge_census(rc.star, rc.pair, rc.tri, config.triangle_mode)
 
 
-def time_slice_bounds(t, world: int) -> List[Tuple[object, object]]:
-    """Per-rank [lo, hi) first-edge time bounds balanced by edge count
-    (None = open end).  Deterministic for the same t on every rank."""
+def time_slice_bounds(t, world: int, delta=None) -> List[Tuple[object, object]]:
+    """Per-rank [lo, hi) first-edge time bounds (None = open end),
+    deterministic for the same t on every rank.  Without `delta` they are
+    edge-count quantiles; with it, quantiles of an estimated work
+    w_e = 1 + n_delta(e), n_delta(e) = edges with t in [t_e, t_e + delta]: a
+    burst's edges have long windows at every center and weigh more, while a
+    stationary stream (configs 1 and 4) keeps the edge-count split."""
     ts = np.asarray(t, np.int64)
     if len(ts) > 1 and not bool(np.all(ts[1:] >= ts[:-1])):
         ts = np.sort(ts)
     m = len(ts)
-    cuts = [int(ts[(r * m) // world]) for r in range(1, world)] if m else []
+    if not m:
+        cuts = []
+    elif delta is None:
+        cuts = [int(ts[(r * m) // world]) for r in range(1, world)]
+    else:
+        top = ts + np.minimum(np.int64(delta), np.int64(2 ** 63 - 1) - ts)
+        w = 1 + (np.searchsorted(ts, top, side="right") - np.arange(m))
+        cw = np.cumsum(w, dtype=np.float64)
+        cuts = [int(ts[min(m - 1, int(np.searchsorted(cw, cw[-1] * r / world)))]) for r in range(1, world)]
     lows = [None] + cuts
     highs = cuts + [None]
     return list(zip(lows, highs))
