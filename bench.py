@@ -37,19 +37,23 @@ DEFAULT_CONFIG = "powerlaw_50m_600m"
 # Algorithmic bytes per STEP for each kernel family:
 # bytes that must cross HBM at least once.  Times are u32 offsets (narrow
 # records) when the time span fits 32 bits, else int64 (wide).
-#   radix_downsweep per key per digit pass: u64 key read + write (keys only)
+#   radix_downsweep per key per digit pass: u64 key read + write, plus (narrow
+#                 records) the u64 payload read + write
 #                 node sort: 2m keys (node << 32 | record), ceil(nb/8) passes
 #                 pair sort: m keys (min << 32 | edge), ceil(nb/8) passes
 #                 t sort:    m keys, ceil(tbits/8) passes (unsorted input only)
-#   gather_s      per incident record: sorted key 8 + edge record 8 (16 wide)
-#                 + S outputs t 4 (8), nbr 4, ord 4, node 4
-#   gather_p      per edge: sorted key 8 + edge record 8 (16) + P outputs t 4 (8),
-#                 ord 4, min 4, max 4, w 4
+#   gather_s      per incident record: sorted key 8 + payload 8 (narrow; wide:
+#                 the 16-byte edge record) + S outputs t 4 (8), nbr 4, ord 4, node 4
+#   gather_p      per edge: sorted key 8 + payload 8 (16) + P outputs t 4 (8), ord 4,
+#                 min 4, max 4, w 4
+#   pair_keys     per incident record: key 8 + S nbr 4 + S t 4; per edge the pair
+#                 key 8 + payload 8 written
 #   star_filter   per edge: P t 4 (8) + P w 4
 #   tri_filter    per forward record (one per edge): F t 4 (8) + F node 4 + F nbr 4
 #   scan          per mask word: 2 words read + 2 prefix words written
 #   work kernels (random access; one 32-byte sector per dependent lookup):
-#   star_work     per candidate: list entry 4 + P record 16 + the S locate 32
+#   star_locate   per candidate: list entry 4 + P record 16 + the S locate 32 + PS entry 8
+#   star_work     per candidate: list entry 4 + P record 16 + its PS entry 8
 #   tri_wedge     per short wedge: wedge 8 + two F records 24 + the closing lookup 32
 #   tri_long      per long wedge: F record 12 + the closing lookup 32
 def algo_bytes(n, m, t, stats=None):
@@ -58,17 +62,21 @@ def algo_bytes(n, m, t, stats=None):
     pbits = max(1, int(m - 1).bit_length())
     tb = int(int(t.max()) - int(t.min())).bit_length() if m else 0
     unsorted = bool(m > 1 and (np.diff(t) < 0).any())
-    sort = R * 8 * 2 * ((nb + 7) // 8)
-    sort += m * 8 * 2 * ((nb + 7) // 8)
+    narrow = tb <= 32
+    kv = 16 if narrow else 8  # key (+ payload) bytes per sorted element
+    sort = R * kv * 2 * ((nb + 7) // 8)
+    sort += m * kv * 2 * ((nb + 7) // 8)
     if unsorted:
         sort += m * (8 if tb + pbits <= 64 else 12) * 2 * ((tb + 7) // 8)
-    narrow = tb <= 32
     tw = 4 if narrow else 8
-    eb = 8 if narrow else 16  # narrow / wide edge records (tm_graph.cu EdgeCodec)
+    eb = 8 if narrow else 16
     out = {"radix_downsweep": sort, "gather_s": R * (8 + eb + tw + 12), "gather_p": m * (8 + eb + tw + 16),
-           "star_filter": m * (tw + 4), "tri_filter": m * (tw + 8), "scan": (R + m) // 32 * 16}
+           "pair_keys": R * 16 + m * 16, "star_filter": m * (tw + 4), "tri_filter": m * (tw + 8),
+           "scan": (R + m) // 32 * 16}
     if stats:
-        out["star_work"] = (stats["star_first_candidates"] + stats["star_third_candidates"]) * 52
+        cand = stats["star_first_candidates"] + stats["star_third_candidates"]
+        out["star_locate"] = cand * 60
+        out["star_work"] = cand * 28
         out["tri_wedge"] = stats["short_wedges"] * 64
         out["tri_long"] = stats["long_wedges"] * 44
     return out

@@ -158,7 +158,8 @@ struct TriStage {
     uint32_t f_begin = 0, f_end = 0;
     uint64_t* wedges = nullptr;
     uint64_t wedge_cap = 0;
-    uint32_t* long_list = nullptr;
+    uint32_t* long_list = nullptr;  // long windows from the front, very long ones from the back
+    uint32_t long_cap = 0;
     uint64_t* wbuf = nullptr;
     unsigned long long* pt = nullptr;  // pair table for the long windows (keys, then values)
     uint64_t pt_cap = 0;

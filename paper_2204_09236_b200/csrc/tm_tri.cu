@@ -179,6 +179,8 @@ __device__ __forceinline__ void wedges_from(const PView& P, const TimeArr& T,
 // runs past kWedgeScan records (or whose wedges do not fit the list) goes to
 // the long list instead and is enumerated by tri_long_kernel.
 constexpr int kWedgeScan = 8;
+constexpr int kGroupCache = 128;
+constexpr uint32_t kGroupCacheMinWindow = 64;  // shorter windows repeat few groups: plain path
 
 constexpr int kFilterItems = 4;  // first edges per thread per block iteration (one reservation)
 __global__ void __launch_bounds__(256) tri_filter_kernel(TimeArr FT,
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(TimeArr FT,
                                                          uint64_t* __restrict__ wedges,
                                                          uint64_t wedge_cap,
                                                          uint32_t* __restrict__ long_list,
+                                                         uint32_t long_cap,
                                                          unsigned long long* __restrict__ wcount,
                                                          uint32_t* __restrict__ lcount) {
     constexpr uint64_t kStep = 256 * kFilterItems;
@@ -216,9 +219,15 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(TimeArr FT,
                 }
             }
             if (alive && i + kWedgeScan + 1 < fe && Fnode[i + kWedgeScan + 1] == node &&
-                FT[i + kWedgeScan + 1] <= lim)
-                longs |= 1u << jj;
-            else
+                FT[i + kWedgeScan + 1] <= lim) {
+                // a window past kGroupCacheMinWindow records goes to the very-long
+                // list, filled from the back of the same buffer (lcount[1])
+                const uint64_t x = i + 1 + kGroupCacheMinWindow;
+                if (x < fe && Fnode[x] == node && FT[x] <= lim)
+                    long_list[long_cap - 1 - atomicAdd(lcount + 1, 1u)] = (uint32_t)i;
+                else
+                    longs |= 1u << jj;
+            } else
                 hits4 |= hits << (8 * jj);
         }
         const uint32_t nw = (uint32_t)__popc(hits4);
@@ -307,37 +316,98 @@ __global__ void __launch_bounds__(256, 5) tri_wedge_kernel(PView P, TimeArr FT,
 }
 
 // first edges with long windows: one warp per first edge, lanes stride the
-// in-window records (the HARE intra-node split, per first edge)
-__global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
+// in-window records (the HARE intra-node split, per first edge).
+//
+// The window of a long first edge i (neighbour v) holds records to few
+// distinct neighbours w -- the long windows are those of high-degree centers,
+// whose forward neighbours are the hubs above them -- so every (v, w) closing
+// group is met many times.  Each warp keeps a direct-mapped cache of its
+// current first edge's groups (keyed by w): the group [kb, ke), the
+// boundaries that depend on e_i only (k2 = first record at or after e_i, k4 =
+// first record past t_i + delta) and the last k1 / k3 found.  A hit costs two
+// short gallops (k1 and k3 only grow with t_j) instead of the block search,
+// the group end and four window searches.
+struct GroupCacheEntry {
+    uint32_t w, k1, k2, k3, k4, d2, d4, pad;  // d2, d4: direction prefix at k2, k4
+};
+
+// first k in [from, end) with t >= x, galloping up from `from`
+__device__ __forceinline__ uint32_t p_gallop_tlower(const PView& P, uint32_t from, uint32_t end, int64_t x) {
+    uint32_t lo = from, hi = end;
+    for (uint32_t span = 1;; span <<= 1) {
+        const uint64_t probe = (uint64_t)lo + span - 1;
+        if (probe >= end) break;
+        if (P.t[probe] >= x) {
+            hi = (uint32_t)probe;
+            break;
+        }
+        lo = (uint32_t)probe + 1;
+    }
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (P.t[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// the v-w group [kb, ke) (empty when no v-w record: kb == ke)
+__device__ __forceinline__ void locate_group(const PView& P, uint32_t v, uint32_t w, uint32_t& kb, uint32_t& ke) {
+    const uint32_t a = min(v, w), b = max(v, w);
+    const uint32_t blk_end = P.pofs[a + 1];
+    kb = p_max_lower(P, P.pofs[a], blk_end, b);
+    if (kb >= blk_end || P.max[kb] != b) {
+        kb = ke = 0;
+        return;
+    }
+    ke = P.gend ? p_group_end(P, kb) : p_max_upper(P, kb, blk_end, b);
+}
+
+// Two instantiations share the long list: kCache = false takes the first
+// edges whose window holds at most kGroupCacheMinWindow records (one closing
+// count per wedge, full occupancy), kCache = true the longer ones (the group
+// cache's shared memory costs a resident block per SM).
+template <bool kCache>
+__global__ void __launch_bounds__(256, kCache ? 4 : 5) tri_long_kernel(PView P, TimeArr FT,
                                                        const uint32_t* __restrict__ FN,
                                                        const uint32_t* __restrict__ FO,
                                                        const uint32_t* __restrict__ Fnode,
                                                        const uint32_t* __restrict__ Foff,
                                                        int64_t delta, int64_t t_last,
-                                                       const uint32_t* __restrict__ list,
+                                                       const uint32_t* __restrict__ list, uint32_t long_cap,
                                                        const uint32_t* __restrict__ lcount,
                                                        const unsigned long long* __restrict__ pt_wsum,
                                                        uint64_t pt_min_wedges, uint64_t gend_min,
                                                        unsigned long long* queue, uint64_t* out,
                                                        uint64_t* stats) {
     __shared__ unsigned long long cells[48];
+    __shared__ GroupCacheEntry gcache[8][kCache ? kGroupCache : 1];
     zero_cells(cells, 24);
     __syncthreads();
     WarpCells wc;
-    const uint32_t cnt = *lcount;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && stats) stats[3] = cnt;
-    if (!P.pt_keys || *pt_wsum < pt_min_wedges) P.pt_keys = nullptr;  // the table was not built
-    if (!P.gend || *pt_wsum < gend_min) P.gend = nullptr;               // nor the group ends
+    // the plain instantiation takes the long list (front), the cached one the
+    // very-long list (back of the buffer)
+    const uint32_t cnt = lcount[kCache ? 1 : 0];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && stats) atomicAdd((unsigned long long*)&stats[3], (unsigned long long)cnt);
+    if (!P.gend || *pt_wsum < gend_min) P.gend = nullptr;  // group ends not built
     uint32_t my_wedges = 0;
     const int lane = threadIdx.x & 31;
+    GroupCacheEntry* gc = gcache[threadIdx.x >> 5];
     for (;;) {  // one first edge per warp from the queue
         const uint64_t idx = warp_take(queue, 1);
         if (idx >= cnt) break;
-        const uint32_t i = list[idx];
+        const uint32_t i = kCache ? list[long_cap - 1 - idx] : list[idx];
         const uint32_t end = Foff[Fnode[i] + 1];
-        const uint32_t v = FN[i] & kNodeMask;
-        const int64_t lim = sat_add(FT[i], delta);
-        for (uint32_t j0 = i + 1; j0 < end; j0 += 32) {
+        const uint32_t ni = FN[i];
+        const uint32_t v = ni & kNodeMask;
+        const int64_t ti = FT[i];
+        const uint32_t oi = FO[i];
+        const int64_t lim = sat_add(ti, delta);
+        // a window of at most kGroupCacheMinWindow records: one closing count
+        // per wedge; a longer one goes through the group cache
+        const bool longwin = kCache;
+        bool more = longwin;
+        uint32_t j0 = i + 1;
+        for (; !longwin && j0 < end; j0 += 32) {
             const uint32_t j = j0 + lane;
             const bool in = j < end && FT[j] <= lim;
             const bool wedge = in && (FN[j] & kNodeMask) != v;
@@ -348,8 +418,84 @@ __global__ void __launch_bounds__(256, 5) tri_long_kernel(PView P, TimeArr FT,
                 ++my_wedges;
             }
             wc.add6(wedge, cb, c, cells, 24);
+            if (!__all_sync(0xffffffffu, in)) {
+                more = false;
+                break;
+            }
+        }
+        if (!more || j0 >= end) continue;
+        for (int x = lane; x < kGroupCache; x += 32) gc[x].w = 0xFFFFFFFFu;
+        __syncwarp();
+        uint32_t misses = 0;
+        for (; j0 < end; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            const bool in = j < end && FT[j] <= lim;
+            const uint32_t nj = in ? FN[j] : 0u;
+            const uint32_t w = nj & kNodeMask;
+            const bool wedge = in && w != v;
+            uint32_t c[6] = {0, 0, 0, 0, 0, 0};
+            int cb = 0;
+            const uint32_t slot = (w * 0x9E3779B1u) >> (32 - 7);
+            GroupCacheEntry e;
+            if (wedge) {
+                const int64_t tj = FT[j];
+                const uint32_t oj = FO[j];
+                e = gc[slot];
+                if (e.w != w) {  // miss: the group and its e_i boundaries
+                    ++misses;
+                    e.w = w;
+                    uint32_t kb, ke;
+                    locate_group(P, v, w, kb, ke);
+                    e.k1 = p_t_lower(P, kb, ke, sat_sub(tj, delta));
+                    e.k2 = p_gallop_rec(P, e.k1, ke, ti, oi);
+                    e.k4 = p_t_upper(P, e.k2, ke, lim);
+                    e.k3 = e.k2;
+                    e.d2 = p_dir_before(P, e.k2);
+                    e.d4 = p_dir_before(P, e.k4);
+                }
+                // the window's lower end t_j - delta and e_j only move forward with j
+                const uint32_t k1 = p_gallop_tlower(P, e.k1, e.k2, sat_sub(tj, delta));
+                const uint32_t k3 = p_gallop_rec(P, e.k3 > e.k2 ? e.k3 : e.k2, e.k4, tj, oj);
+                e.k1 = k1;
+                e.k3 = k3;
+                const uint32_t a = min(v, w);
+                const uint32_t flip = v == a ? 0u : 1u;
+                uint32_t k2e = e.k2;
+                if (t_last != INT64_MAX) {
+                    uint32_t l = k1, r = e.k2;
+                    while (l < r) {
+                        const uint32_t mid = (l + r) >> 1;
+                        if (P.t[mid] <= t_last) l = mid + 1; else r = mid;
+                    }
+                    k2e = l;
+                }
+                // direction split of each type range from the P direction
+                // prefix (at k2 and k4 cached per group)
+                auto add_range = [&](int type, uint32_t x0, uint32_t d0, uint32_t x1, uint32_t d1) {
+                    if (x1 <= x0) return;
+                    const uint32_t n1 = d1 - d0;
+                    const uint32_t n0 = (x1 - x0) - n1;
+                    c[type * 2 + flip] += n0;
+                    c[type * 2 + (flip ^ 1u)] += n1;
+                };
+                const uint32_t d1 = p_dir_before(P, k1), d3 = p_dir_before(P, k3);
+                add_range(0, k1, d1, k2e, k2e == e.k2 ? e.d2 : p_dir_before(P, k2e));
+                if (ti <= t_last) {
+                    add_range(1, e.k2, e.d2, k3, d3);
+                    add_range(2, k3, d3, e.k4, e.d4);
+                }
+                cb = (int)((ni >> 31) * 4 + (nj >> 31) * 2);
+                ++my_wedges;
+            }
+            // one writer per cache slot: the highest wedge lane that maps there
+            const unsigned peers = __match_any_sync(0xffffffffu, wedge ? slot : 0xFFFFFFFFu);
+            if (wedge && (peers >> lane) == 1u) gc[slot] = e;
+            __syncwarp();
+            wc.add6(wedge, cb, c, cells, 24);
             if (!__all_sync(0xffffffffu, in)) break;
         }
+        misses = warp_sum(misses);
+        if (lane == 0 && misses && stats) atomicAdd((unsigned long long*)&stats[5], (unsigned long long)misses);
     }
     wc.flush(cells, 24, 24);
     my_wedges = warp_sum(my_wedges);
@@ -395,13 +541,14 @@ __global__ void __launch_bounds__(256) tri_items_kernel(SView S, PView P, int64_
 // long first edge (one gallop per first edge, warp-aggregated sum)
 __global__ void long_window_sum_kernel(TimeArr FT, const uint32_t* __restrict__ Fnode,
                                        const uint32_t* __restrict__ Foff, int64_t delta,
-                                       const uint32_t* __restrict__ list, const uint32_t* __restrict__ lcount,
+                                       const uint32_t* __restrict__ list, uint32_t long_cap,
+                                       const uint32_t* __restrict__ lcount,
                                        unsigned long long* __restrict__ sum) {
-    const uint32_t cnt = *lcount;
+    const uint32_t n0 = lcount[0], cnt = n0 + lcount[1];
     unsigned long long acc = 0;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
          idx += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t i = list[idx];
+        const uint32_t i = idx < n0 ? list[idx] : list[long_cap - 1 - (idx - n0)];
         const uint32_t end = Foff[Fnode[i] + 1];
         const int64_t lim = sat_add(FT[i], delta);
         uint32_t lo = i + 1, hi = end, span = 8;
@@ -495,17 +642,18 @@ void tri_filter_stage(const DeviceGraph& g, const Forward& f, int64_t delta, uin
     unsigned long long* wcount = reinterpret_cast<unsigned long long*>(ts.wbuf);
     uint32_t* lcount = reinterpret_cast<uint32_t*>(ts.wbuf + 2);
     ts.long_list = dalloc<uint32_t>(work + 1, st);
+    ts.long_cap = (uint32_t)(work + 1);
     TM_CUDA(cudaMemsetAsync(wcount, 0, sizeof(uint64_t), st));
     TM_CUDA(cudaMemsetAsync(wcount + 1, 0xFF, sizeof(uint64_t), st));
-    TM_CUDA(cudaMemsetAsync(lcount, 0, sizeof(uint32_t), st));
+    TM_CUDA(cudaMemsetAsync(lcount, 0, 2 * sizeof(uint32_t), st));
     TM_LAUNCH("tri_filter", st, tri_filter_kernel, (unsigned)grid, 256, 0, f.t.view(g.tbase), f.nbr, f.node, delta,
-              f_begin, f_end, ts.wedges, ts.wedge_cap, ts.long_list, wcount, lcount);
+              f_begin, f_end, ts.wedges, ts.wedge_cap, ts.long_list, (uint32_t)(work + 1), wcount, lcount);
     // the long windows' wedge bound gates the group ends (both counting
     // kernels) and the pair table (long windows) on the device: no host sync
     ts.wsum = dalloc<unsigned long long>(1, st);
     TM_CUDA(cudaMemsetAsync(ts.wsum, 0, sizeof(unsigned long long), st));
     TM_LAUNCH("tri_gate", st, long_window_sum_kernel, (unsigned)cap, 256, 0, f.t.view(g.tbase), f.node, f.off,
-              delta, ts.long_list, lcount, ts.wsum);
+              delta, ts.long_list, (uint32_t)(work + 1), lcount, ts.wsum);
     ts.valid = true;
 }
 
@@ -543,8 +691,8 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
     const uint64_t cap = (uint64_t)sm_count() * 8;
     unsigned long long* wcount = reinterpret_cast<unsigned long long*>(ts.wbuf);
     uint32_t* lcount = reinterpret_cast<uint32_t*>(ts.wbuf + 2);
-    ts.queue = dalloc<unsigned long long>(2, st);
-    TM_CUDA(cudaMemsetAsync(ts.queue, 0, 2 * sizeof(unsigned long long), st));
+    ts.queue = dalloc<unsigned long long>(3, st);
+    TM_CUDA(cudaMemsetAsync(ts.queue, 0, 3 * sizeof(unsigned long long), st));
     PView pv = pview(g);
     const uint64_t gend_min = group_end_min_wedges(g);
     if (gend_min != ~0ull && g.m) {
@@ -579,9 +727,12 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
         pv.pt_vals = ts.pt + pc;
         pv.pt_mask = pc - 1;
     }
-    TM_LAUNCH("tri_long", st, tri_long_kernel, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
-              f.node, f.off, ts.delta, t_last, ts.long_list, lcount, ts.wsum, min_wedges, gend_min, ts.queue + 1, d_out,
-              d_stats);
+    TM_LAUNCH("tri_long", st, tri_long_kernel<false>, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
+              f.node, f.off, ts.delta, t_last, ts.long_list, ts.long_cap, lcount, ts.wsum, min_wedges, gend_min,
+              ts.queue + 1, d_out, d_stats);
+    TM_LAUNCH("tri_long", st, tri_long_kernel<true>, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
+              f.node, f.off, ts.delta, t_last, ts.long_list, ts.long_cap, lcount, ts.wsum, min_wedges, gend_min,
+              ts.queue + 2, d_out, d_stats);
     dfree(ts.pt, st);
     dfree(ts.gend, st);
     dfree(ts.queue, st);

@@ -717,7 +717,7 @@ class GraphContext:
         out = np.zeros(8, np.uint64)
         _raise(self._lib.tm_run_stats(self._h, out.ctypes.data), self._lib)
         keys = ["star_first_candidates", "star_third_candidates", "short_wedges", "long_first_edges",
-                "long_wedges"]
+                "long_wedges", "long_group_lookups"]
         return {k: int(v) for k, v in zip(keys, out)}
 
     def partition(self, world: int, rank: int) -> Tuple[int, int]:
