@@ -1448,8 +1448,8 @@ int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t
             TM_CUDA(cudaMemcpyAsync(sl.dt, t, m * sizeof(int64_t), cudaMemcpyHostToDevice, A.copy));
         }
         TM_CUDA(cudaEventRecord(sl.copied, A.copy));
-        TM_CUDA(cudaStreamWaitEvent(s, sl.copied, 0));
-        // the previous batch's deferred census runs now, behind this copy
+        // the previous batch's deferred census runs now, while this copy is in
+        // flight -- before `s` is made to wait for it
         AsyncSlot& prev = A.slot[(tk & 1) ^ 1];
         if (prev.busy && prev.deferred) {
             try {
@@ -1459,6 +1459,7 @@ int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t
                 prev.res.err = e.what();
             }
         }
+        TM_CUDA(cudaStreamWaitEvent(s, sl.copied, 0));
         if (m && !(m <= kReplayMaxEdges && replay_enabled())) {
             sl.deferred = true;  // eager (host-synchronous) count: issued with the next submission or the wait
             *ticket = tk;

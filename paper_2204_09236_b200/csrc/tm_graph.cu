@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
     uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, uint32_t* __restrict__ counts, uint32_t ntiles,
     BuildStats* __restrict__ st) {
     constexpr int NW = kPackBlock / 32;
-    __shared__ uint32_t hist[NW][256];
+    __shared__ uint32_t hist[NW][kRadix];
     const int w = threadIdx.x >> 5;
     int nbits = 1;
     while (nbits < 32 && ((n > 1 ? n - 1 : 1) >> nbits)) ++nbits;
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
     unsigned bad = 0, uns = 0;
     if (st) tmin = t[0];
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int i = threadIdx.x; i < NW * 256; i += kPackBlock) (&hist[0][0])[i] = 0;
+        for (int i = threadIdx.x; i < NW * kRadix; i += kPackBlock) (&hist[0][0])[i] = 0;
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kPackEdges / kPackBlock; ++j) {
@@ -272,12 +272,28 @@ __global__ void gather_s_pay_kernel(const uint64_t* __restrict__ skeys, const ui
 
 // pair keys from the max-side records of S (in (max, t, ordinal) order):
 // min << 32 | p, compacted by the xmask prefix
+// Degree class for the triangle pass's orientation: the degree itself below
+// 8, else 3 mantissa bits under the leading bit (~12 % steps) -- monotone in
+// the degree, so (class, id) is a strict total order that still puts hubs
+// last.  One byte per node (50 MB at 50M nodes) stays in L2 under pair_keys'
+// random neighbour reads, where the 4-byte CSR offsets (two per read, 200 MB)
+// missed: config 4 pair_keys read 81 GB from HBM for 19 GB of keys and S.
+__device__ __forceinline__ uint8_t degree_class(uint32_t d) {
+    if (d < 8) return (uint8_t)d;
+    const int e = 31 - __clz(d);
+    return (uint8_t)(8 + (e - 3) * 8 + ((d >> (e - 3)) & 7u));
+}
+__global__ void degree_class_kernel(const uint32_t* __restrict__ off, uint64_t n, uint8_t* __restrict__ cls) {
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x)
+        cls[u] = degree_class(off[u + 1] - off[u]);
+}
+
 // (narrow records: also the payload (t - tmin) << 32 | max | dir_rel_min << 31
 // for gather_p_pay, read from S_t / S_nbr)
 __global__ void pair_keys_kernel(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ S_nbr,
                                  const uint32_t* __restrict__ S_tn,
                                  const uint32_t* __restrict__ xmask, const uint32_t* __restrict__ xpref,
-                                 const uint32_t* __restrict__ off, uint64_t R, uint64_t* __restrict__ pkeys,
+                                 const uint8_t* __restrict__ cls, uint64_t R, uint64_t* __restrict__ pkeys,
                                  uint64_t* __restrict__ pvals, uint32_t* __restrict__ fmask) {
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
          base += (uint64_t)gridDim.x * blockDim.x) {
@@ -287,9 +303,9 @@ __global__ void pair_keys_kernel(const uint64_t* __restrict__ skeys, const uint3
             const uint64_t key = __ldcs(skeys + q);
             const uint32_t nbr = __ldcs(S_nbr + q);
             const uint32_t u = (uint32_t)(key >> 32), x = nbr & kNodeMask;
-            // degree-rank orientation of the triangle pass: forward iff (deg, id) of
-            // the neighbour exceeds the center's
-            const uint32_t du = off[u + 1] - off[u], dx = off[x + 1] - off[x];
+            // degree orientation of the triangle pass: forward iff (degree class,
+            // id) of the neighbour exceeds the center's
+            const uint32_t du = cls[u], dx = cls[x];
             fwd = (dx > du || (dx == du && x > u)) ? 1u : 0u;
             const uint32_t word = xmask[q >> 5], bit = 1u << (q & 31);
             if (word & bit) {
@@ -657,7 +673,7 @@ BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d
             ws->nk1 = dalloc<uint64_t>(R + kSortPad, s);
             ws->nv0 = dalloc<uint64_t>(R + kSortPad, s);
             ws->nv1 = dalloc<uint64_t>(R + kSortPad, s);
-            ws->c0 = dalloc<uint32_t>((uint64_t)256 * pl.ntiles, s);
+            ws->c0 = dalloc<uint32_t>((uint64_t)kRadix * pl.ntiles, s);
             ws->E = dalloc<uint8_t>(m * sizeof(WideEdge), s);
             ws->st = dalloc<uint8_t>(sizeof(BuildStats), s);
         }
@@ -674,7 +690,7 @@ BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d
         pl.nk1 = dalloc<uint64_t>(R + kSortPad, s);
         pl.nv0 = dalloc<uint64_t>(R + kSortPad, s);
         pl.nv1 = dalloc<uint64_t>(R + kSortPad, s);
-        pl.c0 = dalloc<uint32_t>((uint64_t)256 * pl.ntiles, s);
+        pl.c0 = dalloc<uint32_t>((uint64_t)kRadix * pl.ntiles, s);
         pl.E = dalloc<uint8_t>(m * sizeof(NarrowEdge), s);
         pl.E_bytes = m * sizeof(NarrowEdge);
         d_st = dalloc<BuildStats>(1, s);
@@ -877,8 +893,11 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         uint64_t* pv0 = narrow ? dalloc<uint64_t>(m + kSortPad, s) : nullptr;
         uint64_t* pv0_alloc = pv0;
         uint64_t* pv1 = nv1;  // the node sort's second value buffer
-        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, g.S_t.n, xmask, xpref, g.off,
+        uint8_t* cls = dalloc<uint8_t>(n + 1, s);
+        TM_LAUNCH("degree_class", s, degree_class_kernel, grid_for(n), 256, 0, g.off, n, cls);
+        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, g.S_t.n, xmask, xpref, cls,
                   R, pk0, pv0, g.S_fmask);
+        dfree(cls, s);
 
         // the forward sequences (degree orientation) only need S and the
         // forward mask: build them on a side stream while the pair index sorts

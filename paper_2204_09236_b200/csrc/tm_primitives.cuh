@@ -383,7 +383,10 @@ void exclusive_scan(Load load, uint64_t n, T* out, cudaStream_t s) {
 // (20 bits: 7 + 7 + 6 rather than 8 + 8 + 4) -- fewer ballot rounds per
 // ranking and longer digit runs per tile in the wide passes (sortbench:
 // 20M node keys' downsweep -3 %, 200M keys of 26 bits -8 %)
-__host__ __device__ inline int radix_passes(int bits) { return (bits + 7) / 8; }
+#ifndef TM_RADIX_MAX_BITS
+#define TM_RADIX_MAX_BITS 8  // digit bits per pass at most (9-bit digits measured slower: 512-row passes)
+#endif
+__host__ __device__ inline int radix_passes(int bits) { return (bits + TM_RADIX_MAX_BITS - 1) / TM_RADIX_MAX_BITS; }
 __host__ __device__ inline int radix_digit_width(int bits_left, int passes_left) {
     return (bits_left + passes_left - 1) / passes_left;
 }
@@ -394,7 +397,7 @@ __host__ __device__ inline int radix_digit_width(int bits_left, int passes_left)
 // count matrix -> downsweep (rank the tile with per-warp __match_any_sync,
 // keeping input order; reorder in shared memory; write each digit run as one
 // burst).  All tile loads are issued before any ranking (ILP).
-constexpr int kRadix = 256;
+constexpr int kRadix = 1 << TM_RADIX_MAX_BITS;  // digit rows a count matrix / histogram may need
 
 template <typename K, int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK) radix_upsweep(const K* __restrict__ keys, uint64_t n,
@@ -542,7 +545,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
                                                                    const uint32_t* __restrict__ totals) {
     constexpr int NW = BLOCK / 32, TILE = BLOCK * ITEMS;
     constexpr int kMatchRounds = NBITS >= 8 ? TM_RANK_MATCH_ROUNDS : TM_RANK_MATCH_ROUNDS_NARROW;
-    static_assert(BLOCK >= kRadix, "one digit per thread");
+    constexpr int RADIX = 1 << NBITS;
+    constexpr uint32_t kNone = RADIX;  // digit of a lane past the tile end
+    constexpr int DPT = (RADIX + BLOCK - 1) / BLOCK;  // digits per thread (consecutive)
     constexpr uint32_t STAGE_BYTES = TILE * (sizeof(K) + (kVals ? sizeof(V) : 0));
     extern __shared__ __align__(128) unsigned char tma_smem[];
     // [stage0][stage1]: each TILE keys (+ TILE vals); a tile is reordered in
@@ -551,8 +556,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
     auto stage_vals = [&](int s) {
         return reinterpret_cast<V*>(tma_smem + s * STAGE_BYTES + TILE * sizeof(K));
     };
-    __shared__ __align__(16) uint16_t wcnt[NW][kRadix];  // per-warp digit counts, then (warp, digit) run starts
-    __shared__ uint32_t dglob[kRadix];
+    __shared__ __align__(16) uint16_t wcnt[NW][RADIX];  // per-warp digit counts, then (warp, digit) run starts
+    __shared__ uint32_t dglob[RADIX];
     __shared__ __align__(8) uint64_t bar[2];
 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -574,19 +579,40 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
         if (kVals) tma_load_1d(stage_vals(s), vin + base, vbytes, &bar[s]);
     };
     // count rows exist for this pass's digits only (<= dmask)
-    const uint32_t dbase = block_exclusive_scan<uint32_t, NW>(tid <= (int)dmask ? totals[tid] : 0u, nullptr);
+    // global base of each of this thread's digits (digits tid * DPT + k)
+    uint32_t dbase[DPT];
+    {
+        uint32_t tot[DPT], tsum = 0;
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+            const int d = tid * DPT + k;
+            tot[k] = d <= (int)dmask ? totals[d] : 0u;
+            tsum += tot[k];
+        }
+        uint32_t run = block_exclusive_scan<uint32_t, NW>(tsum, nullptr);
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+            dbase[k] = run;
+            run += tot[k];
+        }
+    }
     uint32_t tile = blockIdx.x;
     if (tid == 0 && tile < ntiles) issue(tile, 0);
     for (uint32_t it = 0; tile < ntiles; ++it, tile += gridDim.x) {
         const int s = it & 1;
         const uint32_t next = tile + gridDim.x;
         if (tid == 0 && next < ntiles) issue(next, s ^ 1);
-        for (int i = tid; i < NW * kRadix / 8; i += BLOCK) reinterpret_cast<uint4*>(&wcnt[0][0])[i] = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < NW * RADIX / 8; i += BLOCK) reinterpret_cast<uint4*>(&wcnt[0][0])[i] = make_uint4(0, 0, 0, 0);
         const uint64_t tbase = (uint64_t)tile * TILE;
         const uint32_t tile_n = (uint32_t)((n - tbase) < (uint64_t)TILE ? (n - tbase) : (uint64_t)TILE);
         // the tile's digit offsets, loaded now and used after the ranking
         // (keeps the global-load latency off the critical path)
-        const uint32_t toff = tid <= (int)dmask ? __ldg(tile_offsets + (uint64_t)tid * ntiles + tile) : 0u;
+        uint32_t toff[DPT];
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+            const int d = tid * DPT + k;
+            toff[k] = d <= (int)dmask ? __ldg(tile_offsets + (uint64_t)d * ntiles + tile) : 0u;
+        }
         mbar_wait(&bar[s], (it >> 1) & 1);
         __syncthreads();
         K* sk = stage_keys(s);
@@ -601,7 +627,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
             const uint32_t i = w * (ITEMS * 32) + r * 32 + lane;
             key[r] = sk[i];
             if (kVals) val[r] = sv[i];
-            dig[r] = i < tile_n ? ((uint32_t)(key[r] >> shift) & dmask) : 256u;
+            dig[r] = i < tile_n ? ((uint32_t)(key[r] >> shift) & dmask) : kNone;
         }
         // Peer masks (lanes holding the same digit).  match.any costs ~60 clocks
         // per warp-instruction per SM on 8-bit random digits (ADU pipe,
@@ -614,8 +640,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
             if (r < kMatchRounds) {
                 rank[r] = __match_any_sync(0xffffffffu, dig[r]);
             } else {
-                uint32_t peers = full_tile ? 0xffffffffu : __ballot_sync(0xffffffffu, dig[r] < 256u);
-                if (dig[r] >= 256u) peers = ~peers;
+                uint32_t peers = full_tile ? 0xffffffffu : __ballot_sync(0xffffffffu, dig[r] < kNone);
+                if (dig[r] >= kNone) peers = ~peers;
 #pragma unroll
                 for (int b = 0; b < NBITS; ++b) peers &= wlms_bit(dig[r], 1u << b);
                 rank[r] = peers;
@@ -624,7 +650,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
         // running per-warp digit counts, one load -> store step per round
 #pragma unroll
         for (int r = 0; r < ITEMS; ++r) {
-            const bool valid = dig[r] < 256u;
+            const bool valid = dig[r] < kNone;
             const unsigned peers = rank[r];
             const uint32_t prev = valid ? wcnt[w][dig[r]] : 0u;
             rank[r] = prev + __popc(peers & lt);
@@ -633,27 +659,38 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
             __syncwarp();
         }
         __syncthreads();
-        uint32_t cnt = 0;
-        if (tid < kRadix) {
+        uint32_t cnt[DPT], csum = 0;
 #pragma unroll
-            for (int ww = 0; ww < NW; ++ww) cnt += wcnt[ww][tid];
-        }
-        const uint32_t ex = block_exclusive_scan<uint32_t, NW>(cnt, nullptr);
-        if (tid < kRadix) {
-            // tile position of each (warp, digit) run; global minus tile start per digit
-            uint32_t run = ex;
+        for (int k = 0; k < DPT; ++k) {
+            const int d = tid * DPT + k;
+            cnt[k] = 0;
+            if (d < RADIX) {
 #pragma unroll
-            for (int ww = 0; ww < NW; ++ww) {
-                const uint32_t c = wcnt[ww][tid];
-                wcnt[ww][tid] = (uint16_t)run;
-                run += c;
+                for (int ww = 0; ww < NW; ++ww) cnt[k] += wcnt[ww][d];
             }
-            dglob[tid] = toff + dbase - ex;
+            csum += cnt[k];
+        }
+        uint32_t ex = block_exclusive_scan<uint32_t, NW>(csum, nullptr);
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+            const int d = tid * DPT + k;
+            if (d < RADIX) {
+                // tile position of each (warp, digit) run; global minus tile start per digit
+                uint32_t run = ex;
+#pragma unroll
+                for (int ww = 0; ww < NW; ++ww) {
+                    const uint32_t c = wcnt[ww][d];
+                    wcnt[ww][d] = (uint16_t)run;
+                    run += c;
+                }
+                dglob[d] = toff[k] + dbase[k] - ex;
+            }
+            ex += cnt[k];
         }
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < ITEMS; ++r) {
-            if (dig[r] < 256u) {
+            if (dig[r] < kNone) {
                 const uint32_t q = wcnt[w][dig[r]] + rank[r];
                 sk[q] = key[r];
                 if (kVals) sv[q] = val[r];
@@ -710,7 +747,7 @@ void radix_sort_cfg(K*& keys, V*& vals, K*& keys_alt, V*& vals_alt, uint64_t n,
     const uint64_t ncount = (uint64_t)kRadix * ntiles;
     uint32_t* counts = dalloc<uint32_t>(2 * ncount + (uint64_t)kRadix * passes, s);
     uint32_t* offs = counts + ncount;
-    uint32_t* totals = offs + ncount;  // 256 digit totals (per pass, reused)
+    uint32_t* totals = offs + ncount;  // kRadix digit totals (per pass, reused)
     // the key bits spread evenly over ceil(bits / 8) passes (a producer that
     // counts the first digit itself uses the same width: radix_digit_width)
     int shift = bit_lo;
@@ -728,14 +765,17 @@ void radix_sort_cfg(K*& keys, V*& vals, K*& keys_alt, V*& vals_alt, uint64_t n,
                   offs, totals);
         V* vin = with_vals ? vals : nullptr;
         V* vout = with_vals ? vals_alt : nullptr;
+// (u64 keys + u64 payloads: 96 KB of tile stages per block, so 2 resident
+// blocks per SM and the register budget of 2)
 #define TM_DOWNSWEEP(HV, NB)                                                                                    \
-    launch_downsweep<K, V, HV, BLOCK, ITEMS, MINB, NB>(keys, vin, keys_alt, vout, n, shift, dmask, offs, ntiles, \
-                                                       totals, s)
+    launch_downsweep<K, V, HV, BLOCK, ITEMS, (HV && sizeof(K) + sizeof(V) >= 16) ? 2 : MINB, NB>(           \
+        keys, vin, keys_alt, vout, n, shift, dmask, offs, ntiles, totals, s)
         if (with_vals) {
             if (width <= 4) TM_DOWNSWEEP(true, 4);
             else if (width <= 6) TM_DOWNSWEEP(true, 6);
             else if (width <= 7) TM_DOWNSWEEP(true, 7);
-            else TM_DOWNSWEEP(true, 8);
+            else if (width <= 8) TM_DOWNSWEEP(true, 8);
+            else TM_DOWNSWEEP(true, 9);
             V* tv = vals;
             vals = vals_alt;
             vals_alt = tv;
@@ -743,7 +783,8 @@ void radix_sort_cfg(K*& keys, V*& vals, K*& keys_alt, V*& vals_alt, uint64_t n,
             if (width <= 4) TM_DOWNSWEEP(false, 4);
             else if (width <= 6) TM_DOWNSWEEP(false, 6);
             else if (width <= 7) TM_DOWNSWEEP(false, 7);
-            else TM_DOWNSWEEP(false, 8);
+            else if (width <= 8) TM_DOWNSWEEP(false, 8);
+            else TM_DOWNSWEEP(false, 9);
         }
 #undef TM_DOWNSWEEP
         shift += width;

@@ -13,7 +13,7 @@
 // enumerated exactly once, at its lowest-ranked vertex:
 //   * node-index order  == the reference's removal mode (alive = later nodes),
 //     giving Tri cells identical to count_triangles(removal);
-//   * (degree, id) order == the same instances with hubs last, used for
+//   * (degree class, id) order == the same instances with hubs last, used for
 //     count_all: each instance lands once in every cell of its isomorphism
 //     class (one per type, motifs.cpp fibers), so the host expands class sums
 //     into the reference's count_all cells.
