@@ -221,7 +221,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--reader", action="store_true", help="also time the GPU edge-list reader (config 1 sizes)")
     ap.add_argument("--no-reader", action="store_true", help=argparse.SUPPRESS)
-    ap.add_argument("--cpu-sample-edges", type=int, default=1_000_000)
+    ap.add_argument("--cpu-sample-edges", type=int, default=2_000_000)
     ap.add_argument("--delta", type=int, default=None, help="override the config's delta")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="counter all-reduce backend (gloo: CPU tensors, for multi-rank tests on one GPU)")

@@ -1,14 +1,46 @@
 #!/bin/bash
 # The GPU-side captures behind profiles/r02/ (run under gpurun; each ncu pass
-# only after the same command has exited 0 without ncu).
+# only after the same command has exited 0 without ncu).  The ncu reports are
+# summarised on the box (profiles/ncu_summary.py, ncu_lines.py) and deleted,
+# so only text comes back; profiles/refresh_r02.sh copies it into profiles/r02.
 set -x
-mkdir -p gpurun_out/r02cap
-python bench.py > gpurun_out/r02cap/bench.json 2> gpurun_out/r02cap/bench.err; echo bench=$?
-python profiles/census_once.py powerlaw_50m_600m 3600 2 > gpurun_out/r02cap/census_once.jsonl 2>&1; echo once=$?
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02cap/launches.csv \
-    python profiles/census_once.py powerlaw_50m_600m 3600 2 > gpurun_out/r02cap/ncu_launch.log 2>&1; echo launches=$?
-ncu --set full --clock-control none --import-source on -k regex:"radix_downsweep" -c 2 \
-    -o gpurun_out/r02cap/full_sort python profiles/census_once.py powerlaw_50m_600m 3600 1 > gpurun_out/r02cap/ncu_sort.log 2>&1; echo full_sort=$?
+G=gpurun_out/r02cap
+mkdir -p $G
+python bench.py > $G/bench.json 2> $G/bench.err; echo bench=$?
+python profiles/census_once.py powerlaw_50m_600m 3600 2 > $G/census_once.jsonl 2>&1; echo once=$?
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $G/launches.csv \
+    python profiles/census_once.py powerlaw_50m_600m 3600 2 > $G/ncu_launch.log 2>&1; echo launches=$?
+python profiles/summarize_launches.py $G/launches.csv > $G/launches.txt
+ncu --set full --clock-control none --import-source on -k regex:"radix_downsweep" -c 8 \
+    -o $G/full_sort python profiles/census_once.py powerlaw_50m_600m 3600 1 > $G/ncu_sort.log 2>&1; echo full_sort=$?
+# downsweep launches of one census: 4 node passes (2m = 1.2G elements x 32 B,
+# keys + payloads read and written), then 4 pair passes (m = 600M x 32 B)
+for i in 0 1 2 3; do
+  python profiles/ncu_summary.py $G/full_sort.ncu-rep --kernel radix_downsweep --index $i --algo 38400000000 \
+    > $G/ncu_radix_downsweep_node_pass$((i+1)).txt
+  python profiles/ncu_summary.py $G/full_sort.ncu-rep --kernel radix_downsweep --index $((i+4)) --algo 19200000000 \
+    > $G/ncu_radix_downsweep_pair_pass$((i+1)).txt
+done
+python profiles/ncu_summary.py $G/full_sort.ncu-rep --kernel radix_downsweep \
+    --traffic-json $G/traffic_radix_downsweep_powerlaw_50m_600m_3600.json --config powerlaw_50m_600m
+python profiles/ncu_lines.py $G/full_sort.ncu-rep radix_downsweep > $G/lines_radix_downsweep.txt
+rm -f $G/full_sort.ncu-rep
+ncu --set full --clock-control none --import-source on -k regex:"tri_long|tri_wedge" -c 3 \
+    -o $G/full_tri python profiles/census_once.py powerlaw_50m_600m 3600 1 > $G/ncu_tri.log 2>&1; echo full_tri=$?
+python profiles/ncu_summary.py $G/full_tri.ncu-rep --kernel tri_wedge > $G/ncu_tri_wedge.txt
+python profiles/ncu_summary.py $G/full_tri.ncu-rep --kernel tri_long --index 0 > $G/ncu_tri_long_plain.txt
+python profiles/ncu_summary.py $G/full_tri.ncu-rep --kernel tri_long --index 1 > $G/ncu_tri_long_cached.txt
+python profiles/ncu_lines.py $G/full_tri.ncu-rep tri_wedge > $G/lines_tri_wedge.txt
+python profiles/ncu_lines.py $G/full_tri.ncu-rep tri_long > $G/lines_tri_long.txt
+rm -f $G/full_tri.ncu-rep
 ncu --set full --clock-control none --import-source on \
-    -k regex:"tri_long|tri_wedge|pair_keys|gather_s_pay|gather_p_pay|star_work|star_locate|pack_edges|radix_upsweep|forward_scatter|tri_filter" -c 12 \
-    -o gpurun_out/r02cap/full_work python profiles/census_once.py powerlaw_50m_600m 3600 1 > gpurun_out/r02cap/ncu_work.log 2>&1; echo full_work=$?
+    -k regex:"pair_keys|gather_s_pay|gather_p_pay|star_work|star_locate|pack_edges|forward_scatter|tri_filter|star_filter" -c 9 \
+    -o $G/full_work python profiles/census_once.py powerlaw_50m_600m 3600 1 > $G/ncu_work.log 2>&1; echo full_work=$?
+python profiles/ncu_summary.py $G/full_work.ncu-rep --kernel gather_s_pay --algo 38400000000 > $G/ncu_gather_s.txt
+python profiles/ncu_summary.py $G/full_work.ncu-rep --kernel gather_p_pay --algo 21600000000 > $G/ncu_gather_p.txt
+python profiles/ncu_summary.py $G/full_work.ncu-rep --kernel pair_keys --algo 28800000000 > $G/ncu_pair_keys.txt
+for k in pack_edges forward_scatter tri_filter star_filter star_locate star_work; do
+  python profiles/ncu_summary.py $G/full_work.ncu-rep --kernel $k > $G/ncu_$k.txt
+done
+python profiles/ncu_lines.py $G/full_work.ncu-rep star_work > $G/lines_star_work.txt
+rm -f $G/full_work.ncu-rep
