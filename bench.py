@@ -418,7 +418,7 @@ def main():
     names = ["star_filter", "star_locate", "star_work", "tri_filter", "tri_wedge", "tri_long", "radix_upsweep",
              "radix_downsweep", "radix_scan", "scan", "gather_s", "gather_p", "forward_scatter", "pack_edges",
              "pair_keys", "time_keys", "perm_from_keys", "validate", "offsets", "forward_off", "group_end",
-             "pair_table", "tri_gate"]
+             "pair_table", "tri_gate", "orient", "degree_class"]
     ktimes = {}
     for nm in names:
         tot_ms, cnt = tm.kernel_time(nm)

@@ -1057,7 +1057,13 @@ int tm_pair_window(const tm_graph* g, uint32_t v, uint32_t w, int64_t lo, int64_
         if (len) *len = 0;
         if (v == w || lo > hi) return TM_OK;
         cudaStream_t st = G->g.stream;
-        const uint32_t a = std::min(v, w), b = std::max(v, w);
+        // the pair's P block is its lower endpoint's in (degree class, id) order
+        uint8_t cv = 0, cw = 0;
+        TM_CUDA(cudaMemcpyAsync(&cv, G->g.cls + v, 1, cudaMemcpyDeviceToHost, st));
+        TM_CUDA(cudaMemcpyAsync(&cw, G->g.cls + w, 1, cudaMemcpyDeviceToHost, st));
+        TM_CUDA(cudaStreamSynchronize(st));
+        const bool vlow = cv < cw || (cv == cw && v < w);
+        const uint32_t a = vlow ? v : w, b = vlow ? w : v;
         const uint32_t k0 = read_u32(G->g.pofs, a, st), k1 = read_u32(G->g.pofs, a + 1, st);
         std::vector<uint32_t> mx(k1 - k0);
         if (k1 > k0) {

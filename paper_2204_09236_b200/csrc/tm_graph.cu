@@ -181,13 +181,13 @@ __global__ void gather_s_kernel(const typename EdgeCodec<kNarrow>::Rec* __restri
                                 int64_t* __restrict__ S_tw, uint32_t* __restrict__ S_tn,
                                 uint32_t* __restrict__ S_nbr,
                                 uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
-                                uint32_t* __restrict__ omask, uint32_t* __restrict__ xmask,
+                                uint32_t* __restrict__ omask,
                                 int64_t* __restrict__ t32w, uint32_t* __restrict__ t32n,
                                 int64_t* __restrict__ t1kw, uint32_t* __restrict__ t1kn) {
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t q = base + threadIdx.x;
-        uint32_t out = 0, mx = 0;
+        uint32_t out = 0;
         if (q < R) {
             const uint64_t key = __ldcs(skeys + q);  // streamed: leave L2 to the edge records
             const uint32_t r = (uint32_t)key;
@@ -201,7 +201,6 @@ __global__ void gather_s_kernel(const typename EdgeCodec<kNarrow>::Rec* __restri
             if (q == R - 1)
                 for (int64_t y = (int64_t)u + 1; y <= (int64_t)n; ++y) off[y] = (uint32_t)R;
             out = side ^ 1u;
-            mx = x < u ? 1u : 0u;  // u is the pair's larger endpoint
             if (kNarrow) __stcs(S_tn + q, Codec::rel(e));
             else __stcs(S_tw + q, Codec::time(e, tmin));
             if ((q & 31) == 0) {  // the fences (tm_internal.cuh fenced_lower_bound)
@@ -216,11 +215,8 @@ __global__ void gather_s_kernel(const typename EdgeCodec<kNarrow>::Rec* __restri
             __stcs(S_node + q, u);
             __stcs(S_nbr + q, x | (side << 31));
         }
-        const unsigned ob = __ballot_sync(0xffffffffu, out), xb = __ballot_sync(0xffffffffu, mx);
-        if ((threadIdx.x & 31) == 0 && q < R) {
-            omask[q >> 5] = ob;
-            xmask[q >> 5] = xb;
-        }
+        const unsigned ob = __ballot_sync(0xffffffffu, out);
+        if ((threadIdx.x & 31) == 0 && q < R) omask[q >> 5] = ob;
     }
 }
 
@@ -234,12 +230,12 @@ __global__ void gather_s_pay_kernel(const uint64_t* __restrict__ skeys, const ui
                                     uint64_t R, uint64_t n, uint32_t* __restrict__ off,
                                     uint32_t* __restrict__ S_tn, uint32_t* __restrict__ S_nbr,
                                     uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
-                                    uint32_t* __restrict__ omask, uint32_t* __restrict__ xmask,
+                                    uint32_t* __restrict__ omask,
                                     uint32_t* __restrict__ t32n, uint32_t* __restrict__ t1kn) {
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t q = base + threadIdx.x;
-        uint32_t out = 0, mx = 0;
+        uint32_t out = 0;
         if (q < R) {
             const uint64_t key = __ldcs(skeys + q);
             const uint64_t val = __ldcs(svals + q);
@@ -252,7 +248,6 @@ __global__ void gather_s_pay_kernel(const uint64_t* __restrict__ skeys, const ui
             if (q == R - 1)
                 for (int64_t y = (int64_t)u + 1; y <= (int64_t)n; ++y) off[y] = (uint32_t)R;
             out = side ^ 1u;
-            mx = x < u ? 1u : 0u;
             __stcs(S_tn + q, trel);
             __stcs(S_ord + q, p);
             __stcs(S_node + q, u);
@@ -262,16 +257,13 @@ __global__ void gather_s_pay_kernel(const uint64_t* __restrict__ skeys, const ui
                 if ((q & 1023) == 0) t1kn[q >> 10] = trel;
             }
         }
-        const unsigned ob = __ballot_sync(0xffffffffu, out), xb = __ballot_sync(0xffffffffu, mx);
-        if ((threadIdx.x & 31) == 0 && q < R) {
-            omask[q >> 5] = ob;
-            xmask[q >> 5] = xb;
-        }
+        const unsigned ob = __ballot_sync(0xffffffffu, out);
+        if ((threadIdx.x & 31) == 0 && q < R) omask[q >> 5] = ob;
     }
 }
 
-// pair keys from the max-side records of S (in (max, t, ordinal) order):
-// min << 32 | p, compacted by the xmask prefix
+// pair keys from the upper-side records of S (in (upper, t, ordinal) order):
+// lower << 32 | p, compacted by the xmask prefix
 // Degree class for the triangle pass's orientation: the degree itself below
 // 8, else 3 mantissa bits under the leading bit (~12 % steps) -- monotone in
 // the degree, so (class, id) is a strict total order that still puts hubs
@@ -288,35 +280,49 @@ __global__ void degree_class_kernel(const uint32_t* __restrict__ off, uint64_t n
         cls[u] = degree_class(off[u + 1] - off[u]);
 }
 
+// Orientation of every incident record by (degree class, id): forward
+// (fmask: the neighbour ranks above the center -- the degree orientation of
+// the triangle pass) or backward (xmask: the center is the pair's upper
+// endpoint).  P is keyed by each pair's LOWER endpoint in this order, so a
+// pair lookup searches the lower endpoint's block, which holds only its
+// records to nodes ranked above it: a low-degree node's block is short, and a
+// hub's block holds only its records to the few hubs above it.
+__global__ void orient_kernel(const uint32_t* __restrict__ S_node, const uint32_t* __restrict__ S_nbr,
+                              const uint8_t* __restrict__ cls, uint64_t R, uint32_t* __restrict__ xmask,
+                              uint32_t* __restrict__ fmask) {
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R; base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = base + threadIdx.x;
+        uint32_t fwd = 0, bwd = 0;
+        if (q < R) {
+            const uint32_t u = __ldcs(S_node + q), x = __ldcs(S_nbr + q) & kNodeMask;
+            const uint32_t du = cls[u], dx = cls[x];
+            fwd = (dx > du || (dx == du && x > u)) ? 1u : 0u;
+            bwd = fwd ^ 1u;
+        }
+        const unsigned fb = __ballot_sync(0xffffffffu, fwd), bb = __ballot_sync(0xffffffffu, bwd);
+        if ((threadIdx.x & 31) == 0 && q < R) {
+            fmask[q >> 5] = fb;
+            xmask[q >> 5] = bb;
+        }
+    }
+}
+
 // (narrow records: also the payload (t - tmin) << 32 | max | dir_rel_min << 31
 // for gather_p_pay, read from S_t / S_nbr)
 __global__ void pair_keys_kernel(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ S_nbr,
                                  const uint32_t* __restrict__ S_tn,
                                  const uint32_t* __restrict__ xmask, const uint32_t* __restrict__ xpref,
-                                 const uint8_t* __restrict__ cls, uint64_t R, uint64_t* __restrict__ pkeys,
-                                 uint64_t* __restrict__ pvals, uint32_t* __restrict__ fmask) {
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
-         base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t q = base + threadIdx.x;
-        uint32_t fwd = 0;
-        if (q < R) {
-            const uint64_t key = __ldcs(skeys + q);
-            const uint32_t nbr = __ldcs(S_nbr + q);
-            const uint32_t u = (uint32_t)(key >> 32), x = nbr & kNodeMask;
-            // degree orientation of the triangle pass: forward iff (degree class,
-            // id) of the neighbour exceeds the center's
-            const uint32_t du = cls[u], dx = cls[x];
-            fwd = (dx > du || (dx == du && x > u)) ? 1u : 0u;
-            const uint32_t word = xmask[q >> 5], bit = 1u << (q & 31);
-            if (word & bit) {
-                const uint32_t j = xpref[q >> 5] + __popc(word & (bit - 1u));
-                pkeys[j] = ((uint64_t)x << 32) | ((uint32_t)key >> 1);
-                // u is the max endpoint; the min x is the source iff u's record is inward
-                if (pvals) pvals[j] = ((uint64_t)__ldcs(S_tn + q) << 32) | u | ((~nbr) & kDirBit);
-            }
-        }
-        const unsigned fb = __ballot_sync(0xffffffffu, fwd);
-        if ((threadIdx.x & 31) == 0 && q < R) fmask[q >> 5] = fb;
+                                 uint64_t R, uint64_t* __restrict__ pkeys, uint64_t* __restrict__ pvals) {
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t word = xmask[q >> 5], bit = 1u << (q & 31);
+        if (!(word & bit)) continue;
+        const uint64_t key = __ldcs(skeys + q);
+        const uint32_t nbr = __ldcs(S_nbr + q);
+        const uint32_t u = (uint32_t)(key >> 32), x = nbr & kNodeMask;
+        const uint32_t j = xpref[q >> 5] + __popc(word & (bit - 1u));
+        pkeys[j] = ((uint64_t)x << 32) | ((uint32_t)key >> 1);
+        // u is the upper endpoint; the lower one x is the source iff u's record is inward
+        if (pvals) pvals[j] = ((uint64_t)__ldcs(S_tn + q) << 32) | u | ((~nbr) & kDirBit);
     }
 }
 
@@ -806,6 +812,8 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         release_plan(g, pl);
         TM_CUDA(cudaMemsetAsync(g.off, 0, (n + 1) * sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.pofs, 0, (n + 1) * sizeof(uint32_t), s));
+        g.cls = dalloc<uint8_t>(n + 1, s);
+        TM_CUDA(cudaMemsetAsync(g.cls, 0, n + 1, s));
         TM_CUDA(cudaMemsetAsync(g.S_omask, 0, nw * sizeof(uint32_t), s));
         TM_CUDA(cudaMemsetAsync(g.S_opref, 0, (nw + 1) * sizeof(uint32_t), s));
         g.max_degree = 0;
@@ -873,14 +881,19 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         uint32_t* xmask = dalloc<uint32_t>(nw, s);
         uint32_t* xpref = dalloc<uint32_t>(nw + 1, s);
         TM_CUDA(cudaMemsetAsync(xmask + (nw - 1), 0, sizeof(uint32_t), s));
+        g.cls = dalloc<uint8_t>(n + 1, s);  // kept: the pair lookups pick a pair's lower endpoint by it
         if (narrow)
             TM_LAUNCH("gather_s", s, gather_s_pay_kernel, grid_for(R), 256, 0, nk0, nv0, R, n, g.off, g.S_t.n,
-                      g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask, g.S_t32.n, g.S_t1k.n);
+                      g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_t32.n, g.S_t1k.n);
         else
             TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, EW, tmin, nk0, R, n, g.off,
-                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, xmask, g.S_t32.w, g.S_t32.n,
+                      g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_t32.w, g.S_t32.n,
                       g.S_t1k.w, g.S_t1k.n);
-        // outward prefix (stars) and max-side prefix (pair keys) in one scan
+        // orientation by (degree class, id): forward mask (triangle pass) and
+        // upper-side mask (pair keys)
+        TM_LAUNCH("degree_class", s, degree_class_kernel, grid_for(n), 256, 0, g.off, n, g.cls);
+        TM_LAUNCH("orient", s, orient_kernel, grid_for(R), 256, 0, g.S_node, g.S_nbr, g.cls, R, xmask, g.S_fmask);
+        // outward prefix (stars) and upper-side prefix (pair keys) in one scan
         exclusive_scan_to<uint64_t>(PopcLoad2{g.S_omask, xmask}, nw, SplitStore2{g.S_opref, xpref}, s);
 
         // 3. P: the max-side records (one per edge, (max, t, ordinal) order)
@@ -893,11 +906,8 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         uint64_t* pv0 = narrow ? dalloc<uint64_t>(m + kSortPad, s) : nullptr;
         uint64_t* pv0_alloc = pv0;
         uint64_t* pv1 = nv1;  // the node sort's second value buffer
-        uint8_t* cls = dalloc<uint8_t>(n + 1, s);
-        TM_LAUNCH("degree_class", s, degree_class_kernel, grid_for(n), 256, 0, g.off, n, cls);
-        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, g.S_t.n, xmask, xpref, cls,
-                  R, pk0, pv0, g.S_fmask);
-        dfree(cls, s);
+        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, g.S_t.n, xmask, xpref, R, pk0,
+                  pv0);
 
         // the forward sequences (degree orientation) only need S and the
         // forward mask: build them on a side stream while the pair index sorts
@@ -1036,6 +1046,7 @@ void free_graph(DeviceGraph& g) {
     dfree(g.S_t.w, s); dfree(g.S_t.n, s); dfree(g.S_nbr, s); dfree(g.S_ord, s); dfree(g.S_node, s);
     dfree(g.S_omask, s); dfree(g.S_opref, s); dfree(g.S_fmask, s); dfree(g.S_pidx, s);
     dfree(g.off, s);
+    dfree(g.cls, s);
     dfree(g.S_t32.w, s); dfree(g.S_t32.n, s); dfree(g.S_t1k.w, s); dfree(g.S_t1k.n, s);
     dfree(g.P_t.w, s); dfree(g.P_t.n, s); dfree(g.P_ord, s); dfree(g.P_max, s); dfree(g.P_w, s);
     dfree(g.P_min, s); dfree(g.pofs, s); dfree(g.P_dmask, s); dfree(g.P_dpref, s);

@@ -14,12 +14,18 @@
 //     off[n+1]  u32    CSR offsets
 //   P (PairEdgeIndex, indexes.hpp:63-92: one record per edge, grouped by the
 //      unordered pair {min, max}, time-ordered inside a group; the group of
-//      {u, v} is also u's and v's same-neighbour run, shared by both ends)
+//      {u, v} is also u's and v's same-neighbour run, shared by both ends).
+//      "min" / "max" are the pair's lower / upper endpoint in (degree class,
+//      id) order (cls below), so a pair lives in the block of its lower-degree
+//      endpoint, which holds only that node's records to nodes ranked above it
 //     P_t[m]    int64
 //     P_ord[m]  u32
-//     P_min[m], P_max[m]  u32  endpoints (the block of the smaller one is pofs)
+//     P_min[m], P_max[m]  u32  lower / upper endpoints (the block of the lower one is pofs)
 //     P_w[m]    u32    dir_rel_min << 31 | first << 30 | last << 29
-//     pofs[n+1] u32    first P position whose min endpoint is u
+//     pofs[n+1] u32    first P position whose lower endpoint is u
+//     cls[n]    u8     degree class (the degree below 8, else 3 mantissa bits
+//               under the leading bit): the order of both P and the degree
+//               orientation of the triangle pass
 //     P_dmask[m/32+1], P_dpref[m/32+2]  bitmask of dir_rel_min = 1 records and
 //               the prefix of its word popcounts: the direction split of any P
 //               range in four loads (long closing groups)
@@ -198,6 +204,7 @@ struct DeviceGraph {
     uint32_t* off = nullptr;
     TimeBuf S_t32;  // fences: S_t at every 32nd / 1024th record (fenced_lower_bound)
     TimeBuf S_t1k;
+    uint8_t* cls = nullptr;  // degree class per node: the (class, id) order of both orientations' ranks
 
     TimeBuf P_t;
     uint32_t* P_ord = nullptr;
@@ -252,6 +259,7 @@ struct PView {
     const uint32_t* max1k;
     TimeArr t32;
     TimeArr t1k;
+    const uint8_t* cls;  // degree class per node: a pair's lower endpoint (its P block) is the lower (class, id)
     // optional pair table: (min << 32 | max) -> group start << 32 | length,
     // replacing the binary search of max in min's block (hub blocks are long)
     const unsigned long long* pt_keys;
@@ -267,6 +275,12 @@ __device__ __forceinline__ uint64_t pair_slot(uint32_t a, uint32_t b) {
     h *= 0xc4ceb9fe1a85ec53ull;
     h ^= h >> 33;
     return h;
+}
+// (class, id) order of two distinct nodes: true when a ranks below b (a pair's
+// P block is its lower endpoint's; "min" / "max" in P below mean lower / upper)
+__device__ __forceinline__ bool ranks_below(const uint8_t* __restrict__ cls, uint32_t a, uint32_t b) {
+    const uint32_t ca = cls[a], cb = cls[b];
+    return ca < cb || (ca == cb && a < b);
 }
 // P records with dir_rel_min = 1 before position x
 // end (one past the last record) of the P group starting at record x
@@ -385,7 +399,7 @@ __device__ __forceinline__ uint32_t outward_before(const SView& S, uint32_t q) {
 inline PView pview(const DeviceGraph& g) {
     return {g.P_t.view(g.tbase), g.P_ord, g.P_max, g.P_w, g.P_min, g.pofs, g.P_dmask, g.P_dpref,
             g.P_gmask, g.P_gpref, nullptr, g.P_max32, g.P_max1k, g.P_t32.view(g.tbase), g.P_t1k.view(g.tbase),
-            nullptr, nullptr, 0};
+            g.cls, nullptr, nullptr, 0};
 }
 
 // ---- builders / passes (tm_graph.cu, tm_star.cu, tm_tri.cu) ------------

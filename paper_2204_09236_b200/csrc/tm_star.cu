@@ -81,9 +81,12 @@ __device__ __forceinline__ void add_d1(const Sink& sink, int base, uint32_t d1, 
     for (int j = 0; j < 4; ++j) sink.add(base + (int)d1 * 4 + j, x[j]);
 }
 
-// Side of center u in the unordered pair {u, other}: 0 when u is the smaller
-// id (P_min / dir_rel_min describe it), 1 when u is the larger one.
-__device__ __forceinline__ uint32_t side_of(uint32_t u, uint32_t other) { return u > other ? 1u : 0u; }
+// Side of center u in the unordered pair {u, other}: 0 when u is the pair's
+// lower endpoint in (degree class, id) order (P_min / dir_rel_min describe
+// it), 1 when u is the upper one.
+__device__ __forceinline__ uint32_t side_of(const PView& P, uint32_t u, uint32_t other) {
+    return ranks_below(P.cls, u, other) ? 0u : 1u;
+}
 
 // (t, ordinal) strict order between S record p and (t, ord)
 __device__ __forceinline__ bool s_before(const SView& S, uint32_t p, int64_t t, uint32_t ord) {
@@ -551,7 +554,7 @@ __global__ void __launch_bounds__(256) star_items_kernel(
             const uint32_t u = nodes[it];
             const uint32_t start = S.off[u], end = S.off[u + 1];
             const uint32_t q = start + (uint32_t)begin[it] + (uint32_t)(idx - first_off[it]);
-            first_role(S, P, q, S.pidx[q], side_of(u, S.nbr[q] & kNodeMask), start, end, delta,
+            first_role(S, P, q, S.pidx[q], side_of(P, u, S.nbr[q] & kNodeMask), start, end, delta,
                        GlobalSink{(unsigned long long*)out + (uint64_t)it * 64, 32});
         } else {
             const uint64_t j = idx - total_first;
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(256) star_items_kernel(
             const uint32_t rb = (uint32_t)begin[it];
             const uint32_t re = (uint32_t)(endr[it] < (uint64_t)s ? endr[it] : (uint64_t)s);
             const uint32_t q = start + rb + 1 + (uint32_t)(j - third_off[it]);
-            third_role(S, P, q, S.pidx[q], side_of(u, S.nbr[q] & kNodeMask), start, delta, rb, re,
+            third_role(S, P, q, S.pidx[q], side_of(P, u, S.nbr[q] & kNodeMask), start, delta, rb, re,
                        GlobalSink{(unsigned long long*)out + (uint64_t)it * 64, 32});
         }
     }

@@ -88,8 +88,9 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
                                                uint32_t oj, int64_t t_last, uint32_t c[6]) {
 #pragma unroll
     for (int j = 0; j < 6; ++j) c[j] = 0;
-    const uint32_t a = min(v, w), b = max(v, w);
-    const uint32_t flip = v == a ? 0u : 1u;  // dir_rel_min -> dir relative to v
+    const bool vlow = ranks_below(P.cls, v, w);
+    const uint32_t a = vlow ? v : w, b = vlow ? w : v;  // the pair's lower / upper endpoint (P block of a)
+    const uint32_t flip = vlow ? 0u : 1u;  // dir_rel_lower -> dir relative to v
     uint32_t blk_end = P.pofs[a + 1], kb, ke = 0;
     if (P.pt_keys && blk_end - P.pofs[a] > kTableMinBlock) {  // optional pair table (TM_PAIR_TABLE)
         const unsigned long long key = ((unsigned long long)a << 32) | b;
@@ -352,7 +353,8 @@ __device__ __forceinline__ uint32_t p_gallop_tlower(const PView& P, uint32_t fro
 
 // the v-w group [kb, ke) (empty when no v-w record: kb == ke)
 __device__ __forceinline__ void locate_group(const PView& P, uint32_t v, uint32_t w, uint32_t& kb, uint32_t& ke) {
-    const uint32_t a = min(v, w), b = max(v, w);
+    const bool vlow = ranks_below(P.cls, v, w);
+    const uint32_t a = vlow ? v : w, b = vlow ? w : v;
     const uint32_t blk_end = P.pofs[a + 1];
     kb = p_max_lower(P, P.pofs[a], blk_end, b);
     if (kb >= blk_end || P.max[kb] != b) {
@@ -458,8 +460,7 @@ __global__ void __launch_bounds__(256, kCache ? 4 : 5) tri_long_kernel(PView P, 
                 const uint32_t k3 = p_gallop_rec(P, e.k3 > e.k2 ? e.k3 : e.k2, e.k4, tj, oj);
                 e.k1 = k1;
                 e.k3 = k3;
-                const uint32_t a = min(v, w);
-                const uint32_t flip = v == a ? 0u : 1u;
+                const uint32_t flip = ranks_below(P.cls, v, w) ? 0u : 1u;
                 uint32_t k2e = e.k2;
                 if (t_last != INT64_MAX) {
                     uint32_t l = k1, r = e.k2;

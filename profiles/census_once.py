@@ -37,7 +37,7 @@ if os.environ.get("KTIMES"):  # per-kernel CUDA-event times of one more census
     tm.kernel_timing(enable=False)
     names = ["star_filter", "star_locate", "star_work", "tri_filter", "tri_wedge", "tri_long", "radix_upsweep", "radix_downsweep",
              "radix_scan", "scan", "gather_s", "gather_p", "forward_scatter", "pack_edges", "pair_keys", "time_keys",
-             "forward_off", "group_end", "pair_table", "tri_gate"]
+             "forward_off", "group_end", "pair_table", "tri_gate", "orient", "degree_class"]
     kt = {k: round(tm.kernel_time(k)[0], 3) for k in names if tm.kernel_time(k)[1]}
     print(json.dumps({"config": name, "delta": delta, "kernel_ms": kt}), flush=True)
 ctx = tm.GraphContext.build_device(n, s.data_ptr(), d.data_ptr(), t.data_ptr(), s.numel())

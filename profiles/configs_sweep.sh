@@ -1,10 +1,10 @@
 #!/bin/bash
-# bench.py over the five BASELINE configs (config 4 at each delta of its sweep)
-# -> gpurun_out/configs/<name>_<delta>.json; summarise with
+# bench.py over the five BASELINE configs (config 1 and config 4 at each delta
+# of their sweep) -> gpurun_out/configs/<name>_<delta>.json; summarise with
 #    python profiles/configs_table.py gpurun_out/configs
 mkdir -p gpurun_out/configs
 run() {  # name delta
-  timeout 900 python bench.py --config $1 --delta $2 --steps 3 --warmup 3 --no-reader \
+  timeout 900 python bench.py --config $1 --delta $2 --steps 3 --warmup 3 \
     > gpurun_out/configs/$1_$2.json 2> gpurun_out/configs/$1_$2.err
   echo "$1 delta $2 rc=$?"
 }
