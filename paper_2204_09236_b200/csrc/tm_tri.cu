@@ -369,7 +369,7 @@ __device__ __forceinline__ void locate_group(const PView& P, uint32_t v, uint32_
 // count per wedge, full occupancy), kCache = true the longer ones (the group
 // cache's shared memory costs a resident block per SM).
 template <bool kCache>
-__global__ void __launch_bounds__(256, kCache ? 4 : 5) tri_long_kernel(PView P, TimeArr FT,
+__global__ void __launch_bounds__(256, kCache ? 4 : 6) tri_long_kernel(PView P, TimeArr FT,
                                                        const uint32_t* __restrict__ FN,
                                                        const uint32_t* __restrict__ FO,
                                                        const uint32_t* __restrict__ Fnode,

@@ -21,9 +21,11 @@ container, where /root/reference exists).
                         mid-stream) at delta 600 / 3600 / 86400 (optional, slow)
   triadic_reference.json reference census of config 3 (triadic_25m_100m, synth.
                         triadic_hashed) at FULL size, delta 3600 and 86400 (optional, slow)
+  config4_full_reference.json reference census of config 4 (600M edges) at FULL size,
+                        delta 600 (optional; ~100 GB of host memory: run on the GPU box's host)
 
 Usage: python tests/golden/make_golden.py [--powerlaw] [--hubstress] [--powerlaw-deltas]
-          [--config4-slices] [--triadic] [--only-extra]
+          [--config4-slices] [--triadic] [--config4-full] [--only-extra]
 """
 from __future__ import annotations
 
@@ -141,6 +143,43 @@ def config4_slices_golden(R, deltas=(600, 3600, 86400)):
         R.free(g)
 
 
+def config4_full_golden(R, deltas=(600,)):
+    """Reference run_parallel on the WHOLE of config 4 (600M edges; ~100 GB of
+    host memory for the reference's graph and indexes, so it runs on the GPU
+    box's host: `python tests/golden/make_golden.py --only-extra --config4-full`,
+    output written under gpurun_out/ and committed from there)."""
+    import time
+    from paper_2204_09236_b200 import synth
+    name = "config4_full_reference.json"
+    out_dir = os.environ.get("GOLDEN_OUT", HERE)
+    path = os.path.join(out_dir, name)
+    t0 = time.time()
+    n, s, d, tt = synth.power_law_hashed(CONFIG4["n"], CONFIG4["m"], CONFIG4["mean_gap"], CONFIG4["seed"])
+    h = edge_hash(s, d, tt)
+    gen_s = round(time.time() - t0, 1)
+    out = json.load(open(path)) if os.path.exists(path) else {
+        "config": "powerlaw_50m_600m", "generator": "synth.power_law_hashed", **CONFIG4, "edges": int(len(s)),
+        "hash": h, "cases": []}
+    assert out["hash"] == h
+    t0 = time.time()
+    g = R.build_graph(n, s, d, tt)
+    del s, d, tt
+    build_s = round(time.time() - t0, 1)
+    done = {c["delta"] for c in out["cases"]}
+    for delta in deltas:
+        if delta in done:
+            continue
+        t0 = time.time()
+        census = R.run_parallel(g, delta, os.cpu_count() or 1)
+        out["cases"].append({"delta": delta, "census": [int(x) for x in census], "cpu_s": round(time.time() - t0, 1),
+                             "threads": os.cpu_count(), "generate_s": gen_s, "build_s": build_s})
+        tmp = path + ".tmp"
+        json.dump(out, open(tmp, "w"))
+        os.replace(tmp, path)
+        print("config4 full delta", delta, "done in", out["cases"][-1]["cpu_s"], "s", flush=True)
+    R.free(g)
+
+
 def triadic_golden(R, deltas=(3600, 86400)):
     """Reference run_parallel on the whole of config 3 (100M edges)."""
     import time
@@ -180,6 +219,8 @@ def main(with_powerlaw: bool, with_hubstress: bool = False, only_extra: bool = F
             config4_slices_golden(R)
         if "--triadic" in sys.argv:
             triadic_golden(R)
+        if "--config4-full" in sys.argv:
+            config4_full_golden(R)
         return
     sigs = R.signatures()
 
