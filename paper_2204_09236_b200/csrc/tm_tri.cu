@@ -183,6 +183,12 @@ constexpr int kWedgeScan = 8;
 constexpr int kGroupCache = 128;
 constexpr uint32_t kGroupCacheMinWindow = 64;  // shorter windows repeat few groups: plain path
 
+#ifndef TM_WEDGE_MINB
+#define TM_WEDGE_MINB 5
+#endif
+#ifndef TM_LONG_MINB
+#define TM_LONG_MINB 6
+#endif
 constexpr int kFilterItems = 4;  // first edges per thread per block iteration (one reservation)
 __global__ void __launch_bounds__(256) tri_filter_kernel(TimeArr FT,
                                                          const uint32_t* __restrict__ FN,
@@ -275,7 +281,7 @@ __device__ __forceinline__ int wedge_counts(const PView& P, TimeArr FT, const ui
 }
 
 // one wedge per thread
-__global__ void __launch_bounds__(256, 5) tri_wedge_kernel(PView P, TimeArr FT,
+__global__ void __launch_bounds__(256, TM_WEDGE_MINB) tri_wedge_kernel(PView P, TimeArr FT,
                                                         const uint32_t* __restrict__ FN,
                                                         const uint32_t* __restrict__ FO,
                                                         int64_t delta, int64_t t_last,
@@ -369,7 +375,7 @@ __device__ __forceinline__ void locate_group(const PView& P, uint32_t v, uint32_
 // count per wedge, full occupancy), kCache = true the longer ones (the group
 // cache's shared memory costs a resident block per SM).
 template <bool kCache>
-__global__ void __launch_bounds__(256, kCache ? 4 : 6) tri_long_kernel(PView P, TimeArr FT,
+__global__ void __launch_bounds__(256, kCache ? 4 : TM_LONG_MINB) tri_long_kernel(PView P, TimeArr FT,
                                                        const uint32_t* __restrict__ FN,
                                                        const uint32_t* __restrict__ FO,
                                                        const uint32_t* __restrict__ Fnode,

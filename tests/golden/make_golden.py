@@ -154,7 +154,19 @@ def config4_full_golden(R, deltas=(600,)):
     out_dir = os.environ.get("GOLDEN_OUT", HERE)
     path = os.path.join(out_dir, name)
     t0 = time.time()
-    n, s, d, tt = synth.power_law_hashed(CONFIG4["n"], CONFIG4["m"], CONFIG4["mean_gap"], CONFIG4["seed"])
+    try:
+        import torch
+        gpu = torch.cuda.is_available()
+    except ImportError:
+        gpu = False
+    if gpu:  # the torch twin on the GPU makes the identical arrays in seconds
+        n, s, d, tt = synth.power_law_hashed(CONFIG4["n"], CONFIG4["m"], CONFIG4["mean_gap"], CONFIG4["seed"],
+                                             device="cuda")
+        s, d, tt = (x.cpu().numpy() for x in (s, d, tt))
+        s, d = s.view(np.uint32), d.view(np.uint32)
+        torch.cuda.empty_cache()
+    else:
+        n, s, d, tt = synth.power_law_hashed(CONFIG4["n"], CONFIG4["m"], CONFIG4["mean_gap"], CONFIG4["seed"])
     h = edge_hash(s, d, tt)
     gen_s = round(time.time() - t0, 1)
     out = json.load(open(path)) if os.path.exists(path) else {
@@ -220,7 +232,8 @@ def main(with_powerlaw: bool, with_hubstress: bool = False, only_extra: bool = F
         if "--triadic" in sys.argv:
             triadic_golden(R)
         if "--config4-full" in sys.argv:
-            config4_full_golden(R)
+            ds = os.environ.get("GOLDEN_DELTAS")
+            config4_full_golden(R, tuple(int(x) for x in ds.split(",")) if ds else (600,))
         return
     sigs = R.signatures()
 

@@ -7,11 +7,14 @@ produce the identical edge arrays on the host and on the GPU -- pinned here by
 the arrays' hash):
   * config 3 (triadic 25M / 100M) whole, delta 3600 and 86400;
   * config 4 (power-law 50M / 600M): 10M-edge contiguous time slices, one at
-    the start of the stream and one mid-stream, at delta 600, 3600 and 86400;
+    the start of the stream and one mid-stream, at delta 600, 3600 and 86400,
+    and the whole 600M edges at the deltas config4_full_reference.json holds;
 plus size-independent properties of the full 600M-edge result (pair complement
 symmetry, count_all census == removal census, delta monotonicity, center
 partitions summing to the whole) and bit-exact agreement with the C oracle on
 a time slice of each config's input."""
+import os
+
 import numpy as np
 import pytest
 
@@ -133,6 +136,16 @@ def test_config4_slices_vs_reference_and_full_size(cuda, tm, oracle):
             assert got.tolist() == case["census"], (lo, hi, case["delta"])
         del s_, d_, t_
     _slice_parity(tm, oracle, n, src, dst, t, 600, 100_000)
+    # the whole 600M edges against the reference's run_parallel on the same
+    # input (config4_full_reference.json, made on the GPU box's host)
+    full = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "config4_full_reference.json")
+    if os.path.exists(full):
+        fref = load_golden("config4_full_reference.json")
+        assert fref["edges"] == src.numel()
+        assert _hash(src, dst, t) == fref["hash"]
+        for case in fref["cases"]:
+            got = _census_device(tm, n, src, dst, t, case["delta"])
+            assert got.tolist() == case["census"], ("full", case["delta"])
     ctx = _device_ctx(tm, n, src, dst, t)
     prev = None
     for delta in (600, 3600, 86_400):
