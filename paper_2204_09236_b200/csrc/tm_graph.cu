@@ -724,7 +724,8 @@ void plan_from_verdict(DeviceGraph& g, BuildPlan& pl, const BuildVerdict& v) {
         throw tm_error(1, "self-loop or out-of-range endpoint in edge list");
     }
     // narrow 8-byte edge records when the time span fits 32 bits
-    pl.narrow = (uint64_t)v.tmax - (uint64_t)v.tmin < (1ull << 32);
+    // (offsets stay <= 0xFFFFFFFE: TimeKey's u32 threshold 0xFFFFFFFF means "every record")
+    pl.narrow = (uint64_t)v.tmax - (uint64_t)v.tmin < 0xFFFFFFFFull;
     pl.unsorted = v.unsorted != 0;
     pl.tmin = v.tmin;
     pl.tmax = v.tmax;

@@ -129,12 +129,58 @@ void dfree(T*& p, cudaStream_t s) {
 // A timestamp array of an index (S, P or F): int64, or -- when the graph's
 // time span fits 32 bits -- u32 offsets from `base`: half the bytes in every
 // window search, group walk and gather.  Reads return absolute times.
+//
+// Searches compare in the storage domain: a threshold ("v < K") is folded
+// once into the narrow array's u32 offsets (TimeKey), so a probe is one load
+// and one 32-bit compare instead of a widening add and a 64-bit compare.
+// Narrow arrays hold offsets <= 0xFFFFFFFE (plan_from_verdict), so the u32
+// threshold 0xFFFFFFFF means "every record".
+struct TimeKey {
+    int64_t K;     // wide arrays: v < K, or every v when all is set
+    uint32_t nk;   // narrow arrays: offset < nk
+    uint32_t all;
+};
+// a record's (t, ordinal) as a search key; t must be a time of the graph
+struct RecKey {
+    int64_t t;
+    uint32_t tr;  // t - base
+    uint32_t ord;
+};
 struct TimeArr {
     const int64_t* w;
     const uint32_t* n;
     int64_t base;
     __device__ __forceinline__ int64_t operator[](uint64_t i) const {
         return n ? base + (int64_t)n[i] : w[i];
+    }
+    // threshold "v < x"
+    __device__ __forceinline__ TimeKey key_below(int64_t x) const {
+        TimeKey k;
+        k.K = x;
+        k.all = 0u;
+        const uint64_t d = (uint64_t)x - (uint64_t)base;  // exact when x > base
+        k.nk = x <= base ? 0u : d >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)d;
+        return k;
+    }
+    // threshold "v <= x"
+    __device__ __forceinline__ TimeKey key_upto(int64_t x) const {
+        if (x == INT64_MAX) return TimeKey{x, 0xFFFFFFFFu, 1u};
+        return key_below(x + 1);
+    }
+    __device__ __forceinline__ bool below(uint64_t i, const TimeKey& k) const {
+        return n ? n[i] < k.nk : ((k.all != 0u) | (w[i] < k.K));
+    }
+    __device__ __forceinline__ RecKey rec_key(int64_t t, uint32_t ord) const {
+        return RecKey{t, (uint32_t)((uint64_t)t - (uint64_t)base), ord};
+    }
+    // -1 / 0 / +1: the time at i before / equal to / after the record key's
+    __device__ __forceinline__ int cmp(uint64_t i, const RecKey& k) const {
+        if (n) {
+            const uint32_t v = n[i];
+            return v < k.tr ? -1 : v == k.tr ? 0 : 1;
+        }
+        const int64_t v = w[i];
+        return v < k.t ? -1 : v == k.t ? 0 : 1;
     }
 };
 struct TimeBuf {
@@ -337,14 +383,16 @@ struct U32Probe {
     __device__ __forceinline__ bool below32(uint32_t x) const { return cmp(f32[x]); }
     __device__ __forceinline__ bool below1k(uint32_t y) const { return cmp(f1k[y]); }
 };
+// one time array + its fences (all on one base): v < key (kStrict) or v <= key
 template <bool kStrict>
 struct TProbe {
     TimeArr a, f32, f1k;
-    int64_t key;
-    __device__ __forceinline__ bool cmp(int64_t v) const { return kStrict ? v < key : v <= key; }
-    __device__ __forceinline__ bool below0(uint32_t k) const { return cmp(a[k]); }
-    __device__ __forceinline__ bool below32(uint32_t x) const { return cmp(f32[x]); }
-    __device__ __forceinline__ bool below1k(uint32_t y) const { return cmp(f1k[y]); }
+    TimeKey key;
+    __device__ __forceinline__ TProbe(const TimeArr& a_, const TimeArr& f32_, const TimeArr& f1k_, int64_t x)
+        : a(a_), f32(f32_), f1k(f1k_), key(kStrict ? a_.key_below(x) : a_.key_upto(x)) {}
+    __device__ __forceinline__ bool below0(uint32_t k) const { return a.below(k, key); }
+    __device__ __forceinline__ bool below32(uint32_t x) const { return f32.below(x, key); }
+    __device__ __forceinline__ bool below1k(uint32_t y) const { return f1k.below(y, key); }
 };
 // first P position in [lo, hi) with P_max >= b (a block of one min endpoint)
 __device__ __forceinline__ uint32_t p_max_lower(const PView& P, uint32_t lo, uint32_t hi, uint32_t b) {
@@ -356,36 +404,35 @@ __device__ __forceinline__ uint32_t p_max_upper(const PView& P, uint32_t lo, uin
 }
 // first P position in [lo, hi) (one group) with t >= x
 __device__ __forceinline__ uint32_t p_t_lower(const PView& P, uint32_t lo, uint32_t hi, int64_t x) {
-    return fenced_lower_bound(lo, hi, TProbe<true>{P.t, P.t32, P.t1k, x});
+    return fenced_lower_bound(lo, hi, TProbe<true>(P.t, P.t32, P.t1k, x));
 }
 // first P position in [lo, hi) (one group) with t > x
 __device__ __forceinline__ uint32_t p_t_upper(const PView& P, uint32_t lo, uint32_t hi, int64_t x) {
-    return fenced_lower_bound(lo, hi, TProbe<false>{P.t, P.t32, P.t1k, x});
+    return fenced_lower_bound(lo, hi, TProbe<false>(P.t, P.t32, P.t1k, x));
 }
 // S positions in one node's sequence [lo, hi): first with t >= x / t > x
 __device__ __forceinline__ uint32_t s_t_lower(const SView& S, uint32_t lo, uint32_t hi, int64_t x) {
-    return fenced_lower_bound(lo, hi, TProbe<true>{S.t, S.t32, S.t1k, x});
+    return fenced_lower_bound(lo, hi, TProbe<true>(S.t, S.t32, S.t1k, x));
 }
 __device__ __forceinline__ uint32_t s_t_upper(const SView& S, uint32_t lo, uint32_t hi, int64_t x) {
-    return fenced_lower_bound(lo, hi, TProbe<false>{S.t, S.t32, S.t1k, x});
+    return fenced_lower_bound(lo, hi, TProbe<false>(S.t, S.t32, S.t1k, x));
 }
 // the S position of record (t, ord) in one node's sequence [lo, hi): first
 // (t', ord') >= (t, ord); a fence key equal in t reads the ordinal at its
 // position (ties are rare but unbounded: a tie-heavy sequence stays O(log))
 struct SRecProbe {
     SView S;
-    int64_t t;
-    uint32_t ord;
-    __device__ __forceinline__ bool at(int64_t tp, uint32_t p) const {
-        return tp < t || (tp == t && (S.ord[p] & kNodeMask) < ord);
+    RecKey key;
+    __device__ __forceinline__ bool at(int c, uint32_t p) const {
+        return c < 0 || (c == 0 && (S.ord[p] & kNodeMask) < key.ord);
     }
-    __device__ __forceinline__ bool below0(uint32_t k) const { return at(S.t[k], k); }
-    __device__ __forceinline__ bool below32(uint32_t x) const { return at(S.t32[x], x << 5); }
-    __device__ __forceinline__ bool below1k(uint32_t y) const { return at(S.t1k[y], y << 10); }
+    __device__ __forceinline__ bool below0(uint32_t k) const { return at(S.t.cmp(k, key), k); }
+    __device__ __forceinline__ bool below32(uint32_t x) const { return at(S.t32.cmp(x, key), x << 5); }
+    __device__ __forceinline__ bool below1k(uint32_t y) const { return at(S.t1k.cmp(y, key), y << 10); }
 };
 __device__ __forceinline__ uint32_t s_locate_fenced(const SView& S, uint32_t lo, uint32_t hi, int64_t t,
                                                     uint32_t ord) {
-    return fenced_lower_bound(lo, hi, SRecProbe{S, t, ord});
+    return fenced_lower_bound(lo, hi, SRecProbe{S, S.t.rec_key(t, ord)});
 }
 inline SView sview(const DeviceGraph& g) {
     return {g.S_t.view(g.tbase), g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_opref, g.S_pidx, g.off,

@@ -305,24 +305,26 @@ __global__ void __launch_bounds__(256) star_filter_kernel(PView P, int64_t delta
 // short gallop (the window is usually a few lines), then the fenced search
 __device__ __forceinline__ uint32_t s_window_end(const SView& S, uint32_t q, uint32_t end, int64_t lim) {
     uint32_t lo = q + 1;
+    const TProbe<false> pr(S.t, S.t32, S.t1k, lim);
     for (uint32_t span = 1; span <= 32; span <<= 1) {
         const uint64_t probe = (uint64_t)lo + span - 1;
-        if (probe >= end) return fenced_lower_bound(lo, end, TProbe<false>{S.t, S.t32, S.t1k, lim});
-        if (S.t[probe] > lim) return fenced_lower_bound(lo, (uint32_t)probe, TProbe<false>{S.t, S.t32, S.t1k, lim});
+        if (probe >= end) return fenced_lower_bound(lo, end, pr);
+        if (!pr.below0((uint32_t)probe)) return fenced_lower_bound(lo, (uint32_t)probe, pr);
         lo = (uint32_t)probe + 1;
     }
-    return fenced_lower_bound(lo, end, TProbe<false>{S.t, S.t32, S.t1k, lim});
+    return fenced_lower_bound(lo, end, pr);
 }
 // first S position in [start, q] with t >= lim (q itself when none before)
 __device__ __forceinline__ uint32_t s_window_begin(const SView& S, uint32_t start, uint32_t q, int64_t lim) {
     uint32_t hi = q;
+    const TProbe<true> pr(S.t, S.t32, S.t1k, lim);
     for (uint32_t span = 1; span <= 32; span <<= 1) {
-        if (hi - start < span) return fenced_lower_bound(start, hi, TProbe<true>{S.t, S.t32, S.t1k, lim});
+        if (hi - start < span) return fenced_lower_bound(start, hi, pr);
         const uint32_t probe = hi - span;
-        if (S.t[probe] < lim) return fenced_lower_bound(probe + 1, hi, TProbe<true>{S.t, S.t32, S.t1k, lim});
+        if (pr.below0(probe)) return fenced_lower_bound(probe + 1, hi, pr);
         hi = probe;
     }
-    return fenced_lower_bound(start, hi, TProbe<true>{S.t, S.t32, S.t1k, lim});
+    return fenced_lower_bound(start, hi, pr);
 }
 
 __global__ void __launch_bounds__(256) star_locate_kernel(SView S, PView P, uint64_t m,
@@ -351,7 +353,8 @@ __device__ __forceinline__ void first_role_ps(const SView& S, const PView& P, co
     const int64_t ta = P.t[k];
     da = (wa >> 31) ^ side;  // 0: outward from u
     const int64_t lim = sat_add(ta, delta);
-    if ((wa & kPLast) || P.t[k + 1] > lim) return;  // no same-neighbour record in the window
+    const TimeKey limk = P.t.key_upto(lim);
+    if ((wa & kPLast) || !P.t.below(k + 1, limk)) return;  // no same-neighbour record in the window
     const uint32_t base = outward_before(S, start);
     const uint32_t e = s_window_end(S, q, end, lim);
     const uint64_t pe_o = outward_before(S, e) - base, pe_i = (uint64_t)(e - start) - pe_o;
@@ -362,7 +365,7 @@ __device__ __forceinline__ void first_role_ps(const SView& S, const PView& P, co
     uint64_t B00 = 0, B01 = 0, B10 = 0, B11 = 0;   // B[d3][d2]: sum [dir_c=d3] P_d2(c)
     uint64_t P00 = 0, P01 = 0, P10 = 0, P11 = 0;   // Pair[d2][d3]
     for (uint32_t j = k + 1;; ++j) {
-        if (P.t[j] > lim) break;
+        if (!P.t.below(j, limk)) break;
         const uint32_t w = P.w[j];
         const uint2 ps = PSs[j];
         const uint64_t pos = ps.x - start;
@@ -404,7 +407,8 @@ __device__ __forceinline__ void third_role_ps(const SView& S, const PView& P, co
     dc = (wc >> 31) ^ side;
     if (wc & kPFirst) return;
     const int64_t lo_lim = sat_sub(P.t[k], delta);
-    if (P.t[k - 1] < lo_lim) return;  // previous same-neighbour record already before the window
+    const TimeKey lok = P.t.key_below(lo_lim);
+    if (P.t.below(k - 1, lok)) return;  // previous same-neighbour record already before the window
     const uint32_t lo = s_window_begin(S, start, q, lo_lim);
     if (lo >= q) return;
     const uint32_t pl = outward_before(S, lo);
@@ -413,7 +417,7 @@ __device__ __forceinline__ void third_role_ps(const SView& S, const PView& P, co
     for (uint32_t j = k - 1;; --j) {
         // a record before the window is no candidate (its PS entry is not
         // written): stop on its time first; in-window members are candidates
-        if (P.t[j] < lo_lim) break;
+        if (P.t.below(j, lok)) break;
         const uint2 ps = PSs[j];
         if (ps.x <= lo) break;  // the member at the window start itself
         const uint32_t w = P.w[j];

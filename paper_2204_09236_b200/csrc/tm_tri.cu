@@ -32,20 +32,19 @@ namespace {
 // otherwise.
 constexpr uint32_t kTableMinBlock = 256;
 
-// (t, ordinal) strict order of P record k before (t, ord)
-__device__ __forceinline__ bool p_before(const PView& P, uint32_t k, int64_t t, uint32_t ord) {
-    const int64_t tk = P.t[k];
-    return tk < t || (tk == t && P.ord[k] < ord);
+// (t, ordinal) strict order of P record k before the record key
+__device__ __forceinline__ bool p_before(const PView& P, uint32_t k, const RecKey& key) {
+    const int c = P.t.cmp(k, key);
+    return c < 0 || (c == 0 && P.ord[k] < key.ord);
 }
-// first k in [from, end) with (t, ord) >= (t0, o0), galloping up from `from`
-// (the boundaries of one window are close together)
-__device__ __forceinline__ uint32_t p_gallop_rec(const PView& P, uint32_t from, uint32_t end, int64_t t0,
-                                                 uint32_t o0) {
+// first k in [from, end) with (t, ord) >= the record key, galloping up from
+// `from` (the boundaries of one window are close together)
+__device__ __forceinline__ uint32_t p_gallop_rec(const PView& P, uint32_t from, uint32_t end, const RecKey& key) {
     uint32_t lo = from, hi = end;
     for (uint32_t span = 1;; span <<= 1) {
         const uint64_t probe = (uint64_t)lo + span - 1;
         if (probe >= end) break;
-        if (!p_before(P, (uint32_t)probe, t0, o0)) {
+        if (!p_before(P, (uint32_t)probe, key)) {
             hi = (uint32_t)probe;
             break;
         }
@@ -53,27 +52,31 @@ __device__ __forceinline__ uint32_t p_gallop_rec(const PView& P, uint32_t from, 
     }
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (p_before(P, mid, t0, o0)) lo = mid + 1; else hi = mid;
+        if (p_before(P, mid, key)) lo = mid + 1; else hi = mid;
     }
     return lo;
 }
-// first k in [from, end) with t > x, galloping up from `from`
+// first k in [from, end) whose time is not below the threshold key (key_below(x):
+// first t >= x; key_upto(x): first t > x), galloping up from `from`
+__device__ __forceinline__ uint32_t p_gallop_t(const PView& P, uint32_t from, uint32_t end, const TimeKey& key) {
+    uint32_t lo = from, hi = end;
+    for (uint32_t span = 1;; span <<= 1) {
+        const uint64_t probe = (uint64_t)lo + span - 1;
+        if (probe >= end) break;
+        if (!P.t.below(probe, key)) {
+            hi = (uint32_t)probe;
+            break;
+        }
+        lo = (uint32_t)probe + 1;
+    }
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (P.t.below(mid, key)) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
 __device__ __forceinline__ uint32_t p_gallop_tupper(const PView& P, uint32_t from, uint32_t end, int64_t x) {
-    uint32_t lo = from, hi = end;
-    for (uint32_t span = 1;; span <<= 1) {
-        const uint64_t probe = (uint64_t)lo + span - 1;
-        if (probe >= end) break;
-        if (P.t[probe] > x) {
-            hi = (uint32_t)probe;
-            break;
-        }
-        lo = (uint32_t)probe + 1;
-    }
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (P.t[mid] <= x) lo = mid + 1; else hi = mid;
-    }
-    return lo;
+    return p_gallop_t(P, from, end, P.t.key_upto(x));
 }
 
 // One path for every group, short or long: the lanes of a warp hold wedges
@@ -110,8 +113,8 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         ke = P.gend ? p_group_end(P, kb) : p_max_upper(P, kb, blk_end, b);
     }
     const uint32_t k1 = p_t_lower(P, kb, ke, lo);
-    const uint32_t k2 = p_gallop_rec(P, k1, ke, ti, oi);
-    const uint32_t k3 = p_gallop_rec(P, k2, ke, tj, oj);
+    const uint32_t k2 = p_gallop_rec(P, k1, ke, P.t.rec_key(ti, oi));
+    const uint32_t k3 = p_gallop_rec(P, k2, ke, P.t.rec_key(tj, oj));
     const uint32_t k4 = p_gallop_tupper(P, k3, ke, hi);
     uint32_t k2e = k2;  // type I records whose own t is at most t_last
     if (t_last != INT64_MAX) {
@@ -180,7 +183,13 @@ __device__ __forceinline__ void wedges_from(const PView& P, const TimeArr& T,
 // runs past kWedgeScan records (or whose wedges do not fit the list) goes to
 // the long list instead and is enumerated by tri_long_kernel.
 constexpr int kWedgeScan = 8;
-constexpr int kGroupCache = 128;
+#ifndef TM_GCACHE_BITS
+#define TM_GCACHE_BITS 7
+#endif
+#ifndef TM_CACHE_MINB
+#define TM_CACHE_MINB 4
+#endif
+constexpr int kGroupCache = 1 << TM_GCACHE_BITS;  // entries per warp (dynamic shared memory)
 constexpr uint32_t kGroupCacheMinWindow = 64;  // shorter windows repeat few groups: plain path
 
 #ifndef TM_WEDGE_MINB
@@ -211,14 +220,14 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(TimeArr FT,
             if (i + 1 >= fe) continue;
             const uint32_t node = Fnode[i];
             const uint32_t v = FN[i] & kNodeMask;
-            const int64_t lim = sat_add(FT[i], delta);
+            const TimeKey limk = FT.key_upto(sat_add(FT[i], delta));  // in-window: t <= t_i + delta
             bool alive = true;
             uint32_t hits = 0;
 #pragma unroll
             for (int s = 1; s <= kWedgeScan; ++s) {
                 const uint64_t j = i + s;
                 if (alive) {
-                    if (j >= fe || Fnode[j] != node || FT[j] > lim) {
+                    if (j >= fe || Fnode[j] != node || !FT.below(j, limk)) {
                         alive = false;
                     } else if ((FN[j] & kNodeMask) != v) {
                         hits |= 1u << (s - 1);
@@ -226,11 +235,11 @@ __global__ void __launch_bounds__(256) tri_filter_kernel(TimeArr FT,
                 }
             }
             if (alive && i + kWedgeScan + 1 < fe && Fnode[i + kWedgeScan + 1] == node &&
-                FT[i + kWedgeScan + 1] <= lim) {
+                FT.below(i + kWedgeScan + 1, limk)) {
                 // a window past kGroupCacheMinWindow records goes to the very-long
                 // list, filled from the back of the same buffer (lcount[1])
                 const uint64_t x = i + 1 + kGroupCacheMinWindow;
-                if (x < fe && Fnode[x] == node && FT[x] <= lim)
+                if (x < fe && Fnode[x] == node && FT.below(x, limk))
                     long_list[long_cap - 1 - atomicAdd(lcount + 1, 1u)] = (uint32_t)i;
                 else
                     longs |= 1u << jj;
@@ -340,21 +349,7 @@ struct GroupCacheEntry {
 
 // first k in [from, end) with t >= x, galloping up from `from`
 __device__ __forceinline__ uint32_t p_gallop_tlower(const PView& P, uint32_t from, uint32_t end, int64_t x) {
-    uint32_t lo = from, hi = end;
-    for (uint32_t span = 1;; span <<= 1) {
-        const uint64_t probe = (uint64_t)lo + span - 1;
-        if (probe >= end) break;
-        if (P.t[probe] >= x) {
-            hi = (uint32_t)probe;
-            break;
-        }
-        lo = (uint32_t)probe + 1;
-    }
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (P.t[mid] < x) lo = mid + 1; else hi = mid;
-    }
-    return lo;
+    return p_gallop_t(P, from, end, P.t.key_below(x));
 }
 
 // the v-w group [kb, ke) (empty when no v-w record: kb == ke)
@@ -375,7 +370,7 @@ __device__ __forceinline__ void locate_group(const PView& P, uint32_t v, uint32_
 // count per wedge, full occupancy), kCache = true the longer ones (the group
 // cache's shared memory costs a resident block per SM).
 template <bool kCache>
-__global__ void __launch_bounds__(256, kCache ? 4 : TM_LONG_MINB) tri_long_kernel(PView P, TimeArr FT,
+__global__ void __launch_bounds__(256, kCache ? TM_CACHE_MINB : TM_LONG_MINB) tri_long_kernel(PView P, TimeArr FT,
                                                        const uint32_t* __restrict__ FN,
                                                        const uint32_t* __restrict__ FO,
                                                        const uint32_t* __restrict__ Fnode,
@@ -388,7 +383,7 @@ __global__ void __launch_bounds__(256, kCache ? 4 : TM_LONG_MINB) tri_long_kerne
                                                        unsigned long long* queue, uint64_t* out,
                                                        uint64_t* stats) {
     __shared__ unsigned long long cells[48];
-    __shared__ GroupCacheEntry gcache[8][kCache ? kGroupCache : 1];
+    extern __shared__ __align__(16) unsigned char gcache_raw[];  // kCache: 8 warps x kGroupCache entries
     zero_cells(cells, 24);
     __syncthreads();
     WarpCells wc;
@@ -399,7 +394,7 @@ __global__ void __launch_bounds__(256, kCache ? 4 : TM_LONG_MINB) tri_long_kerne
     if (!P.gend || *pt_wsum < gend_min) P.gend = nullptr;  // group ends not built
     uint32_t my_wedges = 0;
     const int lane = threadIdx.x & 31;
-    GroupCacheEntry* gc = gcache[threadIdx.x >> 5];
+    GroupCacheEntry* gc = reinterpret_cast<GroupCacheEntry*>(gcache_raw) + (size_t)(threadIdx.x >> 5) * kGroupCache;
     for (;;) {  // one first edge per warp from the queue
         const uint64_t idx = warp_take(queue, 1);
         if (idx >= cnt) break;
@@ -410,6 +405,8 @@ __global__ void __launch_bounds__(256, kCache ? 4 : TM_LONG_MINB) tri_long_kerne
         const int64_t ti = FT[i];
         const uint32_t oi = FO[i];
         const int64_t lim = sat_add(ti, delta);
+        const TimeKey limk = FT.key_upto(lim);  // in-window: t_j <= t_i + delta
+        const RecKey ki = P.t.rec_key(ti, oi);
         // a window of at most kGroupCacheMinWindow records: one closing count
         // per wedge; a longer one goes through the group cache
         const bool longwin = kCache;
@@ -417,7 +414,7 @@ __global__ void __launch_bounds__(256, kCache ? 4 : TM_LONG_MINB) tri_long_kerne
         uint32_t j0 = i + 1;
         for (; !longwin && j0 < end; j0 += 32) {
             const uint32_t j = j0 + lane;
-            const bool in = j < end && FT[j] <= lim;
+            const bool in = j < end && FT.below(j, limk);
             const bool wedge = in && (FN[j] & kNodeMask) != v;
             uint32_t c[6] = {0, 0, 0, 0, 0, 0};
             int cb = 0;
@@ -435,15 +432,21 @@ __global__ void __launch_bounds__(256, kCache ? 4 : TM_LONG_MINB) tri_long_kerne
         for (int x = lane; x < kGroupCache; x += 32) gc[x].w = 0xFFFFFFFFu;
         __syncwarp();
         uint32_t misses = 0;
+#ifdef TM_TRI_STATS
+        uint32_t empties = 0, miss_iters = 0, iters = 0;
+#endif
         for (; j0 < end; j0 += 32) {
+#ifdef TM_TRI_STATS
+            int miss_flag = 0;
+#endif
             const uint32_t j = j0 + lane;
-            const bool in = j < end && FT[j] <= lim;
+            const bool in = j < end && FT.below(j, limk);
             const uint32_t nj = in ? FN[j] : 0u;
             const uint32_t w = nj & kNodeMask;
             const bool wedge = in && w != v;
             uint32_t c[6] = {0, 0, 0, 0, 0, 0};
             int cb = 0;
-            const uint32_t slot = (w * 0x9E3779B1u) >> (32 - 7);
+            const uint32_t slot = (w * 0x9E3779B1u) >> (32 - TM_GCACHE_BITS);
             GroupCacheEntry e;
             if (wedge) {
                 const int64_t tj = FT[j];
@@ -451,11 +454,17 @@ __global__ void __launch_bounds__(256, kCache ? 4 : TM_LONG_MINB) tri_long_kerne
                 e = gc[slot];
                 if (e.w != w) {  // miss: the group and its e_i boundaries
                     ++misses;
+#ifdef TM_TRI_STATS
+                    miss_flag = 1;
+#endif
                     e.w = w;
                     uint32_t kb, ke;
                     locate_group(P, v, w, kb, ke);
+#ifdef TM_TRI_STATS
+                    if (kb == ke) ++empties;
+#endif
                     e.k1 = p_t_lower(P, kb, ke, sat_sub(tj, delta));
-                    e.k2 = p_gallop_rec(P, e.k1, ke, ti, oi);
+                    e.k2 = p_gallop_rec(P, e.k1, ke, ki);
                     e.k4 = p_t_upper(P, e.k2, ke, lim);
                     e.k3 = e.k2;
                     e.d2 = p_dir_before(P, e.k2);
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(256, kCache ? 4 : TM_LONG_MINB) tri_long_kerne
                 }
                 // the window's lower end t_j - delta and e_j only move forward with j
                 const uint32_t k1 = p_gallop_tlower(P, e.k1, e.k2, sat_sub(tj, delta));
-                const uint32_t k3 = p_gallop_rec(P, e.k3 > e.k2 ? e.k3 : e.k2, e.k4, tj, oj);
+                const uint32_t k3 = p_gallop_rec(P, e.k3 > e.k2 ? e.k3 : e.k2, e.k4, P.t.rec_key(tj, oj));
                 e.k1 = k1;
                 e.k3 = k3;
                 const uint32_t flip = ranks_below(P.cls, v, w) ? 0u : 1u;
@@ -499,14 +508,269 @@ __global__ void __launch_bounds__(256, kCache ? 4 : TM_LONG_MINB) tri_long_kerne
             if (wedge && (peers >> lane) == 1u) gc[slot] = e;
             __syncwarp();
             wc.add6(wedge, cb, c, cells, 24);
+#ifdef TM_TRI_STATS
+            ++iters;
+            if (__any_sync(0xffffffffu, miss_flag)) ++miss_iters;
+#endif
             if (!__all_sync(0xffffffffu, in)) break;
         }
+#ifdef TM_TRI_STATS
+        empties = warp_sum(empties);
+        if (lane == 0 && stats) {
+            atomicAdd((unsigned long long*)&stats[6], (unsigned long long)empties);
+            atomicAdd((unsigned long long*)&stats[7], ((unsigned long long)miss_iters << 32) | iters);
+        }
+#endif
         misses = warp_sum(misses);
         if (lane == 0 && misses && stats) atomicAdd((unsigned long long*)&stats[5], (unsigned long long)misses);
     }
     wc.flush(cells, 24, 24);
     my_wedges = warp_sum(my_wedges);
     if (lane == 0 && my_wedges && stats) atomicAdd((unsigned long long*)&stats[4], (unsigned long long)my_wedges);
+    __syncthreads();
+    flush_cells(cells, 24, out, kAccCarry);
+}
+
+// ---- very long windows: resolve-then-count -------------------------------
+//
+// tri_long_kernel<true> looks a group up the first time a lane meets it, so in
+// nearly every 32-record step a few lanes run the whole lookup (block search,
+// group end, four window searches) while the others wait.  tri_window_kernel
+// splits each window segment in two passes over the same records (they stay
+// in L1):
+//   A. collect the neighbours w the warp's table does not hold yet -- one
+//      claim per distinct w, appended to a pending list -- and resolve the
+//      pending groups 32 at a time, one per lane, so lookups run with every
+//      lane busy;
+//   B. count: every wedge finds its group in the table (linear probing, a
+//      handful of slots) and pays two short gallops for k1 / k3, which only
+//      grow with j; a group with no record inside [t_j - delta, t_i + delta]
+//      is skipped on its cached bounds.
+// The table lives for one first edge (k2, k4 and the direction prefixes there
+// depend on e_i only) and is cleared between segments once half full; a
+// neighbour that finds no free slot within kGcProbes falls back to the
+// one-off closing count.
+#ifndef TM_LONG_SEG
+#define TM_LONG_SEG 128
+#endif
+constexpr uint32_t kGcEmpty = 0xFFFFFFFFu;
+constexpr int kGcProbes = 4;
+constexpr uint32_t kLongSeg = TM_LONG_SEG;  // window records per resolve / count segment
+static_assert(kLongSeg % 32 == 0, "segments are whole 32-record steps");
+
+// slot of w in the warp's table (found), else the first empty slot on its
+// probe path (found = false), else -1 (no room within kGcProbes)
+__device__ __forceinline__ int gc_probe(const GroupCacheEntry* gc, uint32_t w, bool& found) {
+    const uint32_t h = (w * 0x9E3779B1u) >> (32 - TM_GCACHE_BITS);
+    found = false;
+#pragma unroll
+    for (int p = 0; p < kGcProbes; ++p) {
+        const uint32_t s = (h + p) & (kGroupCache - 1);
+        const uint32_t tag = gc[s].w;
+        if (tag == w) {
+            found = true;
+            return (int)s;
+        }
+        if (tag == kGcEmpty) return (int)s;
+    }
+    return -1;
+}
+
+// fill the claimed entry of neighbour w, first met at window record j
+__device__ __forceinline__ void gc_resolve(const PView& P, const TimeArr& FT, GroupCacheEntry* gc, uint32_t v,
+                                           uint32_t w, uint32_t j, int64_t delta, const RecKey& ki, int64_t lim) {
+    GroupCacheEntry e;
+    e.w = w;
+    uint32_t kb, ke;
+    locate_group(P, v, w, kb, ke);
+    e.k1 = p_t_lower(P, kb, ke, sat_sub(FT[j], delta));
+    e.k2 = p_gallop_rec(P, e.k1, ke, ki);
+    e.k4 = p_t_upper(P, e.k2, ke, lim);
+    e.k3 = e.k2;
+    e.d2 = p_dir_before(P, e.k2);
+    e.d4 = p_dir_before(P, e.k4);
+    e.pad = ranks_below(P.cls, v, w) ? 0u : 1u;  // dir_rel_lower -> dir relative to v
+    bool found;
+    const int slot = gc_probe(gc, w, found);  // the slot claimed for w
+    gc[slot] = e;
+}
+
+__global__ void __launch_bounds__(256, TM_CACHE_MINB) tri_window_kernel(PView P, TimeArr FT,
+                                                       const uint32_t* __restrict__ FN,
+                                                       const uint32_t* __restrict__ FO,
+                                                       const uint32_t* __restrict__ Fnode,
+                                                       const uint32_t* __restrict__ Foff,
+                                                       int64_t delta, int64_t t_last,
+                                                       const uint32_t* __restrict__ list, uint32_t long_cap,
+                                                       const uint32_t* __restrict__ lcount,
+                                                       const unsigned long long* __restrict__ pt_wsum,
+                                                       uint64_t gend_min, unsigned long long* queue,
+                                                       uint64_t* out, uint64_t* stats) {
+    __shared__ unsigned long long cells[48];
+    __shared__ uint2 pend_all[8][64];  // per warp: (w, first window record) awaiting a lookup
+    extern __shared__ __align__(16) unsigned char gcache_raw[];  // 8 warps x kGroupCache entries
+    zero_cells(cells, 24);
+    __syncthreads();
+    WarpCells wc;
+    const uint32_t cnt = lcount[1];  // the very-long list (back of the buffer)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && stats) atomicAdd((unsigned long long*)&stats[3], (unsigned long long)cnt);
+    if (!P.gend || *pt_wsum < gend_min) P.gend = nullptr;  // group ends not built
+    P.pt_keys = nullptr;
+    uint32_t my_wedges = 0, lookups = 0;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    GroupCacheEntry* gc = reinterpret_cast<GroupCacheEntry*>(gcache_raw) + (size_t)(threadIdx.x >> 5) * kGroupCache;
+    uint2* pend = pend_all[threadIdx.x >> 5];
+    for (;;) {  // one first edge per warp from the queue
+        const uint64_t idx = warp_take(queue, 1);
+        if (idx >= cnt) break;
+        const uint32_t i = list[long_cap - 1 - idx];
+        const uint32_t end = Foff[Fnode[i] + 1];
+        const uint32_t ni = FN[i];
+        const uint32_t v = ni & kNodeMask;
+        const int64_t ti = FT[i];
+        const uint32_t oi = FO[i];
+        const int64_t lim = sat_add(ti, delta);
+        const TimeKey limk = FT.key_upto(lim);  // in-window: t_j <= t_i + delta
+        const RecKey ki = P.t.rec_key(ti, oi);
+        for (int x = lane; x < kGroupCache; x += 32) gc[x].w = kGcEmpty;
+        __syncwarp();
+        uint32_t used = 0;  // claimed entries (warp-uniform)
+        bool done = false;
+        for (uint32_t s0 = i + 1; s0 < end && !done; s0 += kLongSeg) {
+            const uint32_t s1 = end - s0 > kLongSeg ? s0 + kLongSeg : end;
+            if (used > (uint32_t)kGroupCache / 2) {
+                for (int x = lane; x < kGroupCache; x += 32) gc[x].w = kGcEmpty;
+                used = 0;
+                __syncwarp();
+            }
+            // ---- pass A: claim and resolve the groups the table lacks
+            uint32_t npend = 0;
+            for (uint32_t j0 = s0; j0 < s1; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const bool in = j < s1 && FT.below(j, limk);
+                const uint32_t w = in ? FN[j] & kNodeMask : v;
+                bool found = false;
+                int slot = -1;
+                if (w != v) slot = gc_probe(gc, w, found);
+                const bool need = w != v && !found && slot >= 0;
+                // one candidate per distinct w: its earliest record (lowest lane)
+                const unsigned same_w = __match_any_sync(0xffffffffu, need ? w : (0x80000000u | (uint32_t)lane));
+                bool cand = need && (__ffs(same_w) - 1) == lane;
+                while (__any_sync(0xffffffffu, cand)) {
+                    // two neighbours may want the same empty slot: the lower lane takes it
+                    const unsigned same_s =
+                        __match_any_sync(0xffffffffu, cand ? (uint32_t)slot : (0x80000000u | (uint32_t)lane));
+                    const bool win = cand && (__ffs(same_s) - 1) == lane;
+                    if (win) gc[slot].w = w;
+                    const unsigned wm = __ballot_sync(0xffffffffu, win);
+                    if (win) pend[npend + __popc(wm & lt_mask)] = make_uint2(w, j);
+                    npend += __popc(wm);
+                    used += __popc(wm);
+                    __syncwarp();
+                    if (npend >= 32) {  // a full batch: one lookup per lane
+                        const uint2 pe = pend[lane];
+                        const uint2 rest = pend[32 + lane];
+                        gc_resolve(P, FT, gc, v, pe.x, pe.y, delta, ki, lim);
+                        lookups += 1;
+                        __syncwarp();
+                        pend[lane] = rest;
+                        npend -= 32;
+                        __syncwarp();
+                    }
+                    const bool lose = cand && !win;
+                    cand = false;
+                    if (lose) {
+                        slot = gc_probe(gc, w, found);
+                        cand = slot >= 0;  // (w itself cannot have appeared: one candidate per w)
+                    }
+                }
+                if (!__all_sync(0xffffffffu, in)) break;
+            }
+            if (npend) {  // the rest of the segment's claims
+                if ((uint32_t)lane < npend) {
+                    const uint2 pe = pend[lane];
+                    gc_resolve(P, FT, gc, v, pe.x, pe.y, delta, ki, lim);
+                    lookups += 1;
+                }
+            }
+            __syncwarp();
+            // ---- pass B: count
+            for (uint32_t j0 = s0; j0 < s1; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const bool in = j < s1 && FT.below(j, limk);
+                const uint32_t nj = in ? FN[j] : 0u;
+                const uint32_t w = nj & kNodeMask;
+                const bool wedge = in && w != v;
+                uint32_t c[6] = {0, 0, 0, 0, 0, 0};
+                int cb = 0;
+                bool upd = false;
+                int slot = -1;
+                uint32_t k1 = 0, k3 = 0;
+                if (wedge) {
+                    ++my_wedges;
+                    cb = (int)((ni >> 31) * 4 + (nj >> 31) * 2);
+                    bool found;
+                    slot = gc_probe(gc, w, found);
+                    if (!found) {  // no room in the table: the one-off closing count
+                        wedge_counts(P, FT, FN, FO, i, j, delta, t_last, c);
+                        lookups += 1;
+                    } else {
+                        const GroupCacheEntry e = gc[slot];
+                        if (e.k4 > e.k1) {  // records left inside [t_j - delta, t_i + delta]
+                            const int64_t tj = FT[j];
+                            // the window's lower end t_j - delta and e_j only move forward with j
+                            k1 = p_gallop_tlower(P, e.k1, e.k2, sat_sub(tj, delta));
+                            k3 = p_gallop_rec(P, e.k3, e.k4, P.t.rec_key(tj, FO[j]));
+                            upd = true;
+                            const uint32_t flip = e.pad;
+                            uint32_t k2e = e.k2;
+                            if (t_last != INT64_MAX) {
+                                uint32_t l = k1, r = e.k2;
+                                while (l < r) {
+                                    const uint32_t mid = (l + r) >> 1;
+                                    if (P.t[mid] <= t_last) l = mid + 1; else r = mid;
+                                }
+                                k2e = l;
+                            }
+                            auto add_range = [&](int type, uint32_t x0, uint32_t d0, uint32_t x1, uint32_t d1) {
+                                if (x1 <= x0) return;
+                                const uint32_t n1 = d1 - d0;
+                                const uint32_t n0 = (x1 - x0) - n1;
+                                c[type * 2 + flip] += n0;
+                                c[type * 2 + (flip ^ 1u)] += n1;
+                            };
+                            if (k1 < k2e) add_range(0, k1, p_dir_before(P, k1), k2e, k2e == e.k2 ? e.d2 : p_dir_before(P, k2e));
+                            if (ti <= t_last) {
+                                const uint32_t d3 = (k3 == e.k2) ? e.d2 : (k3 == e.k4) ? e.d4 : p_dir_before(P, k3);
+                                add_range(1, e.k2, e.d2, k3, d3);
+                                add_range(2, k3, d3, e.k4, e.d4);
+                            }
+                        }
+                    }
+                }
+                // one writer per group: the highest lane that advanced it
+                const unsigned peers = __match_any_sync(0xffffffffu, upd ? w : (0x80000000u | (uint32_t)lane));
+                if (upd && (peers >> lane) == 1u) {
+                    gc[slot].k1 = k1;
+                    gc[slot].k3 = k3;
+                }
+                __syncwarp();
+                wc.add6(wedge, cb, c, cells, 24);
+                if (!__all_sync(0xffffffffu, in)) {
+                    done = true;
+                    break;
+                }
+            }
+        }
+    }
+    wc.flush(cells, 24, 24);
+    my_wedges = warp_sum(my_wedges);
+    lookups = warp_sum(lookups);
+    if (lane == 0 && stats) {
+        if (my_wedges) atomicAdd((unsigned long long*)&stats[4], (unsigned long long)my_wedges);
+        if (lookups) atomicAdd((unsigned long long*)&stats[5], (unsigned long long)lookups);
+    }
     __syncthreads();
     flush_cells(cells, 24, out, kAccCarry);
 }
@@ -737,9 +1001,31 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
     TM_LAUNCH("tri_long", st, tri_long_kernel<false>, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
               f.node, f.off, ts.delta, t_last, ts.long_list, ts.long_cap, lcount, ts.wsum, min_wedges, gend_min,
               ts.queue + 1, d_out, d_stats);
-    TM_LAUNCH("tri_long", st, tri_long_kernel<true>, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
+    constexpr size_t kCacheBytes = 8 * (size_t)kGroupCache * sizeof(GroupCacheEntry);
+    static const bool cache_attr = [] {
+        TM_CUDA(cudaFuncSetAttribute(tri_long_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kCacheBytes));
+        return true;
+    }();
+    (void)cache_attr;
+#ifndef TM_TWO_PHASE
+#define TM_TWO_PHASE 1
+#endif
+#if TM_TWO_PHASE
+    static const bool window_attr = [] {
+        TM_CUDA(cudaFuncSetAttribute(tri_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kCacheBytes));
+        return true;
+    }();
+    (void)window_attr;
+    TM_LAUNCH("tri_long", st, tri_window_kernel, (unsigned)cap, 256, kCacheBytes, pv, f.t.view(g.tbase), f.nbr, f.ord,
+              f.node, f.off, ts.delta, t_last, ts.long_list, ts.long_cap, lcount, ts.wsum, gend_min,
+              ts.queue + 2, d_out, d_stats);
+#else
+    TM_LAUNCH("tri_long", st, tri_long_kernel<true>, (unsigned)cap, 256, kCacheBytes, pv, f.t.view(g.tbase), f.nbr, f.ord,
               f.node, f.off, ts.delta, t_last, ts.long_list, ts.long_cap, lcount, ts.wsum, min_wedges, gend_min,
               ts.queue + 2, d_out, d_stats);
+#endif
     dfree(ts.pt, st);
     dfree(ts.gend, st);
     dfree(ts.queue, st);

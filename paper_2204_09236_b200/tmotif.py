@@ -718,7 +718,12 @@ class GraphContext:
         _raise(self._lib.tm_run_stats(self._h, out.ctypes.data), self._lib)
         keys = ["star_first_candidates", "star_third_candidates", "short_wedges", "long_first_edges",
                 "long_wedges", "long_group_lookups"]
-        return {k: int(v) for k, v in zip(keys, out)}
+        stats = {k: int(v) for k, v in zip(keys, out)}
+        if out[6] or out[7]:  # instrumented builds only (-DTM_TRI_STATS)
+            stats["long_empty_lookups"] = int(out[6])
+            stats["long_iterations"] = int(out[7]) & 0xFFFFFFFF
+            stats["long_iterations_with_lookup"] = int(out[7]) >> 32
+        return stats
 
     def partition(self, world: int, rank: int) -> Tuple[int, int]:
         b, e = C.c_uint32(0), C.c_uint32(0)

@@ -169,6 +169,7 @@ def config4_full_golden(R, deltas=(600,)):
         n, s, d, tt = synth.power_law_hashed(CONFIG4["n"], CONFIG4["m"], CONFIG4["mean_gap"], CONFIG4["seed"])
     h = edge_hash(s, d, tt)
     gen_s = round(time.time() - t0, 1)
+    print("config4 full: generated + hashed in", gen_s, "s, hash", h, flush=True)
     out = json.load(open(path)) if os.path.exists(path) else {
         "config": "powerlaw_50m_600m", "generator": "synth.power_law_hashed", **CONFIG4, "edges": int(len(s)),
         "hash": h, "cases": []}
@@ -177,6 +178,7 @@ def config4_full_golden(R, deltas=(600,)):
     g = R.build_graph(n, s, d, tt)
     del s, d, tt
     build_s = round(time.time() - t0, 1)
+    print("config4 full: reference graph + indexes built in", build_s, "s", flush=True)
     done = {c["delta"] for c in out["cases"]}
     for delta in deltas:
         if delta in done:

@@ -230,6 +230,29 @@ def test_extreme_timestamps_saturate(cuda, tm, oracle):
         oracle.free(og)
 
 
+def test_time_span_at_the_narrow_record_boundary(cuda, tm, oracle):
+    """u32 time offsets are used while the span is <= 0xFFFFFFFE (searches
+    compare offsets against a u32 threshold, 0xFFFFFFFF = every record); a
+    span one past that switches to int64 times.  Both sides of the boundary,
+    with records clustered at both ends of the span and deltas that reach
+    across it."""
+    for span in (0xFFFFFFFE, 0xFFFFFFFF, 2 ** 32, 2 ** 32 + 5):
+        for base in (0, -(2 ** 40), 2 ** 62):
+            rng = np.random.default_rng(span % 977 + abs(base) % 13)
+            n, m = 7, 160
+            src = rng.integers(0, n, m).astype(np.uint32)
+            dst = ((src + rng.integers(1, n, m)) % n).astype(np.uint32)
+            off = np.where(rng.random(m) < 0.5, rng.integers(0, 30, m), span - rng.integers(0, 30, m))
+            off[0], off[1] = 0, span
+            t = np.sort(np.int64(base) + off.astype(np.int64))
+            g = tm.TemporalGraph([str(i) for i in range(n)], src, dst, t)
+            og = oracle_graph(oracle, g)
+            ctx = ctx_of(tm, g)
+            for d in (0, 9, 2 ** 31, span - 1, span, 2 ** 33, 2 ** 63 - 1):
+                assert (tm.run_parallel(ctx, tm.RunConfig(delta=d)).counts == oracle.census(og, d)).all(), (span, base, d)
+            oracle.free(og)
+
+
 def test_errors_mirror_reference(cuda, tm):
     g = toy_arrays()
     ctx = ctx_of(tm, g)
