@@ -39,13 +39,20 @@ DEFAULT_CONFIG = "powerlaw_50m_600m"
 # records) when the time span fits 32 bits, else int64 (wide).
 #   radix_downsweep per key per digit pass: u64 key read + write, plus (narrow
 #                 records) the u64 payload read + write
-#                 node sort: 2m keys (node << 32 | record), ceil(nb/8) passes
+#                 node sort: 2m keys (node << 32 | record), ceil(nb/8) passes (the
+#                 first reads the caller's src / dst / t, 8 B per record, when the
+#                 input is time-ordered)
 #                 pair sort: m keys (min << 32 | edge), ceil(nb/8) passes
 #                 t sort:    m keys, ceil(tbits/8) passes (unsorted input only)
-#   gather_s      per incident record: sorted key 8 + payload 8 (narrow; wide:
-#                 the 16-byte edge record) + S outputs t 4 (8), nbr 4, ord 4, node 4
-#   gather_p      per edge: sorted key 8 + payload 8 (16) + P outputs t 4 (8), ord 4,
-#                 min 4, max 4, w 4
+#   gather_s      (wide records only) per incident record: sorted key 8 + the
+#                 16-byte edge record + S outputs t 8, nbr 4, ord 4, node 4; narrow
+#                 records: the node sort's last pass writes S itself (same bytes as
+#                 writing the sorted key + payload), then
+#   s_offsets     per incident record: S node 4; per node: offset 4 written
+#   gather_p      (wide records only) per edge: sorted key 8 + the 16-byte edge
+#                 record + P outputs t 8, ord 4, min 4, max 4, w 4; narrow records:
+#                 the pair sort's last pass writes P itself, then
+#   p_flags       per edge: P min 4 + max 4 + w 4 read, w 4 written; per node pofs 4
 #   pair_keys     per incident record: key 8 + S nbr 4 + S t 4; per edge the pair
 #                 key 8 + payload 8 written
 #   star_filter   per edge: P t 4 (8) + P w 4
@@ -68,11 +75,14 @@ def algo_bytes(n, m, t, stats=None):
     sort += m * kv * 2 * ((nb + 7) // 8)
     if unsorted:
         sort += m * (8 if tb + pbits <= 64 else 12) * 2 * ((tb + 7) // 8)
+    elif narrow:
+        sort -= R * 8  # the node sort's first pass reads the edge arrays (8 B per record), not packed records
     tw = 4 if narrow else 8
     eb = 8 if narrow else 16
     out = {"radix_downsweep": sort, "gather_s": R * (8 + eb + tw + 12), "gather_p": m * (8 + eb + tw + 16),
            "pair_keys": R * 16 + m * 16, "star_filter": m * (tw + 4), "tri_filter": m * (tw + 8),
-           "scan": (R + m) // 32 * 16}
+           "scan": (R + m) // 32 * 16, "s_offsets": R * 4 + n * 4,
+           "p_flags": m * 16 + n * 4}
     if stats:
         cand = stats["star_first_candidates"] + stats["star_third_candidates"]
         out["star_locate"] = cand * 60
@@ -230,6 +240,9 @@ def main():
                          "center ranges over a replicated graph")
     ap.add_argument("--same-device", action="store_true",
                     help="testing only: every rank uses cuda:0 (independent kernels, gloo reduce)")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="testing only: take the N>1 path (process group, counter all-reduce) at world size 1, "
+                         "so the NCCL reduce runs on a single-GPU box")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -267,7 +280,8 @@ def main():
     dev = torch.device("cuda", local)
     red_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
     dist = None
-    if world > 1:
+    multi = world > 1 or (args.force_dist and "RANK" in os.environ)
+    if multi:
         import torch.distributed as dist
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
@@ -327,7 +341,7 @@ def main():
     from paper_2204_09236_b200.distributed import allreduce_counters
 
     def reduce_raw(census):
-        if world > 1:  # one all-reduce of the 56 counters, exact (32-bit halves), checked on merge
+        if multi:  # one all-reduce of the 56 counters, exact (32-bit halves), checked on merge
             with torch.cuda.stream(stream):
                 tot = allreduce_counters(raw, device=red_dev)
             census = tm.merge_census(tm.StarCounter(tot[:24]), tm.PairCounter(tot[24:32]), tm.TriCounter(tot[32:]),
@@ -399,10 +413,16 @@ def main():
     ms_e2e_sync, census_e2e, _ = device_ms(loop(True), max(2, args.steps // 2), args.warmup)
     assert (census == census_e2e).all(), "device and host paths disagree"
     e2e_api = "tm_count_edges_async (two batches in flight: copy of batch i+1 overlaps census i)"
+    h2d_bytes = int(m_local * 16)
     if tuple(center) == (0, 0):
-        # >= 4 batches: the pipeline fill (first copy, last census) is amortised
-        ms_e2e, census_pipe, _ = device_ms(pipelined, max(4, args.steps), 1)
+        # >= 4 batches: the pipeline fill (first copy, last census) is amortised;
+        # two warm-up batches touch both staging slots
+        ms_e2e, census_pipe, _ = device_ms(pipelined, max(4, args.steps), 2)
         assert (census == census_pipe).all(), "device and pipelined host paths disagree"
+        h2d_bytes = tm.async_h2d_bytes()
+        if h2d_bytes < m_local * 16:
+            e2e_api += ("; timestamps travel as per-block i64 bases + u32 offsets packed by host worker threads "
+                        "inside the timed region (12 B per edge on the link)")
     else:  # center ranges go through the synchronous API only
         ms_e2e = ms_e2e_sync
         e2e_api = "tm_count_edges (one batch at a time)"
@@ -416,7 +436,7 @@ def main():
     torch.cuda.synchronize()
     tm.kernel_timing(enable=False)
     names = ["star_filter", "star_locate", "star_work", "tri_filter", "tri_wedge", "tri_long", "radix_upsweep",
-             "radix_downsweep", "radix_scan", "scan", "gather_s", "gather_p", "forward_scatter", "pack_edges",
+             "radix_downsweep", "radix_scan", "scan", "gather_s", "s_offsets", "gather_p", "p_flags", "forward_scatter", "pack_edges",
              "pair_keys", "time_keys", "perm_from_keys", "validate", "offsets", "forward_off", "group_end",
              "pair_table", "tri_gate", "orient", "degree_class"]
     ktimes = {}
@@ -479,10 +499,10 @@ def main():
                                               f"center ranges over {world} GPUs, graph replicated")),
         "census_total": int(np.asarray(census, np.uint64).sum()),
         "census": [int(x) for x in census],
-        "e2e": {"value": m / (ms_e2e * 1e-3), "unit": "edges/s", "h2d_bytes_per_step": int(m_local * 16),
+        "e2e": {"value": m / (ms_e2e * 1e-3), "unit": "edges/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": int(56 * 8 + 36 * 8), "ms_per_step": ms_e2e,
                 "api": e2e_api, "h2d_GBps_measured": h2d,
-                "h2d_bound_ms": m_local * 16 / (h2d * 1e9) * 1e3,
+                "h2d_bound_ms": h2d_bytes / (h2d * 1e9) * 1e3,
                 "sync_api": {"value": m / (ms_e2e_sync * 1e-3), "ms_per_step": ms_e2e_sync,
                              "api": "tm_count_edges (one batch at a time)"}},
         "gpu_launches": int(launches),

@@ -6,12 +6,17 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <random>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/tmotif_b200.h"
@@ -879,6 +884,163 @@ bool complete_pending(ReplayPending& P, cudaEvent_t done, const tm_run_config* c
 // Per-host-thread pipeline of the asynchronous API: two staging slots of
 // device input buffers, filled on a copy stream while the other slot's
 // census runs.
+// ---- host-side timestamp packing for the pipelined batches ----------------
+//
+// A batch's PCIe bytes are 16 per edge (u32 src, u32 dst, i64 t), and the
+// pipelined census of a large batch is bound by that copy (config 4: 9.6 GB at
+// ~53 GB/s = 182 ms against a 151 ms census).  Timestamps of 65536 consecutive
+// edges almost always span less than 2^32, so host worker threads rewrite t as
+// a per-block i64 base + u32 offsets into a pinned staging buffer while the
+// src / dst copies are on the wire; the copy stream waits for each packed piece
+// with a host function, copies it (4 bytes per edge) and one kernel expands the
+// offsets into the i64 array the census reads.  A block whose span does not fit
+// marks the batch, and its census then waits for a plain copy of t.
+constexpr uint64_t kPackBlock = 1u << 16;   // edges per base
+constexpr uint64_t kPackTask = 1u << 20;    // edges per worker task
+constexpr uint64_t kPackPiece = 1u << 26;   // edges per staged copy
+constexpr uint64_t kPackMinEdges = 1u << 24;  // smaller batches: plain copies (TM_H2D_PACK_MIN overrides, tests)
+
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool* p = new HostPool();  // never destroyed: no join at process exit
+        return *p;
+    }
+    void submit(std::function<void()> f) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            q_.push_back(std::move(f));
+        }
+        cv_.notify_one();
+    }
+
+  private:
+    HostPool() {
+        int n = (int)std::thread::hardware_concurrency();
+        if (const char* e = std::getenv("TM_HOST_THREADS")) n = std::atoi(e);
+        n_ = std::max(1, std::min(n, 32));
+        for (int i = 0; i < n_; ++i) std::thread([this] { run(); }).detach();
+    }
+    void run() {
+        for (;;) {
+            std::function<void()> f;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return !q_.empty(); });
+                f = std::move(q_.front());
+                q_.pop_front();
+            }
+            f();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    int n_ = 1;
+};
+
+struct PackPiece {
+    std::atomic<uint32_t> left{0};
+};
+struct PackJob {
+    const int64_t* t = nullptr;
+    uint64_t m = 0;
+    uint32_t* off = nullptr;   // pinned staging
+    int64_t* base = nullptr;   // pinned staging, one per kPackBlock edges
+    std::unique_ptr<PackPiece[]> piece;
+    uint64_t pieces = 0;
+    std::atomic<uint32_t> bad{0};
+    std::mutex mu;
+    std::condition_variable cv;
+    void wait_piece(uint64_t i) {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return piece[i].left.load(std::memory_order_acquire) == 0; });
+    }
+    void wait_all() {
+        for (uint64_t i = 0; i < pieces; ++i) wait_piece(i);
+    }
+};
+
+// offsets of one block from its first timestamp; a second pass from the
+// block's minimum when an edge falls outside [t0, t0 + 2^32)
+bool pack_block(const int64_t* t, uint64_t cnt, uint32_t* off, int64_t* base) {
+    const int64_t t0 = t[0];
+    uint64_t over = 0;
+    for (uint64_t i = 0; i < cnt; ++i) {
+        const uint64_t d = (uint64_t)t[i] - (uint64_t)t0;  // wraps for t[i] < t0: caught by the range test
+        off[i] = (uint32_t)d;
+        over |= d >> 32;
+    }
+    *base = t0;
+    if (!over) return true;
+    int64_t lo = t0, hi = t0;
+    for (uint64_t i = 0; i < cnt; ++i) {
+        lo = std::min(lo, t[i]);
+        hi = std::max(hi, t[i]);
+    }
+    if ((uint64_t)hi - (uint64_t)lo > 0xFFFFFFFFull) return false;
+    for (uint64_t i = 0; i < cnt; ++i) off[i] = (uint32_t)((uint64_t)t[i] - (uint64_t)lo);
+    *base = lo;
+    return true;
+}
+
+void pack_start(PackJob& J) {
+    J.pieces = (J.m + kPackPiece - 1) / kPackPiece;
+    J.piece.reset(new PackPiece[J.pieces]);
+    J.bad.store(0);
+    for (uint64_t p = 0; p < J.pieces; ++p) {
+        const uint64_t b = p * kPackPiece, e = std::min(J.m, b + kPackPiece);
+        J.piece[p].left.store((uint32_t)((e - b + kPackTask - 1) / kPackTask));
+    }
+    HostPool& pool = HostPool::get();
+    for (uint64_t b = 0; b < J.m; b += kPackTask) {
+        const uint64_t e = std::min(J.m, b + kPackTask);
+        PackJob* j = &J;
+        pool.submit([j, b, e] {
+            for (uint64_t x = b; x < e; x += kPackBlock) {
+                const uint64_t c = std::min(kPackBlock, e - x);
+                if (!pack_block(j->t + x, c, j->off + x, j->base + x / kPackBlock)) j->bad.store(1);
+            }
+            PackPiece& pc = j->piece[b / kPackPiece];
+            if (pc.left.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+                std::lock_guard<std::mutex> lk(j->mu);
+                j->cv.notify_all();
+            }
+        });
+    }
+}
+
+struct PieceWait {
+    PackJob* job;
+    uint64_t piece;
+};
+void CUDART_CB pack_wait_cb(void* arg) {
+    PieceWait* w = static_cast<PieceWait*>(arg);
+    w->job->wait_piece(w->piece);
+}
+
+__global__ void unpack_t_kernel(const uint32_t* __restrict__ off, const int64_t* __restrict__ base, uint64_t m,
+                                int64_t* __restrict__ t) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        t[i] = base[i / kPackBlock] + (int64_t)off[i];
+}
+
+bool pack_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TM_H2D_PACK");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+uint64_t pack_min_edges() {
+    static const uint64_t v = [] {
+        const char* e = std::getenv("TM_H2D_PACK_MIN");
+        return e ? (uint64_t)std::strtoull(e, nullptr, 10) : kPackMinEdges;
+    }();
+    return v;
+}
+std::atomic<uint64_t> g_h2d_bytes{0};  // input bytes the last submitted batch put on the wire
+
 struct AsyncResult {
     int rc = TM_OK;
     std::string err;
@@ -893,6 +1055,16 @@ struct AsyncSlot {
     cudaEvent_t copied = nullptr, done = nullptr;
     bool busy = false, pending = false;
     bool deferred = false;  // large batch: census not yet issued (runs when the next batch is submitted)
+    // packed timestamps (large batches): pinned staging, device copies, the running job
+    uint32_t* h_off = nullptr;
+    int64_t* h_base = nullptr;
+    uint32_t* d_off = nullptr;
+    int64_t* d_base = nullptr;
+    uint64_t pack_cap = 0;
+    bool packed = false;
+    const int64_t* host_t = nullptr;
+    std::unique_ptr<PackJob> job;
+    std::vector<PieceWait> waits;
     uint64_t ticket = 0, m = 0, n = 0;
     cudaStream_t s = nullptr;
     tm_run_config cfg;
@@ -908,10 +1080,17 @@ struct AsyncPipe {
         for (auto& sl : slot) {
             if (sl.copied) cudaEventDestroy(sl.copied);
             if (sl.done) cudaEventDestroy(sl.done);
+            if (sl.job) sl.job->wait_all();
             if (sl.ds) {
                 cudaFree(sl.ds);
                 cudaFree(sl.dd);
                 cudaFree(sl.dt);
+            }
+            if (sl.h_off) {
+                cudaFreeHost(sl.h_off);
+                cudaFreeHost(sl.h_base);
+                cudaFree(sl.d_off);
+                cudaFree(sl.d_base);
             }
         }
         if (copy) cudaStreamDestroy(copy);
@@ -927,6 +1106,17 @@ thread_local AsyncPipe g_async;
 void run_deferred(AsyncSlot& sl) {
     if (!sl.deferred) return;
     sl.deferred = false;
+    if (sl.packed) {
+        sl.job->wait_all();  // long done: the copy stream already waited for every piece
+        if (sl.job->bad.load()) {  // a block's span did not fit 32 bits: plain copy of t
+            AsyncPipe& A = g_async;
+            TM_CUDA(cudaMemcpyAsync(sl.dt, sl.host_t, sl.m * sizeof(int64_t), cudaMemcpyHostToDevice, A.copy));
+            TM_CUDA(cudaEventRecord(sl.copied, A.copy));
+            TM_CUDA(cudaStreamWaitEvent(sl.s, sl.copied, 0));
+            g_h2d_bytes.fetch_add(sl.m * sizeof(int64_t));
+        }
+        sl.packed = false;
+    }
     const int rc = tm_count_edges(sl.ds, sl.dd, sl.dt, sl.m, sl.n, 1, sl.s, &sl.cfg, &sl.res.raw, sl.res.census,
                                   nullptr);
     sl.res.rc = rc;
@@ -1448,10 +1638,69 @@ int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t
         sl.res = AsyncResult();
         // copy stream: wait until the slot's previous census stopped reading it
         TM_CUDA(cudaStreamWaitEvent(A.copy, sl.done, 0));
+        const bool eager = m && !(m <= kReplayMaxEdges && replay_enabled());
+        bool pack = eager && m >= pack_min_edges() && pack_enabled();
+        if (pack && sl.pack_cap < m) {  // pinned staging + device copies of the packed timestamps
+            if (sl.h_off) {
+                cudaFreeHost(sl.h_off);
+                cudaFreeHost(sl.h_base);
+                cudaFree(sl.d_off);
+                cudaFree(sl.d_base);
+                sl.h_off = nullptr;
+                sl.pack_cap = 0;
+            }
+            const uint64_t nb = (m + kPackBlock - 1) / kPackBlock;
+            if (cudaHostAlloc(&sl.h_off, m * sizeof(uint32_t), cudaHostAllocDefault) == cudaSuccess &&
+                cudaHostAlloc(&sl.h_base, nb * sizeof(int64_t), cudaHostAllocDefault) == cudaSuccess &&
+                cudaMalloc(&sl.d_off, m * sizeof(uint32_t)) == cudaSuccess &&
+                cudaMalloc(&sl.d_base, nb * sizeof(int64_t)) == cudaSuccess) {
+                sl.pack_cap = m;
+            } else {  // no room for the staging: plain copies
+                cudaGetLastError();
+                if (sl.h_off) cudaFreeHost(sl.h_off);
+                if (sl.h_base) cudaFreeHost(sl.h_base);
+                if (sl.d_off) cudaFree(sl.d_off);
+                if (sl.d_base) cudaFree(sl.d_base);
+                sl.h_off = nullptr;
+                sl.h_base = nullptr;
+                sl.d_off = nullptr;
+                sl.d_base = nullptr;
+                pack = false;
+            }
+        }
+        sl.packed = pack;
+        sl.host_t = t;
+        if (pack) {  // workers pack t while src / dst are on the wire
+            sl.job.reset(new PackJob());
+            sl.job->t = t;
+            sl.job->m = m;
+            sl.job->off = sl.h_off;
+            sl.job->base = sl.h_base;
+            pack_start(*sl.job);
+        }
         if (m) {
             TM_CUDA(cudaMemcpyAsync(sl.ds, src, m * sizeof(uint32_t), cudaMemcpyHostToDevice, A.copy));
             TM_CUDA(cudaMemcpyAsync(sl.dd, dst, m * sizeof(uint32_t), cudaMemcpyHostToDevice, A.copy));
-            TM_CUDA(cudaMemcpyAsync(sl.dt, t, m * sizeof(int64_t), cudaMemcpyHostToDevice, A.copy));
+            if (pack) {
+                const uint64_t nb = (m + kPackBlock - 1) / kPackBlock;
+                sl.waits.resize(sl.job->pieces);
+                for (uint64_t p = 0; p < sl.job->pieces; ++p) {
+                    const uint64_t b = p * kPackPiece, e = std::min(m, b + kPackPiece);
+                    sl.waits[p] = PieceWait{sl.job.get(), p};
+                    TM_CUDA(cudaLaunchHostFunc(A.copy, pack_wait_cb, &sl.waits[p]));
+                    TM_CUDA(cudaMemcpyAsync(sl.d_off + b, sl.h_off + b, (e - b) * sizeof(uint32_t),
+                                            cudaMemcpyHostToDevice, A.copy));
+                }
+                TM_CUDA(cudaMemcpyAsync(sl.d_base, sl.h_base, nb * sizeof(int64_t), cudaMemcpyHostToDevice, A.copy));
+                TM_LAUNCH("unpack_t", A.copy, unpack_t_kernel,
+                          (unsigned)std::min<uint64_t>((m + 255) / 256, (uint64_t)sm_count() * 8), 256, 0, sl.d_off, sl.d_base, m, sl.dt);
+                g_h2d_bytes.store(m * 12 + nb * 8);
+            } else {
+                TM_CUDA(cudaMemcpyAsync(sl.dt, t, m * sizeof(int64_t), cudaMemcpyHostToDevice, A.copy));
+                g_h2d_bytes.store(m * 16);
+            }
+        } else {
+            g_h2d_bytes.store(0);
         }
         TM_CUDA(cudaEventRecord(sl.copied, A.copy));
         // the previous batch's deferred census runs now, while this copy is in
@@ -1466,7 +1715,7 @@ int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t
             }
         }
         TM_CUDA(cudaStreamWaitEvent(s, sl.copied, 0));
-        if (m && !(m <= kReplayMaxEdges && replay_enabled())) {
+        if (eager) {
             sl.deferred = true;  // eager (host-synchronous) count: issued with the next submission or the wait
             *ticket = tk;
             return TM_OK;
@@ -1489,6 +1738,12 @@ int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t
         *ticket = tk;
         return TM_OK;
     });
+}
+
+int tm_async_h2d_bytes(uint64_t* bytes) {
+    if (!bytes) return TM_ERR_INVALID;
+    *bytes = g_h2d_bytes.load();
+    return TM_OK;
 }
 
 int tm_count_edges_wait(uint64_t ticket, tm_counters* raw, uint64_t* census36) {

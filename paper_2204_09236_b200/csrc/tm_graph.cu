@@ -95,7 +95,9 @@ constexpr int kPackEdges = kSortTile / 2;
 // of the time sort's packed keys tkeys[p].  Endpoints are clamped into range
 // in every pass: a speculatively replayed build of input the verdict later
 // rejects stays in bounds.
-template <bool kNarrow, bool kPermuted>
+// kScan: validate, reduce and count only -- nothing is written: the node
+// sort's first pass then reads the caller's arrays itself (RawEdgeLoad).
+template <bool kNarrow, bool kPermuted, bool kScan = false>
 __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
     const uint32_t* __restrict__ perm, const uint64_t* __restrict__ tkeys, uint64_t kmask,
     const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, const int64_t* __restrict__ t,
@@ -136,10 +138,11 @@ __global__ void __launch_bounds__(kPackBlock) pack_edges_kernel(
                     ea = ea < n ? ea : 0u;
                     eb = eb < n ? eb : 0u;
                 }
-                if (!(kNarrow && vals)) E[p] = EdgeCodec<kNarrow>::make(tp, ea, eb, tmin);  // gathered (wide only)
-                reinterpret_cast<ulonglong2*>(keys)[p] =
-                    make_ulonglong2(((uint64_t)a << 32) | (2 * k), ((uint64_t)b << 32) | (2 * k + 1));
-                if (kNarrow && vals) {  // the gathers' payload travels with the node sort
+                if (!kScan && !(kNarrow && vals)) E[p] = EdgeCodec<kNarrow>::make(tp, ea, eb, tmin);  // gathered (wide only)
+                if (!kScan)
+                    reinterpret_cast<ulonglong2*>(keys)[p] =
+                        make_ulonglong2(((uint64_t)a << 32) | (2 * k), ((uint64_t)b << 32) | (2 * k + 1));
+                if (!kScan && kNarrow && vals) {  // the gathers' payload travels with the node sort
                     const uint64_t rel = (uint64_t)(kPermuted ? t[k] : tp) - (uint64_t)tmin;
                     reinterpret_cast<ulonglong2*>(vals)[p] =
                         make_ulonglong2((rel << 32) | b, (rel << 32) | a | kDirBit);
@@ -220,45 +223,92 @@ __global__ void gather_s_kernel(const typename EdgeCodec<kNarrow>::Rec* __restri
     }
 }
 
-// gather_s for narrow records whose payload travelled with the node sort
-// (pack_edges vals: (t - tmin) << 32 | other | side << 31): a streaming pass,
-// no random read of the edge records.  A random 8-byte read costs a whole
-// 128-byte line from HBM on B200 (profiles/gatherbench.cu: 1.2G gathers of a
-// 4.8 GB array = 155 GB of DRAM reads), so carrying 8 more bytes through each
-// sort pass is cheaper than gathering them once.
-__global__ void gather_s_pay_kernel(const uint64_t* __restrict__ skeys, const uint64_t* __restrict__ svals,
-                                    uint64_t R, uint64_t n, uint32_t* __restrict__ off,
-                                    uint32_t* __restrict__ S_tn, uint32_t* __restrict__ S_nbr,
-                                    uint32_t* __restrict__ S_ord, uint32_t* __restrict__ S_node,
-                                    uint32_t* __restrict__ omask,
-                                    uint32_t* __restrict__ t32n, uint32_t* __restrict__ t1kn) {
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R;
-         base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t q = base + threadIdx.x;
-        uint32_t out = 0;
-        if (q < R) {
-            const uint64_t key = __ldcs(skeys + q);
-            const uint64_t val = __ldcs(svals + q);
-            const uint32_t r = (uint32_t)key;
-            const uint32_t p = r >> 1, side = r & 1u;
-            const uint32_t u = (uint32_t)(key >> 32), x = (uint32_t)val & kNodeMask;
-            const uint32_t trel = (uint32_t)(val >> 32);
-            const int64_t prev = q ? (int64_t)(skeys[q - 1] >> 32) : -1;
-            for (int64_t y = prev + 1; y <= (int64_t)u; ++y) off[y] = (uint32_t)q;
-            if (q == R - 1)
-                for (int64_t y = (int64_t)u + 1; y <= (int64_t)n; ++y) off[y] = (uint32_t)R;
-            out = side ^ 1u;
-            __stcs(S_tn + q, trel);
-            __stcs(S_ord + q, p);
-            __stcs(S_node + q, u);
-            __stcs(S_nbr + q, x | (side << 31));
-            if ((q & 31) == 0) {
-                t32n[q >> 5] = trel;
-                if ((q & 1023) == 0) t1kn[q >> 10] = trel;
-            }
+// The node sort's first pass over time-ordered input with a narrow time span:
+// a tile's kSortTile / 2 edges come straight from the caller's src / dst / t
+// (three TMA copies into the tile's key area, 8 bytes per record instead of
+// the 16 of packed keys + payloads) and each thread forms its records' keys
+// node << 32 | 2k + side and payloads (t - tmin) << 32 | other | side << 31 in
+// registers, exactly as pack_edges would have written them.  Needs 16-byte
+// aligned arrays (the tile starts are multiples of 6 KB).
+struct RawEdgeLoad {
+    static constexpr bool kOn = true;
+    static constexpr uint32_t kEdges = kSortTile / 2;
+    const uint32_t* src;
+    const uint32_t* dst;
+    const int64_t* t;
+    uint64_t m, n;
+    int64_t tmin;
+    __device__ __forceinline__ void issue(unsigned char* stage, uint32_t tile, uint64_t* bar) const {
+        const uint64_t e0 = (uint64_t)tile * kEdges;
+        const uint32_t cnt = (uint32_t)(m - e0 < kEdges ? m - e0 : kEdges);
+        uint32_t* ss = reinterpret_cast<uint32_t*>(stage);
+        uint32_t* sd = ss + kEdges;
+        int64_t* st = reinterpret_cast<int64_t*>(stage + kEdges * 8);
+        const uint32_t b4 = (cnt * 4u) & ~15u, b8 = (cnt * 8u) & ~15u;
+        mbar_expect_tx(bar, 2 * b4 + b8);
+        if (b4) {
+            tma_load_1d(ss, src + e0, b4, bar);
+            tma_load_1d(sd, dst + e0, b4, bar);
         }
-        const unsigned ob = __ballot_sync(0xffffffffu, out);
-        if ((threadIdx.x & 31) == 0 && q < R) omask[q >> 5] = ob;
+        if (b8) tma_load_1d(st, t + e0, b8, bar);
+        // the last tile's tail (under 16 bytes per array) by plain loads
+        for (uint32_t i = b4 / 4; i < cnt; ++i) {
+            ss[i] = src[e0 + i];
+            sd[i] = dst[e0 + i];
+        }
+        for (uint32_t i = b8 / 8; i < cnt; ++i) st[i] = t[e0 + i];
+    }
+    __device__ __forceinline__ void fetch(const unsigned char* stage, uint32_t tile, uint32_t i, uint64_t& key,
+                                          uint64_t& val) const {
+        const uint32_t* ss = reinterpret_cast<const uint32_t*>(stage);
+        const uint32_t e = i >> 1, side = i & 1u;
+        uint32_t a = ss[e], b = ss[kEdges + e];
+        a = a < n ? a : 0u;  // clamped like pack_edges: a rejected batch stays in bounds
+        b = b < n ? b : 0u;
+        const uint64_t rel = (uint64_t)reinterpret_cast<const int64_t*>(stage + kEdges * 8)[e] - (uint64_t)tmin;
+        const uint32_t r = 2u * (tile * kEdges + e) + side;
+        key = ((uint64_t)(side ? b : a) << 32) | r;
+        val = (rel << 32) | (side ? (a | kDirBit) : b);
+    }
+};
+
+// S for narrow records: the payload (t - tmin) << 32 | other | side << 31
+// travelled with the node sort's keys (node << 32 | 2k + side), and the sort's
+// LAST downsweep pass hands each (position, key, payload) to this emitter,
+// which writes the S arrays and the S_t fences in place of the sorted keys and
+// payloads -- no gather of the edge records (a random 8-byte read costs a whole
+// 128-byte line from HBM on B200, profiles/gatherbench.cu) and no separate
+// pass over the sorted data either (gather_s: 38 GB of traffic at config 4).
+struct SEmit {
+    static constexpr bool kOn = true;
+    uint32_t* S_tn;
+    uint32_t* S_nbr;
+    uint32_t* S_ord;
+    uint32_t* S_node;
+    uint32_t* t32n;
+    uint32_t* t1kn;
+    __device__ __forceinline__ void operator()(uint32_t q, uint64_t key, uint64_t val) const {
+        const uint32_t r = (uint32_t)key, trel = (uint32_t)(val >> 32);
+        __stcs(S_tn + q, trel);
+        __stcs(S_ord + q, r >> 1);
+        __stcs(S_node + q, (uint32_t)(key >> 32));
+        __stcs(S_nbr + q, ((uint32_t)val & kNodeMask) | ((r & 1u) << 31));
+        if ((q & 31) == 0) {  // the fences (tm_internal.cuh fenced_lower_bound)
+            t32n[q >> 5] = trel;
+            if ((q & 1023) == 0) t1kn[q >> 10] = trel;
+        }
+    }
+};
+
+// CSR offsets from the node boundaries of S_node (the emitter's output)
+__global__ void s_offsets_kernel(const uint32_t* __restrict__ S_node, uint64_t R, uint64_t n,
+                                 uint32_t* __restrict__ off) {
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = __ldcs(S_node + q);
+        const int64_t prev = q ? (int64_t)S_node[q - 1] : -1;
+        for (int64_t y = prev + 1; y <= (int64_t)u; ++y) off[y] = (uint32_t)q;
+        if (q == R - 1)
+            for (int64_t y = (int64_t)u + 1; y <= (int64_t)n; ++y) off[y] = (uint32_t)R;
     }
 }
 
@@ -289,38 +339,40 @@ __global__ void degree_class_kernel(const uint32_t* __restrict__ off, uint64_t n
 // hub's block holds only its records to the few hubs above it.
 __global__ void orient_kernel(const uint32_t* __restrict__ S_node, const uint32_t* __restrict__ S_nbr,
                               const uint8_t* __restrict__ cls, uint64_t R, uint32_t* __restrict__ xmask,
-                              uint32_t* __restrict__ fmask) {
+                              uint32_t* __restrict__ fmask, uint32_t* __restrict__ omask) {
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < R; base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t q = base + threadIdx.x;
-        uint32_t fwd = 0, bwd = 0;
+        uint32_t fwd = 0, bwd = 0, out = 0;
         if (q < R) {
-            const uint32_t u = __ldcs(S_node + q), x = __ldcs(S_nbr + q) & kNodeMask;
+            const uint32_t u = __ldcs(S_node + q), nbr = __ldcs(S_nbr + q), x = nbr & kNodeMask;
             const uint32_t du = cls[u], dx = cls[x];
             fwd = (dx > du || (dx == du && x > u)) ? 1u : 0u;
             bwd = fwd ^ 1u;
+            out = (nbr >> 31) ^ 1u;  // the outward records (the star pass's P_o prefix)
         }
         const unsigned fb = __ballot_sync(0xffffffffu, fwd), bb = __ballot_sync(0xffffffffu, bwd);
+        const unsigned ob = __ballot_sync(0xffffffffu, out);
         if ((threadIdx.x & 31) == 0 && q < R) {
             fmask[q >> 5] = fb;
             xmask[q >> 5] = bb;
+            omask[q >> 5] = ob;
         }
     }
 }
 
 // (narrow records: also the payload (t - tmin) << 32 | max | dir_rel_min << 31
 // for gather_p_pay, read from S_t / S_nbr)
-__global__ void pair_keys_kernel(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ S_nbr,
-                                 const uint32_t* __restrict__ S_tn,
+__global__ void pair_keys_kernel(const uint32_t* __restrict__ S_node, const uint32_t* __restrict__ S_ord,
+                                 const uint32_t* __restrict__ S_nbr, const uint32_t* __restrict__ S_tn,
                                  const uint32_t* __restrict__ xmask, const uint32_t* __restrict__ xpref,
                                  uint64_t R, uint64_t* __restrict__ pkeys, uint64_t* __restrict__ pvals) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R; q += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t word = xmask[q >> 5], bit = 1u << (q & 31);
         if (!(word & bit)) continue;
-        const uint64_t key = __ldcs(skeys + q);
         const uint32_t nbr = __ldcs(S_nbr + q);
-        const uint32_t u = (uint32_t)(key >> 32), x = nbr & kNodeMask;
+        const uint32_t u = __ldcs(S_node + q), x = nbr & kNodeMask;
         const uint32_t j = xpref[q >> 5] + __popc(word & (bit - 1u));
-        pkeys[j] = ((uint64_t)x << 32) | ((uint32_t)key >> 1);
+        pkeys[j] = ((uint64_t)x << 32) | __ldcs(S_ord + q);
         // u is the upper endpoint; the lower one x is the source iff u's record is inward
         if (pvals) pvals[j] = ((uint64_t)__ldcs(S_tn + q) << 32) | u | ((~nbr) & kDirBit);
     }
@@ -412,59 +464,71 @@ __global__ void __launch_bounds__(256) gather_p_kernel(const uint64_t* __restric
     }
 }
 
-// gather_p for narrow records: the payload (t - tmin) << 32 | max |
-// dir_rel_min << 31 came through the pair sort with the keys (min << 32 | p)
-__global__ void __launch_bounds__(256) gather_p_pay_kernel(const uint64_t* __restrict__ pkeys,
-                                                           const uint64_t* __restrict__ pvals, uint64_t m,
-                                                           uint32_t* __restrict__ P_tn, uint32_t* __restrict__ P_ord,
-                                                           uint32_t* __restrict__ P_min, uint32_t* __restrict__ P_max,
-                                                           uint32_t* __restrict__ P_w, uint64_t n,
-                                                           uint32_t* __restrict__ pofs, uint32_t* __restrict__ dmask,
-                                                           uint32_t* __restrict__ gmask, uint32_t* __restrict__ max32,
-                                                           uint32_t* __restrict__ max1k, uint32_t* __restrict__ t32n,
-                                                           uint32_t* __restrict__ t1kn) {
+// P for narrow records: the pair sort's last pass hands (position, key =
+// min << 32 | p, payload = (t - tmin) << 32 | max | dir_rel_min << 31) to this
+// emitter, which writes the P columns, the direction bit of P_w and the P
+// fences; p_flags_kernel then adds what needs a record's neighbours (group
+// first / last flags, pofs, the direction and group-first bitmasks) from
+// P_min / P_max / P_w -- 16 bytes per edge instead of gather_p's 36.
+struct PEmit {
+    static constexpr bool kOn = true;
+    uint32_t* P_tn;
+    uint32_t* P_ord;
+    uint32_t* P_min;
+    uint32_t* P_max;
+    uint32_t* P_w;
+    uint32_t* max32;
+    uint32_t* max1k;
+    uint32_t* t32n;
+    uint32_t* t1kn;
+    __device__ __forceinline__ void operator()(uint32_t k, uint64_t key, uint64_t val) const {
+        const uint32_t trel = (uint32_t)(val >> 32), b = (uint32_t)val & kNodeMask;
+        __stcs(P_tn + k, trel);
+        __stcs(P_ord + k, (uint32_t)key);
+        P_min[k] = (uint32_t)(key >> 32);  // re-read by p_flags_kernel
+        P_max[k] = b;
+        P_w[k] = (uint32_t)val & kDirBit;
+        if ((k & 31) == 0) {
+            max32[k >> 5] = b;
+            t32n[k >> 5] = trel;
+            if ((k & 1023) == 0) {
+                max1k[k >> 10] = b;
+                t1kn[k >> 10] = trel;
+            }
+        }
+    }
+};
+
+__global__ void __launch_bounds__(256) p_flags_kernel(const uint32_t* __restrict__ P_min,
+                                                      const uint32_t* __restrict__ P_max, uint64_t m, uint64_t n,
+                                                      uint32_t* __restrict__ P_w, uint32_t* __restrict__ pofs,
+                                                      uint32_t* __restrict__ dmask, uint32_t* __restrict__ gmask) {
     __shared__ uint32_t s_a[258], s_b[258];
     const int tid = threadIdx.x;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m;
-         base += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m; base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = base + tid;
-        uint32_t a = 0, b = 0, p = 0, dir = 0, trel = 0;
+        uint32_t a = 0, b = 0, dir = 0;
         bool first = false;
         if (k < m) {
-            const uint64_t key = __ldcs(pkeys + k), val = __ldcs(pvals + k);
-            p = (uint32_t)key;
-            a = (uint32_t)(key >> 32);
-            b = (uint32_t)val & kNodeMask;
-            dir = ((uint32_t)val) >> 31;
-            trel = (uint32_t)(val >> 32);
+            a = P_min[k];
+            b = P_max[k];
+            dir = P_w[k] >> 31;
             s_a[tid + 1] = a;
             s_b[tid + 1] = b;
         }
         if (tid == 0 && k > 0 && k - 1 < m) {
-            s_a[0] = (uint32_t)(pkeys[k - 1] >> 32);
-            s_b[0] = (uint32_t)pvals[k - 1] & kNodeMask;
+            s_a[0] = P_min[k - 1];
+            s_b[0] = P_max[k - 1];
         }
         if (tid == (int)blockDim.x - 1 && k + 1 < m) {
-            s_a[tid + 2] = (uint32_t)(pkeys[k + 1] >> 32);
-            s_b[tid + 2] = (uint32_t)pvals[k + 1] & kNodeMask;
+            s_a[tid + 2] = P_min[k + 1];
+            s_b[tid + 2] = P_max[k + 1];
         }
         __syncthreads();
         if (k < m) {
             first = k == 0 || s_a[tid] != a || s_b[tid] != b;
             const bool last = k + 1 == m || s_a[tid + 2] != a || s_b[tid + 2] != b;
-            __stcs(P_tn + k, trel);
-            __stcs(P_ord + k, p);
-            __stcs(P_min + k, a);
-            __stcs(P_max + k, b);
             __stcs(P_w + k, (dir << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u));
-            if ((k & 31) == 0) {
-                max32[k >> 5] = b;
-                t32n[k >> 5] = trel;
-                if ((k & 1023) == 0) {
-                    max1k[k >> 10] = b;
-                    t1kn[k >> 10] = trel;
-                }
-            }
             const int64_t prev = k == 0 ? -1 : (int64_t)s_a[tid];
             for (int64_t x = prev + 1; x <= (int64_t)a; ++x) pofs[x] = (uint32_t)k;
             if (k + 1 == m)
@@ -655,6 +719,14 @@ void release_side(DeviceGraph& g) {
 
 }  // namespace
 
+static bool raw_first_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TM_RAW_FIRST");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d_dst, const int64_t* d_t,
                         uint64_t m, uint64_t n, BuildWorkspace* ws, BuildVerdict* h_async) {
     cudaStream_t s = g.stream;
@@ -706,9 +778,17 @@ BuildPlan build_prepare(DeviceGraph& g, const uint32_t* d_src, const uint32_t* d
     *hv = h_st;
     TM_CUDA(cudaMemcpyAsync(d_st, hv, sizeof(h_st), cudaMemcpyHostToDevice, s));
     if (m) {
-        TM_LAUNCH("pack_edges", s, (pack_edges_kernel<true, false>), grid_for(m, kPackEdges), kPackBlock, 0, nullptr,
-                  nullptr, 0ull, d_src, d_dst, d_t, m, n, (int64_t)0, reinterpret_cast<NarrowEdge*>(pl.E), pl.nk0,
-                  pl.nv0, pl.c0, pl.ntiles, d_st);
+        // scan only when the node sort can read the arrays itself (RawEdgeLoad)
+        pl.raw_first = raw_first_enabled() && ((reinterpret_cast<uintptr_t>(d_src) | reinterpret_cast<uintptr_t>(d_dst) |
+                                                reinterpret_cast<uintptr_t>(d_t)) & 15u) == 0;
+        if (pl.raw_first)
+            TM_LAUNCH("pack_edges", s, (pack_edges_kernel<true, false, true>), grid_for(m, kPackEdges), kPackBlock, 0,
+                      nullptr, nullptr, 0ull, d_src, d_dst, d_t, m, n, (int64_t)0,
+                      reinterpret_cast<NarrowEdge*>(pl.E), pl.nk0, pl.nv0, pl.c0, pl.ntiles, d_st);
+        else
+            TM_LAUNCH("pack_edges", s, (pack_edges_kernel<true, false>), grid_for(m, kPackEdges), kPackBlock, 0,
+                      nullptr, nullptr, 0ull, d_src, d_dst, d_t, m, n, (int64_t)0,
+                      reinterpret_cast<NarrowEdge*>(pl.E), pl.nk0, pl.nv0, pl.c0, pl.ntiles, d_st);
     }
     TM_CUDA(cudaMemcpyAsync(hv, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, s));
     if (h_async) return pl;  // verdict read later (plan_from_verdict)
@@ -874,7 +954,12 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         }
         auto EW = reinterpret_cast<WideEdge*>(E);
         // narrow records: the S payload travels with the keys (no gather)
-        if (narrow) radix_sort<uint64_t, uint64_t>(nk0, nv0, nk1, nv1, R, 32, 32 + nb, s, c0);
+        const SEmit semit{g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_t32.n, g.S_t1k.n};
+        if (narrow && !repack && pl.raw_first)
+            radix_sort<uint64_t, uint64_t, SEmit, RawEdgeLoad>(nk0, nv0, nk1, nv1, R, 32, 32 + nb, s, c0, semit,
+                                                               RawEdgeLoad{d_src, d_dst, d_t, m, n, tmin});
+        else if (narrow)
+            radix_sort<uint64_t, uint64_t, SEmit>(nk0, nv0, nk1, nv1, R, 32, 32 + nb, s, c0, semit);
         else radix_sort<uint64_t>(nk0, nullv, nk1, nullv2, R, 32, 32 + nb, s, c0);
         if (pl.owned) dfree(c0, s);
         TM_CUDA(cudaMemsetAsync(g.S_omask + (nw - 1), 0, sizeof(uint32_t), s));
@@ -883,9 +968,8 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         uint32_t* xpref = dalloc<uint32_t>(nw + 1, s);
         TM_CUDA(cudaMemsetAsync(xmask + (nw - 1), 0, sizeof(uint32_t), s));
         g.cls = dalloc<uint8_t>(n + 1, s);  // kept: the pair lookups pick a pair's lower endpoint by it
-        if (narrow)
-            TM_LAUNCH("gather_s", s, gather_s_pay_kernel, grid_for(R), 256, 0, nk0, nv0, R, n, g.off, g.S_t.n,
-                      g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_t32.n, g.S_t1k.n);
+        if (narrow)  // the sort's last pass wrote S; the CSR offsets from its node column
+            TM_LAUNCH("s_offsets", s, s_offsets_kernel, grid_for(R), 256, 0, g.S_node, R, n, g.off);
         else
             TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, EW, tmin, nk0, R, n, g.off,
                       g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_t32.w, g.S_t32.n,
@@ -893,7 +977,8 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         // orientation by (degree class, id): forward mask (triangle pass) and
         // upper-side mask (pair keys)
         TM_LAUNCH("degree_class", s, degree_class_kernel, grid_for(n), 256, 0, g.off, n, g.cls);
-        TM_LAUNCH("orient", s, orient_kernel, grid_for(R), 256, 0, g.S_node, g.S_nbr, g.cls, R, xmask, g.S_fmask);
+        TM_LAUNCH("orient", s, orient_kernel, grid_for(R), 256, 0, g.S_node, g.S_nbr, g.cls, R, xmask, g.S_fmask,
+                  g.S_omask);
         // outward prefix (stars) and upper-side prefix (pair keys) in one scan
         exclusive_scan_to<uint64_t>(PopcLoad2{g.S_omask, xmask}, nw, SplitStore2{g.S_opref, xpref}, s);
 
@@ -907,7 +992,8 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         uint64_t* pv0 = narrow ? dalloc<uint64_t>(m + kSortPad, s) : nullptr;
         uint64_t* pv0_alloc = pv0;
         uint64_t* pv1 = nv1;  // the node sort's second value buffer
-        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, nk0, g.S_nbr, g.S_t.n, xmask, xpref, R, pk0,
+        TM_LAUNCH("pair_keys", s, pair_keys_kernel, grid_for(R), 256, 0, g.S_node, g.S_ord, g.S_nbr, g.S_t.n, xmask, xpref, R,
+                  pk0,
                   pv0);
 
         // the forward sequences (degree orientation) only need S and the
@@ -925,9 +1011,11 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         dfree(xmask, s);
         dfree(xpref, s);
         if (narrow) {
-            radix_sort<uint64_t, uint64_t>(pk0, pv0, pk1, pv1, m, 32, 32 + nb, s);
-            TM_LAUNCH("gather_p", s, gather_p_pay_kernel, grid_for(m), 256, 0, pk0, pv0, m, g.P_t.n, g.P_ord, g.P_min,
-                      g.P_max, g.P_w, n, g.pofs, g.P_dmask, g.P_gmask, g.P_max32, g.P_max1k, g.P_t32.n, g.P_t1k.n);
+            radix_sort<uint64_t, uint64_t, PEmit>(pk0, pv0, pk1, pv1, m, 32, 32 + nb, s, nullptr,
+                                                  PEmit{g.P_t.n, g.P_ord, g.P_min, g.P_max, g.P_w, g.P_max32,
+                                                        g.P_max1k, g.P_t32.n, g.P_t1k.n});
+            TM_LAUNCH("p_flags", s, p_flags_kernel, grid_for(m), 256, 0, g.P_min, g.P_max, m, n, g.P_w, g.pofs,
+                      g.P_dmask, g.P_gmask);
         } else {
             radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);
             TM_LAUNCH("gather_p", s, gather_p_kernel<false>, grid_for(m), 256, 0, pk0, m, EW, tmin, g.P_t.w, g.P_t.n,

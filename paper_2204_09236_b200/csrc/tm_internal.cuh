@@ -484,6 +484,7 @@ struct BuildPlan {
     uint64_t E_bytes = 0;
     uint32_t ntiles = 0;
     bool narrow = true, unsorted = false, owned = true;
+    bool raw_first = false;  // build_prepare only scanned: nk0 / nv0 hold no packed records yet
     int64_t tmin = 0, tmax = 0;
 };
 // h_async (pinned) set: the verdict is copied there without waiting and the

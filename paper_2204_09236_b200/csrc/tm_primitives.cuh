@@ -532,9 +532,30 @@ __device__ __forceinline__ uint32_t wlms_bit(uint32_t d, uint32_t bit) {
 #define TM_RANK_MATCH_ROUNDS_NARROW 1  // the same for passes of <= 4 digit bits
 #endif
 
+// Last-pass output policy: NoEmit writes the sorted keys (and values); an
+// emitter with kOn = true receives (sorted position, key, value) instead and
+// writes its consumer's arrays directly -- the pass that would re-read the
+// sorted keys + values only to split them into those arrays disappears.
+struct NoEmit {
+    static constexpr bool kOn = false;
+    __device__ __forceinline__ void operator()(uint32_t, uint64_t, uint64_t) const {}
+};
+
+// First-pass input policy: NoLoad streams the key (and value) arrays; a loader
+// with kOn = true fills a tile's stage from the producer's own data instead
+// (issue: the TMA copies of tile `tile` into `stage`, completing on `bar`) and
+// forms each element's (key, value) in registers (fetch) -- the pass that
+// would write the keys + values only for this pass to read them disappears.
+struct NoLoad {
+    static constexpr bool kOn = false;
+    __device__ __forceinline__ void issue(unsigned char*, uint32_t, uint64_t*) const {}
+    __device__ __forceinline__ void fetch(const unsigned char*, uint32_t, uint32_t, uint64_t&, uint64_t&) const {}
+};
+
 // NBITS: digit bits of this pass (8, or 4 for a short last pass); digits are
 // (key >> shift) & dmask with dmask < 2^NBITS
-template <typename K, typename V, bool kVals, int BLOCK, int ITEMS, int MINB, int NBITS>
+template <typename K, typename V, bool kVals, int BLOCK, int ITEMS, int MINB, int NBITS, typename Emit = NoEmit,
+          typename Load = NoLoad>
 __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __restrict__ kin,
                                                                    const V* __restrict__ vin,
                                                                    K* __restrict__ kout,
@@ -542,7 +563,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
                                                                    int shift, uint32_t dmask,
                                                                    const uint32_t* __restrict__ tile_offsets,
                                                                    uint32_t ntiles,
-                                                                   const uint32_t* __restrict__ totals) {
+                                                                   const uint32_t* __restrict__ totals,
+                                                                   Emit emit, Load load) {
     constexpr int NW = BLOCK / 32, TILE = BLOCK * ITEMS;
     constexpr int kMatchRounds = NBITS >= 8 ? TM_RANK_MATCH_ROUNDS : TM_RANK_MATCH_ROUNDS_NARROW;
     constexpr int RADIX = 1 << NBITS;
@@ -574,9 +596,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
         const uint32_t kbytes = (uint32_t)((cnt * sizeof(K) + 15) & ~uint64_t(15));
         const uint32_t vbytes = kVals ? (uint32_t)((cnt * sizeof(V) + 15) & ~uint64_t(15)) : 0u;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[s], kbytes + vbytes);
-        tma_load_1d(stage_keys(s), kin + base, kbytes, &bar[s]);
-        if (kVals) tma_load_1d(stage_vals(s), vin + base, vbytes, &bar[s]);
+        if constexpr (Load::kOn) {
+            load.issue(tma_smem + s * STAGE_BYTES, tile, &bar[s]);
+        } else {
+            mbar_expect_tx(&bar[s], kbytes + vbytes);
+            tma_load_1d(stage_keys(s), kin + base, kbytes, &bar[s]);
+            if (kVals) tma_load_1d(stage_vals(s), vin + base, vbytes, &bar[s]);
+        }
     };
     // count rows exist for this pass's digits only (<= dmask)
     // global base of each of this thread's digits (digits tid * DPT + k)
@@ -625,8 +651,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
 #pragma unroll
         for (int r = 0; r < ITEMS; ++r) {
             const uint32_t i = w * (ITEMS * 32) + r * 32 + lane;
-            key[r] = sk[i];
-            if (kVals) val[r] = sv[i];
+            if constexpr (Load::kOn) {
+                uint64_t lk = 0, lv = 0;
+                load.fetch(tma_smem + s * STAGE_BYTES, tile, i, lk, lv);
+                key[r] = (K)lk;
+                if (kVals) val[r] = (V)lv;
+            } else {
+                key[r] = sk[i];
+                if (kVals) val[r] = sv[i];
+            }
             dig[r] = i < tile_n ? ((uint32_t)(key[r] >> shift) & dmask) : kNone;
         }
         // Peer masks (lanes holding the same digit).  match.any costs ~60 clocks
@@ -703,8 +736,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) radix_downsweep_tma(const K* __re
             if (i < tile_n) {
                 const K k = sk[i];
                 const uint32_t dest = dglob[(uint32_t)(k >> shift) & dmask] + i;
-                kout[dest] = k;
-                if (kVals) vout[dest] = sv[i];
+                if constexpr (Emit::kOn) {
+                    emit(dest, (uint64_t)k, kVals ? (uint64_t)sv[i] : 0ull);
+                } else {
+                    kout[dest] = k;
+                    if (kVals) vout[dest] = sv[i];
+                }
             }
         }
         __syncthreads();
@@ -718,13 +755,14 @@ constexpr int kSortBlock = 256, kSortItems = 12, kSortMinBlocks = 3, kSortTile =
 
 // one downsweep instantiation: sets its shared-memory limit and caches its
 // occupancy on first use, then launches a persistent grid
-template <typename K, typename V, bool kVals, int BLOCK, int ITEMS, int MINB, int NBITS>
+template <typename K, typename V, bool kVals, int BLOCK, int ITEMS, int MINB, int NBITS, typename Emit = NoEmit,
+          typename Load = NoLoad>
 void launch_downsweep(const K* kin, const V* vin, K* kout, V* vout, uint64_t n, int shift,
                       uint32_t dmask, const uint32_t* offs, uint32_t ntiles, const uint32_t* totals,
-                      cudaStream_t s) {
+                      cudaStream_t s, Emit emit = Emit(), Load load = Load()) {
     constexpr int TILE = BLOCK * ITEMS;
     constexpr size_t smem = 2 * TILE * (sizeof(K) + (kVals ? sizeof(V) : 0));
-    auto kern = radix_downsweep_tma<K, V, kVals, BLOCK, ITEMS, MINB, NBITS>;
+    auto kern = radix_downsweep_tma<K, V, kVals, BLOCK, ITEMS, MINB, NBITS, Emit, Load>;
     static int per_sm = 0;  // resident blocks per SM
     if (per_sm == 0) {
         TM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -733,13 +771,14 @@ void launch_downsweep(const K* kin, const V* vin, K* kout, V* vout, uint64_t n, 
     }
     const unsigned pgrid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * per_sm);
     TM_LAUNCH("radix_downsweep", s, kern, pgrid, BLOCK, smem, kin, vin, kout, vout, n, shift, dmask, offs,
-              ntiles, totals);
+              ntiles, totals, emit, load);
 }
 
 // one pass configuration: tile = BLOCK * ITEMS keys
-template <typename K, typename V, int BLOCK, int ITEMS, int MINB>
+template <typename K, typename V, int BLOCK, int ITEMS, int MINB, typename Emit = NoEmit, typename Load = NoLoad>
 void radix_sort_cfg(K*& keys, V*& vals, K*& keys_alt, V*& vals_alt, uint64_t n,
-                    int bit_lo, int bit_hi, cudaStream_t s, const uint32_t* first_counts) {
+                    int bit_lo, int bit_hi, cudaStream_t s, const uint32_t* first_counts, Emit emit = Emit(),
+                    Load load = Load()) {
     constexpr int TILE = BLOCK * ITEMS;
     const bool with_vals = vals != nullptr;
     const int passes = radix_passes(bit_hi - bit_lo);
@@ -767,9 +806,17 @@ void radix_sort_cfg(K*& keys, V*& vals, K*& keys_alt, V*& vals_alt, uint64_t n,
         V* vout = with_vals ? vals_alt : nullptr;
 // (u64 keys + u64 payloads: 96 KB of tile stages per block, so 2 resident
 // blocks per SM and the register budget of 2)
+#define TM_DOWNSWEEP_AS(HV, NB, E, L, ev, lv)                                                                   \
+    launch_downsweep<K, V, HV, BLOCK, ITEMS, (HV && sizeof(K) + sizeof(V) >= 16) ? 2 : MINB, NB, E, L>(         \
+        keys, vin, keys_alt, vout, n, shift, dmask, offs, ntiles, totals, s, ev, lv)
 #define TM_DOWNSWEEP(HV, NB)                                                                                    \
-    launch_downsweep<K, V, HV, BLOCK, ITEMS, (HV && sizeof(K) + sizeof(V) >= 16) ? 2 : MINB, NB>(           \
-        keys, vin, keys_alt, vout, n, shift, dmask, offs, ntiles, totals, s)
+    do {                                                                                                        \
+        const bool el = Emit::kOn && p == passes - 1, lf = Load::kOn && p == 0;                                 \
+        if (el && lf) TM_DOWNSWEEP_AS(HV, NB, Emit, Load, emit, load);                                          \
+        else if (el) TM_DOWNSWEEP_AS(HV, NB, Emit, NoLoad, emit, NoLoad());                                     \
+        else if (lf) TM_DOWNSWEEP_AS(HV, NB, NoEmit, Load, NoEmit(), load);                                     \
+        else TM_DOWNSWEEP_AS(HV, NB, NoEmit, NoLoad, NoEmit(), NoLoad());                                       \
+    } while (0)
         if (with_vals) {
             if (width <= 4) TM_DOWNSWEEP(true, 4);
             else if (width <= 6) TM_DOWNSWEEP(true, 6);
@@ -780,13 +827,15 @@ void radix_sort_cfg(K*& keys, V*& vals, K*& keys_alt, V*& vals_alt, uint64_t n,
             vals = vals_alt;
             vals_alt = tv;
         } else {
-            if (width <= 4) TM_DOWNSWEEP(false, 4);
-            else if (width <= 6) TM_DOWNSWEEP(false, 6);
-            else if (width <= 7) TM_DOWNSWEEP(false, 7);
-            else if (width <= 8) TM_DOWNSWEEP(false, 8);
-            else TM_DOWNSWEEP(false, 9);
+            if (Emit::kOn || Load::kOn) throw tm_error(1, "radix_sort: emitters and loaders sort key + value");
+            if (width <= 4) TM_DOWNSWEEP_AS(false, 4, NoEmit, NoLoad, NoEmit(), NoLoad());
+            else if (width <= 6) TM_DOWNSWEEP_AS(false, 6, NoEmit, NoLoad, NoEmit(), NoLoad());
+            else if (width <= 7) TM_DOWNSWEEP_AS(false, 7, NoEmit, NoLoad, NoEmit(), NoLoad());
+            else if (width <= 8) TM_DOWNSWEEP_AS(false, 8, NoEmit, NoLoad, NoEmit(), NoLoad());
+            else TM_DOWNSWEEP_AS(false, 9, NoEmit, NoLoad, NoEmit(), NoLoad());
         }
 #undef TM_DOWNSWEEP
+#undef TM_DOWNSWEEP_AS
         shift += width;
         K* tk = keys;
         keys = keys_alt;
@@ -799,16 +848,39 @@ void radix_sort_cfg(K*& keys, V*& vals, K*& keys_alt, V*& vals_alt, uint64_t n,
 // [bit_lo, bit_hi).  Buffers need kSortPad elements of slack (TMA tile loads
 // round up to 16 bytes).  On return keys/vals point at the sorted data; the *_alt
 // pointers at the scratch halves (pointers may be swapped).
-template <typename K, typename V = uint32_t>
+// (no pass runs for n <= 1 or an empty bit range: the input order is the output)
+template <typename K, typename V, typename Emit>
+__global__ void emit_in_order_kernel(const K* __restrict__ keys, const V* __restrict__ vals, uint64_t n, Emit emit) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        emit((uint32_t)i, (uint64_t)keys[i], vals ? (uint64_t)vals[i] : 0ull);
+}
+
+// With an emitter the last pass hands every (position, key, value) to it
+// instead of writing the sorted arrays (which are then scratch).
+// With a loader the first pass reads its tiles through it (keys / vals are
+// scratch from the start; n > 1 and a non-empty bit range are the caller's to
+// ensure).
+template <typename K, typename V = uint32_t, typename Emit = NoEmit, typename Load = NoLoad>
 void radix_sort(K*& keys, V*& vals, K*& keys_alt, V*& vals_alt, uint64_t n,
-                int bit_lo, int bit_hi, cudaStream_t s, const uint32_t* first_counts = nullptr) {
-    if (n <= 1 || bit_hi <= bit_lo) return;
+                int bit_lo, int bit_hi, cudaStream_t s, const uint32_t* first_counts = nullptr, Emit emit = Emit(),
+                Load load = Load()) {
+    if (n <= 1 || bit_hi <= bit_lo) {
+        if constexpr (Emit::kOn) {
+            if (n) {
+                const K* kc = keys;
+                const V* vc = vals;
+                TM_LAUNCH("radix_downsweep", s, (emit_in_order_kernel<K, V, Emit>),
+                          (unsigned)std::min<uint64_t>((n + 255) / 256, 1024), 256, 0, kc, vc, n, emit);
+            }
+        }
+        return;
+    }
     // 256 threads x 12 keys, 3 blocks per SM: the same downsweep time as 8
     // keys x 4 blocks with a third fewer tiles, so the count matrix's upsweep
     // and row scan shrink (profiles/sortbench.cu sweeps 256/512 threads x
     // 4-16 keys on B200: 20M node keys 0.457 -> 0.448 ms)
-    radix_sort_cfg<K, V, kSortBlock, kSortItems, kSortMinBlocks>(keys, vals, keys_alt, vals_alt, n, bit_lo, bit_hi, s,
-                                                 first_counts);
+    radix_sort_cfg<K, V, kSortBlock, kSortItems, kSortMinBlocks, Emit, Load>(keys, vals, keys_alt, vals_alt, n, bit_lo,
+                                                                             bit_hi, s, first_counts, emit, load);
 }
 
 inline int bit_width_u64(uint64_t x) {

@@ -127,8 +127,8 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         if (x1 <= x0) return;
         const uint32_t n1 = p_dir_before(P, x1) - p_dir_before(P, x0);  // dir_rel_min = 1
         const uint32_t n0 = (x1 - x0) - n1;
-        c[type * 2 + flip] += n0;
-        c[type * 2 + (flip ^ 1u)] += n1;
+        c[type * 2] += flip ? n1 : n0;  // static cell indices: c[] stays in registers
+        c[type * 2 + 1] += flip ? n0 : n1;
     };
     add_range(0, k1, k2e);
     if (ti <= t_last) {
@@ -190,7 +190,10 @@ constexpr int kWedgeScan = 8;
 #define TM_CACHE_MINB 4
 #endif
 constexpr int kGroupCache = 1 << TM_GCACHE_BITS;  // entries per warp (dynamic shared memory)
-constexpr uint32_t kGroupCacheMinWindow = 64;  // shorter windows repeat few groups: plain path
+#ifndef TM_CACHE_MINWIN
+#define TM_CACHE_MINWIN 64
+#endif
+constexpr uint32_t kGroupCacheMinWindow = TM_CACHE_MINWIN;  // shorter windows repeat few groups: plain path
 
 #ifndef TM_WEDGE_MINB
 #define TM_WEDGE_MINB 5
@@ -491,8 +494,8 @@ __global__ void __launch_bounds__(256, kCache ? TM_CACHE_MINB : TM_LONG_MINB) tr
                     if (x1 <= x0) return;
                     const uint32_t n1 = d1 - d0;
                     const uint32_t n0 = (x1 - x0) - n1;
-                    c[type * 2 + flip] += n0;
-                    c[type * 2 + (flip ^ 1u)] += n1;
+                    c[type * 2] += flip ? n1 : n0;  // static cell indices: c[] stays in registers
+                    c[type * 2 + 1] += flip ? n0 : n1;
                 };
                 const uint32_t d1 = p_dir_before(P, k1), d3 = p_dir_before(P, k3);
                 add_range(0, k1, d1, k2e, k2e == e.k2 ? e.d2 : p_dir_before(P, k2e));
@@ -523,6 +526,98 @@ __global__ void __launch_bounds__(256, kCache ? TM_CACHE_MINB : TM_LONG_MINB) tr
 #endif
         misses = warp_sum(misses);
         if (lane == 0 && misses && stats) atomicAdd((unsigned long long*)&stats[5], (unsigned long long)misses);
+    }
+    wc.flush(cells, 24, 24);
+    my_wedges = warp_sum(my_wedges);
+    if (lane == 0 && my_wedges && stats) atomicAdd((unsigned long long*)&stats[4], (unsigned long long)my_wedges);
+    __syncthreads();
+    flush_cells(cells, 24, out, kAccCarry);
+}
+
+// ---- long windows of at most kGroupCacheMinWindow records: flattened ------
+//
+// tri_long_kernel<false> strides one window with the warp's lanes, so a
+// window of 9..31 records leaves most lanes idle (ncu: 14.5 of 32 threads
+// active per instruction at config 4, delta 3600).  tri_mid_kernel takes 32
+// first edges per warp (one per lane: its window length by a short binary
+// search), scans the lengths and walks the concatenated wedge space 32 wedges
+// per step -- every lane holds a wedge until the warp's last step; a wedge's
+// owner is found by a five-step shuffle search over the scanned lengths.
+#ifndef TM_MID_FLAT
+#define TM_MID_FLAT 1
+#endif
+__global__ void __launch_bounds__(256, TM_LONG_MINB) tri_mid_kernel(PView P, TimeArr FT,
+                                                       const uint32_t* __restrict__ FN,
+                                                       const uint32_t* __restrict__ FO,
+                                                       const uint32_t* __restrict__ Fnode,
+                                                       const uint32_t* __restrict__ Foff,
+                                                       int64_t delta, int64_t t_last,
+                                                       const uint32_t* __restrict__ list,
+                                                       const uint32_t* __restrict__ lcount,
+                                                       const unsigned long long* __restrict__ pt_wsum,
+                                                       uint64_t gend_min, unsigned long long* queue,
+                                                       uint64_t* out, uint64_t* stats) {
+    __shared__ unsigned long long cells[48];
+    zero_cells(cells, 24);
+    __syncthreads();
+    WarpCells wc;
+    const uint32_t cnt = lcount[0];  // the long list (front of the buffer)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && stats) atomicAdd((unsigned long long*)&stats[3], (unsigned long long)cnt);
+    if (!P.gend || *pt_wsum < gend_min) P.gend = nullptr;  // group ends not built
+    P.pt_keys = nullptr;
+    uint32_t my_wedges = 0;
+    const int lane = threadIdx.x & 31;
+    for (;;) {  // 32 first edges per warp from the queue
+        const uint64_t base = warp_take(queue, 32);
+        if (base >= cnt) break;
+        uint32_t i = 0, len = 0;
+        if (base + lane < cnt) {
+            i = list[base + lane];
+            const uint32_t end = Foff[Fnode[i] + 1];
+            const TimeKey limk = FT.key_upto(sat_add(FT[i], delta));  // in-window: t_j <= t_i + delta
+            // first record past the window (the filter saw it end within
+            // kGroupCacheMinWindow records; searched on if it does not)
+            uint32_t lo = i + 1, hi = end - lo > kGroupCacheMinWindow ? lo + kGroupCacheMinWindow : end;
+            const uint32_t cap = hi;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (FT.below(mid, limk)) lo = mid + 1; else hi = mid;
+            }
+            if (lo == cap && cap < end) {
+                hi = end;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (FT.below(mid, limk)) lo = mid + 1; else hi = mid;
+                }
+            }
+            len = lo - (i + 1);
+        }
+        const uint32_t incl = warp_inclusive_scan(len);
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - len;
+        for (uint32_t x0 = 0; x0 < total; x0 += 32) {
+            const uint32_t x = x0 + lane;
+            int o = 0;  // the first lane whose scanned length exceeds x
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, incl, o + step - 1);
+                if (v <= x) o += step;
+            }
+            const uint32_t io = __shfl_sync(0xffffffffu, i, o);
+            const uint32_t so = __shfl_sync(0xffffffffu, excl, o);
+            uint32_t c[6] = {0, 0, 0, 0, 0, 0};
+            int cb = 0;
+            bool wedge = false;
+            if (x < total) {
+                const uint32_t j = io + 1 + (x - so);
+                if ((FN[io] & kNodeMask) != (FN[j] & kNodeMask)) {
+                    wedge = true;
+                    cb = wedge_counts(P, FT, FN, FO, io, j, delta, t_last, c);
+                    ++my_wedges;
+                }
+            }
+            wc.add6(wedge, cb, c, cells, 24);
+        }
     }
     wc.flush(cells, 24, 24);
     my_wedges = warp_sum(my_wedges);
@@ -737,8 +832,8 @@ __global__ void __launch_bounds__(256, TM_CACHE_MINB) tri_window_kernel(PView P,
                                 if (x1 <= x0) return;
                                 const uint32_t n1 = d1 - d0;
                                 const uint32_t n0 = (x1 - x0) - n1;
-                                c[type * 2 + flip] += n0;
-                                c[type * 2 + (flip ^ 1u)] += n1;
+                                c[type * 2] += flip ? n1 : n0;  // static cell indices: c[] stays in registers
+                                c[type * 2 + 1] += flip ? n0 : n1;
                             };
                             if (k1 < k2e) add_range(0, k1, p_dir_before(P, k1), k2e, k2e == e.k2 ? e.d2 : p_dir_before(P, k2e));
                             if (ti <= t_last) {
@@ -998,9 +1093,14 @@ void tri_work_stage(const DeviceGraph& g, const Forward& f, TriStage& ts, int64_
         pv.pt_vals = ts.pt + pc;
         pv.pt_mask = pc - 1;
     }
+#if TM_MID_FLAT
+    TM_LAUNCH("tri_long", st, tri_mid_kernel, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord, f.node,
+              f.off, ts.delta, t_last, ts.long_list, lcount, ts.wsum, gend_min, ts.queue + 1, d_out, d_stats);
+#else
     TM_LAUNCH("tri_long", st, tri_long_kernel<false>, (unsigned)cap, 256, 0, pv, f.t.view(g.tbase), f.nbr, f.ord,
               f.node, f.off, ts.delta, t_last, ts.long_list, ts.long_cap, lcount, ts.wsum, min_wedges, gend_min,
               ts.queue + 1, d_out, d_stats);
+#endif
     constexpr size_t kCacheBytes = 8 * (size_t)kGroupCache * sizeof(GroupCacheEntry);
     static const bool cache_attr = [] {
         TM_CUDA(cudaFuncSetAttribute(tri_long_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

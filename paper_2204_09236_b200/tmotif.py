@@ -143,6 +143,7 @@ def lib():
     L.tm_count_edges_async.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint64, VP, C.POINTER(_RunConfig),
                                        C.POINTER(C.c_uint64)]
     L.tm_count_edges_wait.argtypes = [C.c_uint64, C.POINTER(_Counters), VP]
+    L.tm_async_h2d_bytes.argtypes = [C.POINTER(C.c_uint64)]
     L.tm_count_edges_time_slice.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint64, C.c_int, VP,
                                             C.POINTER(_RunConfig), C.c_int, C.c_int64, C.c_int, C.c_int64,
                                             C.POINTER(_Counters), C.POINTER(_Timings)]
@@ -976,6 +977,16 @@ class PendingCensus:
         if raw_out is not None:
             raw_out[:56] = self._raw
         return self._census
+
+
+def async_h2d_bytes() -> int:
+    """Input bytes the last count_edges_async batch put on the host->device
+    link (tm_async_h2d_bytes: 16 per edge, 12 when its timestamps travel
+    packed)."""
+    L = lib()
+    b = C.c_uint64(0)
+    _raise(L.tm_async_h2d_bytes(C.byref(b)), L)
+    return int(b.value)
 
 
 def count_edges_async(n: int, src, dst, t, config: RunConfig, stream: Optional[int] = None) -> PendingCensus:

@@ -36,7 +36,7 @@ if os.environ.get("KTIMES"):  # per-kernel CUDA-event times of one more census
     torch.cuda.synchronize()
     tm.kernel_timing(enable=False)
     names = ["star_filter", "star_locate", "star_work", "tri_filter", "tri_wedge", "tri_long", "radix_upsweep", "radix_downsweep",
-             "radix_scan", "scan", "gather_s", "gather_p", "forward_scatter", "pack_edges", "pair_keys", "time_keys",
+             "radix_scan", "scan", "gather_s", "s_offsets", "gather_p", "p_flags", "forward_scatter", "pack_edges", "pair_keys", "time_keys",
              "forward_off", "group_end", "pair_table", "tri_gate", "orient", "degree_class"]
     kt = {k: round(tm.kernel_time(k)[0], 3) for k in names if tm.kernel_time(k)[1]}
     print(json.dumps({"config": name, "delta": delta, "kernel_ms": kt}), flush=True)

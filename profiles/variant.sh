@@ -13,5 +13,5 @@ for f in paper_2204_09236_b200/csrc/*.cu; do
   $NVCC $FLAGS -c -o $o $f &
 done
 wait
-$NVCC -gencode arch=compute_100a,code=sm_100a -shared -o ab/lib_$name.so $objs -lcudart
+$NVCC -gencode arch=compute_100a,code=sm_100a -shared -o ab/lib_$name.so $objs -lcudart -lpthread
 echo ab/lib_$name.so

@@ -51,6 +51,11 @@ def test_bench_contract_and_multirank(cuda):
                       "powerlaw_1m_10m", "--steps", "3", "--warmup", "3", "--dist-backend", "gloo",
                       "--same-device", "--partition", part])
         assert multi["n_gpus"] == world and multi["census"] == gold, (world, part)
+    # the NCCL counter all-reduce itself, on this one GPU: world size 1 through the N>1 path
+    nccl = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                 "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--config",
+                 "powerlaw_1m_10m", "--steps", "3", "--warmup", "3", "--force-dist", "--no-cpu-baseline"])
+    assert nccl["n_gpus"] == 1 and nccl["census"] == gold
     ref = _run([sys.executable, "bench.py", "--impl", "reference", "--config", "uniform_10k_200k", "--steps", "1",
                 "--warmup", "3"]) if os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libtmotif_ref.so")) else None
     if ref is not None:
