@@ -289,10 +289,12 @@ struct SEmit {
     uint32_t* t1kn;
     __device__ __forceinline__ void operator()(uint32_t q, uint64_t key, uint64_t val) const {
         const uint32_t r = (uint32_t)key, trel = (uint32_t)(val >> 32);
-        __stcs(S_tn + q, trel);
-        __stcs(S_ord + q, r >> 1);
-        __stcs(S_node + q, (uint32_t)(key >> 32));
-        __stcs(S_nbr + q, ((uint32_t)val & kNodeMask) | ((r & 1u) << 31));
+        // plain stores: a digit run ends inside a sector that the neighbouring
+        // tile's run completes, so the lines should stay in L2 until then
+        S_tn[q] = trel;
+        S_ord[q] = r >> 1;
+        S_node[q] = (uint32_t)(key >> 32);
+        S_nbr[q] = ((uint32_t)val & kNodeMask) | ((r & 1u) << 31);
         if ((q & 31) == 0) {  // the fences (tm_internal.cuh fenced_lower_bound)
             t32n[q >> 5] = trel;
             if ((q & 1023) == 0) t1kn[q >> 10] = trel;
@@ -300,15 +302,32 @@ struct SEmit {
     }
 };
 
-// CSR offsets from the node boundaries of S_node (the emitter's output)
+// CSR offsets from the node boundaries of S_node (the emitter's output):
+// four records per thread (one 16-byte load)
 __global__ void s_offsets_kernel(const uint32_t* __restrict__ S_node, uint64_t R, uint64_t n,
                                  uint32_t* __restrict__ off) {
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < R; q += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t u = __ldcs(S_node + q);
-        const int64_t prev = q ? (int64_t)S_node[q - 1] : -1;
-        for (int64_t y = prev + 1; y <= (int64_t)u; ++y) off[y] = (uint32_t)q;
-        if (q == R - 1)
-            for (int64_t y = (int64_t)u + 1; y <= (int64_t)n; ++y) off[y] = (uint32_t)R;
+    const uint64_t quads = (R + 3) / 4;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < quads; x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q0 = x * 4;
+        uint32_t u[4];
+        if (q0 + 4 <= R) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(S_node) + x);
+            u[0] = v.x; u[1] = v.y; u[2] = v.z; u[3] = v.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) u[k] = q0 + k < R ? S_node[q0 + k] : 0u;
+        }
+        int64_t prev = q0 ? (int64_t)S_node[q0 - 1] : -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint64_t q = q0 + k;
+            if (q < R) {
+                for (int64_t y = prev + 1; y <= (int64_t)u[k]; ++y) off[y] = (uint32_t)q;
+                if (q == R - 1)
+                    for (int64_t y = (int64_t)u[k] + 1; y <= (int64_t)n; ++y) off[y] = (uint32_t)R;
+                prev = u[k];
+            }
+        }
     }
 }
 
@@ -483,8 +502,8 @@ struct PEmit {
     uint32_t* t1kn;
     __device__ __forceinline__ void operator()(uint32_t k, uint64_t key, uint64_t val) const {
         const uint32_t trel = (uint32_t)(val >> 32), b = (uint32_t)val & kNodeMask;
-        __stcs(P_tn + k, trel);
-        __stcs(P_ord + k, (uint32_t)key);
+        P_tn[k] = trel;
+        P_ord[k] = (uint32_t)key;
         P_min[k] = (uint32_t)(key >> 32);  // re-read by p_flags_kernel
         P_max[k] = b;
         P_w[k] = (uint32_t)val & kDirBit;
@@ -503,44 +522,74 @@ __global__ void __launch_bounds__(256) p_flags_kernel(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ P_max, uint64_t m, uint64_t n,
                                                       uint32_t* __restrict__ P_w, uint32_t* __restrict__ pofs,
                                                       uint32_t* __restrict__ dmask, uint32_t* __restrict__ gmask) {
-    __shared__ uint32_t s_a[258], s_b[258];
-    const int tid = threadIdx.x;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m; base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = base + tid;
-        uint32_t a = 0, b = 0, dir = 0;
-        bool first = false;
-        if (k < m) {
-            a = P_min[k];
-            b = P_max[k];
-            dir = P_w[k] >> 31;
-            s_a[tid + 1] = a;
-            s_b[tid + 1] = b;
+    // four records per thread (16-byte loads); the records either side of the
+    // quad come from the neighbouring threads' lines (cache hits); eight lanes
+    // assemble one word of each bitmask
+    const uint64_t quads = (m + 3) / 4, span = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t rounds = (quads + span - 1) / span;  // whole warps stay in the loop (shuffles)
+    const int lane = threadIdx.x & 31;
+    for (uint64_t r = 0; r < rounds; ++r) {
+        const uint64_t x = r * span + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const uint64_t k0 = x * 4;
+        uint32_t a[6], b[6], w[4];  // [0] = record k0 - 1, [5] = record k0 + 4
+        uint32_t dn = 0, gn = 0;
+        if (k0 < m) {
+            if (k0 + 4 <= m) {
+                const uint4 va = *(reinterpret_cast<const uint4*>(P_min) + x), vb = *(reinterpret_cast<const uint4*>(P_max) + x);
+                const uint4 vw = *(reinterpret_cast<const uint4*>(P_w) + x);
+                a[1] = va.x; a[2] = va.y; a[3] = va.z; a[4] = va.w;
+                b[1] = vb.x; b[2] = vb.y; b[3] = vb.z; b[4] = vb.w;
+                w[0] = vw.x; w[1] = vw.y; w[2] = vw.z; w[3] = vw.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const bool in = k0 + i < m;
+                    a[1 + i] = in ? P_min[k0 + i] : 0u;
+                    b[1 + i] = in ? P_max[k0 + i] : 0u;
+                    w[i] = in ? P_w[k0 + i] : 0u;
+                }
+            }
+            a[0] = k0 ? P_min[k0 - 1] : 0u;
+            b[0] = k0 ? P_max[k0 - 1] : 0u;
+            a[5] = k0 + 4 < m ? P_min[k0 + 4] : 0u;
+            b[5] = k0 + 4 < m ? P_max[k0 + 4] : 0u;
+            uint32_t wo[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint64_t k = k0 + i;
+                wo[i] = 0;
+                if (k < m) {
+                    const bool first = k == 0 || a[i] != a[1 + i] || b[i] != b[1 + i];
+                    const bool last = k + 1 == m || a[2 + i] != a[1 + i] || b[2 + i] != b[1 + i];
+                    const uint32_t dir = w[i] >> 31;
+                    wo[i] = (dir << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u);
+                    dn |= dir << i;
+                    gn |= (first ? 1u : 0u) << i;
+                    const int64_t prev = k == 0 ? -1 : (int64_t)a[i];
+                    for (int64_t y = prev + 1; y <= (int64_t)a[1 + i]; ++y) pofs[y] = (uint32_t)k;
+                    if (k + 1 == m)
+                        for (int64_t y = (int64_t)a[1 + i] + 1; y <= (int64_t)n; ++y) pofs[y] = (uint32_t)m;
+                }
+            }
+            if (k0 + 4 <= m) {
+                __stcs(reinterpret_cast<uint4*>(P_w) + x, make_uint4(wo[0], wo[1], wo[2], wo[3]));
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (k0 + i < m) P_w[k0 + i] = wo[i];
+            }
         }
-        if (tid == 0 && k > 0 && k - 1 < m) {
-            s_a[0] = P_min[k - 1];
-            s_b[0] = P_max[k - 1];
+        dn <<= 4 * (lane & 7);
+        gn <<= 4 * (lane & 7);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            dn |= __shfl_xor_sync(0xffffffffu, dn, o);
+            gn |= __shfl_xor_sync(0xffffffffu, gn, o);
         }
-        if (tid == (int)blockDim.x - 1 && k + 1 < m) {
-            s_a[tid + 2] = P_min[k + 1];
-            s_b[tid + 2] = P_max[k + 1];
+        if ((lane & 7) == 0 && k0 < m) {
+            dmask[k0 >> 5] = dn;
+            gmask[k0 >> 5] = gn;
         }
-        __syncthreads();
-        if (k < m) {
-            first = k == 0 || s_a[tid] != a || s_b[tid] != b;
-            const bool last = k + 1 == m || s_a[tid + 2] != a || s_b[tid + 2] != b;
-            __stcs(P_w + k, (dir << 31) | (first ? kPFirst : 0u) | (last ? kPLast : 0u));
-            const int64_t prev = k == 0 ? -1 : (int64_t)s_a[tid];
-            for (int64_t x = prev + 1; x <= (int64_t)a; ++x) pofs[x] = (uint32_t)k;
-            if (k + 1 == m)
-                for (int64_t x = (int64_t)a + 1; x <= (int64_t)n; ++x) pofs[x] = (uint32_t)m;
-        }
-        const unsigned db = __ballot_sync(0xffffffffu, k < m && dir);
-        const unsigned gb = __ballot_sync(0xffffffffu, first);
-        if ((tid & 31) == 0 && k < m) {
-            dmask[k >> 5] = db;
-            gmask[k >> 5] = gb;
-        }
-        __syncthreads();
     }
 }
 
@@ -969,7 +1018,7 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
         TM_CUDA(cudaMemsetAsync(xmask + (nw - 1), 0, sizeof(uint32_t), s));
         g.cls = dalloc<uint8_t>(n + 1, s);  // kept: the pair lookups pick a pair's lower endpoint by it
         if (narrow)  // the sort's last pass wrote S; the CSR offsets from its node column
-            TM_LAUNCH("s_offsets", s, s_offsets_kernel, grid_for(R), 256, 0, g.S_node, R, n, g.off);
+            TM_LAUNCH("s_offsets", s, s_offsets_kernel, grid_for((R + 3) / 4), 256, 0, g.S_node, R, n, g.off);
         else
             TM_LAUNCH("gather_s", s, gather_s_kernel<false>, grid_for(R), 256, 0, EW, tmin, nk0, R, n, g.off,
                       g.S_t.w, g.S_t.n, g.S_nbr, g.S_ord, g.S_node, g.S_omask, g.S_t32.w, g.S_t32.n,
@@ -1014,7 +1063,7 @@ void build_finish(DeviceGraph& g, BuildPlan& pl, const uint32_t* d_src, const ui
             radix_sort<uint64_t, uint64_t, PEmit>(pk0, pv0, pk1, pv1, m, 32, 32 + nb, s, nullptr,
                                                   PEmit{g.P_t.n, g.P_ord, g.P_min, g.P_max, g.P_w, g.P_max32,
                                                         g.P_max1k, g.P_t32.n, g.P_t1k.n});
-            TM_LAUNCH("p_flags", s, p_flags_kernel, grid_for(m), 256, 0, g.P_min, g.P_max, m, n, g.P_w, g.pofs,
+            TM_LAUNCH("p_flags", s, p_flags_kernel, grid_for((m + 3) / 4), 256, 0, g.P_min, g.P_max, m, n, g.P_w, g.pofs,
                       g.P_dmask, g.P_gmask);
         } else {
             radix_sort<uint64_t>(pk0, nullv, pk1, nullv2, m, 32, 32 + nb, s);

@@ -86,32 +86,48 @@ __device__ __forceinline__ uint32_t p_gallop_tupper(const PView& P, uint32_t fro
 // window [k1, k4) = [t_j - delta, t_i + delta] and the type boundaries k2 =
 // (t_i, o_i), k3 = (t_j, o_j) (triangle_engine.cpp:43-51): k1 by the fenced
 // search, k2, k3, k4 each by a gallop from the previous boundary.
-__device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint32_t w, int64_t lo,
-                                               int64_t hi, int64_t ti, uint32_t oi, int64_t tj,
-                                               uint32_t oj, int64_t t_last, uint32_t c[6]) {
-#pragma unroll
-    for (int j = 0; j < 6; ++j) c[j] = 0;
+// A wedge's closing group, found (locate_closing) and counted (count_closing).
+// (Parking the located wedges in shared memory and counting them 32 at a time,
+// so that count_closing runs with every lane busy, measured slower: config 4
+// delta 3600 tri_wedge 18.5 -> 27.3 ms, tri_mid 17.4 -> 21.8 ms.)
+struct GroupRef {
+    uint32_t kb;   // first record of the v-w group
+    uint32_t aux;  // the end of its block, or (bit 31 set) the group end itself
+};
+constexpr uint32_t kGroupEndKnown = 0x80000000u;
+
+__device__ __forceinline__ bool locate_closing(const PView& P, uint32_t v, uint32_t w, GroupRef& g) {
     const bool vlow = ranks_below(P.cls, v, w);
     const uint32_t a = vlow ? v : w, b = vlow ? w : v;  // the pair's lower / upper endpoint (P block of a)
-    const uint32_t flip = vlow ? 0u : 1u;  // dir_rel_lower -> dir relative to v
-    uint32_t blk_end = P.pofs[a + 1], kb, ke = 0;
+    const uint32_t blk_end = P.pofs[a + 1];
     if (P.pt_keys && blk_end - P.pofs[a] > kTableMinBlock) {  // optional pair table (TM_PAIR_TABLE)
         const unsigned long long key = ((unsigned long long)a << 32) | b;
         uint64_t slot = pair_slot(a, b) & P.pt_mask;
         for (;;) {
             const unsigned long long kk = P.pt_keys[slot];
             if (kk == key) break;
-            if (kk == kPairEmpty) return;  // no v-w record
+            if (kk == kPairEmpty) return false;  // no v-w record
             slot = (slot + 1) & P.pt_mask;
         }
         const unsigned long long val = P.pt_vals[slot];
-        kb = (uint32_t)(val >> 32);
-        ke = kb + (uint32_t)val;
-    } else {
-        kb = p_max_lower(P, P.pofs[a], blk_end, b);
-        if (kb >= blk_end || P.max[kb] != b) return;
-        ke = P.gend ? p_group_end(P, kb) : p_max_upper(P, kb, blk_end, b);
+        g.kb = (uint32_t)(val >> 32);
+        g.aux = (g.kb + (uint32_t)val) | kGroupEndKnown;
+        return true;
     }
+    g.kb = p_max_lower(P, P.pofs[a], blk_end, b);
+    g.aux = blk_end;
+    return g.kb < blk_end && P.max[g.kb] == b;
+}
+
+__device__ __forceinline__ void count_closing(const PView& P, uint32_t v, uint32_t w, const GroupRef g, int64_t lo,
+                                              int64_t hi, int64_t ti, uint32_t oi, int64_t tj, uint32_t oj,
+                                              int64_t t_last, uint32_t c[6]) {
+    const bool vlow = ranks_below(P.cls, v, w);
+    const uint32_t flip = vlow ? 0u : 1u;  // dir_rel_lower -> dir relative to v
+    const uint32_t kb = g.kb;
+    const uint32_t ke = (g.aux & kGroupEndKnown) ? (g.aux & ~kGroupEndKnown)
+                        : P.gend                 ? p_group_end(P, kb)
+                                                 : p_max_upper(P, kb, g.aux, vlow ? w : v);
     const uint32_t k1 = p_t_lower(P, kb, ke, lo);
     const uint32_t k2 = p_gallop_rec(P, k1, ke, P.t.rec_key(ti, oi));
     const uint32_t k3 = p_gallop_rec(P, k2, ke, P.t.rec_key(tj, oj));
@@ -135,6 +151,16 @@ __device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint3
         add_range(1, k2, k3);
         add_range(2, k3, k4);
     }
+}
+
+__device__ __forceinline__ void closing_counts(const PView& P, uint32_t v, uint32_t w, int64_t lo,
+                                               int64_t hi, int64_t ti, uint32_t oi, int64_t tj,
+                                               uint32_t oj, int64_t t_last, uint32_t c[6]) {
+#pragma unroll
+    for (int j = 0; j < 6; ++j) c[j] = 0;
+    GroupRef g;
+    if (!locate_closing(P, v, w, g)) return;
+    count_closing(P, v, w, g, lo, hi, ti, oi, tj, oj, t_last, c);
 }
 
 // all wedges with first edge i in sequence arrays (T, NBR, ORD) ending at end
@@ -567,11 +593,16 @@ __global__ void __launch_bounds__(256, TM_LONG_MINB) tri_mid_kernel(PView P, Tim
     P.pt_keys = nullptr;
     uint32_t my_wedges = 0;
     const int lane = threadIdx.x & 31;
-    for (;;) {  // 32 first edges per warp from the queue
-        const uint64_t base = warp_take(queue, 32);
+    // first edges per take: 32, fewer when the list would not reach every warp
+    // (config 1 at delta 3600: a few thousand long first edges)
+    uint32_t take = 32;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    while (take > 1 && take * warps > cnt) take >>= 1;
+    for (;;) {  // `take` first edges per warp from the queue
+        const uint64_t base = warp_take(queue, take);
         if (base >= cnt) break;
         uint32_t i = 0, len = 0;
-        if (base + lane < cnt) {
+        if ((uint32_t)lane < take && base + lane < cnt) {
             i = list[base + lane];
             const uint32_t end = Foff[Fnode[i] + 1];
             const TimeKey limk = FT.key_upto(sat_add(FT[i], delta));  // in-window: t_j <= t_i + delta

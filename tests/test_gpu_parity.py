@@ -922,3 +922,27 @@ print(json.dumps(out))
         assert res[("bytes", kind)] == m * 12 + 8 * ((m + 65535) // 65536), kind
     # (the fallback's extra plain copy is added when its census is issued)
     assert res[("bytes", 3)] >= m * 12
+
+
+def test_unaligned_device_arrays_and_raw_first_pass(cuda, tm, oracle):
+    """The node sort's first pass reads 16-byte aligned src / dst / t with TMA
+    (RawEdgeLoad); arrays at odd offsets take the packed path.  Both must give
+    the oracle's census, at sizes that end inside a sort tile and on tile
+    boundaries (1536 edges per tile)."""
+    import torch
+    n, delta = 300, 200
+    for m in (1, 2, 3, 1535, 1536, 1537, 3072, 10_001):
+        g = tm.generate_random_graph(n, m, 20_000, 900 + m)
+        order = np.argsort(g.t, kind="stable")  # time-ordered input: no re-pack, the raw first pass runs
+        src, dst, tt = g.src[order], g.dst[order], g.t[order]
+        og = oracle.build_graph(n, src, dst, tt)
+        want = oracle.census(og, delta).tolist()
+        oracle.free(og)
+        for shift in (0, 1, 2, 3):
+            pad = np.zeros(shift, np.uint32)
+            s = torch.from_numpy(np.concatenate([pad, src]).view(np.int32)).cuda()[shift:]
+            d = torch.from_numpy(np.concatenate([pad, dst]).view(np.int32)).cuda()[shift:]
+            t = torch.from_numpy(np.concatenate([pad.astype(np.int64), tt])).cuda()[shift:]
+            torch.cuda.synchronize()
+            got = tm.count_edges_device(n, m, s.data_ptr(), d.data_ptr(), t.data_ptr(), tm.RunConfig(delta=delta))
+            assert got.tolist() == want, (m, shift)
