@@ -421,8 +421,9 @@ def main():
         assert (census == census_pipe).all(), "device and pipelined host paths disagree"
         h2d_bytes = tm.async_h2d_bytes()
         if h2d_bytes < m_local * 16:
-            e2e_api += ("; timestamps travel as per-block i64 bases + u32 offsets packed by host worker threads "
-                        "inside the timed region (12 B per edge on the link)")
+            per_edge = h2d_bytes // max(1, m_local)
+            e2e_api += (f"; timestamps travel as per-block i64 bases + u{(per_edge - 8) * 8} offsets packed by host "
+                        f"worker threads inside the timed region ({per_edge} B per edge on the link)")
     else:  # center ranges go through the synchronous API only
         ms_e2e = ms_e2e_sync
         e2e_api = "tm_count_edges (one batch at a time)"

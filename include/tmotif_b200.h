@@ -148,12 +148,15 @@ int tm_count_edges(const uint32_t* src, const uint32_t* dst, const int64_t* t, u
 int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t* t, uint64_t m,
                          uint64_t n, void* stream, const tm_run_config* cfg, uint64_t* ticket);
 /* Input bytes the most recently submitted tm_count_edges_async batch puts on
- * the host->device link: 16 per edge, or 12 per edge (+ 8 per 65536 edges)
- * when the batch's timestamps travel packed -- batches of >= 2^24 edges above
- * the graph-replay size are rewritten by host worker threads (TM_HOST_THREADS,
- * default all cores up to 32) as per-block i64 bases + u32 offsets into pinned
- * staging while src / dst are on the wire, and expanded on the device
- * (TM_H2D_PACK=0 copies t as it is).  Results are identical either way. */
+ * the host->device link: 16 per edge, or 10 per edge (+ 8 per 4096 edges) /
+ * 12 per edge (+ 8 per 65536 edges) when the batch's timestamps travel packed
+ * -- batches of >= 2^24 edges above the graph-replay size are rewritten by host
+ * worker threads (TM_HOST_THREADS, default all cores up to 32) as per-block i64
+ * bases + u16 offsets (u32 offsets from the first batch on that has a block of
+ * 4096 edges spanning 2^16 or more, which itself takes a plain copy of t;
+ * TM_H2D_PACK16=0 starts with u32) into pinned staging while src / dst are on
+ * the wire, and expanded on the device (TM_H2D_PACK=0 copies t as it is).
+ * Results are identical either way. */
 int tm_async_h2d_bytes(uint64_t* bytes);
 /* Blocks until the ticket's census is done and returns it (once per ticket). */
 int tm_count_edges_wait(uint64_t ticket, tm_counters* raw, uint64_t* census36);

@@ -895,7 +895,12 @@ bool complete_pending(ReplayPending& P, cudaEvent_t done, const tm_run_config* c
 // with a host function, copies it (4 bytes per edge) and one kernel expands the
 // offsets into the i64 array the census reads.  A block whose span does not fit
 // marks the batch, and its census then waits for a plain copy of t.
-constexpr uint64_t kPackBlock = 1u << 16;   // edges per base
+// A pipeline starts with u16 offsets from a base per 4096 edges (10 bytes per
+// edge on the link: a dense stream's 4096 consecutive edges span far less than
+// 2^16); the first batch with a block that does not fit takes the plain copy
+// and moves the pipeline to u32 offsets for good (TM_H2D_PACK16=0 starts there).
+constexpr uint64_t kPackBlock = 1u << 16;   // edges per base, u32 offsets
+constexpr uint64_t kPackBlock16 = 1u << 12; // edges per base, u16 offsets
 constexpr uint64_t kPackTask = 1u << 20;    // edges per worker task
 constexpr uint64_t kPackPiece = 1u << 26;   // edges per staged copy
 constexpr uint64_t kPackMinEdges = 1u << 24;  // smaller batches: plain copies (TM_H2D_PACK_MIN overrides, tests)
@@ -945,8 +950,9 @@ struct PackPiece {
 struct PackJob {
     const int64_t* t = nullptr;
     uint64_t m = 0;
-    uint32_t* off = nullptr;   // pinned staging
-    int64_t* base = nullptr;   // pinned staging, one per kPackBlock edges
+    uint32_t* off = nullptr;   // pinned staging (u16 offsets when width == 2)
+    int64_t* base = nullptr;   // pinned staging, one per kPackBlock / kPackBlock16 edges
+    int width = 4;             // bytes per offset
     std::unique_ptr<PackPiece[]> piece;
     uint64_t pieces = 0;
     std::atomic<uint32_t> bad{0};
@@ -963,23 +969,25 @@ struct PackJob {
 
 // offsets of one block from its first timestamp; a second pass from the
 // block's minimum when an edge falls outside [t0, t0 + 2^32)
-bool pack_block(const int64_t* t, uint64_t cnt, uint32_t* off, int64_t* base) {
+template <typename O>
+bool pack_block(const int64_t* t, uint64_t cnt, O* off, int64_t* base) {
+    constexpr uint64_t kMax = (uint64_t)(O)~(O)0;  // 2^k - 1: the OR of the offsets exceeds it iff one of them does
     const int64_t t0 = t[0];
     uint64_t over = 0;
     for (uint64_t i = 0; i < cnt; ++i) {
         const uint64_t d = (uint64_t)t[i] - (uint64_t)t0;  // wraps for t[i] < t0: caught by the range test
-        off[i] = (uint32_t)d;
-        over |= d >> 32;
+        off[i] = (O)d;
+        over |= d;
     }
     *base = t0;
-    if (!over) return true;
+    if (over <= kMax) return true;
     int64_t lo = t0, hi = t0;
     for (uint64_t i = 0; i < cnt; ++i) {
         lo = std::min(lo, t[i]);
         hi = std::max(hi, t[i]);
     }
-    if ((uint64_t)hi - (uint64_t)lo > 0xFFFFFFFFull) return false;
-    for (uint64_t i = 0; i < cnt; ++i) off[i] = (uint32_t)((uint64_t)t[i] - (uint64_t)lo);
+    if ((uint64_t)hi - (uint64_t)lo > kMax) return false;
+    for (uint64_t i = 0; i < cnt; ++i) off[i] = (O)((uint64_t)t[i] - (uint64_t)lo);
     *base = lo;
     return true;
 }
@@ -997,9 +1005,20 @@ void pack_start(PackJob& J) {
         const uint64_t e = std::min(J.m, b + kPackTask);
         PackJob* j = &J;
         pool.submit([j, b, e] {
-            for (uint64_t x = b; x < e; x += kPackBlock) {
-                const uint64_t c = std::min(kPackBlock, e - x);
-                if (!pack_block(j->t + x, c, j->off + x, j->base + x / kPackBlock)) j->bad.store(1);
+            if (j->width == 2) {
+                uint16_t* off16 = reinterpret_cast<uint16_t*>(j->off);
+                for (uint64_t x = b; x < e; x += kPackBlock16) {
+                    const uint64_t c = std::min(kPackBlock16, e - x);
+                    if (!pack_block(j->t + x, c, off16 + x, j->base + x / kPackBlock16)) {
+                        j->bad.store(1);
+                        break;  // the batch takes the plain copy
+                    }
+                }
+            } else {
+                for (uint64_t x = b; x < e; x += kPackBlock) {
+                    const uint64_t c = std::min(kPackBlock, e - x);
+                    if (!pack_block(j->t + x, c, j->off + x, j->base + x / kPackBlock)) j->bad.store(1);
+                }
             }
             PackPiece& pc = j->piece[b / kPackPiece];
             if (pc.left.fetch_sub(1, std::memory_order_acq_rel) == 1) {
@@ -1019,15 +1038,23 @@ void CUDART_CB pack_wait_cb(void* arg) {
     w->job->wait_piece(w->piece);
 }
 
-__global__ void unpack_t_kernel(const uint32_t* __restrict__ off, const int64_t* __restrict__ base, uint64_t m,
+template <typename O, uint64_t kBlock>
+__global__ void unpack_t_kernel(const O* __restrict__ off, const int64_t* __restrict__ base, uint64_t m,
                                 int64_t* __restrict__ t) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
-        t[i] = base[i / kPackBlock] + (int64_t)off[i];
+        t[i] = base[i / kBlock] + (int64_t)off[i];
 }
 
 bool pack_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("TM_H2D_PACK");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+bool pack16_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TM_H2D_PACK16");
         return !(e && e[0] == '0');
     }();
     return on;
@@ -1075,6 +1102,7 @@ struct AsyncPipe {
     cudaStream_t copy = nullptr;
     AsyncSlot slot[2];
     uint64_t next = 1;
+    int t_width = 2;  // bytes per packed timestamp offset: 2 until a batch does not fit, then 4
     std::vector<std::pair<uint64_t, AsyncResult>> finished;  // completed, not yet waited
     ~AsyncPipe() {
         for (auto& sl : slot) {
@@ -1108,8 +1136,9 @@ void run_deferred(AsyncSlot& sl) {
     sl.deferred = false;
     if (sl.packed) {
         sl.job->wait_all();  // long done: the copy stream already waited for every piece
-        if (sl.job->bad.load()) {  // a block's span did not fit 32 bits: plain copy of t
+        if (sl.job->bad.load()) {  // a block's span did not fit the offsets: plain copy of t
             AsyncPipe& A = g_async;
+            if (sl.job->width == 2) A.t_width = 4;  // later batches pack u32 offsets
             TM_CUDA(cudaMemcpyAsync(sl.dt, sl.host_t, sl.m * sizeof(int64_t), cudaMemcpyHostToDevice, A.copy));
             TM_CUDA(cudaEventRecord(sl.copied, A.copy));
             TM_CUDA(cudaStreamWaitEvent(sl.s, sl.copied, 0));
@@ -1649,7 +1678,7 @@ int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t
                 sl.h_off = nullptr;
                 sl.pack_cap = 0;
             }
-            const uint64_t nb = (m + kPackBlock - 1) / kPackBlock;
+            const uint64_t nb = (m + kPackBlock16 - 1) / kPackBlock16;  // room for either block size
             if (cudaHostAlloc(&sl.h_off, m * sizeof(uint32_t), cudaHostAllocDefault) == cudaSuccess &&
                 cudaHostAlloc(&sl.h_base, nb * sizeof(int64_t), cudaHostAllocDefault) == cudaSuccess &&
                 cudaMalloc(&sl.d_off, m * sizeof(uint32_t)) == cudaSuccess &&
@@ -1676,25 +1705,34 @@ int tm_count_edges_async(const uint32_t* src, const uint32_t* dst, const int64_t
             sl.job->m = m;
             sl.job->off = sl.h_off;
             sl.job->base = sl.h_base;
+            sl.job->width = (A.t_width == 2 && pack16_enabled()) ? 2 : 4;
             pack_start(*sl.job);
         }
         if (m) {
             TM_CUDA(cudaMemcpyAsync(sl.ds, src, m * sizeof(uint32_t), cudaMemcpyHostToDevice, A.copy));
             TM_CUDA(cudaMemcpyAsync(sl.dd, dst, m * sizeof(uint32_t), cudaMemcpyHostToDevice, A.copy));
             if (pack) {
-                const uint64_t nb = (m + kPackBlock - 1) / kPackBlock;
+                const uint64_t w = (uint64_t)sl.job->width, blk = w == 2 ? kPackBlock16 : kPackBlock;
+                const uint64_t nb = (m + blk - 1) / blk;
                 sl.waits.resize(sl.job->pieces);
                 for (uint64_t p = 0; p < sl.job->pieces; ++p) {
                     const uint64_t b = p * kPackPiece, e = std::min(m, b + kPackPiece);
                     sl.waits[p] = PieceWait{sl.job.get(), p};
                     TM_CUDA(cudaLaunchHostFunc(A.copy, pack_wait_cb, &sl.waits[p]));
-                    TM_CUDA(cudaMemcpyAsync(sl.d_off + b, sl.h_off + b, (e - b) * sizeof(uint32_t),
+                    TM_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(sl.d_off) + b * w,
+                                            reinterpret_cast<const char*>(sl.h_off) + b * w, (e - b) * w,
                                             cudaMemcpyHostToDevice, A.copy));
                 }
                 TM_CUDA(cudaMemcpyAsync(sl.d_base, sl.h_base, nb * sizeof(int64_t), cudaMemcpyHostToDevice, A.copy));
-                TM_LAUNCH("unpack_t", A.copy, unpack_t_kernel,
-                          (unsigned)std::min<uint64_t>((m + 255) / 256, (uint64_t)sm_count() * 8), 256, 0, sl.d_off, sl.d_base, m, sl.dt);
-                g_h2d_bytes.store(m * 12 + nb * 8);
+                const unsigned ugrid = (unsigned)std::min<uint64_t>((m + 255) / 256, (uint64_t)sm_count() * 8);
+                if (w == 2) {
+                    TM_LAUNCH("unpack_t", A.copy, (unpack_t_kernel<uint16_t, kPackBlock16>), ugrid, 256, 0,
+                              reinterpret_cast<const uint16_t*>(sl.d_off), sl.d_base, m, sl.dt);
+                } else {
+                    TM_LAUNCH("unpack_t", A.copy, (unpack_t_kernel<uint32_t, kPackBlock>), ugrid, 256, 0, sl.d_off,
+                              sl.d_base, m, sl.dt);
+                }
+                g_h2d_bytes.store(m * (8 + w) + nb * 8);
             } else {
                 TM_CUDA(cudaMemcpyAsync(sl.dt, t, m * sizeof(int64_t), cudaMemcpyHostToDevice, A.copy));
                 g_h2d_bytes.store(m * 16);

@@ -29,13 +29,13 @@ python profiles/ncu_summary.py $G/full_sort.ncu-rep --kernel radix_downsweep \
     --traffic-json $G/traffic_radix_downsweep_powerlaw_50m_600m_3600.json --config powerlaw_50m_600m
 python profiles/ncu_lines.py $G/full_sort.ncu-rep radix_downsweep > $G/lines_radix_downsweep.txt
 rm -f $G/full_sort.ncu-rep
-ncu --set full --clock-control none --import-source on -k regex:"tri_long|tri_wedge" -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"tri_mid|tri_window|tri_wedge" -c 3 \
     -o $G/full_tri python profiles/census_once.py powerlaw_50m_600m 3600 1 > $G/ncu_tri.log 2>&1; echo full_tri=$?
 python profiles/ncu_summary.py $G/full_tri.ncu-rep --kernel tri_wedge > $G/ncu_tri_wedge.txt
-python profiles/ncu_summary.py $G/full_tri.ncu-rep --kernel tri_long --index 0 > $G/ncu_tri_long_plain.txt
-python profiles/ncu_summary.py $G/full_tri.ncu-rep --kernel tri_long --index 1 > $G/ncu_tri_long_cached.txt
+python profiles/ncu_summary.py $G/full_tri.ncu-rep --kernel tri_mid > $G/ncu_tri_mid.txt
+python profiles/ncu_summary.py $G/full_tri.ncu-rep --kernel tri_window > $G/ncu_tri_window.txt
 python profiles/ncu_lines.py $G/full_tri.ncu-rep tri_wedge > $G/lines_tri_wedge.txt
-python profiles/ncu_lines.py $G/full_tri.ncu-rep tri_long > $G/lines_tri_long.txt
+python profiles/ncu_lines.py $G/full_tri.ncu-rep tri_mid > $G/lines_tri_mid.txt
 rm -f $G/full_tri.ncu-rep
 ncu --set full --clock-control none --import-source on \
     -k regex:"pair_keys|s_offsets|p_flags|orient_kernel|star_work|star_locate|pack_edges|forward_scatter|tri_filter|star_filter" -c 10 \

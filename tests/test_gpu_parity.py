@@ -858,16 +858,18 @@ print(json.dumps(out))
 
 
 def test_async_packed_timestamps(cuda, tm, oracle):
-    """Large eager batches send t as per-block i64 bases + u32 offsets packed
-    by host threads (tm_async_h2d_bytes = 12 B per edge): sorted input,
-    unsorted input (blocks re-based on their minimum), negative and huge
-    timestamps, and a block whose span exceeds 32 bits (falls back to the plain
-    copy of t) must all give the synchronous census of the same arrays."""
+    """Large eager batches send t as per-block i64 bases + offsets packed by
+    host threads: u16 offsets per 4096 edges (tm_async_h2d_bytes = 10 B per
+    edge) until a batch has a block that does not fit -- that batch takes the
+    plain copy of t and later ones pack u32 offsets per 65536 edges (12 B per
+    edge).  Sorted input, input unsorted inside blocks (re-based on the block
+    minimum), negative and huge timestamps, and a block whose span exceeds 32
+    bits (plain copy) must all give the synchronous census of the same arrays."""
     import json
     import os
     import subprocess
     import sys
-    script = r'''
+    script = r"""
 import json, sys
 import numpy as np
 import torch
@@ -879,34 +881,45 @@ def graph(kind):
     src = rng.integers(0, n, m).astype(np.uint32)
     dst = (src + 1 + rng.integers(0, n - 1, m).astype(np.uint32)) % n
     t = np.sort(rng.integers(0, 400_000, m)).astype(np.int64)
-    if kind == 1:   # unsorted inside blocks, negative base
-        t = rng.permutation(t) - 10**12
+    if kind == 1:    # unsorted inside blocks (groups of 64 permuted), negative base: u16 from the block minimum
+        t = np.concatenate([rng.permutation(g) for g in np.split(t, m // 64)]) - 10**12
     elif kind == 2:  # near the top of int64
         t = t + (2**63 - 1 - 400_000)
-    elif kind == 3:  # one block spans more than 2^32: plain copy
+    elif kind in (3, 4):  # wholly permuted: blocks span ~400000 (not u16; u32 from the block minimum)
+        t = rng.permutation(t) - 10**12
+    elif kind == 5:
+        t = t + (2**63 - 1 - 400_000)
+    elif kind == 6:  # one block spans more than 2^32: plain copy
         t = t.copy(); t[70_000:] += 2**33; t[70_001] -= 2**34
     return src, dst.astype(np.uint32), t
+K = 7
 out = []
 cfg = tm.RunConfig(delta=delta)
 st = torch.cuda.Stream()
 pins, pend = [], []
-for kind in range(4):
+for kind in range(K):
     s, d, t = graph(kind)
     p = tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).pin_memory() for a in (s, d, t))
     pins.append(p)
     pend.append(tm.count_edges_async(n, p[0].numpy().view(np.uint32), p[1].numpy().view(np.uint32), p[2].numpy(),
                                      cfg, stream=st.cuda_stream))
     sent = tm.async_h2d_bytes()
-    if kind >= 1:
-        out.append(["async", kind - 1, pend[kind - 1].result().tolist()])
     out.append(["bytes", kind, sent])
-out.append(["async", 3, pend[3].result().tolist()])
-for kind in range(4):
+    # kinds 0-2 are in flight together (results one batch late); from kind 3 on
+    # each batch is finished before the next is submitted, so the width the
+    # pipeline moved to after a fallback is the next batch's
+    if kind in (1, 2):
+        out.append(["async", kind - 1, pend[kind - 1].result().tolist()])
+    if kind >= 3:
+        if kind == 3:
+            out.append(["async", 2, pend[2].result().tolist()])
+        out.append(["async", kind, pend[kind].result().tolist()])
+for kind in range(K):
     p = pins[kind]
     out.append(["sync", kind, tm.count_edges(n, p[0].numpy().view(np.uint32), p[1].numpy().view(np.uint32),
                                              p[2].numpy(), cfg, stream=st.cuda_stream).tolist()])
 print(json.dumps(out))
-'''
+"""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", script, root],
                        env=dict(os.environ, TM_GRAPHS="0", TM_H2D_PACK_MIN="1000", TM_HOST_THREADS="4"),
@@ -915,13 +928,16 @@ print(json.dumps(out))
     got = json.loads(r.stdout.strip().splitlines()[-1])
     res = {(k, i): v for k, i, v in got}
     m = 200_000
-    for kind in range(4):
+    for kind in range(7):
         assert res[("async", kind)] == res[("sync", kind)], kind
         assert sum(res[("sync", kind)]) > 0
-    for kind in range(3):
+    for kind in range(3):  # u16 offsets
+        assert res[("bytes", kind)] == m * 10 + 8 * ((m + 4095) // 4096), kind
+    # (a fallback's extra plain copy is added when its census is issued)
+    assert res[("bytes", 3)] >= m * 10
+    for kind in (4, 5):    # u32 offsets from here on
         assert res[("bytes", kind)] == m * 12 + 8 * ((m + 65535) // 65536), kind
-    # (the fallback's extra plain copy is added when its census is issued)
-    assert res[("bytes", 3)] >= m * 12
+    assert res[("bytes", 6)] >= m * 12
 
 
 def test_unaligned_device_arrays_and_raw_first_pass(cuda, tm, oracle):
