@@ -317,17 +317,22 @@ __global__ void s_offsets_kernel(const uint32_t* __restrict__ S_node, uint64_t R
 #pragma unroll
             for (int k = 0; k < 4; ++k) u[k] = q0 + k < R ? S_node[q0 + k] : 0u;
         }
-        int64_t prev = q0 ? (int64_t)S_node[q0 - 1] : -1;
+        // node ids are below 2^31, so 0xFFFFFFFF stands for "before node 0";
+        // most records repeat their predecessor's node (one compare each)
+        uint32_t prev = q0 ? S_node[q0 - 1] : 0xFFFFFFFFu;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const uint64_t q = q0 + k;
-            if (q < R) {
-                for (int64_t y = prev + 1; y <= (int64_t)u[k]; ++y) off[y] = (uint32_t)q;
-                if (q == R - 1)
-                    for (int64_t y = (int64_t)u[k] + 1; y <= (int64_t)n; ++y) off[y] = (uint32_t)R;
+            if (q < R && u[k] != prev) {
+                for (uint32_t y = prev + 1u;; ++y) {  // S_node ascends: prev + 1 .. u[k]
+                    off[y] = (uint32_t)q;
+                    if (y == u[k]) break;
+                }
                 prev = u[k];
             }
         }
+        if (q0 + 4 >= R)  // the quad with the last record closes the remaining nodes
+            for (uint64_t y = (uint64_t)prev + 1; y <= n; ++y) off[y] = (uint32_t)R;
     }
 }
 

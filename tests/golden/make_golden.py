@@ -152,7 +152,7 @@ def config4_full_golden(R, deltas=(600,)):
     from paper_2204_09236_b200 import synth
     name = "config4_full_reference.json"
     out_dir = os.environ.get("GOLDEN_OUT", HERE)
-    need_gb = int(os.environ.get("GOLDEN_NEED_GB", "220"))  # never drive the box out of memory
+    need_gb = int(os.environ.get("GOLDEN_NEED_GB", "150"))  # never drive the box out of memory
     avail = [int(l.split()[1]) for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0] >> 20
     if avail < need_gb:
         print("config4 full: only", avail, "GB of host memory available, need", need_gb, "- skipped", flush=True)
