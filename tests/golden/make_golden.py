@@ -119,7 +119,12 @@ def config4_slices_golden(R, deltas=(600, 3600, 86400)):
     path = os.path.join(HERE, name)
     out = json.load(open(path)) if os.path.exists(path) else {
         "config": "powerlaw_50m_600m", "generator": "synth.power_law_hashed", **CONFIG4, "slices": []}
-    for lo, hi in CONFIG4_SLICES:
+    slices = CONFIG4_SLICES
+    if os.environ.get("GOLDEN_SLICES"):  # e.g. "120000000:180000000" (with GOLDEN_DELTAS="600,3600")
+        slices = tuple(tuple(int(x) for x in p.split(":")) for p in os.environ["GOLDEN_SLICES"].split(","))
+    if os.environ.get("GOLDEN_DELTAS"):
+        deltas = tuple(int(x) for x in os.environ["GOLDEN_DELTAS"].split(","))
+    for lo, hi in slices:
         have = [s for s in out["slices"] if s["lo"] == lo and s["hi"] == hi]
         entry = have[0] if have else None
         done = {c["delta"] for c in entry["cases"]} if entry else set()
