@@ -213,7 +213,7 @@ constexpr int kWedgeScan = 8;
 #define TM_GCACHE_BITS 7
 #endif
 #ifndef TM_CACHE_MINB
-#define TM_CACHE_MINB 4
+#define TM_CACHE_MINB 3  // tri_window: config 4 delta 86400 tri_long 884.9 -> 878.6 ms against 4 (profiles/r02/ab)
 #endif
 constexpr int kGroupCache = 1 << TM_GCACHE_BITS;  // entries per warp (dynamic shared memory)
 #ifndef TM_CACHE_MINWIN
@@ -225,7 +225,7 @@ constexpr uint32_t kGroupCacheMinWindow = TM_CACHE_MINWIN;  // shorter windows r
 #define TM_WEDGE_MINB 5
 #endif
 #ifndef TM_LONG_MINB
-#define TM_LONG_MINB 6
+#define TM_LONG_MINB 5  // tri_mid: 17.6 -> 17.2 ms at config 4 delta 3600, 898 -> 885 ms at 86400 against 6; 4 and 7 lose at 3600
 #endif
 constexpr int kFilterItems = 4;  // first edges per thread per block iteration (one reservation)
 __global__ void __launch_bounds__(256) tri_filter_kernel(TimeArr FT,
